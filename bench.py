@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""bench.py — ROAST-MM fwd+bwd effective TFLOP/s on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], the metric's config):
+BERT-base MLP block, L1 768->3072 and L2 3072->768 in ONE global M (GMS) at
+100x compression (|M| = 47 192 fp32), hash tile 64x64, 8192 tokens per GPU,
+bf16 operands / fp32 accumulate.  One step = the whole hot path over one batch:
+
+    Y1 = L1(X); Y2 = L2(Y1)                      (a1, the N-op between them is identity)
+    dY1 = L2.dX(dY2); dM += L2.dM(Y1, dY2)       (a2, a3)
+    dX  = L1.dX(dY1); dM += L1.dM(X, dY1)        (a2, a3)
+    dM  = allreduce(dM)                          (a6; no-op at N = 1)
+
+Effective FLOPs per step per GPU = sum over layers of 6 T H O (ROAST does
+not reduce compute).  Multi-GPU: one process per GPU, tokens per GPU fixed
+(weak scaling), dM all-reduced with NCCL through the C ABI.
+
+`--impl reference` times the oracle (oracle/, CPU fp64) as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+RATIO = 100
+TOKENS = 8192
+LAYERS = [(768, 3072), (3072, 768)]
+TILE = 64
+METRIC = "ROAST-MM fwd+bwd effective TFLOP/s vs dense cuBLAS & bf16 peak, 1/2/4/8 B200"
+UNIT = "TFLOP/s"
+
+
+def flops_per_step(tokens):
+    return sum(6.0 * tokens * H * O for H, O in LAYERS)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["bf16_tflops"], d.get("bf16_tflops_sustained"), d["hbm_gbs"], "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------------------ reference arm
+def cpu_sample(seconds_target=10.0, tokens=256):
+    """Time the oracle on a bounded sample of the workload: `tokens` of the 8192."""
+    import numpy as np
+
+    import synth
+    from oracle import roast_mm as OM
+    mem = synth.mlp_block(RATIO)["mem_size"]
+    M = synth.uniform(synth.SEED_M, (mem,)).astype(np.float32)
+    specs = [OM.LinearSpec(H, O, TILE, TILE, mem, synth.HASH_SEED, i) for i, (H, O) in enumerate(LAYERS)]
+    X = synth.round_to_bf16(synth.normal(synth.SEED_X, (tokens, 768)).astype(np.float32))
+    dY2 = synth.round_to_bf16(synth.normal(synth.SEED_DY, (tokens, 768)).astype(np.float32))
+    t0 = time.perf_counter()
+    steps = 0
+    while True:
+        Y1 = specs[0].forward(X, M, True)
+        specs[1].forward(Y1, M, True)
+        dM = np.zeros(mem)
+        dY1 = specs[1].backward_dx(dY2, M, True)
+        specs[1].backward_dm(Y1, dY2, dM)
+        specs[0].backward_dx(dY1, M, True)
+        specs[0].backward_dm(X, dY1, dM)
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds_target:
+            break
+    per_step = el / steps
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    return dict(value=flops_per_step(tokens) / per_step / 1e12, unit=UNIT, cores=cores, kind="oracle",
+                sample=f"MLP block fwd+bwd at T={tokens} of {TOKENS} tokens (oracle cost is linear in T), "
+                       f"{steps} steps in {el:.1f}s, fp64 numpy", seconds_per_sample_step=per_step)
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+    for _ in range(args.warmup):
+        pass
+    cb = cpu_sample(seconds_target=max(3.0, 2.0 * args.steps))
+    line = dict(metric=METRIC, value=cb["value"], unit=UNIT, n_gpus=args.gpus, steps=args.steps,
+                warmup=args.warmup, ms_per_step=cb["seconds_per_sample_step"] * 1e3, higher_is_better=True,
+                scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
+                config=dict(workload="C2 BERT-base MLP block 768->3072->768, 100x, tile 64x64 (oracle sample)",
+                            tokens_per_gpu=TOKENS, ratio=RATIO),
+                impl="reference",
+                cpu_baseline=dict(value=cb["value"], unit=UNIT, cores=cb["cores"], kind="oracle",
+                                  sample=cb["sample"]),
+                e2e=dict(value=cb["value"], unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ GPU arm
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=5)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        import statistics
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["unsampled"])
+        return dict(sm_mhz=statistics.median(sm), sm_max_mhz=mx, reasons=sorted(reasons), samples=len(sm))
+
+
+def run_gpu(args):
+    import numpy as np
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2207_10702_b200 import roast as R
+    import synth
+
+    T = TOKENS
+    mem = synth.mlp_block(RATIO)["mem_size"]
+    stream = torch.cuda.current_stream()
+    M = torch.tensor(synth.uniform(synth.SEED_M, (mem,)).astype(np.float32), device=dev)
+    ctx = R.Roast(M, TILE, TILE, seed=synth.HASH_SEED, deterministic=args.deterministic)
+    if world > 1:
+        import torch.distributed as dist
+        uid = R.roast_comm_unique_id() if rank == 0 else bytes(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, 0)
+        R.roast_comm_init(ctx.h, rank, world, bytes(t.cpu().tolist()))
+    l1 = ctx.linear(*LAYERS[0])
+    l2 = ctx.linear(*LAYERS[1])
+    bf = torch.bfloat16
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    X = torch.randn(T, 768, device=dev, generator=g).to(bf)
+    dY2 = torch.randn(T, 768, device=dev, generator=g).to(bf)
+    Y1 = torch.empty(T, 3072, device=dev, dtype=bf)
+    Y2 = torch.empty(T, 768, device=dev, dtype=bf)
+    dY1 = torch.empty(T, 3072, device=dev, dtype=bf)
+    dX = torch.empty(T, 768, device=dev, dtype=bf)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    kinds = ["fwd", "dx", "dm"]
+    ev = {k: [] for k in kinds}
+
+    def step(record):
+        def rec(kind, fn):
+            if record:
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                ev[kind].append((a, b))
+            else:
+                fn()
+        ctx.zero_grad()
+        rec("fwd", lambda: ctx.fwd(l1, X, Y1))
+        rec("fwd", lambda: ctx.fwd(l2, Y1, Y2))
+        rec("dx", lambda: ctx.bwd_dx(l2, dY2, dY1))
+        rec("dm", lambda: ctx.bwd_dm(l2, Y1, dY2))
+        rec("dx", lambda: ctx.bwd_dx(l1, dY1, dX))
+        rec("dm", lambda: ctx.bwd_dm(l1, X, dY1))
+        ctx.allreduce()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(False)
+    barrier()
+
+    # timed region: per-step CUDA events; L2 flushed between steps (outside the events)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = ctx.launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record(stream)
+            step(True)
+            ends[i].record(stream)
+        barrier()
+    launches = ctx.launch_count() - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_per_step = total_ms / args.steps
+    value = world * flops_per_step(T) / (ms_per_step * 1e-3) / 1e12
+
+    # per-kernel-kind times (each of our calls is one kernel launch in the atomic mode)
+    kind_ms = {k: float(np.mean([a.elapsed_time(b) for a, b in ev[k]])) for k in kinds}
+    gemm_flop = 2.0 * T * 768 * 3072                       # every call is one 2*T*H*O contraction
+    dom = max(kinds, key=lambda k: kind_ms[k])
+    burst, sustained, hbm, src = load_peaks()
+    achieved = gemm_flop / (kind_ms[dom] * 1e-3) / 1e12
+
+    # end-to-end through the C ABI with host buffers: H2D of the step's inputs, D2H of dM
+    Xh = X.cpu().pin_memory()
+    dY2h = dY2.cpu().pin_memory()
+    dMh = torch.empty(mem, dtype=torch.float32).pin_memory()
+    Xd = torch.empty_like(X)
+    dY2d = torch.empty_like(dY2)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        Xd.copy_(Xh, non_blocking=True)
+        dY2d.copy_(dY2h, non_blocking=True)
+        ctx.zero_grad()
+        ctx.fwd(l1, Xd, Y1)
+        ctx.fwd(l2, Y1, Y2)
+        ctx.bwd_dx(l2, dY2d, dY1)
+        ctx.bwd_dm(l2, Y1, dY2d)
+        ctx.bwd_dx(l1, dY1, dX)
+        ctx.bwd_dm(l1, Xd, dY1)
+        ctx.allreduce()
+        dMh.copy_(ctx.dM, non_blocking=True)
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = world * flops_per_step(T) / (e2e_ms * 1e-3) / 1e12
+
+    # dense cuBLAS layer of the same virtual shapes, same run (context for the metric)
+    W1 = ctx.materialize(l1, bf)
+    W2 = ctx.materialize(l2, bf)
+
+    def dense_step():
+        y1 = X @ W1
+        y2 = y1 @ W2
+        d1 = dY2 @ W2.t()
+        g2 = y1.t() @ dY2
+        dx = d1 @ W1.t()
+        g1 = X.t() @ d1
+        return y2, dx, g1, g2
+    for _ in range(3):
+        dense_step()
+    torch.cuda.synchronize()
+    d0, d1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dn = []
+    for _ in range(max(5, args.steps)):
+        flush.zero_()
+        d0.record(stream)
+        dense_step()
+        d1e.record(stream)
+        torch.cuda.synchronize()
+        dn.append(d0.elapsed_time(d1e))
+    dense_ms = float(np.mean(dn))
+    dense_tflops = flops_per_step(T) / (dense_ms * 1e-3) / 1e12
+
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+    cb = cpu_sample(seconds_target=args.cpu_seconds) if not args.no_cpu else None
+    line = dict(
+        metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
+        ms_per_step=ms_per_step, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="bf16",
+        data="synthetic (M ~ U(-1,1) from synth seed 1; X, dY ~ N(0,1) bf16)",
+        config=dict(workload="C2 BERT-base MLP block 768->3072->768 fwd+bwd, 100x (|M|=%d), tile 64x64" % mem,
+                    tokens_per_gpu=T, global_tokens=T * world, ratio=RATIO, mem_size=mem,
+                    l2="flushed between timed steps (256 MB write outside the events)",
+                    dm_mode="deterministic" if args.deterministic else "atomic",
+                    parallelism=f"dp{world}"),
+        roofline=dict(bound="tensor", kernel=dom, achieved=achieved, peak=burst, unit="TFLOP/s",
+                      frac=achieved / burst, traffic=None,
+                      note=f"peak = {src} bf16 burst (MEASURED_PEAKS.json); algorithmic 2*T*H*O = "
+                           f"{gemm_flop/1e9:.2f} GFLOP per launch / mean CUDA-event duration",
+                      per_kind_ms=kind_ms, sustained_peak=sustained),
+        dense_cublas=dict(tflops=dense_tflops, ms_per_step=dense_ms, roast_over_dense=value / world / dense_tflops),
+        e2e=dict(value=e2e_value, unit=UNIT, h2d_bytes_per_step=int(Xh.numel() * 2 + dY2h.numel() * 2),
+                 d2h_bytes_per_step=int(mem * 4)),
+        gpu_launches=int(launches),
+        clocks=clk.summary(),
+        cpu_baseline=None if cb is None else {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+    )
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="roast", choices=["roast", "reference"])
+    ap.add_argument("--deterministic", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,186 @@
+/*
+ * roast.h — C ABI of libroast.so, the B200 (sm_100a) hot path of ROAST hashing
+ * (Desai, Zhou, Shrivastava, "Efficient model compression with Random Operation
+ * Access Specific Tile (ROAST) hashing", arXiv 2207.10702).
+ *
+ * Citations "P:n" are PAPER.md line numbers (section / equation / algorithm in
+ * brackets); "R<n>" are the readings listed in DESIGN.md §Readings.
+ *
+ * Conventions (all entry points)
+ *   - extern "C"; every call returns roast_status_t; nothing throws; no torch types.
+ *   - Pointers named d_* / tensor arguments are DEVICE pointers owned by the caller,
+ *     row-major and densely packed unless stated otherwise.  Pointers named *_host
+ *     are host pointers.  The library never frees caller memory.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Every device-side effect is stream-ordered and asynchronous; only the
+ *     roast_debug_tile_map call synchronises (it copies to host).
+ *   - Argument / geometry validation is synchronous: on a non-OK return nothing
+ *     was launched.  Device-detected faults (embedding index out of range) are
+ *     sticky and reported by roast_get_error() (and by the next call).
+ *   - A handle is not thread-safe; use one per thread / rank.
+ *   - roast_last_error() returns a human-readable detail string for the last
+ *     non-OK status returned on the calling thread.
+ *
+ * The mapping (P:268-289 [§4.1], P:315, P:326 [§4.2]; concrete family: R1-R3, R8)
+ *   h(key) = A * (poly61(c_off, key) mod R),  R = floor((|M| - T) / A) + 1
+ *   g(key) = (poly61(c_sgn, key) & 1) ? -1 : +1
+ *   poly61 = c3 k^3 + c2 k^2 + c1 k + c0 over GF(2^61 - 1),
+ *   c_r    = splitmix64(seed ^ splitmix64((module << 8) | (role << 4) | r)) mod (2^61 - 1)
+ *   linear tile key  (x << 32) | y        (x = i / Z1 along in_features, y = j / Z2)
+ *   embedding chunk  row * ceil(d / Z) + j
+ *   lambda = fp32(C / sqrt(fan_in))
+ * Module ids are 0-based registration order shared by linears and embeddings;
+ * they key the hash family, so registration order is part of the model.
+ */
+#ifndef ROAST_H_
+#define ROAST_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ROAST_OK = 0,
+  ROAST_ERR_CONFIG = 1,    /* invalid configuration value (C <= 0, bad enum, ...)            */
+  ROAST_ERR_GEOMETRY = 2,  /* tile/chunk does not fit |M|, H % Z1 or O % Z2 != 0, T % A != 0 */
+  ROAST_ERR_SHAPE = 3,     /* tensor sizes inconsistent with the module                        */
+  ROAST_ERR_BOUNDS = 4,    /* embedding index outside [0, num_rows) (sticky, device-detected)  */
+  ROAST_ERR_CAPACITY = 5,  /* allocation failure / too many modules                            */
+  ROAST_ERR_STATE = 6,     /* not bound, unknown module id, comm not initialised, ...          */
+  ROAST_ERR_CUDA = 7,      /* a CUDA runtime / driver call failed                              */
+  ROAST_ERR_NCCL = 8,      /* an NCCL call failed or libnccl could not be loaded               */
+  ROAST_ERR_UNSUPPORTED = 9 /* valid request with no kernel for it (e.g. bf16 with Z2 != 64)   */
+} roast_status_t;
+
+typedef struct roast_ctx* roast_t;
+typedef void* roast_stream_t; /* a cudaStream_t */
+
+/* Hash-tile geometry of every linear (P:280-281 [§4.1]): Z1 rows along
+ * in_features (the K dimension of Y = X W), Z2 columns along out_features.
+ * Fixed at create time and part of the model (R10). */
+typedef struct {
+  int32_t z1, z2;
+} roast_tile_t;
+
+typedef enum { ROAST_FP32 = 0, ROAST_BF16 = 1 } roast_dtype_t;
+
+typedef enum { ROAST_ROW_MAJOR = 0, ROAST_SW128 = 1 } roast_tile_layout_t; /* R4 */
+typedef enum { ROAST_MAP_HASH = 0, ROAST_MAP_IDENTITY = 1 } roast_mapping_t; /* R22 */
+
+typedef struct {
+  double C;              /* GMS init scale: M ~ U(-1/C, 1/C), lambda = C/sqrt(n); default 1 */
+  int32_t align_elems;   /* A: offsets are multiples of A elements; default 8 (16 B in bf16, R3)      */
+  int32_t tile_layout;   /* roast_tile_layout_t; default ROW_MAJOR                            */
+  int32_t mapping;       /* roast_mapping_t; IDENTITY = no sharing, lambda 1, g +1 (test mode)        */
+  int32_t use_sign;      /* 1 = multiply by g, default 1                                       */
+  int32_t deterministic; /* 1 = dM accumulated in a fixed order, bitwise reproducible (default 0)     */
+} roast_config_t;
+
+/* Fill *cfg with the defaults listed above. */
+void roast_config_default(roast_config_t* cfg);
+
+/* Create a handle for a compressed array M of `mem_size` fp32 elements (GMS:
+ * one M for every module, P:318-321 [§4.2]) with master hash seed `seed`.
+ * Errors: CONFIG (mem_size <= 0, bad cfg), GEOMETRY (z1 or z2 <= 0). */
+roast_status_t roast_create(roast_t* out, int64_t mem_size, uint64_t seed, roast_tile_t tile);
+roast_status_t roast_create_ex(roast_t* out, int64_t mem_size, uint64_t seed, roast_tile_t tile,
+                               const roast_config_t* cfg);
+roast_status_t roast_destroy(roast_t h);
+
+/* Bind the caller-owned device arrays d_M (values) and d_dM (gradient), each
+ * mem_size fp32 elements, 16-byte aligned.  Allocates the library-owned bf16
+ * shadow [+bf16(M) | -bf16(M)] (sign folded into the load address) and fills
+ * it on `stream` (= roast_sync_shadow).  Rebinding is allowed. */
+roast_status_t roast_bind(roast_t h, float* d_M, float* d_dM, roast_stream_t stream);
+
+/* Register a ROAST linear W (in_features x out_features), Y = X W (Alg. 1
+ * P:294-313).  Computes and uploads its static tile map (a0).  lambda =
+ * fp32(C / sqrt(in_features)).  *id receives the module id.
+ * Errors: GEOMETRY (Z1 Z2 > |M|, in % Z1, out % Z2, Z1 Z2 % A, or identity
+ * mapping overflowing |M|), CAPACITY, CUDA. */
+roast_status_t roast_register_linear(roast_t h, int64_t in_features, int64_t out_features, int32_t* id);
+
+/* Register a ROAST/ROBE block embedding of num_rows x dim recovered in chunks of
+ * `chunk` elements (P:268-276 [§4.1 Lookup]).  fan_in <= 0 selects dim (R7).
+ * Errors: GEOMETRY (chunk > |M|, chunk % A != 0, chunk % 4 != 0, dim % 4 != 0). */
+roast_status_t roast_register_embedding(roast_t h, int64_t num_rows, int32_t dim, int32_t chunk,
+                                        double fan_in, int32_t* id);
+
+/* a1: Y[tokens x out] = lambda * X[tokens x in] * W~, W~ tiles read from M
+ * through the hash with sign g (Alg. 1; lambda once per output tile,
+ * P:308).  dt = ROAST_FP32: X, Y fp32, SIMT FMA path on M (fp32).
+ * dt = ROAST_BF16: X, Y bf16, tcgen05 path on the bf16 shadow (requires
+ * Z1 = Z2 = 64, in % 64 == 0, out % 64 == 0, tokens any >= 0), fp32 accumulate. */
+roast_status_t roast_linear_fwd(roast_t h, int32_t id, const void* d_X, void* d_Y, int64_t tokens,
+                                roast_dtype_t dt, roast_stream_t stream);
+
+/* a2 + a3: dX = lambda * dY W~^T (skipped if d_dX == NULL), and
+ * dM[h(x,y) + pi(o1,o2)] += lambda * g(x,y) * (X^T dY)[i, j] for every virtual
+ * weight (P:338-346 [§4.3 eq. gradient rule] with g by the chain rule, R12),
+ * without materialising W.  dM accumulates (+=).  Deterministic
+ * mode sums every slot in a fixed order (bitwise reproducible). */
+roast_status_t roast_linear_bwd(roast_t h, int32_t id, const void* d_X, const void* d_dY, void* d_dX,
+                                int64_t tokens, roast_dtype_t dt, roast_stream_t stream);
+
+/* The two halves of roast_linear_bwd, for callers that overlap them on two
+ * streams (dX is on the critical path of the previous layer, dM is not):
+ * a2 alone: dX = lambda * dY W~^T;  a3 alone: dM += scatter(lambda g X^T dY). */
+roast_status_t roast_linear_bwd_dx(roast_t h, int32_t id, const void* d_dY, void* d_dX, int64_t tokens,
+                                   roast_dtype_t dt, roast_stream_t stream);
+roast_status_t roast_linear_bwd_dm(roast_t h, int32_t id, const void* d_X, const void* d_dY, int64_t tokens,
+                                   roast_dtype_t dt, roast_stream_t stream);
+
+/* a4: out[b, jZ + o] = g(c) * fp32(lambda * M[h1(c) + o]),  c = idx[b] * ceil(d/Z) + j
+ * (P:270).  idx: n int64 device indices; out: n x dim fp32.  An index outside
+ * [0, num_rows) yields a zero row and raises the sticky BOUNDS flag. */
+roast_status_t roast_embedding_fwd(roast_t h, int32_t id, const int64_t* d_idx, int64_t n, float* d_out,
+                                   roast_stream_t stream);
+
+/* a5: dM[h1(c) + o] += lambda * g(c) * dOut[b, jZ + o]; duplicate indices add (R15). */
+roast_status_t roast_embedding_bwd(roast_t h, int32_t id, const int64_t* d_idx, int64_t n,
+                                   const float* d_dOut, roast_stream_t stream);
+
+/* a6: data-parallel exchange.  Rank 0 calls roast_comm_unique_id; the caller
+ * broadcasts the 128 bytes (e.g. torch.distributed); every rank calls
+ * roast_comm_init.  roast_grad_allreduce sums dM over ranks in place
+ * (ncclAllReduce, fp32 sum) on `stream`; with world == 1 it is a no-op.
+ * libnccl.so.2 is loaded at run time (ROAST_ERR_NCCL if absent). */
+roast_status_t roast_comm_unique_id(uint8_t id_out[128]);
+roast_status_t roast_comm_init(roast_t h, int32_t rank, int32_t world, const uint8_t id[128]);
+roast_status_t roast_grad_allreduce(roast_t h, roast_stream_t stream);
+
+/* dM <- 0. */
+roast_status_t roast_zero_grad(roast_t h, roast_stream_t stream);
+/* shadow <- [+bf16_RNE(M) | -bf16_RNE(M)]; call after every update of M (H7). */
+roast_status_t roast_sync_shadow(roast_t h, roast_stream_t stream);
+/* (a7, minimal) M <- M - lr * dM, then shadow refresh.  Fused elementwise kernel. */
+roast_status_t roast_sgd_step(roast_t h, float lr, roast_stream_t stream);
+
+/* Sticky device-side error (synchronises the handle's bound stream is NOT done:
+ * call after a stream synchronize to observe faults of completed work). */
+roast_status_t roast_get_error(roast_t h);
+const char* roast_status_str(roast_status_t st);
+const char* roast_last_error(void);
+
+/* ---- test hooks (parity tier T1) ---------------------------------------- */
+/* Copy module `id`'s tile map to host: off_host[x * ny + y], sgn_host[x * ny + y]
+ * (nx = in/Z1, ny = out/Z2).  Synchronous. */
+roast_status_t roast_debug_tile_map(roast_t h, int32_t id, int64_t* off_host, int8_t* sgn_host);
+/* Evaluate the embedding kernels' __device__ chunk hash for n rows: d_off / d_sgn
+ * are n x ceil(dim/chunk) device arrays. */
+roast_status_t roast_debug_chunk_map(roast_t h, int32_t id, const int64_t* d_rows, int64_t n,
+                                     int64_t* d_off, int8_t* d_sgn, roast_stream_t stream);
+/* Recovered W (in x out) on device.  dt = FP32: g * fp32(lambda * M) (fp32 def.);
+ * dt = BF16: g * bf16(M) read from the shadow (the tensor-core operand, lambda deferred). */
+roast_status_t roast_debug_materialize(roast_t h, int32_t id, roast_dtype_t dt, void* d_W,
+                                       roast_stream_t stream);
+/* Number of kernels this handle has launched since creation (bench evidence). */
+int64_t roast_launch_count(roast_t h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ROAST_H_ */

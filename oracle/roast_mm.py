@@ -118,13 +118,18 @@ class LinearSpec:
         raise ValueError(kind)
 
     # -- the passes -----------------------------------------------------------
-    def forward(self, X, M) -> np.ndarray:
-        """Y = X W  (Algorithm 1)."""
-        return np.asarray(X, dtype=np.float64) @ self.materialize(M)
+    def _weights(self, M, bf16_operand: bool) -> np.ndarray:
+        if bf16_operand:      # bf16 path (R18): operand g * bf16(M), lambda once per output
+            return np.float64(self.lam) * self.materialize(M, "operand")
+        return self.materialize(M)
 
-    def backward_dx(self, dY, M) -> np.ndarray:
+    def forward(self, X, M, bf16_operand: bool = False) -> np.ndarray:
+        """Y = X W  (Algorithm 1)."""
+        return np.asarray(X, dtype=np.float64) @ self._weights(M, bf16_operand)
+
+    def backward_dx(self, dY, M, bf16_operand: bool = False) -> np.ndarray:
         """dX = dY W^T."""
-        return np.asarray(dY, dtype=np.float64) @ self.materialize(M).T
+        return np.asarray(dY, dtype=np.float64) @ self._weights(M, bf16_operand).T
 
     def grad_weights(self, X, dY) -> np.ndarray:
         """G = X^T dY, the gradient w.r.t. the virtual weights theta (H x O)."""

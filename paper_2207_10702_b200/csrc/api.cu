@@ -1,0 +1,442 @@
+// api.cu — the C ABI of libroast.so (include/roast.h): validation, module
+// registration (static tile maps, a0), dispatch to the kernels, sticky errors.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <numeric>
+#include <string>
+
+#include "roast_internal.h"
+
+namespace roast {
+
+static thread_local std::string g_last_error;
+
+roast_status_t fail(roast_status_t st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+roast_status_t cuda_fail(cudaError_t e, const char* what) {
+  return fail(ROAST_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+roast_status_t ensure_ws(Ctx* c, size_t bytes, cudaStream_t s) {
+  if (c->ws_bytes >= bytes) return ROAST_OK;
+  if (c->ws) ROAST_CUDA_CHECK(cudaFreeAsync(c->ws, s));
+  c->ws = nullptr;
+  c->ws_bytes = 0;
+  ROAST_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&c->ws), bytes, s));
+  c->ws_bytes = bytes;
+  return ROAST_OK;
+}
+
+static Ctx* ctx(roast_t h) { return reinterpret_cast<Ctx*>(h); }
+
+static roast_status_t get_module(Ctx* c, int32_t id, ModuleKind kind, Module** out) {
+  if (!c) return fail(ROAST_ERR_STATE, "null handle");
+  if (id < 0 || id >= int32_t(c->modules.size())) return fail(ROAST_ERR_STATE, "unknown module id");
+  if (c->modules[id].kind != kind) return fail(ROAST_ERR_STATE, "module kind mismatch");
+  if (!c->M || !c->dM) return fail(ROAST_ERR_STATE, "roast_bind has not been called");
+  *out = &c->modules[id];
+  return ROAST_OK;
+}
+
+static void free_module(Module& m) {
+  cudaFree(m.d_off);
+  cudaFree(m.d_sgn);
+  cudaFree(m.d_sorted);
+  cudaFree(m.d_sorted_off);
+}
+
+}  // namespace roast
+
+using namespace roast;
+
+extern "C" {
+
+void roast_config_default(roast_config_t* cfg) {
+  cfg->C = 1.0;
+  cfg->align_elems = 8;
+  cfg->tile_layout = ROAST_ROW_MAJOR;
+  cfg->mapping = ROAST_MAP_HASH;
+  cfg->use_sign = 1;
+  cfg->deterministic = 0;
+}
+
+const char* roast_status_str(roast_status_t st) {
+  switch (st) {
+    case ROAST_OK: return "ok";
+    case ROAST_ERR_CONFIG: return "config error";
+    case ROAST_ERR_GEOMETRY: return "geometry error";
+    case ROAST_ERR_SHAPE: return "shape error";
+    case ROAST_ERR_BOUNDS: return "bounds error";
+    case ROAST_ERR_CAPACITY: return "capacity error";
+    case ROAST_ERR_STATE: return "state error";
+    case ROAST_ERR_CUDA: return "CUDA error";
+    case ROAST_ERR_NCCL: return "NCCL error";
+    case ROAST_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+const char* roast_last_error(void) { return g_last_error.c_str(); }
+
+roast_status_t roast_create_ex(roast_t* out, int64_t mem_size, uint64_t seed, roast_tile_t tile,
+                               const roast_config_t* cfg_in) {
+  if (!out) return fail(ROAST_ERR_CONFIG, "null out");
+  roast_config_t cfg;
+  if (cfg_in)
+    cfg = *cfg_in;
+  else
+    roast_config_default(&cfg);
+  if (mem_size <= 0) return fail(ROAST_ERR_CONFIG, "mem_size must be > 0");
+  if (!(cfg.C > 0)) return fail(ROAST_ERR_CONFIG, "C must be > 0");
+  if (cfg.align_elems <= 0 || cfg.align_elems % 4 != 0)
+    return fail(ROAST_ERR_CONFIG, "align_elems must be a positive multiple of 4");
+  if (cfg.tile_layout != ROAST_ROW_MAJOR && cfg.tile_layout != ROAST_SW128)
+    return fail(ROAST_ERR_CONFIG, "bad tile_layout");
+  if (cfg.mapping != ROAST_MAP_HASH && cfg.mapping != ROAST_MAP_IDENTITY) return fail(ROAST_ERR_CONFIG, "bad mapping");
+  if (tile.z1 <= 0 || tile.z2 <= 0) return fail(ROAST_ERR_GEOMETRY, "tile dims must be > 0");
+  if (cfg.tile_layout == ROAST_SW128 && tile.z2 != 64)
+    return fail(ROAST_ERR_GEOMETRY, "SW128 tile layout needs Z2 = 64 (128-byte bf16 rows)");
+  Ctx* c = new Ctx();
+  c->mem_size = mem_size;
+  c->seed = seed;
+  c->tile = tile;
+  c->cfg = cfg;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&c->d_err), sizeof(int32_t));
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaMalloc(err flag)");
+  }
+  cudaMemset(c->d_err, 0, sizeof(int32_t));
+  *out = reinterpret_cast<roast_t>(c);
+  return ROAST_OK;
+}
+
+roast_status_t roast_create(roast_t* out, int64_t mem_size, uint64_t seed, roast_tile_t tile) {
+  return roast_create_ex(out, mem_size, seed, tile, nullptr);
+}
+
+roast_status_t roast_destroy(roast_t h) {
+  Ctx* c = ctx(h);
+  if (!c) return ROAST_OK;
+  cudaDeviceSynchronize();
+  for (auto& m : c->modules) free_module(m);
+  cudaFree(c->shadow);
+  cudaFree(c->d_err);
+  cudaFree(c->ws);
+  comm_destroy(c);
+  delete c;
+  return ROAST_OK;
+}
+
+roast_status_t roast_bind(roast_t h, float* d_M, float* d_dM, roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  if (!c) return fail(ROAST_ERR_STATE, "null handle");
+  if (!d_M || !d_dM) return fail(ROAST_ERR_CONFIG, "null M / dM");
+  if ((reinterpret_cast<uintptr_t>(d_M) | reinterpret_cast<uintptr_t>(d_dM)) & 15)
+    return fail(ROAST_ERR_CONFIG, "M and dM must be 16-byte aligned");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  c->M = d_M;
+  c->dM = d_dM;
+  if (!c->shadow) {
+    // [+bf16(M) | pad | -bf16(M) | 64-element tail pad]; the negated copy starts 128-B aligned
+    c->neg_base = (c->mem_size + 63) / 64 * 64;
+    c->shadow_elems = 2 * c->neg_base + 64;
+    ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->shadow), c->shadow_elems * sizeof(uint16_t)));
+    ROAST_CUDA_CHECK(cudaMemsetAsync(c->shadow, 0, c->shadow_elems * sizeof(uint16_t), s));
+    c->tmap_shadow_valid = false;
+  }
+  ROAST_CUDA_CHECK(launch_sync_shadow(c, s));
+  c->launches++;
+  return ROAST_OK;
+}
+
+roast_status_t roast_register_linear(roast_t h, int64_t H, int64_t O, int32_t* id) {
+  Ctx* c = ctx(h);
+  if (!c) return fail(ROAST_ERR_STATE, "null handle");
+  if (H <= 0 || O <= 0) return fail(ROAST_ERR_SHAPE, "in/out features must be > 0");
+  const int64_t z1 = c->tile.z1, z2 = c->tile.z2, T = z1 * z2, A = c->cfg.align_elems;
+  if (T > c->mem_size) return fail(ROAST_ERR_GEOMETRY, "tile Z1*Z2 larger than |M| (S:51)");
+  if (H % z1 || O % z2) return fail(ROAST_ERR_GEOMETRY, "in % Z1 and out % Z2 must be 0 on the GPU path (R9)");
+  if (T % A) return fail(ROAST_ERR_GEOMETRY, "Z1*Z2 must be a multiple of align_elems");
+  if (H / z1 >= (int64_t(1) << 28) || O / z2 >= (int64_t(1) << 31)) return fail(ROAST_ERR_GEOMETRY, "too many tiles");
+  Module m;
+  m.kind = kLinear;
+  m.H = H;
+  m.O = O;
+  m.nx = int32_t(H / z1);
+  m.ny = int32_t(O / z2);
+  const uint32_t mid = uint32_t(c->modules.size());
+  m.hash.off = make_coef(c->seed, mid, 0);
+  m.hash.sgn = make_coef(c->seed, mid, 1);
+  m.hash.R = uint64_t((c->mem_size - T) / A + 1);
+  m.hash.align = uint32_t(A);
+  m.hash.use_sign = c->cfg.use_sign ? 1u : 0u;
+  const int64_t nt = int64_t(m.nx) * m.ny;
+  m.h_off.resize(nt);
+  m.h_sgn.resize(nt);
+  if (c->cfg.mapping == ROAST_MAP_IDENTITY) {
+    if (c->identity_cursor + nt * T > c->mem_size) return fail(ROAST_ERR_GEOMETRY, "identity mapping needs |M| >= n");
+    for (int64_t t = 0; t < nt; ++t) {
+      m.h_off[t] = c->identity_cursor + T * t;
+      m.h_sgn[t] = 1;
+    }
+    c->identity_cursor += nt * T;
+    m.lam = 1.0f;
+  } else {
+    for (int32_t x = 0; x < m.nx; ++x)
+      for (int32_t y = 0; y < m.ny; ++y) {
+        uint64_t k = tile_key(uint32_t(x), uint32_t(y));
+        m.h_off[int64_t(x) * m.ny + y] = int64_t(m.hash.offset(k));
+        m.h_sgn[int64_t(x) * m.ny + y] = int8_t(m.hash.sign(k));
+      }
+    m.lam = float(c->cfg.C / sqrt(double(H)));
+  }
+  // offset-sorted tile order for the deterministic reduce (ties: tile id)
+  std::vector<int32_t> order(nt);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return m.h_off[a] < m.h_off[b]; });
+  std::vector<int64_t> soff(nt);
+  for (int64_t i = 0; i < nt; ++i) soff[i] = m.h_off[order[i]];
+  cudaError_t e = cudaSuccess;
+  e = cudaMalloc(reinterpret_cast<void**>(&m.d_off), nt * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&m.d_sgn), nt * sizeof(int8_t));
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&m.d_sorted), nt * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&m.d_sorted_off), nt * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMemcpy(m.d_off, m.h_off.data(), nt * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(m.d_sgn, m.h_sgn.data(), nt * sizeof(int8_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(m.d_sorted, order.data(), nt * sizeof(int32_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(m.d_sorted_off, soff.data(), nt * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    free_module(m);
+    return cuda_fail(e, "register_linear upload");
+  }
+  c->modules.push_back(std::move(m));
+  if (id) *id = int32_t(mid);
+  return ROAST_OK;
+}
+
+roast_status_t roast_register_embedding(roast_t h, int64_t num_rows, int32_t dim, int32_t chunk, double fan_in,
+                                        int32_t* id) {
+  Ctx* c = ctx(h);
+  if (!c) return fail(ROAST_ERR_STATE, "null handle");
+  if (num_rows <= 0 || dim <= 0 || chunk <= 0) return fail(ROAST_ERR_SHAPE, "rows, dim, chunk must be > 0");
+  const int64_t A = c->cfg.align_elems;
+  if (chunk > c->mem_size) return fail(ROAST_ERR_GEOMETRY, "chunk larger than |M|");
+  if (chunk % A || chunk % 4 || dim % 4) return fail(ROAST_ERR_GEOMETRY, "chunk % A, chunk % 4 and dim % 4 must be 0");
+  Module m;
+  m.kind = kEmbedding;
+  m.rows = num_rows;
+  m.dim = dim;
+  m.chunk = chunk;
+  m.chunks_per_row = (dim + chunk - 1) / chunk;
+  if (double(num_rows) * m.chunks_per_row >= double(int64_t(1) << 60)) return fail(ROAST_ERR_GEOMETRY, "too many chunks");
+  const uint32_t mid = uint32_t(c->modules.size());
+  m.hash.off = make_coef(c->seed, mid, 0);
+  m.hash.sgn = make_coef(c->seed, mid, 1);
+  m.hash.R = uint64_t((c->mem_size - chunk) / A + 1);
+  m.hash.align = uint32_t(A);
+  m.hash.use_sign = c->cfg.use_sign ? 1u : 0u;
+  m.lam = float(c->cfg.C / sqrt(fan_in > 0 ? fan_in : double(dim)));
+  c->modules.push_back(std::move(m));
+  if (id) *id = int32_t(mid);
+  return ROAST_OK;
+}
+
+static bool use_sm100(const Ctx* c, const Module& m) {
+  return c->tile.z1 == 64 && c->tile.z2 == 64 && m.H % 64 == 0 && m.O % 64 == 0 &&
+         getenv("ROAST_FORCE_SIMT") == nullptr;
+}
+
+roast_status_t roast_linear_fwd(roast_t h, int32_t id, const void* X, void* Y, int64_t T, roast_dtype_t dt,
+                                roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module* m;
+  roast_status_t st = get_module(c, id, kLinear, &m);
+  if (st) return st;
+  if (T < 0) return fail(ROAST_ERR_SHAPE, "tokens < 0");
+  if (T > 0 && (!X || !Y)) return fail(ROAST_ERR_CONFIG, "null X / Y");
+  if (dt != ROAST_FP32 && dt != ROAST_BF16) return fail(ROAST_ERR_CONFIG, "bad dtype");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (T == 0) return ROAST_OK;
+  if (dt == ROAST_BF16 && use_sm100(c, *m)) {
+    st = sm100_fwd(c, *m, X, Y, T, s);
+    if (st != ROAST_ERR_UNSUPPORTED) return st;
+  }
+  ROAST_CUDA_CHECK(launch_simt_fwd(c, *m, X, Y, T, dt, false, s));
+  c->launches++;
+  return ROAST_OK;
+}
+
+static roast_status_t linear_args(Ctx* c, int32_t id, int64_t T, roast_dtype_t dt, const void* a, const void* b,
+                                  Module** m) {
+  roast_status_t st = get_module(c, id, kLinear, m);
+  if (st) return st;
+  if (T < 0) return fail(ROAST_ERR_SHAPE, "tokens < 0");
+  if (T > 0 && (!a || !b)) return fail(ROAST_ERR_CONFIG, "null tensor argument");
+  if (dt != ROAST_FP32 && dt != ROAST_BF16) return fail(ROAST_ERR_CONFIG, "bad dtype");
+  return ROAST_OK;
+}
+
+roast_status_t roast_linear_bwd_dx(roast_t h, int32_t id, const void* dY, void* dX, int64_t T, roast_dtype_t dt,
+                                   roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module* m;
+  roast_status_t st = linear_args(c, id, T, dt, dY, dX, &m);
+  if (st || T == 0) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // a2: dX = lambda dY W~^T
+  if (dt == ROAST_BF16 && use_sm100(c, *m)) {
+    st = sm100_dx(c, *m, dY, dX, T, s);
+    if (st != ROAST_ERR_UNSUPPORTED) return st;
+  }
+  ROAST_CUDA_CHECK(launch_simt_fwd(c, *m, dY, dX, T, dt, true, s));
+  c->launches++;
+  return ROAST_OK;
+}
+
+roast_status_t roast_linear_bwd_dm(roast_t h, int32_t id, const void* X, const void* dY, int64_t T, roast_dtype_t dt,
+                                   roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module* m;
+  roast_status_t st = linear_args(c, id, T, dt, X, dY, &m);
+  if (st || T == 0) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // a3: dM += scatter(lambda g X^T dY)
+  if (dt == ROAST_BF16 && use_sm100(c, *m)) {
+    st = sm100_dw(c, *m, X, dY, T, s);
+    if (st != ROAST_ERR_UNSUPPORTED) return st;
+  }
+  if (c->cfg.deterministic) {
+    const size_t bytes = size_t(m->nx) * m->ny * c->tile.z1 * c->tile.z2 * sizeof(float);
+    st = ensure_ws(c, bytes, s);
+    if (st) return st;
+    ROAST_CUDA_CHECK(launch_simt_dw(c, *m, X, dY, T, dt, c->ws, s));
+    ROAST_CUDA_CHECK(launch_det_reduce(c, *m, c->ws, 1, s));
+    c->launches += 2;
+  } else {
+    ROAST_CUDA_CHECK(launch_simt_dw(c, *m, X, dY, T, dt, nullptr, s));
+    c->launches++;
+  }
+  return ROAST_OK;
+}
+
+roast_status_t roast_linear_bwd(roast_t h, int32_t id, const void* X, const void* dY, void* dX, int64_t T,
+                                roast_dtype_t dt, roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module* m;
+  roast_status_t st = linear_args(c, id, T, dt, X, dY, &m);
+  if (st || T == 0) return st;
+  if (dX) {
+    st = roast_linear_bwd_dx(h, id, dY, dX, T, dt, stream);
+    if (st) return st;
+  }
+  return roast_linear_bwd_dm(h, id, X, dY, T, dt, stream);
+}
+
+roast_status_t roast_embedding_fwd(roast_t h, int32_t id, const int64_t* idx, int64_t n, float* out,
+                                   roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module* m;
+  roast_status_t st = get_module(c, id, kEmbedding, &m);
+  if (st) return st;
+  if (n < 0) return fail(ROAST_ERR_SHAPE, "n < 0");
+  if (n > 0 && (!idx || !out)) return fail(ROAST_ERR_CONFIG, "null idx / out");
+  if (reinterpret_cast<uintptr_t>(out) & 15) return fail(ROAST_ERR_CONFIG, "out must be 16-byte aligned");
+  ROAST_CUDA_CHECK(launch_embed_fwd(c, *m, idx, n, out, reinterpret_cast<cudaStream_t>(stream)));
+  c->launches++;
+  return ROAST_OK;
+}
+
+roast_status_t roast_embedding_bwd(roast_t h, int32_t id, const int64_t* idx, int64_t n, const float* dOut,
+                                   roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module* m;
+  roast_status_t st = get_module(c, id, kEmbedding, &m);
+  if (st) return st;
+  if (n < 0) return fail(ROAST_ERR_SHAPE, "n < 0");
+  if (n > 0 && (!idx || !dOut)) return fail(ROAST_ERR_CONFIG, "null idx / dOut");
+  if (reinterpret_cast<uintptr_t>(dOut) & 15) return fail(ROAST_ERR_CONFIG, "dOut must be 16-byte aligned");
+  ROAST_CUDA_CHECK(launch_embed_bwd(c, *m, idx, n, dOut, reinterpret_cast<cudaStream_t>(stream)));
+  c->launches++;
+  return ROAST_OK;
+}
+
+roast_status_t roast_zero_grad(roast_t h, roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  if (!c || !c->dM) return fail(ROAST_ERR_STATE, "not bound");
+  ROAST_CUDA_CHECK(cudaMemsetAsync(c->dM, 0, c->mem_size * sizeof(float), reinterpret_cast<cudaStream_t>(stream)));
+  return ROAST_OK;
+}
+
+roast_status_t roast_sync_shadow(roast_t h, roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  if (!c || !c->M || !c->shadow) return fail(ROAST_ERR_STATE, "not bound");
+  ROAST_CUDA_CHECK(launch_sync_shadow(c, reinterpret_cast<cudaStream_t>(stream)));
+  c->launches++;
+  return ROAST_OK;
+}
+
+roast_status_t roast_sgd_step(roast_t h, float lr, roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  if (!c || !c->M || !c->shadow) return fail(ROAST_ERR_STATE, "not bound");
+  ROAST_CUDA_CHECK(launch_sgd(c, lr, reinterpret_cast<cudaStream_t>(stream)));
+  c->launches++;
+  return ROAST_OK;
+}
+
+roast_status_t roast_get_error(roast_t h) {
+  Ctx* c = ctx(h);
+  if (!c) return fail(ROAST_ERR_STATE, "null handle");
+  int32_t v = 0;
+  cudaError_t e = cudaMemcpy(&v, c->d_err, sizeof(v), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "read error flag");
+  if (v) return fail(ROAST_ERR_BOUNDS, "embedding index out of range (sticky)");
+  return ROAST_OK;
+}
+
+roast_status_t roast_debug_tile_map(roast_t h, int32_t id, int64_t* off_host, int8_t* sgn_host) {
+  Ctx* c = ctx(h);
+  if (!c) return fail(ROAST_ERR_STATE, "null handle");
+  if (id < 0 || id >= int32_t(c->modules.size()) || c->modules[id].kind != kLinear)
+    return fail(ROAST_ERR_STATE, "not a linear module");
+  Module& m = c->modules[id];
+  const int64_t nt = int64_t(m.nx) * m.ny;
+  // read back the DEVICE copy the kernels use
+  if (off_host) ROAST_CUDA_CHECK(cudaMemcpy(off_host, m.d_off, nt * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  if (sgn_host) ROAST_CUDA_CHECK(cudaMemcpy(sgn_host, m.d_sgn, nt * sizeof(int8_t), cudaMemcpyDeviceToHost));
+  return ROAST_OK;
+}
+
+roast_status_t roast_debug_chunk_map(roast_t h, int32_t id, const int64_t* rows, int64_t n, int64_t* off,
+                                     int8_t* sgn, roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  if (!c) return fail(ROAST_ERR_STATE, "null handle");
+  if (id < 0 || id >= int32_t(c->modules.size()) || c->modules[id].kind != kEmbedding)
+    return fail(ROAST_ERR_STATE, "not an embedding module");
+  ROAST_CUDA_CHECK(launch_chunk_map(c, c->modules[id], rows, n, off, sgn, reinterpret_cast<cudaStream_t>(stream)));
+  c->launches++;
+  return ROAST_OK;
+}
+
+roast_status_t roast_debug_materialize(roast_t h, int32_t id, roast_dtype_t dt, void* W, roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module* m;
+  roast_status_t st = get_module(c, id, kLinear, &m);
+  if (st) return st;
+  ROAST_CUDA_CHECK(launch_materialize(c, *m, dt, W, reinterpret_cast<cudaStream_t>(stream)));
+  c->launches++;
+  return ROAST_OK;
+}
+
+int64_t roast_launch_count(roast_t h) {
+  Ctx* c = ctx(h);
+  return c ? c->launches : -1;
+}
+
+}  // extern "C"

@@ -1,0 +1,99 @@
+// roast_internal.h — handle state shared by the C-ABI layer and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/roast.h"
+#include "roast_hash.cuh"
+
+namespace roast {
+
+enum ModuleKind { kLinear = 0, kEmbedding = 1 };
+
+struct Module {
+  ModuleKind kind;
+  float lam;
+  ModuleHash hash;
+  // linear
+  int64_t H = 0, O = 0;
+  int32_t nx = 0, ny = 0;         // tile grid
+  int64_t* d_off = nullptr;       // [nx * ny] tile offsets (elements)
+  int8_t* d_sgn = nullptr;        // [nx * ny] tile signs
+  std::vector<int64_t> h_off;     // host copies
+  std::vector<int8_t> h_sgn;
+  // deterministic reduce (K5): tiles sorted by (offset, tile id); the kernel
+  // binary-searches the covering range [lo, hi) of every A-aligned slot group.
+  int32_t* d_sorted = nullptr;    // [ntiles] tile ids
+  int64_t* d_sorted_off = nullptr;// [ntiles]
+  // embedding
+  int64_t rows = 0;
+  int32_t dim = 0, chunk = 0, chunks_per_row = 0;
+};
+
+struct Ctx {
+  int64_t mem_size = 0;
+  uint64_t seed = 0;
+  roast_tile_t tile{0, 0};
+  roast_config_t cfg{};
+  float* M = nullptr;
+  float* dM = nullptr;
+  uint16_t* shadow = nullptr;     // [2 * mem_size + pad] bf16 bits: +bf16(M) then -bf16(M)
+  int64_t shadow_elems = 0;
+  int64_t neg_base = 0;           // index of the negated copy (128-B aligned)
+  std::vector<Module> modules;
+  int64_t identity_cursor = 0;    // IDENTITY mapping: next free base
+  // device error flag (sticky)
+  int32_t* d_err = nullptr;
+  // workspace (deterministic dM / split-K partials), grown on demand
+  float* ws = nullptr;
+  size_t ws_bytes = 0;
+  // comm
+  void* nccl_comm = nullptr;
+  int32_t rank = 0, world = 1;
+  int64_t launches = 0;
+  // tcgen05 path: cached TMA descriptors of the shadow (rebuilt on bind)
+  alignas(64) unsigned char tmap_shadow[128];
+  bool tmap_shadow_valid = false;
+};
+
+// error reporting (thread-local detail string)
+roast_status_t fail(roast_status_t st, const std::string& msg);
+roast_status_t cuda_fail(cudaError_t e, const char* what);
+#define ROAST_CUDA_CHECK(call)                                   \
+  do {                                                           \
+    cudaError_t _e = (call);                                     \
+    if (_e != cudaSuccess) return ::roast::cuda_fail(_e, #call); \
+  } while (0)
+
+void comm_destroy(Ctx* c);
+
+// workspace of at least `bytes`, stream-ordered
+roast_status_t ensure_ws(Ctx* c, size_t bytes, cudaStream_t s);
+
+// ---- kernel launchers (return cudaError_t of the launch) ----------------------
+// SIMT paths (any tile geometry), T = float or bf16 storage selected by dt
+cudaError_t launch_simt_fwd(const Ctx* c, const Module& m, const void* X, void* Y, int64_t T, roast_dtype_t dt,
+                            bool transpose_w, cudaStream_t s);
+cudaError_t launch_simt_dw(const Ctx* c, const Module& m, const void* X, const void* dY, int64_t T,
+                           roast_dtype_t dt, float* ws, cudaStream_t s);
+cudaError_t launch_det_reduce(const Ctx* c, const Module& m, const float* ws, int nsplit, cudaStream_t s);
+cudaError_t launch_sync_shadow(Ctx* c, cudaStream_t s);
+cudaError_t launch_sgd(Ctx* c, float lr, cudaStream_t s);
+cudaError_t launch_materialize(const Ctx* c, const Module& m, roast_dtype_t dt, void* W, cudaStream_t s);
+cudaError_t launch_embed_fwd(const Ctx* c, const Module& m, const int64_t* idx, int64_t n, float* out,
+                             cudaStream_t s);
+cudaError_t launch_embed_bwd(const Ctx* c, const Module& m, const int64_t* idx, int64_t n, const float* dOut,
+                             cudaStream_t s);
+cudaError_t launch_chunk_map(const Ctx* c, const Module& m, const int64_t* rows, int64_t n, int64_t* off,
+                             int8_t* sgn, cudaStream_t s);
+
+// tcgen05 paths (bf16, Z1 = Z2 = 64)
+roast_status_t sm100_prepare(Ctx* c);  // build shadow tensor map
+roast_status_t sm100_fwd(Ctx* c, const Module& m, const void* X, void* Y, int64_t T, cudaStream_t s);
+roast_status_t sm100_dx(Ctx* c, const Module& m, const void* dY, void* dX, int64_t T, cudaStream_t s);
+roast_status_t sm100_dw(Ctx* c, const Module& m, const void* X, const void* dY, int64_t T, cudaStream_t s);
+
+}  // namespace roast

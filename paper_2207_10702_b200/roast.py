@@ -1,0 +1,338 @@
+"""Thin ctypes binding of libroast.so (include/roast.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels
+of libroast.so.  Functions keep the C names; `Roast` is a small convenience
+wrapper that takes torch tensors (device memory and streams come from torch —
+plumbing, not the product).  If the library is missing the import of this
+module raises: there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libroast.so")
+
+OK, ERR_CONFIG, ERR_GEOMETRY, ERR_SHAPE, ERR_BOUNDS, ERR_CAPACITY, ERR_STATE, ERR_CUDA, ERR_NCCL, \
+    ERR_UNSUPPORTED = range(10)
+FP32, BF16 = 0, 1
+ROW_MAJOR, SW128 = 0, 1
+MAP_HASH, MAP_IDENTITY = 0, 1
+
+EXPORTS = [
+    "roast_config_default", "roast_create", "roast_create_ex", "roast_destroy", "roast_bind",
+    "roast_register_linear", "roast_register_embedding", "roast_linear_fwd", "roast_linear_bwd",
+    "roast_linear_bwd_dx", "roast_linear_bwd_dm", "roast_embedding_fwd", "roast_embedding_bwd", "roast_comm_unique_id", "roast_comm_init",
+    "roast_grad_allreduce", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_get_error",
+    "roast_status_str", "roast_last_error", "roast_debug_tile_map", "roast_debug_chunk_map",
+    "roast_debug_materialize", "roast_launch_count",
+]
+
+
+class roast_tile_t(ctypes.Structure):
+    _fields_ = [("z1", ctypes.c_int32), ("z2", ctypes.c_int32)]
+
+
+class roast_config_t(ctypes.Structure):
+    _fields_ = [("C", ctypes.c_double), ("align_elems", ctypes.c_int32), ("tile_layout", ctypes.c_int32),
+                ("mapping", ctypes.c_int32), ("use_sign", ctypes.c_int32), ("deterministic", ctypes.c_int32)]
+
+
+class RoastError(RuntimeError):
+    def __init__(self, status, where):
+        self.status = status
+        super().__init__(f"{where}: {_lib.roast_status_str(status).decode()} ({status}): "
+                         f"{_lib.roast_last_error().decode()}")
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2207_10702_b200.build` "
+                          "(no CPU fallback exists)")
+    lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    H, I32, I64, U64, P, S = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
+                              ctypes.c_void_p, ctypes.c_void_p)
+    st = ctypes.c_int
+    sig = {
+        "roast_config_default": (None, [ctypes.POINTER(roast_config_t)]),
+        "roast_create": (st, [ctypes.POINTER(H), I64, U64, roast_tile_t]),
+        "roast_create_ex": (st, [ctypes.POINTER(H), I64, U64, roast_tile_t, ctypes.POINTER(roast_config_t)]),
+        "roast_destroy": (st, [H]),
+        "roast_bind": (st, [H, P, P, S]),
+        "roast_register_linear": (st, [H, I64, I64, ctypes.POINTER(I32)]),
+        "roast_register_embedding": (st, [H, I64, I32, I32, ctypes.c_double, ctypes.POINTER(I32)]),
+        "roast_linear_fwd": (st, [H, I32, P, P, I64, ctypes.c_int, S]),
+        "roast_linear_bwd": (st, [H, I32, P, P, P, I64, ctypes.c_int, S]),
+        "roast_linear_bwd_dx": (st, [H, I32, P, P, I64, ctypes.c_int, S]),
+        "roast_linear_bwd_dm": (st, [H, I32, P, P, I64, ctypes.c_int, S]),
+        "roast_embedding_fwd": (st, [H, I32, P, I64, P, S]),
+        "roast_embedding_bwd": (st, [H, I32, P, I64, P, S]),
+        "roast_comm_unique_id": (st, [ctypes.c_char_p]),
+        "roast_comm_init": (st, [H, I32, I32, ctypes.c_char_p]),
+        "roast_grad_allreduce": (st, [H, S]),
+        "roast_zero_grad": (st, [H, S]),
+        "roast_sync_shadow": (st, [H, S]),
+        "roast_sgd_step": (st, [H, ctypes.c_float, S]),
+        "roast_get_error": (st, [H]),
+        "roast_status_str": (ctypes.c_char_p, [st]),
+        "roast_last_error": (ctypes.c_char_p, []),
+        "roast_debug_tile_map": (st, [H, I32, P, P]),
+        "roast_debug_chunk_map": (st, [H, I32, P, I64, P, P, S]),
+        "roast_debug_materialize": (st, [H, I32, ctypes.c_int, P, S]),
+        "roast_launch_count": (I64, [H]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+
+def _check(status, where):
+    if status != OK:
+        raise RoastError(status, where)
+
+
+# ---- same-name functions (thin) ----------------------------------------------------------
+def roast_config_default():
+    cfg = roast_config_t()
+    _lib.roast_config_default(ctypes.byref(cfg))
+    return cfg
+
+
+def roast_create(mem_size, seed, z1, z2, cfg=None):
+    h = ctypes.c_void_p()
+    if cfg is None:
+        _check(_lib.roast_create(ctypes.byref(h), mem_size, seed, roast_tile_t(z1, z2)), "roast_create")
+    else:
+        _check(_lib.roast_create_ex(ctypes.byref(h), mem_size, seed, roast_tile_t(z1, z2), ctypes.byref(cfg)),
+               "roast_create_ex")
+    return h
+
+
+def roast_destroy(h):
+    _check(_lib.roast_destroy(h), "roast_destroy")
+
+
+def roast_bind(h, M_ptr, dM_ptr, stream=0):
+    _check(_lib.roast_bind(h, M_ptr, dM_ptr, stream), "roast_bind")
+
+
+def roast_register_linear(h, in_features, out_features):
+    i = ctypes.c_int32()
+    _check(_lib.roast_register_linear(h, in_features, out_features, ctypes.byref(i)), "roast_register_linear")
+    return i.value
+
+
+def roast_register_embedding(h, num_rows, dim, chunk, fan_in=0.0):
+    i = ctypes.c_int32()
+    _check(_lib.roast_register_embedding(h, num_rows, dim, chunk, fan_in, ctypes.byref(i)),
+           "roast_register_embedding")
+    return i.value
+
+
+def roast_linear_fwd(h, mid, X_ptr, Y_ptr, tokens, dtype, stream=0):
+    _check(_lib.roast_linear_fwd(h, mid, X_ptr, Y_ptr, tokens, dtype, stream), "roast_linear_fwd")
+
+
+def roast_linear_bwd(h, mid, X_ptr, dY_ptr, dX_ptr, tokens, dtype, stream=0):
+    _check(_lib.roast_linear_bwd(h, mid, X_ptr, dY_ptr, dX_ptr, tokens, dtype, stream), "roast_linear_bwd")
+
+
+def roast_linear_bwd_dx(h, mid, dY_ptr, dX_ptr, tokens, dtype, stream=0):
+    _check(_lib.roast_linear_bwd_dx(h, mid, dY_ptr, dX_ptr, tokens, dtype, stream), "roast_linear_bwd_dx")
+
+
+def roast_linear_bwd_dm(h, mid, X_ptr, dY_ptr, tokens, dtype, stream=0):
+    _check(_lib.roast_linear_bwd_dm(h, mid, X_ptr, dY_ptr, tokens, dtype, stream), "roast_linear_bwd_dm")
+
+
+def roast_embedding_fwd(h, mid, idx_ptr, n, out_ptr, stream=0):
+    _check(_lib.roast_embedding_fwd(h, mid, idx_ptr, n, out_ptr, stream), "roast_embedding_fwd")
+
+
+def roast_embedding_bwd(h, mid, idx_ptr, n, dout_ptr, stream=0):
+    _check(_lib.roast_embedding_bwd(h, mid, idx_ptr, n, dout_ptr, stream), "roast_embedding_bwd")
+
+
+def roast_comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.roast_comm_unique_id(buf), "roast_comm_unique_id")
+    return buf.raw
+
+
+def roast_comm_init(h, rank, world, uid: bytes):
+    _check(_lib.roast_comm_init(h, rank, world, uid), "roast_comm_init")
+
+
+def roast_grad_allreduce(h, stream=0):
+    _check(_lib.roast_grad_allreduce(h, stream), "roast_grad_allreduce")
+
+
+def roast_zero_grad(h, stream=0):
+    _check(_lib.roast_zero_grad(h, stream), "roast_zero_grad")
+
+
+def roast_sync_shadow(h, stream=0):
+    _check(_lib.roast_sync_shadow(h, stream), "roast_sync_shadow")
+
+
+def roast_sgd_step(h, lr, stream=0):
+    _check(_lib.roast_sgd_step(h, lr, stream), "roast_sgd_step")
+
+
+def roast_get_error(h):
+    return _lib.roast_get_error(h)
+
+
+def roast_debug_tile_map(h, mid, off_ptr, sgn_ptr):
+    _check(_lib.roast_debug_tile_map(h, mid, off_ptr, sgn_ptr), "roast_debug_tile_map")
+
+
+def roast_debug_chunk_map(h, mid, rows_ptr, n, off_ptr, sgn_ptr, stream=0):
+    _check(_lib.roast_debug_chunk_map(h, mid, rows_ptr, n, off_ptr, sgn_ptr, stream), "roast_debug_chunk_map")
+
+
+def roast_debug_materialize(h, mid, dtype, W_ptr, stream=0):
+    _check(_lib.roast_debug_materialize(h, mid, dtype, W_ptr, stream), "roast_debug_materialize")
+
+
+def roast_launch_count(h):
+    return _lib.roast_launch_count(h)
+
+
+# ---- torch convenience wrapper --------------------------------------------------------------
+class Roast:
+    """One handle + its caller-owned M / dM (torch fp32 CUDA tensors)."""
+
+    def __init__(self, M, z1, z2, seed=0x5EED, C=1.0, align=8, tile_layout=ROW_MAJOR, mapping=MAP_HASH,
+                 use_sign=True, deterministic=False, dM=None):
+        import torch
+        assert M.is_cuda and M.dtype == torch.float32 and M.is_contiguous()
+        self.torch = torch
+        self.M = M
+        self.dM = torch.zeros_like(M) if dM is None else dM
+        cfg = roast_config_default()
+        cfg.C, cfg.align_elems, cfg.tile_layout = C, align, tile_layout
+        cfg.mapping, cfg.use_sign, cfg.deterministic = mapping, int(use_sign), int(deterministic)
+        self.mem_size = M.numel()
+        self.z1, self.z2 = z1, z2
+        self.h = roast_create(self.mem_size, seed, z1, z2, cfg)
+        self.dims = {}
+        roast_bind(self.h, M.data_ptr(), self.dM.data_ptr(), self._s())
+
+    def _s(self, stream=None):
+        s = stream if stream is not None else self.torch.cuda.current_stream()
+        return s.cuda_stream
+
+    def close(self):
+        if self.h:
+            roast_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def linear(self, in_features, out_features):
+        mid = roast_register_linear(self.h, in_features, out_features)
+        self.dims[mid] = ("linear", in_features, out_features)
+        return mid
+
+    def embedding(self, num_rows, dim, chunk, fan_in=0.0):
+        mid = roast_register_embedding(self.h, num_rows, dim, chunk, fan_in)
+        self.dims[mid] = ("embedding", num_rows, dim, chunk)
+        return mid
+
+    @staticmethod
+    def _dt(t):
+        import torch
+        return BF16 if t.dtype == torch.bfloat16 else FP32
+
+    def fwd(self, mid, X, Y=None, stream=None):
+        _, H, O = self.dims[mid]
+        assert X.is_contiguous() and X.shape[-1] == H
+        T = X.numel() // H
+        if Y is None:
+            Y = self.torch.empty(*X.shape[:-1], O, dtype=X.dtype, device=X.device)
+        roast_linear_fwd(self.h, mid, X.data_ptr(), Y.data_ptr(), T, self._dt(X), self._s(stream))
+        return Y
+
+    def bwd(self, mid, X, dY, dX=None, need_dx=True, stream=None):
+        _, H, O = self.dims[mid]
+        T = X.numel() // H
+        assert dY.numel() == T * O and X.dtype == dY.dtype
+        if need_dx and dX is None:
+            dX = self.torch.empty_like(X)
+        roast_linear_bwd(self.h, mid, X.data_ptr(), dY.data_ptr(), dX.data_ptr() if need_dx else None, T,
+                         self._dt(X), self._s(stream))
+        return dX
+
+    def bwd_dx(self, mid, dY, dX, stream=None):
+        _, H, O = self.dims[mid]
+        roast_linear_bwd_dx(self.h, mid, dY.data_ptr(), dX.data_ptr(), dY.numel() // O, self._dt(dY),
+                            self._s(stream))
+        return dX
+
+    def bwd_dm(self, mid, X, dY, stream=None):
+        _, H, O = self.dims[mid]
+        roast_linear_bwd_dm(self.h, mid, X.data_ptr(), dY.data_ptr(), X.numel() // H, self._dt(X),
+                            self._s(stream))
+
+    def emb_fwd(self, mid, idx, out=None, stream=None):
+        _, rows, dim, chunk = self.dims[mid]
+        if out is None:
+            out = self.torch.empty(idx.numel(), dim, dtype=self.torch.float32, device=idx.device)
+        roast_embedding_fwd(self.h, mid, idx.data_ptr(), idx.numel(), out.data_ptr(), self._s(stream))
+        return out
+
+    def emb_bwd(self, mid, idx, dout, stream=None):
+        roast_embedding_bwd(self.h, mid, idx.data_ptr(), idx.numel(), dout.data_ptr(), self._s(stream))
+
+    def zero_grad(self, stream=None):
+        roast_zero_grad(self.h, self._s(stream))
+
+    def sync_shadow(self, stream=None):
+        roast_sync_shadow(self.h, self._s(stream))
+
+    def sgd(self, lr, stream=None):
+        roast_sgd_step(self.h, lr, self._s(stream))
+
+    def allreduce(self, stream=None):
+        roast_grad_allreduce(self.h, self._s(stream))
+
+    def tile_map(self, mid):
+        import numpy as np
+        _, H, O = self.dims[mid]
+        n = (H // self.z1) * (O // self.z2)
+        off = np.zeros(n, dtype=np.int64)
+        sgn = np.zeros(n, dtype=np.int8)
+        roast_debug_tile_map(self.h, mid, off.ctypes.data, sgn.ctypes.data)
+        return off.reshape(H // self.z1, O // self.z2), sgn.reshape(H // self.z1, O // self.z2)
+
+    def chunk_map(self, mid, rows):
+        _, nrows, dim, chunk = self.dims[mid]
+        q = -(-dim // chunk)
+        off = self.torch.empty(rows.numel(), q, dtype=self.torch.int64, device=rows.device)
+        sgn = self.torch.empty(rows.numel(), q, dtype=self.torch.int8, device=rows.device)
+        roast_debug_chunk_map(self.h, mid, rows.data_ptr(), rows.numel(), off.data_ptr(), sgn.data_ptr(),
+                              self._s())
+        return off, sgn
+
+    def materialize(self, mid, dtype):
+        _, H, O = self.dims[mid]
+        W = self.torch.empty(H, O, dtype=dtype, device=self.M.device)
+        roast_debug_materialize(self.h, mid, self._dt(W), W.data_ptr(), self._s())
+        return W
+
+    def check(self):
+        _check(roast_get_error(self.h), "roast_get_error")
+
+    def launch_count(self):
+        return roast_launch_count(self.h)

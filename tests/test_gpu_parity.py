@@ -1,0 +1,243 @@
+"""GPU <-> oracle parity through the C ABI (run on a B200: pytest -m gpu).
+
+Tolerances (BASELINE.json north_star): mapping, recovered tiles and embedding
+values bit-exact; fp32 path rel. Frobenius <= 1e-5; bf16 path <= 1e-2;
+deterministic dM bitwise reproducible.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import embedding as OE
+from oracle import roast_mm as OM
+from tests.gpu_helpers import bf16_input, rel_frob, store, to_dev
+
+pytestmark = pytest.mark.gpu
+
+HS = synth.HASH_SEED
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+@pytest.fixture(scope="module")
+def R():
+    from paper_2207_10702_b200 import roast   # raises if libroast.so is missing: no fallback
+    return roast
+
+
+def make_ctx(R, torch, M_np, z1, z2, **kw):
+    M = to_dev(M_np, torch.float32)
+    return R.Roast(M, z1, z2, seed=HS, **kw), M
+
+
+# ---------------------------------------------------------------- a0: the mapping
+@pytest.mark.parametrize("mem,z,layers", [
+    (8192, 32, [(256, 256)]),                                           # C1
+    (synth.mlp_block(100)["mem_size"], 64, [(768, 3072), (3072, 768)]),   # C2 100x
+    (synth.mlp_block(1000)["mem_size"], 64, [(768, 3072), (3072, 768)]),  # C2 1000x
+])
+def test_tile_map_bit_exact(R, torch, mem, z, layers):
+    ctx, _ = make_ctx(R, torch, np.zeros(mem, np.float32), z, z)
+    for mid, (H, O) in enumerate(layers):
+        assert ctx.linear(H, O) == mid
+        spec = OM.LinearSpec(H, O, z, z, mem, HS, mid)
+        off, sgn = ctx.tile_map(mid)
+        assert np.array_equal(off, spec.off)
+        assert np.array_equal(sgn.astype(np.int64), spec.sgn)
+
+
+def test_chunk_map_bit_exact(R, torch):
+    mem = 33_280_000
+    ctx, _ = make_ctx(R, torch, np.zeros(mem, np.float32), 64, 64)
+    rows_np = np.concatenate([synth.uniform_indices(synth.SEED_IDX, 3000, 10 ** 7),
+                              [0, 1, 10 ** 7 - 1]])
+    for table in range(3):
+        mid = ctx.embedding(10 ** 7, 128, 32)
+        off, sgn = ctx.chunk_map(mid, to_dev(rows_np, torch.int64))
+        spec = OE.EmbeddingSpec(10 ** 7, 128, 32, mem, HS, mid)
+        o_ref, s_ref = spec.chunk_map(rows_np)
+        assert np.array_equal(off.cpu().numpy(), o_ref)
+        assert np.array_equal(sgn.cpu().numpy().astype(np.int64), s_ref)
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+def test_recovered_weights_bit_exact(R, torch, layout):
+    mem = 47192
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64, tile_layout=layout)
+    mid = ctx.linear(768, 3072)
+    spec = OM.LinearSpec(768, 3072, 64, 64, mem, HS, mid, layout=layout)
+    W32 = ctx.materialize(mid, torch.float32).cpu().numpy()
+    assert np.array_equal(W32.astype(np.float64), spec.materialize(M_np, "fp32"))
+    Wbf = ctx.materialize(mid, torch.bfloat16).float().cpu().numpy()
+    assert np.array_equal(Wbf.astype(np.float64), spec.materialize(M_np, "operand"))
+
+
+# ---------------------------------------------------------------- a1-a3: ROAST-MM
+def run_linear(R, torch, ctx, mid, X_np, dY_np, dtype):
+    X = to_dev(X_np, dtype)
+    dY = to_dev(dY_np, dtype)
+    ctx.zero_grad()
+    Y = ctx.fwd(mid, X)
+    dX = ctx.bwd(mid, X, dY)
+    torch.cuda.synchronize()
+    return (Y.float().cpu().numpy(), dX.float().cpu().numpy(), ctx.dM.cpu().numpy().astype(np.float64))
+
+
+@pytest.mark.parametrize("deterministic", [False, True])
+@pytest.mark.parametrize("T", [64, 1, 130])
+def test_c1_fp32_path(R, torch, deterministic, T):
+    """C1: 256x256, tile 32x32, |M| = 8192 (8x), fp32 path, <= 1e-5."""
+    M_np = store(8192)
+    ctx, _ = make_ctx(R, torch, M_np, 32, 32, deterministic=deterministic)
+    mid = ctx.linear(256, 256)
+    X = synth.uniform(synth.SEED_X, (T, 256)).astype(np.float32)
+    dY = synth.uniform(synth.SEED_DY, (T, 256)).astype(np.float32)
+    Y, dX, dM = run_linear(R, torch, ctx, mid, X, dY, torch.float32)
+    spec = OM.LinearSpec(256, 256, 32, 32, 8192, HS, mid)
+    assert rel_frob(Y, spec.forward(X, M_np)) <= 1e-5
+    assert rel_frob(dX, spec.backward_dx(dY, M_np)) <= 1e-5
+    assert rel_frob(dM, spec.backward_dm(X, dY)) <= 1e-5
+
+
+def test_c1_bf16_variant(R, torch):
+    M_np = store(8192)
+    ctx, _ = make_ctx(R, torch, M_np, 32, 32)
+    mid = ctx.linear(256, 256)
+    X = bf16_input(synth.SEED_X, (64, 256), "uniform")
+    dY = bf16_input(synth.SEED_DY, (64, 256), "uniform")
+    Y, dX, dM = run_linear(R, torch, ctx, mid, X, dY, torch.bfloat16)
+    spec = OM.LinearSpec(256, 256, 32, 32, 8192, HS, mid)
+    assert rel_frob(Y, spec.forward(X, M_np, bf16_operand=True)) <= 1e-2
+    assert rel_frob(dX, spec.backward_dx(dY, M_np, bf16_operand=True)) <= 1e-2
+    assert rel_frob(dM, spec.backward_dm(X, dY)) <= 1e-2
+
+
+def test_deterministic_dm_bitwise_reproducible(R, torch):
+    for dtype, z, shape, T in [(torch.float32, 32, (256, 256), 64), (torch.bfloat16, 64, (768, 3072), 512)]:
+        H, O = shape
+        mem = 8192 if z == 32 else 47192
+        M_np = store(mem)
+        ctx, _ = make_ctx(R, torch, M_np, z, z, deterministic=True)
+        mid = ctx.linear(H, O)
+        X = to_dev(bf16_input(synth.SEED_X, (T, H)), dtype)
+        dY = to_dev(bf16_input(synth.SEED_DY, (T, O)), dtype)
+        outs = []
+        for _ in range(3):
+            ctx.zero_grad()
+            ctx.bwd(mid, X, dY, need_dx=False)
+            torch.cuda.synchronize()
+            outs.append(ctx.dM.clone())
+        assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+
+
+@pytest.mark.parametrize("ratio", [10, 100, 1000])
+@pytest.mark.parametrize("deterministic", [False, True])
+def test_c2_block_bf16_subset(R, torch, ratio, deterministic):
+    """C2 shapes at T = 512 (oracle in seconds), both layers in one GMS M."""
+    cfg = synth.mlp_block(ratio, tokens=512)
+    mem = cfg["mem_size"]
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64, deterministic=deterministic)
+    ids = [ctx.linear(H, O) for H, O in cfg["layers"]]
+    T = cfg["tokens"]
+    dM_ref = np.zeros(mem)
+    dM_gpu = None
+    ctx.zero_grad()
+    for mid, (H, O) in zip(ids, cfg["layers"]):
+        X_np = bf16_input(synth.SEED_X + 10 * mid, (T, H))
+        dY_np = bf16_input(synth.SEED_DY + 10 * mid, (T, O))
+        X, dY = to_dev(X_np, torch.bfloat16), to_dev(dY_np, torch.bfloat16)
+        Y = ctx.fwd(mid, X)
+        dX = ctx.bwd(mid, X, dY)
+        torch.cuda.synchronize()
+        spec = OM.LinearSpec(H, O, 64, 64, mem, HS, mid)
+        assert rel_frob(Y.float().cpu().numpy(), spec.forward(X_np, M_np, True)) <= 1e-2
+        assert rel_frob(dX.float().cpu().numpy(), spec.backward_dx(dY_np, M_np, True)) <= 1e-2
+        spec.backward_dm(X_np, dY_np, dM_ref)
+    dM_gpu = ctx.dM.cpu().numpy()
+    assert rel_frob(dM_gpu, dM_ref) <= 1e-2
+
+
+@pytest.mark.parametrize("T", [0, 1, 127, 129, 300])
+def test_ragged_and_empty_tokens_bf16(R, torch, T):
+    mem = 47192
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64)
+    mid = ctx.linear(768, 3072)
+    spec = OM.LinearSpec(768, 3072, 64, 64, mem, HS, mid)
+    X_np = bf16_input(synth.SEED_X, (T, 768))
+    dY_np = bf16_input(synth.SEED_DY, (T, 3072))
+    Y, dX, dM = run_linear(R, torch, ctx, mid, X_np, dY_np, torch.bfloat16)
+    if T == 0:
+        assert Y.size == 0 and np.all(dM == 0)
+        return
+    assert rel_frob(Y, spec.forward(X_np, M_np, True)) <= 1e-2
+    assert rel_frob(dX, spec.backward_dx(dY_np, M_np, True)) <= 1e-2
+    assert rel_frob(dM, spec.backward_dm(X_np, dY_np)) <= 1e-2
+
+
+def test_identity_mapping_is_dense_layer(R, torch):
+    """North star: |M| >= n, identity mapping -> ROAST-MM == dense X @ reshape(M)."""
+    H, O, T = 256, 128, 200
+    M_np = store(H * O)
+    ctx, _ = make_ctx(R, torch, M_np, 32, 32, mapping=1)
+    mid = ctx.linear(H, O)
+    spec = OM.LinearSpec(H, O, 32, 32, H * O, HS, mid, mapping=OM.IDENTITY, use_sign=False)
+    X = synth.uniform(synth.SEED_X, (T, H)).astype(np.float32)
+    dY = synth.uniform(synth.SEED_DY, (T, O)).astype(np.float32)
+    Y, dX, dM = run_linear(R, torch, ctx, mid, X, dY, torch.float32)
+    assert rel_frob(Y, spec.forward(X, M_np)) <= 1e-5
+    assert rel_frob(dX, spec.backward_dx(dY, M_np)) <= 1e-5
+    assert rel_frob(dM, spec.backward_dm(X, dY)) <= 1e-5
+
+
+# ---------------------------------------------------------------- a4-a5: embedding
+@pytest.mark.parametrize("n,dist", [(5000, "uniform"), (4096, "zipf"), (1, "uniform"), (0, "uniform")])
+def test_embedding_parity(R, torch, n, dist):
+    mem, rows, d, Z = 1_000_000, 10 ** 7, 128, 32
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64)
+    mids = [ctx.embedding(rows, d, Z) for _ in range(2)]
+    idx_np = (synth.uniform_indices if dist == "uniform" else synth.zipf_indices)(synth.SEED_IDX, n, rows)
+    dout_np = synth.normal(synth.SEED_DY, (n, d)).astype(np.float32)
+    idx = to_dev(idx_np, torch.int64)
+    dout = to_dev(dout_np, torch.float32)
+    ctx.zero_grad()
+    ref_dM = np.zeros(mem)
+    for mid in mids:
+        out = ctx.emb_fwd(mid, idx)
+        ctx.emb_bwd(mid, idx, dout)
+        torch.cuda.synchronize()
+        spec = OE.EmbeddingSpec(rows, d, Z, mem, HS, mid)
+        if n:
+            assert np.array_equal(out.cpu().numpy().astype(np.float64), spec.forward(idx_np, M_np))
+        spec.backward(idx_np, dout_np, ref_dM)
+    ctx.check()
+    assert rel_frob(ctx.dM.cpu().numpy(), ref_dM) <= 1e-5
+
+
+def test_embedding_duplicates_and_bounds(R, torch):
+    from paper_2207_10702_b200 import roast
+    mem = 4096
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64)
+    mid = ctx.embedding(100, 64, 32)
+    idx_np = np.array([5, 5, 5, 7, 99], dtype=np.int64)
+    dout_np = synth.normal(3, (5, 64)).astype(np.float32)
+    ctx.zero_grad()
+    ctx.emb_bwd(mid, to_dev(idx_np, torch.int64), to_dev(dout_np, torch.float32))
+    torch.cuda.synchronize()
+    ref = OE.EmbeddingSpec(100, 64, 32, mem, HS, mid).backward(idx_np, dout_np)
+    assert rel_frob(ctx.dM.cpu().numpy(), ref) <= 1e-6
+    ctx.check()
+    bad = to_dev(np.array([3, 100, -1], dtype=np.int64), torch.int64)
+    out = ctx.emb_fwd(mid, bad)
+    torch.cuda.synchronize()
+    assert torch.all(out[1:] == 0)
+    assert roast.roast_get_error(ctx.h) == roast.ERR_BOUNDS
