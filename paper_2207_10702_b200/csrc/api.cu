@@ -49,6 +49,8 @@ static void free_module(Module& m) {
   cudaFree(m.d_sgn);
   cudaFree(m.d_sorted);
   cudaFree(m.d_sorted_off);
+  cudaFree(m.d_coord_xy);
+  cudaFree(m.d_coord_yx);
 }
 
 }  // namespace roast
@@ -212,6 +214,21 @@ roast_status_t roast_register_linear(roast_t h, int64_t H, int64_t O, int32_t* i
   if (e == cudaSuccess) e = cudaMemcpy(m.d_sgn, m.h_sgn.data(), nt * sizeof(int8_t), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(m.d_sorted, order.data(), nt * sizeof(int32_t), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(m.d_sorted_off, soff.data(), nt * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && c->mem_size < (int64_t(1) << 33) && A % 8 == 0) {
+    std::vector<int32_t> cxy(nt), cyx(nt);
+    for (int32_t x = 0; x < m.nx; ++x)
+      for (int32_t y = 0; y < m.ny; ++y) {
+        const int64_t t = int64_t(x) * m.ny + y;
+        const int64_t off = m.h_off[t];
+        const int32_t packed = int32_t(((off >> 6) << 4) | (m.h_sgn[t] < 0 ? 8 : 0) | ((off >> 3) & 7));
+        cxy[t] = packed;
+        cyx[int64_t(y) * m.nx + x] = packed;
+      }
+    e = cudaMalloc(reinterpret_cast<void**>(&m.d_coord_xy), nt * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&m.d_coord_yx), nt * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMemcpy(m.d_coord_xy, cxy.data(), nt * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(m.d_coord_yx, cyx.data(), nt * sizeof(int32_t), cudaMemcpyHostToDevice);
+  }
   if (e != cudaSuccess) {
     free_module(m);
     return cuda_fail(e, "register_linear upload");

@@ -1,0 +1,772 @@
+// gemm_sm100.cu — tcgen05 / TMEM / TMA ROAST-MM for sm_100a (K2 fwd, K3 dX, K4 dW->dM).
+//
+// What is computed (Algorithm 1; backward P:338-346):
+//   FWD  Y  = lambda * X  . W~         M = tokens, N = out, K = in
+//   DX   dX = lambda * dY . W~^T       M = tokens, N = in,  K = out
+//   DW   G  = X^T . dY                 M = in,     N = out, K = tokens
+//        dM[h(x,y) + 64 o1 + o2] += lambda * g(x,y) * G[64x + o1, 64y + o2]
+// with W~ the signed 64x64 hash tiles of M read through the tile map (a0).
+//
+// How it maps to B200:
+//  * Persistent, warp-specialised: warp 0 issues TMA, warp 1 issues
+//    tcgen05.mma (one thread), warp 2 owns TMEM, warps 4..7 drain the
+//    accumulator (tcgen05.ld) and run the epilogue.  smem ring with full/empty
+//    mbarriers, 2 TMEM accumulators (2 x 256 fp32 columns) so the epilogue of
+//    one tile overlaps the MMAs of the next.
+//  * CG = 2 (default): a CTA pair (cluster of 2) runs tcgen05.mma.cta_group::2
+//    on a 256 x 256 x 16 instruction; each CTA stages its 128 rows of A and
+//    half (128 columns) of B, so operand traffic from L2 is 2/3 of the 1-CTA
+//    128 x 256 tile and smem operand reads halve.  The leader CTA issues the
+//    MMAs; TMA completion bytes of both CTAs land on the leader's barrier;
+//    commits multicast to both CTAs.  CG = 1 keeps the 1-SM 128 x 256 tile.
+//  * Hashed weight tiles: each 64x64 bf16 tile is 64 rows of 128 B in M.  A
+//    2-D TMA box {64, 64} with SWIZZLE_128B lands it in smem as a canonical
+//    SW128 operand: MN-major B for FWD (rows = K), and — the same bytes —
+//    K-major B for DX (rows = N).  Offsets are only 16-B aligned (A = 8), so
+//    the shadow is described by 8 tensor maps, one per 16-byte phase
+//    (base + 16 r), each a plain non-overlapping [rows x 128 B] view.
+//  * The sign g is folded into the load address: the shadow holds
+//    [+bf16(M) | -bf16(M)], and a tile with g = -1 is read from the negated
+//    copy (bf16 negation is exact), so no transform pass touches smem.
+//  * lambda is applied once in the epilogue (Algorithm 1).
+//  * DW: A = X^T and B = dY are both MN-major TMA tiles; the epilogue writes
+//    lambda * g * G per hash tile either into a per-tile workspace (reduced
+//    in fixed order by K5: deterministic) or with 16-byte vector atomics into
+//    dM (fast mode).  Split-K over tokens fills the SMs.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstring>
+
+#include "roast_internal.h"
+
+namespace roast {
+namespace sm100 {
+
+constexpr int BM = 128;   // accumulator rows per CTA
+constexpr int BN = 256;   // MMA N (columns of the output tile)
+constexpr int BK = 64;    // K per pipeline stage (one 128-byte swizzle row of bf16)
+constexpr int NUM_THREADS = 256;
+constexpr int EPI_WARP0 = 4;
+constexpr int TMEM_COLS = 512;
+constexpr int MAX_KB = 256;   // k-blocks per work unit whose coordinates fit the smem stage
+
+template <int CG>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;            // 16 KB: this CTA's 128 rows of A
+  static constexpr int B_BYTES = (BN / CG) * BK * 2;     // this CTA's BN/CG columns of B
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = CG == 2 ? 5 : 3;
+  static constexpr int B_SUB = 4 / CG;                   // 64-wide B sub-tiles per CTA
+  static constexpr int STAGING = 4 * 2 * 4096;           // epilogue: 4 warps x 2 x (32 rows x 128 B)
+  static constexpr int SMEM = STAGES * STAGE_BYTES + STAGING + 1024 + 256 + MAX_KB * 4 * 4;
+};
+
+enum Mode { FWD = 0, DX = 1, DW = 2 };
+
+struct WMaps {
+  CUtensorMap m[8];  // shadow viewed from base + 16 r bytes, r = 0..7
+};
+
+struct Params {
+  int64_t T;            // tokens
+  int M, N, K;          // GEMM dims in elements (M, N multiples of 64; K ragged only for DW)
+  int m_tiles, n_tiles, k_blocks, splits, kb_per_split, units;
+  const int64_t* off;   // tile map
+  const int8_t* sgn;
+  const int32_t* coord; // packed TMA coordinates (FWD: [x][y], DX: [y][x])
+  int coord_ld;         // row length of `coord`
+  int ny;               // tiles per row of the tile map (out / 64)
+  int64_t neg_row;      // row (128 B units) of the negated shadow copy
+  float lam;
+  __nv_bfloat16* out;   // FWD: Y [T x N], DX: dX [T x N]
+  float* dM;            // DW atomic target
+  float* ws;            // DW deterministic workspace [splits][ntiles][4096]
+  int ntiles;
+  long long* prof;      // debug (ROAST_PROF): per-CTA cycle counters, else null
+};
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same smem location in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// arrive on a barrier given by its shared::cluster address (own or peer CTA)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, void* dst, uint32_t bar_cluster, int c0, int c1) {
+  if (CG == 1)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// MMA completion -> arrive on `bar` (CG = 2: on the same barrier in both CTAs of the pair)
+template <int CG>
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  if (CG == 1)
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  if (CG == 1)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+#define TMEM_LD32(taddr, r)                                                                                       \
+  asm volatile(                                                                                                   \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%" \
+      "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                              \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),           \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),     \
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),   \
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])    \
+      : "r"(taddr))
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Shared-memory matrix descriptor, SWIZZLE_128B, sm_100 version bits.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;  // version 1 (tcgen05)
+  d |= uint64_t(2) << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: bf16 x bf16 -> f32, M = 128 * CG, N = 256.
+__host__ __device__ constexpr uint32_t make_idesc(int a_mn_major, int b_mn_major, int m) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(a_mn_major) << 15) | (uint32_t(b_mn_major) << 16) |
+         (uint32_t(BN >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void decode_unit(const Params& p, int u, int& mb, int& nb, int& split) {
+  split = u / (p.m_tiles * p.n_tiles);
+  int r = u - split * p.m_tiles * p.n_tiles;
+  mb = r / p.n_tiles;
+  nb = r - mb * p.n_tiles;
+}
+
+// ---------------------------------------------------------------- the kernel
+template <int MODE, int CG>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    roast_mm_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                   const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ WMaps wmaps, const Params p) {
+  using C = Cfg<CG>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                                        // [STAGES][A_BYTES]
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;               // [STAGES][B_BYTES]
+  uint8_t* sStage = smem + C::STAGES * C::STAGE_BYTES;      // epilogue staging [4 warps][2][4 KB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStage + C::STAGING);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int32_t* sCoord = reinterpret_cast<int32_t*>(sStage + C::STAGING + 256);  // [<= MAX_KB * 4]
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  long long prof_acc[5] = {0, 0, 0, 0, 0};
+  const long long t_start = clock64();
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x / CG;
+  const int npairs = gridDim.x / CG;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4 * CG);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_map(&mapA);
+    if (MODE == DW) prefetch_map(&mapB);
+  }
+  if (warp == 2) {
+    if (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+  }
+  tc_fence_before();
+  if (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer (warp 0, both CTAs) =====================
+    // Per work unit the whole warp stages the unit's packed tile coordinates
+    // (k-blocks x 4, FWD/DX) into smem with coalesced loads; lane 0 then walks
+    // the k-blocks and issues this CTA's TMA copies.  The one load latency per
+    // unit hides behind the k-blocks already buffered in the ring.
+    int s = 0;
+    uint32_t ph = 0;
+    for (int u = pair; u < p.units; u += npairs) {
+      int mb, nb, split;
+      decode_unit(p, u, mb, nb, split);
+      const int kb0 = split * p.kb_per_split;
+      const int kb1 = min(kb0 + p.kb_per_split, p.k_blocks);
+      const int n_sub = min(4, (p.N - nb * BN) / 64);   // valid 64-wide N sub-tiles of the unit
+      // this CTA's B sub-tiles: [j0, j1)
+      const int j0 = int(rank) * C::B_SUB;
+      const int j1 = min(j0 + C::B_SUB, n_sub);
+      // DW: valid 64-wide M boxes of this CTA and of the whole pair (for the tx byte count)
+      const int row0 = mb * BM * CG + int(rank) * BM;
+      const int m_sub = MODE == DW ? max(0, min(2, (p.M - row0) / 64)) : 0;
+      const int m_sub_pair = MODE == DW ? max(0, min(2 * CG, (p.M - mb * BM * CG) / 64)) : 0;
+      if (MODE != DW) {
+        __syncwarp();
+        for (int i = lane; i < (kb1 - kb0) * 4; i += 32) {
+          const int j = i & 3;
+          sCoord[i] = j < n_sub ? __ldg(p.coord + int64_t(kb0 + (i >> 2)) * p.coord_ld + nb * 4 + j) : 0;
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        // bytes landing on the leader's full barrier per stage (both CTAs)
+        const uint32_t tx = MODE == DW ? uint32_t((m_sub_pair + n_sub) * 64 * 64 * 2)
+                                       : uint32_t(CG * C::A_BYTES + n_sub * 64 * 64 * 2);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          long long tw0 = p.prof ? clock64() : 0;
+          mbar_wait(&empty[s], ph ^ 1);
+          if (p.prof) prof_acc[0] += clock64() - tw0;
+          uint8_t* a = sA + s * C::A_BYTES;
+          uint8_t* b = sB + s * C::B_BYTES;
+          const uint32_t fb = CG == 2 ? map_to_rank(smem_u32(&full[s]), 0) : smem_u32(&full[s]);
+          if (leader) mbar_expect_tx(&full[s], tx);
+          if (MODE == DW) {
+            for (int i = 0; i < m_sub; ++i) tma_load_2d<CG>(&mapA, a + i * 8192, fb, row0 + i * 64, kb * BK);
+            for (int j = j0; j < j1; ++j)
+              tma_load_2d<CG>(&mapB, b + (j - j0) * 8192, fb, nb * BN + j * 64, kb * BK);
+          } else {
+            tma_load_2d<CG>(&mapA, a, fb, kb * BK, row0);
+            const int32_t* cc = sCoord + (kb - kb0) * 4;
+            for (int j = j0; j < j1; ++j) {
+              // FWD: tile (x = kb, y = nb*4 + j); DX: tile (x = nb*4 + j, y = kb).
+              // Packed: row << 4 | neg << 3 | phase; negative tiles read the negated shadow.
+              const int32_t c = cc[j];
+              const int row = (c >> 4) + ((c & 8) ? int(p.neg_row) : 0);
+              tma_load_2d<CG>(&wmaps.m[c & 7], b + (j - j0) * 8192, fb, 0, row);
+            }
+          }
+          if (++s == C::STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ===================== MMA issuer (leader CTA, single thread) =====================
+      constexpr uint32_t idesc = make_idesc(MODE == DW ? 1 : 0, MODE == FWD || MODE == DW ? 1 : 0, BM * CG);
+      // B descriptor strides: MN-major = 64-col sub-tiles 8 KB apart; K-major = 8-row groups 1 KB apart
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int u = pair; u < p.units; u += npairs) {
+        int mb, nb, split;
+        decode_unit(p, u, mb, nb, split);
+        const int kb0 = split * p.kb_per_split;
+        const int kb1 = min(kb0 + p.kb_per_split, p.k_blocks);
+        long long tw1 = p.prof ? clock64() : 0;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        if (p.prof) prof_acc[2] += clock64() - tw1;
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          long long tw2 = p.prof ? clock64() : 0;
+          mbar_wait(&full[s], ph);
+          if (p.prof) prof_acc[1] += clock64() - tw2;
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * C::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + s * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            uint64_t ad, bd;
+            if (MODE == DW) {
+              ad = sw128_desc(a0 + k * 2048, 8192, 1024);   // MN-major: LBO = next 64 M, SBO = next 8 K rows
+              bd = sw128_desc(b0 + k * 2048, 8192, 1024);
+            } else if (MODE == FWD) {
+              ad = sw128_desc(a0 + k * 32, 16, 1024);       // K-major: +32 B per K=16 step
+              bd = sw128_desc(b0 + k * 2048, 8192, 1024);   // MN-major hashed tiles
+            } else {
+              ad = sw128_desc(a0 + k * 32, 16, 1024);
+              bd = sw128_desc(b0 + k * 32, 16, 1024);       // K-major view of the same tile bytes
+            }
+            tc_mma<CG>(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          tc_commit<CG>(&empty[s]);
+          if (++s == C::STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        tc_commit<CG>(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ===================== epilogue: TMEM -> registers -> global =====================
+    const int q = warp & 3;          // TMEM lane quadrant this warp may access
+    const int row = q * 32 + lane;   // accumulator row owned by this thread
+    const uint32_t tempty_leader0 = CG == 2 ? map_to_rank(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
+    int stg = 0;   // staging buffer counter (double buffer per warp)
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int u = pair; u < p.units; u += npairs) {
+      int mb, nb, split;
+      decode_unit(p, u, mb, nb, split);
+      const int n_valid = min(BN, p.N - nb * BN);
+      const int row_base = mb * BM * CG + int(rank) * BM;
+      // DW: the warp's 32 rows lie in one hash-tile row x; lanes 0..3 fetch the
+      // (offset, lambda*g) of tiles (x, 4 nb + lane) before waiting on the accumulator.
+      int64_t t_off = 0;
+      float t_scale = 0.f;
+      if (MODE == DW) {
+        const int x = (row_base + q * 32) >> 6;
+        const int y = nb * 4 + (lane & 3);
+        if (lane < 4 && (row_base + q * 32) < p.M && y * 64 < p.N) {
+          const int t = x * p.ny + y;
+          t_off = p.ws ? (int64_t(split) * p.ntiles + t) * 4096 : p.off[t];
+          t_scale = p.sgn[t] < 0 ? -p.lam : p.lam;
+        }
+      }
+      long long tw3 = p.prof ? clock64() : 0;
+      mbar_wait(&tfull[acc], aph);
+      long long tw4 = p.prof ? clock64() : 0;
+      if (p.prof) prof_acc[3] += tw4 - tw3;
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + uint32_t(acc * BN) + (uint32_t(q * 32) << 16);
+      // Each step drains 32 rows x 128 B of output through a 4 KB SW128-swizzled
+      // staging buffer (conflict-free st.shared) and one TMA bulk tensor op:
+      // FWD/DX store 64 bf16 columns of Y / dX; DW stores (deterministic
+      // workspace) or reduce-adds in L2 (dM) 32 fp32 columns of one hash tile.
+      constexpr int COLS = MODE == DW ? 32 : 64;
+      for (int c = 0; c < n_valid / COLS; ++c) {
+        uint32_t pk[32];
+        int64_t tb = 0;
+        if (MODE != DW) {
+          uint32_t r0[32], r1[32];
+          TMEM_LD32(tbase + uint32_t(c * 64), r0);
+          TMEM_LD32(tbase + uint32_t(c * 64 + 32), r1);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            __nv_bfloat162 v = __floats2bfloat162_rn(p.lam * __uint_as_float(r0[2 * i]),
+                                                     p.lam * __uint_as_float(r0[2 * i + 1]));
+            pk[i] = *reinterpret_cast<uint32_t*>(&v);
+            __nv_bfloat162 w = __floats2bfloat162_rn(p.lam * __uint_as_float(r1[2 * i]),
+                                                     p.lam * __uint_as_float(r1[2 * i + 1]));
+            pk[16 + i] = *reinterpret_cast<uint32_t*>(&w);
+          }
+        } else {
+          TMEM_LD32(tbase + uint32_t(c * 32), pk);
+          tmem_wait_ld();
+          const float scale = __shfl_sync(0xffffffffu, t_scale, c >> 1);
+          tb = __shfl_sync(0xffffffffu, t_off, c >> 1);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) pk[i] = __float_as_uint(scale * __uint_as_float(pk[i]));
+        }
+        uint8_t* buf = sStage + (warp - EPI_WARP0) * 8192 + (stg & 1) * 4096;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const uint32_t a = smem_u32(buf + lane * 128 + ((cc ^ (lane & 7)) << 4));
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pk[4 * cc]), "r"(pk[4 * cc + 1]),
+                       "r"(pk[4 * cc + 2]), "r"(pk[4 * cc + 3])
+                       : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t sb = smem_u32(buf);
+          if (MODE != DW) {
+            const int x0 = nb * BN + c * 64, y0 = row_base + q * 32;
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                             reinterpret_cast<uint64_t>(&mapOut)),
+                         "r"(x0), "r"(y0), "r"(sb)
+                         : "memory");
+          } else if (row_base + q * 32 < p.M) {   // warps past the last hash-tile row write nothing
+            const int x0 = (c & 1) * 32;
+            const int o1_0 = (row_base + q * 32) & 63;
+            if (p.ws) {   // deterministic: plain store into the per-tile workspace [.. x 64] fp32
+              const int y0 = int(tb >> 6) + o1_0;
+              asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                               reinterpret_cast<uint64_t>(&mapOut)),
+                           "r"(x0), "r"(y0), "r"(sb)
+                           : "memory");
+            } else {      // fast: TMA reduce-add into dM in L2 through the 16-byte-phase view of dM
+              const int y0 = int(tb >> 6) + o1_0;
+              asm volatile(
+                  "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                      reinterpret_cast<uint64_t>(&wmaps.m[(tb >> 3) & 7])),
+                  "r"(x0), "r"(y0), "r"(sb)
+                  : "memory");
+            }
+          }
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        ++stg;
+      }
+      if (p.prof) prof_acc[4] += clock64() - tw4;
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + uint32_t(acc * 8));
+      acc ^= 1;
+      if (acc == 0) aph ^= 1;
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // staging reads + writes done
+    __syncwarp();
+  }
+
+  if (p.prof && lane == 0) {
+    long long* o = p.prof + blockIdx.x * 8;
+    if (warp == 0) { o[0] = prof_acc[0]; o[5] = clock64() - t_start; }
+    if (warp == 1) { o[1] = prof_acc[1]; o[2] = prof_acc[2]; }
+    if (warp == EPI_WARP0) { o[3] = prof_acc[3]; o[4] = prof_acc[4]; }
+  }
+  tc_fence_before();
+  if (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    if (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// 2-D tensor [rows x cols] (cols contiguous, bf16 or fp32), box {box_c, box_r}, SWIZZLE_128B.
+roast_status_t make_map_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t row_bytes,
+                           uint32_t box_c, uint32_t box_r, bool fp32 = false) {
+  auto fn = encode_fn();
+  if (!fn) return fail(ROAST_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_c, box_r};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ROAST_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return ROAST_OK;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+int cta_group() {
+  static int cg = 0;
+  if (!cg) {
+    const char* e = getenv("ROAST_CTA_GROUP");
+    cg = (e && atoi(e) == 1) ? 1 : 2;
+  }
+  return cg;
+}
+
+template <int MODE, int CG>
+roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o, const WMaps& w,
+                         const Params& p, cudaStream_t s) {
+  using C = Cfg<CG>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e =
+        cudaFuncSetAttribute(roast_mm_sm100<MODE, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(smem)");
+    attr = true;
+  }
+  const int pairs = std::min(p.units, num_sms() / CG);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(pairs * CG));
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CG;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  static long long* prof = nullptr;
+  Params pp = p;
+  if (getenv("ROAST_PROF")) {
+    if (!prof) cudaMallocManaged(&prof, sizeof(long long) * 8 * 512);
+    cudaMemset(prof, 0, sizeof(long long) * 8 * 512);
+    pp.prof = prof;
+  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mm_sm100<MODE, CG>, a, b, o, w, pp);
+  if (e != cudaSuccess) return cuda_fail(e, "roast_mm_sm100 launch");
+  if (pp.prof) {
+    cudaDeviceSynchronize();
+    double acc[8] = {0};
+    long long mx = 0;
+    for (int i = 0; i < pairs * CG; ++i) {
+      for (int k = 0; k < 8; ++k) acc[k] += double(prof[i * 8 + k]);
+      mx = std::max(mx, prof[i * 8 + 5]);
+    }
+    const int n = pairs * CG, nl = (pairs * CG + CG - 1) / CG;
+    fprintf(stderr, "[roast prof] mode %d cg %d units %d kb %d | total %.0f (max %lld) | prod wait-empty %.0f | "
+            "mma wait-full %.0f wait-tempty %.0f | epi wait-tfull %.0f busy %.0f  (cycles, mean/CTA)\n",
+            MODE, CG, p.units, p.k_blocks, acc[5] / n, mx, acc[0] / n, acc[1] / nl, acc[2] / nl, acc[3] / n,
+            acc[4] / n);
+  }
+  return ROAST_OK;
+}
+
+template <int MODE>
+roast_status_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o, const WMaps& w, Params p,
+                      cudaStream_t s) {
+  return cta_group() == 2 ? launch_cg<MODE, 2>(a, b, o, w, p, s) : launch_cg<MODE, 1>(a, b, o, w, p, s);
+}
+
+}  // namespace sm100
+
+using namespace sm100;
+
+
+roast_status_t sm100_prepare(Ctx* c) {
+  if (c->tmap_shadow_valid) return ROAST_OK;
+  static_assert(sizeof(WMaps) <= sizeof(Ctx::tmap_shadow), "tmap storage");
+  WMaps* w = reinterpret_cast<WMaps*>(c->tmap_shadow);
+  for (int r = 0; r < 8; ++r) {
+    const int64_t elems = c->shadow_elems - 8 * r;
+    roast_status_t st = make_map_2d(&w->m[r], c->shadow + 8 * r, 64, uint64_t(elems / 64), 128, 64, 64);
+    if (st) return st;
+  }
+  c->tmap_shadow_valid = true;
+  return ROAST_OK;
+}
+
+static bool supported(const Ctx* c, const Module& m) {
+  return m.d_coord_xy != nullptr && c->cfg.tile_layout == ROAST_ROW_MAJOR && c->tile.z1 == 64 &&
+         c->tile.z2 == 64 && m.H % 64 == 0 && m.O % 64 == 0 && m.H / 64 <= MAX_KB && m.O / 64 <= MAX_KB;
+}
+
+static Params base_params(const Ctx* c, const Module& m, int64_t T) {
+  Params p{};
+  p.T = T;
+  p.off = m.d_off;
+  p.sgn = m.d_sgn;
+  p.ny = m.ny;
+  p.neg_row = c->neg_base / 64;
+  p.lam = m.lam;
+  p.ntiles = m.nx * m.ny;
+  p.splits = 1;
+  return p;
+}
+
+// FWD / DX share the geometry: M = tokens, N = the module's output side, K = its input side.
+static roast_status_t run_tok_major(Ctx* c, const Module& m, const void* A, void* out, int64_t T, int N, int K,
+                                    const int32_t* coord, int coord_ld, bool dx, cudaStream_t s) {
+  if (!supported(c, m) || T >= (int64_t(1) << 31)) return ROAST_ERR_UNSUPPORTED;
+  roast_status_t st = sm100_prepare(c);
+  if (st) return st;
+  CUtensorMap a;
+  st = make_map_2d(&a, A, uint64_t(K), uint64_t(T), uint64_t(K) * 2, BK, BM);
+  if (st) return st;
+  Params p = base_params(c, m, T);
+  p.M = int(std::min<int64_t>(T, 1 << 30));
+  p.N = N;
+  p.K = K;
+  p.m_tiles = int((T + BM * cta_group() - 1) / (BM * cta_group()));
+  p.n_tiles = (p.N + BN - 1) / BN;
+  p.k_blocks = p.K / BK;
+  p.kb_per_split = p.k_blocks;
+  p.units = p.m_tiles * p.n_tiles;
+  p.out = reinterpret_cast<__nv_bfloat16*>(out);
+  p.coord = coord;
+  p.coord_ld = coord_ld;
+  CUtensorMap o;   // output [T x N] bf16, stored 32 rows x 64 columns per TMA op
+  st = make_map_2d(&o, out, uint64_t(N), uint64_t(T), uint64_t(N) * 2, 64, 32);
+  if (st) return st;
+  const WMaps& w = *reinterpret_cast<const WMaps*>(c->tmap_shadow);
+  st = dx ? launch<DX>(a, a, o, w, p, s) : launch<FWD>(a, a, o, w, p, s);
+  if (!st) c->launches++;
+  return st;
+}
+
+roast_status_t sm100_fwd(Ctx* c, const Module& m, const void* X, void* Y, int64_t T, cudaStream_t s) {
+  return run_tok_major(c, m, X, Y, T, int(m.O), int(m.H), m.d_coord_xy, m.ny, false, s);
+}
+
+roast_status_t sm100_dx(Ctx* c, const Module& m, const void* dY, void* dX, int64_t T, cudaStream_t s) {
+  return run_tok_major(c, m, dY, dX, T, int(m.H), int(m.O), m.d_coord_yx, m.nx, true, s);
+}
+
+roast_status_t sm100_dw(Ctx* c, const Module& m, const void* X, const void* dY, int64_t T, cudaStream_t s) {
+  if (!supported(c, m) || T >= (int64_t(1) << 31)) return ROAST_ERR_UNSUPPORTED;
+  CUtensorMap a, b;
+  roast_status_t st = make_map_2d(&a, X, uint64_t(m.H), uint64_t(T), uint64_t(m.H) * 2, 64, BK);
+  if (st) return st;
+  st = make_map_2d(&b, dY, uint64_t(m.O), uint64_t(T), uint64_t(m.O) * 2, 64, BK);
+  if (st) return st;
+  const int cg = cta_group();
+  const int slots = num_sms() / cg;   // concurrent work units
+  Params p = base_params(c, m, T);
+  p.M = int(m.H);
+  p.N = int(m.O);
+  p.m_tiles = (p.M + BM * cg - 1) / (BM * cg);
+  p.n_tiles = (p.N + BN - 1) / BN;
+  p.k_blocks = int((T + BK - 1) / BK);
+  // split-K over tokens: the smallest split s minimising the makespan ceil(tiles*s / slots) / s
+  const int tiles = p.m_tiles * p.n_tiles;
+  int splits = 1;
+  double best = 1e30;
+  for (int sp = 1; sp <= std::min(p.k_blocks, 16); ++sp) {
+    const double cost = double((tiles * sp + slots - 1) / slots) / sp;
+    if (cost < best - 1e-9) {
+      best = cost;
+      splits = sp;
+    }
+  }
+  p.kb_per_split = (p.k_blocks + splits - 1) / splits;
+  splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;   // no empty splits
+  p.splits = splits;
+  p.units = tiles * splits;
+  p.dM = c->dM;
+  const bool det = c->cfg.deterministic != 0;
+  if (det) {
+    st = ensure_ws(c, size_t(splits) * p.ntiles * 4096 * sizeof(float), s);
+    if (st) return st;
+    p.ws = c->ws;
+  }
+  // dM viewed as 8 [rows x 64] fp32 tensors, one per 32-byte phase (tile offsets are multiples of A = 8)
+  CUtensorMap o;
+  WMaps dmaps;
+  memset(&o, 0, sizeof(o));
+  if (det) {
+    const uint64_t rows = uint64_t(splits) * p.ntiles * 64;
+    st = make_map_2d(&o, c->ws, 64, rows, 256, 32, 32, true);
+    if (st) return st;
+  } else {
+    for (int r = 0; r < 8; ++r) {
+      const int64_t elems = c->mem_size - 8 * r;
+      st = make_map_2d(&dmaps.m[r], c->dM + 8 * r, 64, uint64_t(elems / 64), 256, 32, 32, true);
+      if (st) return st;
+    }
+  }
+  st = launch<DW>(a, b, o, dmaps, p, s);
+  if (st) return st;
+  c->launches++;
+  if (det) {
+    cudaError_t e = launch_det_reduce(c, m, c->ws, splits, s);
+    if (e != cudaSuccess) return cuda_fail(e, "det_reduce");
+    c->launches++;
+  }
+  return ROAST_OK;
+}
+
+}  // namespace roast

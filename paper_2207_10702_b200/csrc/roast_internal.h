@@ -28,6 +28,10 @@ struct Module {
   // binary-searches the covering range [lo, hi) of every A-aligned slot group.
   int32_t* d_sorted = nullptr;    // [ntiles] tile ids
   int64_t* d_sorted_off = nullptr;// [ntiles]
+  // tcgen05 producer: packed TMA coordinates of every tile, (off >> 6) << 4 | neg << 3 | (off >> 3) & 7,
+  // in [x][y] order (FWD walks a row) and [y][x] order (DX walks a column).  Empty if off >= 2^33.
+  int32_t* d_coord_xy = nullptr;
+  int32_t* d_coord_yx = nullptr;
   // embedding
   int64_t rows = 0;
   int32_t dim = 0, chunk = 0, chunks_per_row = 0;
@@ -55,7 +59,7 @@ struct Ctx {
   int32_t rank = 0, world = 1;
   int64_t launches = 0;
   // tcgen05 path: cached TMA descriptors of the shadow (rebuilt on bind)
-  alignas(64) unsigned char tmap_shadow[128];
+  alignas(64) unsigned char tmap_shadow[1024];
   bool tmap_shadow_valid = false;
 };
 
