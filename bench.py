@@ -115,46 +115,55 @@ def run_reference(args):
 
 # ------------------------------------------------------------------------------ GPU arm
 class ClockSampler:
+    """SM clock + clock-event reasons sampled every ~2 ms by an NVML thread during the timed region."""
+
     def __init__(self, index):
         self.index = index
-        self.proc = None
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+
+    def _run(self):
+        import pynvml as N
+        names = {N.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
+                 N.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                 N.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                 N.nvmlClocksEventReasonSwPowerCap: "sw_power_cap",
+                 N.nvmlClocksEventReasonHwPowerBrakeSlowdown: "hw_power_brake"}
+        while not self.stop:
+            self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+            r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for bit, name in names.items():
+                if r & bit:
+                    self.reasons.add(name)
+            time.sleep(0.002)
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
+        import threading
+        self.stop = False
+        self.thread = None
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml as N
+            N.nvmlInit()
+            self.h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._run, daemon=True)
+            self.thread.start()
         except Exception:
-            self.proc = None
+            self.thread = None
         return self
 
     def __exit__(self, *a):
-        self.lines = []
-        if self.proc:
-            self.proc.terminate()
-            out, _ = self.proc.communicate(timeout=5)
-            self.lines = [l for l in out.splitlines() if l.strip()]
+        self.stop = True
+        if self.thread:
+            self.thread.join(timeout=2)
 
     def summary(self):
         import statistics
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
-            f = [x.strip() for x in l.split(",")]
-            try:
-                sm.append(float(f[0]))
-                mx = max(mx, float(f[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, f[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        if not sm:
-            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["unsampled"])
-        return dict(sm_mhz=statistics.median(sm), sm_max_mhz=mx, reasons=sorted(reasons), samples=len(sm))
+        if not self.samples:
+            return dict(sm_mhz=None, sm_max_mhz=self.max_mhz, reasons=["unsampled"])
+        return dict(sm_mhz=statistics.median(self.samples), sm_max_mhz=self.max_mhz,
+                    reasons=sorted(self.reasons), samples=len(self.samples))
 
 
 def run_gpu(args):
@@ -196,25 +205,44 @@ def run_gpu(args):
 
     kinds = ["fwd", "dx", "dm"]
     ev = {k: [] for k in kinds}
+    side = torch.cuda.Stream(device=dev)
 
-    def step(record):
+    def step_body(Xin, dY2in, record=False):
+        """One step of the hot path.  dX and dM of each layer are independent, so with
+        --streams 2 every dM GEMM runs on a second stream and fills the SMs the dX GEMM
+        leaves idle (the C ABI exposes the two halves of roast_linear_bwd for this)."""
+        cur = torch.cuda.current_stream()
+
         def rec(kind, fn):
             if record:
                 a = torch.cuda.Event(enable_timing=True)
                 b = torch.cuda.Event(enable_timing=True)
-                a.record(stream)
+                a.record(cur)
                 fn()
-                b.record(stream)
+                b.record(cur)
                 ev[kind].append((a, b))
             else:
                 fn()
         ctx.zero_grad()
-        rec("fwd", lambda: ctx.fwd(l1, X, Y1))
+        rec("fwd", lambda: ctx.fwd(l1, Xin, Y1))
         rec("fwd", lambda: ctx.fwd(l2, Y1, Y2))
-        rec("dx", lambda: ctx.bwd_dx(l2, dY2, dY1))
-        rec("dm", lambda: ctx.bwd_dm(l2, Y1, dY2))
-        rec("dx", lambda: ctx.bwd_dx(l1, dY1, dX))
-        rec("dm", lambda: ctx.bwd_dm(l1, X, dY1))
+        if args.streams == 2 and not record:
+            side.wait_stream(cur)
+            ctx.bwd_dx(l2, dY2in, dY1)
+            e_dy1 = torch.cuda.Event()
+            e_dy1.record(cur)
+            with torch.cuda.stream(side):
+                ctx.bwd_dm(l2, Y1, dY2in)
+            ctx.bwd_dx(l1, dY1, dX)
+            side.wait_event(e_dy1)
+            with torch.cuda.stream(side):
+                ctx.bwd_dm(l1, Xin, dY1)
+            cur.wait_stream(side)
+        else:
+            rec("dx", lambda: ctx.bwd_dx(l2, dY2in, dY1))
+            rec("dm", lambda: ctx.bwd_dm(l2, Y1, dY2in))
+            rec("dx", lambda: ctx.bwd_dx(l1, dY1, dX))
+            rec("dm", lambda: ctx.bwd_dm(l1, Xin, dY1))
         ctx.allreduce()
 
     def barrier():
@@ -223,23 +251,41 @@ def run_gpu(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    # warm-up (eager), launches per step, then capture the step in a CUDA graph
     for _ in range(args.warmup):
-        step(False)
+        step_body(X, dY2)
     barrier()
+    l0 = ctx.launch_count()
+    step_body(X, dY2)
+    launches_per_step = ctx.launch_count() - l0
+    barrier()
+    graph = None
+    if args.graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step_body(X, dY2)
+        for _ in range(args.warmup):
+            graph.replay()
+        barrier()
+
+    def run_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            step_body(X, dY2)
 
     # timed region: per-step CUDA events; L2 flushed between steps (outside the events)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    launches0 = ctx.launch_count()
     with ClockSampler(local) as clk:
         barrier()
         for i in range(args.steps):
             flush.zero_()
             starts[i].record(stream)
-            step(True)
+            run_step()
             ends[i].record(stream)
         barrier()
-    launches = ctx.launch_count() - launches0
+    launches = launches_per_step * args.steps
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = sum(step_ms)
     if world > 1:
@@ -250,34 +296,47 @@ def run_gpu(args):
     ms_per_step = total_ms / args.steps
     value = world * flops_per_step(T) / (ms_per_step * 1e-3) / 1e12
 
-    # per-kernel-kind times (each of our calls is one kernel launch in the atomic mode)
+    # per-kernel-kind launch durations: eager single-stream pass with events around each call
+    # (every call is one kernel launch in the atomic dM mode), same flush discipline
+    for _ in range(args.steps):
+        flush.zero_()
+        step_body(X, dY2, record=True)
+    torch.cuda.synchronize()
     kind_ms = {k: float(np.mean([a.elapsed_time(b) for a, b in ev[k]])) for k in kinds}
     gemm_flop = 2.0 * T * 768 * 3072                       # every call is one 2*T*H*O contraction
     dom = max(kinds, key=lambda k: kind_ms[k])
     burst, sustained, hbm, src = load_peaks()
     achieved = gemm_flop / (kind_ms[dom] * 1e-3) / 1e12
 
-    # end-to-end through the C ABI with host buffers: H2D of the step's inputs, D2H of dM
+    # end-to-end through the C ABI with host buffers: H2D of the step's inputs and D2H of dM,
+    # inside the timed region, the whole thing captured in one graph
     Xh = X.cpu().pin_memory()
     dY2h = dY2.cpu().pin_memory()
     dMh = torch.empty(mem, dtype=torch.float32).pin_memory()
     Xd = torch.empty_like(X)
     dY2d = torch.empty_like(dY2)
+
+    def e2e_body():
+        Xd.copy_(Xh, non_blocking=True)
+        dY2d.copy_(dY2h, non_blocking=True)
+        step_body(Xd, dY2d)
+        dMh.copy_(ctx.dM, non_blocking=True)
+    e2e_body()
+    barrier()
+    e2e_graph = None
+    if args.graph:
+        e2e_graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(e2e_graph):
+            e2e_body()
+        e2e_graph.replay()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        Xd.copy_(Xh, non_blocking=True)
-        dY2d.copy_(dY2h, non_blocking=True)
-        ctx.zero_grad()
-        ctx.fwd(l1, Xd, Y1)
-        ctx.fwd(l2, Y1, Y2)
-        ctx.bwd_dx(l2, dY2d, dY1)
-        ctx.bwd_dm(l2, Y1, dY2d)
-        ctx.bwd_dx(l1, dY1, dX)
-        ctx.bwd_dm(l1, Xd, dY1)
-        ctx.allreduce()
-        dMh.copy_(ctx.dM, non_blocking=True)
+        if e2e_graph is not None:
+            e2e_graph.replay()
+        else:
+            e2e_body()
     e1.record(stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1) / args.steps
@@ -303,12 +362,22 @@ def run_gpu(args):
     for _ in range(3):
         dense_step()
     torch.cuda.synchronize()
+    dense_graph = None
+    if args.graph:   # same launch discipline as the ROAST step
+        dense_graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(dense_graph):
+            dense_step()
+        dense_graph.replay()
+        torch.cuda.synchronize()
     d0, d1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dn = []
     for _ in range(max(5, args.steps)):
         flush.zero_()
         d0.record(stream)
-        dense_step()
+        if dense_graph is not None:
+            dense_graph.replay()
+        else:
+            dense_step()
         d1e.record(stream)
         torch.cuda.synchronize()
         dn.append(d0.elapsed_time(d1e))
@@ -329,6 +398,7 @@ def run_gpu(args):
                     tokens_per_gpu=T, global_tokens=T * world, ratio=RATIO, mem_size=mem,
                     l2="flushed between timed steps (256 MB write outside the events)",
                     dm_mode="deterministic" if args.deterministic else "atomic",
+                    streams=args.streams, cuda_graph=bool(args.graph),
                     parallelism=f"dp{world}"),
         roofline=dict(bound="tensor", kernel=dom, achieved=achieved, peak=burst, unit="TFLOP/s",
                       frac=achieved / burst, traffic=None,
@@ -351,12 +421,14 @@ def run_gpu(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="roast", choices=["roast", "reference"])
     ap.add_argument("--deterministic", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--streams", type=int, default=2, choices=[1, 2])
+    ap.add_argument("--graph", type=int, default=1, choices=[0, 1])
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -51,17 +51,21 @@ constexpr int BK = 64;    // K per pipeline stage (one 128-byte swizzle row of b
 constexpr int NUM_THREADS = 256;
 constexpr int EPI_WARP0 = 4;
 constexpr int TMEM_COLS = 512;
-constexpr int MAX_KB = 256;   // k-blocks per work unit whose coordinates fit the smem stage
+constexpr int KB_CHUNK = 64;  // k-blocks whose tile coordinates are staged in smem at a time
 
-template <int CG>
+// CG: CTAs per MMA (cta_group). WM: M sub-tiles of 128 rows per CTA sharing each B load
+// (WM = 2 uses both 256-column TMEM halves for one unit, so the accumulator is single-buffered).
+template <int CG, int WM>
 struct Cfg {
-  static constexpr int A_BYTES = BM * BK * 2;            // 16 KB: this CTA's 128 rows of A
+  static constexpr int A_BYTES = BM * WM * BK * 2;       // this CTA's 128*WM rows of A
   static constexpr int B_BYTES = (BN / CG) * BK * 2;     // this CTA's BN/CG columns of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = CG == 2 ? 5 : 3;
+  static constexpr int NBUF = 2;                         // epilogue staging buffers per warp
+  static constexpr int STAGING = 4 * NBUF * 4096;        // 4 warps x NBUF x (32 rows x 128 B)
+  static constexpr int FIXED = STAGING + 1024 + 256 + KB_CHUNK * 4 * 4;
+  static constexpr int STAGES = (227 * 1024 - FIXED) / STAGE_BYTES > 6 ? 6 : (227 * 1024 - FIXED) / STAGE_BYTES;
   static constexpr int B_SUB = 4 / CG;                   // 64-wide B sub-tiles per CTA
-  static constexpr int STAGING = 4 * 2 * 4096;           // epilogue: 4 warps x 2 x (32 rows x 128 B)
-  static constexpr int SMEM = STAGES * STAGE_BYTES + STAGING + 1024 + 256 + MAX_KB * 4 * 4;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + FIXED;
 };
 
 enum Mode { FWD = 0, DX = 1, DW = 2 };
@@ -86,6 +90,7 @@ struct Params {
   float* ws;            // DW deterministic workspace [splits][ntiles][4096]
   int ntiles;
   long long* prof;      // debug (ROAST_PROF): per-CTA cycle counters, else null
+  int epi;              // 0: TMA bulk store / reduce from staging; 1: coalesced st.global / red.global.v4
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -219,11 +224,11 @@ __device__ __forceinline__ void decode_unit(const Params& p, int u, int& mb, int
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int MODE, int CG>
+template <int MODE, int CG, int WM>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     roast_mm_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ WMaps wmaps, const Params p) {
-  using C = Cfg<CG>;
+  using C = Cfg<CG, WM>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                        // [STAGES][A_BYTES]
@@ -234,11 +239,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int32_t* sCoord = reinterpret_cast<int32_t*>(sStage + C::STAGING + 256);  // [<= MAX_KB * 4]
+  int32_t* sCoord = reinterpret_cast<int32_t*>(sStage + C::STAGING + 256);  // [KB_CHUNK * 4]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   long long prof_acc[5] = {0, 0, 0, 0, 0};
+  long long prof_epi[4] = {0, 0, 0, 0};   // epilogue: TMEM load+wait, staging wait, STS, fence+issue
   const long long t_start = clock64();
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
   const bool leader = rank == 0;
@@ -295,47 +301,50 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int j0 = int(rank) * C::B_SUB;
       const int j1 = min(j0 + C::B_SUB, n_sub);
       // DW: valid 64-wide M boxes of this CTA and of the whole pair (for the tx byte count)
-      const int row0 = mb * BM * CG + int(rank) * BM;
-      const int m_sub = MODE == DW ? max(0, min(2, (p.M - row0) / 64)) : 0;
-      const int m_sub_pair = MODE == DW ? max(0, min(2 * CG, (p.M - mb * BM * CG) / 64)) : 0;
-      if (MODE != DW) {
-        __syncwarp();
-        for (int i = lane; i < (kb1 - kb0) * 4; i += 32) {
-          const int j = i & 3;
-          sCoord[i] = j < n_sub ? __ldg(p.coord + int64_t(kb0 + (i >> 2)) * p.coord_ld + nb * 4 + j) : 0;
-        }
-        __syncwarp();
-      }
-      if (lane == 0) {
-        // bytes landing on the leader's full barrier per stage (both CTAs)
-        const uint32_t tx = MODE == DW ? uint32_t((m_sub_pair + n_sub) * 64 * 64 * 2)
-                                       : uint32_t(CG * C::A_BYTES + n_sub * 64 * 64 * 2);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          long long tw0 = p.prof ? clock64() : 0;
-          mbar_wait(&empty[s], ph ^ 1);
-          if (p.prof) prof_acc[0] += clock64() - tw0;
-          uint8_t* a = sA + s * C::A_BYTES;
-          uint8_t* b = sB + s * C::B_BYTES;
-          const uint32_t fb = CG == 2 ? map_to_rank(smem_u32(&full[s]), 0) : smem_u32(&full[s]);
-          if (leader) mbar_expect_tx(&full[s], tx);
-          if (MODE == DW) {
-            for (int i = 0; i < m_sub; ++i) tma_load_2d<CG>(&mapA, a + i * 8192, fb, row0 + i * 64, kb * BK);
-            for (int j = j0; j < j1; ++j)
-              tma_load_2d<CG>(&mapB, b + (j - j0) * 8192, fb, nb * BN + j * 64, kb * BK);
-          } else {
-            tma_load_2d<CG>(&mapA, a, fb, kb * BK, row0);
-            const int32_t* cc = sCoord + (kb - kb0) * 4;
-            for (int j = j0; j < j1; ++j) {
-              // FWD: tile (x = kb, y = nb*4 + j); DX: tile (x = nb*4 + j, y = kb).
-              // Packed: row << 4 | neg << 3 | phase; negative tiles read the negated shadow.
-              const int32_t c = cc[j];
-              const int row = (c >> 4) + ((c & 8) ? int(p.neg_row) : 0);
-              tma_load_2d<CG>(&wmaps.m[c & 7], b + (j - j0) * 8192, fb, 0, row);
-            }
+      const int row0 = mb * BM * CG * WM + int(rank) * BM * WM;
+      const int m_sub = MODE == DW ? max(0, min(2 * WM, (p.M - row0) / 64)) : 0;
+      const int m_sub_pair = MODE == DW ? max(0, min(2 * CG * WM, (p.M - mb * BM * CG * WM) / 64)) : 0;
+      // bytes landing on the leader's full barrier per stage (both CTAs)
+      const uint32_t tx = MODE == DW ? uint32_t((m_sub_pair + n_sub) * 64 * 64 * 2)
+                                     : uint32_t(CG * C::A_BYTES + n_sub * 64 * 64 * 2);
+      for (int kc = kb0; kc < kb1; kc += KB_CHUNK) {
+        const int kc1 = min(kc + KB_CHUNK, kb1);
+        if (MODE != DW) {
+          __syncwarp();
+          for (int i = lane; i < (kc1 - kc) * 4; i += 32) {
+            const int j = i & 3;
+            sCoord[i] = j < n_sub ? __ldg(p.coord + int64_t(kc + (i >> 2)) * p.coord_ld + nb * 4 + j) : 0;
           }
-          if (++s == C::STAGES) {
-            s = 0;
-            ph ^= 1;
+          __syncwarp();
+        }
+        if (lane == 0) {
+          for (int kb = kc; kb < kc1; ++kb) {
+            long long tw0 = p.prof ? clock64() : 0;
+            mbar_wait(&empty[s], ph ^ 1);
+            if (p.prof) prof_acc[0] += clock64() - tw0;
+            uint8_t* a = sA + s * C::A_BYTES;
+            uint8_t* b = sB + s * C::B_BYTES;
+            const uint32_t fb = CG == 2 ? map_to_rank(smem_u32(&full[s]), 0) : smem_u32(&full[s]);
+            if (leader) mbar_expect_tx(&full[s], tx);
+            if (MODE == DW) {
+              for (int i = 0; i < m_sub; ++i) tma_load_2d<CG>(&mapA, a + i * 8192, fb, row0 + i * 64, kb * BK);
+              for (int j = j0; j < j1; ++j)
+                tma_load_2d<CG>(&mapB, b + (j - j0) * 8192, fb, nb * BN + j * 64, kb * BK);
+            } else {
+              tma_load_2d<CG>(&mapA, a, fb, kb * BK, row0);
+              const int32_t* cc = sCoord + (kb - kc) * 4;
+              for (int j = j0; j < j1; ++j) {
+                // FWD: tile (x = kb, y = nb*4 + j); DX: tile (x = nb*4 + j, y = kb).
+                // Packed: row << 4 | neg << 3 | phase; negative tiles read the negated shadow.
+                const int32_t c = cc[j];
+                const int row = (c >> 4) + ((c & 8) ? int(p.neg_row) : 0);
+                tma_load_2d<CG>(&wmaps.m[c & 7], b + (j - j0) * 8192, fb, 0, row);
+              }
+            }
+            if (++s == C::STAGES) {
+              s = 0;
+              ph ^= 1;
+            }
           }
         }
       }
@@ -347,7 +356,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // B descriptor strides: MN-major = 64-col sub-tiles 8 KB apart; K-major = 8-row groups 1 KB apart
       int s = 0;
       uint32_t ph = 0;
-      int acc = 0;
+      int acc = 0;          // WM = 1: double-buffered accumulator index
       uint32_t aph = 0;
       for (int u = pair; u < p.units; u += npairs) {
         int mb, nb, split;
@@ -368,18 +377,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t b0 = smem_u32(sB + s * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            uint64_t ad, bd;
-            if (MODE == DW) {
-              ad = sw128_desc(a0 + k * 2048, 8192, 1024);   // MN-major: LBO = next 64 M, SBO = next 8 K rows
-              bd = sw128_desc(b0 + k * 2048, 8192, 1024);
-            } else if (MODE == FWD) {
-              ad = sw128_desc(a0 + k * 32, 16, 1024);       // K-major: +32 B per K=16 step
-              bd = sw128_desc(b0 + k * 2048, 8192, 1024);   // MN-major hashed tiles
-            } else {
-              ad = sw128_desc(a0 + k * 32, 16, 1024);
-              bd = sw128_desc(b0 + k * 32, 16, 1024);       // K-major view of the same tile bytes
+            uint64_t bd;
+            if (MODE == FWD || MODE == DW)
+              bd = sw128_desc(b0 + k * 2048, 8192, 1024);   // MN-major: LBO = next 64 N, SBO = next 8 K rows
+            else
+              bd = sw128_desc(b0 + k * 32, 16, 1024);       // K-major view of the same tile bytes (+32 B / K16)
+#pragma unroll
+            for (int j = 0; j < WM; ++j) {                  // WM M sub-tiles share this B
+              const uint32_t aj = a0 + uint32_t(j * BM * 128);
+              const uint64_t ad = MODE == DW ? sw128_desc(aj + k * 2048, 8192, 1024)   // MN-major A
+                                             : sw128_desc(aj + k * 32, 16, 1024);      // K-major A
+              tc_mma<CG>(d_tmem + uint32_t(j * 256), ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
             }
-            tc_mma<CG>(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           tc_commit<CG>(&empty[s]);
           if (++s == C::STAGES) {
@@ -388,7 +397,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         tc_commit<CG>(&tfull[acc]);
-        acc ^= 1;
+        if (WM == 1) acc ^= 1;
         if (acc == 0) aph ^= 1;
       }
     }
@@ -404,18 +413,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int mb, nb, split;
       decode_unit(p, u, mb, nb, split);
       const int n_valid = min(BN, p.N - nb * BN);
-      const int row_base = mb * BM * CG + int(rank) * BM;
-      // DW: the warp's 32 rows lie in one hash-tile row x; lanes 0..3 fetch the
-      // (offset, lambda*g) of tiles (x, 4 nb + lane) before waiting on the accumulator.
-      int64_t t_off = 0;
-      float t_scale = 0.f;
-      if (MODE == DW) {
-        const int x = (row_base + q * 32) >> 6;
+      // DW: each warp's 32 rows of sub-tile j lie in one hash-tile row x; lanes 0..3
+      // fetch the (offset, lambda*g) of tiles (x, 4 nb + lane) before the accumulator wait.
+      int64_t t_off[WM];
+      float t_scale[WM];
+#pragma unroll
+      for (int j = 0; j < WM; ++j) {
+        t_off[j] = 0;
+        t_scale[j] = 0.f;
+        const int rb = mb * BM * CG * WM + int(rank) * BM * WM + j * BM + q * 32;
         const int y = nb * 4 + (lane & 3);
-        if (lane < 4 && (row_base + q * 32) < p.M && y * 64 < p.N) {
-          const int t = x * p.ny + y;
-          t_off = p.ws ? (int64_t(split) * p.ntiles + t) * 4096 : p.off[t];
-          t_scale = p.sgn[t] < 0 ? -p.lam : p.lam;
+        if (MODE == DW && lane < 4 && rb < p.M && y * 64 < p.N) {
+          const int t = (rb >> 6) * p.ny + y;
+          t_off[j] = p.ws ? (int64_t(split) * p.ntiles + t) * 4096 : p.off[t];
+          t_scale[j] = p.sgn[t] < 0 ? -p.lam : p.lam;
         }
       }
       long long tw3 = p.prof ? clock64() : 0;
@@ -423,84 +434,126 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       long long tw4 = p.prof ? clock64() : 0;
       if (p.prof) prof_acc[3] += tw4 - tw3;
       tc_fence_after();
-      const uint32_t tbase = tmem_base + uint32_t(acc * BN) + (uint32_t(q * 32) << 16);
-      // Each step drains 32 rows x 128 B of output through a 4 KB SW128-swizzled
-      // staging buffer (conflict-free st.shared) and one TMA bulk tensor op:
-      // FWD/DX store 64 bf16 columns of Y / dX; DW stores (deterministic
-      // workspace) or reduce-adds in L2 (dM) 32 fp32 columns of one hash tile.
-      constexpr int COLS = MODE == DW ? 32 : 64;
-      for (int c = 0; c < n_valid / COLS; ++c) {
-        uint32_t pk[32];
-        int64_t tb = 0;
-        if (MODE != DW) {
-          uint32_t r0[32], r1[32];
-          TMEM_LD32(tbase + uint32_t(c * 64), r0);
-          TMEM_LD32(tbase + uint32_t(c * 64 + 32), r1);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            __nv_bfloat162 v = __floats2bfloat162_rn(p.lam * __uint_as_float(r0[2 * i]),
-                                                     p.lam * __uint_as_float(r0[2 * i + 1]));
-            pk[i] = *reinterpret_cast<uint32_t*>(&v);
-            __nv_bfloat162 w = __floats2bfloat162_rn(p.lam * __uint_as_float(r1[2 * i]),
-                                                     p.lam * __uint_as_float(r1[2 * i + 1]));
-            pk[16 + i] = *reinterpret_cast<uint32_t*>(&w);
-          }
-        } else {
-          TMEM_LD32(tbase + uint32_t(c * 32), pk);
-          tmem_wait_ld();
-          const float scale = __shfl_sync(0xffffffffu, t_scale, c >> 1);
-          tb = __shfl_sync(0xffffffffu, t_off, c >> 1);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) pk[i] = __float_as_uint(scale * __uint_as_float(pk[i]));
-        }
-        uint8_t* buf = sStage + (warp - EPI_WARP0) * 8192 + (stg & 1) * 4096;
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        __syncwarp();
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc) {
-          const uint32_t a = smem_u32(buf + lane * 128 + ((cc ^ (lane & 7)) << 4));
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pk[4 * cc]), "r"(pk[4 * cc + 1]),
-                       "r"(pk[4 * cc + 2]), "r"(pk[4 * cc + 3])
-                       : "memory");
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          const uint32_t sb = smem_u32(buf);
+#pragma unroll 1
+      for (int j = 0; j < WM; ++j) {
+        const int row_base = mb * BM * CG * WM + int(rank) * BM * WM + j * BM;
+        const uint32_t tbase = tmem_base + uint32_t(acc * BN + j * 256) + (uint32_t(q * 32) << 16);
+        // Each step drains 32 rows x 128 B of output through a 4 KB SW128-swizzled
+        // staging buffer (conflict-free st.shared) and one TMA bulk tensor op:
+        // FWD/DX store 64 bf16 columns of Y / dX; DW stores (deterministic
+        // workspace) or reduce-adds in L2 (dM) 32 fp32 columns of one hash tile.
+        constexpr int COLS = MODE == DW ? 32 : 64;
+        const int nsteps = n_valid / COLS;
+        auto tload = [&](int c, uint32_t (&r)[64]) {
           if (MODE != DW) {
-            const int x0 = nb * BN + c * 64, y0 = row_base + q * 32;
-            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                             reinterpret_cast<uint64_t>(&mapOut)),
-                         "r"(x0), "r"(y0), "r"(sb)
+            TMEM_LD32(tbase + uint32_t(c * 64), r);
+            TMEM_LD32(tbase + uint32_t(c * 64 + 32), (r + 32));
+          } else {
+            TMEM_LD32(tbase + uint32_t(c * 32), r);
+          }
+        };
+        auto process = [&](int c, uint32_t (&r)[64]) {
+          uint32_t pk[32];
+          int64_t tb = 0;
+          if (MODE != DW) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              __nv_bfloat162 v = __floats2bfloat162_rn(p.lam * __uint_as_float(r[2 * i]),
+                                                       p.lam * __uint_as_float(r[2 * i + 1]));
+              pk[i] = *reinterpret_cast<uint32_t*>(&v);
+            }
+          } else {
+            const float scale = __shfl_sync(0xffffffffu, t_scale[j], c >> 1);
+            tb = __shfl_sync(0xffffffffu, t_off[j], c >> 1);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) pk[i] = __float_as_uint(scale * __uint_as_float(r[i]));
+          }
+          uint8_t* buf = sStage + (warp - EPI_WARP0) * (C::NBUF * 4096) + (stg % C::NBUF) * 4096;
+          long long e1 = p.prof ? clock64() : 0;
+          if (lane == 0 && p.epi == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+          long long e2 = p.prof ? clock64() : 0;
+          if (p.prof) prof_epi[1] += e2 - e1;
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            const uint32_t a = smem_u32(buf + lane * 128 + ((cc ^ (lane & 7)) << 4));
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pk[4 * cc]), "r"(pk[4 * cc + 1]),
+                         "r"(pk[4 * cc + 2]), "r"(pk[4 * cc + 3])
                          : "memory");
-          } else if (row_base + q * 32 < p.M) {   // warps past the last hash-tile row write nothing
-            const int x0 = (c & 1) * 32;
-            const int o1_0 = (row_base + q * 32) & 63;
-            if (p.ws) {   // deterministic: plain store into the per-tile workspace [.. x 64] fp32
-              const int y0 = int(tb >> 6) + o1_0;
+          }
+          if (p.epi == 1) {
+            // transpose through the staging buffer: each warp store covers 4 full 128-B rows
+            __syncwarp();
+            const int rb = row_base + q * 32;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int idx = i * 32 + lane, rr = idx >> 3, ch = idx & 7;
+              uint4 v;
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                           : "r"(smem_u32(buf + rr * 128 + ((ch ^ (rr & 7)) << 4))));
+              if (MODE != DW) {
+                const int64_t m = int64_t(rb) + rr;
+                if (m < p.T) *reinterpret_cast<uint4*>(p.out + m * p.N + nb * BN + c * 64 + ch * 8) = v;
+              } else if (rb < p.M) {
+                float* dst = (p.ws ? p.ws : p.dM) + tb + ((rb + rr) & 63) * 64 + (c & 1) * 32 + ch * 4;
+                const float4 f = make_float4(__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z),
+                                             __uint_as_float(v.w));
+                if (p.ws)
+                  *reinterpret_cast<float4*>(dst) = f;
+                else
+                  atomicAdd(reinterpret_cast<float4*>(dst), f);
+              }
+            }
+            ++stg;
+            return;
+          }
+          long long e3 = p.prof ? clock64() : 0;
+          if (p.prof) prof_epi[2] += e3 - e2;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (p.prof) prof_epi[3] += clock64() - e3;
+          if (lane == 0) {
+            const uint32_t sb = smem_u32(buf);
+            if (MODE != DW) {
+              const int x0 = nb * BN + c * 64, y0 = row_base + q * 32;
               asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                                reinterpret_cast<uint64_t>(&mapOut)),
                            "r"(x0), "r"(y0), "r"(sb)
                            : "memory");
-            } else {      // fast: TMA reduce-add into dM in L2 through the 16-byte-phase view of dM
-              const int y0 = int(tb >> 6) + o1_0;
-              asm volatile(
-                  "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                      reinterpret_cast<uint64_t>(&wmaps.m[(tb >> 3) & 7])),
-                  "r"(x0), "r"(y0), "r"(sb)
-                  : "memory");
+            } else if (row_base + q * 32 < p.M) {   // warps past the last hash-tile row write nothing
+              const int x0 = (c & 1) * 32;
+              const int y0 = int(tb >> 6) + ((row_base + q * 32) & 63);
+              if (p.ws)   // deterministic: plain store into the per-tile workspace [.. x 64] fp32
+                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                 reinterpret_cast<uint64_t>(&mapOut)),
+                             "r"(x0), "r"(y0), "r"(sb)
+                             : "memory");
+              else        // fast: TMA reduce-add into dM in L2 through the 32-byte-phase view of dM
+                asm volatile(
+                    "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                        reinterpret_cast<uint64_t>(&wmaps.m[(tb >> 3) & 7])),
+                    "r"(x0), "r"(y0), "r"(sb)
+                    : "memory");
             }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          ++stg;
+        };
+        uint32_t ra[64];
+        for (int c = 0; c < nsteps; ++c) {
+          long long e0 = p.prof ? clock64() : 0;
+          tload(c, ra);
+          tmem_wait_ld();
+          if (p.prof) prof_epi[0] += clock64() - e0;
+          process(c, ra);
         }
-        ++stg;
       }
       if (p.prof) prof_acc[4] += clock64() - tw4;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader0 + uint32_t(acc * 8));
-      acc ^= 1;
+      if (WM == 1) acc ^= 1;
       if (acc == 0) aph ^= 1;
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // staging reads + writes done
@@ -509,9 +562,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (p.prof && lane == 0) {
     long long* o = p.prof + blockIdx.x * 8;
-    if (warp == 0) { o[0] = prof_acc[0]; o[5] = clock64() - t_start; }
-    if (warp == 1) { o[1] = prof_acc[1]; o[2] = prof_acc[2]; }
-    if (warp == EPI_WARP0) { o[3] = prof_acc[3]; o[4] = prof_acc[4]; }
+    if (warp == 0) { o[5] = clock64() - t_start; }
+    if (warp == 1) { o[1] = prof_acc[1]; }
+    if (warp == EPI_WARP0) { o[3] = prof_acc[3]; o[4] = prof_acc[4]; o[6] = prof_epi[0]; o[7] = prof_epi[1]; o[2] = prof_epi[2]; o[0] = prof_epi[3]; }
   }
   tc_fence_before();
   if (CG == 2)
@@ -576,14 +629,14 @@ int cta_group() {
   return cg;
 }
 
-template <int MODE, int CG>
+template <int MODE, int CG, int WM>
 roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o, const WMaps& w,
                          const Params& p, cudaStream_t s) {
-  using C = Cfg<CG>;
+  using C = Cfg<CG, WM>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
-        cudaFuncSetAttribute(roast_mm_sm100<MODE, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(roast_mm_sm100<MODE, CG, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(smem)");
     attr = true;
   }
@@ -602,12 +655,13 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
   cfg.numAttrs = 1;
   static long long* prof = nullptr;
   Params pp = p;
+  if (const char* e = getenv("ROAST_EPI")) pp.epi = atoi(e);
   if (getenv("ROAST_PROF")) {
     if (!prof) cudaMallocManaged(&prof, sizeof(long long) * 8 * 512);
     cudaMemset(prof, 0, sizeof(long long) * 8 * 512);
     pp.prof = prof;
   }
-  cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mm_sm100<MODE, CG>, a, b, o, w, pp);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mm_sm100<MODE, CG, WM>, a, b, o, w, pp);
   if (e != cudaSuccess) return cuda_fail(e, "roast_mm_sm100 launch");
   if (pp.prof) {
     cudaDeviceSynchronize();
@@ -618,18 +672,19 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
       mx = std::max(mx, prof[i * 8 + 5]);
     }
     const int n = pairs * CG, nl = (pairs * CG + CG - 1) / CG;
-    fprintf(stderr, "[roast prof] mode %d cg %d units %d kb %d | total %.0f (max %lld) | prod wait-empty %.0f | "
-            "mma wait-full %.0f wait-tempty %.0f | epi wait-tfull %.0f busy %.0f  (cycles, mean/CTA)\n",
+    fprintf(stderr, "[roast prof] mode %d cg %d units %d kb %d | total %.0f (max %lld) | epi-fence %.0f | "
+            "mma wait-full %.0f epi-sts %.0f | epi wait-tfull %.0f busy %.0f (tmem %.0f, stg-wait %.0f)  (cycles, mean/CTA)\n",
             MODE, CG, p.units, p.k_blocks, acc[5] / n, mx, acc[0] / n, acc[1] / nl, acc[2] / nl, acc[3] / n,
-            acc[4] / n);
+            acc[4] / n, acc[6] / n, acc[7] / n);
   }
   return ROAST_OK;
 }
 
 template <int MODE>
 roast_status_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o, const WMaps& w, Params p,
-                      cudaStream_t s) {
-  return cta_group() == 2 ? launch_cg<MODE, 2>(a, b, o, w, p, s) : launch_cg<MODE, 1>(a, b, o, w, p, s);
+                      int wm, cudaStream_t s) {
+  if (cta_group() == 1) return launch_cg<MODE, 1, 1>(a, b, o, w, p, s);
+  return wm == 2 ? launch_cg<MODE, 2, 2>(a, b, o, w, p, s) : launch_cg<MODE, 2, 1>(a, b, o, w, p, s);
 }
 
 }  // namespace sm100
@@ -652,7 +707,7 @@ roast_status_t sm100_prepare(Ctx* c) {
 
 static bool supported(const Ctx* c, const Module& m) {
   return m.d_coord_xy != nullptr && c->cfg.tile_layout == ROAST_ROW_MAJOR && c->tile.z1 == 64 &&
-         c->tile.z2 == 64 && m.H % 64 == 0 && m.O % 64 == 0 && m.H / 64 <= MAX_KB && m.O / 64 <= MAX_KB;
+         c->tile.z2 == 64 && m.H % 64 == 0 && m.O % 64 == 0;
 }
 
 static Params base_params(const Ctx* c, const Module& m, int64_t T) {
@@ -668,20 +723,35 @@ static Params base_params(const Ctx* c, const Module& m, int64_t T) {
   return p;
 }
 
+// WM (M sub-tiles per CTA) from a makespan model: WM = 2 halves the TMA box rate per
+// MMA (one 256-row A box + the same B feeds two MMAs) but doubles the unit size and
+// exposes the epilogue (single-buffered accumulator).  eff = measured MMA-busy share.
+static int choose_wm(int64_t m_rows, int n_tiles, int splits) {
+  if (const char* e = getenv("ROAST_WM")) return atoi(e) == 2 ? 2 : 1;
+  if (cta_group() != 2) return 1;
+  const int pairs = num_sms() / 2;
+  auto cost = [&](int wm, double eff) {
+    const int64_t units = ((m_rows + 256 * wm - 1) / (256 * wm)) * n_tiles * splits;
+    return double((units + pairs - 1) / pairs) * wm / eff;
+  };
+  return cost(2, 0.85) < cost(1, 0.6) ? 2 : 1;
+}
+
 // FWD / DX share the geometry: M = tokens, N = the module's output side, K = its input side.
 static roast_status_t run_tok_major(Ctx* c, const Module& m, const void* A, void* out, int64_t T, int N, int K,
                                     const int32_t* coord, int coord_ld, bool dx, cudaStream_t s) {
   if (!supported(c, m) || T >= (int64_t(1) << 31)) return ROAST_ERR_UNSUPPORTED;
   roast_status_t st = sm100_prepare(c);
   if (st) return st;
+  const int wm = choose_wm(T, (N + BN - 1) / BN, 1);
   CUtensorMap a;
-  st = make_map_2d(&a, A, uint64_t(K), uint64_t(T), uint64_t(K) * 2, BK, BM);
+  st = make_map_2d(&a, A, uint64_t(K), uint64_t(T), uint64_t(K) * 2, BK, BM * wm);
   if (st) return st;
   Params p = base_params(c, m, T);
   p.M = int(std::min<int64_t>(T, 1 << 30));
   p.N = N;
   p.K = K;
-  p.m_tiles = int((T + BM * cta_group() - 1) / (BM * cta_group()));
+  p.m_tiles = int((T + BM * cta_group() * wm - 1) / (BM * cta_group() * wm));
   p.n_tiles = (p.N + BN - 1) / BN;
   p.k_blocks = p.K / BK;
   p.kb_per_split = p.k_blocks;
@@ -693,7 +763,7 @@ static roast_status_t run_tok_major(Ctx* c, const Module& m, const void* A, void
   st = make_map_2d(&o, out, uint64_t(N), uint64_t(T), uint64_t(N) * 2, 64, 32);
   if (st) return st;
   const WMaps& w = *reinterpret_cast<const WMaps*>(c->tmap_shadow);
-  st = dx ? launch<DX>(a, a, o, w, p, s) : launch<FWD>(a, a, o, w, p, s);
+  st = dx ? launch<DX>(a, a, o, w, p, wm, s) : launch<FWD>(a, a, o, w, p, wm, s);
   if (!st) c->launches++;
   return st;
 }
@@ -718,20 +788,28 @@ roast_status_t sm100_dw(Ctx* c, const Module& m, const void* X, const void* dY, 
   Params p = base_params(c, m, T);
   p.M = int(m.H);
   p.N = int(m.O);
-  p.m_tiles = (p.M + BM * cg - 1) / (BM * cg);
   p.n_tiles = (p.N + BN - 1) / BN;
   p.k_blocks = int((T + BK - 1) / BK);
-  // split-K over tokens: the smallest split s minimising the makespan ceil(tiles*s / slots) / s
-  const int tiles = p.m_tiles * p.n_tiles;
-  int splits = 1;
+  // (WM, split-K over tokens) minimising the makespan ceil(units / slots) * WM / (eff * s);
+  // eff = TMA-box-rate bound MMA share (4 boxes / 512 clk for WM 1, 6 / 1024 for WM 2)
+  int wm = 1, splits = 1;
   double best = 1e30;
-  for (int sp = 1; sp <= std::min(p.k_blocks, 16); ++sp) {
-    const double cost = double((tiles * sp + slots - 1) / slots) / sp;
-    if (cost < best - 1e-9) {
-      best = cost;
-      splits = sp;
+  const char* ewm = getenv("ROAST_WM");
+  for (int w = 1; w <= (cg == 2 ? 2 : 1); ++w) {
+    if (ewm && atoi(ewm) != w) continue;
+    const int tiles_w = ((p.M + BM * cg * w - 1) / (BM * cg * w)) * p.n_tiles;
+    const double eff = w == 2 ? 0.78 : 0.58;
+    for (int sp = 1; sp <= std::min(p.k_blocks, 16); ++sp) {
+      const double cost = double((tiles_w * sp + slots - 1) / slots) * w / (eff * sp);
+      if (cost < best - 1e-9) {
+        best = cost;
+        splits = sp;
+        wm = w;
+      }
     }
   }
+  p.m_tiles = (p.M + BM * cg * wm - 1) / (BM * cg * wm);
+  const int tiles = p.m_tiles * p.n_tiles;
   p.kb_per_split = (p.k_blocks + splits - 1) / splits;
   splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;   // no empty splits
   p.splits = splits;
@@ -758,7 +836,7 @@ roast_status_t sm100_dw(Ctx* c, const Module& m, const void* X, const void* dY, 
       if (st) return st;
     }
   }
-  st = launch<DW>(a, b, o, dmaps, p, s);
+  st = launch<DW>(a, b, o, dmaps, p, wm, s);
   if (st) return st;
   c->launches++;
   if (det) {
