@@ -184,12 +184,8 @@ def run_gpu(args):
     stream = torch.cuda.current_stream()
     M = torch.tensor(synth.uniform(synth.SEED_M, (mem,)).astype(np.float32), device=dev)
     ctx = R.Roast(M, TILE, TILE, seed=synth.HASH_SEED, deterministic=args.deterministic)
-    if world > 1:
-        import torch.distributed as dist
-        uid = R.roast_comm_unique_id() if rank == 0 else bytes(128)
-        t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
-        dist.broadcast(t, 0)
-        R.roast_comm_init(ctx.h, rank, world, bytes(t.cpu().tolist()))
+    from paper_2207_10702_b200 import dp
+    dp.init_comm(ctx, rank, world, device=dev)   # NCCL communicator inside libroast (no-op at N = 1)
     l1 = ctx.linear(*LAYERS[0])
     l2 = ctx.linear(*LAYERS[1])
     bf = torch.bfloat16

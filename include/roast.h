@@ -176,6 +176,13 @@ roast_status_t roast_debug_chunk_map(roast_t h, int32_t id, const int64_t* d_row
  * dt = BF16: g * bf16(M) read from the shadow (the tensor-core operand, lambda deferred). */
 roast_status_t roast_debug_materialize(roast_t h, int32_t id, roast_dtype_t dt, void* d_W,
                                        roast_stream_t stream);
+/* Evaluate the library's hash (the same __host__ __device__ code the kernels run,
+ * including the reciprocal `mod R`) on the HOST for n keys of module `module`:
+ * off_out[i] = A * (poly(key) mod R), R = floor((mem_size - span)/align) + 1, and
+ * sgn_out[i] = g(key).  Needs no GPU (CPU parity tests).  keys < 2^60. */
+roast_status_t roast_debug_hash_host(uint64_t seed, int32_t module, const uint64_t* keys_host, int64_t n,
+                                     int64_t mem_size, int64_t span, int32_t align, int32_t use_sign,
+                                     int64_t* off_out_host, int8_t* sgn_out_host);
 /* Number of kernels this handle has launched since creation (bench evidence). */
 int64_t roast_launch_count(roast_t h);
 

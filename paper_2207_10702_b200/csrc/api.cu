@@ -176,7 +176,7 @@ roast_status_t roast_register_linear(roast_t h, int64_t H, int64_t O, int32_t* i
   const uint32_t mid = uint32_t(c->modules.size());
   m.hash.off = make_coef(c->seed, mid, 0);
   m.hash.sgn = make_coef(c->seed, mid, 1);
-  m.hash.R = uint64_t((c->mem_size - T) / A + 1);
+  m.hash.set_range(uint64_t((c->mem_size - T) / A + 1));
   m.hash.align = uint32_t(A);
   m.hash.use_sign = c->cfg.use_sign ? 1u : 0u;
   const int64_t nt = int64_t(m.nx) * m.ny;
@@ -256,7 +256,7 @@ roast_status_t roast_register_embedding(roast_t h, int64_t num_rows, int32_t dim
   const uint32_t mid = uint32_t(c->modules.size());
   m.hash.off = make_coef(c->seed, mid, 0);
   m.hash.sgn = make_coef(c->seed, mid, 1);
-  m.hash.R = uint64_t((c->mem_size - chunk) / A + 1);
+  m.hash.set_range(uint64_t((c->mem_size - chunk) / A + 1));
   m.hash.align = uint32_t(A);
   m.hash.use_sign = c->cfg.use_sign ? 1u : 0u;
   m.lam = float(c->cfg.C / sqrt(fan_in > 0 ? fan_in : double(dim)));
@@ -457,3 +457,22 @@ int64_t roast_launch_count(roast_t h) {
 }
 
 }  // extern "C"
+
+extern "C" roast_status_t roast_debug_hash_host(uint64_t seed, int32_t module, const uint64_t* keys, int64_t n,
+                                                int64_t mem_size, int64_t span, int32_t align, int32_t use_sign,
+                                                int64_t* off_out, int8_t* sgn_out) {
+  if (!keys || n < 0 || span <= 0 || align <= 0) return fail(ROAST_ERR_CONFIG, "bad arguments");
+  if (span > mem_size) return fail(ROAST_ERR_GEOMETRY, "span larger than |M|");
+  ModuleHash h;
+  h.off = make_coef(seed, uint32_t(module), 0);
+  h.sgn = make_coef(seed, uint32_t(module), 1);
+  h.set_range(uint64_t((mem_size - span) / align + 1));
+  h.align = uint32_t(align);
+  h.use_sign = use_sign ? 1u : 0u;
+  for (int64_t i = 0; i < n; ++i) {
+    if (keys[i] >= (uint64_t(1) << 60)) return fail(ROAST_ERR_CONFIG, "key >= 2^60");
+    if (off_out) off_out[i] = int64_t(h.offset(keys[i]));
+    if (sgn_out) sgn_out[i] = int8_t(h.sign(keys[i]));
+  }
+  return ROAST_OK;
+}

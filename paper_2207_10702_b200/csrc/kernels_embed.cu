@@ -39,7 +39,7 @@ __device__ __forceinline__ void pair_hash(const EmbArgs& a, const int64_t* idx, 
   sg = float(a.hash.sign(key));
 }
 
-template <bool kBwd>
+template <bool kBwd, int U>
 __global__ void __launch_bounds__(256) embed_kernel(EmbArgs a, const int64_t* __restrict__ idx, int64_t n,
                                                     const float* __restrict__ M, float* __restrict__ out,
                                                     const float* __restrict__ dOut, float* __restrict__ dM,
@@ -54,35 +54,46 @@ __global__ void __launch_bounds__(256) embed_kernel(EmbArgs a, const int64_t* __
     float sg;
     int j;
     pair_hash(a, idx, n, base + lane, off, sg, b, j, err);
+    // 32 pairs x Z/4 float4 per pair; each lane moves 8 float4 per batch with all 8
+    // loads in flight before the first use (memory-level parallelism for the gathers)
     const int total = 32 * v_per_chunk;
-    for (int e = lane; e < total; e += 32) {
-      int p = e / v_per_chunk;
-      int part = e - p * v_per_chunk;
-      int64_t poff = __shfl_sync(0xffffffff, off, p);
-      float psg = __shfl_sync(0xffffffff, sg, p);
-      int64_t pb = __shfl_sync(0xffffffff, b, p);
-      int pj = __shfl_sync(0xffffffff, j, p);
-      if (pb >= n) continue;
-      int col = pj * a.chunk + part * 4;
-      if (col >= a.dim) continue;  // padded tail of the last chunk (R16)
-      float* o = (kBwd ? nullptr : out) + pb * a.dim + col;
-      if (!kBwd) {
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (poff >= 0) {
-          float4 m = __ldg(reinterpret_cast<const float4*>(M + poff + part * 4));
+    for (int e0 = 0; e0 < total; e0 += 32 * U) {
+      float4 val[U];
+      int64_t dst[U];
+      float scl[U];
+      int st[U];  // 0: skip, 1: write (zeros if invalid row), 2: data
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * 32 + lane;
+        const int pp = e / v_per_chunk;
+        const int part = e - pp * v_per_chunk;
+        const int64_t poff = __shfl_sync(0xffffffff, off, pp & 31);
+        const float psg = __shfl_sync(0xffffffff, sg, pp & 31);
+        const int64_t pb = __shfl_sync(0xffffffff, b, pp & 31);
+        const int pj = __shfl_sync(0xffffffff, j, pp & 31);
+        const int col = pj * a.chunk + part * 4;
+        st[u] = (e < total && pb < n && col < a.dim) ? (poff >= 0 ? 2 : 1) : 0;   // R16 padded tail
+        scl[u] = kBwd ? psg * a.lam : psg;
+        dst[u] = kBwd ? poff + part * 4 : pb * a.dim + col;
+        val[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (st[u] == 2)
+          val[u] = __ldg(reinterpret_cast<const float4*>(kBwd ? dOut + pb * a.dim + col : M + poff + part * 4));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!kBwd) {
+          if (st[u] == 0) continue;
           // g * fp32(lambda * M): one rounding, then an exact sign flip
-          v.x = psg * __fmul_rn(a.lam, m.x);
-          v.y = psg * __fmul_rn(a.lam, m.y);
-          v.z = psg * __fmul_rn(a.lam, m.z);
-          v.w = psg * __fmul_rn(a.lam, m.w);
+          const float4 m = val[u];
+          const float4 v = make_float4(scl[u] * __fmul_rn(a.lam, m.x), scl[u] * __fmul_rn(a.lam, m.y),
+                                       scl[u] * __fmul_rn(a.lam, m.z), scl[u] * __fmul_rn(a.lam, m.w));
+          *reinterpret_cast<float4*>(out + dst[u]) = v;
+        } else {
+          if (st[u] != 2) continue;
+          const float4 g = val[u];
+          atomicAdd(reinterpret_cast<float4*>(dM + dst[u]),
+                    make_float4(scl[u] * g.x, scl[u] * g.y, scl[u] * g.z, scl[u] * g.w));
         }
-        *reinterpret_cast<float4*>(o) = v;
-      } else {
-        if (poff < 0) continue;
-        float4 g = __ldg(reinterpret_cast<const float4*>(dOut + pb * a.dim + col));
-        float s = psg * a.lam;
-        float4 v = make_float4(s * g.x, s * g.y, s * g.z, s * g.w);
-        atomicAdd(reinterpret_cast<float4*>(dM + poff + part * 4), v);
       }
     }
   }
@@ -113,7 +124,7 @@ EmbArgs emb_args(const Module& m) {
 int emb_grid(int64_t n, int q) {
   int64_t warps = (n * q + 31) / 32;
   int64_t blocks = (warps + 7) / 8;
-  int64_t cap = 148 * 8;  // persistent-ish: 8 CTAs of 8 warps per SM
+  int64_t cap = 148 * 8;  // persistent-ish: up to 8 CTAs of 8 warps per SM
   if (blocks > cap) blocks = cap;
   return int(blocks < 1 ? 1 : blocks);
 }
@@ -123,7 +134,9 @@ int emb_grid(int64_t n, int q) {
 cudaError_t launch_embed_fwd(const Ctx* c, const Module& m, const int64_t* idx, int64_t n, float* out,
                              cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  embed_kernel<false><<<emb_grid(n, m.chunks_per_row), 256, 0, s>>>(emb_args(m), idx, n, c->M, out, nullptr,
+  static const int U = getenv("ROAST_EMB_U") ? atoi(getenv("ROAST_EMB_U")) : 4;
+  if (U == 8) embed_kernel<false, 8><<<emb_grid(n, m.chunks_per_row), 256, 0, s>>>(emb_args(m), idx, n, c->M, out, nullptr, nullptr, c->d_err);
+  else embed_kernel<false, 4><<<emb_grid(n, m.chunks_per_row), 256, 0, s>>>(emb_args(m), idx, n, c->M, out, nullptr,
                                                                       nullptr, c->d_err);
   return cudaGetLastError();
 }
@@ -131,7 +144,9 @@ cudaError_t launch_embed_fwd(const Ctx* c, const Module& m, const int64_t* idx, 
 cudaError_t launch_embed_bwd(const Ctx* c, const Module& m, const int64_t* idx, int64_t n, const float* dOut,
                              cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  embed_kernel<true><<<emb_grid(n, m.chunks_per_row), 256, 0, s>>>(emb_args(m), idx, n, nullptr, nullptr, dOut,
+  static const int U = getenv("ROAST_EMB_U") ? atoi(getenv("ROAST_EMB_U")) : 4;
+  if (U == 8) embed_kernel<true, 8><<<emb_grid(n, m.chunks_per_row), 256, 0, s>>>(emb_args(m), idx, n, nullptr, nullptr, dOut, c->dM, c->d_err);
+  else embed_kernel<true, 4><<<emb_grid(n, m.chunks_per_row), 256, 0, s>>>(emb_args(m), idx, n, nullptr, nullptr, dOut,
                                                                      c->dM, c->d_err);
   return cudaGetLastError();
 }

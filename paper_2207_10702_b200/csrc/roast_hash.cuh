@@ -69,13 +69,50 @@ RH_HD uint64_t poly61(const PolyCoef& p, uint64_t key) {
 
 RH_HD uint64_t tile_key(uint32_t x, uint32_t y) { return (uint64_t(x) << 32) | y; }
 
+// Exact v mod R for v < 2^61 by an invariant-divisor reciprocal (Granlund & Montgomery
+// 1994, Thm 4.2 with N = 61): l = ceil(log2 R), m = ceil(2^(61+l) / R) < 2^63,
+// q = floor(v m / 2^(61+l)) = floor(v / R) for every v < 2^61.  The device path avoids
+// the ~100-instruction software 64-bit division of `%`.
+struct ModReciprocal {
+  uint64_t R = 1, m = 0;
+  uint32_t s = 0;  // 61 + l
+  void init(uint64_t r) {
+    R = r;
+    uint32_t l = 0;
+    while ((uint64_t(1) << l) < r) ++l;
+    s = 61 + l;
+    // m = ceil(2^s / R) with 128-bit arithmetic (host only)
+    unsigned __int128 p = (unsigned __int128)1 << s;
+    m = uint64_t((p + R - 1) / R);
+  }
+};
+
+RH_HD uint64_t mod_recip(uint64_t v, const ModReciprocal& d) {
+  uint64_t lo, hi;
+#ifdef __CUDA_ARCH__
+  lo = v * d.m;
+  hi = __umul64hi(v, d.m);
+#else
+  unsigned __int128 p = (unsigned __int128)v * d.m;
+  lo = (uint64_t)p;
+  hi = (uint64_t)(p >> 64);
+#endif
+  const uint64_t q = d.s >= 64 ? (hi >> (d.s - 64)) : ((hi << (64 - d.s)) | (lo >> d.s));
+  return v - q * d.R;
+}
+
 struct ModuleHash {
   PolyCoef off, sgn;
   uint64_t R;       // number of legal aligned positions
   uint32_t align;   // A
   uint32_t use_sign;
+  ModReciprocal rdiv;  // v mod R without division (set by set_range)
 
-  RH_HD uint64_t offset(uint64_t key) const { return uint64_t(align) * (poly61(off, key) % R); }
+  void set_range(uint64_t r) {
+    R = r;
+    rdiv.init(r);
+  }
+  RH_HD uint64_t offset(uint64_t key) const { return uint64_t(align) * mod_recip(poly61(off, key), rdiv); }
   RH_HD int sign(uint64_t key) const {
     return (use_sign && (poly61(sgn, key) & 1)) ? -1 : 1;
   }

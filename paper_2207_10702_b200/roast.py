@@ -26,7 +26,7 @@ EXPORTS = [
     "roast_linear_bwd_dx", "roast_linear_bwd_dm", "roast_embedding_fwd", "roast_embedding_bwd", "roast_comm_unique_id", "roast_comm_init",
     "roast_grad_allreduce", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_get_error",
     "roast_status_str", "roast_last_error", "roast_debug_tile_map", "roast_debug_chunk_map",
-    "roast_debug_materialize", "roast_launch_count",
+    "roast_debug_materialize", "roast_debug_hash_host", "roast_launch_count",
 ]
 
 
@@ -81,6 +81,7 @@ def _load():
         "roast_debug_chunk_map": (st, [H, I32, P, I64, P, P, S]),
         "roast_debug_materialize": (st, [H, I32, ctypes.c_int, P, S]),
         "roast_launch_count": (I64, [H]),
+        "roast_debug_hash_host": (st, [U64, I32, P, I64, I64, I64, I32, I32, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -203,6 +204,17 @@ def roast_debug_materialize(h, mid, dtype, W_ptr, stream=0):
 
 def roast_launch_count(h):
     return _lib.roast_launch_count(h)
+
+
+def roast_debug_hash_host(seed, module, keys, mem_size, span, align=8, use_sign=True):
+    """(offsets, signs) of the library hash evaluated on the host (no GPU needed)."""
+    import numpy as np
+    keys = np.ascontiguousarray(keys, dtype=np.uint64)
+    off = np.empty(len(keys), dtype=np.int64)
+    sgn = np.empty(len(keys), dtype=np.int8)
+    _check(_lib.roast_debug_hash_host(seed, module, keys.ctypes.data, len(keys), mem_size, span, align,
+                                      int(use_sign), off.ctypes.data, sgn.ctypes.data), "roast_debug_hash_host")
+    return off, sgn
 
 
 # ---- torch convenience wrapper --------------------------------------------------------------
