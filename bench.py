@@ -292,11 +292,27 @@ def run_gpu(args):
     ms_per_step = total_ms / args.steps
     value = world * flops_per_step(T) / (ms_per_step * 1e-3) / 1e12
 
-    # per-kernel-kind launch durations: eager single-stream pass with events around each call
-    # (every call is one kernel launch in the atomic dM mode), same flush discipline
+    # per-kernel-kind launch durations: each call captured alone in a CUDA graph and replayed
+    # between CUDA events (device time of exactly that launch, no host launch latency)
+    calls = [("fwd", lambda: ctx.fwd(l1, X, Y1)), ("fwd", lambda: ctx.fwd(l2, Y1, Y2)),
+             ("dx", lambda: ctx.bwd_dx(l2, dY2, dY1)), ("dm", lambda: ctx.bwd_dm(l2, Y1, dY2)),
+             ("dx", lambda: ctx.bwd_dx(l1, dY1, dX)), ("dm", lambda: ctx.bwd_dm(l1, X, dY1))]
+    call_graphs = []
+    for kind, fn in calls:
+        cg_ = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(cg_):
+            fn()
+        call_graphs.append((kind, cg_))
+    torch.cuda.synchronize()
     for _ in range(args.steps):
         flush.zero_()
-        step_body(X, dY2, record=True)
+        for kind, cg_ in call_graphs:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            cg_.replay()
+            b.record(stream)
+            ev[kind].append((a, b))
     torch.cuda.synchronize()
     kind_ms = {k: float(np.mean([a.elapsed_time(b) for a, b in ev[k]])) for k in kinds}
     gemm_flop = 2.0 * T * 768 * 3072                       # every call is one 2*T*H*O contraction

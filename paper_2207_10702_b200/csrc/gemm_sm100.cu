@@ -91,6 +91,7 @@ struct Params {
   int ntiles;
   long long* prof;      // debug (ROAST_PROF): per-CTA cycle counters, else null
   int epi;              // 0: TMA bulk store / reduce from staging; 1: coalesced st.global / red.global.v4
+  int dw3d;             // DW operands loaded as one 3-D TMA box per operand (else 64x64 2-D boxes)
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -148,6 +149,22 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, void* dst, u
         "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
         "%3}], [%4];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
+        : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, void* dst, uint32_t bar_cluster, int c0, int c1,
+                                            int c2) {
+  if (CG == 1)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cluster)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cluster)
         : "memory");
 }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
@@ -246,6 +263,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   long long prof_acc[5] = {0, 0, 0, 0, 0};
   long long prof_epi[4] = {0, 0, 0, 0};   // epilogue: TMEM load+wait, staging wait, STS, fence+issue
   const long long t_start = clock64();
+  uint64_t g_start = 0;
+  if (p.prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
   const bool leader = rank == 0;
   const int pair = blockIdx.x / CG;
@@ -305,7 +324,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int m_sub = MODE == DW ? max(0, min(2 * WM, (p.M - row0) / 64)) : 0;
       const int m_sub_pair = MODE == DW ? max(0, min(2 * CG * WM, (p.M - mb * BM * CG * WM) / 64)) : 0;
       // bytes landing on the leader's full barrier per stage (both CTAs)
-      const uint32_t tx = MODE == DW ? uint32_t((m_sub_pair + n_sub) * 64 * 64 * 2)
+      // DW: one 3-D box per operand per CTA (2*WM 64-wide h blocks of X, 2 o blocks of dY);
+      // out-of-range blocks are zero-filled and still counted
+      const uint32_t tx = MODE == DW ? (p.dw3d ? uint32_t(CG * (C::A_BYTES + C::B_BYTES))
+                                               : uint32_t((m_sub_pair + n_sub) * 64 * 64 * 2))
                                      : uint32_t(CG * C::A_BYTES + n_sub * 64 * 64 * 2);
       for (int kc = kb0; kc < kb1; kc += KB_CHUNK) {
         const int kc1 = min(kc + KB_CHUNK, kb1);
@@ -326,7 +348,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint8_t* b = sB + s * C::B_BYTES;
             const uint32_t fb = CG == 2 ? map_to_rank(smem_u32(&full[s]), 0) : smem_u32(&full[s]);
             if (leader) mbar_expect_tx(&full[s], tx);
-            if (MODE == DW) {
+            if (MODE == DW && p.dw3d) {
+              tma_load_3d<CG>(&mapA, a, fb, 0, kb * BK, row0 >> 6);
+              tma_load_3d<CG>(&mapB, b, fb, 0, kb * BK, (nb * BN + j0 * 64) >> 6);
+            } else if (MODE == DW) {
               for (int i = 0; i < m_sub; ++i) tma_load_2d<CG>(&mapA, a + i * 8192, fb, row0 + i * 64, kb * BK);
               for (int j = j0; j < j1; ++j)
                 tma_load_2d<CG>(&mapB, b + (j - j0) * 8192, fb, nb * BN + j * 64, kb * BK);
@@ -562,9 +587,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (p.prof && lane == 0) {
     long long* o = p.prof + blockIdx.x * 8;
-    if (warp == 0) { o[5] = clock64() - t_start; }
+    if (warp == 0) {
+      o[5] = clock64() - t_start;
+      uint64_t g_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+      o[3] = (long long)(g_end - g_start);   // ns
+    }
     if (warp == 1) { o[1] = prof_acc[1]; }
-    if (warp == EPI_WARP0) { o[3] = prof_acc[3]; o[4] = prof_acc[4]; o[6] = prof_epi[0]; o[7] = prof_epi[1]; o[2] = prof_epi[2]; o[0] = prof_epi[3]; }
+    if (warp == EPI_WARP0) { o[4] = prof_acc[4]; o[6] = prof_epi[0]; o[7] = prof_epi[1]; o[2] = prof_epi[2]; o[0] = prof_epi[3]; }
   }
   tc_fence_before();
   if (CG == 2)
@@ -607,6 +637,24 @@ roast_status_t make_map_2d(CUtensorMap* map, const void* base, uint64_t cols, ui
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ROAST_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return ROAST_OK;
+}
+
+// 3-D view of a row-major bf16 [rows x cols] tensor as {64 cols, rows, cols / 64 blocks}: one box
+// {64, box_r, nblk} fetches nblk 64-wide column blocks, each landing as its own [box_r x 128 B]
+// SW128 atom column — the MN-major operand layout — in a single TMA operation.
+roast_status_t make_map_blocks(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint32_t box_r,
+                               uint32_t nblk) {
+  auto fn = encode_fn();
+  if (!fn) return fail(ROAST_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {64, rows, cols / 64};
+  cuuint64_t strides[2] = {cols * 2, 128};
+  cuuint32_t box[3] = {64, box_r, nblk};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ROAST_ERR_CUDA, "cuTensorMapEncodeTiled(3d) failed (" + std::to_string(int(r)) + ")");
   return ROAST_OK;
 }
 
@@ -672,9 +720,9 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
       mx = std::max(mx, prof[i * 8 + 5]);
     }
     const int n = pairs * CG, nl = (pairs * CG + CG - 1) / CG;
-    fprintf(stderr, "[roast prof] mode %d cg %d units %d kb %d | total %.0f (max %lld) | epi-fence %.0f | "
-            "mma wait-full %.0f epi-sts %.0f | epi wait-tfull %.0f busy %.0f (tmem %.0f, stg-wait %.0f)  (cycles, mean/CTA)\n",
-            MODE, CG, p.units, p.k_blocks, acc[5] / n, mx, acc[0] / n, acc[1] / nl, acc[2] / nl, acc[3] / n,
+    fprintf(stderr, "[roast prof] dw3d %d wm %d mode %d cg %d units %d kb %d | total %.0f (max %lld) | epi-fence %.0f | "
+            "mma wait-full %.0f epi-sts %.0f | %.0f MHz | epi busy %.0f (tmem %.0f, stg-wait %.0f)  (cycles, mean/CTA)\n",
+            p.dw3d, WM, MODE, CG, p.units, p.k_blocks, acc[5] / n, mx, acc[0] / n, acc[1] / nl, acc[2] / nl, acc[5] / (acc[3] > 0 ? acc[3] : 1) * 1e3,
             acc[4] / n, acc[6] / n, acc[7] / n);
   }
   return ROAST_OK;
@@ -798,7 +846,7 @@ roast_status_t sm100_dw(Ctx* c, const Module& m, const void* X, const void* dY, 
   for (int w = 1; w <= (cg == 2 ? 2 : 1); ++w) {
     if (ewm && atoi(ewm) != w) continue;
     const int tiles_w = ((p.M + BM * cg * w - 1) / (BM * cg * w)) * p.n_tiles;
-    const double eff = w == 2 ? 0.78 : 0.58;
+    const double eff = w == 2 ? 0.95 : 0.9;   // measured MMA-busy share with 3-D operand boxes
     for (int sp = 1; sp <= std::min(p.k_blocks, 16); ++sp) {
       const double cost = double((tiles_w * sp + slots - 1) / slots) * w / (eff * sp);
       if (cost < best - 1e-9) {
@@ -810,6 +858,16 @@ roast_status_t sm100_dw(Ctx* c, const Module& m, const void* X, const void* dY, 
   }
   p.m_tiles = (p.M + BM * cg * wm - 1) / (BM * cg * wm);
   const int tiles = p.m_tiles * p.n_tiles;
+  // one 3-D box per operand per stage (falls back to 64x64 2-D boxes if the driver rejects the view)
+  if (!getenv("ROAST_DW2D")) {
+    CUtensorMap a3, b3;
+    if (make_map_blocks(&a3, X, uint64_t(m.H), uint64_t(T), BK, 2 * wm) == ROAST_OK &&
+        make_map_blocks(&b3, dY, uint64_t(m.O), uint64_t(T), BK, 4 / cg) == ROAST_OK) {
+      a = a3;
+      b = b3;
+      p.dw3d = 1;
+    }
+  }
   p.kb_per_split = (p.k_blocks + splits - 1) / splits;
   splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;   // no empty splits
   p.splits = splits;
@@ -823,18 +881,19 @@ roast_status_t sm100_dw(Ctx* c, const Module& m, const void* X, const void* dY, 
   }
   // dM viewed as 8 [rows x 64] fp32 tensors, one per 32-byte phase (tile offsets are multiples of A = 8)
   CUtensorMap o;
-  WMaps dmaps;
+  WMaps& dmaps = *reinterpret_cast<WMaps*>(c->tmap_dm);
   memset(&o, 0, sizeof(o));
   if (det) {
     const uint64_t rows = uint64_t(splits) * p.ntiles * 64;
     st = make_map_2d(&o, c->ws, 64, rows, 256, 32, 32, true);
     if (st) return st;
-  } else {
+  } else if (c->tmap_dm_for != c->dM) {   // cached until dM is rebound
     for (int r = 0; r < 8; ++r) {
       const int64_t elems = c->mem_size - 8 * r;
       st = make_map_2d(&dmaps.m[r], c->dM + 8 * r, 64, uint64_t(elems / 64), 256, 32, 32, true);
       if (st) return st;
     }
+    c->tmap_dm_for = c->dM;
   }
   st = launch<DW>(a, b, o, dmaps, p, wm, s);
   if (st) return st;

@@ -61,6 +61,9 @@ struct Ctx {
   // tcgen05 path: cached TMA descriptors of the shadow (rebuilt on bind)
   alignas(64) unsigned char tmap_shadow[1024];
   bool tmap_shadow_valid = false;
+  // ... and of dM (8 fp32 phase views for the TMA reduce-add epilogue), valid for dM == tmap_dm_for
+  alignas(64) unsigned char tmap_dm[1024];
+  const float* tmap_dm_for = nullptr;
 };
 
 // error reporting (thread-local detail string)
