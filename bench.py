@@ -49,6 +49,19 @@ def load_peaks():
     return 1590.0, 1400.0, 6650.0, "fallback"
 
 
+def ncu_traffic(kind):
+    """DRAM bytes (read + write) per launch of `kind` from the newest committed ncu --set full
+    capture summary (profiles/round*/traffic.json, written by tools/traffic_from_ncu.py), else None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "round*", "traffic.json")))
+    if not files:
+        return None
+    try:
+        return json.load(open(files[-1])).get(kind)
+    except Exception:
+        return None
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -413,7 +426,7 @@ def run_gpu(args):
                     streams=args.streams, cuda_graph=bool(args.graph),
                     parallelism=f"dp{world}"),
         roofline=dict(bound="tensor", kernel=dom, achieved=achieved, peak=burst, unit="TFLOP/s",
-                      frac=achieved / burst, traffic=None,
+                      frac=achieved / burst, traffic=ncu_traffic(dom),
                       note=f"peak = {src} bf16 burst (MEASURED_PEAKS.json); algorithmic 2*T*H*O = "
                            f"{gemm_flop/1e9:.2f} GFLOP per launch / mean CUDA-event duration",
                       per_kind_ms=kind_ms, sustained_peak=sustained),
