@@ -12,7 +12,7 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libroast.so")
+LIB_PATH = os.environ.get("ROAST_LIB", os.path.join(_PKG, "libroast.so"))   # override: A/B experiments
 
 OK, ERR_CONFIG, ERR_GEOMETRY, ERR_SHAPE, ERR_BOUNDS, ERR_CAPACITY, ERR_STATE, ERR_CUDA, ERR_NCCL, \
     ERR_UNSUPPORTED = range(10)
