@@ -131,10 +131,6 @@ roast_status_t roast_destroy(roast_t h) {
   cudaFree(c->shadow);
   cudaFree(c->d_err);
   cudaFree(c->ws);
-  for (int k = 0; k < 2; ++k) {
-    cudaFree(c->sk_scratch[k]);
-    cudaFree(c->sk_cnt[k]);
-  }
   comm_destroy(c);
   delete c;
   return ROAST_OK;

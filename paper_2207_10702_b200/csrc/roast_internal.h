@@ -63,13 +63,7 @@ struct Ctx {
   bool tmap_shadow_valid = false;
   // ... and of dM (8 fp32 phase views for the TMA reduce-add epilogue), valid for dM == tmap_dm_for
   alignas(64) unsigned char tmap_dm[1024];
-  const float* tmap_dm_for = nullptr;
-  // stream-K partial accumulators + arrival counters, one set per GEMM kind (FWD, DX)
-  float* sk_scratch[2] = {nullptr, nullptr};
-  size_t sk_scratch_bytes[2] = {0, 0};
-  int* sk_cnt[2] = {nullptr, nullptr};
-  size_t sk_cnt_n[2] = {0, 0};
-};
+  const float* tmap_dm_for = nullptr;};
 
 // error reporting (thread-local detail string)
 roast_status_t fail(roast_status_t st, const std::string& msg);
