@@ -1,0 +1,72 @@
+"""End-to-end composition check (GPU): a BERT encoder layer whose six linears are ROAST
+linears in one GMS store, trained through torch autograd + the C ABI, against the same
+model in fp32 torch autograd with the recovered weights materialised densely.
+
+The reference dM is the paper's gradient rule applied to the dense model's weight
+gradients: dM[slot] = sum over (i, j) mapped to slot of lambda * g * dL/dW[i, j]
+(R12), scattered by the oracle (oracle/roast_mm.py).  Activations are bf16 on
+the ROAST side (fp32 in the reference), so the tolerance is a composition bound (3e-2),
+not the per-operation 1e-2 of the parity tests.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import roast_mm as OM
+
+pytestmark = pytest.mark.gpu
+
+
+def test_encoder_layer_gradients_match_dense_autograd():
+    import torch
+    from paper_2207_10702_b200 import nn as RN, roast as R
+    torch.manual_seed(0)
+    d, ff, heads, B, S = 256, 512, 4, 2, 128
+    n = 4 * d * d + 2 * d * ff
+    mem = synth.compressed_size(n, 8)
+    M_np = synth.uniform(synth.SEED_M, (mem,)).astype(np.float32)
+    M = torch.tensor(M_np, device="cuda")
+    store = R.Roast(M, 64, 64, seed=synth.HASH_SEED)
+    layer = RN.EncoderLayer(store, d, ff, heads).cuda()
+    for m in layer.modules():
+        if isinstance(m, torch.nn.LayerNorm):
+            m.to(torch.bfloat16)
+    x = torch.randn(B, S, d, device="cuda").to(torch.bfloat16)
+    Rw = torch.randn(B, S, d, device="cuda")       # L = <R, y>: not invariant under the final LayerNorm
+    store.zero_grad()
+    y = layer(x)
+    loss = (y.float() * Rw).sum()
+    loss.backward()
+    torch.cuda.synchronize()
+    dM = store.dM.cpu().numpy().astype(np.float64)
+
+    # dense fp32 reference with W = lambda * g * bf16(M) (the tensor-core operand, R18)
+    lins = [layer.q, layer.k, layer.v, layer.o, layer.ff1, layer.ff2]
+    W = [torch.nn.Parameter(store.materialize(l.mid, torch.bfloat16).float() * store_lam(l, M_np))
+         for l in lins]
+    xr = x.float()
+
+    def lin(t, i):
+        return t @ W[i]
+
+    def split(t):
+        return t.reshape(B, S, heads, d // heads).transpose(1, 2)
+    a = torch.nn.functional.scaled_dot_product_attention(split(lin(xr, 0)), split(lin(xr, 1)), split(lin(xr, 2)))
+    a = a.transpose(1, 2).reshape(B, S, d)
+    h1 = torch.nn.functional.layer_norm(xr + lin(a, 3), (d,))
+    yr = torch.nn.functional.layer_norm(h1 + lin(torch.nn.functional.gelu(lin(h1, 4)), 5), (d,))
+    lr = (yr * Rw).sum()
+    lr.backward()
+    assert abs(float(loss) - float(lr)) <= 2e-2 * float((yr.abs() * Rw.abs()).sum())
+    dM_ref = np.zeros(mem)
+    for l, w in zip(lins, W):
+        _, H, O = store.dims[l.mid]
+        spec = OM.LinearSpec(H, O, 64, 64, mem, synth.HASH_SEED, l.mid)
+        spec.scatter(w.grad.double().cpu().numpy(), dM_ref)
+    err = np.linalg.norm(dM - dM_ref) / np.linalg.norm(dM_ref)
+    assert err < 3e-2, err
+
+
+def store_lam(lin, M_np):
+    _, H, O = lin.store.dims[lin.mid]
+    return OM.LinearSpec(H, O, 64, 64, len(M_np), synth.HASH_SEED, lin.mid).lam

@@ -1,0 +1,124 @@
+"""C3 (BASELINE.json configs[2]): full BERT-base-shaped encoder training step, all 72 linears
+(12 layers x Q, K, V, O, FFN1, FFN2) ROAST-hashed into ONE global M at 100x
+(|M| = 849 352 fp32), data parallel: per-GPU batch 64 x 128 tokens, dM all-reduced with
+NCCL inside libroast, SGD on M + bf16 shadow refresh fused in one kernel.
+
+    python tools/bert_step.py [--steps 10] [--dense]          (1 GPU)
+    torchrun --nproc-per-node N tools/bert_step.py             (N GPUs, weak scaling)
+
+Reports tokens/s, ms per step and the linears' effective TFLOP/s (6 T n_linear_params per
+step); --dense runs the same model with dense bf16 nn.Linear weights for comparison.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+from paper_2207_10702_b200 import dp, nn as RN, roast as R  # noqa: E402
+
+D, FF, HEADS, LAYERS = 768, 3072, 12, 12
+N_LIN = LAYERS * (4 * D * D + 2 * D * FF)   # 84 934 656 ("~85M MM params")
+
+
+class DenseLayer(torch.nn.Module):
+    def __init__(self):
+        super().__init__()
+        L = lambda i, o: torch.nn.Linear(i, o, bias=False, dtype=torch.bfloat16)  # noqa: E731
+        self.q, self.k, self.v, self.o, self.ff1, self.ff2 = L(D, D), L(D, D), L(D, D), L(D, D), L(D, FF), L(FF, D)
+        self.ln1 = torch.nn.LayerNorm(D, dtype=torch.bfloat16)
+        self.ln2 = torch.nn.LayerNorm(D, dtype=torch.bfloat16)
+
+    forward = RN.EncoderLayer.forward
+    heads = HEADS
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--seq", type=int, default=128)
+    ap.add_argument("--ratio", type=float, default=100)
+    ap.add_argument("--dense", action="store_true")
+    args = ap.parse_args()
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    torch.manual_seed(1234 + rank)
+    B, S = args.batch, args.seq
+    T = B * S
+    x = torch.randn(B, S, D, device=dev, dtype=torch.bfloat16)
+    proj = torch.randn(B, S, D, device=dev, dtype=torch.bfloat16)   # L = <proj, y> / T
+    if args.dense:
+        model = torch.nn.Sequential(*[DenseLayer() for _ in range(LAYERS)]).to(dev)
+        opt = torch.optim.SGD(model.parameters(), lr=1e-4)
+        store = None
+    else:
+        mem = synth.compressed_size(N_LIN, args.ratio)
+        M = (torch.rand(mem, device=dev) * 2 - 1).contiguous()
+        store = R.Roast(M, 64, 64, seed=synth.HASH_SEED)
+        dp.init_comm(store, rank, world, device=dev)
+        model = torch.nn.Sequential(*[RN.EncoderLayer(store, D, FF, HEADS) for _ in range(LAYERS)]).to(dev)
+        for m in model.modules():
+            if isinstance(m, torch.nn.LayerNorm):
+                m.to(torch.bfloat16)
+
+    def step():
+        y = model(x)
+        loss = (y * proj).float().sum() / T
+        if store is None:
+            opt.zero_grad(set_to_none=True)
+            loss.backward()
+            if world > 1:
+                import torch.distributed as dist
+                for p in model.parameters():
+                    dist.all_reduce(p.grad)
+            opt.step()
+        else:
+            store.zero_grad()
+            loss.backward()
+            store.allreduce()              # a6: one ncclAllReduce of dM (|M| fp32) per step
+            store.sgd(1e-4)                # M -= lr dM; shadow refresh (same kernel)
+        return loss
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        loss = step()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        print(json.dumps(dict(config="C3 BERT-base encoder step, 72 linears in one GMS M",
+                              impl="dense-torch" if args.dense else "roast", ratio=args.ratio,
+                              mem_size=None if store is None else store.mem_size, n_gpus=world,
+                              tokens_per_gpu=T, ms_per_step=ms, tokens_per_s=world * T / (ms * 1e-3),
+                              linear_eff_tflops=world * 6.0 * T * N_LIN / (ms * 1e-3) / 1e12,
+                              loss=float(loss.detach()))))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
