@@ -379,6 +379,7 @@ roast_status_t roast_embedding_bwd(roast_t h, int32_t id, const int64_t* idx, in
   if (n < 0) return fail(ROAST_ERR_SHAPE, "n < 0");
   if (n > 0 && (!idx || !dOut)) return fail(ROAST_ERR_CONFIG, "null idx / dOut");
   if (reinterpret_cast<uintptr_t>(dOut) & 15) return fail(ROAST_ERR_CONFIG, "dOut must be 16-byte aligned");
+  if (c->cfg.deterministic) return embed_bwd_deterministic(c, *m, idx, n, dOut, reinterpret_cast<cudaStream_t>(stream));
   ROAST_CUDA_CHECK(launch_embed_bwd(c, *m, idx, n, dOut, reinterpret_cast<cudaStream_t>(stream)));
   c->launches++;
   return ROAST_OK;
