@@ -158,6 +158,24 @@ roast_status_t roast_sync_shadow(roast_t h, roast_stream_t stream);
 /* (a7, minimal) M <- M - lr * dM, then shadow refresh.  Fused elementwise kernel. */
 roast_status_t roast_sgd_step(roast_t h, float lr, roast_stream_t stream);
 
+/* NEXT #1: the update after the exchange, fused into ONE elementwise pass
+ * over |M| (`tab:total-opt` P:749-813: optimizer cost scales with |M|, not with
+ * the virtual model): read M, dM and the optimizer state, write M, the bf16 shadow
+ * [+bf16(M) | -bf16(M)], the state, and (zero_grad != 0) dM <- 0.  State (fp32, |M|
+ * elements each) is owned by the handle and allocated on first use.  Formulas are
+ * PyTorch's (the paper's optimizers): with g = dM + weight_decay * M,
+ *   SGD      M -= lr g
+ *   ADAGRAD  G += g^2;                      M -= lr g / (sqrt(G) + eps)
+ *   ADAM     m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
+ *            M -= lr (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)     (t = step >= 1). */
+typedef enum { ROAST_OPT_SGD = 0, ROAST_OPT_ADAGRAD = 1, ROAST_OPT_ADAM = 2 } roast_opt_kind_t;
+typedef struct {
+  int32_t kind;        /* roast_opt_kind_t */
+  float lr, beta1, beta2, eps, weight_decay;
+  int32_t zero_grad;   /* 1: dM <- 0 in the same pass */
+} roast_opt_config_t;
+roast_status_t roast_optimizer_step(roast_t h, const roast_opt_config_t* cfg, int64_t step, roast_stream_t stream);
+
 /* Sticky device-side error (synchronises the handle's bound stream is NOT done:
  * call after a stream synchronize to observe faults of completed work). */
 roast_status_t roast_get_error(roast_t h);

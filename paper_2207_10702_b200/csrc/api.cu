@@ -131,6 +131,8 @@ roast_status_t roast_destroy(roast_t h) {
   cudaFree(c->shadow);
   cudaFree(c->d_err);
   cudaFree(c->ws);
+  cudaFree(c->opt_s1);
+  cudaFree(c->opt_s2);
   comm_destroy(c);
   delete c;
   return ROAST_OK;
@@ -404,6 +406,27 @@ roast_status_t roast_sgd_step(roast_t h, float lr, roast_stream_t stream) {
   Ctx* c = ctx(h);
   if (!c || !c->M || !c->shadow) return fail(ROAST_ERR_STATE, "not bound");
   ROAST_CUDA_CHECK(launch_sgd(c, lr, reinterpret_cast<cudaStream_t>(stream)));
+  c->launches++;
+  return ROAST_OK;
+}
+
+roast_status_t roast_optimizer_step(roast_t h, const roast_opt_config_t* cfg, int64_t step, roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  if (!c || !c->M || !c->shadow) return fail(ROAST_ERR_STATE, "not bound");
+  if (!cfg || cfg->kind < ROAST_OPT_SGD || cfg->kind > ROAST_OPT_ADAM) return fail(ROAST_ERR_CONFIG, "bad optimizer");
+  if (cfg->kind == ROAST_OPT_ADAM && step < 1) return fail(ROAST_ERR_CONFIG, "Adam step must be >= 1");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t bytes = size_t(c->mem_size) * sizeof(float);
+  if (cfg->kind >= ROAST_OPT_ADAGRAD && !c->opt_s1) {
+    ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->opt_s1), bytes));
+    ROAST_CUDA_CHECK(cudaMemsetAsync(c->opt_s1, 0, bytes, s));
+  }
+  if (cfg->kind == ROAST_OPT_ADAM && !c->opt_s2) {
+    ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->opt_s2), bytes));
+    ROAST_CUDA_CHECK(cudaMemsetAsync(c->opt_s2, 0, bytes, s));
+  }
+  ROAST_CUDA_CHECK(launch_optimizer(c, cfg->kind, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay, step,
+                                    cfg->zero_grad, s));
   c->launches++;
   return ROAST_OK;
 }

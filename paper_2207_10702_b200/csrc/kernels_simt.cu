@@ -325,3 +325,58 @@ cudaError_t launch_materialize(const Ctx* c, const Module& m, roast_dtype_t dt, 
 }
 
 }  // namespace roast
+
+namespace roast {
+namespace {
+
+// One pass over |M|: update M from dM (and the optimizer state), refresh both halves of the
+// bf16 shadow, optionally zero dM.  kind: 0 SGD, 1 Adagrad, 2 Adam (PyTorch formulas).
+template <int KIND>
+__global__ void opt_kernel(float* __restrict__ M, float* __restrict__ dM, __nv_bfloat16* __restrict__ sh,
+                           float* __restrict__ s1, float* __restrict__ s2, int64_t n, int64_t neg_base, float lr,
+                           float b1, float b2, float eps, float wd, float bc1, float bc2, int zero) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    float w = M[i];
+    const float g = dM[i] + wd * w;
+    if (KIND == 0) {
+      w -= lr * g;
+    } else if (KIND == 1) {
+      const float G = s1[i] + g * g;
+      s1[i] = G;
+      w -= lr * g / (sqrtf(G) + eps);
+    } else {
+      const float m = b1 * s1[i] + (1.f - b1) * g;
+      const float v = b2 * s2[i] + (1.f - b2) * g * g;
+      s1[i] = m;
+      s2[i] = v;
+      w -= lr * (m / bc1) / (sqrtf(v / bc2) + eps);
+    }
+    M[i] = w;
+    const __nv_bfloat16 b = __float2bfloat16_rn(w);
+    sh[i] = b;
+    sh[neg_base + i] = __hneg(b);
+    if (zero) dM[i] = 0.f;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_optimizer(Ctx* c, int kind, float lr, float b1, float b2, float eps, float wd, int64_t step,
+                             int zero, cudaStream_t s) {
+  const float bc1 = kind == 2 ? float(1.0 - pow(double(b1), double(step))) : 1.f;
+  const float bc2 = kind == 2 ? float(1.0 - pow(double(b2), double(step))) : 1.f;
+  auto* sh = reinterpret_cast<__nv_bfloat16*>(c->shadow);
+  const int grid = grid_1d(c->mem_size, 256);
+  if (kind == 0)
+    opt_kernel<0><<<grid, 256, 0, s>>>(c->M, c->dM, sh, nullptr, nullptr, c->mem_size, c->neg_base, lr, b1, b2, eps,
+                                       wd, bc1, bc2, zero);
+  else if (kind == 1)
+    opt_kernel<1><<<grid, 256, 0, s>>>(c->M, c->dM, sh, c->opt_s1, nullptr, c->mem_size, c->neg_base, lr, b1, b2,
+                                       eps, wd, bc1, bc2, zero);
+  else
+    opt_kernel<2><<<grid, 256, 0, s>>>(c->M, c->dM, sh, c->opt_s1, c->opt_s2, c->mem_size, c->neg_base, lr, b1, b2,
+                                       eps, wd, bc1, bc2, zero);
+  return cudaGetLastError();
+}
+
+}  // namespace roast

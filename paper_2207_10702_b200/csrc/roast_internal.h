@@ -63,7 +63,10 @@ struct Ctx {
   bool tmap_shadow_valid = false;
   // ... and of dM (8 fp32 phase views for the TMA reduce-add epilogue), valid for dM == tmap_dm_for
   alignas(64) unsigned char tmap_dm[1024];
-  const float* tmap_dm_for = nullptr;};
+  const float* tmap_dm_for = nullptr;
+  // optimizer state, |M| fp32 each (Adagrad: s1 = G; Adam: s1 = m, s2 = v)
+  float* opt_s1 = nullptr;
+  float* opt_s2 = nullptr;};
 
 // error reporting (thread-local detail string)
 roast_status_t fail(roast_status_t st, const std::string& msg);
@@ -88,6 +91,8 @@ cudaError_t launch_simt_dw(const Ctx* c, const Module& m, const void* X, const v
 cudaError_t launch_det_reduce(const Ctx* c, const Module& m, const float* ws, int nsplit, cudaStream_t s);
 cudaError_t launch_sync_shadow(Ctx* c, cudaStream_t s);
 cudaError_t launch_sgd(Ctx* c, float lr, cudaStream_t s);
+cudaError_t launch_optimizer(Ctx* c, int kind, float lr, float b1, float b2, float eps, float wd, int64_t step,
+                             int zero, cudaStream_t s);
 cudaError_t launch_materialize(const Ctx* c, const Module& m, roast_dtype_t dt, void* W, cudaStream_t s);
 cudaError_t launch_embed_fwd(const Ctx* c, const Module& m, const int64_t* idx, int64_t n, float* out,
                              cudaStream_t s);

@@ -24,7 +24,8 @@ EXPORTS = [
     "roast_config_default", "roast_create", "roast_create_ex", "roast_destroy", "roast_bind",
     "roast_register_linear", "roast_register_embedding", "roast_linear_fwd", "roast_linear_bwd",
     "roast_linear_bwd_dx", "roast_linear_bwd_dm", "roast_embedding_fwd", "roast_embedding_bwd", "roast_comm_unique_id", "roast_comm_init",
-    "roast_grad_allreduce", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_get_error",
+    "roast_grad_allreduce", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step",
+    "roast_get_error",
     "roast_status_str", "roast_last_error", "roast_debug_tile_map", "roast_debug_chunk_map",
     "roast_debug_materialize", "roast_debug_hash_host", "roast_launch_count",
 ]
@@ -37,6 +38,15 @@ class roast_tile_t(ctypes.Structure):
 class roast_config_t(ctypes.Structure):
     _fields_ = [("C", ctypes.c_double), ("align_elems", ctypes.c_int32), ("tile_layout", ctypes.c_int32),
                 ("mapping", ctypes.c_int32), ("use_sign", ctypes.c_int32), ("deterministic", ctypes.c_int32)]
+
+
+class roast_opt_config_t(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("lr", ctypes.c_float), ("beta1", ctypes.c_float),
+                ("beta2", ctypes.c_float), ("eps", ctypes.c_float), ("weight_decay", ctypes.c_float),
+                ("zero_grad", ctypes.c_int32)]
+
+
+OPT_SGD, OPT_ADAGRAD, OPT_ADAM = 0, 1, 2
 
 
 class RoastError(RuntimeError):
@@ -74,6 +84,7 @@ def _load():
         "roast_zero_grad": (st, [H, S]),
         "roast_sync_shadow": (st, [H, S]),
         "roast_sgd_step": (st, [H, ctypes.c_float, S]),
+        "roast_optimizer_step": (st, [H, ctypes.POINTER(roast_opt_config_t), I64, S]),
         "roast_get_error": (st, [H]),
         "roast_status_str": (ctypes.c_char_p, [st]),
         "roast_last_error": (ctypes.c_char_p, []),
@@ -184,6 +195,12 @@ def roast_sync_shadow(h, stream=0):
 
 def roast_sgd_step(h, lr, stream=0):
     _check(_lib.roast_sgd_step(h, lr, stream), "roast_sgd_step")
+
+
+def roast_optimizer_step(h, kind, lr, step=1, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, zero_grad=True,
+                         stream=0):
+    cfg = roast_opt_config_t(kind, lr, beta1, beta2, eps, weight_decay, int(zero_grad))
+    _check(_lib.roast_optimizer_step(h, ctypes.byref(cfg), step, stream), "roast_optimizer_step")
 
 
 def roast_get_error(h):
@@ -315,6 +332,9 @@ class Roast:
 
     def sgd(self, lr, stream=None):
         roast_sgd_step(self.h, lr, self._s(stream))
+
+    def optimizer_step(self, kind, lr, step=1, stream=None, **kw):
+        roast_optimizer_step(self.h, kind, lr, step, stream=self._s(stream), **kw)
 
     def allreduce(self, stream=None):
         roast_grad_allreduce(self.h, self._s(stream))

@@ -269,3 +269,29 @@ def test_embedding_deterministic_parity_and_reproducible(R, torch, dist, align):
         OE.EmbeddingSpec(rows, d, Z, mem, HS, mid, align=align).backward(idx_np, dout_np, ref)
     assert rel_frob(outs[0].cpu().numpy(), ref) <= 1e-5
     ctx.check()
+
+
+@pytest.mark.parametrize("kind,name", [(0, "sgd"), (1, "adagrad"), (2, "adam")])
+def test_optimizer_step_parity(R, torch, kind, name):
+    """NEXT #1: fused update of M + state + bf16 shadow (+ dM zeroing) vs the oracle formulas."""
+    from oracle import optim as OO
+    mem = 100_003 - 3
+    M_np = store(mem)
+    ctx, M = make_ctx(R, torch, M_np, 64, 64)
+    mid = ctx.linear(128, 128)
+    g1 = synth.normal(synth.SEED_DY, (mem,)).astype(np.float32)
+    g2 = synth.normal(synth.SEED_DY + 1, (mem,)).astype(np.float32)
+    ref_M, st = M_np.astype(np.float64), {}
+    for t, g in [(1, g1), (2, g2)]:
+        ctx.dM.copy_(to_dev(g, torch.float32))
+        ctx.optimizer_step(kind, 1e-2, step=t, weight_decay=0.01)
+        torch.cuda.synchronize()
+        ref_M, st = OO.step(name, ref_M.astype(np.float32).astype(np.float64), g, st, lr=1e-2, t=t, wd=0.01)
+        got = ctx.M.cpu().numpy()
+        assert np.max(np.abs(got - ref_M)) <= 1e-5 * max(1.0, np.max(np.abs(ref_M)))
+        assert torch.count_nonzero(ctx.dM).item() == 0          # zero_grad fused
+        ref_M = got.astype(np.float64)                           # continue from the device state
+    # the shadow follows M bit-exactly: operand tile == g * bf16(M)
+    spec = OM.LinearSpec(128, 128, 64, 64, mem, HS, mid)
+    Wbf = ctx.materialize(mid, torch.bfloat16).float().cpu().numpy()
+    assert np.array_equal(Wbf.astype(np.float64), spec.materialize(ctx.M.cpu().numpy(), "operand"))
