@@ -96,8 +96,9 @@ roast_status_t roast_create_ex(roast_t* out, int64_t mem_size, uint64_t seed, ro
     roast_config_default(&cfg);
   if (mem_size <= 0) return fail(ROAST_ERR_CONFIG, "mem_size must be > 0");
   if (!(cfg.C > 0)) return fail(ROAST_ERR_CONFIG, "C must be > 0");
-  if (cfg.align_elems <= 0 || cfg.align_elems % 4 != 0)
-    return fail(ROAST_ERR_CONFIG, "align_elems must be a positive multiple of 4");
+  // A = 1 is legal (HashedNet-style 1x1 tiles on the SIMT path); embeddings need A % 4 == 0
+  // and the tcgen05 path A % 8 == 0 (16-byte TMA offsets); both are checked where they apply.
+  if (cfg.align_elems <= 0) return fail(ROAST_ERR_CONFIG, "align_elems must be positive");
   if (cfg.tile_layout != ROAST_ROW_MAJOR && cfg.tile_layout != ROAST_SW128)
     return fail(ROAST_ERR_CONFIG, "bad tile_layout");
   if (cfg.mapping != ROAST_MAP_HASH && cfg.mapping != ROAST_MAP_IDENTITY) return fail(ROAST_ERR_CONFIG, "bad mapping");
@@ -168,6 +169,8 @@ roast_status_t roast_register_linear(roast_t h, int64_t H, int64_t O, int32_t* i
   if (T > c->mem_size) return fail(ROAST_ERR_GEOMETRY, "tile Z1*Z2 larger than |M| (S:51)");
   if (H % z1 || O % z2) return fail(ROAST_ERR_GEOMETRY, "in % Z1 and out % Z2 must be 0 on the GPU path (R9)");
   if (T % A) return fail(ROAST_ERR_GEOMETRY, "Z1*Z2 must be a multiple of align_elems");
+  if (c->cfg.deterministic && A % 4)
+    return fail(ROAST_ERR_GEOMETRY, "deterministic dM needs align_elems % 4 == 0 (4-slot reduce groups)");
   if (H / z1 >= (int64_t(1) << 28) || O / z2 >= (int64_t(1) << 31)) return fail(ROAST_ERR_GEOMETRY, "too many tiles");
   Module m;
   m.kind = kLinear;
@@ -247,7 +250,8 @@ roast_status_t roast_register_embedding(roast_t h, int64_t num_rows, int32_t dim
   if (num_rows <= 0 || dim <= 0 || chunk <= 0) return fail(ROAST_ERR_SHAPE, "rows, dim, chunk must be > 0");
   const int64_t A = c->cfg.align_elems;
   if (chunk > c->mem_size) return fail(ROAST_ERR_GEOMETRY, "chunk larger than |M|");
-  if (chunk % A || chunk % 4 || dim % 4) return fail(ROAST_ERR_GEOMETRY, "chunk % A, chunk % 4 and dim % 4 must be 0");
+  if (chunk % A || chunk % 4 || dim % 4 || A % 4)
+    return fail(ROAST_ERR_GEOMETRY, "chunk % A, chunk % 4, dim % 4 and A % 4 must be 0 (16-byte vector access)");
   Module m;
   m.kind = kEmbedding;
   m.rows = num_rows;

@@ -295,3 +295,29 @@ def test_optimizer_step_parity(R, torch, kind, name):
     spec = OM.LinearSpec(128, 128, 64, 64, mem, HS, mid)
     Wbf = ctx.materialize(mid, torch.bfloat16).float().cpu().numpy()
     assert np.array_equal(Wbf.astype(np.float64), spec.materialize(ctx.M.cpu().numpy(), "operand"))
+
+
+@pytest.mark.parametrize("dtype_name", ["fp32", "bf16"])
+def test_hashednet_per_element_mapping(R, torch, dtype_name):
+    """NEXT #2: HashedNet = ROAST-MM with 1x1 tiles and A = 1: every weight
+    hashed independently.  Same oracle, same kernels (SIMT gather path)."""
+    H, O, T, mem = 192, 256, 96, 4099
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 1, 1, align=1)
+    mid = ctx.linear(H, O)
+    spec = OM.LinearSpec(H, O, 1, 1, mem, HS, mid, align=1)
+    off, sgn = ctx.tile_map(mid)
+    assert np.array_equal(off, spec.off) and np.array_equal(sgn.astype(np.int64), spec.sgn)
+    if dtype_name == "fp32":
+        X = synth.uniform(synth.SEED_X, (T, H)).astype(np.float32)
+        dY = synth.uniform(synth.SEED_DY, (T, O)).astype(np.float32)
+        Y, dX, dM = run_linear(R, torch, ctx, mid, X, dY, torch.float32)
+        tol, bf = 1e-5, False
+    else:
+        X = bf16_input(synth.SEED_X, (T, H))
+        dY = bf16_input(synth.SEED_DY, (T, O))
+        Y, dX, dM = run_linear(R, torch, ctx, mid, X, dY, torch.bfloat16)
+        tol, bf = 1e-2, True
+    assert rel_frob(Y, spec.forward(X, M_np, bf)) <= tol
+    assert rel_frob(dX, spec.backward_dx(dY, M_np, bf)) <= tol
+    assert rel_frob(dM, spec.backward_dm(X, dY)) <= tol
