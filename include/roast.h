@@ -145,7 +145,8 @@ roast_status_t roast_embedding_bwd(roast_t h, int32_t id, const int64_t* d_idx, 
 /* a6: data-parallel exchange.  Rank 0 calls roast_comm_unique_id; the caller
  * broadcasts the 128 bytes (e.g. torch.distributed); every rank calls
  * roast_comm_init.  roast_grad_allreduce sums dM over ranks in place
- * (ncclAllReduce, fp32 sum) on `stream`; with world == 1 it is a no-op.
+ * (ncclAllReduce, fp32 sum) on `stream`.  world == 1 with id == NULL creates no communicator
+ * and the exchange is a no-op; world == 1 with an id builds a 1-rank NCCL communicator.
  * libnccl.so.2 is loaded at run time (ROAST_ERR_NCCL if absent). */
 roast_status_t roast_comm_unique_id(uint8_t id_out[128]);
 roast_status_t roast_comm_init(roast_t h, int32_t rank, int32_t world, const uint8_t id[128]);

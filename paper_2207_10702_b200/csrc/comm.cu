@@ -75,7 +75,7 @@ roast_status_t roast_comm_init(roast_t h, int32_t rank, int32_t world, const uin
   comm_destroy(c);
   c->rank = rank;
   c->world = world;
-  if (world == 1) return ROAST_OK;
+  if (world == 1 && !id) return ROAST_OK;   // single rank, no communicator (exchange is a no-op)
   if (!id) return fail(ROAST_ERR_CONFIG, "null id");
   if (!api().loaded) return fail(ROAST_ERR_NCCL, "libnccl.so.2 not found");
   ncclUniqueId uid;
@@ -90,8 +90,10 @@ roast_status_t roast_comm_init(roast_t h, int32_t rank, int32_t world, const uin
 roast_status_t roast_grad_allreduce(roast_t h, roast_stream_t stream) {
   Ctx* c = reinterpret_cast<Ctx*>(h);
   if (!c || !c->dM) return fail(ROAST_ERR_STATE, "not bound");
-  if (c->world == 1) return ROAST_OK;
-  if (!c->nccl_comm) return fail(ROAST_ERR_STATE, "roast_comm_init has not been called");
+  if (!c->nccl_comm) {
+    if (c->world == 1) return ROAST_OK;
+    return fail(ROAST_ERR_STATE, "roast_comm_init has not been called");
+  }
   ncclResult_t r = api().AllReduce(c->dM, c->dM, size_t(c->mem_size), ncclFloat32, ncclSum,
                                    reinterpret_cast<ncclComm_t>(c->nccl_comm), reinterpret_cast<cudaStream_t>(stream));
   if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");

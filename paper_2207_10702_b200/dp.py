@@ -31,7 +31,9 @@ def broadcast_bytes(payload: bytes | None, rank: int, nbytes: int, group=None, d
 def init_comm(ctx, rank: int, world: int, group=None, device=None) -> None:
     """Create libroast's NCCL communicator for this process group (no-op at world 1)."""
     from . import roast as R
-    uid = R.roast_comm_unique_id() if (rank == 0 and world > 1) else bytes(128)
-    if world > 1:
-        uid = broadcast_bytes(uid, rank, 128, group=group, device=device)
+    if world == 1:
+        R.roast_comm_init(ctx.h, 0, 1, None)        # no communicator: the exchange is a no-op
+        return
+    uid = R.roast_comm_unique_id() if rank == 0 else bytes(128)
+    uid = broadcast_bytes(uid, rank, 128, group=group, device=device)
     R.roast_comm_init(ctx.h, rank, world, uid)

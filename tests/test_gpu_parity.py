@@ -321,3 +321,23 @@ def test_hashednet_per_element_mapping(R, torch, dtype_name):
     assert rel_frob(Y, spec.forward(X, M_np, bf)) <= tol
     assert rel_frob(dX, spec.backward_dx(dY, M_np, bf)) <= tol
     assert rel_frob(dM, spec.backward_dm(X, dY)) <= tol
+
+
+def test_nccl_allreduce_single_rank_and_graph_capture(R, torch):
+    """a6 through NCCL with a 1-rank communicator: dlopen, init, in-place fp32 sum (identity at
+    world 1), and capture of the exchange inside a CUDA graph as bench.py does."""
+    from paper_2207_10702_b200 import roast
+    mem = 47192
+    ctx, _ = make_ctx(R, torch, store(mem), 64, 64)
+    roast.roast_comm_init(ctx.h, 0, 1, roast.roast_comm_unique_id())
+    g = to_dev(synth.normal(3, (mem,)).astype(np.float32), torch.float32)
+    ctx.dM.copy_(g)
+    ctx.allreduce()
+    torch.cuda.synchronize()
+    assert torch.equal(ctx.dM, g)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        ctx.allreduce()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(ctx.dM, g)
