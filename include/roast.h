@@ -142,6 +142,19 @@ roast_status_t roast_embedding_fwd(roast_t h, int32_t id, const int64_t* d_idx, 
 roast_status_t roast_embedding_bwd(roast_t h, int32_t id, const int64_t* d_idx, int64_t n,
                                    const float* d_dOut, roast_stream_t stream);
 
+/* a4 / a5 over several tables in one launch (DLRM's 26 sparse features, C4):
+ * table t = ids[t] (host array of ntables embedding ids, all with the same dim and
+ * chunk; a table may repeat) looks up idx[t n + b]; batch rows are table-major, so
+ * d_idx is ntables x n int64, d_out / d_dOut are (ntables n) x dim fp32 and row
+ * t n + b equals roast_embedding_fwd(ids[t], idx[t n + b]) bit for bit.  Backward
+ * adds every table's gradient into dM (same result as ntables single calls,
+ * bitwise in deterministic mode).  Errors: CONFIG (null / unaligned pointers, ids
+ * of differing dim or chunk), BAD_ID, SHAPE. */
+roast_status_t roast_embedding_fwd_multi(roast_t h, const int32_t* ids, int32_t ntables, const int64_t* d_idx,
+                                         int64_t n, float* d_out, roast_stream_t stream);
+roast_status_t roast_embedding_bwd_multi(roast_t h, const int32_t* ids, int32_t ntables, const int64_t* d_idx,
+                                         int64_t n, const float* d_dOut, roast_stream_t stream);
+
 /* a6: data-parallel exchange.  Rank 0 calls roast_comm_unique_id; the caller
  * broadcasts the 128 bytes (e.g. torch.distributed); every rank calls
  * roast_comm_init.  roast_grad_allreduce sums dM over ranks in place

@@ -391,6 +391,54 @@ roast_status_t roast_embedding_bwd(roast_t h, int32_t id, const int64_t* idx, in
   return ROAST_OK;
 }
 
+static roast_status_t embedding_multi(roast_t h, const int32_t* ids, int32_t nt, const int64_t* idx, int64_t n,
+                                      float* out, const float* dOut, roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  if (!c) return fail(ROAST_ERR_STATE, "null handle");
+  if (nt < 0 || n < 0) return fail(ROAST_ERR_SHAPE, "ntables < 0 or n < 0");
+  if (nt == 0 || n == 0) return ROAST_OK;
+  if (!ids || !idx || (!out && !dOut)) return fail(ROAST_ERR_CONFIG, "null ids / idx / out");
+  const void* rows = out ? static_cast<const void*>(out) : static_cast<const void*>(dOut);
+  if (reinterpret_cast<uintptr_t>(rows) & 15) return fail(ROAST_ERR_CONFIG, "out / dOut must be 16-byte aligned");
+  std::vector<const Module*> mods(nt);
+  for (int t = 0; t < nt; ++t) {
+    Module* m;
+    roast_status_t st = get_module(c, ids[t], kEmbedding, &m);
+    if (st) return st;
+    if (t && (m->dim != mods[0]->dim || m->chunk != mods[0]->chunk))
+      return fail(ROAST_ERR_CONFIG, "multi-table call needs equal dim and chunk");
+    mods[t] = m;
+  }
+  const cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t dim = mods[0]->dim;
+  if (dOut && c->cfg.deterministic) {  // fixed order: table by table, each sorted (K7 det)
+    for (int t = 0; t < nt; ++t) {
+      roast_status_t st = embed_bwd_deterministic(c, *mods[t], idx + t * n, n, dOut + t * n * dim, s);
+      if (st) return st;
+    }
+    return ROAST_OK;
+  }
+  for (int t0 = 0; t0 < nt; t0 += kEmbMaxTables) {
+    const int k = std::min(nt - t0, kEmbMaxTables);
+    ROAST_CUDA_CHECK(launch_embed_multi(c, mods.data() + t0, k, idx + t0 * n, n, out ? out + t0 * n * dim : nullptr,
+                                        dOut ? dOut + t0 * n * dim : nullptr, s));
+    c->launches++;
+  }
+  return ROAST_OK;
+}
+
+roast_status_t roast_embedding_fwd_multi(roast_t h, const int32_t* ids, int32_t ntables, const int64_t* idx,
+                                         int64_t n, float* out, roast_stream_t stream) {
+  if (!out && ntables > 0 && n > 0) return fail(ROAST_ERR_CONFIG, "null out");
+  return embedding_multi(h, ids, ntables, idx, n, out, nullptr, stream);
+}
+
+roast_status_t roast_embedding_bwd_multi(roast_t h, const int32_t* ids, int32_t ntables, const int64_t* idx,
+                                         int64_t n, const float* dOut, roast_stream_t stream) {
+  if (!dOut && ntables > 0 && n > 0) return fail(ROAST_ERR_CONFIG, "null dOut");
+  return embedding_multi(h, ids, ntables, idx, n, nullptr, dOut, stream);
+}
+
 roast_status_t roast_zero_grad(roast_t h, roast_stream_t stream) {
   Ctx* c = ctx(h);
   if (!c || !c->dM) return fail(ROAST_ERR_STATE, "not bound");

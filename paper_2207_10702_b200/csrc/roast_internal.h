@@ -98,6 +98,11 @@ cudaError_t launch_embed_fwd(const Ctx* c, const Module& m, const int64_t* idx, 
                              cudaStream_t s);
 cudaError_t launch_embed_bwd(const Ctx* c, const Module& m, const int64_t* idx, int64_t n, const float* dOut,
                              cudaStream_t s);
+constexpr int kEmbMaxTables = 64;  // tables per fused launch (kernel-parameter budget)
+// nt <= kEmbMaxTables tables of equal dim / chunk; idx / out / dOut are table-major
+// (nt x n rows); dOut == nullptr selects the forward
+cudaError_t launch_embed_multi(const Ctx* c, const Module* const* mods, int nt, const int64_t* idx, int64_t n,
+                               float* out, const float* dOut, cudaStream_t s);
 cudaError_t launch_chunk_map(const Ctx* c, const Module& m, const int64_t* rows, int64_t n, int64_t* off,
                              int8_t* sgn, cudaStream_t s);
 

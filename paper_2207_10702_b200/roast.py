@@ -23,7 +23,8 @@ MAP_HASH, MAP_IDENTITY = 0, 1
 EXPORTS = [
     "roast_config_default", "roast_create", "roast_create_ex", "roast_destroy", "roast_bind",
     "roast_register_linear", "roast_register_embedding", "roast_linear_fwd", "roast_linear_bwd",
-    "roast_linear_bwd_dx", "roast_linear_bwd_dm", "roast_embedding_fwd", "roast_embedding_bwd", "roast_comm_unique_id", "roast_comm_init",
+    "roast_linear_bwd_dx", "roast_linear_bwd_dm", "roast_embedding_fwd", "roast_embedding_bwd",
+    "roast_embedding_fwd_multi", "roast_embedding_bwd_multi", "roast_comm_unique_id", "roast_comm_init",
     "roast_grad_allreduce", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step",
     "roast_get_error",
     "roast_status_str", "roast_last_error", "roast_debug_tile_map", "roast_debug_chunk_map",
@@ -78,6 +79,8 @@ def _load():
         "roast_linear_bwd_dm": (st, [H, I32, P, P, I64, ctypes.c_int, S]),
         "roast_embedding_fwd": (st, [H, I32, P, I64, P, S]),
         "roast_embedding_bwd": (st, [H, I32, P, I64, P, S]),
+        "roast_embedding_fwd_multi": (st, [H, ctypes.POINTER(I32), I32, P, I64, P, S]),
+        "roast_embedding_bwd_multi": (st, [H, ctypes.POINTER(I32), I32, P, I64, P, S]),
         "roast_comm_unique_id": (st, [ctypes.c_char_p]),
         "roast_comm_init": (st, [H, I32, I32, ctypes.c_char_p]),
         "roast_grad_allreduce": (st, [H, S]),
@@ -169,6 +172,20 @@ def roast_embedding_fwd(h, mid, idx_ptr, n, out_ptr, stream=0):
 
 def roast_embedding_bwd(h, mid, idx_ptr, n, dout_ptr, stream=0):
     _check(_lib.roast_embedding_bwd(h, mid, idx_ptr, n, dout_ptr, stream), "roast_embedding_bwd")
+
+
+def _ids(ids):
+    return (ctypes.c_int32 * len(ids))(*ids), len(ids)
+
+
+def roast_embedding_fwd_multi(h, ids, idx_ptr, n, out_ptr, stream=0):
+    arr, nt = _ids(ids)
+    _check(_lib.roast_embedding_fwd_multi(h, arr, nt, idx_ptr, n, out_ptr, stream), "roast_embedding_fwd_multi")
+
+
+def roast_embedding_bwd_multi(h, ids, idx_ptr, n, dout_ptr, stream=0):
+    arr, nt = _ids(ids)
+    _check(_lib.roast_embedding_bwd_multi(h, arr, nt, idx_ptr, n, dout_ptr, stream), "roast_embedding_bwd_multi")
 
 
 def roast_comm_unique_id() -> bytes:
@@ -323,6 +340,19 @@ class Roast:
 
     def emb_bwd(self, mid, idx, dout, stream=None):
         roast_embedding_bwd(self.h, mid, idx.data_ptr(), idx.numel(), dout.data_ptr(), self._s(stream))
+
+    def emb_fwd_multi(self, mids, idx, out=None, stream=None):
+        """idx: ntables x n (table-major); returns (ntables n) x dim."""
+        _, rows, dim, chunk = self.dims[mids[0]]
+        n = idx.numel() // len(mids)
+        if out is None:
+            out = self.torch.empty(idx.numel(), dim, dtype=self.torch.float32, device=idx.device)
+        roast_embedding_fwd_multi(self.h, list(mids), idx.data_ptr(), n, out.data_ptr(), self._s(stream))
+        return out
+
+    def emb_bwd_multi(self, mids, idx, dout, stream=None):
+        roast_embedding_bwd_multi(self.h, list(mids), idx.data_ptr(), idx.numel() // len(mids), dout.data_ptr(),
+                                  self._s(stream))
 
     def zero_grad(self, stream=None):
         roast_zero_grad(self.h, self._s(stream))

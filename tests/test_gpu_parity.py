@@ -222,6 +222,61 @@ def test_embedding_parity(R, torch, n, dist):
     assert rel_frob(ctx.dM.cpu().numpy(), ref_dM) <= 1e-5
 
 
+@pytest.mark.parametrize("det", [False, True])
+@pytest.mark.parametrize("nt,n,d,Z", [(3, 1000, 128, 32), (26, 257, 64, 16), (70, 33, 20, 8), (2, 0, 128, 32)])
+def test_embedding_multi_table_parity(R, torch, nt, n, d, Z, det):
+    """Fused multi-table a4/a5 (one launch per <= 64 tables): each table's rows bit-exact vs the
+    oracle (ragged d % Z, > 64 tables, repeated ids, empty batch); dM vs the oracle sum; in
+    deterministic mode bitwise equal to the single-table calls."""
+    mem, rows = 300_000, 10 ** 6
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64, deterministic=det)
+    reg = [ctx.embedding(rows, d, Z) for _ in range(min(nt, 5))]
+    mids = [reg[t % len(reg)] for t in range(nt)]
+    idx_np = np.concatenate([synth.zipf_indices(synth.SEED_IDX + t, n, rows) for t in range(nt)])
+    dout_np = synth.normal(synth.SEED_DY, (nt * n, d)).astype(np.float32)
+    idx, dout = to_dev(idx_np, torch.int64), to_dev(dout_np, torch.float32)
+    ctx.zero_grad()
+    out = ctx.emb_fwd_multi(mids, idx)
+    ctx.emb_bwd_multi(mids, idx, dout)
+    torch.cuda.synchronize()
+    ctx.check()
+    ref_dM = np.zeros(mem)
+    got = out.cpu().numpy().astype(np.float64)
+    for t, mid in enumerate(mids):
+        spec = OE.EmbeddingSpec(rows, d, Z, mem, HS, mid)
+        sl = slice(t * n, (t + 1) * n)
+        if n:
+            assert np.array_equal(got[sl], spec.forward(idx_np[sl], M_np)), t
+        spec.backward(idx_np[sl], dout_np[sl], ref_dM)
+    assert rel_frob(ctx.dM.cpu().numpy(), ref_dM) <= 1e-5
+    if det:
+        multi = ctx.dM.clone()
+        ctx.zero_grad()
+        for t, mid in enumerate(mids):
+            ctx.emb_bwd(mid, idx[t * n:(t + 1) * n], dout[t * n:(t + 1) * n])
+        torch.cuda.synchronize()
+        assert torch.equal(multi, ctx.dM)
+
+
+def test_embedding_multi_table_errors(R, torch):
+    from paper_2207_10702_b200 import roast
+    M_np = store(4096)
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64)
+    a, b = ctx.embedding(100, 64, 32), ctx.embedding(100, 32, 32)
+    idx = to_dev(np.array([1, 2, 3, 4], dtype=np.int64), torch.int64)
+    out = torch.empty(4, 64, device="cuda")
+    with pytest.raises(roast.RoastError):
+        roast.roast_embedding_fwd_multi(ctx.h, [a, b], idx.data_ptr(), 2, out.data_ptr())
+    with pytest.raises(roast.RoastError):
+        roast.roast_embedding_fwd_multi(ctx.h, [a, 999], idx.data_ptr(), 2, out.data_ptr())
+    bad = to_dev(np.array([1, 100, 3, -5], dtype=np.int64), torch.int64)
+    out = ctx.emb_fwd_multi([a, a], bad)
+    torch.cuda.synchronize()
+    assert torch.all(out[1] == 0) and torch.all(out[3] == 0) and torch.any(out[0] != 0)
+    assert roast.roast_get_error(ctx.h) == roast.ERR_BOUNDS
+
+
 def test_embedding_duplicates_and_bounds(R, torch):
     from paper_2207_10702_b200 import roast
     mem = 4096

@@ -45,9 +45,20 @@ def main():
         for t in range(tables):
             ctx.emb_bwd(ids[t], idx[t], dout)
 
+    idx_all = torch.cat(idx)                       # table-major 26 x batch
+    out_all = torch.empty(tables * batch, dim, device="cuda")
+    dout_all = dout.repeat(tables, 1)
+
+    def fwd_multi():                               # all 26 tables in one launch
+        ctx.emb_fwd_multi(ids, idx_all, out_all)
+
+    def bwd_multi():
+        ctx.emb_bwd_multi(ids, idx_all, dout_all)
+
     res = {}
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    for name, fn, bpl in [("fwd", fwd, 1032), ("bwd", bwd, 1544)]:
+    for name, fn, bpl in [("fwd", fwd, 1032), ("bwd", bwd, 1544), ("fwd_multi", fwd_multi, 1032),
+                          ("bwd_multi", bwd_multi, 1544)]:
         for _ in range(3):
             fn()
         g = torch.cuda.CUDAGraph()
@@ -66,6 +77,29 @@ def main():
         gbs = tables * batch * bpl / (ms * 1e-3) / 1e9
         res[name] = dict(ms=ms, GBps=gbs, hbm_frac=gbs / 6558.1, lookups=tables * batch)
     ctx.check()
+    # library baseline: torch gather / index_add_ of the same 128-B chunks at the same offsets
+    # (precomputed, no hashing) -> what the raw access pattern costs on this GPU
+    if args.align * 4 == 128:
+        offs = torch.cat([ctx.chunk_map(ids[t], idx[t])[0].reshape(-1) for t in range(tables)]) // 32
+        Mv = M.view(-1, 32)
+        dflat = dout.reshape(-1, 32).repeat(tables, 1)
+        g = torch.empty(offs.numel(), 32, device="cuda")
+        for name, fn in [("torch_gather", lambda: torch.index_select(Mv, 0, offs, out=g)),
+                         ("torch_index_add", lambda: Mv.index_add_(0, offs, dflat))]:
+            for _ in range(3):
+                fn()
+            times = []
+            for _ in range(args.steps):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                fn()
+                b.record()
+                torch.cuda.synchronize()
+                times.append(a.elapsed_time(b))
+            ms = float(np.median(times))
+            bpl = 1032 if name == "torch_gather" else 1544
+            res[name] = dict(ms=ms, GBps=tables * batch * bpl / (ms * 1e-3) / 1e9)
     print(json.dumps(dict(config="C4 26x1e7x128 chunk 32 1000x", dist=args.dist, batch=batch, align=args.align,
                           **res)))
 
