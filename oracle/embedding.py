@@ -24,11 +24,14 @@ from . import hashing
 
 class EmbeddingSpec:
     def __init__(self, num_rows, dim, chunk, mem_size, seed, module, align=8, C=1.0,
-                 fan_in=None, use_sign=True):
+                 fan_in=None, use_sign=True, segment=None):
         self.num_rows, self.dim, self.chunk = num_rows, dim, chunk
         self.mem_size = mem_size
         self.chunks_per_row = -(-dim // chunk)
-        self.mh = hashing.ModuleHash(seed, module, mem_size, chunk, align, use_sign)
+        # segment = (base, size): LMS memory M_i of this table; None = GMS
+        seg_base, seg_size = segment if segment is not None else (0, mem_size)
+        assert 0 <= seg_base and seg_base + seg_size <= mem_size
+        self.mh = hashing.ModuleHash(seed, module, seg_size, chunk, align, use_sign, base=seg_base)
         self.lam = hashing.lam(C, dim if fan_in is None else fan_in)
 
     def chunk_map(self, rows) -> tuple[np.ndarray, np.ndarray]:

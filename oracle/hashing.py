@@ -88,19 +88,40 @@ def lam(C: float, fan_in: float) -> float:
     return float(np.float32(C / math.sqrt(fan_in)))
 
 
+def lms_segments(sizes, mem_size: int, align: int) -> list[tuple[int, int]]:
+    """Local memory sharing: piece i of n_i parameters gets its own
+    memory M_i of |M_i| = f_i |M|, f_i = n_i / n, sum |M_i| = |M|.  Reading R14/R23:
+    |M_i| = floor(f_i |M|) rounded down to a multiple of A (so every segment base
+    stays A-aligned), the remainder goes to the last piece.  Returns (base, size)."""
+    n = sum(sizes)
+    out, base = [], 0
+    for i, ni in enumerate(sizes):
+        if i == len(sizes) - 1:
+            size = mem_size - base
+        else:
+            size = (ni * mem_size // n) // align * align
+        out.append((base, size))
+        base += size
+    return out
+
+
 class ModuleHash:
-    """The hash functions of one registered module (offset + sign), cached coefficients."""
+    """The hash functions of one registered module (offset + sign), cached coefficients.
+
+    GMS: the module hashes into all of M (base 0, mem_size = |M|).  LMS
+    (P:320): into its own segment M_i = M[base, base + mem_size)."""
 
     def __init__(self, seed: int, module: int, mem_size: int, span: int, align: int,
-                 use_sign: bool = True):
+                 use_sign: bool = True, base: int = 0):
         self.c_off = coefficients(seed, module, ROLE_OFFSET)
         self.c_sgn = coefficients(seed, module, ROLE_SIGN)
         self.R = num_positions(mem_size, span, align)
         self.align = align
         self.use_sign = use_sign
+        self.base = base
 
     def offset(self, key: int) -> int:
-        return self.align * (poly61(self.c_off, key) % self.R)
+        return self.base + self.align * (poly61(self.c_off, key) % self.R)
 
     def sign(self, key: int) -> int:
         if not self.use_sign:

@@ -59,7 +59,7 @@ class LinearSpec:
     """
 
     def __init__(self, H, O, z1, z2, mem_size, seed, module, align=8, C=1.0,
-                 mapping=HASH, use_sign=True, layout=ROW_MAJOR, base=0, lam=None):
+                 mapping=HASH, use_sign=True, layout=ROW_MAJOR, base=0, lam=None, segment=None):
         self.H, self.O, self.z1, self.z2 = H, O, z1, z2
         self.mem_size = mem_size
         self.layout = layout
@@ -69,7 +69,10 @@ class LinearSpec:
         self.off = np.zeros((self.nx, self.ny), dtype=np.int64)
         self.sgn = np.ones((self.nx, self.ny), dtype=np.int64)
         if mapping == HASH:
-            mh = hashing.ModuleHash(seed, module, mem_size, T, align, use_sign)
+            # segment = (base, size): LMS memory M_i of this module; None = GMS
+            seg_base, seg_size = segment if segment is not None else (0, mem_size)
+            assert 0 <= seg_base and seg_base + seg_size <= mem_size
+            mh = hashing.ModuleHash(seed, module, seg_size, T, align, use_sign, base=seg_base)
             for x in range(self.nx):
                 for y in range(self.ny):
                     k = hashing.tile_key(x, y)
