@@ -197,6 +197,7 @@ def run_gpu(args):
     stream = torch.cuda.current_stream()
     M = torch.tensor(synth.uniform(synth.SEED_M, (mem,)).astype(np.float32), device=dev)
     ctx = R.Roast(M, TILE, TILE, seed=synth.HASH_SEED, deterministic=args.deterministic)
+    ctx.set_autotune(args.autotune)   # tuned in the eager warm-up, before graph capture
     from paper_2207_10702_b200 import dp
     dp.init_comm(ctx, rank, world, device=dev)   # NCCL communicator inside libroast (no-op at N = 1)
     l1 = ctx.linear(*LAYERS[0])
@@ -253,6 +254,16 @@ def run_gpu(args):
             rec("dx", lambda: ctx.bwd_dx(l1, dY1, dX))
             rec("dm", lambda: ctx.bwd_dm(l1, Xin, dY1))
         ctx.allreduce()
+
+    if args.autotune:   # tune every kernel once, sequentially on one stream (no concurrent work skews it)
+        ctx.zero_grad()
+        ctx.fwd(l1, X, Y1)
+        ctx.fwd(l2, Y1, Y2)
+        ctx.bwd_dx(l2, dY2, dY1)
+        ctx.bwd_dm(l2, Y1, dY2)
+        ctx.bwd_dx(l1, dY1, dX)
+        ctx.bwd_dm(l1, X, dY1)
+        torch.cuda.synchronize()
 
     def barrier():
         if world > 1:
@@ -424,6 +435,9 @@ def run_gpu(args):
                     l2="flushed between timed steps (256 MB write outside the events)",
                     dm_mode="deterministic" if args.deterministic else "atomic",
                     streams=args.streams, cuda_graph=bool(args.graph),
+                    autotune=["makespan model", "inference-optimal", "training-optimal"][args.autotune],
+                    tuned={f"L{i + 1}.{k}": ctx.tuned(mid, j, T) for i, mid in enumerate((l1, l2))
+                           for j, k in enumerate(("fwd", "dx", "dm"))},
                     parallelism=f"dp{world}"),
         roofline=dict(bound="tensor", kernel=dom, achieved=achieved, peak=burst, unit="TFLOP/s",
                       frac=achieved / burst, traffic=ncu_traffic(dom),
@@ -454,6 +468,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--streams", type=int, default=2, choices=[1, 2])
     ap.add_argument("--graph", type=int, default=1, choices=[0, 1])
+    ap.add_argument("--autotune", type=int, default=2, choices=[0, 1, 2],
+                    help="kernel-config autotuner: 0 makespan model, 1 inference-optimal, 2 training-optimal")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

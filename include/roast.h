@@ -108,6 +108,35 @@ roast_status_t roast_register_linear(roast_t h, int64_t in_features, int64_t out
 roast_status_t roast_register_embedding(roast_t h, int64_t num_rows, int32_t dim, int32_t chunk,
                                         double fan_in, int32_t* id);
 
+/* LMS (NEXT #4): the same registrations, but the module hashes into
+ * its own memory M_i = M[seg_base, seg_base + seg_size) instead of all of M (GMS,
+ * P:322; roast_register_* == the _seg form with 0, |M|).  offset = seg_base +
+ * A * (poly mod R_i), R_i = floor((seg_size - span) / A) + 1.  The segments of a
+ * LMS model are the caller's (roast.lms_segments: |M_i| = floor(f_i |M|) aligned
+ * down to A, f_i = n_i / n, remainder to the last piece - reading R23); overlapping
+ * segments are legal (they share memory).  Errors: GEOMETRY (segment outside M,
+ * seg_base % A != 0, span > seg_size), CONFIG (identity mapping), as above otherwise. */
+roast_status_t roast_register_linear_seg(roast_t h, int64_t in_features, int64_t out_features, int64_t seg_base,
+                                         int64_t seg_size, int32_t* id);
+roast_status_t roast_register_embedding_seg(roast_t h, int64_t num_rows, int32_t dim, int32_t chunk,
+                                            double fan_in, int64_t seg_base, int64_t seg_size, int32_t* id);
+
+/* Kernel-configuration autotuner (NEXT #4).  The paper autotunes its
+ * tile per layer shape, either inference-optimal (tune the forward kernel, the
+ * backward kernels share its tile) or training-optimal (tune forward and backward
+ * kernels together).  Here the hash tile is part of the model (R10), so the tuned
+ * parameter is the tcgen05 kernel configuration: WM for the forward / dX kernels and
+ * (WM, split-K) for the dM kernel.  The first call for a (kernel, in, out, tokens)
+ * outside CUDA-graph capture times each candidate with CUDA events on its stream
+ * (synchronising the host once) and caches the winner; the dM kernel's timed runs
+ * are undone (dM is snapshot and restored).  OFF (default) = the makespan model.
+ * Results never depend on the choice beyond fp32 summation order. */
+typedef enum { ROAST_TUNE_OFF = 0, ROAST_TUNE_INFERENCE = 1, ROAST_TUNE_TRAINING = 2 } roast_autotune_t;
+roast_status_t roast_set_autotune(roast_t h, roast_autotune_t strategy);
+/* The cached choice for a kernel (0 forward, 1 dX, 2 dM) of linear `id` at `tokens`:
+ * *wm and *splits; ROAST_ERR_STATE if that shape was never tuned, BAD_ID. */
+roast_status_t roast_get_tuned(roast_t h, int32_t id, int32_t kernel, int64_t tokens, int32_t* wm, int32_t* splits);
+
 /* a1: Y[tokens x out] = lambda * X[tokens x in] * W~, W~ tiles read from M
  * through the hash with sign g (Alg. 1; lambda once per output tile,
  * P:308).  dt = ROAST_FP32: X, Y fp32, SIMT FMA path on M (fp32).

@@ -161,12 +161,32 @@ roast_status_t roast_bind(roast_t h, float* d_M, float* d_dM, roast_stream_t str
   return ROAST_OK;
 }
 
+// [seg_base, seg_base + seg_size) must be an A-aligned piece of M holding at least one span
+static roast_status_t check_segment(const Ctx* c, int64_t seg_base, int64_t seg_size, int64_t span) {
+  const int64_t A = c->cfg.align_elems;
+  if (seg_base < 0 || seg_size <= 0 || seg_base > c->mem_size - seg_size)
+    return fail(ROAST_ERR_GEOMETRY, "segment outside M");
+  if (seg_base % A) return fail(ROAST_ERR_GEOMETRY, "segment base must be a multiple of align_elems");
+  if (span > seg_size) return fail(ROAST_ERR_GEOMETRY, "tile / chunk larger than the module's memory (S:51)");
+  return ROAST_OK;
+}
+
 roast_status_t roast_register_linear(roast_t h, int64_t H, int64_t O, int32_t* id) {
+  Ctx* c = ctx(h);
+  if (!c) return fail(ROAST_ERR_STATE, "null handle");
+  return roast_register_linear_seg(h, H, O, 0, c->mem_size, id);
+}
+
+roast_status_t roast_register_linear_seg(roast_t h, int64_t H, int64_t O, int64_t seg_base, int64_t seg_size,
+                                         int32_t* id) {
   Ctx* c = ctx(h);
   if (!c) return fail(ROAST_ERR_STATE, "null handle");
   if (H <= 0 || O <= 0) return fail(ROAST_ERR_SHAPE, "in/out features must be > 0");
   const int64_t z1 = c->tile.z1, z2 = c->tile.z2, T = z1 * z2, A = c->cfg.align_elems;
   if (T > c->mem_size) return fail(ROAST_ERR_GEOMETRY, "tile Z1*Z2 larger than |M| (S:51)");
+  if (roast_status_t st = check_segment(c, seg_base, seg_size, T)) return st;
+  if (c->cfg.mapping == ROAST_MAP_IDENTITY && (seg_base != 0 || seg_size != c->mem_size))
+    return fail(ROAST_ERR_CONFIG, "segments apply to the hashed mapping only");
   if (H % z1 || O % z2) return fail(ROAST_ERR_GEOMETRY, "in % Z1 and out % Z2 must be 0 on the GPU path (R9)");
   if (T % A) return fail(ROAST_ERR_GEOMETRY, "Z1*Z2 must be a multiple of align_elems");
   if (c->cfg.deterministic && A % 4)
@@ -181,7 +201,8 @@ roast_status_t roast_register_linear(roast_t h, int64_t H, int64_t O, int32_t* i
   const uint32_t mid = uint32_t(c->modules.size());
   m.hash.off = make_coef(c->seed, mid, 0);
   m.hash.sgn = make_coef(c->seed, mid, 1);
-  m.hash.set_range(uint64_t((c->mem_size - T) / A + 1));
+  m.hash.set_range(uint64_t((seg_size - T) / A + 1));
+  m.hash.base = uint64_t(seg_base);
   m.hash.align = uint32_t(A);
   m.hash.use_sign = c->cfg.use_sign ? 1u : 0u;
   const int64_t nt = int64_t(m.nx) * m.ny;
@@ -247,9 +268,17 @@ roast_status_t roast_register_embedding(roast_t h, int64_t num_rows, int32_t dim
                                         int32_t* id) {
   Ctx* c = ctx(h);
   if (!c) return fail(ROAST_ERR_STATE, "null handle");
+  return roast_register_embedding_seg(h, num_rows, dim, chunk, fan_in, 0, c->mem_size, id);
+}
+
+roast_status_t roast_register_embedding_seg(roast_t h, int64_t num_rows, int32_t dim, int32_t chunk, double fan_in,
+                                            int64_t seg_base, int64_t seg_size, int32_t* id) {
+  Ctx* c = ctx(h);
+  if (!c) return fail(ROAST_ERR_STATE, "null handle");
   if (num_rows <= 0 || dim <= 0 || chunk <= 0) return fail(ROAST_ERR_SHAPE, "rows, dim, chunk must be > 0");
   const int64_t A = c->cfg.align_elems;
   if (chunk > c->mem_size) return fail(ROAST_ERR_GEOMETRY, "chunk larger than |M|");
+  if (roast_status_t st = check_segment(c, seg_base, seg_size, chunk)) return st;
   if (chunk % A || chunk % 4 || dim % 4 || A % 4)
     return fail(ROAST_ERR_GEOMETRY, "chunk % A, chunk % 4, dim % 4 and A % 4 must be 0 (16-byte vector access)");
   Module m;
@@ -262,7 +291,8 @@ roast_status_t roast_register_embedding(roast_t h, int64_t num_rows, int32_t dim
   const uint32_t mid = uint32_t(c->modules.size());
   m.hash.off = make_coef(c->seed, mid, 0);
   m.hash.sgn = make_coef(c->seed, mid, 1);
-  m.hash.set_range(uint64_t((c->mem_size - chunk) / A + 1));
+  m.hash.set_range(uint64_t((seg_size - chunk) / A + 1));
+  m.hash.base = uint64_t(seg_base);
   m.hash.align = uint32_t(A);
   m.hash.use_sign = c->cfg.use_sign ? 1u : 0u;
   m.lam = float(c->cfg.C / sqrt(fan_in > 0 ? fan_in : double(dim)));
@@ -437,6 +467,27 @@ roast_status_t roast_embedding_bwd_multi(roast_t h, const int32_t* ids, int32_t 
                                          int64_t n, const float* dOut, roast_stream_t stream) {
   if (!dOut && ntables > 0 && n > 0) return fail(ROAST_ERR_CONFIG, "null dOut");
   return embedding_multi(h, ids, ntables, idx, n, nullptr, dOut, stream);
+}
+
+roast_status_t roast_set_autotune(roast_t h, roast_autotune_t strategy) {
+  Ctx* c = ctx(h);
+  if (!c) return fail(ROAST_ERR_STATE, "null handle");
+  if (strategy < ROAST_TUNE_OFF || strategy > ROAST_TUNE_TRAINING) return fail(ROAST_ERR_CONFIG, "bad strategy");
+  if (c->autotune != int(strategy)) c->tuned.clear();
+  c->autotune = int(strategy);
+  return ROAST_OK;
+}
+
+roast_status_t roast_get_tuned(roast_t h, int32_t id, int32_t kernel, int64_t tokens, int32_t* wm, int32_t* splits) {
+  Ctx* c = ctx(h);
+  Module* m;
+  roast_status_t st = get_module(c, id, kLinear, &m);
+  if (st) return st;
+  auto it = c->tuned.find(std::array<int64_t, 4>{kernel, m->H, m->O, tokens});
+  if (it == c->tuned.end()) return fail(ROAST_ERR_STATE, "shape not tuned");
+  if (wm) *wm = it->second.first;
+  if (splits) *splits = it->second.second;
+  return ROAST_OK;
 }
 
 roast_status_t roast_zero_grad(roast_t h, roast_stream_t stream) {

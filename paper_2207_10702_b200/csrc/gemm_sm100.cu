@@ -39,6 +39,9 @@
 
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
+#include <array>
+#include <vector>
 
 #include "roast_internal.h"
 
@@ -785,15 +788,51 @@ static int choose_wm(int64_t m_rows, int n_tiles, int splits) {
   return cost(2, 0.85) < cost(1, 0.6) ? 2 : 1;
 }
 
+// ---- autotuner (NEXT #4) ---------------------------------------------
+// The paper autotunes its Triton tile per layer shape with two strategies: inference-
+// optimal (tune the forward, share its tile with the backward kernels) and training-
+// optimal (tune forward and backward kernels together).  Here the hash tile is part of
+// the model (64 x 64, R10), so what is tuned is the kernel configuration: WM (M sub-tiles
+// per CTA pair) for FWD / DX and (WM, split-K) for DW.  Each candidate is timed once with
+// CUDA events on the caller's stream (1 warm-up + 3 timed launches) the first time a
+// shape is seen outside stream capture; the winner is cached per (kernel, H, O, tokens).
+namespace {
+enum { kTuneFwd = 0, kTuneDx = 1, kTuneDw = 2 };
+
+std::array<int64_t, 4> tune_key(int kind, const Module& m, int64_t T) { return {kind, m.H, m.O, T}; }
+
+bool can_tune(const Ctx* c, cudaStream_t s) {
+  if (c->autotune == ROAST_TUNE_OFF) return false;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+}
+
+template <class F>
+float time_candidate(F&& f, cudaStream_t s) {
+  cudaEvent_t e0, e1;
+  if (cudaEventCreate(&e0) != cudaSuccess) return -1.f;
+  if (cudaEventCreate(&e1) != cudaSuccess) {
+    cudaEventDestroy(e0);
+    return -1.f;
+  }
+  float ms = -1.f;
+  if (f() == ROAST_OK) {   // warm-up (also sets smem attributes / builds descriptors)
+    bool ok = cudaEventRecord(e0, s) == cudaSuccess;
+    for (int r = 0; r < 3 && ok; ++r) ok = f() == ROAST_OK;
+    ok = ok && cudaEventRecord(e1, s) == cudaSuccess && cudaEventSynchronize(e1) == cudaSuccess;
+    if (ok && cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) ms = -1.f;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return ms;
+}
+}  // namespace
+
 // FWD / DX share the geometry: M = tokens, N = the module's output side, K = its input side.
-static roast_status_t run_tok_major(Ctx* c, const Module& m, const void* A, void* out, int64_t T, int N, int K,
-                                    const int32_t* coord, int coord_ld, bool dx, cudaStream_t s) {
-  if (!supported(c, m) || T >= (int64_t(1) << 31)) return ROAST_ERR_UNSUPPORTED;
-  roast_status_t st = sm100_prepare(c);
-  if (st) return st;
-  const int wm = choose_wm(T, (N + BN - 1) / BN, 1);
+static roast_status_t tok_major_launch(Ctx* c, const Module& m, const void* A, void* out, int64_t T, int N, int K,
+                                       const int32_t* coord, int coord_ld, bool dx, int wm, cudaStream_t s) {
   CUtensorMap a;
-  st = make_map_2d(&a, A, uint64_t(K), uint64_t(T), uint64_t(K) * 2, BK, BM * wm);
+  roast_status_t st = make_map_2d(&a, A, uint64_t(K), uint64_t(T), uint64_t(K) * 2, BK, BM * wm);
   if (st) return st;
   Params p = base_params(c, m, T);
   p.M = int(std::min<int64_t>(T, 1 << 30));
@@ -816,6 +855,36 @@ static roast_status_t run_tok_major(Ctx* c, const Module& m, const void* A, void
   return st;
 }
 
+static roast_status_t run_tok_major(Ctx* c, const Module& m, const void* A, void* out, int64_t T, int N, int K,
+                                    const int32_t* coord, int coord_ld, bool dx, cudaStream_t s) {
+  if (!supported(c, m) || T >= (int64_t(1) << 31)) return ROAST_ERR_UNSUPPORTED;
+  roast_status_t st = sm100_prepare(c);
+  if (st) return st;
+  const auto key = tune_key(dx ? kTuneDx : kTuneFwd, m, T);
+  auto it = c->tuned.find(key);
+  auto fwd = c->tuned.find(tune_key(kTuneFwd, m, T));
+  int wm;
+  if (it != c->tuned.end()) {
+    wm = it->second.first;
+  } else if (dx && c->autotune == ROAST_TUNE_INFERENCE && fwd != c->tuned.end()) {
+    wm = fwd->second.first;   // inference-optimal: the backward shares the forward's tile
+  } else if ((!dx || c->autotune == ROAST_TUNE_TRAINING) && can_tune(c, s)) {
+    float best = 1e30f;
+    wm = choose_wm(T, (N + BN - 1) / BN, 1);
+    for (int w = 1; w <= (cta_group() == 2 ? 2 : 1); ++w) {
+      const float ms = time_candidate([&] { return tok_major_launch(c, m, A, out, T, N, K, coord, coord_ld, dx, w, s); }, s);
+      if (ms >= 0.f && ms < best) {
+        best = ms;
+        wm = w;
+      }
+    }
+    c->tuned[key] = {wm, 1};
+  } else {
+    wm = choose_wm(T, (N + BN - 1) / BN, 1);
+  }
+  return tok_major_launch(c, m, A, out, T, N, K, coord, coord_ld, dx, wm, s);
+}
+
 roast_status_t sm100_fwd(Ctx* c, const Module& m, const void* X, void* Y, int64_t T, cudaStream_t s) {
   return run_tok_major(c, m, X, Y, T, int(m.O), int(m.H), m.d_coord_xy, m.ny, false, s);
 }
@@ -824,38 +893,52 @@ roast_status_t sm100_dx(Ctx* c, const Module& m, const void* dY, void* dX, int64
   return run_tok_major(c, m, dY, dX, T, int(m.H), int(m.O), m.d_coord_yx, m.nx, true, s);
 }
 
-roast_status_t sm100_dw(Ctx* c, const Module& m, const void* X, const void* dY, int64_t T, cudaStream_t s) {
-  if (!supported(c, m) || T >= (int64_t(1) << 31)) return ROAST_ERR_UNSUPPORTED;
+// makespan model for DW: cost of (WM, split-K over tokens) = ceil(units / slots) * WM / (eff * s);
+// eff = TMA-box-rate bound MMA share (4 boxes / 512 clk for WM 1, 6 / 1024 for WM 2)
+static double dw_cost(const Module& m, int64_t T, int w, int sp) {
+  const int cg = cta_group();
+  const int slots = num_sms() / cg;
+  const int n_tiles = int((m.O + BN - 1) / BN);
+  const int tiles_w = int((m.H + BM * cg * w - 1) / (BM * cg * w)) * n_tiles;
+  const double eff = w == 2 ? 0.95 : 0.9;   // measured MMA-busy share with 3-D operand boxes
+  return double((int64_t(tiles_w) * sp + slots - 1) / slots) * w / (eff * sp);
+}
+
+// the split-K count with the lowest model cost (ties within 1e-9: the smaller count);
+// skip = 1 gives the runner-up
+static int dw_best_splits(const Module& m, int64_t T, int w, int skip = 0) {
+  const int kb = int((T + BK - 1) / BK);
+  int first = 0;
+  for (int pass = 0; pass <= skip; ++pass) {
+    int pick = 0;
+    double best = 1e30;
+    for (int sp = 1; sp <= std::min(kb, 16); ++sp) {
+      if (pass == 1 && sp == first) continue;
+      const double cst = dw_cost(m, T, w, sp);
+      if (cst < best - 1e-9) {
+        best = cst;
+        pick = sp;
+      }
+    }
+    if (pass == 0) first = pick;
+    if (pass == skip) return pick ? pick : first;
+  }
+  return first;
+}
+
+static roast_status_t dw_launch(Ctx* c, const Module& m, const void* X, const void* dY, int64_t T, int wm, int splits,
+                                cudaStream_t s) {
   CUtensorMap a, b;
   roast_status_t st = make_map_2d(&a, X, uint64_t(m.H), uint64_t(T), uint64_t(m.H) * 2, 64, BK);
   if (st) return st;
   st = make_map_2d(&b, dY, uint64_t(m.O), uint64_t(T), uint64_t(m.O) * 2, 64, BK);
   if (st) return st;
   const int cg = cta_group();
-  const int slots = num_sms() / cg;   // concurrent work units
   Params p = base_params(c, m, T);
   p.M = int(m.H);
   p.N = int(m.O);
   p.n_tiles = (p.N + BN - 1) / BN;
   p.k_blocks = int((T + BK - 1) / BK);
-  // (WM, split-K over tokens) minimising the makespan ceil(units / slots) * WM / (eff * s);
-  // eff = TMA-box-rate bound MMA share (4 boxes / 512 clk for WM 1, 6 / 1024 for WM 2)
-  int wm = 1, splits = 1;
-  double best = 1e30;
-  const char* ewm = getenv("ROAST_WM");
-  for (int w = 1; w <= (cg == 2 ? 2 : 1); ++w) {
-    if (ewm && atoi(ewm) != w) continue;
-    const int tiles_w = ((p.M + BM * cg * w - 1) / (BM * cg * w)) * p.n_tiles;
-    const double eff = w == 2 ? 0.95 : 0.9;   // measured MMA-busy share with 3-D operand boxes
-    for (int sp = 1; sp <= std::min(p.k_blocks, 16); ++sp) {
-      const double cost = double((tiles_w * sp + slots - 1) / slots) * w / (eff * sp);
-      if (cost < best - 1e-9) {
-        best = cost;
-        splits = sp;
-        wm = w;
-      }
-    }
-  }
   p.m_tiles = (p.M + BM * cg * wm - 1) / (BM * cg * wm);
   const int tiles = p.m_tiles * p.n_tiles;
   // one 3-D box per operand per stage (falls back to 64x64 2-D boxes if the driver rejects the view)
@@ -904,6 +987,57 @@ roast_status_t sm100_dw(Ctx* c, const Module& m, const void* X, const void* dY, 
     c->launches++;
   }
   return ROAST_OK;
+}
+
+roast_status_t sm100_dw(Ctx* c, const Module& m, const void* X, const void* dY, int64_t T, cudaStream_t s) {
+  if (!supported(c, m) || T >= (int64_t(1) << 31)) return ROAST_ERR_UNSUPPORTED;
+  const int wmax = cta_group() == 2 ? 2 : 1;
+  int wm = 1, splits = 1;
+  const auto key = tune_key(kTuneDw, m, T);
+  auto it = c->tuned.find(key);
+  auto fwd = c->tuned.find(tune_key(kTuneFwd, m, T));
+  const char* ewm = getenv("ROAST_WM");
+  {   // the makespan model's choice (also the fallback of the tuner)
+    double best = 1e30;
+    for (int w = 1; w <= wmax; ++w) {
+      if (ewm && atoi(ewm) != w) continue;
+      const int sp = dw_best_splits(m, T, w);
+      if (dw_cost(m, T, w, sp) < best - 1e-9) {
+        best = dw_cost(m, T, w, sp);
+        wm = w;
+        splits = sp;
+      }
+    }
+  }
+  if (it != c->tuned.end()) {
+    wm = it->second.first;
+    splits = it->second.second;
+  } else if (c->autotune == ROAST_TUNE_INFERENCE && fwd != c->tuned.end() && fwd->second.first <= wmax) {
+    wm = fwd->second.first;   // inference-optimal: share the forward's tile, model picks split-K
+    splits = dw_best_splits(m, T, wm);
+  } else if (c->autotune == ROAST_TUNE_TRAINING && can_tune(c, s)) {
+    // every timed candidate accumulates into dM: snapshot it and restore afterwards
+    float* save = nullptr;
+    ROAST_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&save), c->mem_size * sizeof(float), s));
+    ROAST_CUDA_CHECK(cudaMemcpyAsync(save, c->dM, c->mem_size * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    float best = 1e30f;
+    for (int w = 1; w <= wmax; ++w)
+      for (int k = 0; k < 2; ++k) {   // the model's two best split-K counts per WM
+        const int sp = dw_best_splits(m, T, w, k);
+        if (k == 1 && sp == dw_best_splits(m, T, w, 0)) continue;
+        const float ms = time_candidate([&] { return dw_launch(c, m, X, dY, T, w, sp, s); }, s);
+        if (ms >= 0.f && ms < best) {
+          best = ms;
+          wm = w;
+          splits = sp;
+        }
+      }
+    cudaError_t e = cudaMemcpyAsync(c->dM, save, c->mem_size * sizeof(float), cudaMemcpyDeviceToDevice, s);
+    cudaFreeAsync(save, s);
+    if (e != cudaSuccess) return cuda_fail(e, "autotune dM restore");
+    c->tuned[key] = {wm, splits};
+  }
+  return dw_launch(c, m, X, dY, T, wm, splits, s);
 }
 
 }  // namespace roast

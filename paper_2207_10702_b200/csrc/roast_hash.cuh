@@ -107,12 +107,13 @@ struct ModuleHash {
   uint32_t align;   // A
   uint32_t use_sign;
   ModReciprocal rdiv;  // v mod R without division (set by set_range)
+  uint64_t base = 0;   // first element of the module's memory: 0 under GMS, its segment under LMS
 
   void set_range(uint64_t r) {
     R = r;
     rdiv.init(r);
   }
-  RH_HD uint64_t offset(uint64_t key) const { return uint64_t(align) * mod_recip(poly61(off, key), rdiv); }
+  RH_HD uint64_t offset(uint64_t key) const { return base + uint64_t(align) * mod_recip(poly61(off, key), rdiv); }
   RH_HD int sign(uint64_t key) const {
     return (use_sign && (poly61(sgn, key) & 1)) ? -1 : 1;
   }

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <array>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -66,7 +68,11 @@ struct Ctx {
   const float* tmap_dm_for = nullptr;
   // optimizer state, |M| fp32 each (Adagrad: s1 = G; Adam: s1 = m, s2 = v)
   float* opt_s1 = nullptr;
-  float* opt_s2 = nullptr;};
+  float* opt_s2 = nullptr;
+  // kernel-configuration autotuner (roast_set_autotune): (kernel, H, O, tokens) -> (WM, split-K)
+  int autotune = 0;
+  std::map<std::array<int64_t, 4>, std::pair<int, int>> tuned;
+};
 
 // error reporting (thread-local detail string)
 roast_status_t fail(roast_status_t st, const std::string& msg);

@@ -22,9 +22,10 @@ MAP_HASH, MAP_IDENTITY = 0, 1
 
 EXPORTS = [
     "roast_config_default", "roast_create", "roast_create_ex", "roast_destroy", "roast_bind",
-    "roast_register_linear", "roast_register_embedding", "roast_linear_fwd", "roast_linear_bwd",
+    "roast_register_linear", "roast_register_embedding", "roast_register_linear_seg",
+    "roast_register_embedding_seg", "roast_linear_fwd", "roast_linear_bwd",
     "roast_linear_bwd_dx", "roast_linear_bwd_dm", "roast_embedding_fwd", "roast_embedding_bwd",
-    "roast_embedding_fwd_multi", "roast_embedding_bwd_multi", "roast_comm_unique_id", "roast_comm_init",
+    "roast_embedding_fwd_multi", "roast_embedding_bwd_multi", "roast_set_autotune", "roast_get_tuned", "roast_comm_unique_id", "roast_comm_init",
     "roast_grad_allreduce", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step",
     "roast_get_error",
     "roast_status_str", "roast_last_error", "roast_debug_tile_map", "roast_debug_chunk_map",
@@ -73,6 +74,10 @@ def _load():
         "roast_bind": (st, [H, P, P, S]),
         "roast_register_linear": (st, [H, I64, I64, ctypes.POINTER(I32)]),
         "roast_register_embedding": (st, [H, I64, I32, I32, ctypes.c_double, ctypes.POINTER(I32)]),
+        "roast_set_autotune": (st, [H, ctypes.c_int]),
+        "roast_get_tuned": (st, [H, I32, I32, I64, ctypes.POINTER(I32), ctypes.POINTER(I32)]),
+        "roast_register_linear_seg": (st, [H, I64, I64, I64, I64, ctypes.POINTER(I32)]),
+        "roast_register_embedding_seg": (st, [H, I64, I32, I32, ctypes.c_double, I64, I64, ctypes.POINTER(I32)]),
         "roast_linear_fwd": (st, [H, I32, P, P, I64, ctypes.c_int, S]),
         "roast_linear_bwd": (st, [H, I32, P, P, P, I64, ctypes.c_int, S]),
         "roast_linear_bwd_dx": (st, [H, I32, P, P, I64, ctypes.c_int, S]),
@@ -148,6 +153,49 @@ def roast_register_embedding(h, num_rows, dim, chunk, fan_in=0.0):
     _check(_lib.roast_register_embedding(h, num_rows, dim, chunk, fan_in, ctypes.byref(i)),
            "roast_register_embedding")
     return i.value
+
+
+def roast_register_linear_seg(h, in_features, out_features, seg_base, seg_size):
+    i = ctypes.c_int32()
+    _check(_lib.roast_register_linear_seg(h, in_features, out_features, seg_base, seg_size, ctypes.byref(i)),
+           "roast_register_linear_seg")
+    return i.value
+
+
+def roast_register_embedding_seg(h, num_rows, dim, chunk, fan_in, seg_base, seg_size):
+    i = ctypes.c_int32()
+    _check(_lib.roast_register_embedding_seg(h, num_rows, dim, chunk, fan_in, seg_base, seg_size, ctypes.byref(i)),
+           "roast_register_embedding_seg")
+    return i.value
+
+
+TUNE_OFF, TUNE_INFERENCE, TUNE_TRAINING = 0, 1, 2
+
+
+def roast_set_autotune(h, strategy):
+    _check(_lib.roast_set_autotune(h, strategy), "roast_set_autotune")
+
+
+def roast_get_tuned(h, mid, kernel, tokens):
+    """(WM, split-K) the autotuner cached for kernel 0 fwd / 1 dX / 2 dM, or None."""
+    wm, sp = ctypes.c_int32(), ctypes.c_int32()
+    if _lib.roast_get_tuned(h, mid, kernel, tokens, ctypes.byref(wm), ctypes.byref(sp)) != 0:
+        return None
+    return wm.value, sp.value
+
+
+def lms_segments(sizes, mem_size, align=8):
+    """LMS memories: piece i of sizes[i] parameters gets
+    |M_i| = floor(f_i |M|), f_i = n_i / n, aligned down to `align` so every base
+    stays aligned; the remainder goes to the last piece (R23).
+    Returns [(seg_base, seg_size)] for roast_register_*_seg / Roast.linear(segment=)."""
+    n = sum(int(x) for x in sizes)
+    segs, base = [], 0
+    for i, ni in enumerate(sizes):
+        size = mem_size - base if i == len(sizes) - 1 else (int(ni) * mem_size // n) // align * align
+        segs.append((base, size))
+        base += size
+    return segs
 
 
 def roast_linear_fwd(h, mid, X_ptr, Y_ptr, tokens, dtype, stream=0):
@@ -286,13 +334,22 @@ class Roast:
         except Exception:
             pass
 
-    def linear(self, in_features, out_features):
-        mid = roast_register_linear(self.h, in_features, out_features)
+    def linear(self, in_features, out_features, segment=None):
+        """segment = (seg_base, seg_size): LMS memory of this module (None = GMS)."""
+        mid = (roast_register_linear(self.h, in_features, out_features) if segment is None else
+               roast_register_linear_seg(self.h, in_features, out_features, *segment))
         self.dims[mid] = ("linear", in_features, out_features)
         return mid
 
-    def embedding(self, num_rows, dim, chunk, fan_in=0.0):
-        mid = roast_register_embedding(self.h, num_rows, dim, chunk, fan_in)
+    def set_autotune(self, strategy):
+        roast_set_autotune(self.h, strategy)
+
+    def tuned(self, mid, kernel, tokens):
+        return roast_get_tuned(self.h, mid, kernel, tokens)
+
+    def embedding(self, num_rows, dim, chunk, fan_in=0.0, segment=None):
+        mid = (roast_register_embedding(self.h, num_rows, dim, chunk, fan_in) if segment is None else
+               roast_register_embedding_seg(self.h, num_rows, dim, chunk, fan_in, *segment))
         self.dims[mid] = ("embedding", num_rows, dim, chunk)
         return mid
 

@@ -396,3 +396,117 @@ def test_nccl_allreduce_single_rank_and_graph_capture(R, torch):
     graph.replay()
     torch.cuda.synchronize()
     assert torch.equal(ctx.dM, g)
+
+
+# ---------------------------------------------------------------- NEXT #4: LMS segments
+@pytest.mark.parametrize("dtype,z,deterministic", [("bf16", 64, False), ("bf16", 64, True), ("fp32", 32, False)])
+def test_lms_segments_parity(R, torch, dtype, z, deterministic):
+    """LMS: each module hashes into its own segment of M; tile / chunk maps bit-exact,
+    fwd / dX / dM vs the oracle with the same segments, and a module's dM stays inside its
+    segment."""
+    from oracle import hashing as OH
+    from paper_2207_10702_b200 import roast
+    layers = [(768, 3072), (3072, 768)] if z == 64 else [(256, 256), (256, 128)]
+    emb = (1000, 64, 32)
+    mem = 200_000 if z == 64 else 30_000
+    sizes = [H * O for H, O in layers] + [emb[0] * emb[1]]
+    segs = roast.lms_segments(sizes, mem, 8)
+    assert segs == OH.lms_segments(sizes, mem, 8)
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, z, z, deterministic=deterministic)
+    ids = [ctx.linear(H, O, segment=segs[i]) for i, (H, O) in enumerate(layers)]
+    eid = ctx.embedding(*emb, segment=segs[-1])
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    T = 300
+    for i, (mid, (H, O)) in enumerate(zip(ids, layers)):
+        spec = OM.LinearSpec(H, O, z, z, mem, HS, mid, segment=segs[i])
+        off, sgn = ctx.tile_map(mid)
+        assert np.array_equal(off, spec.off)
+        assert np.array_equal(sgn.astype(np.int64), spec.sgn)
+        X_np = bf16_input(synth.SEED_X + i, (T, H))
+        dY_np = bf16_input(synth.SEED_DY + i, (T, O))
+        Y, dX, dM = run_linear(R, torch, ctx, mid, X_np, dY_np, tdt)
+        b, s = segs[i]
+        assert not dM[:b].any() and not dM[b + s:].any()
+        tol = 1e-2 if dtype == "bf16" else 1e-5
+        assert rel_frob(Y, spec.forward(X_np, M_np, dtype == "bf16")) <= tol
+        assert rel_frob(dX, spec.backward_dx(dY_np, M_np, dtype == "bf16")) <= tol
+        assert rel_frob(dM, spec.backward_dm(X_np, dY_np)) <= tol
+    espec = OE.EmbeddingSpec(*emb, mem, HS, eid, segment=segs[-1])
+    idx_np = synth.zipf_indices(synth.SEED_IDX, 777, emb[0])
+    dout_np = synth.normal(synth.SEED_DY, (777, emb[1])).astype(np.float32)
+    out = ctx.emb_fwd(eid, to_dev(idx_np, torch.int64))
+    ctx.zero_grad()
+    ctx.emb_bwd(eid, to_dev(idx_np, torch.int64), to_dev(dout_np, torch.float32))
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().astype(np.float64), espec.forward(idx_np, M_np))
+    b, s = segs[-1]
+    dM = ctx.dM.cpu().numpy()
+    assert not dM[:b].any()
+    assert rel_frob(dM, espec.backward(idx_np, dout_np)) <= 1e-5
+    ctx.check()
+
+
+def test_lms_segment_errors(R, torch):
+    from paper_2207_10702_b200 import roast
+    ctx, _ = make_ctx(R, torch, store(10_000), 64, 64)
+    for seg in [(-8, 5000), (4, 5000), (8000, 4000), (0, 4000)]:        # outside, unaligned, past end, < tile
+        with pytest.raises(roast.RoastError):
+            ctx.linear(128, 128, segment=seg)
+    with pytest.raises(roast.RoastError):
+        ctx.embedding(10, 64, 32, segment=(0, 16))
+
+
+# ---------------------------------------------------------------- NEXT #4: autotuner
+@pytest.mark.parametrize("strategy", [1, 2])
+@pytest.mark.parametrize("deterministic", [False, True])
+def test_autotune_strategies_keep_parity(R, torch, strategy, deterministic):
+    """Inference-optimal (1) tunes the forward only and shares its WM; training-optimal (2)
+    tunes fwd, dX and dM.  Timed dM candidates must leave dM exactly as one call would."""
+    cfg = synth.mlp_block(100, tokens=1024)
+    mem, T = cfg["mem_size"], cfg["tokens"]
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64, deterministic=deterministic)
+    ctx.set_autotune(strategy)
+    ids = [ctx.linear(H, O) for H, O in cfg["layers"]]
+    dM_ref = np.zeros(mem)
+    ctx.zero_grad()
+    for mid, (H, O) in zip(ids, cfg["layers"]):
+        X_np = bf16_input(synth.SEED_X + mid, (T, H))
+        dY_np = bf16_input(synth.SEED_DY + mid, (T, O))
+        X, dY = to_dev(X_np, torch.bfloat16), to_dev(dY_np, torch.bfloat16)
+        Y = ctx.fwd(mid, X)
+        dX = ctx.bwd(mid, X, dY)
+        torch.cuda.synchronize()
+        spec = OM.LinearSpec(H, O, 64, 64, mem, HS, mid)
+        assert rel_frob(Y.float().cpu().numpy(), spec.forward(X_np, M_np, True)) <= 1e-2
+        assert rel_frob(dX.float().cpu().numpy(), spec.backward_dx(dY_np, M_np, True)) <= 1e-2
+        spec.backward_dm(X_np, dY_np, dM_ref)
+        assert ctx.tuned(mid, 0, T) is not None
+        assert (ctx.tuned(mid, 1, T) is not None) == (strategy == 2)
+        assert (ctx.tuned(mid, 2, T) is not None) == (strategy == 2)
+    assert rel_frob(ctx.dM.cpu().numpy(), dM_ref) <= 1e-2
+    ctx.check()
+
+
+def test_autotune_skips_graph_capture(R, torch):
+    """First use inside CUDA-graph capture: no timing (it would break the capture), the
+    makespan model is used and nothing is cached; the captured graph replays correctly."""
+    mem, T, H, O = 47192, 512, 768, 3072
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64)
+    ctx.set_autotune(2)
+    mid = ctx.linear(H, O)
+    X_np = bf16_input(synth.SEED_X, (T, H))
+    X = to_dev(X_np, torch.bfloat16)
+    Y = torch.empty(T, O, device="cuda", dtype=torch.bfloat16)
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            ctx.fwd(mid, X, Y)
+    g.replay()
+    torch.cuda.synchronize()
+    assert ctx.tuned(mid, 0, T) is None
+    spec = OM.LinearSpec(H, O, 64, 64, mem, HS, mid)
+    assert rel_frob(Y.float().cpu().numpy(), spec.forward(X_np, M_np, True)) <= 1e-2

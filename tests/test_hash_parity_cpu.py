@@ -51,3 +51,12 @@ def test_rejects_bad_geometry(R):
         R.roast_debug_hash_host(1, 0, [1, 2], 10, 11, 1)
     with pytest.raises(R.RoastError):
         R.roast_debug_hash_host(1, 0, [1 << 60], 100, 1, 1)
+
+
+def test_lms_segments_product_matches_oracle():
+    """The binding's LMS partition helper (product) == the oracle's reading R23."""
+    from oracle import hashing as OH
+    from paper_2207_10702_b200 import roast
+    for sizes, mem, A in [([768 * 3072, 3072 * 768], 47_192, 8), ([1, 2, 3, 4, 5], 100_000, 32), ([7], 64, 8),
+                          ([10 ** 9, 1, 1], 1 << 20, 8)]:
+        assert roast.lms_segments(sizes, mem, A) == OH.lms_segments(sizes, mem, A)
