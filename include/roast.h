@@ -145,6 +145,25 @@ roast_status_t roast_get_tuned(roast_t h, int32_t id, int32_t kernel, int64_t to
 roast_status_t roast_linear_fwd(roast_t h, int32_t id, const void* d_X, void* d_Y, int64_t tokens,
                                 roast_dtype_t dt, roast_stream_t stream);
 
+/* a1 with a bias (NEXT #3): Y = lambda X W~ + b, b added in fp32 inside the GEMM
+ * epilogue before the single rounding to the output type.  d_bias: out_features fp32
+ * on the device, 16-byte aligned, or NULL (== roast_linear_fwd).  A model whose bias
+ * is ROAST-compressed gets b from roast_bias_fwd. */
+roast_status_t roast_linear_fwd_bias(roast_t h, int32_t id, const void* d_X, void* d_Y, int64_t tokens,
+                                     roast_dtype_t dt, const float* d_bias, roast_stream_t stream);
+
+/* Bias vectors via L ("ROAST uses L to implement ... bias vectors").  A bias of
+ * n elements is row 0 of an embedding registered as (num_rows 1, dim n, chunk Z,
+ * fan_in = the owning layer's in_features, reading R24).
+ *   roast_bias_fwd:  d_b[0..n) = row 0 of bias_id (== roast_embedding_fwd of index 0).
+ *   roast_bias_bwd:  dM[h1(c) + o] += lambda g(c) sum_t dY[t, jZ + o]  (P:340 with
+ *                    dOut = the column sums of dY [tokens x n], bf16 or fp32, fp32
+ *                    accumulation in a fixed order; deterministic mode as a5).
+ * Errors: BAD_ID (not an embedding), CONFIG (null / unaligned: d_b 16 B, dY 8 B), SHAPE. */
+roast_status_t roast_bias_fwd(roast_t h, int32_t bias_id, float* d_b, roast_stream_t stream);
+roast_status_t roast_bias_bwd(roast_t h, int32_t bias_id, const void* d_dY, int64_t tokens, roast_dtype_t dt,
+                              roast_stream_t stream);
+
 /* a2 + a3: dX = lambda * dY W~^T (skipped if d_dX == NULL), and
  * dM[h(x,y) + pi(o1,o2)] += lambda * g(x,y) * (X^T dY)[i, j] for every virtual
  * weight (P:338-346 [§4.3 eq. gradient rule] with g by the chain rule, R12),

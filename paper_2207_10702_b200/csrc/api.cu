@@ -110,12 +110,14 @@ roast_status_t roast_create_ex(roast_t* out, int64_t mem_size, uint64_t seed, ro
   c->seed = seed;
   c->tile = tile;
   c->cfg = cfg;
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&c->d_err), sizeof(int32_t));
+  // one 16-byte block: the sticky error flag, then an int64 0 (row 0 of a bias via L)
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&c->d_err), 16);
   if (e != cudaSuccess) {
     delete c;
     return cuda_fail(e, "cudaMalloc(err flag)");
   }
-  cudaMemset(c->d_err, 0, sizeof(int32_t));
+  cudaMemset(c->d_err, 0, 16);
+  c->d_zero_idx = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(c->d_err) + 8);
   *out = reinterpret_cast<roast_t>(c);
   return ROAST_OK;
 }
@@ -308,6 +310,11 @@ static bool use_sm100(const Ctx* c, const Module& m) {
 
 roast_status_t roast_linear_fwd(roast_t h, int32_t id, const void* X, void* Y, int64_t T, roast_dtype_t dt,
                                 roast_stream_t stream) {
+  return roast_linear_fwd_bias(h, id, X, Y, T, dt, nullptr, stream);
+}
+
+roast_status_t roast_linear_fwd_bias(roast_t h, int32_t id, const void* X, void* Y, int64_t T, roast_dtype_t dt,
+                                     const float* bias, roast_stream_t stream) {
   Ctx* c = ctx(h);
   Module* m;
   roast_status_t st = get_module(c, id, kLinear, &m);
@@ -315,15 +322,61 @@ roast_status_t roast_linear_fwd(roast_t h, int32_t id, const void* X, void* Y, i
   if (T < 0) return fail(ROAST_ERR_SHAPE, "tokens < 0");
   if (T > 0 && (!X || !Y)) return fail(ROAST_ERR_CONFIG, "null X / Y");
   if (dt != ROAST_FP32 && dt != ROAST_BF16) return fail(ROAST_ERR_CONFIG, "bad dtype");
+  if (reinterpret_cast<uintptr_t>(bias) & 15) return fail(ROAST_ERR_CONFIG, "bias must be 16-byte aligned");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (T == 0) return ROAST_OK;
   if (dt == ROAST_BF16 && use_sm100(c, *m)) {
-    st = sm100_fwd(c, *m, X, Y, T, s);
+    st = sm100_fwd(c, *m, X, Y, T, bias, s);
     if (st != ROAST_ERR_UNSUPPORTED) return st;
   }
-  ROAST_CUDA_CHECK(launch_simt_fwd(c, *m, X, Y, T, dt, false, s));
+  ROAST_CUDA_CHECK(launch_simt_fwd(c, *m, X, Y, T, dt, false, s, bias));
   c->launches++;
   return ROAST_OK;
+}
+
+roast_status_t roast_bias_fwd(roast_t h, int32_t bias_id, float* b, roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module* m;
+  roast_status_t st = get_module(c, bias_id, kEmbedding, &m);
+  if (st) return st;
+  if (!b) return fail(ROAST_ERR_CONFIG, "null bias output");
+  if (reinterpret_cast<uintptr_t>(b) & 15) return fail(ROAST_ERR_CONFIG, "bias must be 16-byte aligned");
+  ROAST_CUDA_CHECK(launch_embed_fwd(c, *m, c->d_zero_idx, 1, b, reinterpret_cast<cudaStream_t>(stream)));
+  c->launches++;
+  return ROAST_OK;
+}
+
+roast_status_t roast_bias_bwd(roast_t h, int32_t bias_id, const void* dY, int64_t T, roast_dtype_t dt,
+                              roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module* m;
+  roast_status_t st = get_module(c, bias_id, kEmbedding, &m);
+  if (st) return st;
+  if (T < 0) return fail(ROAST_ERR_SHAPE, "tokens < 0");
+  if (dt != ROAST_FP32 && dt != ROAST_BF16) return fail(ROAST_ERR_CONFIG, "bad dtype");
+  if (T == 0) return ROAST_OK;
+  if (!dY) return fail(ROAST_ERR_CONFIG, "null dY");
+  if (reinterpret_cast<uintptr_t>(dY) & 7) return fail(ROAST_ERR_CONFIG, "dY must be 8-byte aligned");
+  const cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int n = m->dim;
+  const int slabs = colsum_slabs(T, n);
+  float* tmp = nullptr;   // stream-ordered scratch: slab partials, then db (capturable)
+  ROAST_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), (size_t(slabs) + 1) * n * sizeof(float) + 16, s));
+  float* db = tmp + size_t(slabs) * n;
+  db = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(db) + 15) & ~uintptr_t(15));
+  cudaError_t e = launch_colsum(dY, T, n, dt, tmp, db, s);
+  c->launches += 2;
+  if (e == cudaSuccess) {
+    if (c->cfg.deterministic) {
+      st = embed_bwd_deterministic(c, *m, c->d_zero_idx, 1, db, s);
+    } else {
+      e = launch_embed_bwd(c, *m, c->d_zero_idx, 1, db, s);
+      c->launches++;
+    }
+  }
+  cudaFreeAsync(tmp, s);
+  if (e != cudaSuccess) return cuda_fail(e, "bias backward");
+  return st;
 }
 
 static roast_status_t linear_args(Ctx* c, int32_t id, int64_t T, roast_dtype_t dt, const void* a, const void* b,
@@ -348,7 +401,7 @@ roast_status_t roast_linear_bwd_dx(roast_t h, int32_t id, const void* dY, void* 
     st = sm100_dx(c, *m, dY, dX, T, s);
     if (st != ROAST_ERR_UNSUPPORTED) return st;
   }
-  ROAST_CUDA_CHECK(launch_simt_fwd(c, *m, dY, dX, T, dt, true, s));
+  ROAST_CUDA_CHECK(launch_simt_fwd(c, *m, dY, dX, T, dt, true, s, nullptr));
   c->launches++;
   return ROAST_OK;
 }

@@ -89,6 +89,7 @@ struct Params {
   int64_t neg_row;      // row (128 B units) of the negated shadow copy
   float lam;
   __nv_bfloat16* out;   // FWD: Y [T x N], DX: dX [T x N]
+  const float* bias;    // FWD only: fp32 [N] added after lambda (recovered by L), or null
   float* dM;            // DW atomic target
   float* ws;            // DW deterministic workspace [splits][ntiles][4096]
   int ntiles;
@@ -483,7 +484,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         auto process = [&](int c, uint32_t (&r)[64]) {
           uint32_t pk[32];
           int64_t tb = 0;
-          if (MODE != DW) {
+          if (MODE == FWD && p.bias) {
+            // Y = bf16(lambda acc + b): the 64 columns' bias, broadcast to every lane from L1
+            const float4* b4 = reinterpret_cast<const float4*>(p.bias + nb * BN + c * 64);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float4 bv = __ldg(b4 + i);
+              __nv_bfloat162 v0 = __floats2bfloat162_rn(fmaf(p.lam, __uint_as_float(r[4 * i]), bv.x),
+                                                        fmaf(p.lam, __uint_as_float(r[4 * i + 1]), bv.y));
+              __nv_bfloat162 v1 = __floats2bfloat162_rn(fmaf(p.lam, __uint_as_float(r[4 * i + 2]), bv.z),
+                                                        fmaf(p.lam, __uint_as_float(r[4 * i + 3]), bv.w));
+              pk[2 * i] = *reinterpret_cast<uint32_t*>(&v0);
+              pk[2 * i + 1] = *reinterpret_cast<uint32_t*>(&v1);
+            }
+          } else if (MODE != DW) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               __nv_bfloat162 v = __floats2bfloat162_rn(p.lam * __uint_as_float(r[2 * i]),
@@ -830,7 +844,8 @@ float time_candidate(F&& f, cudaStream_t s) {
 
 // FWD / DX share the geometry: M = tokens, N = the module's output side, K = its input side.
 static roast_status_t tok_major_launch(Ctx* c, const Module& m, const void* A, void* out, int64_t T, int N, int K,
-                                       const int32_t* coord, int coord_ld, bool dx, int wm, cudaStream_t s) {
+                                       const int32_t* coord, int coord_ld, bool dx, int wm, const float* bias,
+                                       cudaStream_t s) {
   CUtensorMap a;
   roast_status_t st = make_map_2d(&a, A, uint64_t(K), uint64_t(T), uint64_t(K) * 2, BK, BM * wm);
   if (st) return st;
@@ -844,6 +859,7 @@ static roast_status_t tok_major_launch(Ctx* c, const Module& m, const void* A, v
   p.kb_per_split = p.k_blocks;
   p.units = p.m_tiles * p.n_tiles;
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
+  p.bias = dx ? nullptr : bias;
   p.coord = coord;
   p.coord_ld = coord_ld;
   CUtensorMap o;   // output [T x N] bf16, stored 32 rows x 64 columns per TMA op
@@ -856,7 +872,7 @@ static roast_status_t tok_major_launch(Ctx* c, const Module& m, const void* A, v
 }
 
 static roast_status_t run_tok_major(Ctx* c, const Module& m, const void* A, void* out, int64_t T, int N, int K,
-                                    const int32_t* coord, int coord_ld, bool dx, cudaStream_t s) {
+                                    const int32_t* coord, int coord_ld, bool dx, const float* bias, cudaStream_t s) {
   if (!supported(c, m) || T >= (int64_t(1) << 31)) return ROAST_ERR_UNSUPPORTED;
   roast_status_t st = sm100_prepare(c);
   if (st) return st;
@@ -872,7 +888,7 @@ static roast_status_t run_tok_major(Ctx* c, const Module& m, const void* A, void
     float best = 1e30f;
     wm = choose_wm(T, (N + BN - 1) / BN, 1);
     for (int w = 1; w <= (cta_group() == 2 ? 2 : 1); ++w) {
-      const float ms = time_candidate([&] { return tok_major_launch(c, m, A, out, T, N, K, coord, coord_ld, dx, w, s); }, s);
+      const float ms = time_candidate([&] { return tok_major_launch(c, m, A, out, T, N, K, coord, coord_ld, dx, w, bias, s); }, s);
       if (ms >= 0.f && ms < best) {
         best = ms;
         wm = w;
@@ -882,15 +898,16 @@ static roast_status_t run_tok_major(Ctx* c, const Module& m, const void* A, void
   } else {
     wm = choose_wm(T, (N + BN - 1) / BN, 1);
   }
-  return tok_major_launch(c, m, A, out, T, N, K, coord, coord_ld, dx, wm, s);
+  return tok_major_launch(c, m, A, out, T, N, K, coord, coord_ld, dx, wm, bias, s);
 }
 
-roast_status_t sm100_fwd(Ctx* c, const Module& m, const void* X, void* Y, int64_t T, cudaStream_t s) {
-  return run_tok_major(c, m, X, Y, T, int(m.O), int(m.H), m.d_coord_xy, m.ny, false, s);
+roast_status_t sm100_fwd(Ctx* c, const Module& m, const void* X, void* Y, int64_t T, const float* bias,
+                         cudaStream_t s) {
+  return run_tok_major(c, m, X, Y, T, int(m.O), int(m.H), m.d_coord_xy, m.ny, false, bias, s);
 }
 
 roast_status_t sm100_dx(Ctx* c, const Module& m, const void* dY, void* dX, int64_t T, cudaStream_t s) {
-  return run_tok_major(c, m, dY, dX, T, int(m.H), int(m.O), m.d_coord_yx, m.nx, true, s);
+  return run_tok_major(c, m, dY, dX, T, int(m.H), int(m.O), m.d_coord_yx, m.nx, true, nullptr, s);
 }
 
 // makespan model for DW: cost of (WM, split-K over tokens) = ceil(units / slots) * WM / (eff * s);

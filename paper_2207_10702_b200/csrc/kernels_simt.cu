@@ -59,7 +59,7 @@ constexpr int BM = 64, BN = 64, BK = 16;
 template <typename XT, typename MT, bool kTransW>
 __global__ void __launch_bounds__(256) simt_mm_kernel(const XT* __restrict__ A, XT* __restrict__ C,
                                                       const MT* __restrict__ Mop, MapArgs map, int64_t T,
-                                                      int K, int N, float lam) {
+                                                      int K, int N, float lam, const float* __restrict__ bias) {
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int tid = threadIdx.x;
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(256) simt_mm_kernel(const XT* __restrict__ A, 
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       int n = n0 + tc * 4 + j;
-      if (n < N) store_val(C, m * N + n, lam * acc[i][j]);
+      if (n < N) store_val(C, m * N + n, bias ? fmaf(lam, acc[i][j], bias[n]) : lam * acc[i][j]);
     }
   }
 }
@@ -258,7 +258,7 @@ int grid_1d(int64_t n, int threads) {
 }  // namespace
 
 cudaError_t launch_simt_fwd(const Ctx* c, const Module& m, const void* X, void* Y, int64_t T, roast_dtype_t dt,
-                            bool transpose_w, cudaStream_t s) {
+                            bool transpose_w, cudaStream_t s, const float* bias) {
   if (T == 0) return cudaSuccess;
   const int K = int(transpose_w ? m.O : m.H);
   const int N = int(transpose_w ? m.H : m.O);
@@ -266,17 +266,17 @@ cudaError_t launch_simt_fwd(const Ctx* c, const Module& m, const void* X, void* 
   MapArgs a = map_args(c, m);
   if (dt == ROAST_FP32) {
     if (transpose_w)
-      simt_mm_kernel<float, float, true><<<grid, 256, 0, s>>>((const float*)X, (float*)Y, c->M, a, T, K, N, m.lam);
+      simt_mm_kernel<float, float, true><<<grid, 256, 0, s>>>((const float*)X, (float*)Y, c->M, a, T, K, N, m.lam, bias);
     else
-      simt_mm_kernel<float, float, false><<<grid, 256, 0, s>>>((const float*)X, (float*)Y, c->M, a, T, K, N, m.lam);
+      simt_mm_kernel<float, float, false><<<grid, 256, 0, s>>>((const float*)X, (float*)Y, c->M, a, T, K, N, m.lam, bias);
   } else {
     auto* sh = reinterpret_cast<const __nv_bfloat16*>(c->shadow);
     if (transpose_w)
       simt_mm_kernel<__nv_bfloat16, __nv_bfloat16, true>
-          <<<grid, 256, 0, s>>>((const __nv_bfloat16*)X, (__nv_bfloat16*)Y, sh, a, T, K, N, m.lam);
+          <<<grid, 256, 0, s>>>((const __nv_bfloat16*)X, (__nv_bfloat16*)Y, sh, a, T, K, N, m.lam, bias);
     else
       simt_mm_kernel<__nv_bfloat16, __nv_bfloat16, false>
-          <<<grid, 256, 0, s>>>((const __nv_bfloat16*)X, (__nv_bfloat16*)Y, sh, a, T, K, N, m.lam);
+          <<<grid, 256, 0, s>>>((const __nv_bfloat16*)X, (__nv_bfloat16*)Y, sh, a, T, K, N, m.lam, bias);
   }
   return cudaGetLastError();
 }

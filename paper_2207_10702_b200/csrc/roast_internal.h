@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <array>
 #include <map>
 #include <string>
@@ -53,6 +54,7 @@ struct Ctx {
   int64_t identity_cursor = 0;    // IDENTITY mapping: next free base
   // device error flag (sticky)
   int32_t* d_err = nullptr;
+  int64_t* d_zero_idx = nullptr;  // device int64 0 (inside the d_err block): row 0 for biases via L
   // workspace (deterministic dM / split-K partials), grown on demand
   float* ws = nullptr;
   size_t ws_bytes = 0;
@@ -91,7 +93,12 @@ roast_status_t ensure_ws(Ctx* c, size_t bytes, cudaStream_t s);
 // ---- kernel launchers (return cudaError_t of the launch) ----------------------
 // SIMT paths (any tile geometry), T = float or bf16 storage selected by dt
 cudaError_t launch_simt_fwd(const Ctx* c, const Module& m, const void* X, void* Y, int64_t T, roast_dtype_t dt,
-                            bool transpose_w, cudaStream_t s);
+                            bool transpose_w, cudaStream_t s, const float* bias = nullptr);
+// bias backward, first half: db[j] = sum_t dY[t, j] in fp32, fixed order (slab partials
+// then an in-order sum over slabs) -> db [n]
+cudaError_t launch_colsum(const void* dY, int64_t T, int n, roast_dtype_t dt, float* partial, float* db,
+                          cudaStream_t s);
+int colsum_slabs(int64_t T, int n);
 cudaError_t launch_simt_dw(const Ctx* c, const Module& m, const void* X, const void* dY, int64_t T,
                            roast_dtype_t dt, float* ws, cudaStream_t s);
 cudaError_t launch_det_reduce(const Ctx* c, const Module& m, const float* ws, int nsplit, cudaStream_t s);
@@ -117,7 +124,8 @@ cudaError_t launch_chunk_map(const Ctx* c, const Module& m, const int64_t* rows,
 roast_status_t embed_bwd_deterministic(Ctx* c, const Module& m, const int64_t* idx, int64_t n, const float* dOut,
                                        cudaStream_t s);
 roast_status_t sm100_prepare(Ctx* c);  // build shadow tensor map
-roast_status_t sm100_fwd(Ctx* c, const Module& m, const void* X, void* Y, int64_t T, cudaStream_t s);
+roast_status_t sm100_fwd(Ctx* c, const Module& m, const void* X, void* Y, int64_t T, const float* bias,
+                         cudaStream_t s);
 roast_status_t sm100_dx(Ctx* c, const Module& m, const void* dY, void* dX, int64_t T, cudaStream_t s);
 roast_status_t sm100_dw(Ctx* c, const Module& m, const void* X, const void* dY, int64_t T, cudaStream_t s);
 

@@ -26,13 +26,18 @@ def _anchor(store):
 
 
 class _LinearFn(torch.autograd.Function):
+    """y = x W~ (+ b).  With a bias via L the bias is recovered by roast_bias_fwd and
+    added inside the forward GEMM's epilogue; its gradient (column sums of dy, scattered by
+    the L rule) is roast_bias_bwd."""
+
     @staticmethod
-    def forward(ctx, x, anchor, store, mid):
+    def forward(ctx, x, anchor, store, mid, bias_mid):
         H = store.dims[mid][1]
         x2 = x.reshape(-1, H).contiguous()
-        y = store.fwd(mid, x2)
+        b = store.bias_fwd(bias_mid) if bias_mid is not None else None
+        y = store.fwd(mid, x2, bias=b)
         ctx.save_for_backward(x2)
-        ctx.store, ctx.mid, ctx.shape = store, mid, x.shape
+        ctx.store, ctx.mid, ctx.bias_mid, ctx.shape = store, mid, bias_mid, x.shape
         return y.reshape(*x.shape[:-1], y.shape[-1])
 
     @staticmethod
@@ -45,19 +50,39 @@ class _LinearFn(torch.autograd.Function):
             dx = torch.empty_like(x2)
             store.bwd_dx(mid, dy2, dx)
         store.bwd_dm(mid, x2, dy2)          # dM += lambda g X^T dY scattered into M's slots
-        return (dx.reshape(ctx.shape) if dx is not None else None), None, None, None
+        if ctx.bias_mid is not None:
+            store.bias_bwd(ctx.bias_mid, dy2)
+        return (dx.reshape(ctx.shape) if dx is not None else None), None, None, None, None
+
+
+class RoastBias(torch.nn.Module):
+    """A bias vector of n elements recovered with L in chunks of `chunk` (reading R24:
+    registered as a 1 x n embedding, lambda = fp32(C / sqrt(fan_in)) with fan_in the
+    owning linear's in_features, the nn.Linear bias scale).  Used by RoastLinear."""
+
+    def __init__(self, store: "R.Roast", n: int, fan_in: float, chunk: int = 64):
+        super().__init__()
+        self.store = store
+        self.mid = store.embedding(1, n, chunk, fan_in)
+
+    def vector(self):
+        """The recovered bias (fp32), e.g. for a dense reference."""
+        return self.store.bias_fwd(self.mid)
 
 
 class RoastLinear(torch.nn.Module):
-    """y = x W~ with W~ (in x out) read from the shared store through the ROAST-MM mapping."""
+    """y = x W~ (+ b) with W~ (in x out) read from the shared store through the ROAST-MM
+    mapping and the optional bias b through L, both in the same GMS store."""
 
-    def __init__(self, store: "R.Roast", in_features: int, out_features: int):
+    def __init__(self, store: "R.Roast", in_features: int, out_features: int, bias: bool = False):
         super().__init__()
         self.store = store
         self.mid = store.linear(in_features, out_features)
+        self.bias = RoastBias(store, out_features, in_features) if bias else None
 
     def forward(self, x):
-        return _LinearFn.apply(x, _anchor(self.store), self.store, self.mid)
+        return _LinearFn.apply(x, _anchor(self.store), self.store, self.mid,
+                               self.bias.mid if self.bias is not None else None)
 
 
 class _EmbeddingFn(torch.autograd.Function):
@@ -88,18 +113,19 @@ class RoastEmbedding(torch.nn.Module):
 
 
 class EncoderLayer(torch.nn.Module):
-    """Post-LN BERT encoder layer whose six linears are ROAST linears in one GMS store.
-    N-operations (attention math, GELU, LayerNorm) are plain torch."""
+    """Post-LN BERT encoder layer whose six linears (and, with bias=True, their biases via L)
+    are ROAST modules in one GMS store.  N-operations (attention math, GELU, LayerNorm;
+    P:263-265) are plain torch."""
 
-    def __init__(self, store, d_model=768, d_ff=3072, heads=12):
+    def __init__(self, store, d_model=768, d_ff=3072, heads=12, bias=False):
         super().__init__()
         self.heads = heads
-        self.q = RoastLinear(store, d_model, d_model)
-        self.k = RoastLinear(store, d_model, d_model)
-        self.v = RoastLinear(store, d_model, d_model)
-        self.o = RoastLinear(store, d_model, d_model)
-        self.ff1 = RoastLinear(store, d_model, d_ff)
-        self.ff2 = RoastLinear(store, d_ff, d_model)
+        self.q = RoastLinear(store, d_model, d_model, bias)
+        self.k = RoastLinear(store, d_model, d_model, bias)
+        self.v = RoastLinear(store, d_model, d_model, bias)
+        self.o = RoastLinear(store, d_model, d_model, bias)
+        self.ff1 = RoastLinear(store, d_model, d_ff, bias)
+        self.ff2 = RoastLinear(store, d_ff, d_model, bias)
         self.ln1 = torch.nn.LayerNorm(d_model)
         self.ln2 = torch.nn.LayerNorm(d_model)
 
@@ -113,3 +139,50 @@ class EncoderLayer(torch.nn.Module):
         a = a.transpose(1, 2).reshape(B, S, d)
         x = self.ln1(x + self.o(a))
         return self.ln2(x + self.ff2(torch.nn.functional.gelu(self.ff1(x))))
+
+
+class BertEmbeddings(torch.nn.Module):
+    """Word + position + token-type embeddings, each a ROAST block embedding via L in the
+    same GMS store (NEXT #3), summed in fp32 and LayerNorm-ed, output bf16."""
+
+    def __init__(self, store, vocab=30522, d_model=768, max_pos=512, type_vocab=2, chunk=32):
+        super().__init__()
+        self.word = RoastEmbedding(store, vocab, d_model, chunk)
+        self.pos = RoastEmbedding(store, max_pos, d_model, chunk)
+        self.tok_type = RoastEmbedding(store, type_vocab, d_model, chunk)
+        self.ln = torch.nn.LayerNorm(d_model)
+
+    def forward(self, ids, types=None):                 # ids: [B, S] int64
+        B, S = ids.shape
+        pos = torch.arange(S, device=ids.device).expand(B, S)
+        types = torch.zeros_like(ids) if types is None else types
+        e = self.word(ids) + self.pos(pos.contiguous()) + self.tok_type(types)
+        return self.ln(e).to(torch.bfloat16)
+
+
+class RoastBert(torch.nn.Module):
+    """ROASTed BERT-base encoder (NEXT #3): embeddings via L, 12 post-LN layers of
+    ROAST linears with biases via L — every weight of the model except the LayerNorm
+    affines lives in ONE global array M (GMS).  Returns the last hidden states."""
+
+    def __init__(self, store, vocab=30522, d_model=768, d_ff=3072, heads=12, layers=12, max_pos=512,
+                 type_vocab=2, chunk=32, bias=True):
+        super().__init__()
+        self.emb = BertEmbeddings(store, vocab, d_model, max_pos, type_vocab, chunk)
+        self.layers = torch.nn.ModuleList([EncoderLayer(store, d_model, d_ff, heads, bias) for _ in range(layers)])
+        for m in self.layers.modules():
+            if isinstance(m, torch.nn.LayerNorm):
+                m.to(torch.bfloat16)
+
+    def forward(self, ids, types=None):
+        x = self.emb(ids, types)
+        for layer in self.layers:
+            x = layer(x)
+        return x
+
+
+def bert_param_count(vocab=30522, d_model=768, d_ff=3072, layers=12, max_pos=512, type_vocab=2, bias=True):
+    """Virtual parameters RoastBert maps into M (for sizing |M| = n / ratio)."""
+    lin = layers * (4 * d_model * d_model + 2 * d_model * d_ff)
+    b = layers * (5 * d_model + d_ff) if bias else 0
+    return lin + b + (vocab + max_pos + type_vocab) * d_model

@@ -25,7 +25,8 @@ EXPORTS = [
     "roast_register_linear", "roast_register_embedding", "roast_register_linear_seg",
     "roast_register_embedding_seg", "roast_linear_fwd", "roast_linear_bwd",
     "roast_linear_bwd_dx", "roast_linear_bwd_dm", "roast_embedding_fwd", "roast_embedding_bwd",
-    "roast_embedding_fwd_multi", "roast_embedding_bwd_multi", "roast_set_autotune", "roast_get_tuned", "roast_comm_unique_id", "roast_comm_init",
+    "roast_embedding_fwd_multi", "roast_embedding_bwd_multi", "roast_set_autotune", "roast_get_tuned",
+    "roast_linear_fwd_bias", "roast_bias_fwd", "roast_bias_bwd", "roast_comm_unique_id", "roast_comm_init",
     "roast_grad_allreduce", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step",
     "roast_get_error",
     "roast_status_str", "roast_last_error", "roast_debug_tile_map", "roast_debug_chunk_map",
@@ -75,6 +76,9 @@ def _load():
         "roast_register_linear": (st, [H, I64, I64, ctypes.POINTER(I32)]),
         "roast_register_embedding": (st, [H, I64, I32, I32, ctypes.c_double, ctypes.POINTER(I32)]),
         "roast_set_autotune": (st, [H, ctypes.c_int]),
+        "roast_linear_fwd_bias": (st, [H, I32, P, P, I64, ctypes.c_int, P, S]),
+        "roast_bias_fwd": (st, [H, I32, P, S]),
+        "roast_bias_bwd": (st, [H, I32, P, I64, ctypes.c_int, S]),
         "roast_get_tuned": (st, [H, I32, I32, I64, ctypes.POINTER(I32), ctypes.POINTER(I32)]),
         "roast_register_linear_seg": (st, [H, I64, I64, I64, I64, ctypes.POINTER(I32)]),
         "roast_register_embedding_seg": (st, [H, I64, I32, I32, ctypes.c_double, I64, I64, ctypes.POINTER(I32)]),
@@ -196,6 +200,18 @@ def lms_segments(sizes, mem_size, align=8):
         segs.append((base, size))
         base += size
     return segs
+
+
+def roast_linear_fwd_bias(h, mid, X_ptr, Y_ptr, tokens, dtype, bias_ptr, stream=0):
+    _check(_lib.roast_linear_fwd_bias(h, mid, X_ptr, Y_ptr, tokens, dtype, bias_ptr, stream), "roast_linear_fwd_bias")
+
+
+def roast_bias_fwd(h, bias_id, b_ptr, stream=0):
+    _check(_lib.roast_bias_fwd(h, bias_id, b_ptr, stream), "roast_bias_fwd")
+
+
+def roast_bias_bwd(h, bias_id, dY_ptr, tokens, dtype, stream=0):
+    _check(_lib.roast_bias_bwd(h, bias_id, dY_ptr, tokens, dtype, stream), "roast_bias_bwd")
 
 
 def roast_linear_fwd(h, mid, X_ptr, Y_ptr, tokens, dtype, stream=0):
@@ -358,14 +374,34 @@ class Roast:
         import torch
         return BF16 if t.dtype == torch.bfloat16 else FP32
 
-    def fwd(self, mid, X, Y=None, stream=None):
+    def fwd(self, mid, X, Y=None, stream=None, bias=None):
+        """Y = lambda X W~ (+ bias: fp32 [out] vector added in the epilogue)."""
         _, H, O = self.dims[mid]
         assert X.is_contiguous() and X.shape[-1] == H
         T = X.numel() // H
         if Y is None:
             Y = self.torch.empty(*X.shape[:-1], O, dtype=X.dtype, device=X.device)
-        roast_linear_fwd(self.h, mid, X.data_ptr(), Y.data_ptr(), T, self._dt(X), self._s(stream))
+        if bias is None:
+            roast_linear_fwd(self.h, mid, X.data_ptr(), Y.data_ptr(), T, self._dt(X), self._s(stream))
+        else:
+            assert bias.dtype == self.torch.float32 and bias.numel() == O and bias.is_contiguous()
+            roast_linear_fwd_bias(self.h, mid, X.data_ptr(), Y.data_ptr(), T, self._dt(X), bias.data_ptr(),
+                                  self._s(stream))
         return Y
+
+    def bias_fwd(self, bias_mid, out=None, stream=None):
+        """The bias vector (row 0 of a 1 x n embedding registered for it) recovered with L."""
+        n = self.dims[bias_mid][2]
+        if out is None:
+            out = self.torch.empty(n, dtype=self.torch.float32, device=self.M.device)
+        roast_bias_fwd(self.h, bias_mid, out.data_ptr(), self._s(stream))
+        return out
+
+    def bias_bwd(self, bias_mid, dY, stream=None):
+        """dM += lambda g * (column sums of dY) scattered through the bias's L mapping."""
+        n = self.dims[bias_mid][2]
+        assert dY.is_contiguous() and dY.shape[-1] == n
+        roast_bias_bwd(self.h, bias_mid, dY.data_ptr(), dY.numel() // n, self._dt(dY), self._s(stream))
 
     def bwd(self, mid, X, dY, dX=None, need_dx=True, stream=None):
         _, H, O = self.dims[mid]

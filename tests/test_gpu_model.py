@@ -70,3 +70,68 @@ def test_encoder_layer_gradients_match_dense_autograd():
 def store_lam(lin, M_np):
     _, H, O = lin.store.dims[lin.mid]
     return OM.LinearSpec(H, O, 64, 64, len(M_np), synth.HASH_SEED, lin.mid).lam
+
+
+def test_roast_bert_embeddings_and_biases_match_dense_autograd():
+    """NEXT #3: word / position / type embeddings and every linear's bias via L, plus the
+    linears via ROAST-MM, all in ONE GMS store; dM of the whole model vs the
+    dense fp32 model built from the recovered weights, its gradients scattered by the oracle
+    (linears: the MM rule; embeddings and biases: the L rule)."""
+    import torch
+    from oracle import embedding as OE
+    from paper_2207_10702_b200 import nn as RN, roast as R
+    torch.manual_seed(1)
+    vocab, max_pos, d, ff, heads, B, S, Z = 1000, 128, 256, 512, 4, 2, 64, 32
+    n = RN.bert_param_count(vocab, d, ff, 1, max_pos, 2, True)
+    mem = synth.compressed_size(n, 8)
+    M_np = synth.uniform(synth.SEED_M, (mem,)).astype(np.float32)
+    M = torch.tensor(M_np, device="cuda")
+    store = R.Roast(M, 64, 64, seed=synth.HASH_SEED)
+    model = RN.RoastBert(store, vocab, d, ff, heads, 1, max_pos, 2, Z, bias=True).cuda()
+    ids = torch.randint(0, vocab, (B, S), device="cuda")
+    types = torch.randint(0, 2, (B, S), device="cuda")
+    Rw = torch.randn(B, S, d, device="cuda")
+    store.zero_grad()
+    y = model(ids, types)
+    loss = (y.float() * Rw).sum()
+    loss.backward()
+    torch.cuda.synchronize()
+    dM = store.dM.cpu().numpy().astype(np.float64)
+
+    # dense fp32 reference from the recovered weights
+    emb = model.emb
+    tables = [torch.nn.Parameter(store.emb_fwd(m.mid, torch.arange(r, device="cuda")).clone())
+              for m, r in [(emb.word, vocab), (emb.pos, max_pos), (emb.tok_type, 2)]]
+    layer = model.layers[0]
+    lins = [layer.q, layer.k, layer.v, layer.o, layer.ff1, layer.ff2]
+    W = [torch.nn.Parameter(store.materialize(l.mid, torch.bfloat16).float() * store_lam(l, M_np)) for l in lins]
+    bs = [torch.nn.Parameter(l.bias.vector().clone()) for l in lins]
+    pos = torch.arange(S, device="cuda").expand(B, S)
+    e = tables[0][ids] + tables[1][pos] + tables[2][types]
+    xr = torch.nn.functional.layer_norm(e, (d,))
+
+    def lin(t, i):
+        return t @ W[i] + bs[i]
+
+    def split(t):
+        return t.reshape(B, S, heads, d // heads).transpose(1, 2)
+    a = torch.nn.functional.scaled_dot_product_attention(split(lin(xr, 0)), split(lin(xr, 1)), split(lin(xr, 2)))
+    a = a.transpose(1, 2).reshape(B, S, d)
+    h1 = torch.nn.functional.layer_norm(xr + lin(a, 3), (d,))
+    yr = torch.nn.functional.layer_norm(h1 + lin(torch.nn.functional.gelu(lin(h1, 4)), 5), (d,))
+    (yr * Rw).sum().backward()
+    parts = {k: np.zeros(mem) for k in ("linears", "biases", "embeddings")}
+    for l, w, b in zip(lins, W, bs):
+        _, H, O = store.dims[l.mid]
+        OM.LinearSpec(H, O, 64, 64, mem, synth.HASH_SEED, l.mid).scatter(w.grad.double().cpu().numpy(),
+                                                                         parts["linears"])
+        OE.EmbeddingSpec(1, O, 64, mem, synth.HASH_SEED, l.bias.mid, fan_in=H).backward(
+            np.zeros(1, np.int64), b.grad.double().cpu().numpy()[None], parts["biases"])
+    for m, r, t in [(emb.word, vocab, tables[0]), (emb.pos, max_pos, tables[1]), (emb.tok_type, 2, tables[2])]:
+        OE.EmbeddingSpec(r, d, Z, mem, synth.HASH_SEED, m.mid).backward(
+            np.arange(r, dtype=np.int64), t.grad.double().cpu().numpy(), parts["embeddings"])
+    dM_ref = sum(parts.values())
+    for k, v in parts.items():   # every family contributes a visible share of the whole
+        assert np.linalg.norm(v) > 1e-3 * np.linalg.norm(dM_ref), k
+    err = np.linalg.norm(dM - dM_ref) / np.linalg.norm(dM_ref)
+    assert err < 3e-2, err

@@ -510,3 +510,43 @@ def test_autotune_skips_graph_capture(R, torch):
     assert ctx.tuned(mid, 0, T) is None
     spec = OM.LinearSpec(H, O, 64, 64, mem, HS, mid)
     assert rel_frob(Y.float().cpu().numpy(), spec.forward(X_np, M_np, True)) <= 1e-2
+
+
+# ---------------------------------------------------------------- NEXT #3: biases via L
+@pytest.mark.parametrize("dtype,z,H,O,T,det", [("bf16", 64, 768, 3072, 300, False), ("bf16", 64, 3072, 768, 129, True),
+                                               ("fp32", 32, 256, 256, 130, False), ("bf16", 64, 256, 192, 0, False)])
+def test_linear_bias_via_L(R, torch, dtype, z, H, O, T, det):
+    """b = L(bias) bit-exact; Y = lambda X W~ + b with b added in the GEMM epilogue; the bias
+    backward = the L rule applied to the column sums of dY."""
+    mem = 60_000
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, z, z, deterministic=det)
+    mid = ctx.linear(H, O)
+    bmid = ctx.embedding(1, O, z, float(H))
+    spec = OM.LinearSpec(H, O, z, z, mem, HS, mid)
+    bspec = OE.EmbeddingSpec(1, O, z, mem, HS, bmid, fan_in=H)
+    b = ctx.bias_fwd(bmid)
+    torch.cuda.synchronize()
+    b_ref = bspec.forward(np.zeros(1, np.int64), M_np)[0]
+    assert np.array_equal(b.cpu().numpy().astype(np.float64), b_ref)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    X_np = bf16_input(synth.SEED_X, (T, H))
+    dY_np = bf16_input(synth.SEED_DY, (T, O))
+    Y = ctx.fwd(mid, to_dev(X_np, tdt), bias=b)
+    outs = []
+    for _ in range(2 if det else 1):
+        ctx.zero_grad()
+        ctx.bias_bwd(bmid, to_dev(dY_np, tdt))
+        torch.cuda.synchronize()
+        outs.append(ctx.dM.clone())
+    ctx.check()
+    if T == 0:
+        assert not outs[0].any()
+        return
+    tol = 1e-2 if dtype == "bf16" else 1e-5
+    Y_ref = spec.forward(X_np, M_np, dtype == "bf16") + b_ref[None, :]
+    assert rel_frob(Y.float().cpu().numpy(), Y_ref) <= tol
+    dM_ref = bspec.backward(np.zeros(1, np.int64), dY_np.sum(0, keepdims=True))
+    assert rel_frob(outs[0].cpu().numpy(), dM_ref) <= 1e-5
+    if det:
+        assert torch.equal(outs[0], outs[1])

@@ -26,15 +26,36 @@ N_LIN = LAYERS * (4 * D * D + 2 * D * FF)   # 84 934 656 ("~85M MM params", P:52
 
 
 class DenseLayer(torch.nn.Module):
-    def __init__(self):
+    def __init__(self, bias=False):
         super().__init__()
-        L = lambda i, o: torch.nn.Linear(i, o, bias=False, dtype=torch.bfloat16)  # noqa: E731
+        L = lambda i, o: torch.nn.Linear(i, o, bias=bias, dtype=torch.bfloat16)  # noqa: E731
         self.q, self.k, self.v, self.o, self.ff1, self.ff2 = L(D, D), L(D, D), L(D, D), L(D, D), L(D, FF), L(FF, D)
         self.ln1 = torch.nn.LayerNorm(D, dtype=torch.bfloat16)
         self.ln2 = torch.nn.LayerNorm(D, dtype=torch.bfloat16)
 
     forward = RN.EncoderLayer.forward
     heads = HEADS
+
+
+class DenseBert(torch.nn.Module):
+    """The --full model with dense torch weights: nn.Embedding word / position / type,
+    LayerNorm, 12 layers with biased bf16 nn.Linear."""
+
+    def __init__(self, vocab=30522, max_pos=512):
+        super().__init__()
+        self.word = torch.nn.Embedding(vocab, D)
+        self.pos = torch.nn.Embedding(max_pos, D)
+        self.tok_type = torch.nn.Embedding(2, D)
+        self.ln = torch.nn.LayerNorm(D)
+        self.layers = torch.nn.ModuleList([DenseLayer(bias=True) for _ in range(LAYERS)])
+
+    def forward(self, ids, types):
+        B, S = ids.shape
+        pos = torch.arange(S, device=ids.device).expand(B, S)
+        x = self.ln(self.word(ids) + self.pos(pos) + self.tok_type(types)).to(torch.bfloat16)
+        for layer in self.layers:
+            x = layer(x)
+        return x
 
 
 def main():
@@ -45,6 +66,11 @@ def main():
     ap.add_argument("--seq", type=int, default=128)
     ap.add_argument("--ratio", type=float, default=100)
     ap.add_argument("--dense", action="store_true")
+    ap.add_argument("--graph", type=int, default=1, choices=[0, 1],
+                    help="capture the whole training step (fwd + bwd + all-reduce + update) in a CUDA graph")
+    ap.add_argument("--profile", action="store_true")
+    ap.add_argument("--full", action="store_true",
+                    help="whole BERT-base: word/pos/type embeddings and biases via L too (NEXT #3)")
     args = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -58,25 +84,34 @@ def main():
     T = B * S
     x = torch.randn(B, S, D, device=dev, dtype=torch.bfloat16)
     proj = torch.randn(B, S, D, device=dev, dtype=torch.bfloat16)   # L = <proj, y> / T
+    ids = torch.randint(0, 30522, (B, S), device=dev)
+    types = torch.randint(0, 2, (B, S), device=dev)
+    n_virtual = RN.bert_param_count() if args.full else N_LIN
     if args.dense:
-        model = torch.nn.Sequential(*[DenseLayer() for _ in range(LAYERS)]).to(dev)
+        if args.full:
+            model = DenseBert().to(dev)
+        else:
+            model = torch.nn.Sequential(*[DenseLayer() for _ in range(LAYERS)]).to(dev)
         opt = torch.optim.SGD(model.parameters(), lr=1e-4)
         store = None
     else:
-        mem = synth.compressed_size(N_LIN, args.ratio)
+        mem = synth.compressed_size(n_virtual, args.ratio)
         M = (torch.rand(mem, device=dev) * 2 - 1).contiguous()
         store = R.Roast(M, 64, 64, seed=synth.HASH_SEED)
         dp.init_comm(store, rank, world, device=dev)
-        model = torch.nn.Sequential(*[RN.EncoderLayer(store, D, FF, HEADS) for _ in range(LAYERS)]).to(dev)
-        for m in model.modules():
-            if isinstance(m, torch.nn.LayerNorm):
-                m.to(torch.bfloat16)
+        if args.full:
+            model = RN.RoastBert(store).to(dev)
+        else:
+            model = torch.nn.Sequential(*[RN.EncoderLayer(store, D, FF, HEADS) for _ in range(LAYERS)]).to(dev)
+            for m in model.modules():
+                if isinstance(m, torch.nn.LayerNorm):
+                    m.to(torch.bfloat16)
 
     def step():
-        y = model(x)
+        y = model(ids, types) if args.full else model(x)
         loss = (y * proj).float().sum() / T
         if store is None:
-            opt.zero_grad(set_to_none=True)
+            opt.zero_grad(set_to_none=False)
             loss.backward()
             if world > 1:
                 import torch.distributed as dist
@@ -90,16 +125,34 @@ def main():
             store.sgd(1e-4)                # M -= lr dM; shadow refresh (same kernel)
         return loss
 
-    for _ in range(args.warmup):
-        step()
+    side = torch.cuda.Stream(device=dev) if args.graph else torch.cuda.current_stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):          # eager warm-up (also allocates grads / lazy state)
+        for _ in range(args.warmup):
+            step()
+    torch.cuda.current_stream().wait_stream(side)
     torch.cuda.synchronize()
+    if args.profile and rank == 0:         # top GPU kernels of one eager step
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step()
+            torch.cuda.synchronize()
+        print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25), file=sys.stderr)
+    run = step
+    if args.graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            static_loss = step()
+        run = lambda: (g.replay(), static_loss)[1]   # noqa: E731
+        run()
+        torch.cuda.synchronize()
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(args.steps):
-        loss = step()
+        loss = run()
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / args.steps
@@ -109,7 +162,9 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     if rank == 0:
-        print(json.dumps(dict(config="C3 BERT-base encoder step, 72 linears in one GMS M",
+        print(json.dumps(dict(config="C3 BERT-base encoder step, 72 linears in one GMS M" +
+                              (" + word/pos/type embeddings and biases via L" if args.full else ""),
+                              virtual_params=n_virtual, cuda_graph=bool(args.graph),
                               impl="dense-torch" if args.dense else "roast", ratio=args.ratio,
                               mem_size=None if store is None else store.mem_size, n_gpus=world,
                               tokens_per_gpu=T, ms_per_step=ms, tokens_per_s=world * T / (ms * 1e-3),
