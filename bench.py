@@ -234,9 +234,21 @@ def run_gpu(args):
             else:
                 fn()
         ctx.zero_grad()
-        rec("fwd", lambda: ctx.fwd(l1, Xin, Y1))
-        rec("fwd", lambda: ctx.fwd(l2, Y1, Y2))
-        if args.streams == 2 and not record:
+        if args.chain and not record:     # both forward GEMMs in one persistent launch
+            ctx.fwd_chain(l1, l2, Xin, Y1, Y2)
+        else:
+            rec("fwd", lambda: ctx.fwd(l1, Xin, Y1))
+            rec("fwd", lambda: ctx.fwd(l2, Y1, Y2))
+        if args.streams == 2 and args.chain == 2 and not record:
+            side.wait_stream(cur)
+            with torch.cuda.stream(side):
+                ctx.bwd_dm(l2, Y1, dY2in)
+            ctx.bwd_dx_chain(l1, l2, dY2in, dY1, dX)   # dY1 and dX in one launch
+            side.wait_stream(cur)
+            with torch.cuda.stream(side):
+                ctx.bwd_dm(l1, Xin, dY1)
+            cur.wait_stream(side)
+        elif args.streams == 2 and not record:
             side.wait_stream(cur)
             ctx.bwd_dx(l2, dY2in, dY1)
             e_dy1 = torch.cuda.Event()
@@ -259,6 +271,9 @@ def run_gpu(args):
         ctx.zero_grad()
         ctx.fwd(l1, X, Y1)
         ctx.fwd(l2, Y1, Y2)
+        if args.chain:
+            ctx.fwd_chain(l1, l2, X, Y1, Y2)            # plans the chained schedules eagerly
+            ctx.bwd_dx_chain(l1, l2, dY2, dY1, dX)
         ctx.bwd_dx(l2, dY2, dY1)
         ctx.bwd_dm(l2, Y1, dY2)
         ctx.bwd_dx(l1, dY1, dX)
@@ -435,6 +450,7 @@ def run_gpu(args):
                     l2="flushed between timed steps (256 MB write outside the events)",
                     dm_mode="deterministic" if args.deterministic else "atomic",
                     streams=args.streams, cuda_graph=bool(args.graph),
+                    chain=["off", "forward pair", "forward + dX pairs"][args.chain],
                     autotune=["makespan model", "inference-optimal", "training-optimal"][args.autotune],
                     tuned={f"L{i + 1}.{k}": ctx.tuned(mid, j, T) for i, mid in enumerate((l1, l2))
                            for j, k in enumerate(("fwd", "dx", "dm"))},
@@ -468,6 +484,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--streams", type=int, default=2, choices=[1, 2])
     ap.add_argument("--graph", type=int, default=1, choices=[0, 1])
+    ap.add_argument("--chain", type=int, default=1, choices=[0, 1, 2],
+                    help="1: forward GEMM pair in one launch (roast_linear_fwd_chain); 2: also the dX pair")
     ap.add_argument("--autotune", type=int, default=2, choices=[0, 1, 2],
                     help="kernel-config autotuner: 0 makespan model, 1 inference-optimal, 2 training-optimal")
     args = ap.parse_args()

@@ -152,6 +152,22 @@ roast_status_t roast_linear_fwd(roast_t h, int32_t id, const void* d_X, void* d_
 roast_status_t roast_linear_fwd_bias(roast_t h, int32_t id, const void* d_X, void* d_Y, int64_t tokens,
                                      roast_dtype_t dt, const float* d_bias, roast_stream_t stream);
 
+/* Two dependent linears in ONE persistent tcgen05 launch (C2's MLP block: in -> a -> b).
+ *   fwd_chain:    Y_a = lambda_a X W~_a (+ bias_a),  Y_b = lambda_b Y_a W~_b (+ bias_b)
+ *   bwd_dx_chain: dY_a = lambda_b dY_b W~_b^T,       dX = lambda_a dY_a W~_a^T
+ * Same results as the two single calls (each output rounded once); Y_a / dY_a are still
+ * written (the backward needs them).  The second GEMM's work units start on CTA pairs the
+ * first leaves idle and wait per output tile of the first (ready counters), filling the
+ * quantisation gaps each launch has alone.  Shapes that are not on the tcgen05 path, or for
+ * which the scheduler predicts no gain, run as two launches.  The first call for a shape
+ * must not be under stream capture to chain (it plans and uploads a static schedule).
+ * Requires out_features(a) == in_features(b).  Errors as roast_linear_fwd / _bwd_dx. */
+roast_status_t roast_linear_fwd_chain(roast_t h, int32_t id_a, int32_t id_b, const void* d_X, void* d_Y_a,
+                                      void* d_Y_b, int64_t tokens, roast_dtype_t dt, const float* d_bias_a,
+                                      const float* d_bias_b, roast_stream_t stream);
+roast_status_t roast_linear_bwd_dx_chain(roast_t h, int32_t id_a, int32_t id_b, const void* d_dY_b, void* d_dY_a,
+                                         void* d_dX, int64_t tokens, roast_dtype_t dt, roast_stream_t stream);
+
 /* Bias vectors via L ("ROAST uses L to implement ... bias vectors").  A bias of
  * n elements is row 0 of an embedding registered as (num_rows 1, dim n, chunk Z,
  * fan_in = the owning layer's in_features, reading R24).

@@ -136,6 +136,8 @@ roast_status_t roast_destroy(roast_t h) {
   cudaFree(c->ws);
   cudaFree(c->opt_s1);
   cudaFree(c->opt_s2);
+  for (auto& kv : c->chain_plans) cudaFree(kv.second.first);
+  cudaFree(c->chain_flags);
   comm_destroy(c);
   delete c;
   return ROAST_OK;
@@ -332,6 +334,49 @@ roast_status_t roast_linear_fwd_bias(roast_t h, int32_t id, const void* X, void*
   ROAST_CUDA_CHECK(launch_simt_fwd(c, *m, X, Y, T, dt, false, s, bias));
   c->launches++;
   return ROAST_OK;
+}
+
+roast_status_t roast_linear_fwd_chain(roast_t h, int32_t id_a, int32_t id_b, const void* X, void* Y_a, void* Y_b,
+                                      int64_t T, roast_dtype_t dt, const float* bias_a, const float* bias_b,
+                                      roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module *ma, *mb;
+  roast_status_t st = get_module(c, id_a, kLinear, &ma);
+  if (st) return st;
+  if ((st = get_module(c, id_b, kLinear, &mb))) return st;
+  if (ma->O != mb->H) return fail(ROAST_ERR_SHAPE, "chain: out_features of a != in_features of b");
+  if (T < 0) return fail(ROAST_ERR_SHAPE, "tokens < 0");
+  if (T > 0 && (!X || !Y_a || !Y_b)) return fail(ROAST_ERR_CONFIG, "null X / Y_a / Y_b");
+  if ((reinterpret_cast<uintptr_t>(bias_a) | reinterpret_cast<uintptr_t>(bias_b)) & 15)
+    return fail(ROAST_ERR_CONFIG, "bias must be 16-byte aligned");
+  if (T == 0) return ROAST_OK;
+  const cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (dt == ROAST_BF16 && use_sm100(c, *ma) && use_sm100(c, *mb)) {
+    st = sm100_chain(c, *ma, *mb, X, Y_a, Y_b, T, false, bias_a, bias_b, s);
+    if (st != ROAST_ERR_UNSUPPORTED) return st;
+  }
+  if ((st = roast_linear_fwd_bias(h, id_a, X, Y_a, T, dt, bias_a, stream))) return st;
+  return roast_linear_fwd_bias(h, id_b, Y_a, Y_b, T, dt, bias_b, stream);
+}
+
+roast_status_t roast_linear_bwd_dx_chain(roast_t h, int32_t id_a, int32_t id_b, const void* dY_b, void* dY_a,
+                                         void* dX, int64_t T, roast_dtype_t dt, roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module *ma, *mb;
+  roast_status_t st = get_module(c, id_a, kLinear, &ma);
+  if (st) return st;
+  if ((st = get_module(c, id_b, kLinear, &mb))) return st;
+  if (ma->O != mb->H) return fail(ROAST_ERR_SHAPE, "chain: out_features of a != in_features of b");
+  if (T < 0) return fail(ROAST_ERR_SHAPE, "tokens < 0");
+  if (T > 0 && (!dY_b || !dY_a || !dX)) return fail(ROAST_ERR_CONFIG, "null dY_b / dY_a / dX");
+  if (T == 0) return ROAST_OK;
+  const cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (dt == ROAST_BF16 && use_sm100(c, *ma) && use_sm100(c, *mb)) {
+    st = sm100_chain(c, *mb, *ma, dY_b, dY_a, dX, T, true, nullptr, nullptr, s);
+    if (st != ROAST_ERR_UNSUPPORTED) return st;
+  }
+  if ((st = roast_linear_bwd_dx(h, id_b, dY_b, dY_a, T, dt, stream))) return st;
+  return roast_linear_bwd_dx(h, id_a, dY_a, dX, T, dt, stream);
 }
 
 roast_status_t roast_bias_fwd(roast_t h, int32_t bias_id, float* b, roast_stream_t stream) {

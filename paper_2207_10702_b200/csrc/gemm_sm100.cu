@@ -96,6 +96,16 @@ struct Params {
   long long* prof;      // debug (ROAST_PROF): per-CTA cycle counters, else null
   int epi;              // 0: TMA bulk store / reduce from staging; 1: coalesced st.global / red.global.v4
   int dw3d;             // DW operands loaded as one 3-D TMA box per operand (else 64x64 2-D boxes)
+  // chain mode (FWD / DX only; set in the first problem's Params): two GEMMs in one persistent
+  // launch, problem 1's A = problem 0's output.  Each pair walks its own static unit list
+  // sched[pair * sched_len + i] = prob << 24 | unit (-1 = end), every problem-0 unit before any
+  // problem-1 unit (so the waits below cannot deadlock).  flags[u0] counts the epilogue warps
+  // whose TMA stores of problem-0 unit u0 are complete; problem 1 loads k-block kb of m-block mb
+  // only after flags[mb * n_tiles0 + kb / 4] == 4 * CG.
+  int chain;
+  const int32_t* sched;
+  int sched_len;
+  int* flags;
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -237,6 +247,18 @@ __host__ __device__ constexpr uint32_t make_idesc(int a_mn_major, int b_mn_major
          (uint32_t(BN >> 3) << 17) | (uint32_t(m >> 4) << 24);
 }
 
+// spin until *flag >= target (acquire), then order the async proxy (TMA loads) after it
+__device__ __forceinline__ void wait_ready(const int* flag, int target) {
+  int v;
+  for (uint32_t spins = 0;; ++spins) {
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v >= target) break;
+    if (spins > (1u << 26)) __trap();   // ~4 s: a broken schedule fails loudly instead of hanging
+    __nanosleep(64);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 __device__ __forceinline__ void decode_unit(const Params& p, int u, int& mb, int& nb, int& split) {
   split = u / (p.m_tiles * p.n_tiles);
   int r = u - split * p.m_tiles * p.n_tiles;
@@ -245,10 +267,12 @@ __device__ __forceinline__ void decode_unit(const Params& p, int u, int& mb, int
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int MODE, int CG, int WM>
+template <int MODE, int CG, int WM, bool CHAIN = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     roast_mm_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                   const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ WMaps wmaps, const Params p) {
+                   const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ WMaps wmaps,
+                   const __grid_constant__ Params p0, const __grid_constant__ CUtensorMap mapA1,
+                   const __grid_constant__ CUtensorMap mapOut1, const __grid_constant__ Params p1) {
   using C = Cfg<CG, WM>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -268,11 +292,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   long long prof_epi[4] = {0, 0, 0, 0};   // epilogue: TMEM load+wait, staging wait, STS, fence+issue
   const long long t_start = clock64();
   uint64_t g_start = 0;
-  if (p.prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+  if (p0.prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
   const bool leader = rank == 0;
   const int pair = blockIdx.x / CG;
   const int npairs = gridDim.x / CG;
+  // i-th unit of this pair: round-robin over one problem, or the pair's chain schedule
+  auto unit_at = [&](int i, int& prob, int& u) -> bool {
+    if (!CHAIN) {
+      prob = 0;
+      u = pair + i * npairs;
+      return u < p0.units;
+    }
+    if (i >= p0.sched_len) return false;
+    const int code = __ldg(p0.sched + pair * p0.sched_len + i);
+    if (code < 0) return false;
+    prob = code >> 24;
+    u = code & 0xFFFFFF;
+    return true;
+  };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -285,6 +323,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_map(&mapA);
+    if (CHAIN) prefetch_map(&mapA1);
     if (MODE == DW) prefetch_map(&mapB);
   }
   if (warp == 2) {
@@ -314,7 +353,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // unit hides behind the k-blocks already buffered in the ring.
     int s = 0;
     uint32_t ph = 0;
-    for (int u = pair; u < p.units; u += npairs) {
+    for (int it = 0;; ++it) {
+      int prob, u;
+      if (!unit_at(it, prob, u)) break;
+      const Params& p = (CHAIN && prob) ? p1 : p0;
+      const CUtensorMap* mA = (CHAIN && prob) ? &mapA1 : &mapA;
       int mb, nb, split;
       decode_unit(p, u, mb, nb, split);
       const int kb0 = split * p.kb_per_split;
@@ -353,14 +396,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t fb = CG == 2 ? map_to_rank(smem_u32(&full[s]), 0) : smem_u32(&full[s]);
             if (leader) mbar_expect_tx(&full[s], tx);
             if (MODE == DW && p.dw3d) {
-              tma_load_3d<CG>(&mapA, a, fb, 0, kb * BK, row0 >> 6);
+              tma_load_3d<CG>(mA, a, fb, 0, kb * BK, row0 >> 6);
               tma_load_3d<CG>(&mapB, b, fb, 0, kb * BK, (nb * BN + j0 * 64) >> 6);
             } else if (MODE == DW) {
-              for (int i = 0; i < m_sub; ++i) tma_load_2d<CG>(&mapA, a + i * 8192, fb, row0 + i * 64, kb * BK);
+              for (int i = 0; i < m_sub; ++i) tma_load_2d<CG>(mA, a + i * 8192, fb, row0 + i * 64, kb * BK);
               for (int j = j0; j < j1; ++j)
                 tma_load_2d<CG>(&mapB, b + (j - j0) * 8192, fb, nb * BN + j * 64, kb * BK);
             } else {
-              tma_load_2d<CG>(&mapA, a, fb, kb * BK, row0);
+              // chain: these 64 columns of A are problem 0's output tile (mb, kb / 4)
+              if (CHAIN && prob == 1 && (kb & 3) == 0) wait_ready(p0.flags + mb * p0.n_tiles + (kb >> 2), 4 * CG);
+              tma_load_2d<CG>(mA, a, fb, kb * BK, row0);
               const int32_t* cc = sCoord + (kb - kc) * 4;
               for (int j = j0; j < j1; ++j) {
                 // FWD: tile (x = kb, y = nb*4 + j); DX: tile (x = nb*4 + j, y = kb).
@@ -387,7 +432,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t ph = 0;
       int acc = 0;          // WM = 1: double-buffered accumulator index
       uint32_t aph = 0;
-      for (int u = pair; u < p.units; u += npairs) {
+      for (int it = 0;; ++it) {
+        int prob, u;
+        if (!unit_at(it, prob, u)) break;
+        const Params& p = (CHAIN && prob) ? p1 : p0;
         int mb, nb, split;
         decode_unit(p, u, mb, nb, split);
         const int kb0 = split * p.kb_per_split;
@@ -438,7 +486,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int stg = 0;   // staging buffer counter (double buffer per warp)
     int acc = 0;
     uint32_t aph = 0;
-    for (int u = pair; u < p.units; u += npairs) {
+    for (int it = 0;; ++it) {
+      int prob, u;
+      if (!unit_at(it, prob, u)) break;
+      const Params& p = (CHAIN && prob) ? p1 : p0;
+      const CUtensorMap* mO = (CHAIN && prob) ? &mapOut1 : &mapOut;
       int mb, nb, split;
       decode_unit(p, u, mb, nb, split);
       const int n_valid = min(BN, p.N - nb * BN);
@@ -560,7 +612,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (MODE != DW) {
               const int x0 = nb * BN + c * 64, y0 = row_base + q * 32;
               asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                               reinterpret_cast<uint64_t>(&mapOut)),
+                               reinterpret_cast<uint64_t>(mO)),
                            "r"(x0), "r"(y0), "r"(sb)
                            : "memory");
             } else if (row_base + q * 32 < p.M) {   // warps past the last hash-tile row write nothing
@@ -568,7 +620,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const int y0 = int(tb >> 6) + ((row_base + q * 32) & 63);
               if (p.ws)   // deterministic: plain store into the per-tile workspace [.. x 64] fp32
                 asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                                 reinterpret_cast<uint64_t>(&mapOut)),
+                                 reinterpret_cast<uint64_t>(mO)),
                              "r"(x0), "r"(y0), "r"(sb)
                              : "memory");
               else        // fast: TMA reduce-add into dM in L2 through the 32-byte-phase view of dM
@@ -595,6 +647,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader0 + uint32_t(acc * 8));
+      if (CHAIN && prob == 0) {
+        // publish this warp's 32 rows of the problem-0 tile: writes complete, then release
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p0.flags + u) : "memory");
+        }
+        __syncwarp();
+      }
       if (WM == 1) acc ^= 1;
       if (acc == 0) aph ^= 1;
     }
@@ -602,8 +663,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncwarp();
   }
 
-  if (p.prof && lane == 0) {
-    long long* o = p.prof + blockIdx.x * 8;
+  if (p0.prof && lane == 0) {
+    long long* o = p0.prof + blockIdx.x * 8;
     if (warp == 0) {
       o[5] = clock64() - t_start;
       uint64_t g_end;
@@ -694,18 +755,19 @@ int cta_group() {
   return cg;
 }
 
-template <int MODE, int CG, int WM>
+template <int MODE, int CG, int WM, bool CHAIN = false>
 roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o, const WMaps& w,
-                         const Params& p, cudaStream_t s) {
+                         const Params& p, const CUtensorMap& a1, const CUtensorMap& o1, const Params& p1,
+                         int grid_pairs, cudaStream_t s) {
   using C = Cfg<CG, WM>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
-        cudaFuncSetAttribute(roast_mm_sm100<MODE, CG, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(roast_mm_sm100<MODE, CG, WM, CHAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(smem)");
     attr = true;
   }
-  const int pairs = std::min(p.units, num_sms() / CG);
+  const int pairs = grid_pairs > 0 ? grid_pairs : std::min(p.units, num_sms() / CG);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(pairs * CG));
   cfg.blockDim = dim3(NUM_THREADS);
@@ -719,14 +781,15 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
   cfg.attrs = at;
   cfg.numAttrs = 1;
   static long long* prof = nullptr;
-  Params pp = p;
+  Params pp = p, pp1 = p1;
   if (const char* e = getenv("ROAST_EPI")) pp.epi = atoi(e);
   if (getenv("ROAST_PROF")) {
     if (!prof) cudaMallocManaged(&prof, sizeof(long long) * 8 * 512);
     cudaMemset(prof, 0, sizeof(long long) * 8 * 512);
     pp.prof = prof;
+    pp1.prof = prof;
   }
-  cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mm_sm100<MODE, CG, WM>, a, b, o, w, pp);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mm_sm100<MODE, CG, WM, CHAIN>, a, b, o, w, pp, a1, o1, pp1);
   if (e != cudaSuccess) return cuda_fail(e, "roast_mm_sm100 launch");
   if (pp.prof) {
     cudaDeviceSynchronize();
@@ -748,8 +811,9 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
 template <int MODE>
 roast_status_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o, const WMaps& w, Params p,
                       int wm, cudaStream_t s) {
-  if (cta_group() == 1) return launch_cg<MODE, 1, 1>(a, b, o, w, p, s);
-  return wm == 2 ? launch_cg<MODE, 2, 2>(a, b, o, w, p, s) : launch_cg<MODE, 2, 1>(a, b, o, w, p, s);
+  if (cta_group() == 1) return launch_cg<MODE, 1, 1>(a, b, o, w, p, a, o, p, 0, s);
+  return wm == 2 ? launch_cg<MODE, 2, 2>(a, b, o, w, p, a, o, p, 0, s)
+                 : launch_cg<MODE, 2, 1>(a, b, o, w, p, a, o, p, 0, s);
 }
 
 }  // namespace sm100
@@ -910,6 +974,150 @@ roast_status_t sm100_dx(Ctx* c, const Module& m, const void* dY, void* dX, int64
   return run_tok_major(c, m, dY, dX, T, int(m.H), int(m.O), m.d_coord_yx, m.nx, true, nullptr, s);
 }
 
+// ---- chained pair of GEMMs ------------------------------------------------------
+// Problem 0 (N0 = 4 * 64 * n_tiles0 output columns) feeds problem 1 as its A operand
+// (K1 = N0).  Alone, each launch is quantised on its own: C2's 3072 -> 768 GEMM has 48
+// units for 74 CTA pairs and the 768 -> 3072 one 192 units (2.6 rounds).  Chained, the
+// second GEMM's units start on the pairs the first leaves idle and stream their K loop
+// behind the first GEMM's output tiles (per-tile ready counters).  The static per-pair
+// schedule comes from a list-scheduling simulation in k-block time units (an MMA k-block
+// of a WM = 2 unit ~ 1024 clk; per-unit epilogue exposure EPI); every pair runs all its
+// problem-0 units before any problem-1 unit, which keeps the waits deadlock-free.
+namespace {
+struct ChainPlan {
+  std::vector<int32_t> sched;   // [pairs][len], -1 padded
+  int len = 0;
+  double makespan = 0, sequential = 0;
+};
+
+ChainPlan plan_chain(int m_tiles, int nt0, int kb0, int nt1, int kb1, int npairs) {
+  const double EPI = 5.0, LAT = 1.0;
+  const int units0 = m_tiles * nt0, units1 = m_tiles * nt1;
+  const double c0 = kb0 + EPI, c1 = kb1 + EPI;
+  ChainPlan best;
+  best.makespan = 1e30;
+  best.sequential = double((units0 + npairs - 1) / npairs) * c0 + double((units1 + npairs - 1) / npairs) * c1;
+  const int n2 = std::min(npairs, units1);   // pairs that run problem-1 units
+  // problem-0 units in m-major or n-major order (n-major completes the K groups every
+  // problem-1 unit needs first, so all of them can stream early); k2 = problem-0 units on
+  // each problem-1 pair before its problem-1 work
+  for (int order = 0; order < 2; ++order)
+    for (int k2 = 0; k2 <= 8; ++k2) {
+      std::vector<double> free_t(npairs, 0.0), fin0(units0, 0.0);
+      std::vector<int> cnt0(npairs, 0);
+      std::vector<std::vector<int32_t>> lists(npairs);
+      for (int i = 0; i < units0; ++i) {
+        const int u = order == 0 ? i : (i % m_tiles) * nt0 + i / m_tiles;
+        int pick = -1;
+        for (int q = 0; q < npairs; ++q) {
+          if (q < n2 && cnt0[q] >= k2 && n2 < npairs) continue;
+          if (pick < 0 || free_t[q] < free_t[pick]) pick = q;
+        }
+        fin0[u] = free_t[pick] + c0;
+        free_t[pick] = fin0[u];
+        cnt0[pick]++;
+        lists[pick].push_back(u);
+      }
+      for (int u = 0; u < units1; ++u) {
+        const int mb = u / nt1;
+        int pick = 0;
+        for (int q = 1; q < n2; ++q)
+          if (free_t[q] < free_t[pick]) pick = q;
+        double t = free_t[pick];
+        for (int g = 0; g < nt0; ++g) t = std::max(t, fin0[mb * nt0 + g] + LAT) + double(kb1) / nt0;
+        free_t[pick] = t + EPI;
+        lists[pick].push_back((1 << 24) | u);
+      }
+      const double mk = *std::max_element(free_t.begin(), free_t.end());
+      if (mk < best.makespan - 1e-9) {
+        best.makespan = mk;
+        best.len = 0;
+        for (auto& l : lists) best.len = std::max<int>(best.len, int(l.size()));
+        best.sched.assign(size_t(npairs) * best.len, -1);
+        for (int q = 0; q < npairs; ++q)
+          for (size_t i = 0; i < lists[q].size(); ++i) best.sched[size_t(q) * best.len + i] = lists[q][i];
+      }
+    }
+  return best;
+}
+}  // namespace
+
+roast_status_t sm100_chain(Ctx* c, const Module& m0, const Module& m1, const void* A0, void* out0, void* out1,
+                           int64_t T, bool dx, const float* bias0, const float* bias1, cudaStream_t s) {
+  if (!supported(c, m0) || !supported(c, m1) || cta_group() != 2 || T >= (int64_t(1) << 31) || T <= 0)
+    return ROAST_ERR_UNSUPPORTED;
+  if (getenv("ROAST_NO_CHAIN")) return ROAST_ERR_UNSUPPORTED;
+  // geometry: FWD problem 0 = m0 (K = H0, N = O0), problem 1 = m1 (K = H1 = O0, N = O1);
+  //           DX  problem 0 = m0 (K = O0, N = H0), problem 1 = m1 (K = O1 = H0, N = H1)
+  const int N0 = int(dx ? m0.H : m0.O), K0 = int(dx ? m0.O : m0.H);
+  const int N1 = int(dx ? m1.H : m1.O), K1 = int(dx ? m1.O : m1.H);
+  if (K1 != N0 || N0 % BN) return ROAST_ERR_UNSUPPORTED;   // problem-0 tiles must cover whole 4-k-block groups
+  constexpr int WMC = 2;
+  const int pairs = num_sms() / 2;
+  const int m_tiles = int((T + BM * 2 * WMC - 1) / (BM * 2 * WMC));
+  const int nt0 = N0 / BN, nt1 = (N1 + BN - 1) / BN;
+  const std::array<int64_t, 6> key{dx ? 1 : 0, m0.H, m0.O, m1.H, m1.O, T};
+  auto it = c->chain_plans.find(key);
+  if (it == c->chain_plans.end()) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+      return ROAST_ERR_UNSUPPORTED;   // planning allocates; plan on an eager call first
+    ChainPlan plan = plan_chain(m_tiles, nt0, K0 / BK, nt1, K1 / BK, pairs);
+    int32_t* d = nullptr;
+    if (plan.makespan < 0.97 * plan.sequential) {
+      ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&d), plan.sched.size() * sizeof(int32_t)));
+      ROAST_CUDA_CHECK(cudaMemcpy(d, plan.sched.data(), plan.sched.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    it = c->chain_plans.emplace(key, std::make_pair(d, plan.len)).first;
+    const int64_t need = int64_t(m_tiles) * nt0;
+    if (d && c->chain_flags_n < need) {
+      cudaFree(c->chain_flags);
+      c->chain_flags = nullptr;
+      c->chain_flags_n = 0;
+      ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->chain_flags), need * sizeof(int)));
+      c->chain_flags_n = need;
+    }
+  }
+  if (!it->second.first) return ROAST_ERR_UNSUPPORTED;
+  roast_status_t st = sm100_prepare(c);
+  if (st) return st;
+  auto prob = [&](const Module& m, const void* A, void* out, int N, int K, bool is_dx, const float* bias, Params& p,
+                  CUtensorMap& ma, CUtensorMap& mo) -> roast_status_t {
+    roast_status_t r = make_map_2d(&ma, A, uint64_t(K), uint64_t(T), uint64_t(K) * 2, BK, BM * WMC);
+    if (r) return r;
+    r = make_map_2d(&mo, out, uint64_t(N), uint64_t(T), uint64_t(N) * 2, 64, 32);
+    if (r) return r;
+    p = base_params(c, m, T);
+    p.M = int(T);
+    p.N = N;
+    p.K = K;
+    p.m_tiles = m_tiles;
+    p.n_tiles = (N + BN - 1) / BN;
+    p.k_blocks = K / BK;
+    p.kb_per_split = p.k_blocks;
+    p.units = p.m_tiles * p.n_tiles;
+    p.out = reinterpret_cast<__nv_bfloat16*>(out);
+    p.bias = is_dx ? nullptr : bias;
+    p.coord = is_dx ? m.d_coord_yx : m.d_coord_xy;
+    p.coord_ld = is_dx ? m.nx : m.ny;
+    return ROAST_OK;
+  };
+  Params p0, p1;
+  CUtensorMap a0, o0, a1, o1;
+  if ((st = prob(m0, A0, out0, N0, K0, dx, bias0, p0, a0, o0))) return st;
+  if ((st = prob(m1, out0, out1, N1, K1, dx, bias1, p1, a1, o1))) return st;
+  p0.chain = 1;
+  p0.sched = it->second.first;
+  p0.sched_len = it->second.second;
+  p0.flags = c->chain_flags;
+  ROAST_CUDA_CHECK(cudaMemsetAsync(c->chain_flags, 0, size_t(p0.units) * sizeof(int), s));
+  const WMaps& w = *reinterpret_cast<const WMaps*>(c->tmap_shadow);
+  st = dx ? launch_cg<DX, 2, WMC, true>(a0, a0, o0, w, p0, a1, o1, p1, pairs, s)
+          : launch_cg<FWD, 2, WMC, true>(a0, a0, o0, w, p0, a1, o1, p1, pairs, s);
+  if (!st) c->launches++;
+  return st;
+}
+
 // makespan model for DW: cost of (WM, split-K over tokens) = ceil(units / slots) * WM / (eff * s);
 // eff = TMA-box-rate bound MMA share (4 boxes / 512 clk for WM 1, 6 / 1024 for WM 2)
 static double dw_cost(const Module& m, int64_t T, int w, int sp) {
@@ -1038,10 +1246,10 @@ roast_status_t sm100_dw(Ctx* c, const Module& m, const void* X, const void* dY, 
     ROAST_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&save), c->mem_size * sizeof(float), s));
     ROAST_CUDA_CHECK(cudaMemcpyAsync(save, c->dM, c->mem_size * sizeof(float), cudaMemcpyDeviceToDevice, s));
     float best = 1e30f;
+    const int kbt = int((T + BK - 1) / BK);
     for (int w = 1; w <= wmax; ++w)
-      for (int k = 0; k < 2; ++k) {   // the model's two best split-K counts per WM
-        const int sp = dw_best_splits(m, T, w, k);
-        if (k == 1 && sp == dw_best_splits(m, T, w, 0)) continue;
+      for (int sp : {1, 2, 3, 4, 6, 8, 12, 16}) {   // the model ignores epilogue exposure: time them all
+        if (sp > kbt) continue;
         const float ms = time_candidate([&] { return dw_launch(c, m, X, dY, T, w, sp, s); }, s);
         if (ms >= 0.f && ms < best) {
           best = ms;

@@ -74,6 +74,12 @@ struct Ctx {
   // kernel-configuration autotuner (roast_set_autotune): (kernel, H, O, tokens) -> (WM, split-K)
   int autotune = 0;
   std::map<std::array<int64_t, 4>, std::pair<int, int>> tuned;
+  // chained GEMM pairs (roast_linear_fwd_chain / roast_linear_bwd_dx_chain): per-shape static
+  // schedules on the device (pointer, per-pair length; null = chaining does not pay) and the
+  // ready counters of the first GEMM's output tiles
+  std::map<std::array<int64_t, 6>, std::pair<int32_t*, int>> chain_plans;
+  int* chain_flags = nullptr;
+  int64_t chain_flags_n = 0;
 };
 
 // error reporting (thread-local detail string)
@@ -126,6 +132,12 @@ roast_status_t embed_bwd_deterministic(Ctx* c, const Module& m, const int64_t* i
 roast_status_t sm100_prepare(Ctx* c);  // build shadow tensor map
 roast_status_t sm100_fwd(Ctx* c, const Module& m, const void* X, void* Y, int64_t T, const float* bias,
                          cudaStream_t s);
+// two dependent GEMMs in one persistent launch: FWD Y_a = X W_a, Y_b = Y_a W_b (dx = false) or
+// DX dY_a = dY_b W_b^T, dX = dY_a W_a^T (dx = true; m0 = the layer whose dX is computed first).
+// Returns ROAST_ERR_UNSUPPORTED when the shapes are not on the tcgen05 path or chaining would
+// not beat two launches (the caller then makes two launches).
+roast_status_t sm100_chain(Ctx* c, const Module& m0, const Module& m1, const void* A0, void* out0, void* out1,
+                           int64_t T, bool dx, const float* bias0, const float* bias1, cudaStream_t s);
 roast_status_t sm100_dx(Ctx* c, const Module& m, const void* dY, void* dX, int64_t T, cudaStream_t s);
 roast_status_t sm100_dw(Ctx* c, const Module& m, const void* X, const void* dY, int64_t T, cudaStream_t s);
 

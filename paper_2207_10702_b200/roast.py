@@ -26,7 +26,8 @@ EXPORTS = [
     "roast_register_embedding_seg", "roast_linear_fwd", "roast_linear_bwd",
     "roast_linear_bwd_dx", "roast_linear_bwd_dm", "roast_embedding_fwd", "roast_embedding_bwd",
     "roast_embedding_fwd_multi", "roast_embedding_bwd_multi", "roast_set_autotune", "roast_get_tuned",
-    "roast_linear_fwd_bias", "roast_bias_fwd", "roast_bias_bwd", "roast_comm_unique_id", "roast_comm_init",
+    "roast_linear_fwd_bias", "roast_bias_fwd", "roast_bias_bwd", "roast_linear_fwd_chain",
+    "roast_linear_bwd_dx_chain", "roast_comm_unique_id", "roast_comm_init",
     "roast_grad_allreduce", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step",
     "roast_get_error",
     "roast_status_str", "roast_last_error", "roast_debug_tile_map", "roast_debug_chunk_map",
@@ -78,6 +79,8 @@ def _load():
         "roast_set_autotune": (st, [H, ctypes.c_int]),
         "roast_linear_fwd_bias": (st, [H, I32, P, P, I64, ctypes.c_int, P, S]),
         "roast_bias_fwd": (st, [H, I32, P, S]),
+        "roast_linear_fwd_chain": (st, [H, I32, I32, P, P, P, I64, ctypes.c_int, P, P, S]),
+        "roast_linear_bwd_dx_chain": (st, [H, I32, I32, P, P, P, I64, ctypes.c_int, S]),
         "roast_bias_bwd": (st, [H, I32, P, I64, ctypes.c_int, S]),
         "roast_get_tuned": (st, [H, I32, I32, I64, ctypes.POINTER(I32), ctypes.POINTER(I32)]),
         "roast_register_linear_seg": (st, [H, I64, I64, I64, I64, ctypes.POINTER(I32)]),
@@ -204,6 +207,16 @@ def lms_segments(sizes, mem_size, align=8):
 
 def roast_linear_fwd_bias(h, mid, X_ptr, Y_ptr, tokens, dtype, bias_ptr, stream=0):
     _check(_lib.roast_linear_fwd_bias(h, mid, X_ptr, Y_ptr, tokens, dtype, bias_ptr, stream), "roast_linear_fwd_bias")
+
+
+def roast_linear_fwd_chain(h, id_a, id_b, X_ptr, Ya_ptr, Yb_ptr, tokens, dtype, bias_a=None, bias_b=None, stream=0):
+    _check(_lib.roast_linear_fwd_chain(h, id_a, id_b, X_ptr, Ya_ptr, Yb_ptr, tokens, dtype, bias_a, bias_b, stream),
+           "roast_linear_fwd_chain")
+
+
+def roast_linear_bwd_dx_chain(h, id_a, id_b, dYb_ptr, dYa_ptr, dX_ptr, tokens, dtype, stream=0):
+    _check(_lib.roast_linear_bwd_dx_chain(h, id_a, id_b, dYb_ptr, dYa_ptr, dX_ptr, tokens, dtype, stream),
+           "roast_linear_bwd_dx_chain")
 
 
 def roast_bias_fwd(h, bias_id, b_ptr, stream=0):
@@ -388,6 +401,29 @@ class Roast:
             roast_linear_fwd_bias(self.h, mid, X.data_ptr(), Y.data_ptr(), T, self._dt(X), bias.data_ptr(),
                                   self._s(stream))
         return Y
+
+    def fwd_chain(self, a, b, X, Ya=None, Yb=None, stream=None, bias_a=None, bias_b=None):
+        """Y_a = X W~_a (+bias_a), Y_b = Y_a W~_b (+bias_b) in one launch; returns (Y_a, Y_b)."""
+        _, H, O = self.dims[a]
+        _, H2, O2 = self.dims[b]
+        T = X.numel() // H
+        Ya = self.torch.empty(T, O, dtype=X.dtype, device=X.device) if Ya is None else Ya
+        Yb = self.torch.empty(T, O2, dtype=X.dtype, device=X.device) if Yb is None else Yb
+        ptr = (lambda t: None if t is None else t.data_ptr())   # noqa: E731
+        roast_linear_fwd_chain(self.h, a, b, X.data_ptr(), Ya.data_ptr(), Yb.data_ptr(), T, self._dt(X),
+                               ptr(bias_a), ptr(bias_b), self._s(stream))
+        return Ya, Yb
+
+    def bwd_dx_chain(self, a, b, dYb, dYa=None, dX=None, stream=None):
+        """dY_a = dY_b W~_b^T, dX = dY_a W~_a^T in one launch; returns (dY_a, dX)."""
+        _, H, O = self.dims[a]
+        _, H2, O2 = self.dims[b]
+        T = dYb.numel() // O2
+        dYa = self.torch.empty(T, H2, dtype=dYb.dtype, device=dYb.device) if dYa is None else dYa
+        dX = self.torch.empty(T, H, dtype=dYb.dtype, device=dYb.device) if dX is None else dX
+        roast_linear_bwd_dx_chain(self.h, a, b, dYb.data_ptr(), dYa.data_ptr(), dX.data_ptr(), T, self._dt(dYb),
+                                  self._s(stream))
+        return dYa, dX
 
     def bias_fwd(self, bias_mid, out=None, stream=None):
         """The bias vector (row 0 of a 1 x n embedding registered for it) recovered with L."""

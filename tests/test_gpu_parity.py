@@ -550,3 +550,42 @@ def test_linear_bias_via_L(R, torch, dtype, z, H, O, T, det):
     assert rel_frob(outs[0].cpu().numpy(), dM_ref) <= 1e-5
     if det:
         assert torch.equal(outs[0], outs[1])
+
+
+# ---------------------------------------------------------------- chained GEMM pairs
+@pytest.mark.parametrize("T", [8192, 4096, 3000, 300, 1])
+def test_chain_fwd_and_dx_match_single_calls(R, torch, T):
+    """roast_linear_fwd_chain / roast_linear_bwd_dx_chain: one persistent launch for the MLP
+    block's two GEMMs, the second streaming behind the first's output tiles.  Every output
+    tile runs the same MMA sequence as the single calls, so results are bitwise equal
+    (repeated to catch a missing wait), and match the oracle."""
+    cfg = synth.mlp_block(100)
+    mem = cfg["mem_size"]
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64)
+    a, b = [ctx.linear(H, O) for H, O in cfg["layers"]]
+    X_np = bf16_input(synth.SEED_X, (T, 768))
+    dY_np = bf16_input(synth.SEED_DY, (T, 768))
+    X, dY2 = to_dev(X_np, torch.bfloat16), to_dev(dY_np, torch.bfloat16)
+    Ya_ref = ctx.fwd(a, X)
+    Yb_ref = ctx.fwd(b, Ya_ref)
+    dYa_ref = torch.empty(T, 3072, device="cuda", dtype=torch.bfloat16)
+    dX_ref = torch.empty(T, 768, device="cuda", dtype=torch.bfloat16)
+    ctx.bwd_dx(b, dY2, dYa_ref)
+    ctx.bwd_dx(a, dYa_ref, dX_ref)
+    for _ in range(4):
+        Ya, Yb = ctx.fwd_chain(a, b, X)
+        dYa, dX = ctx.bwd_dx_chain(a, b, dY2)
+        torch.cuda.synchronize()
+        assert torch.equal(Ya, Ya_ref) and torch.equal(Yb, Yb_ref)
+        assert torch.equal(dYa, dYa_ref) and torch.equal(dX, dX_ref)
+    ctx.check()
+    if T <= 300:   # oracle on the small case (the bitwise equality above carries the large ones)
+        sa = OM.LinearSpec(768, 3072, 64, 64, mem, HS, a)
+        sb = OM.LinearSpec(3072, 768, 64, 64, mem, HS, b)
+        Ya_np = Ya.float().cpu().numpy().astype(np.float64)
+        assert rel_frob(Ya_np, sa.forward(X_np, M_np, True)) <= 1e-2
+        assert rel_frob(Yb.float().cpu().numpy(), sb.forward(Ya_np, M_np, True)) <= 1e-2
+        dYa_np = dYa.float().cpu().numpy().astype(np.float64)
+        assert rel_frob(dYa_np, sb.backward_dx(dY_np, M_np, True)) <= 1e-2
+        assert rel_frob(dX.float().cpu().numpy(), sa.backward_dx(dYa_np, M_np, True)) <= 1e-2
