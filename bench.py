@@ -213,33 +213,22 @@ def run_gpu(args):
     dX = torch.empty(T, 768, device=dev, dtype=bf)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
-    kinds = ["fwd", "dx", "dm"]
-    ev = {k: [] for k in kinds}
     side = torch.cuda.Stream(device=dev)
 
-    def step_body(Xin, dY2in, record=False):
-        """One step of the hot path.  dX and dM of each layer are independent, so with
-        --streams 2 every dM GEMM runs on a second stream and fills the SMs the dX GEMM
-        leaves idle (the C ABI exposes the two halves of roast_linear_bwd for this)."""
+    def step_body(Xin, dY2in):
+        """One step of the hot path: Y1 = X W1, Y2 = Y1 W2, dY1 = dY2 W2^T, dX = dY1 W1^T,
+        dM += scatter(X^T dY1) + scatter(Y1^T dY2), then the dM exchange.  With --chain the
+        forward pair (and with --chain 2 the dX pair) runs as ONE persistent launch.  dX and dM
+        of each layer are independent, so with --streams 2 every dM GEMM runs on a second
+        stream and fills the SMs the dX GEMMs leave idle (roast_linear_bwd_dx / _dm)."""
         cur = torch.cuda.current_stream()
-
-        def rec(kind, fn):
-            if record:
-                a = torch.cuda.Event(enable_timing=True)
-                b = torch.cuda.Event(enable_timing=True)
-                a.record(cur)
-                fn()
-                b.record(cur)
-                ev[kind].append((a, b))
-            else:
-                fn()
         ctx.zero_grad()
-        if args.chain and not record:     # both forward GEMMs in one persistent launch
+        if args.chain:
             ctx.fwd_chain(l1, l2, Xin, Y1, Y2)
         else:
-            rec("fwd", lambda: ctx.fwd(l1, Xin, Y1))
-            rec("fwd", lambda: ctx.fwd(l2, Y1, Y2))
-        if args.streams == 2 and args.chain == 2 and not record:
+            ctx.fwd(l1, Xin, Y1)
+            ctx.fwd(l2, Y1, Y2)
+        if args.streams == 2 and args.chain == 2:
             side.wait_stream(cur)
             with torch.cuda.stream(side):
                 ctx.bwd_dm(l2, Y1, dY2in)
@@ -248,7 +237,7 @@ def run_gpu(args):
             with torch.cuda.stream(side):
                 ctx.bwd_dm(l1, Xin, dY1)
             cur.wait_stream(side)
-        elif args.streams == 2 and not record:
+        elif args.streams == 2:
             side.wait_stream(cur)
             ctx.bwd_dx(l2, dY2in, dY1)
             e_dy1 = torch.cuda.Event()
@@ -261,12 +250,23 @@ def run_gpu(args):
                 ctx.bwd_dm(l1, Xin, dY1)
             cur.wait_stream(side)
         else:
-            rec("dx", lambda: ctx.bwd_dx(l2, dY2in, dY1))
-            rec("dm", lambda: ctx.bwd_dm(l2, Y1, dY2in))
-            rec("dx", lambda: ctx.bwd_dx(l1, dY1, dX))
-            rec("dm", lambda: ctx.bwd_dm(l1, Xin, dY1))
+            if args.chain == 2:
+                ctx.bwd_dx_chain(l1, l2, dY2in, dY1, dX)
+            else:
+                ctx.bwd_dx(l2, dY2in, dY1)
+                ctx.bwd_dx(l1, dY1, dX)
+            ctx.bwd_dm(l2, Y1, dY2in)
+            ctx.bwd_dm(l1, Xin, dY1)
         ctx.allreduce()
 
+    if args.tuned_file:   # reuse a tuning (e.g. the plain bench run's) instead of timing under a profiler
+        saved = json.load(open(args.tuned_file))
+        saved = saved.get("config", {}).get("tuned", saved)
+        for i, mid in enumerate((l1, l2)):
+            for j, k in enumerate(("fwd", "dx", "dm")):
+                v = saved.get(f"L{i + 1}.{k}")
+                if v:
+                    ctx.set_tuned(mid, j, T, int(v[0]), int(v[1]))
     if args.autotune:   # tune every kernel once, sequentially on one stream (no concurrent work skews it)
         ctx.zero_grad()
         ctx.fwd(l1, X, Y1)
@@ -333,11 +333,22 @@ def run_gpu(args):
 
     # per-kernel-kind launch durations: each call captured alone in a CUDA graph and replayed
     # between CUDA events (device time of exactly that launch, no host launch latency)
-    calls = [("fwd", lambda: ctx.fwd(l1, X, Y1)), ("fwd", lambda: ctx.fwd(l2, Y1, Y2)),
-             ("dx", lambda: ctx.bwd_dx(l2, dY2, dY1)), ("dm", lambda: ctx.bwd_dm(l2, Y1, dY2)),
-             ("dx", lambda: ctx.bwd_dx(l1, dY1, dX)), ("dm", lambda: ctx.bwd_dm(l1, X, dY1))]
+    gemm_flop = 2.0 * T * 768 * 3072                       # every GEMM is one 2*T*H*O contraction
+    if args.chain:
+        calls = [("fwd_chain", lambda: ctx.fwd_chain(l1, l2, X, Y1, Y2), 2 * gemm_flop)]
+    else:
+        calls = [("fwd", lambda: ctx.fwd(l1, X, Y1), gemm_flop), ("fwd", lambda: ctx.fwd(l2, Y1, Y2), gemm_flop)]
+    if args.chain == 2:
+        calls += [("dx_chain", lambda: ctx.bwd_dx_chain(l1, l2, dY2, dY1, dX), 2 * gemm_flop)]
+    else:
+        calls += [("dx", lambda: ctx.bwd_dx(l2, dY2, dY1), gemm_flop), ("dx", lambda: ctx.bwd_dx(l1, dY1, dX), gemm_flop)]
+    calls += [("dm", lambda: ctx.bwd_dm(l2, Y1, dY2), gemm_flop), ("dm", lambda: ctx.bwd_dm(l1, X, dY1), gemm_flop)]
+    kinds = list(dict.fromkeys(k for k, _, _ in calls))
+    ev = {k: [] for k in kinds}
+    kind_flop = {k: f for k, _, f in calls}
+    kind_count = {k: sum(1 for c in calls if c[0] == k) for k in kinds}
     call_graphs = []
-    for kind, fn in calls:
+    for kind, fn, _ in calls:
         cg_ = torch.cuda.CUDAGraph()
         with torch.cuda.graph(cg_):
             fn()
@@ -354,10 +365,10 @@ def run_gpu(args):
             ev[kind].append((a, b))
     torch.cuda.synchronize()
     kind_ms = {k: float(np.mean([a.elapsed_time(b) for a, b in ev[k]])) for k in kinds}
-    gemm_flop = 2.0 * T * 768 * 3072                       # every call is one 2*T*H*O contraction
-    dom = max(kinds, key=lambda k: kind_ms[k])
+    # dominant kernel = the kind with the largest share of the step's launch time
+    dom = max(kinds, key=lambda k: kind_ms[k] * kind_count[k])
     burst, sustained, hbm, src = load_peaks()
-    achieved = gemm_flop / (kind_ms[dom] * 1e-3) / 1e12
+    achieved = kind_flop[dom] / (kind_ms[dom] * 1e-3) / 1e12
 
     # end-to-end through the C ABI with host buffers: H2D of the step's inputs and D2H of dM,
     # inside the timed region, the whole thing captured in one graph
@@ -435,6 +446,13 @@ def run_gpu(args):
     dense_ms = float(np.mean(dn))
     dense_tflops = flops_per_step(T) / (dense_ms * 1e-3) / 1e12
 
+    if args.nvtx_step:   # one more eager step inside an NVTX range, for `ncu --nvtx-include roast_step/`
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_push("roast_step")
+        step_body(X, dY2)
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
+
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
@@ -458,7 +476,7 @@ def run_gpu(args):
         roofline=dict(bound="tensor", kernel=dom, achieved=achieved, peak=burst, unit="TFLOP/s",
                       frac=achieved / burst, traffic=ncu_traffic(dom),
                       note=f"peak = {src} bf16 burst (MEASURED_PEAKS.json); algorithmic 2*T*H*O = "
-                           f"{gemm_flop/1e9:.2f} GFLOP per launch / mean CUDA-event duration",
+                           f"{kind_flop[dom]/1e9:.2f} GFLOP per launch / mean CUDA-event duration",
                       per_kind_ms=kind_ms, sustained_peak=sustained),
         dense_cublas=dict(tflops=dense_tflops, ms_per_step=dense_ms, roast_over_dense=value / world / dense_tflops),
         e2e=dict(value=e2e_value, unit=UNIT, h2d_bytes_per_step=int(Xh.numel() * 2 + dY2h.numel() * 2),
@@ -484,6 +502,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--streams", type=int, default=2, choices=[1, 2])
     ap.add_argument("--graph", type=int, default=1, choices=[0, 1])
+    ap.add_argument("--tuned-file", default=None,
+                    help="bench JSON (or its config.tuned dict) whose kernel choices seed the tuner")
+    ap.add_argument("--nvtx-step", action="store_true",
+                    help="run one extra eager step in NVTX range 'roast_step' (profiling)")
     ap.add_argument("--chain", type=int, default=1, choices=[0, 1, 2],
                     help="1: forward GEMM pair in one launch (roast_linear_fwd_chain); 2: also the dX pair")
     ap.add_argument("--autotune", type=int, default=2, choices=[0, 1, 2],

@@ -136,6 +136,10 @@ roast_status_t roast_set_autotune(roast_t h, roast_autotune_t strategy);
 /* The cached choice for a kernel (0 forward, 1 dX, 2 dM) of linear `id` at `tokens`:
  * *wm and *splits; ROAST_ERR_STATE if that shape was never tuned, BAD_ID. */
 roast_status_t roast_get_tuned(roast_t h, int32_t id, int32_t kernel, int64_t tokens, int32_t* wm, int32_t* splits);
+/* Seed the cache with a known choice (e.g. one tuned earlier and saved: a tuning cache
+ * shared across processes); used whatever the strategy.  Errors: CONFIG (kernel not
+ * 0..2, wm not 1..2, splits not 1..64, or splits != 1 for kernels 0 / 1), BAD_ID. */
+roast_status_t roast_set_tuned(roast_t h, int32_t id, int32_t kernel, int64_t tokens, int32_t wm, int32_t splits);
 
 /* a1: Y[tokens x out] = lambda * X[tokens x in] * W~, W~ tiles read from M
  * through the hash with sign g (Alg. 1; lambda once per output tile,

@@ -25,7 +25,7 @@ EXPORTS = [
     "roast_register_linear", "roast_register_embedding", "roast_register_linear_seg",
     "roast_register_embedding_seg", "roast_linear_fwd", "roast_linear_bwd",
     "roast_linear_bwd_dx", "roast_linear_bwd_dm", "roast_embedding_fwd", "roast_embedding_bwd",
-    "roast_embedding_fwd_multi", "roast_embedding_bwd_multi", "roast_set_autotune", "roast_get_tuned",
+    "roast_embedding_fwd_multi", "roast_embedding_bwd_multi", "roast_set_autotune", "roast_get_tuned", "roast_set_tuned",
     "roast_linear_fwd_bias", "roast_bias_fwd", "roast_bias_bwd", "roast_linear_fwd_chain",
     "roast_linear_bwd_dx_chain", "roast_comm_unique_id", "roast_comm_init",
     "roast_grad_allreduce", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step",
@@ -83,6 +83,7 @@ def _load():
         "roast_linear_bwd_dx_chain": (st, [H, I32, I32, P, P, P, I64, ctypes.c_int, S]),
         "roast_bias_bwd": (st, [H, I32, P, I64, ctypes.c_int, S]),
         "roast_get_tuned": (st, [H, I32, I32, I64, ctypes.POINTER(I32), ctypes.POINTER(I32)]),
+        "roast_set_tuned": (st, [H, I32, I32, I64, I32, I32]),
         "roast_register_linear_seg": (st, [H, I64, I64, I64, I64, ctypes.POINTER(I32)]),
         "roast_register_embedding_seg": (st, [H, I64, I32, I32, ctypes.c_double, I64, I64, ctypes.POINTER(I32)]),
         "roast_linear_fwd": (st, [H, I32, P, P, I64, ctypes.c_int, S]),
@@ -189,6 +190,10 @@ def roast_get_tuned(h, mid, kernel, tokens):
     if _lib.roast_get_tuned(h, mid, kernel, tokens, ctypes.byref(wm), ctypes.byref(sp)) != 0:
         return None
     return wm.value, sp.value
+
+
+def roast_set_tuned(h, mid, kernel, tokens, wm, splits):
+    _check(_lib.roast_set_tuned(h, mid, kernel, tokens, wm, splits), "roast_set_tuned")
 
 
 def lms_segments(sizes, mem_size, align=8):
@@ -375,6 +380,9 @@ class Roast:
 
     def tuned(self, mid, kernel, tokens):
         return roast_get_tuned(self.h, mid, kernel, tokens)
+
+    def set_tuned(self, mid, kernel, tokens, wm, splits=1):
+        roast_set_tuned(self.h, mid, kernel, tokens, wm, splits)
 
     def embedding(self, num_rows, dim, chunk, fan_in=0.0, segment=None):
         mid = (roast_register_embedding(self.h, num_rows, dim, chunk, fan_in) if segment is None else

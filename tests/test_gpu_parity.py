@@ -589,3 +589,28 @@ def test_chain_fwd_and_dx_match_single_calls(R, torch, T):
         dYa_np = dYa.float().cpu().numpy().astype(np.float64)
         assert rel_frob(dYa_np, sb.backward_dx(dY_np, M_np, True)) <= 1e-2
         assert rel_frob(dX.float().cpu().numpy(), sa.backward_dx(dYa_np, M_np, True)) <= 1e-2
+
+
+def test_set_tuned_seeds_the_cache(R, torch):
+    """roast_set_tuned (a saved tuning): the given WM / split-K is used and results keep parity;
+    invalid choices are rejected."""
+    from paper_2207_10702_b200 import roast
+    mem, T, H, O = 47192, 700, 768, 3072
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64)
+    mid = ctx.linear(H, O)
+    for wm, sp in [(1, 3), (2, 5)]:
+        ctx.set_tuned(mid, 0, T, wm)
+        ctx.set_tuned(mid, 1, T, wm)
+        ctx.set_tuned(mid, 2, T, wm, sp)
+        assert ctx.tuned(mid, 2, T) == (wm, sp)
+        X_np = bf16_input(synth.SEED_X, (T, H))
+        dY_np = bf16_input(synth.SEED_DY, (T, O))
+        Y, dX, dM = run_linear(R, torch, ctx, mid, X_np, dY_np, torch.bfloat16)
+        spec = OM.LinearSpec(H, O, 64, 64, mem, HS, mid)
+        assert rel_frob(Y, spec.forward(X_np, M_np, True)) <= 1e-2
+        assert rel_frob(dX, spec.backward_dx(dY_np, M_np, True)) <= 1e-2
+        assert rel_frob(dM, spec.backward_dm(X_np, dY_np)) <= 1e-2
+    for bad in [(0, T, 3, 1), (0, T, 1, 2), (3, T, 1, 1), (2, T, 1, 0)]:
+        with pytest.raises(roast.RoastError):
+            ctx.set_tuned(mid, *bad)

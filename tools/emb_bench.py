@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--dist", default="uniform", choices=["uniform", "zipf"])
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--align", type=int, default=32, help="offset alignment A in elements (32 = 128-B lines)")
+    ap.add_argument("--nvtx", action="store_true", help="one eager fused fwd + bwd in NVTX range 'emb_step' (ncu)")
     args = ap.parse_args()
     tables, rows, dim, Z = 26, 10 ** 7, 128, 32
     batch = 8192 if args.quick else 65536
@@ -57,6 +58,16 @@ def main():
 
     res = {}
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    if args.nvtx:
+        fwd_multi()
+        bwd_multi()
+        flush.zero_()
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_push("emb_step")
+        fwd_multi()
+        bwd_multi()
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
     for name, fn, bpl in [("fwd", fwd, 1032), ("bwd", bwd, 1544), ("fwd_multi", fwd_multi, 1032),
                           ("bwd_multi", bwd_multi, 1544)]:
         for _ in range(3):

@@ -1,8 +1,8 @@
 #!/usr/bin/env python
 """Write profiles/<round>/traffic.json: mean DRAM bytes (read + write) per launch of each
 tcgen05 kernel kind, from an `ncu --set full` capture of one bench step
-(launch order fwd L1, fwd L2, dx L2, dm L2, dx L1, dm L1).  bench.py reports it as
-roofline.traffic."""
+(kinds by template arguments: <0,..> fwd, <1,..> dx, <2,..> dm; a trailing `true` = the
+chained pair: fwd_chain / dx_chain).  bench.py reports it as roofline.traffic."""
 import csv
 import io
 import json
@@ -19,9 +19,13 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 kinds = {"<0,": "fwd", "<1,": "dx", "<2,": "dm"}
 acc = {}
 for r in rows[2:]:
-    kind = next((v for k, v in kinds.items() if k in r[iname].replace(" ", "")), None)
+    name = r[iname].replace(" ", "")
+    kind = next((v for k, v in kinds.items() if k in name), None)
     if kind is None:
         continue
+    targs = name[name.index("<") + 1:name.index(">")].split(",")
+    if len(targs) >= 4 and targs[3] in ("1", "true"):
+        kind += "_chain"
     b = float(r[ir]) * scale[units[ir]] + float(r[iw]) * scale[units[iw]]
     acc.setdefault(kind, []).append(b)
 res = {k: sum(v) / len(v) for k, v in acc.items()}
