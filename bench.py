@@ -475,7 +475,7 @@ def run_gpu(args):
                     parallelism=f"dp{world}"),
         roofline=dict(bound="tensor", kernel=dom, achieved=achieved, peak=burst, unit="TFLOP/s",
                       frac=achieved / burst, traffic=ncu_traffic(dom),
-                      note=f"peak = {src} bf16 burst (MEASURED_PEAKS.json); algorithmic 2*T*H*O = "
+                      note=f"peak = {src} bf16 burst ({'of measured, MEASURED_PEAKS.json' if src == 'measured' else 'of fallback, B200_PROFILING.md: MEASURED_PEAKS.json absent'}); algorithmic 2*T*H*O = "
                            f"{kind_flop[dom]/1e9:.2f} GFLOP per launch / mean CUDA-event duration",
                       per_kind_ms=kind_ms, sustained_peak=sustained),
         dense_cublas=dict(tflops=dense_tflops, ms_per_step=dense_ms, roast_over_dense=value / world / dense_tflops),

@@ -83,7 +83,7 @@ int main() {
   long long* out;
   cudaMalloc(&out, 148 * 8);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  struct Case { const char* name; int na, ra, nbx, depth; size_t brows; } cases[] = {
+  struct Case { const char* name; int na, ra, nbx, depth; size_t brows; int boff = 0; } cases[] = {
       {"A 16KB box{64,128}", 1, 128, 0, 6, b_rows_small},
       {"A 16KB x2 (32KB/stage)", 2, 128, 0, 6, b_rows_small},
       {"B 8KB box{64,64} small-region x4", 0, 128, 4, 6, b_rows_small},
@@ -92,11 +92,16 @@ int main() {
       {"A16K + B 2x8K small depth 4", 1, 128, 2, 4, b_rows_small},
       {"A16K + B 4x8K small (our CG1)", 1, 128, 4, 4, b_rows_small},
       {"A 32KB box{64,256}", 1, 256, 0, 6, b_rows_small},
+      {"B 8KB small x4, base +16 B", 0, 128, 4, 6, b_rows_small, 16},
+      {"B 8KB small x2 depth 6", 0, 128, 2, 6, b_rows_small},
+      {"B 8KB small x2 depth 12", 0, 128, 2, 12, b_rows_small},
+      {"A16K + B 2x8K small +16B", 1, 128, 2, 6, b_rows_small, 16},
+      {"A32K + B 2x8K small (WM2)", 1, 256, 2, 4, b_rows_small},
   };
   for (auto& c : cases) {
     Maps m;
     mk(&m.a, A, 768, a_rows, 64, c.ra);
-    mk(&m.b, B, 64, c.brows, 64, 64);
+    mk(&m.b, (char*)B + c.boff, 64, c.brows - 1, 64, 64);
     int iters = 2000;
     k<<<148, 32, 220 * 1024>>>(m, 10, c.depth, c.na, c.ra, c.nbx, (int)a_rows, (int)c.brows, out);
     cudaEvent_t e0, e1;
