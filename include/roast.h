@@ -233,6 +233,29 @@ roast_status_t roast_comm_unique_id(uint8_t id_out[128]);
 roast_status_t roast_comm_init(roast_t h, int32_t rank, int32_t world, const uint8_t id[128]);
 roast_status_t roast_grad_allreduce(roast_t h, roast_stream_t stream);
 
+/* a6 in the large-|M| regime ("communication is directly
+ * proportional to model size"): the touched-set exchange.  Offsets are static, so the
+ * slots any rank can write are the union of [off_t, off_t + Z1 Z2) over every linear's
+ * tiles plus, per embedding, its exact chunks (tables of <= 2^16 chunks, e.g. biases
+ * via L) or its whole memory (GMS: all of M; LMS: its segment).  All other slots of dM
+ * are zero on every rank.  In TOUCHED mode roast_grad_allreduce packs the touched
+ * intervals (a library-owned fp32 buffer), all-reduces the packed buffer and unpacks it:
+ * the same sum, with NVLink traffic <= min(|M|, n) elements.  AUTO (default) picks
+ * TOUCHED when the touched set is at most |M| / 2, else DENSE.  The interval tables are
+ * built on the host on first use after a registration (synchronous); under CUDA-graph
+ * capture they must already exist (call roast_touched_size first), else ROAST_ERR_STATE.
+ * Slots outside the touched set are neither read nor written by the exchange. */
+typedef enum { ROAST_EXCHANGE_AUTO = 0, ROAST_EXCHANGE_DENSE = 1, ROAST_EXCHANGE_TOUCHED = 2 } roast_exchange_mode_t;
+roast_status_t roast_set_exchange(roast_t h, int32_t mode);
+/* Builds the interval tables if needed; *n_touched = elements in the touched set,
+ * *n_intervals = disjoint intervals (either pointer may be NULL). */
+roast_status_t roast_touched_size(roast_t h, int64_t* n_touched, int64_t* n_intervals);
+/* Host utility (no GPU, no handle): merge [starts_in[i], starts_in[i] + span) into sorted
+ * disjoint, non-adjacent intervals -> starts_out / lens_out (host arrays of cap entries);
+ * *count = number of intervals.  ROAST_ERR_CAPACITY (count still set) if count > cap. */
+roast_status_t roast_touched_intervals(const int64_t* starts_in, int64_t n, int64_t span, int64_t* starts_out,
+                                       int64_t* lens_out, int64_t cap, int64_t* count);
+
 /* dM <- 0. */
 roast_status_t roast_zero_grad(roast_t h, roast_stream_t stream);
 /* shadow <- [+bf16_RNE(M) | -bf16_RNE(M)]; call after every update of M (H7). */
@@ -283,6 +306,10 @@ roast_status_t roast_debug_materialize(roast_t h, int32_t id, roast_dtype_t dt, 
 roast_status_t roast_debug_hash_host(uint64_t seed, int32_t module, const uint64_t* keys_host, int64_t n,
                                      int64_t mem_size, int64_t span, int32_t align, int32_t use_sign,
                                      int64_t* off_out_host, int8_t* sgn_out_host);
+/* Touched-set exchange without NCCL: pack dM's touched intervals, then unpack them
+ * scaled: dM[touched] *= scale, every other slot untouched (tests the interval maps on
+ * one GPU). */
+roast_status_t roast_debug_exchange(roast_t h, float scale, roast_stream_t stream);
 /* Number of kernels this handle has launched since creation (bench evidence). */
 int64_t roast_launch_count(roast_t h);
 

@@ -94,9 +94,32 @@ roast_status_t roast_grad_allreduce(roast_t h, roast_stream_t stream) {
     if (c->world == 1) return ROAST_OK;
     return fail(ROAST_ERR_STATE, "roast_comm_init has not been called");
   }
-  ncclResult_t r = api().AllReduce(c->dM, c->dM, size_t(c->mem_size), ncclFloat32, ncclSum,
-                                   reinterpret_cast<ncclComm_t>(c->nccl_comm), reinterpret_cast<cudaStream_t>(stream));
-  if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  bool touched = false;
+  if (c->exchange_mode != ROAST_EXCHANGE_DENSE) {
+    // the interval tables are built on the first (eager) call; under graph capture they must exist
+    if (!(c->touched_valid && c->touched_for == int64_t(c->modules.size()))) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+        return fail(ROAST_ERR_STATE, "touched-set exchange: call roast_touched_size (or one eager exchange) "
+                                     "before capturing");
+      if (roast_status_t st = touched_prepare(c, s)) return st;
+    }
+    touched = c->exchange_mode == ROAST_EXCHANGE_TOUCHED || 2 * c->touched_n <= c->mem_size;
+  }
+  if (!touched) {
+    ncclResult_t r = api().AllReduce(c->dM, c->dM, size_t(c->mem_size), ncclFloat32, ncclSum,
+                                     reinterpret_cast<ncclComm_t>(c->nccl_comm), s);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
+    return ROAST_OK;
+  }
+  if (c->touched_n == 0) return ROAST_OK;
+  ROAST_CUDA_CHECK(launch_pack(c, 0, 1.f, s));
+  ncclResult_t r = api().AllReduce(c->d_pack, c->d_pack, size_t(c->touched_n), ncclFloat32, ncclSum,
+                                   reinterpret_cast<ncclComm_t>(c->nccl_comm), s);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce(touched)");
+  ROAST_CUDA_CHECK(launch_pack(c, 1, 1.f, s));
+  c->launches += 2;
   return ROAST_OK;
 }
 

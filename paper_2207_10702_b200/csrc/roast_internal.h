@@ -80,6 +80,15 @@ struct Ctx {
   std::map<std::array<int64_t, 6>, std::pair<int32_t*, int>> chain_plans;
   int* chain_flags = nullptr;
   int64_t chain_flags_n = 0;
+  // touched-set dM exchange (exchange.cu): merged intervals of the slots the registered modules
+  // can write; d_iv = [starts (n_iv) | exclusive prefix of lengths (n_iv + 1)], d_pack = the
+  // packed buffer (touched_n fp32); rebuilt when the module count changes
+  int32_t exchange_mode = 0;      // roast_exchange_mode_t
+  bool touched_valid = false, touched_vec = false;
+  int64_t touched_for = -1, touched_n = 0;
+  int32_t n_iv = 0;
+  int64_t* d_iv = nullptr;
+  float* d_pack = nullptr;
 };
 
 // error reporting (thread-local detail string)
@@ -92,6 +101,11 @@ roast_status_t cuda_fail(cudaError_t e, const char* what);
   } while (0)
 
 void comm_destroy(Ctx* c);
+
+// touched-set exchange (exchange.cu): build the interval tables (host, synchronous uploads);
+// pack (dir 0: d_pack <- dM[touched]) or unpack (dir 1: dM[touched] <- scale * d_pack)
+roast_status_t touched_prepare(Ctx* c, cudaStream_t s);
+cudaError_t launch_pack(Ctx* c, int dir, float scale, cudaStream_t s);
 
 // workspace of at least `bytes`, stream-ordered
 roast_status_t ensure_ws(Ctx* c, size_t bytes, cudaStream_t s);

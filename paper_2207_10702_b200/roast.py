@@ -28,7 +28,8 @@ EXPORTS = [
     "roast_embedding_fwd_multi", "roast_embedding_bwd_multi", "roast_set_autotune", "roast_get_tuned", "roast_set_tuned",
     "roast_linear_fwd_bias", "roast_bias_fwd", "roast_bias_bwd", "roast_linear_fwd_chain",
     "roast_linear_bwd_dx_chain", "roast_comm_unique_id", "roast_comm_init",
-    "roast_grad_allreduce", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step",
+    "roast_grad_allreduce", "roast_set_exchange", "roast_touched_size", "roast_touched_intervals",
+    "roast_debug_exchange", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step",
     "roast_get_error",
     "roast_status_str", "roast_last_error", "roast_debug_tile_map", "roast_debug_chunk_map",
     "roast_debug_materialize", "roast_debug_hash_host", "roast_launch_count",
@@ -97,6 +98,10 @@ def _load():
         "roast_comm_unique_id": (st, [ctypes.c_char_p]),
         "roast_comm_init": (st, [H, I32, I32, ctypes.c_char_p]),
         "roast_grad_allreduce": (st, [H, S]),
+        "roast_set_exchange": (st, [H, I32]),
+        "roast_touched_size": (st, [H, ctypes.POINTER(I64), ctypes.POINTER(I64)]),
+        "roast_touched_intervals": (st, [P, I64, I64, P, P, I64, ctypes.POINTER(I64)]),
+        "roast_debug_exchange": (st, [H, ctypes.c_float, S]),
         "roast_zero_grad": (st, [H, S]),
         "roast_sync_shadow": (st, [H, S]),
         "roast_sgd_step": (st, [H, ctypes.c_float, S]),
@@ -282,6 +287,37 @@ def roast_comm_init(h, rank, world, uid: bytes):
 
 def roast_grad_allreduce(h, stream=0):
     _check(_lib.roast_grad_allreduce(h, stream), "roast_grad_allreduce")
+
+
+EXCHANGE_AUTO, EXCHANGE_DENSE, EXCHANGE_TOUCHED = 0, 1, 2
+
+
+def roast_set_exchange(h, mode):
+    _check(_lib.roast_set_exchange(h, mode), "roast_set_exchange")
+
+
+def roast_touched_size(h):
+    """(elements, intervals) of the touched set the exchange moves."""
+    n, k = ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib.roast_touched_size(h, ctypes.byref(n), ctypes.byref(k)), "roast_touched_size")
+    return n.value, k.value
+
+
+def roast_touched_intervals(starts, span):
+    """Host utility: merged [s, s + span) intervals -> (starts, lengths) int64 arrays (no GPU)."""
+    import numpy as np
+    s = np.ascontiguousarray(starts, dtype=np.int64)
+    cap = max(1, len(s))
+    out_s = np.empty(cap, dtype=np.int64)
+    out_l = np.empty(cap, dtype=np.int64)
+    cnt = ctypes.c_int64()
+    _check(_lib.roast_touched_intervals(s.ctypes.data, len(s), span, out_s.ctypes.data, out_l.ctypes.data, cap,
+                                        ctypes.byref(cnt)), "roast_touched_intervals")
+    return out_s[:cnt.value].copy(), out_l[:cnt.value].copy()
+
+
+def roast_debug_exchange(h, scale, stream=0):
+    _check(_lib.roast_debug_exchange(h, scale, stream), "roast_debug_exchange")
 
 
 def roast_zero_grad(h, stream=0):
@@ -505,6 +541,12 @@ class Roast:
 
     def allreduce(self, stream=None):
         roast_grad_allreduce(self.h, self._s(stream))
+
+    def set_exchange(self, mode):
+        roast_set_exchange(self.h, mode)
+
+    def touched_size(self):
+        return roast_touched_size(self.h)
 
     def tile_map(self, mid):
         import numpy as np

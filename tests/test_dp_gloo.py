@@ -94,3 +94,54 @@ def test_world2_allreduce_equals_full_batch():
     assert all(p.exitcode == 0 for p in procs)
     for rank, err_mm, err_emb in results:
         assert err_mm <= 1e-12 and err_emb <= 1e-12, (rank, err_mm, err_emb)
+
+
+def _touched_worker(rank, world, port, q):
+    """The touched-set exchange at world 2: pack the library's intervals,
+    all-reduce only the packed vector, unpack — equals the dense full-batch dM."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2207_10702_b200 import roast as R
+        mem = 1 << 18                                      # |M| >> n: most of dM is never written
+        layers = [OM.LinearSpec(128, 192, 64, 64, mem, synth.HASH_SEED, 0),
+                  OM.LinearSpec(192, 128, 64, 64, mem, synth.HASH_SEED, 1)]
+        T = 77
+        X1, dY1 = synth.normal(2, (T, 128)), synth.normal(3, (T, 192))
+        X2, dY2 = synth.normal(4, (T, 192)), synth.normal(5, (T, 128))
+        a, b = dp.shard(T, rank, world)
+        local = np.zeros(mem)
+        layers[0].backward_dm(X1[a:b], dY1[a:b], local)
+        layers[1].backward_dm(X2[a:b], dY2[a:b], local)
+        starts, lens = R.roast_touched_intervals(np.concatenate([sp.off.ravel() for sp in layers]), 64 * 64)
+        packed = torch.tensor(np.concatenate([local[s:s + n] for s, n in zip(starts, lens)]))
+        dist.all_reduce(packed)
+        out = np.zeros(mem)
+        p = 0
+        for s, n in zip(starts, lens):
+            out[s:s + n] = packed.numpy()[p:p + n]
+            p += n
+        full = np.zeros(mem)
+        layers[0].backward_dm(X1, dY1, full)
+        layers[1].backward_dm(X2, dY2, full)
+        err = float(np.max(np.abs(out - full)) / np.max(np.abs(full)))
+        q.put((rank, err, int(lens.sum()), mem))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_touched_set_exchange_equals_dense():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_touched_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    results = [q.get(timeout=5) for _ in range(2)]
+    assert all(p.exitcode == 0 for p in procs)
+    for rank, err, moved, mem in results:
+        assert err <= 1e-12, (rank, err)
+        assert moved <= 2 * 6 * 4096 < mem       # 2 x 6 tiles of 4096 slots at most, << |M|

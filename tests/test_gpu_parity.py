@@ -385,6 +385,7 @@ def test_nccl_allreduce_single_rank_and_graph_capture(R, torch):
     mem = 47192
     ctx, _ = make_ctx(R, torch, store(mem), 64, 64)
     roast.roast_comm_init(ctx.h, 0, 1, roast.roast_comm_unique_id())
+    ctx.set_exchange(roast.EXCHANGE_DENSE)      # no modules: AUTO would move nothing
     g = to_dev(synth.normal(3, (mem,)).astype(np.float32), torch.float32)
     ctx.dM.copy_(g)
     ctx.allreduce()
