@@ -278,6 +278,10 @@ typedef struct {
   int32_t kind;        /* roast_opt_kind_t */
   float lr, beta1, beta2, eps, weight_decay;
   int32_t zero_grad;   /* 1: dM <- 0 in the same pass */
+  int32_t touched_only;/* 1: visit only the touched set of roast_touched_size ("the
+                          same restriction applies to zeroing and updates"); slots outside it are
+                          never read by any module, so every model output is unchanged, at
+                          O(touched) instead of O(|M|) cost.  Under capture the tables must exist. */
 } roast_opt_config_t;
 roast_status_t roast_optimizer_step(roast_t h, const roast_opt_config_t* cfg, int64_t step, roast_stream_t stream);
 

@@ -620,7 +620,8 @@ roast_status_t roast_sync_shadow(roast_t h, roast_stream_t stream) {
 roast_status_t roast_sgd_step(roast_t h, float lr, roast_stream_t stream) {
   Ctx* c = ctx(h);
   if (!c || !c->M || !c->shadow) return fail(ROAST_ERR_STATE, "not bound");
-  ROAST_CUDA_CHECK(launch_sgd(c, lr, reinterpret_cast<cudaStream_t>(stream)));
+  ROAST_CUDA_CHECK(launch_optimizer(c, ROAST_OPT_SGD, lr, 0.f, 0.f, 0.f, 0.f, 1, 0, false,
+                                    reinterpret_cast<cudaStream_t>(stream)));
   c->launches++;
   return ROAST_OK;
 }
@@ -640,8 +641,16 @@ roast_status_t roast_optimizer_step(roast_t h, const roast_opt_config_t* cfg, in
     ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->opt_s2), bytes));
     ROAST_CUDA_CHECK(cudaMemsetAsync(c->opt_s2, 0, bytes, s));
   }
+  if (cfg->touched_only) {   // the interval tables of the exchange (built eagerly, not under capture)
+    if (!(c->touched_valid && c->touched_for == int64_t(c->modules.size()))) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+        return fail(ROAST_ERR_STATE, "touched_only: call roast_touched_size before capturing");
+      if (roast_status_t st = touched_prepare(c, s)) return st;
+    }
+  }
   ROAST_CUDA_CHECK(launch_optimizer(c, cfg->kind, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay, step,
-                                    cfg->zero_grad, s));
+                                    cfg->zero_grad, cfg->touched_only != 0, s));
   c->launches++;
   return ROAST_OK;
 }

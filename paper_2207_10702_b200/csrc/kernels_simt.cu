@@ -209,17 +209,6 @@ __global__ void sync_shadow_kernel(const float* __restrict__ M, __nv_bfloat16* _
   }
 }
 
-__global__ void sgd_kernel(float* __restrict__ M, const float* __restrict__ dM, __nv_bfloat16* __restrict__ sh,
-                           int64_t n, int64_t neg_base, float lr) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    float v = M[i] - lr * dM[i];
-    M[i] = v;
-    __nv_bfloat16 b = __float2bfloat16_rn(v);
-    sh[i] = b;
-    sh[neg_base + i] = __hneg(b);
-  }
-}
-
 __global__ void materialize_kernel(const float* __restrict__ M, const __nv_bfloat16* __restrict__ sh, MapArgs map,
                                    int H, int O, float lam, int bf16_out, void* W) {
   int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -309,12 +298,6 @@ cudaError_t launch_sync_shadow(Ctx* c, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_sgd(Ctx* c, float lr, cudaStream_t s) {
-  sgd_kernel<<<grid_1d(c->mem_size, 256), 256, 0, s>>>(c->M, c->dM, reinterpret_cast<__nv_bfloat16*>(c->shadow),
-                                                       c->mem_size, c->neg_base, lr);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_materialize(const Ctx* c, const Module& m, roast_dtype_t dt, void* W, cudaStream_t s) {
   int64_t n = m.H * m.O;
   if (n == 0) return cudaSuccess;
@@ -331,51 +314,154 @@ namespace {
 
 // One pass over |M|: update M from dM (and the optimizer state), refresh both halves of the
 // bf16 shadow, optionally zero dM.  kind: 0 SGD, 1 Adagrad, 2 Adam (PyTorch formulas).
+// One optimizer update of a single slot (fp32 registers in / out).
 template <int KIND>
-__global__ void opt_kernel(float* __restrict__ M, float* __restrict__ dM, __nv_bfloat16* __restrict__ sh,
-                           float* __restrict__ s1, float* __restrict__ s2, int64_t n, int64_t neg_base, float lr,
-                           float b1, float b2, float eps, float wd, float bc1, float bc2, int zero) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    float w = M[i];
-    const float g = dM[i] + wd * w;
-    if (KIND == 0) {
-      w -= lr * g;
-    } else if (KIND == 1) {
-      const float G = s1[i] + g * g;
-      s1[i] = G;
-      w -= lr * g / (sqrtf(G) + eps);
-    } else {
-      const float m = b1 * s1[i] + (1.f - b1) * g;
-      const float v = b2 * s2[i] + (1.f - b2) * g * g;
-      s1[i] = m;
-      s2[i] = v;
-      w -= lr * (m / bc1) / (sqrtf(v / bc2) + eps);
-    }
-    M[i] = w;
-    const __nv_bfloat16 b = __float2bfloat16_rn(w);
-    sh[i] = b;
-    sh[neg_base + i] = __hneg(b);
-    if (zero) dM[i] = 0.f;
+__device__ __forceinline__ float opt_update(float w, float g0, float& a, float& b, float lr, float b1, float b2,
+                                            float eps, float wd, float bc1, float bc2) {
+  const float g = g0 + wd * w;
+  if (KIND == 0) {
+    w -= lr * g;
+  } else if (KIND == 1) {
+    a = a + g * g;
+    w -= lr * g / (sqrtf(a) + eps);
+  } else {
+    a = b1 * a + (1.f - b1) * g;
+    b = b2 * b + (1.f - b2) * g * g;
+    w -= lr * (a / bc1) / (sqrtf(b / bc2) + eps);
   }
+  return w;
+}
+
+struct OptArgs {
+  float* M;
+  float* dM;
+  __nv_bfloat16* sh;
+  float* s1;
+  float* s2;
+  int64_t neg_base;
+  float lr, b1, b2, eps, wd, bc1, bc2;
+  int zero;
+  // index space: n elements; slot = p (n_iv == 0) or the p-th touched slot (exchange.cu tables)
+  int64_t n;
+  const int64_t* iv_start;
+  const int64_t* iv_prefix;
+  int n_iv;
+};
+
+__device__ __forceinline__ int64_t opt_slot(const OptArgs& a, int64_t p) {
+  if (a.n_iv == 0) return p;
+  int lo = 0, hi = a.n_iv - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(a.iv_prefix + mid) <= p) lo = mid; else hi = mid - 1;
+  }
+  return __ldg(a.iv_start + lo) + (p - __ldg(a.iv_prefix + lo));
+}
+
+// One pass over |M| (or over the touched slots): update M from dM (and the optimizer state),
+// refresh both halves of the bf16 shadow, optionally zero dM.  kind: 0 SGD, 1 Adagrad, 2 Adam
+// (PyTorch formulas).  V = 4: 16-byte vectors (every index-space run is a multiple of 4 and
+// 16-byte aligned), V = 1: scalar.
+template <int KIND, int V>
+__global__ void opt_kernel(OptArgs a) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x * V;
+  for (int64_t p = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * V; p < a.n; p += stride) {
+    const int64_t i = opt_slot(a, p);
+    float w[V], g[V], x[V], y[V];
+    if constexpr (V == 4) {
+      const float4 wv = *reinterpret_cast<const float4*>(a.M + i);
+      const float4 gv = *reinterpret_cast<const float4*>(a.dM + i);
+      w[0] = wv.x; w[1] = wv.y; w[2] = wv.z; w[3] = wv.w;
+      g[0] = gv.x; g[1] = gv.y; g[2] = gv.z; g[3] = gv.w;
+      if (KIND >= 1) {
+        const float4 v = *reinterpret_cast<const float4*>(a.s1 + i);
+        x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+      }
+      if (KIND == 2) {
+        const float4 v = *reinterpret_cast<const float4*>(a.s2 + i);
+        y[0] = v.x; y[1] = v.y; y[2] = v.z; y[3] = v.w;
+      }
+    } else {
+      w[0] = a.M[i];
+      g[0] = a.dM[i];
+      if (KIND >= 1) x[0] = a.s1[i];
+      if (KIND == 2) y[0] = a.s2[i];
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k) w[k] = opt_update<KIND>(w[k], g[k], x[k], y[k], a.lr, a.b1, a.b2, a.eps, a.wd, a.bc1, a.bc2);
+    if constexpr (V == 4) {
+      *reinterpret_cast<float4*>(a.M + i) = make_float4(w[0], w[1], w[2], w[3]);
+      if (KIND >= 1) *reinterpret_cast<float4*>(a.s1 + i) = make_float4(x[0], x[1], x[2], x[3]);
+      if (KIND == 2) *reinterpret_cast<float4*>(a.s2 + i) = make_float4(y[0], y[1], y[2], y[3]);
+      const __nv_bfloat162 p0 = __floats2bfloat162_rn(w[0], w[1]), p1 = __floats2bfloat162_rn(w[2], w[3]);
+      uint2 pos, neg;
+      pos.x = *reinterpret_cast<const uint32_t*>(&p0);
+      pos.y = *reinterpret_cast<const uint32_t*>(&p1);
+      neg.x = pos.x ^ 0x80008000u;   // bf16 negation = sign flip (exact)
+      neg.y = pos.y ^ 0x80008000u;
+      *reinterpret_cast<uint2*>(a.sh + i) = pos;
+      *reinterpret_cast<uint2*>(a.sh + a.neg_base + i) = neg;
+      if (a.zero) *reinterpret_cast<float4*>(a.dM + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      a.M[i] = w[0];
+      if (KIND >= 1) a.s1[i] = x[0];
+      if (KIND == 2) a.s2[i] = y[0];
+      const __nv_bfloat16 b = __float2bfloat16_rn(w[0]);
+      a.sh[i] = b;
+      a.sh[a.neg_base + i] = __hneg(b);
+      if (a.zero) a.dM[i] = 0.f;
+    }
+  }
+}
+
+template <int KIND>
+void launch_opt_kind(const OptArgs& a, bool vec, cudaStream_t s) {
+  const int V = vec ? 4 : 1;
+  int64_t blocks = (a.n / V + 255) / 256;
+  blocks = std::min<int64_t>(std::max<int64_t>(blocks, 1), 148 * 16);
+  if (vec)
+    opt_kernel<KIND, 4><<<unsigned(blocks), 256, 0, s>>>(a);
+  else
+    opt_kernel<KIND, 1><<<unsigned(blocks), 256, 0, s>>>(a);
 }
 
 }  // namespace
 
 cudaError_t launch_optimizer(Ctx* c, int kind, float lr, float b1, float b2, float eps, float wd, int64_t step,
-                             int zero, cudaStream_t s) {
-  const float bc1 = kind == 2 ? float(1.0 - pow(double(b1), double(step))) : 1.f;
-  const float bc2 = kind == 2 ? float(1.0 - pow(double(b2), double(step))) : 1.f;
-  auto* sh = reinterpret_cast<__nv_bfloat16*>(c->shadow);
-  const int grid = grid_1d(c->mem_size, 256);
+                             int zero, bool touched_only, cudaStream_t s) {
+  OptArgs a{};
+  a.M = c->M;
+  a.dM = c->dM;
+  a.sh = reinterpret_cast<__nv_bfloat16*>(c->shadow);
+  a.s1 = c->opt_s1;
+  a.s2 = c->opt_s2;
+  a.neg_base = c->neg_base;
+  a.lr = lr;
+  a.b1 = b1;
+  a.b2 = b2;
+  a.eps = eps;
+  a.wd = wd;
+  a.bc1 = kind == 2 ? float(1.0 - pow(double(b1), double(step))) : 1.f;
+  a.bc2 = kind == 2 ? float(1.0 - pow(double(b2), double(step))) : 1.f;
+  a.zero = zero;
+  bool vec;
+  if (touched_only) {   // the slots some module can read or write (exchange.cu); the rest are dead
+    a.n = c->touched_n;
+    a.iv_start = c->d_iv;
+    a.iv_prefix = c->d_iv + c->n_iv;
+    a.n_iv = c->n_iv;
+    vec = c->touched_vec;
+    if (a.n == 0) return cudaSuccess;
+  } else {
+    a.n = c->mem_size;
+    vec = c->mem_size % 4 == 0;
+  }
   if (kind == 0)
-    opt_kernel<0><<<grid, 256, 0, s>>>(c->M, c->dM, sh, nullptr, nullptr, c->mem_size, c->neg_base, lr, b1, b2, eps,
-                                       wd, bc1, bc2, zero);
+    launch_opt_kind<0>(a, vec, s);
   else if (kind == 1)
-    opt_kernel<1><<<grid, 256, 0, s>>>(c->M, c->dM, sh, c->opt_s1, nullptr, c->mem_size, c->neg_base, lr, b1, b2,
-                                       eps, wd, bc1, bc2, zero);
+    launch_opt_kind<1>(a, vec, s);
   else
-    opt_kernel<2><<<grid, 256, 0, s>>>(c->M, c->dM, sh, c->opt_s1, c->opt_s2, c->mem_size, c->neg_base, lr, b1, b2,
-                                       eps, wd, bc1, bc2, zero);
+    launch_opt_kind<2>(a, vec, s);
   return cudaGetLastError();
 }
 

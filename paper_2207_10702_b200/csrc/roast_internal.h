@@ -123,9 +123,8 @@ cudaError_t launch_simt_dw(const Ctx* c, const Module& m, const void* X, const v
                            roast_dtype_t dt, float* ws, cudaStream_t s);
 cudaError_t launch_det_reduce(const Ctx* c, const Module& m, const float* ws, int nsplit, cudaStream_t s);
 cudaError_t launch_sync_shadow(Ctx* c, cudaStream_t s);
-cudaError_t launch_sgd(Ctx* c, float lr, cudaStream_t s);
 cudaError_t launch_optimizer(Ctx* c, int kind, float lr, float b1, float b2, float eps, float wd, int64_t step,
-                             int zero, cudaStream_t s);
+                             int zero, bool touched_only, cudaStream_t s);
 cudaError_t launch_materialize(const Ctx* c, const Module& m, roast_dtype_t dt, void* W, cudaStream_t s);
 cudaError_t launch_embed_fwd(const Ctx* c, const Module& m, const int64_t* idx, int64_t n, float* out,
                              cudaStream_t s);

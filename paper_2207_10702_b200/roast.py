@@ -48,7 +48,7 @@ class roast_config_t(ctypes.Structure):
 class roast_opt_config_t(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("lr", ctypes.c_float), ("beta1", ctypes.c_float),
                 ("beta2", ctypes.c_float), ("eps", ctypes.c_float), ("weight_decay", ctypes.c_float),
-                ("zero_grad", ctypes.c_int32)]
+                ("zero_grad", ctypes.c_int32), ("touched_only", ctypes.c_int32)]
 
 
 OPT_SGD, OPT_ADAGRAD, OPT_ADAM = 0, 1, 2
@@ -333,8 +333,8 @@ def roast_sgd_step(h, lr, stream=0):
 
 
 def roast_optimizer_step(h, kind, lr, step=1, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, zero_grad=True,
-                         stream=0):
-    cfg = roast_opt_config_t(kind, lr, beta1, beta2, eps, weight_decay, int(zero_grad))
+                         stream=0, touched_only=False):
+    cfg = roast_opt_config_t(kind, lr, beta1, beta2, eps, weight_decay, int(zero_grad), int(touched_only))
     _check(_lib.roast_optimizer_step(h, ctypes.byref(cfg), step, stream), "roast_optimizer_step")
 
 

@@ -110,3 +110,34 @@ def test_touched_exchange_nccl_matches_dense(R, torch):
     torch.cuda.synchronize()
     assert torch.equal(ctx.dM, ref)
     ctx.close()
+
+
+@pytest.mark.parametrize("kind", [0, 2])
+def test_optimizer_touched_only_equals_dense_on_the_touched_set(R, torch, kind):
+    """Update restricted to the touched set: touched slots of M, state, shadow
+    and dM bit-identical to the dense pass; every other slot left as it was; the recovered
+    weights (what any module reads) identical."""
+    mem = 1 << 20
+    M0 = store(mem)
+    g = to_dev(synth.normal(11, (mem,)).astype(np.float32), torch.float32)
+    ctxs = []
+    for touched in (False, True):
+        ctx = R.Roast(to_dev(M0, torch.float32), 64, 64, seed=HS)
+        lid = ctx.linear(256, 512)
+        ctx.touched_size()
+        for t in (1, 2):
+            ctx.dM.copy_(g)
+            ctx.optimizer_step(kind, 1e-2, step=t, weight_decay=0.01, touched_only=touched)
+        torch.cuda.synchronize()
+        ctxs.append((ctx, lid))
+    (dense, l0), (tch, l1) = ctxs
+    spec = OM.LinearSpec(256, 512, 64, 64, mem, HS, l0)
+    inside = torch.tensor(_oracle_slots([spec], mem), device="cuda")
+    M0d = to_dev(M0, torch.float32)
+    assert torch.equal(tch.M[inside], dense.M[inside])
+    assert torch.equal(tch.M[~inside], M0d[~inside])
+    assert torch.count_nonzero(tch.dM[inside]).item() == 0 and torch.equal(tch.dM[~inside], g[~inside])
+    assert torch.equal(tch.materialize(l1, torch.bfloat16), dense.materialize(l0, torch.bfloat16))
+    assert torch.equal(tch.materialize(l1, torch.float32), dense.materialize(l0, torch.float32))
+    for c, _ in ctxs:
+        c.close()

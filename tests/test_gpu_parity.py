@@ -327,10 +327,10 @@ def test_embedding_deterministic_parity_and_reproducible(R, torch, dist, align):
 
 
 @pytest.mark.parametrize("kind,name", [(0, "sgd"), (1, "adagrad"), (2, "adam")])
-def test_optimizer_step_parity(R, torch, kind, name):
+@pytest.mark.parametrize("mem", [100_000, 100_003])   # 16-byte vector path / scalar path
+def test_optimizer_step_parity(R, torch, kind, name, mem):
     """NEXT #1: fused update of M + state + bf16 shadow (+ dM zeroing) vs the oracle formulas."""
     from oracle import optim as OO
-    mem = 100_003 - 3
     M_np = store(mem)
     ctx, M = make_ctx(R, torch, M_np, 64, 64)
     mid = ctx.linear(128, 128)

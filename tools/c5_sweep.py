@@ -6,7 +6,8 @@ replays; the 134 MB activations exceed the 126 MB L2, so no flush is needed):
   * ROAST fwd, dX, dM and the fwd + bwd sequence (effective TFLOP/s = 6 T H O / t);
   * dense cuBLAS fwd + bwd on the same virtual shape (materialised bf16 W);
   * the O(|M|) passes the paper's optimizer tables time: bf16 shadow refresh,
-    fused Adam step (+ shadow + dM zero), dM zeroing;
+    fused Adam step (+ shadow + dM zero; 36 B per slot of HBM traffic) over all of M and over
+    the touched set only, dM zeroing;
   * the exchange (a6 at W ranks): dense all-reduce bytes 4 |M| vs the touched-set exchange
     (4 n_touched) and the pack + unpack time it adds.
 
@@ -96,6 +97,7 @@ def main():
         t_adam = graph_time_us(lambda: ctx.optimizer_step(R.OPT_ADAM, 1e-3, step=1))
         t_zero = graph_time_us(ctx.zero_grad)
         n_touched, n_iv = ctx.touched_size()
+        t_adam_t = graph_time_us(lambda: ctx.optimizer_step(R.OPT_ADAM, 1e-3, step=1, touched_only=True))
         t_pack = graph_time_us(lambda: R.roast_debug_exchange(ctx.h, 1.0, torch.cuda.current_stream().cuda_stream))
         line = dict(config="C5 4096x4096 ROAST-MM, batch 16384, 1 B200", mem_elems=mem, mem_mb_fp32=mem * 4 / 2 ** 20,
                     compression=round(D * D / mem, 3), us=dict(fwd=round(t_fwd, 1), dx=round(t_dx, 1),
@@ -104,7 +106,8 @@ def main():
                     dense_tflops=round(flop / dense_us / 1e6, 1), roast_over_dense=round(dense_us / t_step, 3),
                     tuned={k: ctx.tuned(lid, j, T) for j, k in enumerate(("fwd", "dx", "dm"))},
                     o_m_passes_us=dict(sync_shadow=round(t_shadow, 1), adam_step=round(t_adam, 1),
-                                       zero_grad=round(t_zero, 1)),
+                                       adam_step_touched_only=round(t_adam_t, 1), zero_grad=round(t_zero, 1),
+                                       adam_hbm_gbs=round(36.0 * mem / t_adam / 1e3, 1)),
                     exchange=dict(dense_bytes=mem * 4, touched_elems=n_touched, touched_intervals=n_iv,
                                   touched_bytes=n_touched * 4, reduction=round(mem / max(n_touched, 1), 2),
                                   pack_unpack_us=round(t_pack, 1),
