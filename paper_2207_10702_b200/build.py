@@ -20,6 +20,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
+if os.environ.get("ROAST_DIAG"):   # timing-diagnostic knobs (ROAST_EXP) compiled in; never the product build
+    FLAGS.append("-DROAST_DIAG")
 
 
 def sources():

@@ -51,17 +51,8 @@ namespace sm100 {
 constexpr int BM = 128;   // accumulator rows per CTA
 constexpr int BN = 256;   // MMA N (columns of the output tile)
 constexpr int BK = 64;    // K per pipeline stage (one 128-byte swizzle row of bf16)
-#ifndef ROAST_EPI_WARPS
-#define ROAST_EPI_WARPS 4
-#endif
-// Epilogue warps: groups of four, one per TMEM lane quadrant (warp w may only read lanes
-// 32 (w % 4) ..); with 8 warps the two groups drain alternate 64-column steps.  FWD / DX: the
-// four warps of a group stage their 32-row slices of one 64-column step side by side and one
-// thread stores the 128-row box (one TMA op per 16 KB: the store op rate, not bytes, bounded
-// the per-warp 4 KB stores).
-constexpr int EPI_WARPS = ROAST_EPI_WARPS;
+constexpr int NUM_THREADS = 256;
 constexpr int EPI_WARP0 = 4;
-constexpr int NUM_THREADS = 32 * (EPI_WARP0 + EPI_WARPS);
 constexpr int TMEM_COLS = 512;
 constexpr int KB_CHUNK = 64;  // k-blocks whose tile coordinates are staged in smem at a time
 
@@ -72,10 +63,8 @@ struct Cfg {
   static constexpr int A_BYTES = BM * WM * BK * 2;       // this CTA's 128*WM rows of A
   static constexpr int B_BYTES = (BN / CG) * BK * 2;     // this CTA's BN/CG columns of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int NBUF = EPI_WARPS >= 8 ? 1 : 2;    // epilogue staging buffers per warp
-  static constexpr int STAGING = EPI_WARPS * NBUF * 4096;  // EPI_WARPS x NBUF x (32 rows x 128 B)
-  // FWD / DX: group g's buffer b = 4 consecutive 4 KB slices (quadrant q at q * 4 KB) = one
-  // [128 rows x 128 B] SW128 box at sStage + (g * NBUF + b) * 16 KB; DW: per-warp 4 KB buffers.
+  static constexpr int NBUF = 2;                         // epilogue staging buffers per warp
+  static constexpr int STAGING = 4 * NBUF * 4096;        // 4 warps x NBUF x (32 rows x 128 B)
   static constexpr int FIXED = STAGING + 1024 + 256 + KB_CHUNK * 4 * 4;
   static constexpr int STAGES = (227 * 1024 - FIXED) / STAGE_BYTES > 6 ? 6 : (227 * 1024 - FIXED) / STAGE_BYTES;
   static constexpr int B_SUB = 4 / CG;                   // 64-wide B sub-tiles per CTA
@@ -83,6 +72,12 @@ struct Cfg {
 };
 
 enum Mode { FWD = 0, DX = 1, DW = 2 };
+
+#ifdef ROAST_DIAG
+#define DIAG(p) ((p).exp)
+#else
+#define DIAG(p) 0
+#endif
 
 struct WMaps {
   CUtensorMap m[8];  // shadow viewed from base + 16 r bytes, r = 0..7
@@ -107,16 +102,16 @@ struct Params {
   long long* prof;      // debug (ROAST_PROF): per-CTA cycle counters, else null
   int epi;              // 0: TMA bulk store / reduce from staging; 1: coalesced st.global / red.global.v4
   int dw3d;             // DW operands loaded as one 3-D TMA box per operand (else 64x64 2-D boxes)
-  // diagnostics only (ROAST_EXP; timing experiments, results are garbage): bit 0 skips the epilogue
-  // drain, 1 all operand loads, 2 uses one shadow phase map, 3 reads every B tile from row 0, 4 skips
-  // the B loads, 5 the A loads, 6 the output stores, 7 the staging + stores
+  // diagnostics only (built with -DROAST_DIAG, set by ROAST_EXP; tools/prof_shapes.py; results
+  // are garbage): bit 0 skips the epilogue drain, 1 all operand loads, 4 the B loads, 5 the A
+  // loads, 6 the output stores.  Compiled out of the product build.
   int exp;
   // chain mode (FWD / DX only; set in the first problem's Params): two GEMMs in one persistent
   // launch, problem 1's A = problem 0's output.  Each pair walks its own static unit list
   // sched[pair * sched_len + i] = prob << 24 | unit (-1 = end), every problem-0 unit before any
   // problem-1 unit (so the waits below cannot deadlock).  flags[u0] counts the epilogue warps
   // whose TMA stores of problem-0 unit u0 are complete; problem 1 loads k-block kb of m-block mb
-  // only after flags[mb * n_tiles0 + kb / 4] == EPI_WARPS * CG.
+  // only after flags[mb * n_tiles0 + kb / 4] == 4 * CG.
   int chain;
   const int32_t* sched;
   int sched_len;
@@ -334,7 +329,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], EPI_WARPS * CG);
+      mbar_init(&tempty[a], 4 * CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_map(&mapA);
@@ -390,8 +385,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // out-of-range blocks are zero-filled and still counted
       const uint32_t tx = MODE == DW ? (p.dw3d ? uint32_t(CG * (C::A_BYTES + C::B_BYTES))
                                                : uint32_t((m_sub_pair + n_sub) * 64 * 64 * 2))
-                                     : uint32_t(((p.exp & 32) ? 0 : CG * C::A_BYTES) +
-                                                ((p.exp & 16) ? 0 : n_sub * 64 * 64 * 2));
+                                     : uint32_t(((DIAG(p) & 32) ? 0 : CG * C::A_BYTES) +
+                                                ((DIAG(p) & 16) ? 0 : n_sub * 64 * 64 * 2));
       for (int kc = kb0; kc < kb1; kc += KB_CHUNK) {
         const int kc1 = min(kc + KB_CHUNK, kb1);
         if (MODE != DW) {
@@ -410,10 +405,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint8_t* a = sA + s * C::A_BYTES;
             uint8_t* b = sB + s * C::B_BYTES;
             const uint32_t fb = CG == 2 ? map_to_rank(smem_u32(&full[s]), 0) : smem_u32(&full[s]);
-            if (p.exp & 2) {   // diagnostics: MMAs on stale smem, no operand traffic
+            if (DIAG(p) & 2) {   // diagnostics: MMAs on stale smem, no operand traffic
               if (leader) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
             } else if (leader) mbar_expect_tx(&full[s], tx);
-            if (p.exp & 2) {
+            if (DIAG(p) & 2) {
             } else if (MODE == DW && p.dw3d) {
               tma_load_3d<CG>(mA, a, fb, 0, kb * BK, row0 >> 6);
               tma_load_3d<CG>(&mapB, b, fb, 0, kb * BK, (nb * BN + j0 * 64) >> 6);
@@ -423,16 +418,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 tma_load_2d<CG>(&mapB, b + (j - j0) * 8192, fb, nb * BN + j * 64, kb * BK);
             } else {
               // chain: these 64 columns of A are problem 0's output tile (mb, kb / 4)
-              if (CHAIN && prob == 1 && (kb & 3) == 0) wait_ready(p0.flags + mb * p0.n_tiles + (kb >> 2), EPI_WARPS * CG);
-              if (!(p.exp & 32)) tma_load_2d<CG>(mA, a, fb, kb * BK, row0);
+              if (CHAIN && prob == 1 && (kb & 3) == 0) wait_ready(p0.flags + mb * p0.n_tiles + (kb >> 2), 4 * CG);
+              if (!(DIAG(p) & 32)) tma_load_2d<CG>(mA, a, fb, kb * BK, row0);
               const int32_t* cc = sCoord + (kb - kc) * 4;
-              for (int j = j0; j < j1 && !(p.exp & 16); ++j) {
+              for (int j = j0; j < j1 && !(DIAG(p) & 16); ++j) {
                 // FWD: tile (x = kb, y = nb*4 + j); DX: tile (x = nb*4 + j, y = kb).
                 // Packed: row << 4 | neg << 3 | phase; negative tiles read the negated shadow.
                 const int32_t c = cc[j];
-                int row = (c >> 4) + ((c & 8) ? int(p.neg_row) : 0);
-                if (p.exp & 8) row = 0;
-                tma_load_2d<CG>(&wmaps.m[(p.exp & 4) ? 0 : (c & 7)], b + (j - j0) * 8192, fb, 0, row);
+                const int row = (c >> 4) + ((c & 8) ? int(p.neg_row) : 0);
+                tma_load_2d<CG>(&wmaps.m[c & 7], b + (j - j0) * 8192, fb, 0, row);
               }
             }
             if (++s == C::STAGES) {
@@ -501,8 +495,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp >= EPI_WARP0) {
     // ===================== epilogue: TMEM -> registers -> global =====================
     const int q = warp & 3;          // TMEM lane quadrant this warp may access
-    const int egrp = (warp - EPI_WARP0) >> 2;    // epilogue group (8 warps: alternate steps)
-    const int ehalf = egrp;
     const int row = q * 32 + lane;   // accumulator row owned by this thread
     const uint32_t tempty_leader0 = CG == 2 ? map_to_rank(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
     int stg = 0;   // staging buffer counter (double buffer per warp)
@@ -584,27 +576,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) pk[i] = __float_as_uint(scale * __uint_as_float(r[i]));
           }
-          const bool grouped = MODE != DW && p.epi == 0;
-          uint8_t* buf = grouped ? sStage + (egrp * C::NBUF + stg % C::NBUF) * 16384 + q * 4096
-                                 : sStage + (warp - EPI_WARP0) * (C::NBUF * 4096) + (stg % C::NBUF) * 4096;
+          uint8_t* buf = sStage + (warp - EPI_WARP0) * (C::NBUF * 4096) + (stg % C::NBUF) * 4096;
           long long e1 = p.prof ? clock64() : 0;
-          if (lane == 0 && p.epi == 0 && !grouped) {
-            if (C::NBUF == 1)
-              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            else
-              asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          }
+          if (lane == 0 && p.epi == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           __syncwarp();
           long long e2 = p.prof ? clock64() : 0;
           if (p.prof) prof_epi[1] += e2 - e1;
-          if (p.exp & 128) {   // diagnostics: keep the math, drop staging + store
-            uint32_t x = 0;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) x ^= pk[i];
-            if (x == 0x12345678u) p.out[0] = __nv_bfloat16();
-            ++stg;
-            return;
-          }
 #pragma unroll
           for (int cc = 0; cc < 8; ++cc) {
             const uint32_t a = smem_u32(buf + lane * 128 + ((cc ^ (lane & 7)) << 4));
@@ -642,27 +619,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           long long e3 = p.prof ? clock64() : 0;
           if (p.prof) prof_epi[2] += e3 - e2;
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          if (grouped) {
-            // the issuer's previous store must have finished reading the other buffer (written
-            // next step) before the group passes this barrier; after it, all four slices of this
-            // step are in smem and visible to the async proxy
-            if (q == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            asm volatile("bar.sync %0, 128;" ::"r"(1 + egrp) : "memory");
-            if (p.prof) prof_epi[3] += clock64() - e3;
-            if (q == 0 && lane == 0 && !(p.exp & 64)) {
-              const int x0 = nb * BN + c * 64, y0 = row_base;
-              asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                               reinterpret_cast<uint64_t>(mO)),
-                           "r"(x0), "r"(y0), "r"(smem_u32(buf))
-                           : "memory");
-              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            }
-            ++stg;
-            return;
-          }
           __syncwarp();
           if (p.prof) prof_epi[3] += clock64() - e3;
-          if (lane == 0 && !(p.exp & 64)) {
+          if (lane == 0 && !(DIAG(p) & 64)) {
             const uint32_t sb = smem_u32(buf);
             if (MODE != DW) {
               const int x0 = nb * BN + c * 64, y0 = row_base + q * 32;
@@ -690,7 +649,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ++stg;
         };
         uint32_t ra[64];
-        for (int c = ehalf; c < ((p.exp & 1) ? 0 : nsteps); c += EPI_WARPS / 4) {
+        for (int c = 0; c < ((DIAG(p) & 1) ? 0 : nsteps); ++c) {
           long long e0 = p.prof ? clock64() : 0;
           tload(c, ra);
           tmem_wait_ld();
@@ -822,7 +781,7 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(smem)");
     attr = true;
   }
-  int pairs = grid_pairs > 0 ? grid_pairs : std::min(p.units, num_sms() / CG);
+  const int pairs = grid_pairs > 0 ? grid_pairs : std::min(p.units, num_sms() / CG);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(pairs * CG));
   cfg.blockDim = dim3(NUM_THREADS);
@@ -982,8 +941,8 @@ static roast_status_t tok_major_launch(Ctx* c, const Module& m, const void* A, v
   p.bias = dx ? nullptr : bias;
   p.coord = coord;
   p.coord_ld = coord_ld;
-  CUtensorMap o;   // output [T x N] bf16, stored 128 rows x 64 columns per TMA op (epi 0) or by st.global
-  st = make_map_2d(&o, out, uint64_t(N), uint64_t(T), uint64_t(N) * 2, 64, 128);
+  CUtensorMap o;   // output [T x N] bf16, stored 32 rows x 64 columns per TMA op
+  st = make_map_2d(&o, out, uint64_t(N), uint64_t(T), uint64_t(N) * 2, 64, 32);
   if (st) return st;
   const WMaps& w = *reinterpret_cast<const WMaps*>(c->tmap_shadow);
   st = dx ? launch<DX>(a, a, o, w, p, wm, s) : launch<FWD>(a, a, o, w, p, wm, s);
@@ -1141,7 +1100,7 @@ roast_status_t sm100_chain(Ctx* c, const Module& m0, const Module& m1, const voi
                   CUtensorMap& ma, CUtensorMap& mo) -> roast_status_t {
     roast_status_t r = make_map_2d(&ma, A, uint64_t(K), uint64_t(T), uint64_t(K) * 2, BK, BM * WMC);
     if (r) return r;
-    r = make_map_2d(&mo, out, uint64_t(N), uint64_t(T), uint64_t(N) * 2, 64, 128);
+    r = make_map_2d(&mo, out, uint64_t(N), uint64_t(T), uint64_t(N) * 2, 64, 32);
     if (r) return r;
     p = base_params(c, m, T);
     p.M = int(T);

@@ -6,6 +6,7 @@ epilogue drain, 2 = no TMA operand loads, 3 = MMAs only) next to cuBLAS on the s
 virtual shape.  The gaps between the four say what bounds each kernel: MMA issue, operand
 feed, or the accumulator drain.  Timing only: diagnostic launches compute garbage.
 
+    ROAST_DIAG=1 python -m paper_2207_10702_b200.build -f    # knobs are compiled out otherwise
     python tools/prof_shapes.py [--T 8192] [--exps 0,1,2,3]
 """
 import argparse
