@@ -58,10 +58,13 @@ constexpr int KB_CHUNK = 64;  // k-blocks whose tile coordinates are staged in s
 
 // CG: CTAs per MMA (cta_group). WM: M sub-tiles of 128 rows per CTA sharing each B load
 // (WM = 2 uses both 256-column TMEM halves for one unit, so the accumulator is single-buffered).
-template <int CG, int WM>
+// NU: output columns per unit (MMA N): 256, or 192 (DX, CG = 2, WM = 2 only) for N = 768-wide
+// outputs, whose 48 units of 512 x 256 leave 26 of 74 CTA pairs idle (64 units of 512 x 192
+// fill one round of 74 with 25 % less work per unit).
+template <int CG, int WM, int NU = BN>
 struct Cfg {
   static constexpr int A_BYTES = BM * WM * BK * 2;       // this CTA's 128*WM rows of A
-  static constexpr int B_BYTES = (BN / CG) * BK * 2;     // this CTA's BN/CG columns of B
+  static constexpr int B_BYTES = (NU / CG) * BK * 2;     // this CTA's NU/CG columns of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int NBUF = 2;                         // epilogue staging buffers per warp
   static constexpr int STAGING = 4 * NBUF * 4096;        // 4 warps x NBUF x (32 rows x 128 B)
@@ -81,6 +84,9 @@ enum Mode { FWD = 0, DX = 1, DW = 2 };
 
 struct WMaps {
   CUtensorMap m[8];  // shadow viewed from base + 16 r bytes, r = 0..7
+};
+struct WMapsHalf {
+  CUtensorMap m[8];  // the same views with 32-row boxes (half hash tiles, NU = 192)
 };
 
 struct Params {
@@ -251,10 +257,10 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uin
   return d;
 }
 
-// Instruction descriptor: bf16 x bf16 -> f32, M = 128 * CG, N = 256.
-__host__ __device__ constexpr uint32_t make_idesc(int a_mn_major, int b_mn_major, int m) {
+// Instruction descriptor: bf16 x bf16 -> f32, M = 128 * CG, N = n.
+__host__ __device__ constexpr uint32_t make_idesc(int a_mn_major, int b_mn_major, int m, int n = BN) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(a_mn_major) << 15) | (uint32_t(b_mn_major) << 16) |
-         (uint32_t(BN >> 3) << 17) | (uint32_t(m >> 4) << 24);
+         (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
 }
 
 // spin until *flag >= target (acquire), then order the async proxy (TMA loads) after it
@@ -277,13 +283,15 @@ __device__ __forceinline__ void decode_unit(const Params& p, int u, int& mb, int
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int MODE, int CG, int WM, bool CHAIN = false>
+template <int MODE, int CG, int WM, bool CHAIN = false, int NU = BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     roast_mm_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ WMaps wmaps,
                    const __grid_constant__ Params p0, const __grid_constant__ CUtensorMap mapA1,
-                   const __grid_constant__ CUtensorMap mapOut1, const __grid_constant__ Params p1) {
-  using C = Cfg<CG, WM>;
+                   const __grid_constant__ CUtensorMap mapOut1, const __grid_constant__ Params p1,
+                   const __grid_constant__ WMapsHalf hmaps) {
+  static_assert(NU == BN || (NU == 192 && MODE == DX && CG == 2 && WM == 2 && !CHAIN), "NU = 192: DX, 2 x 2 only");
+  using C = Cfg<CG, WM, NU>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                        // [STAGES][A_BYTES]
@@ -372,7 +380,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       decode_unit(p, u, mb, nb, split);
       const int kb0 = split * p.kb_per_split;
       const int kb1 = min(kb0 + p.kb_per_split, p.k_blocks);
-      const int n_sub = min(4, (p.N - nb * BN) / 64);   // valid 64-wide N sub-tiles of the unit
+      const int n_sub = min(NU / 64, (p.N - nb * NU) / 64);   // valid 64-wide N sub-tiles of the unit
       // this CTA's B sub-tiles: [j0, j1)
       const int j0 = int(rank) * C::B_SUB;
       const int j1 = min(j0 + C::B_SUB, n_sub);
@@ -393,7 +401,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
           for (int i = lane; i < (kc1 - kc) * 4; i += 32) {
             const int j = i & 3;
-            sCoord[i] = j < n_sub ? __ldg(p.coord + int64_t(kc + (i >> 2)) * p.coord_ld + nb * 4 + j) : 0;
+            sCoord[i] = j < n_sub ? __ldg(p.coord + int64_t(kc + (i >> 2)) * p.coord_ld + nb * (NU / 64) + j) : 0;
           }
           __syncwarp();
         }
@@ -421,7 +429,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (CHAIN && prob == 1 && (kb & 3) == 0) wait_ready(p0.flags + mb * p0.n_tiles + (kb >> 2), 4 * CG);
               if (!(DIAG(p) & 32)) tma_load_2d<CG>(mA, a, fb, kb * BK, row0);
               const int32_t* cc = sCoord + (kb - kc) * 4;
-              for (int j = j0; j < j1 && !(DIAG(p) & 16); ++j) {
+              if (NU == 192 && !(DIAG(p) & 16)) {
+                // 96 B rows (N) per CTA: rank 0 = tile 0 + rows 0-31 of tile 1, rank 1 = rows
+                // 32-63 of tile 1 + tile 2; every piece lands at a 1024-B multiple (SW128 phase)
+                const int32_t ca = cc[rank ? 1 : 0], cb = cc[rank ? 2 : 1];
+                const int ra = (ca >> 4) + ((ca & 8) ? int(p.neg_row) : 0);
+                const int rb = (cb >> 4) + ((cb & 8) ? int(p.neg_row) : 0);
+                if (rank == 0) {
+                  tma_load_2d<CG>(&wmaps.m[ca & 7], b, fb, 0, ra);
+                  tma_load_2d<CG>(&hmaps.m[cb & 7], b + 8192, fb, 0, rb);
+                } else {
+                  tma_load_2d<CG>(&hmaps.m[ca & 7], b, fb, 0, ra + 32);
+                  tma_load_2d<CG>(&wmaps.m[cb & 7], b + 4096, fb, 0, rb);
+                }
+              }
+              for (int j = j0; j < j1 && NU == BN && !(DIAG(p) & 16); ++j) {
                 // FWD: tile (x = kb, y = nb*4 + j); DX: tile (x = nb*4 + j, y = kb).
                 // Packed: row << 4 | neg << 3 | phase; negative tiles read the negated shadow.
                 const int32_t c = cc[j];
@@ -440,7 +462,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ===================== MMA issuer (leader CTA, single thread) =====================
-      constexpr uint32_t idesc = make_idesc(MODE == DW ? 1 : 0, MODE == FWD || MODE == DW ? 1 : 0, BM * CG);
+      constexpr uint32_t idesc = make_idesc(MODE == DW ? 1 : 0, MODE == FWD || MODE == DW ? 1 : 0, BM * CG, NU);
       // B descriptor strides: MN-major = 64-col sub-tiles 8 KB apart; K-major = 8-row groups 1 KB apart
       int s = 0;
       uint32_t ph = 0;
@@ -507,7 +529,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const CUtensorMap* mO = (CHAIN && prob) ? &mapOut1 : &mapOut;
       int mb, nb, split;
       decode_unit(p, u, mb, nb, split);
-      const int n_valid = min(BN, p.N - nb * BN);
+      const int n_valid = min(NU, p.N - nb * NU);
       // DW: each warp's 32 rows of sub-tile j lie in one hash-tile row x; lanes 0..3
       // fetch the (offset, lambda*g) of tiles (x, 4 nb + lane) before the accumulator wait.
       int64_t t_off[WM];
@@ -552,7 +574,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           int64_t tb = 0;
           if (MODE == FWD && p.bias) {
             // Y = bf16(lambda acc + b): the 64 columns' bias, broadcast to every lane from L1
-            const float4* b4 = reinterpret_cast<const float4*>(p.bias + nb * BN + c * 64);
+            const float4* b4 = reinterpret_cast<const float4*>(p.bias + nb * NU + c * 64);
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const float4 bv = __ldg(b4 + i);
@@ -602,7 +624,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                            : "r"(smem_u32(buf + rr * 128 + ((ch ^ (rr & 7)) << 4))));
               if (MODE != DW) {
                 const int64_t m = int64_t(rb) + rr;
-                if (m < p.T) *reinterpret_cast<uint4*>(p.out + m * p.N + nb * BN + c * 64 + ch * 8) = v;
+                if (m < p.T) *reinterpret_cast<uint4*>(p.out + m * p.N + nb * NU + c * 64 + ch * 8) = v;
               } else if (rb < p.M) {
                 float* dst = (p.ws ? p.ws : p.dM) + tb + ((rb + rr) & 63) * 64 + (c & 1) * 32 + ch * 4;
                 const float4 f = make_float4(__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z),
@@ -624,7 +646,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (lane == 0 && !(DIAG(p) & 64)) {
             const uint32_t sb = smem_u32(buf);
             if (MODE != DW) {
-              const int x0 = nb * BN + c * 64, y0 = row_base + q * 32;
+              const int x0 = nb * NU + c * 64, y0 = row_base + q * 32;
               asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                                reinterpret_cast<uint64_t>(mO)),
                            "r"(x0), "r"(y0), "r"(sb)
@@ -769,15 +791,15 @@ int cta_group() {
   return cg;
 }
 
-template <int MODE, int CG, int WM, bool CHAIN = false>
+template <int MODE, int CG, int WM, bool CHAIN = false, int NU = BN>
 roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o, const WMaps& w,
                          const Params& p, const CUtensorMap& a1, const CUtensorMap& o1, const Params& p1,
-                         int grid_pairs, cudaStream_t s) {
-  using C = Cfg<CG, WM>;
+                         int grid_pairs, cudaStream_t s, const WMapsHalf* hw = nullptr) {
+  using C = Cfg<CG, WM, NU>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
-        cudaFuncSetAttribute(roast_mm_sm100<MODE, CG, WM, CHAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(roast_mm_sm100<MODE, CG, WM, CHAIN, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(smem)");
     attr = true;
   }
@@ -804,7 +826,9 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
     pp.prof = prof;
     pp1.prof = prof;
   }
-  cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mm_sm100<MODE, CG, WM, CHAIN>, a, b, o, w, pp, a1, o1, pp1);
+  static const WMapsHalf no_half{};
+  cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mm_sm100<MODE, CG, WM, CHAIN, NU>, a, b, o, w, pp, a1, o1, pp1,
+                                     hw ? *hw : no_half);
   if (e != cudaSuccess) return cuda_fail(e, "roast_mm_sm100 launch");
   if (pp.prof) {
     cudaDeviceSynchronize();
@@ -825,7 +849,10 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
 
 template <int MODE>
 roast_status_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o, const WMaps& w, Params p,
-                      int wm, cudaStream_t s) {
+                      int wm, cudaStream_t s, int nu = BN, const WMapsHalf* hw = nullptr) {
+  if constexpr (MODE == DX) {
+    if (nu == 192) return launch_cg<DX, 2, 2, false, 192>(a, b, o, w, p, a, o, p, 0, s, hw);
+  }
   if (cta_group() == 1) return launch_cg<MODE, 1, 1>(a, b, o, w, p, a, o, p, 0, s);
   return wm == 2 ? launch_cg<MODE, 2, 2>(a, b, o, w, p, a, o, p, 0, s)
                  : launch_cg<MODE, 2, 1>(a, b, o, w, p, a, o, p, 0, s);
@@ -839,10 +866,14 @@ using namespace sm100;
 roast_status_t sm100_prepare(Ctx* c) {
   if (c->tmap_shadow_valid) return ROAST_OK;
   static_assert(sizeof(WMaps) <= sizeof(Ctx::tmap_shadow), "tmap storage");
+  static_assert(sizeof(WMapsHalf) <= sizeof(Ctx::tmap_shadow_half), "tmap storage");
   WMaps* w = reinterpret_cast<WMaps*>(c->tmap_shadow);
+  WMapsHalf* hw = reinterpret_cast<WMapsHalf*>(c->tmap_shadow_half);
   for (int r = 0; r < 8; ++r) {
     const int64_t elems = c->shadow_elems - 8 * r;
     roast_status_t st = make_map_2d(&w->m[r], c->shadow + 8 * r, 64, uint64_t(elems / 64), 128, 64, 64);
+    if (st) return st;
+    st = make_map_2d(&hw->m[r], c->shadow + 8 * r, 64, uint64_t(elems / 64), 128, 64, 32);
     if (st) return st;
   }
   c->tmap_shadow_valid = true;
@@ -922,9 +953,10 @@ float time_candidate(F&& f, cudaStream_t s) {
 }  // namespace
 
 // FWD / DX share the geometry: M = tokens, N = the module's output side, K = its input side.
+// nu = output columns per unit (256, or 192 for DX with WM = 2).
 static roast_status_t tok_major_launch(Ctx* c, const Module& m, const void* A, void* out, int64_t T, int N, int K,
                                        const int32_t* coord, int coord_ld, bool dx, int wm, const float* bias,
-                                       cudaStream_t s) {
+                                       cudaStream_t s, int nu = BN) {
   CUtensorMap a;
   roast_status_t st = make_map_2d(&a, A, uint64_t(K), uint64_t(T), uint64_t(K) * 2, BK, BM * wm);
   if (st) return st;
@@ -933,7 +965,7 @@ static roast_status_t tok_major_launch(Ctx* c, const Module& m, const void* A, v
   p.N = N;
   p.K = K;
   p.m_tiles = int((T + BM * cta_group() * wm - 1) / (BM * cta_group() * wm));
-  p.n_tiles = (p.N + BN - 1) / BN;
+  p.n_tiles = (p.N + nu - 1) / nu;
   p.k_blocks = p.K / BK;
   p.kb_per_split = p.k_blocks;
   p.units = p.m_tiles * p.n_tiles;
@@ -945,9 +977,27 @@ static roast_status_t tok_major_launch(Ctx* c, const Module& m, const void* A, v
   st = make_map_2d(&o, out, uint64_t(N), uint64_t(T), uint64_t(N) * 2, 64, 32);
   if (st) return st;
   const WMaps& w = *reinterpret_cast<const WMaps*>(c->tmap_shadow);
-  st = dx ? launch<DX>(a, a, o, w, p, wm, s) : launch<FWD>(a, a, o, w, p, wm, s);
+  const WMapsHalf* hw = reinterpret_cast<const WMapsHalf*>(c->tmap_shadow_half);
+  st = dx ? launch<DX>(a, a, o, w, p, wm, s, nu, hw) : launch<FWD>(a, a, o, w, p, wm, s);
   if (!st) c->launches++;
   return st;
+}
+
+// (WM, N per unit) configurations a FWD / DX launch may use; the tuned map stores N / 64 in
+// the `splits` slot (legacy 1 = 256)
+static bool nu192_ok(bool dx, int wm, int N) { return dx && wm == 2 && cta_group() == 2 && N % 192 == 0; }
+
+// makespan model (no tuning): rounds of units over the CTA pairs x per-unit MMA work
+static void choose_tok_major(int64_t T, int N, bool dx, int& wm, int& nu) {
+  wm = choose_wm(T, (N + BN - 1) / BN, 1);
+  nu = BN;
+  if (nu192_ok(dx, wm, N) && !getenv("ROAST_NO_NU192")) {
+    const int pairs = num_sms() / 2;
+    const int64_t mt = (T + 511) / 512;
+    const double c256 = double((mt * ((N + 255) / 256) + pairs - 1) / pairs) * 256;
+    const double c192 = double((mt * (N / 192) + pairs - 1) / pairs) * 192;
+    if (c192 < c256) nu = 192;
+  }
 }
 
 static roast_status_t run_tok_major(Ctx* c, const Module& m, const void* A, void* out, int64_t T, int N, int K,
@@ -958,26 +1008,30 @@ static roast_status_t run_tok_major(Ctx* c, const Module& m, const void* A, void
   const auto key = tune_key(dx ? kTuneDx : kTuneFwd, m, T);
   auto it = c->tuned.find(key);
   auto fwd = c->tuned.find(tune_key(kTuneFwd, m, T));
-  int wm;
+  int wm, nu;
+  choose_tok_major(T, N, dx, wm, nu);
   if (it != c->tuned.end()) {
     wm = it->second.first;
+    nu = it->second.second == 3 && nu192_ok(dx, wm, N) ? 192 : BN;
   } else if (dx && c->autotune == ROAST_TUNE_INFERENCE && fwd != c->tuned.end()) {
     wm = fwd->second.first;   // inference-optimal: the backward shares the forward's tile
+    nu = BN;
   } else if ((!dx || c->autotune == ROAST_TUNE_TRAINING) && can_tune(c, s)) {
     float best = 1e30f;
-    wm = choose_wm(T, (N + BN - 1) / BN, 1);
-    for (int w = 1; w <= (cta_group() == 2 ? 2 : 1); ++w) {
-      const float ms = time_candidate([&] { return tok_major_launch(c, m, A, out, T, N, K, coord, coord_ld, dx, w, bias, s); }, s);
-      if (ms >= 0.f && ms < best) {
-        best = ms;
-        wm = w;
+    for (int w = 1; w <= (cta_group() == 2 ? 2 : 1); ++w)
+      for (int u : {BN, 192}) {
+        if (u == 192 && !nu192_ok(dx, w, N)) continue;
+        const float ms = time_candidate(
+            [&] { return tok_major_launch(c, m, A, out, T, N, K, coord, coord_ld, dx, w, bias, s, u); }, s);
+        if (ms >= 0.f && ms < best) {
+          best = ms;
+          wm = w;
+          nu = u;
+        }
       }
-    }
-    c->tuned[key] = {wm, 1};
-  } else {
-    wm = choose_wm(T, (N + BN - 1) / BN, 1);
+    c->tuned[key] = {wm, nu / 64};
   }
-  return tok_major_launch(c, m, A, out, T, N, K, coord, coord_ld, dx, wm, bias, s);
+  return tok_major_launch(c, m, A, out, T, N, K, coord, coord_ld, dx, wm, bias, s, nu);
 }
 
 roast_status_t sm100_fwd(Ctx* c, const Module& m, const void* X, void* Y, int64_t T, const float* bias,

@@ -64,6 +64,7 @@ struct Ctx {
   int64_t launches = 0;
   // tcgen05 path: cached TMA descriptors of the shadow (rebuilt on bind)
   alignas(64) unsigned char tmap_shadow[1024];
+  alignas(64) unsigned char tmap_shadow_half[1024];   // the same views with 32-row boxes (DX, N per unit 192)
   bool tmap_shadow_valid = false;
   // ... and of dM (8 fp32 phase views for the TMA reduce-add epilogue), valid for dM == tmap_dm_for
   alignas(64) unsigned char tmap_dm[1024];

@@ -592,6 +592,25 @@ def test_chain_fwd_and_dx_match_single_calls(R, torch, T):
         assert rel_frob(dX.float().cpu().numpy(), sa.backward_dx(dYa_np, M_np, True)) <= 1e-2
 
 
+@pytest.mark.parametrize("H,O,T", [(768, 3072, 8192), (768, 3072, 1000), (3072, 768, 129), (768, 192, 513)])
+def test_dx_192_column_units(R, torch, H, O, T):
+    """dX with 512 x 192 units (N per unit = 3 hash tiles; each CTA of the pair stages 1.5 of
+    them as K-major B: a 64-row and a 32-row TMA box of the shadow) == oracle."""
+    mem = 47192
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64)
+    mid = ctx.linear(H, O)
+    ctx.set_tuned(mid, 1, T, 2, 3)
+    dY_np = bf16_input(synth.SEED_DY, (T, O))
+    dX = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
+    ctx.bwd_dx(mid, to_dev(dY_np, torch.bfloat16), dX)
+    torch.cuda.synchronize()
+    spec = OM.LinearSpec(H, O, 64, 64, mem, HS, mid)
+    assert ctx.tuned(mid, 1, T) == (2, 3)
+    assert rel_frob(dX.float().cpu().numpy(), spec.backward_dx(dY_np, M_np, True)) <= 1e-2
+    ctx.check()
+
+
 def test_set_tuned_seeds_the_cache(R, torch):
     """roast_set_tuned (a saved tuning): the given WM / split-K is used and results keep parity;
     invalid choices are rejected."""
