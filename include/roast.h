@@ -289,6 +289,18 @@ typedef struct {
 } roast_opt_config_t;
 roast_status_t roast_optimizer_step(roast_t h, const roast_opt_config_t* cfg, int64_t step, roast_stream_t stream);
 
+/* NEXT #1, the exchange fused with its consumer: a6 + the update in one call.  Dense
+ * exchange (see roast_set_exchange): in-place ncclAllReduce of dM, then the optimizer pass
+ * over |M|.  Touched exchange (AUTO / TOUCHED mode, or cfg->touched_only): pack the touched
+ * intervals, all-reduce the packed buffer, and the optimizer pass over the touched slots
+ * reads the summed gradient directly from the packed buffer (the unpack pass and its dM
+ * round trip disappear) and zeroes dM there.  Same M, state and shadow as
+ * roast_grad_allreduce + roast_optimizer_step (touched_only = the mode's choice) bit for bit.
+ * Without a communicator (world 1) the exchange is the identity.  dM afterwards: zero on
+ * the touched slots if zero_grad, else the summed gradient.  Errors as roast_optimizer_step. */
+roast_status_t roast_grad_exchange_step(roast_t h, const roast_opt_config_t* cfg, int64_t step,
+                                        roast_stream_t stream);
+
 /* Sticky device-side error (synchronises the handle's bound stream is NOT done:
  * call after a stream synchronize to observe faults of completed work). */
 roast_status_t roast_get_error(roast_t h);

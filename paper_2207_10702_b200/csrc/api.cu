@@ -57,6 +57,32 @@ static void free_module(Module& m) {
 
 using namespace roast;
 
+namespace roast {
+// validation + lazily allocated optimizer state + (touched) interval tables, shared by
+// roast_optimizer_step and roast_grad_exchange_step
+roast_status_t opt_prepare(Ctx* c, const roast_opt_config_t* cfg, int64_t step, bool need_touched, cudaStream_t s) {
+  if (!c || !c->M || !c->shadow) return fail(ROAST_ERR_STATE, "not bound");
+  if (!cfg || cfg->kind < ROAST_OPT_SGD || cfg->kind > ROAST_OPT_ADAM) return fail(ROAST_ERR_CONFIG, "bad optimizer");
+  if (cfg->kind == ROAST_OPT_ADAM && step < 1) return fail(ROAST_ERR_CONFIG, "Adam step must be >= 1");
+  const size_t bytes = size_t(c->mem_size) * sizeof(float);
+  if (cfg->kind >= ROAST_OPT_ADAGRAD && !c->opt_s1) {
+    ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->opt_s1), bytes));
+    ROAST_CUDA_CHECK(cudaMemsetAsync(c->opt_s1, 0, bytes, s));
+  }
+  if (cfg->kind == ROAST_OPT_ADAM && !c->opt_s2) {
+    ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->opt_s2), bytes));
+    ROAST_CUDA_CHECK(cudaMemsetAsync(c->opt_s2, 0, bytes, s));
+  }
+  if (need_touched && !(c->touched_valid && c->touched_for == int64_t(c->modules.size()))) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+      return fail(ROAST_ERR_STATE, "touched set: call roast_touched_size before capturing");
+    if (roast_status_t st = touched_prepare(c, s)) return st;
+  }
+  return ROAST_OK;
+}
+}  // namespace roast
+
 extern "C" {
 
 void roast_config_default(roast_config_t* cfg) {
@@ -626,29 +652,11 @@ roast_status_t roast_sgd_step(roast_t h, float lr, roast_stream_t stream) {
   return ROAST_OK;
 }
 
+
 roast_status_t roast_optimizer_step(roast_t h, const roast_opt_config_t* cfg, int64_t step, roast_stream_t stream) {
   Ctx* c = ctx(h);
-  if (!c || !c->M || !c->shadow) return fail(ROAST_ERR_STATE, "not bound");
-  if (!cfg || cfg->kind < ROAST_OPT_SGD || cfg->kind > ROAST_OPT_ADAM) return fail(ROAST_ERR_CONFIG, "bad optimizer");
-  if (cfg->kind == ROAST_OPT_ADAM && step < 1) return fail(ROAST_ERR_CONFIG, "Adam step must be >= 1");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const size_t bytes = size_t(c->mem_size) * sizeof(float);
-  if (cfg->kind >= ROAST_OPT_ADAGRAD && !c->opt_s1) {
-    ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->opt_s1), bytes));
-    ROAST_CUDA_CHECK(cudaMemsetAsync(c->opt_s1, 0, bytes, s));
-  }
-  if (cfg->kind == ROAST_OPT_ADAM && !c->opt_s2) {
-    ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->opt_s2), bytes));
-    ROAST_CUDA_CHECK(cudaMemsetAsync(c->opt_s2, 0, bytes, s));
-  }
-  if (cfg->touched_only) {   // the interval tables of the exchange (built eagerly, not under capture)
-    if (!(c->touched_valid && c->touched_for == int64_t(c->modules.size()))) {
-      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-      if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
-        return fail(ROAST_ERR_STATE, "touched_only: call roast_touched_size before capturing");
-      if (roast_status_t st = touched_prepare(c, s)) return st;
-    }
-  }
+  if (roast_status_t st = opt_prepare(c, cfg, step, cfg && cfg->touched_only, s)) return st;
   ROAST_CUDA_CHECK(launch_optimizer(c, cfg->kind, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay, step,
                                     cfg->zero_grad, cfg->touched_only != 0, s));
   c->launches++;

@@ -123,4 +123,44 @@ roast_status_t roast_grad_allreduce(roast_t h, roast_stream_t stream) {
   return ROAST_OK;
 }
 
+roast_status_t roast_grad_exchange_step(roast_t h, const roast_opt_config_t* cfg, int64_t step,
+                                        roast_stream_t stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  if (!c || !c->dM) return fail(ROAST_ERR_STATE, "not bound");
+  if (!c->nccl_comm && c->world > 1) return fail(ROAST_ERR_STATE, "roast_comm_init has not been called");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool want_touched = cfg && (cfg->touched_only || c->exchange_mode != ROAST_EXCHANGE_DENSE);
+  if (roast_status_t st = opt_prepare(c, cfg, step, want_touched, s)) return st;
+  const bool touched = cfg->touched_only || (c->exchange_mode == ROAST_EXCHANGE_TOUCHED) ||
+                       (c->exchange_mode == ROAST_EXCHANGE_AUTO && 2 * c->touched_n <= c->mem_size);
+  const ncclComm_t comm = reinterpret_cast<ncclComm_t>(c->nccl_comm);
+  if (!touched) {   // dense: the in-place sum, then one pass over |M|
+    if (comm) {
+      ncclResult_t r = api().AllReduce(c->dM, c->dM, size_t(c->mem_size), ncclFloat32, ncclSum, comm, s);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
+    }
+    ROAST_CUDA_CHECK(launch_optimizer(c, cfg->kind, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay,
+                                      step, cfg->zero_grad, false, s));
+    c->launches++;
+    return ROAST_OK;
+  }
+  // touched: pack -> sum of the packed buffer -> the update reads the summed gradient straight
+  // from the packed buffer (no unpack pass) and zeroes dM on the touched slots
+  if (c->touched_n == 0) return ROAST_OK;
+  ROAST_CUDA_CHECK(launch_pack(c, 0, 1.f, s));
+  c->launches++;
+  if (comm) {
+    ncclResult_t r = api().AllReduce(c->d_pack, c->d_pack, size_t(c->touched_n), ncclFloat32, ncclSum, comm, s);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce(touched)");
+  }
+  if (!cfg->zero_grad) {   // keep the documented dM contents (the summed gradient) when dM is not zeroed
+    ROAST_CUDA_CHECK(launch_pack(c, 1, 1.f, s));
+    c->launches++;
+  }
+  ROAST_CUDA_CHECK(launch_optimizer(c, cfg->kind, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay, step,
+                                    cfg->zero_grad, true, s, c->d_pack));
+  c->launches++;
+  return ROAST_OK;
+}
+
 }  // extern "C"

@@ -343,6 +343,7 @@ struct OptArgs {
   int zero;
   // index space: n elements; slot = p (n_iv == 0) or the p-th touched slot (exchange.cu tables)
   int64_t n;
+  const float* gpack;   // non-null: the gradient of index p is gpack[p] (the all-reduced packed buffer)
   const int64_t* iv_start;
   const int64_t* iv_prefix;
   int n_iv;
@@ -370,7 +371,7 @@ __global__ void opt_kernel(OptArgs a) {
     float w[V], g[V], x[V], y[V];
     if constexpr (V == 4) {
       const float4 wv = *reinterpret_cast<const float4*>(a.M + i);
-      const float4 gv = *reinterpret_cast<const float4*>(a.dM + i);
+      const float4 gv = *reinterpret_cast<const float4*>(a.gpack ? a.gpack + p : a.dM + i);
       w[0] = wv.x; w[1] = wv.y; w[2] = wv.z; w[3] = wv.w;
       g[0] = gv.x; g[1] = gv.y; g[2] = gv.z; g[3] = gv.w;
       if (KIND >= 1) {
@@ -383,7 +384,7 @@ __global__ void opt_kernel(OptArgs a) {
       }
     } else {
       w[0] = a.M[i];
-      g[0] = a.dM[i];
+      g[0] = a.gpack ? a.gpack[p] : a.dM[i];
       if (KIND >= 1) x[0] = a.s1[i];
       if (KIND == 2) y[0] = a.s2[i];
     }
@@ -428,8 +429,9 @@ void launch_opt_kind(const OptArgs& a, bool vec, cudaStream_t s) {
 }  // namespace
 
 cudaError_t launch_optimizer(Ctx* c, int kind, float lr, float b1, float b2, float eps, float wd, int64_t step,
-                             int zero, bool touched_only, cudaStream_t s) {
+                             int zero, bool touched_only, cudaStream_t s, const float* gpack) {
   OptArgs a{};
+  a.gpack = gpack;
   a.M = c->M;
   a.dM = c->dM;
   a.sh = reinterpret_cast<__nv_bfloat16*>(c->shadow);

@@ -106,6 +106,8 @@ void comm_destroy(Ctx* c);
 // touched-set exchange (exchange.cu): build the interval tables (host, synchronous uploads);
 // pack (dir 0: d_pack <- dM[touched]) or unpack (dir 1: dM[touched] <- scale * d_pack)
 roast_status_t touched_prepare(Ctx* c, cudaStream_t s);
+// optimizer-call validation, state allocation and (need_touched) the interval tables
+roast_status_t opt_prepare(Ctx* c, const roast_opt_config_t* cfg, int64_t step, bool need_touched, cudaStream_t s);
 cudaError_t launch_pack(Ctx* c, int dir, float scale, cudaStream_t s);
 
 // workspace of at least `bytes`, stream-ordered
@@ -125,7 +127,7 @@ cudaError_t launch_simt_dw(const Ctx* c, const Module& m, const void* X, const v
 cudaError_t launch_det_reduce(const Ctx* c, const Module& m, const float* ws, int nsplit, cudaStream_t s);
 cudaError_t launch_sync_shadow(Ctx* c, cudaStream_t s);
 cudaError_t launch_optimizer(Ctx* c, int kind, float lr, float b1, float b2, float eps, float wd, int64_t step,
-                             int zero, bool touched_only, cudaStream_t s);
+                             int zero, bool touched_only, cudaStream_t s, const float* gpack = nullptr);
 cudaError_t launch_materialize(const Ctx* c, const Module& m, roast_dtype_t dt, void* W, cudaStream_t s);
 cudaError_t launch_embed_fwd(const Ctx* c, const Module& m, const int64_t* idx, int64_t n, float* out,
                              cudaStream_t s);

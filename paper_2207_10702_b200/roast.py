@@ -29,7 +29,7 @@ EXPORTS = [
     "roast_linear_fwd_bias", "roast_bias_fwd", "roast_bias_bwd", "roast_linear_fwd_chain",
     "roast_linear_bwd_dx_chain", "roast_comm_unique_id", "roast_comm_init",
     "roast_grad_allreduce", "roast_set_exchange", "roast_touched_size", "roast_touched_intervals",
-    "roast_debug_exchange", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step",
+    "roast_debug_exchange", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step", "roast_grad_exchange_step",
     "roast_get_error",
     "roast_status_str", "roast_last_error", "roast_debug_tile_map", "roast_debug_chunk_map",
     "roast_debug_materialize", "roast_debug_hash_host", "roast_launch_count",
@@ -106,6 +106,7 @@ def _load():
         "roast_sync_shadow": (st, [H, S]),
         "roast_sgd_step": (st, [H, ctypes.c_float, S]),
         "roast_optimizer_step": (st, [H, ctypes.POINTER(roast_opt_config_t), I64, S]),
+        "roast_grad_exchange_step": (st, [H, ctypes.POINTER(roast_opt_config_t), I64, S]),
         "roast_get_error": (st, [H]),
         "roast_status_str": (ctypes.c_char_p, [st]),
         "roast_last_error": (ctypes.c_char_p, []),
@@ -338,6 +339,12 @@ def roast_optimizer_step(h, kind, lr, step=1, beta1=0.9, beta2=0.999, eps=1e-8, 
     _check(_lib.roast_optimizer_step(h, ctypes.byref(cfg), step, stream), "roast_optimizer_step")
 
 
+def roast_grad_exchange_step(h, kind, lr, step=1, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0,
+                             zero_grad=True, stream=0, touched_only=False):
+    cfg = roast_opt_config_t(kind, lr, beta1, beta2, eps, weight_decay, int(zero_grad), int(touched_only))
+    _check(_lib.roast_grad_exchange_step(h, ctypes.byref(cfg), step, stream), "roast_grad_exchange_step")
+
+
 def roast_get_error(h):
     return _lib.roast_get_error(h)
 
@@ -538,6 +545,9 @@ class Roast:
 
     def optimizer_step(self, kind, lr, step=1, stream=None, **kw):
         roast_optimizer_step(self.h, kind, lr, step, stream=self._s(stream), **kw)
+
+    def exchange_step(self, kind, lr, step=1, stream=None, **kw):
+        roast_grad_exchange_step(self.h, kind, lr, step, stream=self._s(stream), **kw)
 
     def allreduce(self, stream=None):
         roast_grad_allreduce(self.h, self._s(stream))

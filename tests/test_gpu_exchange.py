@@ -141,3 +141,38 @@ def test_optimizer_touched_only_equals_dense_on_the_touched_set(R, torch, kind):
     assert torch.equal(tch.materialize(l1, torch.float32), dense.materialize(l0, torch.float32))
     for c, _ in ctxs:
         c.close()
+
+
+@pytest.mark.parametrize("kind", [0, 2])
+@pytest.mark.parametrize("mode,comm,zero", [(0, True, True), (2, False, True), (1, True, True), (0, True, False)])
+def test_exchange_step_equals_allreduce_then_update(R, torch, kind, mode, comm, zero):
+    """roast_grad_exchange_step (exchange fused with the update; the touched path reads the summed
+    gradient from the packed buffer) == roast_grad_allreduce + roast_optimizer_step, bit for bit,
+    over two steps: M, the bf16 shadow (recovered operand tiles) and dM."""
+    mem = 1 << 22
+    M0 = store(mem)
+    g = to_dev(synth.normal(13, (mem,)).astype(np.float32), torch.float32)
+    res = []
+    for fused in (False, True):
+        ctx = R.Roast(to_dev(M0, torch.float32), 64, 64, seed=HS)
+        lid = ctx.linear(512, 1024)
+        if comm:
+            R.roast_comm_init(ctx.h, 0, 1, R.roast_comm_unique_id())
+        ctx.set_exchange(mode)
+        n, _ = ctx.touched_size()
+        touched = mode == 2 or (mode == 0 and 2 * n <= mem)
+        spec = OM.LinearSpec(512, 1024, 64, 64, mem, HS, lid)
+        inside = torch.tensor(_oracle_slots([spec], mem), device="cuda")
+        for t in (1, 2):
+            ctx.dM.zero_()
+            ctx.dM[inside] = g[inside]          # a backward writes only the touched slots
+            if fused:
+                ctx.exchange_step(kind, 1e-2, step=t, weight_decay=0.01, zero_grad=zero)
+            else:
+                ctx.allreduce()
+                ctx.optimizer_step(kind, 1e-2, step=t, weight_decay=0.01, zero_grad=zero, touched_only=touched)
+        torch.cuda.synchronize()
+        res.append((ctx.M.clone(), ctx.dM.clone(), ctx.materialize(lid, torch.bfloat16)))
+        ctx.close()
+    for a, b in zip(res[0], res[1]):
+        assert torch.equal(a, b)

@@ -71,3 +71,40 @@ def test_c5_sweep_endpoints_sampled(R, torch, mem_mb):
     """C5: 4096 x 4096 at batch 16384, |M| from L2-resident (8 MB) to HBM-resident (2 GB)."""
     mem = mem_mb * 1024 * 1024 // 4
     _layer_check(R, torch, 4096, 4096, 16384, mem, n_rows=24, n_slots=16)
+
+
+@pytest.mark.parametrize("dist,align", [("uniform", 32), ("zipf", 32), ("zipf", 8)])
+def test_c4_full_size(R, torch, dist, align):
+    """C4 at its real size in the bench's launch configuration (26 tables x 10^7 rows, dim 128,
+    chunk 32, 1000x, 65 536 lookups per table, all tables in one launch): sampled forward rows
+    bit-exact against the oracle; the backward through the adjoint identity that holds at any
+    size, <dOut, L(M)> = <M, dM(dOut)> (L is linear in M, P:268-276 / P:338-341), in fp64."""
+    from oracle import embedding as OE
+    tables, rows, dim, Z, batch = 26, 10 ** 7, 128, 32, 65536
+    mem = synth.compressed_size(tables * rows * dim, 1000, align=align)
+    M_np = synth.uniform(synth.SEED_M, (mem,)).astype(np.float32)
+    M = to_dev(M_np, torch.float32)
+    ctx = R.Roast(M, 64, 64, seed=HS, align=align)
+    mids = [ctx.embedding(rows, dim, Z) for _ in range(tables)]
+    gen = synth.uniform_indices if dist == "uniform" else synth.zipf_indices
+    idx_np = np.stack([gen(synth.SEED_IDX + t, batch, rows) for t in range(tables)])
+    idx = to_dev(idx_np, torch.int64)
+    out = ctx.emb_fwd_multi(mids, idx)
+    torch.cuda.synchronize()
+    M64 = M_np.astype(np.float64)
+    rng = np.random.default_rng(5)
+    for t, b in zip(rng.integers(0, tables, 48), rng.integers(0, batch, 48)):
+        spec = OE.EmbeddingSpec(rows, dim, Z, mem, HS, mids[t], align=align)
+        ref = spec.forward(idx_np[t, b:b + 1], M64)
+        assert np.array_equal(out[t * batch + b].cpu().numpy().astype(np.float64), ref[0]), (t, b)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    dout = torch.randn(tables * batch, dim, device="cuda", generator=g)
+    ctx.zero_grad()
+    ctx.emb_bwd_multi(mids, idx, dout)
+    torch.cuda.synchronize()
+    lhs = float((dout.double() * out.double()).sum())
+    rhs = float((ctx.M.double() * ctx.dM.double()).sum())
+    assert abs(lhs - rhs) <= 1e-5 * abs(lhs), (lhs, rhs)
+    ctx.check()
+    ctx.close()
