@@ -53,7 +53,10 @@ __device__ __forceinline__ float wtile(const MT* Mop, const MapArgs& a, int h, i
   return a.sgn[t] < 0 ? -v : v;
 }
 
-constexpr int BM = 64, BN = 64, BK = 16;
+// BK = 64: the hashed B gathers (tile map -> M, two dependent loads) of a whole 64-deep
+// K slice are in flight at once; with BK = 16 the small fp32 configs (C1: 4 blocks) were
+// bound by 16 serial load-latency rounds.
+constexpr int BM = 64, BN = 64, BK = 64;
 
 // C[T x N] = lam * A[T x K] * B[K x N]; B[k][n] = W~[k][n] (fwd) or W~[n][k] (dX).
 template <typename XT, typename MT, bool kTransW>
