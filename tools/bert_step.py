@@ -1,7 +1,8 @@
 """C3 (BASELINE.json configs[2]): full BERT-base-shaped encoder training step, all 72 linears
 (12 layers x Q, K, V, O, FFN1, FFN2) ROAST-hashed into ONE global M at 100x
 (|M| = 849 352 fp32), data parallel: per-GPU batch 64 x 128 tokens, dM all-reduced with
-NCCL inside libroast, SGD on M + bf16 shadow refresh fused in one kernel.
+NCCL inside libroast, SGD on M + bf16 shadow refresh + dM zeroing fused in one kernel
+(roast_grad_exchange_step).
 
     python tools/bert_step.py [--steps 10] [--dense]          (1 GPU)
     torchrun --nproc-per-node N tools/bert_step.py             (N GPUs, weak scaling)
@@ -119,10 +120,10 @@ def main():
                     dist.all_reduce(p.grad)
             opt.step()
         else:
-            store.zero_grad()
-            loss.backward()
-            store.allreduce()              # a6: one ncclAllReduce of dM (|M| fp32) per step
-            store.sgd(1e-4)                # M -= lr dM; shadow refresh (same kernel)
+            loss.backward()                # dM starts zeroed: the exchange step below zeroes it
+            # a6 + a7 in one call: ncclAllReduce of dM (or of its packed touched set), then
+            # M -= lr dM, bf16 shadow refresh and dM <- 0 in the same pass
+            store.exchange_step(R.OPT_SGD, 1e-4, zero_grad=True)
         return loss
 
     side = torch.cuda.Stream(device=dev) if args.graph else torch.cuda.current_stream()

@@ -24,7 +24,13 @@ __device__ __forceinline__ void load(const CUtensorMap* m, void* dst, uint64_t* 
 struct Maps { CUtensorMap a, b; };
 
 // each stage: na boxes from map a (box rows ra) + nb boxes from map b (box rows 64); depth = stages in flight
-__global__ void k(const __grid_constant__ Maps maps, int iters, int depth, int na, int ra, int nbx, int arows,
+#ifdef CLUSTER2
+#define CLUSTER_ATTR __cluster_dims__(2, 1, 1)
+#else
+#define CLUSTER_ATTR
+#endif
+// -DCLUSTER2: the same kernel launched as clusters of 2 CTAs (as the tcgen05 GEMM is)
+__global__ void CLUSTER_ATTR k(const __grid_constant__ Maps maps, int iters, int depth, int na, int ra, int nbx, int arows,
                   int brows, long long* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~uintptr_t(1023));
