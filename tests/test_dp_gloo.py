@@ -81,16 +81,17 @@ def test_shard_partitions_exactly():
             assert max(sizes) - min(sizes) <= 1
 
 
-def test_world2_allreduce_equals_full_batch():
+@pytest.mark.parametrize("world", [2, 8])     # "at world = 2 and 8"
+def test_world_allreduce_equals_full_batch(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
-        p.join(timeout=180)
-    results = [q.get(timeout=5) for _ in range(2)]
+        p.join(timeout=300)
+    results = [q.get(timeout=5) for _ in range(world)]
     assert all(p.exitcode == 0 for p in procs)
     for rank, err_mm, err_emb in results:
         assert err_mm <= 1e-12 and err_emb <= 1e-12, (rank, err_mm, err_emb)
