@@ -326,11 +326,13 @@ __device__ __forceinline__ float opt_update(float w, float g0, float& a, float& 
     w -= lr * g;
   } else if (KIND == 1) {
     a = a + g * g;
-    w -= lr * g / (sqrtf(a) + eps);
+    w -= __fdividef(lr * g, sqrtf(a) + eps);
   } else {
+    // bc1 / bc2 arrive as reciprocals of the bias corrections; one fast division per slot keeps
+    // the pass HBM-bound (IEEE divisions made it ~70 % issue-bound at 2 GB)
     a = b1 * a + (1.f - b1) * g;
     b = b2 * b + (1.f - b2) * g * g;
-    w -= lr * (a / bc1) / (sqrtf(b / bc2) + eps);
+    w -= __fdividef(lr * (a * bc1), sqrtf(b * bc2) + eps);
   }
   return w;
 }
@@ -446,8 +448,8 @@ cudaError_t launch_optimizer(Ctx* c, int kind, float lr, float b1, float b2, flo
   a.b2 = b2;
   a.eps = eps;
   a.wd = wd;
-  a.bc1 = kind == 2 ? float(1.0 - pow(double(b1), double(step))) : 1.f;
-  a.bc2 = kind == 2 ? float(1.0 - pow(double(b2), double(step))) : 1.f;
+  a.bc1 = kind == 2 ? float(1.0 / (1.0 - pow(double(b1), double(step)))) : 1.f;   // reciprocals
+  a.bc2 = kind == 2 ? float(1.0 / (1.0 - pow(double(b2), double(step)))) : 1.f;
   a.zero = zero;
   bool vec;
   if (touched_only) {   // the slots some module can read or write (exchange.cu); the rest are dead
