@@ -1060,7 +1060,9 @@ struct ChainPlan {
 };
 
 ChainPlan plan_chain(int m_tiles, int nt0, int kb0, int nt1, int kb1, int npairs) {
-  const double EPI = 5.0, LAT = 1.0;
+  double EPI = 5.0, LAT = 1.0;
+  if (const char* e = getenv("ROAST_CHAIN_EPI")) EPI = atof(e);   // planner-model experiments
+  if (const char* e = getenv("ROAST_CHAIN_LAT")) LAT = atof(e);
   const int units0 = m_tiles * nt0, units1 = m_tiles * nt1;
   const double c0 = kb0 + EPI, c1 = kb1 + EPI;
   ChainPlan best;
