@@ -12,8 +12,12 @@
  *     row-major and densely packed unless stated otherwise.  Pointers named *_host
  *     are host pointers.  The library never frees caller memory.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
- *     Every device-side effect is stream-ordered and asynchronous; only the
- *     roast_debug_tile_map call synchronises (it copies to host).
+ *     Every device-side effect of the compute calls is stream-ordered and
+ *     asynchronous.  Calls that build or read host-side tables synchronise: the
+ *     registrations (tile-map upload), roast_touched_size and the first touched
+ *     exchange / touched-only update after a registration (interval tables; never
+ *     under graph capture), the first autotuned launch of a shape, roast_get_error
+ *     and roast_debug_tile_map.
  *   - Argument / geometry validation is synchronous: on a non-OK return nothing
  *     was launched.  Device-detected faults (embedding index out of range) are
  *     sticky and reported by roast_get_error() (and by the next call).
