@@ -42,10 +42,25 @@ def flops_per_step(tokens):
 
 
 def load_peaks():
+    """(bf16 burst TFLOP/s, sustained, HBM GB/s, source) from the driver-written
+    MEASURED_PEAKS.json, else the B200_PROFILING.md fallback (1590 / ~1400 / 6650).
+    Tolerates a missing file, missing keys or a nested layout (never fails the bench)."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(p):
+    try:
         d = json.load(open(p))
-        return d["bf16_tflops"], d.get("bf16_tflops_sustained"), d["hbm_gbs"], "measured"
+
+        def find(key):
+            if isinstance(d, dict) and key in d:
+                return float(d[key])
+            for v in (d.values() if isinstance(d, dict) else []):
+                if isinstance(v, dict) and key in v:
+                    return float(v[key])
+            return None
+        burst, sus, hbm = find("bf16_tflops"), find("bf16_tflops_sustained"), find("hbm_gbs")
+        if burst and hbm:
+            return burst, sus, hbm, "measured"
+    except Exception:
+        pass
     return 1590.0, 1400.0, 6650.0, "fallback"
 
 

@@ -19,6 +19,21 @@ import synth  # noqa: E402
 from paper_2207_10702_b200 import roast as R  # noqa: E402
 
 
+
+def _hbm_gbs():
+    """HBM roofline: MEASURED_PEAKS.json when present (driver-written), else the measured copy
+    bandwidth of this pool recorded in SURVEY.md §8(d) (6558.1 GB/s)."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    try:
+        import bench
+        _, _, hbm, src = bench.load_peaks()
+        return hbm if src == "measured" else 6558.1
+    except Exception:
+        return 6558.1
+
+
+HBM_GBS = _hbm_gbs()
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
@@ -86,7 +101,7 @@ def main():
             times.append(a.elapsed_time(b))
         ms = float(np.median(times))
         gbs = tables * batch * bpl / (ms * 1e-3) / 1e9
-        res[name] = dict(ms=ms, GBps=gbs, hbm_frac=gbs / 6558.1, lookups=tables * batch)
+        res[name] = dict(ms=ms, GBps=gbs, hbm_frac=gbs / HBM_GBS, lookups=tables * batch)
     ctx.check()
     # library baseline: torch gather / index_add_ of the same 128-B chunks at the same offsets
     # (precomputed, no hashing) -> what the raw access pattern costs on this GPU
