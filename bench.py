@@ -29,7 +29,32 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-RATIO = 100
+RATIO = 100   # the metric's configuration (BASELINE.json configs[1] at 100x); --ratio 10 / 1000 for the others
+
+
+def _num(x):
+    return int(x) if float(x).is_integer() else x
+
+
+def workload(ratio, mem):
+    """config.workload of both arms (the same string: same metric, same configuration)."""
+    r = int(ratio) if float(ratio).is_integer() else ratio
+    return "C2 BERT-base MLP block 768->3072->768 fwd+bwd, %sx (|M|=%d), tile 64x64" % (r, mem)
+
+
+def synth_mem(ratio):
+    import synth
+    return synth.mlp_block(ratio)["mem_size"]
+
+
+def args_ratio():
+    """--ratio of the current command line (the reference arm's sample uses the same |M|)."""
+    for i, a in enumerate(sys.argv):
+        if a == "--ratio" and i + 1 < len(sys.argv):
+            return float(sys.argv[i + 1])
+        if a.startswith("--ratio="):
+            return float(a.split("=", 1)[1])
+    return RATIO
 TOKENS = 8192
 LAYERS = [(768, 3072), (3072, 768)]
 TILE = 64
@@ -91,7 +116,7 @@ def cpu_sample(seconds_target=10.0, tokens=256):
 
     import synth
     from oracle import roast_mm as OM
-    mem = synth.mlp_block(RATIO)["mem_size"]
+    mem = synth.mlp_block(args_ratio())["mem_size"]
     M = synth.uniform(synth.SEED_M, (mem,)).astype(np.float32)
     specs = [OM.LinearSpec(H, O, TILE, TILE, mem, synth.HASH_SEED, i) for i, (H, O) in enumerate(LAYERS)]
     X = synth.round_to_bf16(synth.normal(synth.SEED_X, (tokens, 768)).astype(np.float32))
@@ -132,8 +157,8 @@ def run_reference(args):
     line = dict(metric=METRIC, value=cb["value"], unit=UNIT, n_gpus=args.gpus, steps=args.steps,
                 warmup=args.warmup, ms_per_step=cb["seconds_per_sample_step"] * 1e3, higher_is_better=True,
                 scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
-                config=dict(workload="C2 BERT-base MLP block 768->3072->768, 100x, tile 64x64 (oracle sample)",
-                            tokens_per_gpu=TOKENS, ratio=RATIO),
+                config=dict(workload=workload(args_ratio(), synth_mem(args_ratio())),
+                            tokens_per_gpu=TOKENS, ratio=_num(args_ratio())),
                 impl="reference",
                 cpu_baseline=dict(value=cb["value"], unit=UNIT, cores=cb["cores"], kind="oracle",
                                   sample=cb["sample"]),
@@ -208,7 +233,7 @@ def run_gpu(args):
     import synth
 
     T = TOKENS
-    mem = synth.mlp_block(RATIO)["mem_size"]
+    mem = synth.mlp_block(args.ratio)["mem_size"]
     stream = torch.cuda.current_stream()
     M = torch.tensor(synth.uniform(synth.SEED_M, (mem,)).astype(np.float32), device=dev)
     ctx = R.Roast(M, TILE, TILE, seed=synth.HASH_SEED, deterministic=args.deterministic)
@@ -536,8 +561,8 @@ def run_gpu(args):
         metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
         ms_per_step=ms_per_step, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="bf16",
         data="synthetic (M ~ U(-1,1) from synth seed 1; X, dY ~ N(0,1) bf16)",
-        config=dict(workload="C2 BERT-base MLP block 768->3072->768 fwd+bwd, 100x (|M|=%d), tile 64x64" % mem,
-                    tokens_per_gpu=T, global_tokens=T * world, ratio=RATIO, mem_size=mem,
+        config=dict(workload=workload(args.ratio, mem),
+                    tokens_per_gpu=T, global_tokens=T * world, ratio=_num(args.ratio), mem_size=mem,
                     l2="flushed between timed steps (256 MB write outside the events)",
                     dm_mode="deterministic" if args.deterministic else "atomic",
                     streams=args.streams, cuda_graph=bool(args.graph),
@@ -576,6 +601,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--streams", type=int, default=2, choices=[1, 2])
+    ap.add_argument("--ratio", type=float, default=RATIO, help="compression (C2 at 10x / 100x / 1000x)")
     ap.add_argument("--e2e-mode", default="pipelined", choices=["pipelined", "serial"],
                     help="e2e: H2D of the next step overlapped with this step's kernels, or in sequence")
     ap.add_argument("--graph", type=int, default=1, choices=[0, 1])
