@@ -2,77 +2,192 @@
 //
 //   dM[h1(c) + o] += lambda * g(c) * dOut[b, jZ + o]     (R15, R19)
 //
-// The fast path scatters with vector atomics (order unspecified).  Here every slot is
-// owned by one thread and summed in a fixed order:
-//   1. key each (lookup b, chunk j) pair by its offset / A (the hash, on the device);
-//   2. stable radix sort (CUB) -> pairs ordered by (offset, pair index);
-//   3. for each 4-slot vector s, binary-search the pairs whose chunk [off, off + Z) covers s
-//      (offsets in (s - Z, s]) and add their contributions in that order.
-// Bitwise reproducible run to run; the same structure as the linear-layer K5 reduce.
+// The fast path scatters with vector atomics (order unspecified).  Here every slot is summed
+// in a fixed order, and only the slots some lookup touches are visited:
+//   1. each (lookup b, chunk j) pair covers G = Z / A slot groups of A slots (offsets are
+//      multiples of A); emit one item per (pair, group i) with the sort key
+//      (offset / A + i) * G + (G - 1 - i)   — group first, then ascending chunk offset;
+//   2. stable radix sort (CUB) -> items ordered by (group, chunk offset, pair index);
+//   3. a group (a run of equal key / G) is cut into fixed chunks of 64 items; one warp per
+//      chunk (lanes 0..A-1 own the group's A slots) adds the chunk's lambda * g * dOut terms
+//      in item order; one-chunk groups add straight into dM, longer ones (Zipf-hot rows:
+//      thousands of duplicates) leave partials that a second pass adds in chunk order.
+// Bitwise reproducible run to run (every order is fixed by the sorted data, not by timing).
+// Work is O(lookups), not O(|M|), and hot rows are summed in parallel.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 #include "roast_internal.h"
 
 namespace roast {
 namespace {
 
-__global__ void emb_keys_kernel(ModuleHash h, const int64_t* __restrict__ idx, int64_t n, int64_t rows, int q,
-                                uint32_t* __restrict__ keys, int32_t* __restrict__ vals, int32_t* err) {
+__global__ void emb_items_kernel(ModuleHash h, const int64_t* __restrict__ idx, int64_t n, int64_t rows, int q,
+                                 int G, uint32_t* __restrict__ keys, int32_t* __restrict__ vals, int32_t* err,
+                                 int32_t* __restrict__ nvalid) {
   const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p == 0) *nvalid = int32_t(n * q * G);   // lowered by emb_heads_kernel if rows were out of range
   if (p >= n * q) return;
   const int64_t b = p / q;
   const int j = int(p - b * q);
   const int64_t r = idx[b];
   if (r < 0 || r >= rows) {
     atomicOr(err, 1);
-    keys[p] = 0xFFFFFFFFu;   // sorts last; the reduce never reaches it (no slot >= 2^32 * A)
-    vals[p] = -1;
+    for (int i = 0; i < G; ++i) {   // sorts last; the reduce skips the sentinel group
+      keys[p * G + i] = 0xFFFFFFFFu;
+      vals[p * G + i] = -1;
+    }
     return;
   }
   const uint64_t key = uint64_t(r) * uint64_t(q) + uint64_t(j);
-  keys[p] = uint32_t(h.offset(key) / h.align);
-  vals[p] = int32_t(p) | (h.sign(key) < 0 ? int32_t(0x80000000) : 0);   // sign in the top bit
+  const uint32_t k0 = uint32_t(h.offset(key) / h.align);
+  const int32_t neg = h.sign(key) < 0 ? int32_t(0x80000000) : 0;
+  for (int i = 0; i < G; ++i) {
+    keys[p * G + i] = (k0 + uint32_t(i)) * uint32_t(G) + uint32_t(G - 1 - i);
+    vals[p * G + i] = int32_t(p * G + i) | neg;   // item index, sign in the top bit
+  }
 }
 
-__global__ void emb_det_reduce_kernel(float* __restrict__ dM, const uint32_t* __restrict__ keys,
-                                      const int32_t* __restrict__ vals, int64_t npairs, const float* __restrict__ dOut,
-                                      int dim, int chunk, int q, int align, float lam, int64_t mem_size) {
-  const int64_t s = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
-  if (s >= mem_size) return;
-  // covering chunks: off in (s - Z, s]  <=>  key = off / A in [ceil((s - Z + 1) / A), floor(s / A)]
-  const int64_t klo = s - chunk + 1 <= 0 ? 0 : (s - chunk + 1 + align - 1) / align;
-  const int64_t khi = s / align;
-  int64_t a = 0, e = npairs;
-  while (a < e) {
-    const int64_t mid = (a + e) >> 1;
-    if (int64_t(keys[mid]) < klo) a = mid + 1; else e = mid;
+__global__ void emb_heads_kernel(const uint32_t* __restrict__ keys, int64_t nitems, int G, uint8_t* __restrict__ head,
+                                 int32_t* __restrict__ nvalid) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nitems) return;
+  const uint32_t k = keys[i];
+  const bool sent = k == 0xFFFFFFFFu;
+  head[i] = !sent && (i == 0 || keys[i - 1] / uint32_t(G) != k / uint32_t(G));
+  if (sent && (i == 0 || keys[i - 1] != 0xFFFFFFFFu)) *nvalid = int32_t(i);   // first sentinel
+}
+
+constexpr int kW = 64;   // items per chunk of a group's sum (fixed: the order is data-independent)
+
+// per segment (group): number of kW-item chunks, and the same count for multi-chunk segments only
+__global__ void emb_seginfo_kernel(const int32_t* __restrict__ heads, const int32_t* __restrict__ nseg_p,
+                                   const int32_t* __restrict__ nvalid_p, int64_t nitems, int32_t* __restrict__ nch,
+                                   int32_t* __restrict__ nlong) {
+  const int64_t sg = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (sg > nitems) return;
+  const int64_t nseg = *nseg_p;
+  int32_t c = 0;
+  if (sg < nseg) {
+    const int64_t e = sg + 1 < nseg ? int64_t(heads[sg + 1]) : int64_t(*nvalid_p);
+    c = int32_t((e - heads[sg] + kW - 1) / kW);
   }
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  bool any = false;
-  for (int64_t i = a; i < npairs && int64_t(keys[i]) <= khi; ++i) {
-    const int32_t v = vals[i];
-    const int64_t p = int64_t(v & 0x7FFFFFFF);
-    const float sc = (v < 0 ? -lam : lam);
-    const int64_t b = p / q;
-    const int j = int(p - b * q);
-    const int o = int(s - int64_t(keys[i]) * align);      // position of s inside the chunk
-    const int col = j * chunk + o;
-    if (col >= dim) continue;                             // padded tail of the last chunk (R16)
-    const float4 g = __ldg(reinterpret_cast<const float4*>(dOut + b * dim + col));
-    acc.x += sc * g.x;
-    acc.y += sc * g.y;
-    acc.z += sc * g.z;
-    acc.w += sc * g.w;
-    any = true;
+  nch[sg] = c;
+  nlong[sg] = c > 1 ? c : 0;
+}
+
+// per chunk: [item begin, item end) of the sorted items, the destination group, and where the
+// chunk's sum goes (-1: straight into dM, else its partial slot) — one 16-byte load in pass 1
+struct ChunkInfo {
+  int32_t begin, end;
+  uint32_t group;
+  int32_t dst;
+};
+
+__global__ void emb_chunkmap_kernel(const uint32_t* __restrict__ keys, const int32_t* __restrict__ heads,
+                                    const int32_t* __restrict__ nseg_p, const int32_t* __restrict__ nvalid_p,
+                                    const int32_t* __restrict__ nch, const int32_t* __restrict__ choff,
+                                    const int32_t* __restrict__ loff, int G, ChunkInfo* __restrict__ info) {
+  const int64_t sg = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nseg = *nseg_p;
+  if (sg >= nseg) return;
+  const int32_t h = heads[sg];
+  const int32_t e = sg + 1 < nseg ? heads[sg + 1] : *nvalid_p;
+  const uint32_t group = keys[h] / uint32_t(G);
+  const int c = nch[sg];
+  for (int k = 0; k < c; ++k) {   // a Zipf-hot group writes its few dozen entries serially
+    ChunkInfo ci;
+    ci.begin = h + k * kW;
+    ci.end = min(e, ci.begin + kW);
+    ci.group = group;
+    ci.dst = c == 1 ? -1 : loff[sg] + k;
+    info[choff[sg] + k] = ci;
   }
-  if (!any) return;
-  float4* d = reinterpret_cast<float4*>(dM + s);
-  float4 m = *d;
-  m.x += acc.x;
-  m.y += acc.y;
-  m.z += acc.z;
-  m.w += acc.w;
-  *d = m;
+}
+
+// sum of one chunk's terms in item order (8 independent loads in flight)
+__device__ __forceinline__ float chunk_sum(const ChunkInfo& ci, const int32_t* __restrict__ vals,
+                                           const float* __restrict__ dOut, int dim, int chunk, int q, int G, int A,
+                                           float lam, int lane) {
+  float acc = 0.f;
+  constexpr int U = 8;
+  for (int it0 = ci.begin; it0 < ci.end; it0 += U) {
+    float t[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      t[u] = 0.f;
+      const int it = it0 + u;
+      if (it >= ci.end) continue;
+      const int32_t v = __ldg(vals + it);
+      const int64_t item = int64_t(v & 0x7FFFFFFF);
+      const int64_t p = item / G;
+      const int i = int(item - p * G);
+      const int64_t b = p / q;
+      const int j = int(p - b * q);
+      const int col = j * chunk + i * A + lane;
+      if (lane < A && col < dim)   // padded tail of the last chunk (R16) contributes nothing
+        t[u] = (v < 0 ? -lam : lam) * __ldg(dOut + b * dim + col);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += t[u];
+  }
+  return acc;
+}
+
+// pass 1: one warp per chunk, two chunks in flight per warp; lanes 0..A-1 own the group's A
+// slots.  A single-chunk group goes straight to dM; a longer one leaves a partial.
+__global__ void emb_chunk_kernel(float* __restrict__ dM, float* __restrict__ partial,
+                                 const int32_t* __restrict__ vals, const ChunkInfo* __restrict__ info,
+                                 const int32_t* __restrict__ nseg_p, const int32_t* __restrict__ nch,
+                                 const int32_t* __restrict__ choff, const float* __restrict__ dOut, int dim, int chunk,
+                                 int q, int G, int A, float lam, int64_t mem_size) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nseg = *nseg_p;
+  if (nseg == 0) return;
+  const int64_t total = int64_t(choff[nseg - 1]) + nch[nseg - 1];
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t c = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; c < total; c += 2 * nwarps) {
+    const int64_t c2 = c + nwarps;
+    const ChunkInfo i1 = info[c];
+    ChunkInfo i2{0, 0, 0, -2};
+    if (c2 < total) i2 = info[c2];
+    const float s1 = chunk_sum(i1, vals, dOut, dim, chunk, q, G, A, lam, lane);
+    const float s2 = chunk_sum(i2, vals, dOut, dim, chunk, q, G, A, lam, lane);
+    if (lane >= A) continue;
+    const ChunkInfo* ci[2] = {&i1, &i2};
+    const float sum[2] = {s1, s2};
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const ChunkInfo& x = *ci[u];
+      if (x.dst == -2) continue;
+      if (x.dst < 0) {
+        const int64_t sl = int64_t(x.group) * A + lane;
+        if (sl < mem_size) dM[sl] += sum[u];
+      } else {
+        partial[int64_t(x.dst) * A + lane] = sum[u];
+      }
+    }
+  }
+}
+
+// pass 2: one warp per multi-chunk group: its partials in chunk order, then dM
+__global__ void emb_longseg_kernel(float* __restrict__ dM, const float* __restrict__ partial,
+                                   const uint32_t* __restrict__ keys, const int32_t* __restrict__ heads,
+                                   const int32_t* __restrict__ nseg_p, const int32_t* __restrict__ nch,
+                                   const int32_t* __restrict__ loff, int G, int A, int64_t mem_size) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nseg = *nseg_p;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t sg = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; sg < nseg; sg += nwarps) {
+    const int c = nch[sg];
+    if (c <= 1 || lane >= A) continue;
+    float acc = 0.f;
+    for (int k = 0; k < c; ++k) acc += partial[(int64_t(loff[sg]) + k) * A + lane];
+    const int64_t s = int64_t(keys[heads[sg]] / uint32_t(G)) * A + lane;
+    if (s < mem_size) dM[s] += acc;
+  }
 }
 
 }  // namespace
@@ -81,32 +196,71 @@ roast_status_t embed_bwd_deterministic(Ctx* c, const Module& m, const int64_t* i
                                        cudaStream_t s) {
   const int64_t np = n * m.chunks_per_row;
   if (np == 0) return ROAST_OK;
-  if (np >= (int64_t(1) << 31) || c->mem_size / m.hash.align >= (int64_t(1) << 32) - 1)
-    return fail(ROAST_ERR_UNSUPPORTED, "deterministic embedding backward: too many pairs or slots");
-  size_t temp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, temp, static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
-                                  static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr), int(np), 0,
-                                  32, s);
-  const size_t bytes = size_t(np) * 16 + temp + 256;
+  const int A = int(m.hash.align);
+  const int G = m.chunk / A;
+  const int64_t ni = np * G;
+  if (ni >= (int64_t(1) << 30) || (c->mem_size / A + G) * G >= (int64_t(1) << 32) - 1 || A > 32)
+    return fail(ROAST_ERR_UNSUPPORTED, "deterministic embedding backward: too many items or slot groups");
+  const int ni1 = int(ni) + 1;
+  size_t t_sort = 0, t_sel = 0, t_scan = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t_sort, static_cast<const uint32_t*>(nullptr),
+                                  static_cast<uint32_t*>(nullptr), static_cast<const int32_t*>(nullptr),
+                                  static_cast<int32_t*>(nullptr), int(ni), 0, 32, s);
+  cub::CountingInputIterator<int32_t> count_it(0);
+  cub::DeviceSelect::Flagged(nullptr, t_sel, count_it, static_cast<const uint8_t*>(nullptr),
+                             static_cast<int32_t*>(nullptr), static_cast<int32_t*>(nullptr), int(ni), s);
+  cub::DeviceScan::ExclusiveSum(nullptr, t_scan, static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
+                                ni1, s);
+  const size_t temp = std::max(t_sort, std::max(t_sel, t_scan));
+  const int64_t max_long = 2 * (ni / kW) + 2;   // chunks of multi-chunk groups (each has > kW items)
+  // [keys in | keys out | vals in | vals out | heads | nch | choff | nlong | loff (ni + 1 each) |
+  //  partial (max_long x A fp32) | flags (u8) | 4 scalars | temp]
+  const size_t bytes = size_t(ni) * 16 + size_t(ni1) * 20 + size_t(ni1 + ni / kW + 1) * 16 + 16 +
+                       size_t(max_long) * A * 4 + size_t(ni) + 1024 + temp;
   roast_status_t st = ensure_ws(c, bytes, s);
   if (st) return st;
   uint8_t* base = reinterpret_cast<uint8_t*>(c->ws);
   uint32_t* k_in = reinterpret_cast<uint32_t*>(base);
-  uint32_t* k_out = k_in + np;
-  int32_t* v_in = reinterpret_cast<int32_t*>(k_out + np);
-  int32_t* v_out = v_in + np;
-  void* tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(v_out + np) + 255) & ~uintptr_t(255));
-  emb_keys_kernel<<<unsigned((np + 255) / 256), 256, 0, s>>>(m.hash, idx, n, m.rows, m.chunks_per_row, k_in, v_in,
-                                                             c->d_err);
+  uint32_t* k_out = k_in + ni;
+  int32_t* v_in = reinterpret_cast<int32_t*>(k_out + ni);
+  int32_t* v_out = v_in + ni;
+  int32_t* heads = v_out + ni;
+  int32_t* nch = heads + ni1;
+  int32_t* choff = nch + ni1;
+  int32_t* nlong = choff + ni1;
+  int32_t* loff = nlong + ni1;
+  ChunkInfo* info = reinterpret_cast<ChunkInfo*>((reinterpret_cast<uintptr_t>(loff + ni1) + 15) & ~uintptr_t(15));
+  float* partial = reinterpret_cast<float*>(info + ni1 + ni / kW + 1);   // total chunks <= ni + ni / kW
+  uint8_t* flags = reinterpret_cast<uint8_t*>(partial + max_long * A);
+  int32_t* scal = reinterpret_cast<int32_t*>((reinterpret_cast<uintptr_t>(flags + ni) + 15) & ~uintptr_t(15));
+  int32_t* nseg = scal;
+  int32_t* nvalid = scal + 1;
+  void* tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(scal + 4) + 255) & ~uintptr_t(255));
+  emb_items_kernel<<<unsigned((np + 255) / 256), 256, 0, s>>>(m.hash, idx, n, m.rows, m.chunks_per_row, G, k_in, v_in,
+                                                              c->d_err, nvalid);
   ROAST_CUDA_CHECK(cudaGetLastError());
-  // invalid rows carry key 0xFFFFFFFF: sort all 32 bits when any could be present
-  ROAST_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, temp, k_in, k_out, v_in, v_out, int(np), 0, 32, s));
-  const int64_t vecs = (c->mem_size + 3) / 4;
-  emb_det_reduce_kernel<<<unsigned((vecs + 255) / 256), 256, 0, s>>>(c->dM, k_out, v_out, np, dOut, m.dim, m.chunk,
-                                                                      m.chunks_per_row, int(m.hash.align), m.lam,
-                                                                      c->mem_size);
+  size_t t1 = temp;
+  ROAST_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, t1, k_in, k_out, v_in, v_out, int(ni), 0, 32, s));
+  emb_heads_kernel<<<unsigned((ni + 255) / 256), 256, 0, s>>>(k_out, ni, G, flags, nvalid);
   ROAST_CUDA_CHECK(cudaGetLastError());
-  c->launches += 3;
+  size_t t2 = temp;
+  ROAST_CUDA_CHECK(cub::DeviceSelect::Flagged(tmp, t2, count_it, flags, heads, nseg, int(ni), s));
+  emb_seginfo_kernel<<<unsigned((ni1 + 255) / 256), 256, 0, s>>>(heads, nseg, nvalid, ni, nch, nlong);
+  ROAST_CUDA_CHECK(cudaGetLastError());
+  size_t t3 = temp;
+  ROAST_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp, t3, nch, choff, ni1, s));
+  t3 = temp;
+  ROAST_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp, t3, nlong, loff, ni1, s));
+  emb_chunkmap_kernel<<<unsigned((ni1 + 255) / 256), 256, 0, s>>>(k_out, heads, nseg, nvalid, nch, choff, loff, G,
+                                                                    info);
+  ROAST_CUDA_CHECK(cudaGetLastError());
+  const int grid = 148 * 8;
+  emb_chunk_kernel<<<grid, 256, 0, s>>>(c->dM, partial, v_out, info, nseg, nch, choff, dOut, m.dim, m.chunk,
+                                        m.chunks_per_row, G, A, m.lam, c->mem_size);
+  ROAST_CUDA_CHECK(cudaGetLastError());
+  emb_longseg_kernel<<<grid, 256, 0, s>>>(c->dM, partial, k_out, heads, nseg, nch, loff, G, A, c->mem_size);
+  ROAST_CUDA_CHECK(cudaGetLastError());
+  c->launches += 9;
   return ROAST_OK;
 }
 

@@ -34,19 +34,21 @@ def _hbm_gbs():
 
 HBM_GBS = _hbm_gbs()
 
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--dist", default="uniform", choices=["uniform", "zipf"])
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--align", type=int, default=32, help="offset alignment A in elements (32 = 128-B lines)")
+    ap.add_argument("--deterministic", action="store_true", help="fixed-order dM (sort-based backward)")
     ap.add_argument("--nvtx", action="store_true", help="one eager fused fwd + bwd in NVTX range 'emb_step' (ncu)")
     args = ap.parse_args()
     tables, rows, dim, Z = 26, 10 ** 7, 128, 32
     batch = 8192 if args.quick else 65536
     mem = synth.compressed_size(tables * rows * dim, 1000, align=args.align)
     M = torch.tensor(synth.uniform(synth.SEED_M, (mem,)).astype(np.float32), device="cuda")
-    ctx = R.Roast(M, 64, 64, seed=synth.HASH_SEED, align=args.align)
+    ctx = R.Roast(M, 64, 64, seed=synth.HASH_SEED, align=args.align, deterministic=args.deterministic)
     ids = [ctx.embedding(rows, dim, Z) for _ in range(tables)]
     gen = synth.uniform_indices if args.dist == "uniform" else synth.zipf_indices
     idx = [torch.tensor(gen(synth.SEED_IDX + t, batch, rows), device="cuda") for t in range(tables)]
@@ -127,6 +129,7 @@ def main():
             bpl = 1032 if name == "torch_gather" else 1544
             res[name] = dict(ms=ms, GBps=tables * batch * bpl / (ms * 1e-3) / 1e9)
     print(json.dumps(dict(config="C4 26x1e7x128 chunk 32 1000x", dist=args.dist, batch=batch, align=args.align,
+                          deterministic=args.deterministic,
                           **res)))
 
 
