@@ -277,6 +277,27 @@ def test_embedding_multi_table_errors(R, torch):
     assert roast.roast_get_error(ctx.h) == roast.ERR_BOUNDS
 
 
+@pytest.mark.parametrize("align", [8, 32])
+def test_deterministic_embedding_bwd_skips_out_of_range_rows(R, torch, align):
+    """Deterministic a5 with rows outside [0, num_rows) mixed in: they contribute nothing (their
+    items sort last and are never summed), the valid rows' gradient equals the oracle's, and
+    the sticky BOUNDS flag is raised."""
+    from paper_2207_10702_b200 import roast
+    mem, rows, d, Z = 50_000, 1000, 64, 32
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64, deterministic=True, align=align)
+    mid = ctx.embedding(rows, d, Z)
+    idx_np = np.array([5, 1000, 5, -3, 999, 5, 10 ** 9, 17], dtype=np.int64)
+    dout_np = synth.normal(3, (len(idx_np), d)).astype(np.float32)
+    ctx.zero_grad()
+    ctx.emb_bwd(mid, to_dev(idx_np, torch.int64), to_dev(dout_np, torch.float32))
+    torch.cuda.synchronize()
+    ok = (idx_np >= 0) & (idx_np < rows)
+    ref = OE.EmbeddingSpec(rows, d, Z, mem, HS, mid, align=align).backward(idx_np[ok], dout_np[ok])
+    assert rel_frob(ctx.dM.cpu().numpy(), ref) <= 1e-6
+    assert roast.roast_get_error(ctx.h) == roast.ERR_BOUNDS
+
+
 def test_embedding_duplicates_and_bounds(R, torch):
     from paper_2207_10702_b200 import roast
     mem = 4096
