@@ -170,11 +170,25 @@ __global__ void __launch_bounds__(256) simt_dw_kernel(const XT* __restrict__ X, 
 // K5: dM[s] += sum over covering tiles (ascending (offset, tile id)), then over
 // split-K partials (ascending), of ws[split][tile][s - off].  One thread per
 // 4 consecutive slots; A % 4 == 0 and T % A == 0 so all 4 share one covering set.
+// Visited slots: every 4-slot group of |M| (n_iv == 0), or only the touched set (the exchange's
+// interval tables, exchange.cu): slot groups no tile covers are skipped without a search,
+// which at |M| >> n (C5: 512 M slots, 16.5 M touched) is most of the pass.
 __global__ void det_reduce_kernel(float* __restrict__ dM, const float* __restrict__ ws,
                                   const int32_t* __restrict__ sorted, const int64_t* __restrict__ sorted_off,
-                                  int ntiles, int64_t tile_elems, int nsplit, int64_t mem_size) {
+                                  int ntiles, int64_t tile_elems, int nsplit, int64_t mem_size,
+                                  const int64_t* __restrict__ iv_start, const int64_t* __restrict__ iv_prefix,
+                                  int n_iv, int64_t n_touched) {
   int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   int64_t s = q * 4;
+  if (n_iv > 0) {
+    if (s >= n_touched) return;
+    int a = 0, b = n_iv - 1;   // interval: the largest i with prefix[i] <= s (runs are multiples of 4)
+    while (a < b) {
+      const int mid = (a + b + 1) >> 1;
+      if (__ldg(iv_prefix + mid) <= s) a = mid; else b = mid - 1;
+    }
+    s = __ldg(iv_start + a) + (s - __ldg(iv_prefix + a));
+  }
   if (s >= mem_size) return;
   // lo = first i with sorted_off[i] > s - T ; hi = first i with sorted_off[i] > s
   int lo = 0, hi = ntiles;
@@ -197,10 +211,15 @@ __global__ void det_reduce_kernel(float* __restrict__ dM, const float* __restric
       acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     }
   }
-  float4* d = reinterpret_cast<float4*>(dM + s);
-  float4 o = *d;
-  o.x += acc.x; o.y += acc.y; o.z += acc.z; o.w += acc.w;
-  *d = o;
+  if (s + 4 <= mem_size) {
+    float4* d = reinterpret_cast<float4*>(dM + s);
+    float4 o = *d;
+    o.x += acc.x; o.y += acc.y; o.z += acc.z; o.w += acc.w;
+    *d = o;
+  } else {   // |M| % 4 != 0: the last group is partial
+    const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+    for (int k = 0; s + k < mem_size; ++k) dM[s + k] += a4[k];
+  }
 }
 
 __global__ void sync_shadow_kernel(const float* __restrict__ M, __nv_bfloat16* __restrict__ sh, int64_t n,
@@ -286,12 +305,21 @@ cudaError_t launch_simt_dw(const Ctx* c, const Module& m, const void* X, const v
   return cudaGetLastError();
 }
 
-cudaError_t launch_det_reduce(const Ctx* c, const Module& m, const float* ws, int nsplit, cudaStream_t s) {
-  int64_t nthreads = c->mem_size / 4;
+cudaError_t launch_det_reduce(Ctx* c, const Module& m, const float* ws, int nsplit, cudaStream_t s) {
+  if (!(c->touched_valid && c->touched_for == int64_t(c->modules.size()))) {   // build once, eagerly
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) touched_prepare(c, s);
+  }
+  const bool touched = c->touched_valid && c->touched_for == int64_t(c->modules.size()) && c->touched_vec &&
+                       c->n_iv > 0;
+  int64_t nthreads = ((touched ? c->touched_n : c->mem_size) + 3) / 4;
   int threads = 256;
   int64_t blocks = (nthreads + threads - 1) / threads;
   det_reduce_kernel<<<unsigned(blocks), threads, 0, s>>>(c->dM, ws, m.d_sorted, m.d_sorted_off, m.nx * m.ny,
-                                                         int64_t(c->tile.z1) * c->tile.z2, nsplit, c->mem_size);
+                                                         int64_t(c->tile.z1) * c->tile.z2, nsplit, c->mem_size,
+                                                         touched ? c->d_iv : nullptr,
+                                                         touched ? c->d_iv + c->n_iv : nullptr,
+                                                         touched ? c->n_iv : 0, touched ? c->touched_n : 0);
   return cudaGetLastError();
 }
 
