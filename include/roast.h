@@ -125,6 +125,18 @@ roast_status_t roast_register_linear_seg(roast_t h, int64_t in_features, int64_t
 roast_status_t roast_register_embedding_seg(roast_t h, int64_t num_rows, int32_t dim, int32_t chunk,
                                             double fan_in, int64_t seg_base, int64_t seg_size, int32_t* id);
 
+/* Fuse already-registered linears that share in_features into one GEMM along out_features
+ * (e.g. BERT's Q, K, V projections of the same input): the group's virtual weight is
+ * [W_1 | W_2 | ... | W_n] (in x sum out_i), its tile map the members' maps side by side, so
+ * every slot, sign and lambda is the members' own (each keeps its independent hash)
+ * and Y_group = [Y_1 | ... | Y_n], dX_group = sum_i dY_i W_i^T, dM += every member's
+ * scatter — one launch each instead of n, over a wider N (more CTA pairs busy on small
+ * layers).  *group_id is usable wherever a linear id is (fwd / fwd_bias / bwd / bwd_dx /
+ * bwd_dm / tuning / debug_materialize); group ids live outside the module id space
+ * (>= 2^24), so creating a group never changes the hash keys of later registrations.
+ * Errors: STATE (a member is not a registered linear), SHAPE (in_features differ). */
+roast_status_t roast_register_linear_concat(roast_t h, const int32_t* ids, int32_t n, int32_t* group_id);
+
 /* Kernel-configuration autotuner (NEXT #4).  The paper autotunes its
  * tile per layer shape, either inference-optimal (tune the forward kernel, the
  * backward kernels share its tile) or training-optimal (tune forward and backward
@@ -191,6 +203,10 @@ roast_status_t roast_linear_bwd_dx_chain(roast_t h, int32_t id_a, int32_t id_b, 
 roast_status_t roast_bias_fwd(roast_t h, int32_t bias_id, float* d_b, roast_stream_t stream);
 roast_status_t roast_bias_bwd(roast_t h, int32_t bias_id, const void* d_dY, int64_t tokens, roast_dtype_t dt,
                               roast_stream_t stream);
+/* The same with dY rows `ld` elements apart (ld >= the bias length, even): the bias of one
+ * member of a roast_register_linear_concat group reads its column slice of the group's dY. */
+roast_status_t roast_bias_bwd_ld(roast_t h, int32_t bias_id, const void* d_dY, int64_t tokens, int64_t ld,
+                                 roast_dtype_t dt, roast_stream_t stream);
 
 /* a2 + a3: dX = lambda * dY W~^T (skipped if d_dX == NULL), and
  * dM[h(x,y) + pi(o1,o2)] += lambda * g(x,y) * (X^T dY)[i, j] for every virtual

@@ -37,6 +37,13 @@ static Ctx* ctx(roast_t h) { return reinterpret_cast<Ctx*>(h); }
 
 static roast_status_t get_module(Ctx* c, int32_t id, ModuleKind kind, Module** out) {
   if (!c) return fail(ROAST_ERR_STATE, "null handle");
+  if (id >= kGroupIdBase) {   // roast_register_linear_concat groups (their own id space)
+    if (kind != kLinear || id - kGroupIdBase >= int32_t(c->groups.size()))
+      return fail(ROAST_ERR_STATE, "unknown linear group id");
+    if (!c->M || !c->dM) return fail(ROAST_ERR_STATE, "roast_bind has not been called");
+    *out = &c->groups[id - kGroupIdBase];
+    return ROAST_OK;
+  }
   if (id < 0 || id >= int32_t(c->modules.size())) return fail(ROAST_ERR_STATE, "unknown module id");
   if (c->modules[id].kind != kind) return fail(ROAST_ERR_STATE, "module kind mismatch");
   if (!c->M || !c->dM) return fail(ROAST_ERR_STATE, "roast_bind has not been called");
@@ -78,6 +85,50 @@ roast_status_t opt_prepare(Ctx* c, const roast_opt_config_t* cfg, int64_t step, 
     if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
       return fail(ROAST_ERR_STATE, "touched set: call roast_touched_size before capturing");
     if (roast_status_t st = touched_prepare(c, s)) return st;
+  }
+  return ROAST_OK;
+}
+}  // namespace roast
+
+namespace roast {
+// Device copies of a linear's tile map (h_off / h_sgn [x][y] filled): offsets, signs, the
+// offset-sorted order for the deterministic reduce, and the packed TMA coordinates.
+roast_status_t upload_linear_tables(Ctx* c, Module& m) {
+  const int64_t A = c->cfg.align_elems;
+  const int64_t nt = int64_t(m.nx) * m.ny;
+  // offset-sorted tile order for the deterministic reduce (ties: tile id)
+  std::vector<int32_t> order(nt);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return m.h_off[a] < m.h_off[b]; });
+  std::vector<int64_t> soff(nt);
+  for (int64_t i = 0; i < nt; ++i) soff[i] = m.h_off[order[i]];
+  cudaError_t e = cudaSuccess;
+  e = cudaMalloc(reinterpret_cast<void**>(&m.d_off), nt * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&m.d_sgn), nt * sizeof(int8_t));
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&m.d_sorted), nt * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&m.d_sorted_off), nt * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMemcpy(m.d_off, m.h_off.data(), nt * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(m.d_sgn, m.h_sgn.data(), nt * sizeof(int8_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(m.d_sorted, order.data(), nt * sizeof(int32_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(m.d_sorted_off, soff.data(), nt * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && c->mem_size < (int64_t(1) << 33) && A % 8 == 0) {
+    std::vector<int32_t> cxy(nt), cyx(nt);
+    for (int32_t x = 0; x < m.nx; ++x)
+      for (int32_t y = 0; y < m.ny; ++y) {
+        const int64_t t = int64_t(x) * m.ny + y;
+        const int64_t off = m.h_off[t];
+        const int32_t packed = int32_t(((off >> 6) << 4) | (m.h_sgn[t] < 0 ? 8 : 0) | ((off >> 3) & 7));
+        cxy[t] = packed;
+        cyx[int64_t(y) * m.nx + x] = packed;
+      }
+    e = cudaMalloc(reinterpret_cast<void**>(&m.d_coord_xy), nt * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&m.d_coord_yx), nt * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMemcpy(m.d_coord_xy, cxy.data(), nt * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(m.d_coord_yx, cyx.data(), nt * sizeof(int32_t), cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) {
+    free_module(m);
+    return cuda_fail(e, "register_linear upload");
   }
   return ROAST_OK;
 }
@@ -157,6 +208,7 @@ roast_status_t roast_destroy(roast_t h) {
   if (!c) return ROAST_OK;
   cudaDeviceSynchronize();
   for (auto& m : c->modules) free_module(m);
+  for (auto& m : c->groups) free_module(m);
   cudaFree(c->shadow);
   cudaFree(c->d_err);
   cudaFree(c->ws);
@@ -257,42 +309,51 @@ roast_status_t roast_register_linear_seg(roast_t h, int64_t H, int64_t O, int64_
       }
     m.lam = float(c->cfg.C / sqrt(double(H)));
   }
-  // offset-sorted tile order for the deterministic reduce (ties: tile id)
-  std::vector<int32_t> order(nt);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return m.h_off[a] < m.h_off[b]; });
-  std::vector<int64_t> soff(nt);
-  for (int64_t i = 0; i < nt; ++i) soff[i] = m.h_off[order[i]];
-  cudaError_t e = cudaSuccess;
-  e = cudaMalloc(reinterpret_cast<void**>(&m.d_off), nt * sizeof(int64_t));
-  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&m.d_sgn), nt * sizeof(int8_t));
-  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&m.d_sorted), nt * sizeof(int32_t));
-  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&m.d_sorted_off), nt * sizeof(int64_t));
-  if (e == cudaSuccess) e = cudaMemcpy(m.d_off, m.h_off.data(), nt * sizeof(int64_t), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(m.d_sgn, m.h_sgn.data(), nt * sizeof(int8_t), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(m.d_sorted, order.data(), nt * sizeof(int32_t), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(m.d_sorted_off, soff.data(), nt * sizeof(int64_t), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && c->mem_size < (int64_t(1) << 33) && A % 8 == 0) {
-    std::vector<int32_t> cxy(nt), cyx(nt);
-    for (int32_t x = 0; x < m.nx; ++x)
-      for (int32_t y = 0; y < m.ny; ++y) {
-        const int64_t t = int64_t(x) * m.ny + y;
-        const int64_t off = m.h_off[t];
-        const int32_t packed = int32_t(((off >> 6) << 4) | (m.h_sgn[t] < 0 ? 8 : 0) | ((off >> 3) & 7));
-        cxy[t] = packed;
-        cyx[int64_t(y) * m.nx + x] = packed;
-      }
-    e = cudaMalloc(reinterpret_cast<void**>(&m.d_coord_xy), nt * sizeof(int32_t));
-    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&m.d_coord_yx), nt * sizeof(int32_t));
-    if (e == cudaSuccess) e = cudaMemcpy(m.d_coord_xy, cxy.data(), nt * sizeof(int32_t), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(m.d_coord_yx, cyx.data(), nt * sizeof(int32_t), cudaMemcpyHostToDevice);
-  }
-  if (e != cudaSuccess) {
-    free_module(m);
-    return cuda_fail(e, "register_linear upload");
-  }
+  if (roast_status_t st = upload_linear_tables(c, m)) return st;
   c->modules.push_back(std::move(m));
   if (id) *id = int32_t(mid);
+  return ROAST_OK;
+}
+
+
+roast_status_t roast_register_linear_concat(roast_t h, const int32_t* ids, int32_t n, int32_t* group_id) {
+  Ctx* c = ctx(h);
+  if (!c) return fail(ROAST_ERR_STATE, "null handle");
+  if (!ids || n < 1) return fail(ROAST_ERR_CONFIG, "null / empty member list");
+  std::vector<const Module*> mem(n);
+  for (int i = 0; i < n; ++i) {
+    if (ids[i] < 0 || ids[i] >= int32_t(c->modules.size()) || c->modules[ids[i]].kind != kLinear)
+      return fail(ROAST_ERR_STATE, "member is not a registered linear");
+    mem[i] = &c->modules[ids[i]];
+    if (mem[i]->H != mem[0]->H || mem[i]->lam != mem[0]->lam)
+      return fail(ROAST_ERR_SHAPE, "members need equal in_features (and lambda)");
+  }
+  Module g;
+  g.kind = kLinear;
+  g.lam = mem[0]->lam;
+  g.hash = mem[0]->hash;   // unused: the group's tiles come from its members' maps
+  g.H = mem[0]->H;
+  g.nx = mem[0]->nx;
+  for (const Module* m : mem) {
+    g.O += m->O;
+    g.ny += m->ny;
+  }
+  const int64_t nt = int64_t(g.nx) * g.ny;
+  g.h_off.resize(nt);
+  g.h_sgn.resize(nt);
+  for (int32_t x = 0; x < g.nx; ++x) {
+    int32_t y0 = 0;
+    for (const Module* m : mem) {   // row x of the group = row x of every member, side by side
+      for (int32_t y = 0; y < m->ny; ++y) {
+        g.h_off[int64_t(x) * g.ny + y0 + y] = m->h_off[int64_t(x) * m->ny + y];
+        g.h_sgn[int64_t(x) * g.ny + y0 + y] = m->h_sgn[int64_t(x) * m->ny + y];
+      }
+      y0 += m->ny;
+    }
+  }
+  if (roast_status_t st = upload_linear_tables(c, g)) return st;
+  c->groups.push_back(std::move(g));
+  if (group_id) *group_id = kGroupIdBase + int32_t(c->groups.size()) - 1;
   return ROAST_OK;
 }
 
@@ -421,6 +482,11 @@ roast_status_t roast_bias_fwd(roast_t h, int32_t bias_id, float* b, roast_stream
 
 roast_status_t roast_bias_bwd(roast_t h, int32_t bias_id, const void* dY, int64_t T, roast_dtype_t dt,
                               roast_stream_t stream) {
+  return roast_bias_bwd_ld(h, bias_id, dY, T, -1, dt, stream);
+}
+
+roast_status_t roast_bias_bwd_ld(roast_t h, int32_t bias_id, const void* dY, int64_t T, int64_t ld, roast_dtype_t dt,
+                                 roast_stream_t stream) {
   Ctx* c = ctx(h);
   Module* m;
   roast_status_t st = get_module(c, bias_id, kEmbedding, &m);
@@ -432,12 +498,14 @@ roast_status_t roast_bias_bwd(roast_t h, int32_t bias_id, const void* dY, int64_
   if (reinterpret_cast<uintptr_t>(dY) & 7) return fail(ROAST_ERR_CONFIG, "dY must be 8-byte aligned");
   const cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int n = m->dim;
+  if (ld < 0) ld = n;
+  if (ld < n || (ld % 2)) return fail(ROAST_ERR_SHAPE, "ld must be >= the bias length and even");
   const int slabs = colsum_slabs(T, n);
   float* tmp = nullptr;   // stream-ordered scratch: slab partials, then db (capturable)
   ROAST_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), (size_t(slabs) + 1) * n * sizeof(float) + 16, s));
   float* db = tmp + size_t(slabs) * n;
   db = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(db) + 15) & ~uintptr_t(15));
-  cudaError_t e = launch_colsum(dY, T, n, dt, tmp, db, s);
+  cudaError_t e = launch_colsum(dY, T, n, ld, dt, tmp, db, s);
   c->launches += 2;
   if (e == cudaSuccess) {
     if (c->cfg.deterministic) {

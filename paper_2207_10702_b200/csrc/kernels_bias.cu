@@ -19,8 +19,8 @@ namespace roast {
 namespace {
 
 template <typename XT>
-__global__ void __launch_bounds__(256) colsum_kernel(const XT* __restrict__ dY, int64_t T, int n, int64_t rows_per_slab,
-                                                     float* __restrict__ partial) {
+__global__ void __launch_bounds__(256) colsum_kernel(const XT* __restrict__ dY, int64_t T, int n, int64_t ld,
+                                                     int64_t rows_per_slab, float* __restrict__ partial) {
   __shared__ float2 red[8][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int col = blockIdx.x * 64 + 2 * lane;
@@ -34,10 +34,10 @@ __global__ void __launch_bounds__(256) colsum_kernel(const XT* __restrict__ dY, 
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if constexpr (sizeof(XT) == 2) {
-          const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(dY + (r + 8 * u) * n + col);
+          const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(dY + (r + 8 * u) * ld + col);
           v[u] = __bfloat1622float2(b);
         } else {
-          v[u] = *reinterpret_cast<const float2*>(dY + (r + 8 * u) * n + col);
+          v[u] = *reinterpret_cast<const float2*>(dY + (r + 8 * u) * ld + col);
         }
       }
 #pragma unroll
@@ -49,9 +49,9 @@ __global__ void __launch_bounds__(256) colsum_kernel(const XT* __restrict__ dY, 
     for (; r < r1; r += 8) {
       float2 v;
       if constexpr (sizeof(XT) == 2)
-        v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dY + r * n + col));
+        v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dY + r * ld + col));
       else
-        v = *reinterpret_cast<const float2*>(dY + r * n + col);
+        v = *reinterpret_cast<const float2*>(dY + r * ld + col);
       acc.x += v.x;
       acc.y += v.y;
     }
@@ -86,15 +86,15 @@ int colsum_slabs(int64_t T, int n) {
   return int(std::max<int64_t>(slabs, 1));
 }
 
-cudaError_t launch_colsum(const void* dY, int64_t T, int n, roast_dtype_t dt, float* partial, float* db,
+cudaError_t launch_colsum(const void* dY, int64_t T, int n, int64_t ld, roast_dtype_t dt, float* partial, float* db,
                           cudaStream_t s) {
   const int slabs = colsum_slabs(T, n);
   const int64_t rows = (T + slabs - 1) / slabs;
   dim3 grid(unsigned((n + 63) / 64), unsigned(slabs));
   if (dt == ROAST_BF16)
-    colsum_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(dY), T, n, rows, partial);
+    colsum_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(dY), T, n, ld, rows, partial);
   else
-    colsum_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(dY), T, n, rows, partial);
+    colsum_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(dY), T, n, ld, rows, partial);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   slab_sum_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(partial, slabs, n, db);

@@ -15,6 +15,7 @@
 namespace roast {
 
 enum ModuleKind { kLinear = 0, kEmbedding = 1 };
+constexpr int32_t kGroupIdBase = 1 << 24;
 
 struct Module {
   ModuleKind kind;
@@ -51,6 +52,10 @@ struct Ctx {
   int64_t shadow_elems = 0;
   int64_t neg_base = 0;           // index of the negated copy (128-B aligned)
   std::vector<Module> modules;
+  // roast_register_linear_concat: linears sharing in_features fused along out_features (their
+  // tile maps side by side, one GEMM per call); ids kGroupIdBase + index, outside the module
+  // id space so they never shift the hash keys of later registrations
+  std::vector<Module> groups;
   int64_t identity_cursor = 0;    // IDENTITY mapping: next free base
   // device error flag (sticky)
   int32_t* d_err = nullptr;
@@ -119,7 +124,7 @@ cudaError_t launch_simt_fwd(const Ctx* c, const Module& m, const void* X, void* 
                             bool transpose_w, cudaStream_t s, const float* bias = nullptr);
 // bias backward, first half: db[j] = sum_t dY[t, j] in fp32, fixed order (slab partials
 // then an in-order sum over slabs) -> db [n]
-cudaError_t launch_colsum(const void* dY, int64_t T, int n, roast_dtype_t dt, float* partial, float* db,
+cudaError_t launch_colsum(const void* dY, int64_t T, int n, int64_t ld, roast_dtype_t dt, float* partial, float* db,
                           cudaStream_t s);
 int colsum_slabs(int64_t T, int n);
 cudaError_t launch_simt_dw(const Ctx* c, const Module& m, const void* X, const void* dY, int64_t T,

@@ -55,6 +55,40 @@ class _LinearFn(torch.autograd.Function):
         return (dx.reshape(ctx.shape) if dx is not None else None), None, None, None, None
 
 
+class _LinearGroupFn(torch.autograd.Function):
+    """y = x [W_1 | ... | W_n] (+ [b_1 | ... | b_n]) for a roast_register_linear_concat group:
+    one forward GEMM, one dX GEMM (dX = sum_i dY_i W_i^T over the concatenated K), one dM GEMM;
+    each member bias's backward reads its column slice of dY in place."""
+
+    @staticmethod
+    def forward(ctx, x, anchor, store, gid, bias_mids):
+        H = store.dims[gid][1]
+        x2 = x.reshape(-1, H).contiguous()
+        b = torch.cat([store.bias_fwd(m) for m in bias_mids]) if bias_mids else None
+        y = store.fwd(gid, x2, bias=b)
+        ctx.save_for_backward(x2)
+        ctx.store, ctx.gid, ctx.bias_mids, ctx.shape = store, gid, bias_mids, x.shape
+        return y.reshape(*x.shape[:-1], y.shape[-1])
+
+    @staticmethod
+    def backward(ctx, dy):
+        (x2,) = ctx.saved_tensors
+        store, gid = ctx.store, ctx.gid
+        dy2 = dy.reshape(x2.shape[0], -1).contiguous().to(x2.dtype)
+        dx = None
+        if ctx.needs_input_grad[0]:
+            dx = torch.empty_like(x2)
+            store.bwd_dx(gid, dy2, dx)
+        store.bwd_dm(gid, x2, dy2)
+        if ctx.bias_mids:
+            c0 = 0
+            for m in ctx.bias_mids:
+                n = store.dims[m][2]
+                store.bias_bwd(m, dy2[:, c0:c0 + n])
+                c0 += n
+        return (dx.reshape(ctx.shape) if dx is not None else None), None, None, None, None
+
+
 class RoastBias(torch.nn.Module):
     """A bias vector of n elements recovered with L in chunks of `chunk` (reading R24:
     registered as a 1 x n embedding, lambda = fp32(C / sqrt(fan_in)) with fan_in the
@@ -117,7 +151,7 @@ class EncoderLayer(torch.nn.Module):
     are ROAST modules in one GMS store.  N-operations (attention math, GELU, LayerNorm;
     P:263-265) are plain torch."""
 
-    def __init__(self, store, d_model=768, d_ff=3072, heads=12, bias=False):
+    def __init__(self, store, d_model=768, d_ff=3072, heads=12, bias=False, fuse_qkv=True):
         super().__init__()
         self.heads = heads
         self.q = RoastLinear(store, d_model, d_model, bias)
@@ -128,6 +162,20 @@ class EncoderLayer(torch.nn.Module):
         self.ff2 = RoastLinear(store, d_ff, d_model, bias)
         self.ln1 = torch.nn.LayerNorm(d_model)
         self.ln2 = torch.nn.LayerNorm(d_model)
+        # Q, K, V read the same input: one 768 x 2304 GEMM over the three modules' own tiles
+        # (registration order and hashes unchanged; the group id lives outside the module ids)
+        self.qkv_gid = store.linear_concat([self.q.mid, self.k.mid, self.v.mid]) if fuse_qkv else None
+
+    def _qkv(self, x):
+        """(q, k, v) projections: fused ROAST group, a fused dense Linear, or three calls."""
+        d = x.shape[-1]
+        dense = getattr(self, "qkv_dense", None)
+        if dense is not None:
+            return dense(x).split(d, dim=-1)
+        if getattr(self, "qkv_gid", None) is not None:
+            bias = tuple(lin.bias.mid for lin in (self.q, self.k, self.v)) if self.q.bias is not None else ()
+            return _LinearGroupFn.apply(x, _anchor(self.q.store), self.q.store, self.qkv_gid, bias).split(d, dim=-1)
+        return self.q(x), self.k(x), self.v(x)
 
     def forward(self, x):                   # x: [B, S, d]
         B, S, d = x.shape
@@ -135,7 +183,8 @@ class EncoderLayer(torch.nn.Module):
 
         def split(t):
             return t.reshape(B, S, h, d // h).transpose(1, 2)
-        a = torch.nn.functional.scaled_dot_product_attention(split(self.q(x)), split(self.k(x)), split(self.v(x)))
+        q, k, v = self._qkv(x)
+        a = torch.nn.functional.scaled_dot_product_attention(split(q), split(k), split(v))
         a = a.transpose(1, 2).reshape(B, S, d)
         x = self.ln1(x + self.o(a))
         return self.ln2(x + self.ff2(torch.nn.functional.gelu(self.ff1(x))))

@@ -26,7 +26,7 @@ EXPORTS = [
     "roast_register_embedding_seg", "roast_linear_fwd", "roast_linear_bwd",
     "roast_linear_bwd_dx", "roast_linear_bwd_dm", "roast_embedding_fwd", "roast_embedding_bwd",
     "roast_embedding_fwd_multi", "roast_embedding_bwd_multi", "roast_set_autotune", "roast_get_tuned", "roast_set_tuned",
-    "roast_linear_fwd_bias", "roast_bias_fwd", "roast_bias_bwd", "roast_linear_fwd_chain",
+    "roast_linear_fwd_bias", "roast_bias_fwd", "roast_bias_bwd", "roast_bias_bwd_ld", "roast_register_linear_concat", "roast_linear_fwd_chain",
     "roast_linear_bwd_dx_chain", "roast_comm_unique_id", "roast_comm_init",
     "roast_grad_allreduce", "roast_set_exchange", "roast_touched_size", "roast_touched_intervals",
     "roast_debug_exchange", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step", "roast_grad_exchange_step",
@@ -83,6 +83,8 @@ def _load():
         "roast_linear_fwd_chain": (st, [H, I32, I32, P, P, P, I64, ctypes.c_int, P, P, S]),
         "roast_linear_bwd_dx_chain": (st, [H, I32, I32, P, P, P, I64, ctypes.c_int, S]),
         "roast_bias_bwd": (st, [H, I32, P, I64, ctypes.c_int, S]),
+        "roast_bias_bwd_ld": (st, [H, I32, P, I64, I64, ctypes.c_int, S]),
+        "roast_register_linear_concat": (st, [H, P, I32, ctypes.POINTER(I32)]),
         "roast_get_tuned": (st, [H, I32, I32, I64, ctypes.POINTER(I32), ctypes.POINTER(I32)]),
         "roast_set_tuned": (st, [H, I32, I32, I64, I32, I32]),
         "roast_register_linear_seg": (st, [H, I64, I64, I64, I64, ctypes.POINTER(I32)]),
@@ -236,6 +238,17 @@ def roast_bias_fwd(h, bias_id, b_ptr, stream=0):
 
 def roast_bias_bwd(h, bias_id, dY_ptr, tokens, dtype, stream=0):
     _check(_lib.roast_bias_bwd(h, bias_id, dY_ptr, tokens, dtype, stream), "roast_bias_bwd")
+
+
+def roast_bias_bwd_ld(h, bias_id, dY_ptr, tokens, ld, dtype, stream=0):
+    _check(_lib.roast_bias_bwd_ld(h, bias_id, dY_ptr, tokens, ld, dtype, stream), "roast_bias_bwd_ld")
+
+
+def roast_register_linear_concat(h, ids):
+    arr = (ctypes.c_int32 * len(ids))(*ids)
+    out = ctypes.c_int32()
+    _check(_lib.roast_register_linear_concat(h, arr, len(ids), ctypes.byref(out)), "roast_register_linear_concat")
+    return out.value
 
 
 def roast_linear_fwd(h, mid, X_ptr, Y_ptr, tokens, dtype, stream=0):
@@ -418,6 +431,12 @@ class Roast:
         self.dims[mid] = ("linear", in_features, out_features)
         return mid
 
+    def linear_concat(self, mids):
+        """One GEMM over linears sharing in_features: W = [W_1 | ... | W_n] (their own tiles)."""
+        gid = roast_register_linear_concat(self.h, list(mids))
+        self.dims[gid] = ("linear", self.dims[mids[0]][1], sum(self.dims[m][2] for m in mids))
+        return gid
+
     def set_autotune(self, strategy):
         roast_set_autotune(self.h, strategy)
 
@@ -485,10 +504,14 @@ class Roast:
         return out
 
     def bias_bwd(self, bias_mid, dY, stream=None):
-        """dM += lambda g * (column sums of dY) scattered through the bias's L mapping."""
+        """dM += lambda g * (column sums of dY) scattered through the bias's L mapping.  dY may be
+        a column slice of a wider row-major matrix (rows dY.stride(0) elements apart)."""
         n = self.dims[bias_mid][2]
-        assert dY.is_contiguous() and dY.shape[-1] == n
-        roast_bias_bwd(self.h, bias_mid, dY.data_ptr(), dY.numel() // n, self._dt(dY), self._s(stream))
+        if dY.dim() != 2:
+            dY = dY.reshape(-1, n)
+        assert dY.shape[-1] == n and (dY.shape[0] == 0 or dY.stride(-1) == 1)
+        ld = dY.stride(0) if dY.shape[0] > 1 else n
+        roast_bias_bwd_ld(self.h, bias_mid, dY.data_ptr(), dY.shape[0], ld, self._dt(dY), self._s(stream))
 
     def bwd(self, mid, X, dY, dX=None, need_dx=True, stream=None):
         _, H, O = self.dims[mid]

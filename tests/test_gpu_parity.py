@@ -655,3 +655,32 @@ def test_set_tuned_seeds_the_cache(R, torch):
     for bad in [(0, T, 3, 1), (0, T, 1, 2), (3, T, 1, 1), (2, T, 1, 0)]:
         with pytest.raises(roast.RoastError):
             ctx.set_tuned(mid, *bad)
+
+
+@pytest.mark.parametrize("T", [8192, 1000])
+def test_linear_concat_group(R, torch, T):
+    """roast_register_linear_concat: Q, K, V-style linears sharing in_features as ONE GEMM each
+    way == the oracle on [W_q | W_k | W_v] (each member its own tiles, signs and lambda); the
+    group id does not shift the hash keys of later registrations."""
+    mem, H, O = 47192, 768, 768
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64)
+    mids = [ctx.linear(H, O) for _ in range(3)]
+    gid = ctx.linear_concat(mids)
+    after = ctx.linear(H, 3072)
+    specs = [OM.LinearSpec(H, O, 64, 64, mem, HS, m) for m in mids]
+    off, sgn = ctx.tile_map(after)
+    ref_after = OM.LinearSpec(H, 3072, 64, 64, mem, HS, 3)   # module id 3: the group took none
+    assert np.array_equal(off, ref_after.off) and np.array_equal(sgn.astype(np.int64), ref_after.sgn)
+    X_np = bf16_input(synth.SEED_X, (T, H))
+    dY_np = bf16_input(synth.SEED_DY, (T, 3 * O))
+    Y, dX, dM = run_linear(R, torch, ctx, gid, X_np, dY_np, torch.bfloat16)
+    W = np.concatenate([np.float64(sp.lam) * sp.materialize(M_np, "operand") for sp in specs], axis=1)
+    assert rel_frob(Y, X_np @ W) <= 1e-2
+    assert rel_frob(dX, dY_np @ W.T) <= 1e-2
+    ref_dM = np.zeros(mem)
+    for i, sp in enumerate(specs):
+        sp.backward_dm(X_np, dY_np[:, i * O:(i + 1) * O], ref_dM)
+    assert rel_frob(dM, ref_dM) <= 1e-2
+    Wg = ctx.materialize(gid, torch.bfloat16).float().cpu().numpy()
+    assert np.array_equal(Wg.astype(np.float64), np.concatenate([sp.materialize(M_np, "operand") for sp in specs], 1))

@@ -27,14 +27,18 @@ N_LIN = LAYERS * (4 * D * D + 2 * D * FF)   # 84 934 656 ("~85M MM params", P:52
 
 
 class DenseLayer(torch.nn.Module):
+    """The same layer with dense bf16 weights; Q, K, V fused into one 768 x 2304 Linear exactly
+    as the ROAST layer fuses them (one GEMM each way), so the comparison is like for like."""
+
     def __init__(self, bias=False):
         super().__init__()
         L = lambda i, o: torch.nn.Linear(i, o, bias=bias, dtype=torch.bfloat16)  # noqa: E731
-        self.q, self.k, self.v, self.o, self.ff1, self.ff2 = L(D, D), L(D, D), L(D, D), L(D, D), L(D, FF), L(FF, D)
+        self.qkv_dense, self.o, self.ff1, self.ff2 = L(D, 3 * D), L(D, D), L(D, FF), L(FF, D)
         self.ln1 = torch.nn.LayerNorm(D, dtype=torch.bfloat16)
         self.ln2 = torch.nn.LayerNorm(D, dtype=torch.bfloat16)
 
     forward = RN.EncoderLayer.forward
+    _qkv = RN.EncoderLayer._qkv
     heads = HEADS
 
 
@@ -70,6 +74,8 @@ def main():
     ap.add_argument("--graph", type=int, default=1, choices=[0, 1],
                     help="capture the whole training step (fwd + bwd + all-reduce + update) in a CUDA graph")
     ap.add_argument("--profile", action="store_true")
+    ap.add_argument("--breakdown", action="store_true",
+                    help="SURVEY §8(d): split one step's GPU time into linears / N-ops / exchange / update")
     ap.add_argument("--full", action="store_true",
                     help="whole BERT-base: word/pos/type embeddings and biases via L too (NEXT #3)")
     args = ap.parse_args()
@@ -133,6 +139,29 @@ def main():
             step()
     torch.cuda.current_stream().wait_stream(side)
     torch.cuda.synchronize()
+    if args.breakdown and rank == 0:       # GPU time of one eager step by kernel category
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step()
+            torch.cuda.synchronize()
+        cats = {"linears (ROAST-MM / dense GEMM)": 0.0, "embeddings + biases via L": 0.0, "exchange": 0.0,
+                "update + shadow": 0.0, "N-ops (attention, LayerNorm, GELU, elementwise)": 0.0}
+        for ev in prof.key_averages():
+            t = getattr(ev, "device_time_total", getattr(ev, "cuda_time_total", 0.0)) / 1e3   # ms
+            n = ev.key
+            if "roast_mm_sm100" in n or "gemm" in n.lower() or "sm90_xmma" in n or "cutlass" in n.lower() or "nvjet" in n:
+                cats["linears (ROAST-MM / dense GEMM)"] += t
+            elif "embed" in n or "colsum" in n or "bias" in n:
+                cats["embeddings + biases via L"] += t
+            elif "nccl" in n.lower() or "pack_kernel" in n:
+                cats["exchange"] += t
+            elif "opt_kernel" in n or "sync_shadow" in n or "Sgd" in n or "sgd" in n or "foreach" in n:
+                cats["update + shadow"] += t
+            elif "memset" not in n.lower() and "memcpy" not in n.lower():
+                cats["N-ops (attention, LayerNorm, GELU, elementwise)"] += t
+        print(json.dumps(dict(breakdown_ms={k: round(v, 3) for k, v in cats.items()},
+                              impl="dense-torch" if args.dense else "roast", full=bool(args.full),
+                              note="one eager step under torch.profiler (kernel time; launch gaps excluded)")))
     if args.profile and rank == 0:         # top GPU kernels of one eager step
         from torch.profiler import ProfilerActivity, profile
         with profile(activities=[ProfilerActivity.CUDA]) as prof:

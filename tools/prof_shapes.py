@@ -38,39 +38,41 @@ def main():
     ap.add_argument("--T", type=int, default=8192)
     ap.add_argument("--exps", default="0,1,2,3")
     ap.add_argument("--only", default="", help="substring filter on the kernel name")
+    ap.add_argument("--dims", default="768,3072", help="d_model,d_ff of the two layers (C3 attention: 768,768)")
     ap.add_argument("--wm", default="", help="restrict to these WM values, e.g. 1,2")
     ap.add_argument("--prof", action="store_true", help="also print one ROAST_PROF counter line per config")
     args = ap.parse_args()
     T = args.T
+    D, F = [int(v) for v in args.dims.split(",")]
     M = torch.rand(47192, device="cuda") * 2 - 1
     ctx = R.Roast(M, 64, 64)
     ctx.set_autotune(0)
-    l1 = ctx.linear(768, 3072)
-    l2 = ctx.linear(3072, 768)
+    l1 = ctx.linear(D, F)
+    l2 = ctx.linear(F, D)
     bf = torch.bfloat16
-    X = torch.randn(T, 768, device="cuda").to(bf)
-    dY2 = torch.randn(T, 768, device="cuda").to(bf)
-    Y1 = torch.randn(T, 3072, device="cuda").to(bf)
-    Y2 = torch.empty(T, 768, device="cuda", dtype=bf)
-    dY1 = torch.randn(T, 3072, device="cuda").to(bf)
-    dX = torch.empty(T, 768, device="cuda", dtype=bf)
+    X = torch.randn(T, D, device="cuda").to(bf)
+    dY2 = torch.randn(T, D, device="cuda").to(bf)
+    Y1 = torch.randn(T, F, device="cuda").to(bf)
+    Y2 = torch.empty(T, D, device="cuda", dtype=bf)
+    dY1 = torch.randn(T, F, device="cuda").to(bf)
+    dX = torch.empty(T, D, device="cuda", dtype=bf)
     W1 = ctx.materialize(l1, bf)
     W2 = ctx.materialize(l2, bf)
     rows = [
-        ("fwd L1 768->3072", l1, 0, lambda: ctx.fwd(l1, X, Y1), lambda: torch.matmul(X, W1, out=Y1)),
-        ("fwd L2 3072->768", l2, 0, lambda: ctx.fwd(l2, Y1, Y2), lambda: torch.matmul(Y1, W2, out=Y2)),
-        ("dx L2 768->3072", l2, 1, lambda: ctx.bwd_dx(l2, dY2, dY1), lambda: torch.matmul(dY2, W2.t(), out=dY1)),
-        ("dx L1 3072->768", l1, 1, lambda: ctx.bwd_dx(l1, dY1, dX), lambda: torch.matmul(dY1, W1.t(), out=dX)),
-        ("dm L2 3072x768", l2, 2, lambda: ctx.bwd_dm(l2, Y1, dY2), lambda: torch.matmul(Y1.t(), dY2)),
-        ("dm L1 768x3072", l1, 2, lambda: ctx.bwd_dm(l1, X, dY1), lambda: torch.matmul(X.t(), dY1)),
+        (f"fwd L1 {D}->{F}", l1, 0, lambda: ctx.fwd(l1, X, Y1), lambda: torch.matmul(X, W1, out=Y1)),
+        (f"fwd L2 {F}->{D}", l2, 0, lambda: ctx.fwd(l2, Y1, Y2), lambda: torch.matmul(Y1, W2, out=Y2)),
+        (f"dx L2 {D}->{F}", l2, 1, lambda: ctx.bwd_dx(l2, dY2, dY1), lambda: torch.matmul(dY2, W2.t(), out=dY1)),
+        (f"dx L1 {F}->{D}", l1, 1, lambda: ctx.bwd_dx(l1, dY1, dX), lambda: torch.matmul(dY1, W1.t(), out=dX)),
+        (f"dm L2 {F}x{D}", l2, 2, lambda: ctx.bwd_dm(l2, Y1, dY2), lambda: torch.matmul(Y1.t(), dY2)),
+        (f"dm L1 {D}x{F}", l1, 2, lambda: ctx.bwd_dm(l1, X, dY1), lambda: torch.matmul(X.t(), dY1)),
     ]
-    flop = 2.0 * T * 768 * 3072
+    flop = 2.0 * T * D * F
     exps = [int(e) for e in args.exps.split(",")]
     for name, mid, kind, f, d in rows:
         if args.only and args.only not in name:
             continue
         td = time_us(d)
-        cfgs = [(1, 1), (2, 1)] if kind < 2 else [(1, 1), (1, 2), (1, 3), (2, 1), (2, 2)]
+        cfgs = [(1, 1), (2, 1)] if kind < 2 else [(1, 1), (1, 2), (1, 3), (1, 4), (1, 8), (2, 1), (2, 2), (2, 4)]
         if args.wm:
             cfgs = [c for c in cfgs if str(c[0]) in args.wm.split(",")]
         for wm, sp in cfgs:
