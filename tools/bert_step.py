@@ -74,6 +74,8 @@ def main():
     ap.add_argument("--graph", type=int, default=1, choices=[0, 1],
                     help="capture the whole training step (fwd + bwd + all-reduce + update) in a CUDA graph")
     ap.add_argument("--profile", action="store_true")
+    ap.add_argument("--autotune", type=int, default=2, choices=[0, 1, 2],
+                    help="kernel-configuration tuning: 0 makespan model, 1 inference-, 2 training-optimal")
     ap.add_argument("--breakdown", action="store_true",
                     help="SURVEY §8(d): split one step's GPU time into linears / N-ops / exchange / update")
     ap.add_argument("--full", action="store_true",
@@ -105,6 +107,7 @@ def main():
         mem = synth.compressed_size(n_virtual, args.ratio)
         M = (torch.rand(mem, device=dev) * 2 - 1).contiguous()
         store = R.Roast(M, 64, 64, seed=synth.HASH_SEED)
+        store.set_autotune(args.autotune)   # tuned during the eager warm-up, before capture
         dp.init_comm(store, rank, world, device=dev)
         if args.full:
             model = RN.RoastBert(store).to(dev)
