@@ -684,3 +684,33 @@ def test_linear_concat_group(R, torch, T):
     assert rel_frob(dM, ref_dM) <= 1e-2
     Wg = ctx.materialize(gid, torch.bfloat16).float().cpu().numpy()
     assert np.array_equal(Wg.astype(np.float64), np.concatenate([sp.materialize(M_np, "operand") for sp in specs], 1))
+
+
+def test_tcgen05_shape_fuzz(R, torch):
+    """Seeded random geometries through the tcgen05 path with forced kernel configurations
+    (WM 1 / 2, 192- or 256-column dX units, split-K 1-3 for dM): ragged tokens, N not a multiple
+    of the unit width, single-tile layers — Y, dX and dM against the oracle (bf16 bar)."""
+    rng = np.random.default_rng(2024)
+    mem = 60_000
+    M_np = store(mem)
+    for case in range(10):
+        H = 64 * int(rng.integers(1, 25))
+        O = 64 * int(rng.integers(1, 25))
+        T = int(rng.integers(1, 2500))
+        ctx, _ = make_ctx(R, torch, M_np, 64, 64)
+        mid = ctx.linear(H, O)
+        wm = int(rng.integers(1, 3))
+        ctx.set_tuned(mid, 0, T, wm, 4)
+        nu = 3 if (wm == 2 and H % 192 == 0 and rng.random() < 0.5) else 4
+        ctx.set_tuned(mid, 1, T, wm, nu)
+        ctx.set_tuned(mid, 2, T, int(rng.integers(1, 3)), int(rng.integers(1, 4)))
+        X_np = bf16_input(synth.SEED_X + case, (T, H))
+        dY_np = bf16_input(synth.SEED_DY + case, (T, O))
+        Y, dX, dM = run_linear(R, torch, ctx, mid, X_np, dY_np, torch.bfloat16)
+        spec = OM.LinearSpec(H, O, 64, 64, mem, HS, mid)
+        where = (case, H, O, T, wm, nu)
+        assert rel_frob(Y, spec.forward(X_np, M_np, True)) <= 1e-2, where
+        assert rel_frob(dX, spec.backward_dx(dY_np, M_np, True)) <= 1e-2, where
+        assert rel_frob(dM, spec.backward_dm(X_np, dY_np)) <= 1e-2, where
+        ctx.check()
+        ctx.close()
