@@ -326,6 +326,20 @@ def run_gpu(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    if world > 1:
+        # every rank must run the same configuration: the step-level choice below replays steps
+        # with the NCCL exchange inside, so a rank-dependent branch would mismatch collectives
+        import torch.distributed as dist
+        cfgs = torch.tensor([v for mid in (l1, l2) for j in range(3) for v in (ctx.tuned(mid, j, T) or (0, 0))],
+                            dtype=torch.int32, device=dev)
+        dist.broadcast(cfgs, 0)
+        vals = cfgs.tolist()
+        for i, mid in enumerate((l1, l2)):
+            for j in range(3):
+                wm, sp = vals[6 * i + 2 * j], vals[6 * i + 2 * j + 1]
+                if wm:
+                    ctx.set_tuned(mid, j, T, wm, sp)
+
     # training-optimal at the step level (P:428-429 tunes forward and backward together): a dX
     # GEMM tuned alone may pick 192-column units, which fill more CTA pairs but leave fewer
     # SMs to the dM GEMM running beside it on the second stream; keep whichever whole step
@@ -353,7 +367,13 @@ def run_gpu(args):
                 t192 = step_ms()
                 ctx.set_tuned(mid, 1, T, wm, 4)
                 t256 = step_ms()
-                if t192 < t256:
+                keep = t192 < t256
+                if world > 1:   # rank 0 decides for everyone (same configuration on every rank)
+                    import torch.distributed as dist
+                    flag = torch.tensor([int(keep)], dtype=torch.int32, device=dev)
+                    dist.broadcast(flag, 0)
+                    keep = bool(flag.item())
+                if keep:
                     ctx.set_tuned(mid, 1, T, wm, 3)
 
     # warm-up (eager), launches per step, then capture the step in a CUDA graph
