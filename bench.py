@@ -576,7 +576,8 @@ def run_gpu(args):
             import torch.distributed as dist
             dist.destroy_process_group()
         return
-    cb = cpu_sample(seconds_target=args.cpu_seconds) if not args.no_cpu else None
+    # the oracle baseline on the host cores: rank 0 at N = 1 only (the contract's cpu_baseline)
+    cb = cpu_sample(seconds_target=args.cpu_seconds) if not args.no_cpu and world == 1 else None
     line = dict(
         metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
         ms_per_step=ms_per_step, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="bf16",
