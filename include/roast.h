@@ -151,14 +151,14 @@ typedef enum { ROAST_TUNE_OFF = 0, ROAST_TUNE_INFERENCE = 1, ROAST_TUNE_TRAINING
 roast_status_t roast_set_autotune(roast_t h, roast_autotune_t strategy);
 /* The cached choice for a kernel (0 forward, 1 dX, 2 dM) of linear `id` at `tokens`:
  * *wm and *splits; for kernels 0 / 1 `splits` holds the output columns per unit / 64
- * (4 = 256; 3 = 192, dX with wm = 2 on 192-divisible outputs: C2's 768-wide dX fills 64 of
+ * (4 = 256; 3 = 192, with wm = 2 on 192-divisible outputs: a 768-wide output fills 64 of
  * 74 CTA pairs instead of 48; 1 = legacy, read as 4).  ROAST_ERR_STATE if that shape was
  * never tuned, BAD_ID. */
 roast_status_t roast_get_tuned(roast_t h, int32_t id, int32_t kernel, int64_t tokens, int32_t* wm, int32_t* splits);
 /* Seed the cache with a known choice (e.g. one tuned earlier and saved: a tuning cache
  * shared across processes); used whatever the strategy.  Errors: CONFIG (kernel not
- * 0..2, wm not 1..2, splits not 1..64, or splits not in {1, 4} for kernel 0 / {1, 3, 4}
- * for kernel 1), BAD_ID. */
+ * 0..2, wm not 1..2, splits not 1..64, or splits not in {1, 3, 4} for kernels 0 / 1),
+ * BAD_ID. */
 roast_status_t roast_set_tuned(roast_t h, int32_t id, int32_t kernel, int64_t tokens, int32_t wm, int32_t splits);
 
 /* a1: Y[tokens x out] = lambda * X[tokens x in] * W~, W~ tiles read from M

@@ -678,7 +678,7 @@ roast_status_t roast_set_tuned(roast_t h, int32_t id, int32_t kernel, int64_t to
   roast_status_t st = get_module(c, id, kLinear, &m);
   if (st) return st;
   if (kernel < 0 || kernel > 2 || wm < 1 || wm > 2 || splits < 1 || splits > 64 || tokens < 0 ||
-      (kernel < 2 && splits != 1 && splits != 4 && !(kernel == 1 && splits == 3)))
+      (kernel < 2 && splits != 1 && splits != 3 && splits != 4))
     return fail(ROAST_ERR_CONFIG, "bad tuned configuration");
   c->tuned[std::array<int64_t, 4>{kernel, m->H, m->O, tokens}] = {wm, splits};
   return ROAST_OK;

@@ -64,7 +64,9 @@ constexpr int KB_CHUNK = 64;  // k-blocks whose tile coordinates are staged in s
 template <int CG, int WM, int NU = BN>
 struct Cfg {
   static constexpr int A_BYTES = BM * WM * BK * 2;       // this CTA's 128*WM rows of A
-  static constexpr int B_BYTES = (NU / CG) * BK * 2;     // this CTA's NU/CG columns of B
+  // this CTA's NU/CG columns of B, in whole 64-wide tiles (NU = 192: 96 K-major rows for DX,
+  // two MN-major 64-column atoms for FWD)
+  static constexpr int B_BYTES = ((NU / CG + 63) / 64) * 64 * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int NBUF = 2;                         // epilogue staging buffers per warp
   static constexpr int STAGING = 4 * NBUF * 4096;        // 4 warps x NBUF x (32 rows x 128 B)
@@ -290,7 +292,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                    const __grid_constant__ Params p0, const __grid_constant__ CUtensorMap mapA1,
                    const __grid_constant__ CUtensorMap mapOut1, const __grid_constant__ Params p1,
                    const __grid_constant__ WMapsHalf hmaps) {
-  static_assert(NU == BN || (NU == 192 && MODE == DX && CG == 2 && WM == 2 && !CHAIN), "NU = 192: DX, 2 x 2 only");
+  static_assert(NU == BN || (NU == 192 && MODE != DW && CG == 2 && WM == 2 && !CHAIN), "NU = 192: FWD / DX, 2 x 2");
   using C = Cfg<CG, WM, NU>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t tx = MODE == DW ? (p.dw3d ? uint32_t(CG * (C::A_BYTES + C::B_BYTES))
                                                : uint32_t((m_sub_pair + n_sub) * 64 * 64 * 2))
                                      : uint32_t(((DIAG(p) & 32) ? 0 : CG * C::A_BYTES) +
-                                                ((DIAG(p) & 16) ? 0 : n_sub * 64 * 64 * 2));
+                                                ((DIAG(p) & 16) ? 0 : (MODE == FWD && NU == 192 ? 4 : n_sub) * 64 * 64 * 2));
       for (int kc = kb0; kc < kb1; kc += KB_CHUNK) {
         const int kc1 = min(kc + KB_CHUNK, kb1);
         if (MODE != DW) {
@@ -429,7 +431,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (CHAIN && prob == 1 && (kb & 3) == 0) wait_ready(p0.flags + mb * p0.n_tiles + (kb >> 2), 4 * CG);
               if (!(DIAG(p) & 32)) tma_load_2d<CG>(mA, a, fb, kb * BK, row0);
               const int32_t* cc = sCoord + (kb - kc) * 4;
-              if (NU == 192 && !(DIAG(p) & 16)) {
+              if (MODE == FWD && NU == 192 && !(DIAG(p) & 16)) {
+                // 96 MN-major B columns per CTA, whole tiles only (a 64-column SW128 atom cannot
+                // be half-filled from its right half): rank 0 = tile 0 | tile 1 loaded from its
+                // column 32 (its right half lands in the atom's left half, zeros after); rank 1 =
+                // tile 2 | tile 1 (left half used).  Accumulator columns [0,64) [64,96) [96,160)
+                // [160,192) hold output columns 0-63, 96-127, 128-191, 64-95 (epilogue permutes).
+                const int32_t ca = cc[rank ? 2 : 0], cb = cc[1];
+                const int ra = (ca >> 4) + ((ca & 8) ? int(p.neg_row) : 0);
+                const int rb = (cb >> 4) + ((cb & 8) ? int(p.neg_row) : 0);
+                tma_load_2d<CG>(&wmaps.m[ca & 7], b, fb, 0, ra);
+                tma_load_2d<CG>(&wmaps.m[cb & 7], b + 8192, fb, rank ? 0 : 32, rb);
+              } else if (NU == 192 && !(DIAG(p) & 16)) {
                 // 96 B rows (N) per CTA: rank 0 = tile 0 + rows 0-31 of tile 1, rank 1 = rows
                 // 32-63 of tile 1 + tile 2; every piece lands at a 1024-B multiple (SW128 phase)
                 const int32_t ca = cc[rank ? 1 : 0], cb = cc[rank ? 2 : 1];
@@ -562,7 +575,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         constexpr int COLS = MODE == DW ? 32 : 64;
         const int nsteps = n_valid / COLS;
         auto tload = [&](int c, uint32_t (&r)[64]) {
-          if (MODE != DW) {
+          if (MODE == FWD && NU == 192) {   // output step c from the permuted accumulator columns
+            const uint32_t lo = c == 0 ? 0u : c == 1 ? 160u : 96u, hi = c == 0 ? 32u : c == 1 ? 64u : 128u;
+            TMEM_LD32(tbase + lo, r);
+            TMEM_LD32(tbase + hi, (r + 32));
+          } else if (MODE != DW) {
             TMEM_LD32(tbase + uint32_t(c * 64), r);
             TMEM_LD32(tbase + uint32_t(c * 64 + 32), (r + 32));
           } else {
@@ -850,8 +867,8 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
 template <int MODE>
 roast_status_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o, const WMaps& w, Params p,
                       int wm, cudaStream_t s, int nu = BN, const WMapsHalf* hw = nullptr) {
-  if constexpr (MODE == DX) {
-    if (nu == 192) return launch_cg<DX, 2, 2, false, 192>(a, b, o, w, p, a, o, p, 0, s, hw);
+  if constexpr (MODE != DW) {
+    if (nu == 192) return launch_cg<MODE, 2, 2, false, 192>(a, b, o, w, p, a, o, p, 0, s, hw);
   }
   if (cta_group() == 1) return launch_cg<MODE, 1, 1>(a, b, o, w, p, a, o, p, 0, s);
   return wm == 2 ? launch_cg<MODE, 2, 2>(a, b, o, w, p, a, o, p, 0, s)
@@ -978,14 +995,14 @@ static roast_status_t tok_major_launch(Ctx* c, const Module& m, const void* A, v
   if (st) return st;
   const WMaps& w = *reinterpret_cast<const WMaps*>(c->tmap_shadow);
   const WMapsHalf* hw = reinterpret_cast<const WMapsHalf*>(c->tmap_shadow_half);
-  st = dx ? launch<DX>(a, a, o, w, p, wm, s, nu, hw) : launch<FWD>(a, a, o, w, p, wm, s);
+  st = dx ? launch<DX>(a, a, o, w, p, wm, s, nu, hw) : launch<FWD>(a, a, o, w, p, wm, s, nu, hw);
   if (!st) c->launches++;
   return st;
 }
 
 // (WM, N per unit) configurations a FWD / DX launch may use; the tuned map stores N / 64 in
 // the `splits` slot (legacy 1 = 256)
-static bool nu192_ok(bool dx, int wm, int N) { return dx && wm == 2 && cta_group() == 2 && N % 192 == 0; }
+static bool nu192_ok(bool dx, int wm, int N) { (void)dx; return wm == 2 && cta_group() == 2 && N % 192 == 0; }
 
 // makespan model (no tuning): rounds of units over the CTA pairs x per-unit MMA work
 static void choose_tok_major(int64_t T, int N, bool dx, int& wm, int& nu) {

@@ -615,8 +615,10 @@ def test_chain_fwd_and_dx_match_single_calls(R, torch, T):
 
 @pytest.mark.parametrize("H,O,T", [(768, 3072, 8192), (768, 3072, 1000), (3072, 768, 129), (768, 192, 513)])
 def test_dx_192_column_units(R, torch, H, O, T):
-    """dX with 512 x 192 units (N per unit = 3 hash tiles; each CTA of the pair stages 1.5 of
-    them as K-major B: a 64-row and a 32-row TMA box of the shadow) == oracle."""
+    """512 x 192 units (N per unit = 3 hash tiles).  dX: each CTA of the pair stages 1.5 tiles
+    as K-major B (a 64-row and a 32-row TMA box).  Forward: 1.5 MN-major tiles per CTA as two
+    whole boxes (one read from its column 32), the epilogue permuting accumulator columns;
+    with a bias added in the epilogue.  Both == oracle."""
     mem = 47192
     M_np = store(mem)
     ctx, _ = make_ctx(R, torch, M_np, 64, 64)
@@ -629,6 +631,14 @@ def test_dx_192_column_units(R, torch, H, O, T):
     spec = OM.LinearSpec(H, O, 64, 64, mem, HS, mid)
     assert ctx.tuned(mid, 1, T) == (2, 3)
     assert rel_frob(dX.float().cpu().numpy(), spec.backward_dx(dY_np, M_np, True)) <= 1e-2
+    if O % 192 == 0:
+        ctx.set_tuned(mid, 0, T, 2, 3)
+        X_np = bf16_input(synth.SEED_X, (T, H))
+        b_np = synth.normal(5, (O,)).astype(np.float32)
+        Y = ctx.fwd(mid, to_dev(X_np, torch.bfloat16), bias=to_dev(b_np, torch.float32))
+        torch.cuda.synchronize()
+        assert ctx.tuned(mid, 0, T) == (2, 3)
+        assert rel_frob(Y.float().cpu().numpy(), spec.forward(X_np, M_np, True) + b_np) <= 1e-2
     ctx.check()
 
 
@@ -700,7 +710,8 @@ def test_tcgen05_shape_fuzz(R, torch):
         ctx, _ = make_ctx(R, torch, M_np, 64, 64)
         mid = ctx.linear(H, O)
         wm = int(rng.integers(1, 3))
-        ctx.set_tuned(mid, 0, T, wm, 4)
+        nuf = 3 if (wm == 2 and O % 192 == 0 and rng.random() < 0.5) else 4
+        ctx.set_tuned(mid, 0, T, wm, nuf)
         nu = 3 if (wm == 2 and H % 192 == 0 and rng.random() < 0.5) else 4
         ctx.set_tuned(mid, 1, T, wm, nu)
         ctx.set_tuned(mid, 2, T, int(rng.integers(1, 3)), int(rng.integers(1, 4)))
@@ -708,7 +719,7 @@ def test_tcgen05_shape_fuzz(R, torch):
         dY_np = bf16_input(synth.SEED_DY + case, (T, O))
         Y, dX, dM = run_linear(R, torch, ctx, mid, X_np, dY_np, torch.bfloat16)
         spec = OM.LinearSpec(H, O, 64, 64, mem, HS, mid)
-        where = (case, H, O, T, wm, nu)
+        where = (case, H, O, T, wm, nuf, nu)
         assert rel_frob(Y, spec.forward(X_np, M_np, True)) <= 1e-2, where
         assert rel_frob(dX, spec.backward_dx(dY_np, M_np, True)) <= 1e-2, where
         assert rel_frob(dM, spec.backward_dm(X_np, dY_np)) <= 1e-2, where

@@ -72,7 +72,7 @@ def main():
         if args.only and args.only not in name:
             continue
         td = time_us(d)
-        cfgs = [(1, 1), (2, 1)] if kind < 2 else [(1, 1), (1, 2), (1, 3), (1, 4), (1, 8), (2, 1), (2, 2), (2, 4)]
+        cfgs = [(1, 1), (2, 1), (2, 3)] if kind < 2 else [(1, 1), (1, 2), (1, 3), (1, 4), (1, 8), (2, 1), (2, 2), (2, 4)]
         if args.wm:
             cfgs = [c for c in cfgs if str(c[0]) in args.wm.split(",")]
         for wm, sp in cfgs:
