@@ -207,6 +207,13 @@ roast_status_t roast_bias_bwd(roast_t h, int32_t bias_id, const void* d_dY, int6
  * member of a roast_register_linear_concat group reads its column slice of the group's dY. */
 roast_status_t roast_bias_bwd_ld(roast_t h, int32_t bias_id, const void* d_dY, int64_t tokens, int64_t ld,
                                  roast_dtype_t dt, roast_stream_t stream);
+/* The first half of the bias backward alone: db[j] = sum_t dY[t, j] (fp32, fixed order; rows
+ * `ld` elements apart, -1 = n; n and ld even; db 8-byte aligned, caller-owned, overwritten).
+ * A model with many biases via L (BERT: 72) collects every bias's db this way and scatters
+ * them all with one roast_embedding_bwd_multi per (dim, chunk) group (row 0 of each 1 x n
+ * table) instead of one L backward per bias. */
+roast_status_t roast_colsum(const void* d_dY, int64_t tokens, int32_t n, int64_t ld, roast_dtype_t dt, float* d_db,
+                            roast_stream_t stream);
 
 /* a2 + a3: dX = lambda * dY W~^T (skipped if d_dX == NULL), and
  * dM[h(x,y) + pi(o1,o2)] += lambda * g(x,y) * (X^T dY)[i, j] for every virtual

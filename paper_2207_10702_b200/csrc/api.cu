@@ -485,6 +485,28 @@ roast_status_t roast_bias_bwd(roast_t h, int32_t bias_id, const void* dY, int64_
   return roast_bias_bwd_ld(h, bias_id, dY, T, -1, dt, stream);
 }
 
+roast_status_t roast_colsum(const void* dY, int64_t T, int32_t n, int64_t ld, roast_dtype_t dt, float* db,
+                            roast_stream_t stream) {
+  if (T < 0 || n <= 0) return fail(ROAST_ERR_SHAPE, "tokens < 0 or n <= 0");
+  if (dt != ROAST_FP32 && dt != ROAST_BF16) return fail(ROAST_ERR_CONFIG, "bad dtype");
+  if (ld < 0) ld = n;
+  if (ld < n || (ld % 2) || (n % 2)) return fail(ROAST_ERR_SHAPE, "ld must be >= n; n and ld even");
+  if (!db || (reinterpret_cast<uintptr_t>(db) & 7)) return fail(ROAST_ERR_CONFIG, "db must be 8-byte aligned");
+  const cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (T == 0) {
+    ROAST_CUDA_CHECK(cudaMemsetAsync(db, 0, size_t(n) * sizeof(float), s));
+    return ROAST_OK;
+  }
+  if (!dY || (reinterpret_cast<uintptr_t>(dY) & 7)) return fail(ROAST_ERR_CONFIG, "dY must be 8-byte aligned");
+  const int slabs = colsum_slabs(T, n);
+  float* tmp = nullptr;   // stream-ordered scratch for the slab partials (capturable)
+  ROAST_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), size_t(slabs) * n * sizeof(float), s));
+  cudaError_t e = launch_colsum(dY, T, n, ld, dt, tmp, db, s);
+  cudaFreeAsync(tmp, s);
+  if (e != cudaSuccess) return cuda_fail(e, "column sum");
+  return ROAST_OK;
+}
+
 roast_status_t roast_bias_bwd_ld(roast_t h, int32_t bias_id, const void* dY, int64_t T, int64_t ld, roast_dtype_t dt,
                                  roast_stream_t stream) {
   Ctx* c = ctx(h);

@@ -34,7 +34,7 @@ class _LinearFn(torch.autograd.Function):
     def forward(ctx, x, anchor, store, mid, bias_mid):
         H = store.dims[mid][1]
         x2 = x.reshape(-1, H).contiguous()
-        b = store.bias_fwd(bias_mid) if bias_mid is not None else None
+        b = store.bias_vector(bias_mid) if bias_mid is not None else None
         y = store.fwd(mid, x2, bias=b)
         ctx.save_for_backward(x2)
         ctx.store, ctx.mid, ctx.bias_mid, ctx.shape = store, mid, bias_mid, x.shape
@@ -51,7 +51,7 @@ class _LinearFn(torch.autograd.Function):
             store.bwd_dx(mid, dy2, dx)
         store.bwd_dm(mid, x2, dy2)          # dM += lambda g X^T dY scattered into M's slots
         if ctx.bias_mid is not None:
-            store.bias_bwd(ctx.bias_mid, dy2)
+            store.bias_grad(ctx.bias_mid, dy2)
         return (dx.reshape(ctx.shape) if dx is not None else None), None, None, None, None
 
 
@@ -64,7 +64,7 @@ class _LinearGroupFn(torch.autograd.Function):
     def forward(ctx, x, anchor, store, gid, bias_mids):
         H = store.dims[gid][1]
         x2 = x.reshape(-1, H).contiguous()
-        b = torch.cat([store.bias_fwd(m) for m in bias_mids]) if bias_mids else None
+        b = torch.cat([store.bias_vector(m) for m in bias_mids]) if bias_mids else None
         y = store.fwd(gid, x2, bias=b)
         ctx.save_for_backward(x2)
         ctx.store, ctx.gid, ctx.bias_mids, ctx.shape = store, gid, bias_mids, x.shape
@@ -84,7 +84,7 @@ class _LinearGroupFn(torch.autograd.Function):
             c0 = 0
             for m in ctx.bias_mids:
                 n = store.dims[m][2]
-                store.bias_bwd(m, dy2[:, c0:c0 + n])
+                store.bias_grad(m, dy2[:, c0:c0 + n])
                 c0 += n
         return (dx.reshape(ctx.shape) if dx is not None else None), None, None, None, None
 
@@ -97,7 +97,7 @@ class RoastBias(torch.nn.Module):
     def __init__(self, store: "R.Roast", n: int, fan_in: float, chunk: int = 64):
         super().__init__()
         self.store = store
-        self.mid = store.embedding(1, n, chunk, fan_in)
+        self.mid = store.bias(n, fan_in, chunk)
 
     def vector(self):
         """The recovered bias (fp32), e.g. for a dense reference."""

@@ -26,7 +26,7 @@ EXPORTS = [
     "roast_register_embedding_seg", "roast_linear_fwd", "roast_linear_bwd",
     "roast_linear_bwd_dx", "roast_linear_bwd_dm", "roast_embedding_fwd", "roast_embedding_bwd",
     "roast_embedding_fwd_multi", "roast_embedding_bwd_multi", "roast_set_autotune", "roast_get_tuned", "roast_set_tuned",
-    "roast_linear_fwd_bias", "roast_bias_fwd", "roast_bias_bwd", "roast_bias_bwd_ld", "roast_register_linear_concat", "roast_linear_fwd_chain",
+    "roast_linear_fwd_bias", "roast_bias_fwd", "roast_bias_bwd", "roast_bias_bwd_ld", "roast_colsum", "roast_register_linear_concat", "roast_linear_fwd_chain",
     "roast_linear_bwd_dx_chain", "roast_comm_unique_id", "roast_comm_init",
     "roast_grad_allreduce", "roast_set_exchange", "roast_touched_size", "roast_touched_intervals",
     "roast_debug_exchange", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step", "roast_grad_exchange_step",
@@ -84,6 +84,7 @@ def _load():
         "roast_linear_bwd_dx_chain": (st, [H, I32, I32, P, P, P, I64, ctypes.c_int, S]),
         "roast_bias_bwd": (st, [H, I32, P, I64, ctypes.c_int, S]),
         "roast_bias_bwd_ld": (st, [H, I32, P, I64, I64, ctypes.c_int, S]),
+        "roast_colsum": (st, [P, I64, I32, I64, ctypes.c_int, P, S]),
         "roast_register_linear_concat": (st, [H, P, I32, ctypes.POINTER(I32)]),
         "roast_get_tuned": (st, [H, I32, I32, I64, ctypes.POINTER(I32), ctypes.POINTER(I32)]),
         "roast_set_tuned": (st, [H, I32, I32, I64, I32, I32]),
@@ -242,6 +243,10 @@ def roast_bias_bwd(h, bias_id, dY_ptr, tokens, dtype, stream=0):
 
 def roast_bias_bwd_ld(h, bias_id, dY_ptr, tokens, ld, dtype, stream=0):
     _check(_lib.roast_bias_bwd_ld(h, bias_id, dY_ptr, tokens, ld, dtype, stream), "roast_bias_bwd_ld")
+
+
+def roast_colsum(dY_ptr, tokens, n, ld, dtype, db_ptr, stream=0):
+    _check(_lib.roast_colsum(dY_ptr, tokens, n, ld, dtype, db_ptr, stream), "roast_colsum")
 
 
 def roast_register_linear_concat(h, ids):
@@ -408,6 +413,17 @@ class Roast:
         self.h = roast_create(self.mem_size, seed, z1, z2, cfg)
         self.dims = {}
         roast_bind(self.h, M.data_ptr(), self.dM.data_ptr(), self._s())
+        # biases via L (registered with bias()): with batch_biases, every bias is recovered by one
+        # multi-table lookup per (dim, chunk) group per parameter generation, and their
+        # gradients are column sums collected into one buffer and scattered by one multi-table
+        # L backward at flush time (exchange / update / flush_bias_grads) — not ~4 small
+        # kernels per bias per step
+        self.batch_biases = False
+        self._biases = []
+        self._gen = 0
+        self._bias_gen = -1
+        self._bias_groups = None
+        self._bias_pending = False
 
     def _s(self, stream=None):
         s = stream if stream is not None else self.torch.cuda.current_stream()
@@ -451,6 +467,71 @@ class Roast:
                roast_register_embedding_seg(self.h, num_rows, dim, chunk, fan_in, *segment))
         self.dims[mid] = ("embedding", num_rows, dim, chunk)
         return mid
+
+    # ---- biases via L (reading R24) ---------------------------------------------------
+    def bias(self, n, fan_in, chunk=64):
+        """Register a bias of n elements recovered with L (a 1 x n ROAST embedding)."""
+        mid = self.embedding(1, n, chunk, fan_in)
+        self._biases.append(mid)
+        self._bias_groups = None
+        return mid
+
+    def _groups(self):
+        if self._bias_groups is None:
+            torch = self.torch
+            by = {}
+            for m in self._biases:
+                by.setdefault((self.dims[m][2], self.dims[m][3]), []).append(m)
+            self._bias_groups = []
+            for (dim, chunk), mids in by.items():
+                vals = torch.empty(len(mids), dim, dtype=torch.float32, device=self.M.device)
+                grads = torch.zeros(len(mids), dim, dtype=torch.float32, device=self.M.device)
+                idx = torch.zeros(len(mids), dtype=torch.int64, device=self.M.device)
+                slot = {m: i for i, m in enumerate(mids)}
+                self._bias_groups.append((mids, vals, grads, idx, slot))
+            self._bias_gen = -1
+        return self._bias_groups
+
+    def bias_vector(self, mid, stream=None):
+        """The recovered bias (fp32 [n]); batched: a view into its group's buffer, refreshed
+        once per parameter generation by one multi-table lookup per group."""
+        if not self.batch_biases:
+            return self.bias_fwd(mid, stream=stream)
+        groups = self._groups()
+        if self._bias_gen != self._gen:
+            for mids, vals, _, idx, _ in groups:
+                roast_embedding_fwd_multi(self.h, mids, idx.data_ptr(), 1, vals.data_ptr(), self._s(stream))
+            self._bias_gen = self._gen
+        for mids, vals, _, _, slot in groups:
+            if mid in slot:
+                return vals[slot[mid]]
+        raise KeyError(mid)
+
+    def bias_grad(self, mid, dY, stream=None):
+        """Bias backward; batched: only the column sums now (into the group buffer), the L
+        scatter of every bias at flush_bias_grads()."""
+        if not self.batch_biases:
+            return self.bias_bwd(mid, dY, stream=stream)
+        n = self.dims[mid][2]
+        if dY.dim() != 2:
+            dY = dY.reshape(-1, n)
+        ld = dY.stride(0) if dY.shape[0] > 1 else n
+        for _, _, grads, _, slot in self._groups():
+            if mid in slot:
+                roast_colsum(dY.data_ptr(), dY.shape[0], n, ld, self._dt(dY), grads[slot[mid]].data_ptr(),
+                             self._s(stream))
+                self._bias_pending = True
+                return
+        raise KeyError(mid)
+
+    def flush_bias_grads(self, stream=None):
+        """dM += every collected bias gradient (one multi-table L backward per group)."""
+        if not self._bias_pending:
+            return
+        for mids, _, grads, idx, _ in self._groups():
+            roast_embedding_bwd_multi(self.h, mids, idx.data_ptr(), 1, grads.data_ptr(), self._s(stream))
+            grads.zero_()
+        self._bias_pending = False
 
     @staticmethod
     def _dt(t):
@@ -562,17 +643,25 @@ class Roast:
 
     def sync_shadow(self, stream=None):
         roast_sync_shadow(self.h, self._s(stream))
+        self._gen += 1
 
     def sgd(self, lr, stream=None):
+        self.flush_bias_grads(stream)
         roast_sgd_step(self.h, lr, self._s(stream))
+        self._gen += 1
 
     def optimizer_step(self, kind, lr, step=1, stream=None, **kw):
+        self.flush_bias_grads(stream)
         roast_optimizer_step(self.h, kind, lr, step, stream=self._s(stream), **kw)
+        self._gen += 1
 
     def exchange_step(self, kind, lr, step=1, stream=None, **kw):
+        self.flush_bias_grads(stream)
         roast_grad_exchange_step(self.h, kind, lr, step, stream=self._s(stream), **kw)
+        self._gen += 1
 
     def allreduce(self, stream=None):
+        self.flush_bias_grads(stream)
         roast_grad_allreduce(self.h, self._s(stream))
 
     def set_exchange(self, mode):

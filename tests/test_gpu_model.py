@@ -37,6 +37,7 @@ def test_encoder_layer_gradients_match_dense_autograd():
     y = layer(x)
     loss = (y.float() * Rw).sum()
     loss.backward()
+    store.flush_bias_grads()
     torch.cuda.synchronize()
     dM = store.dM.cpu().numpy().astype(np.float64)
 
@@ -72,7 +73,8 @@ def store_lam(lin, M_np):
     return OM.LinearSpec(H, O, 64, 64, len(M_np), synth.HASH_SEED, lin.mid).lam
 
 
-def test_roast_bert_embeddings_and_biases_match_dense_autograd():
+@pytest.mark.parametrize("batch_biases", [False, True])
+def test_roast_bert_embeddings_and_biases_match_dense_autograd(batch_biases):
     """NEXT #3: word / position / type embeddings and every linear's bias via L, plus the
     linears via ROAST-MM, all in ONE GMS store; dM of the whole model vs the
     dense fp32 model built from the recovered weights, its gradients scattered by the oracle
@@ -87,6 +89,7 @@ def test_roast_bert_embeddings_and_biases_match_dense_autograd():
     M_np = synth.uniform(synth.SEED_M, (mem,)).astype(np.float32)
     M = torch.tensor(M_np, device="cuda")
     store = R.Roast(M, 64, 64, seed=synth.HASH_SEED)
+    store.batch_biases = batch_biases   # True: one multi-table lookup / scatter for all biases
     model = RN.RoastBert(store, vocab, d, ff, heads, 1, max_pos, 2, Z, bias=True).cuda()
     ids = torch.randint(0, vocab, (B, S), device="cuda")
     types = torch.randint(0, 2, (B, S), device="cuda")
@@ -95,6 +98,7 @@ def test_roast_bert_embeddings_and_biases_match_dense_autograd():
     y = model(ids, types)
     loss = (y.float() * Rw).sum()
     loss.backward()
+    store.flush_bias_grads()
     torch.cuda.synchronize()
     dM = store.dM.cpu().numpy().astype(np.float64)
 

@@ -108,6 +108,7 @@ def main():
         M = (torch.rand(mem, device=dev) * 2 - 1).contiguous()
         store = R.Roast(M, 64, 64, seed=synth.HASH_SEED)
         store.set_autotune(args.autotune)   # tuned during the eager warm-up, before capture
+        store.batch_biases = True           # 72 biases via L: one lookup / one scatter per step
         dp.init_comm(store, rank, world, device=dev)
         if args.full:
             model = RN.RoastBert(store).to(dev)
