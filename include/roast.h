@@ -261,6 +261,8 @@ roast_status_t roast_embedding_bwd_multi(roast_t h, const int32_t* ids, int32_t 
  * and the exchange is a no-op; world == 1 with an id builds a 1-rank NCCL communicator.
  * libnccl.so.2 is loaded at run time (ROAST_ERR_NCCL if absent). */
 roast_status_t roast_comm_unique_id(uint8_t id_out[128]);
+/* In deterministic mode roast_comm_init sets NCCL_ALGO=Ring (unless already set) before
+ * creating the communicator, so the cross-rank sum is taken in a fixed order run to run. */
 roast_status_t roast_comm_init(roast_t h, int32_t rank, int32_t world, const uint8_t id[128]);
 roast_status_t roast_grad_allreduce(roast_t h, roast_stream_t stream);
 

@@ -7,6 +7,7 @@
 // library has no link-time NCCL dependency.
 #include <dlfcn.h>
 #include <nccl.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "roast_internal.h"
@@ -77,6 +78,9 @@ roast_status_t roast_comm_init(roast_t h, int32_t rank, int32_t world, const uin
   c->world = world;
   if (world == 1 && !id) return ROAST_OK;   // single rank, no communicator (exchange is a no-op)
   if (!id) return fail(ROAST_ERR_CONFIG, "null id");
+  // deterministic mode: a fixed all-reduce algorithm keeps the cross-rank summation order the
+  // same run to run (NCCL_ALGO=Ring); a value the user set is kept
+  if (c->cfg.deterministic) setenv("NCCL_ALGO", "Ring", 0);
   if (!api().loaded) return fail(ROAST_ERR_NCCL, "libnccl.so.2 not found");
   ncclUniqueId uid;
   memcpy(&uid, id, 128);
