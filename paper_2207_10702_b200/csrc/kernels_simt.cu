@@ -56,20 +56,21 @@ __device__ __forceinline__ float wtile(const MT* Mop, const MapArgs& a, int h, i
 // BK = 64: the hashed B gathers (tile map -> M, two dependent loads) of a whole 64-deep
 // K slice are in flight at once; with BK = 16 the small fp32 configs (C1: 4 blocks) were
 // bound by 16 serial load-latency rounds.
-constexpr int BM = 64, BN = 64, BK = 64;
+constexpr int BK = 64;
 
 // C[T x N] = lam * A[T x K] * B[K x N]; B[k][n] = W~[k][n] (fwd) or W~[n][k] (dX).
-template <typename XT, typename MT, bool kTransW>
+template <typename XT, typename MT, bool kTransW, int TS>
 __global__ void __launch_bounds__(256) simt_mm_kernel(const XT* __restrict__ A, XT* __restrict__ C,
                                                       const MT* __restrict__ Mop, MapArgs map, int64_t T,
                                                       int K, int N, float lam, const float* __restrict__ bias) {
+  constexpr int BM = TS, BN = TS, RM = TS / 16;
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int tid = threadIdx.x;
   const int tr = tid / 16, tc = tid % 16;
   const int64_t m0 = int64_t(blockIdx.y) * BM;
   const int n0 = blockIdx.x * BN;
-  float acc[4][4] = {};
+  float acc[RM][RM] = {};
   for (int k0 = 0; k0 < K; k0 += BK) {
     for (int e = tid; e < BM * BK; e += 256) {
       int r = e / BK, kk = e % BK;
@@ -87,25 +88,25 @@ __global__ void __launch_bounds__(256) simt_mm_kernel(const XT* __restrict__ A, 
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
-      float a[4], b[4];
+      float a[RM], b[RM];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][tr * 4 + i];
+      for (int i = 0; i < RM; ++i) a[i] = As[kk][tr * RM + i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tc * 4 + j];
+      for (int j = 0; j < RM; ++j) b[j] = Bs[kk][tc * RM + j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < RM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < RM; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int64_t m = m0 + tr * 4 + i;
+  for (int i = 0; i < RM; ++i) {
+    int64_t m = m0 + tr * RM + i;
     if (m >= T) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int n = n0 + tc * 4 + j;
+    for (int j = 0; j < RM; ++j) {
+      int n = n0 + tc * RM + j;
       if (n < N) store_val(C, m * N + n, bias ? fmaf(lam, acc[i][j], bias[n]) : lam * acc[i][j]);
     }
   }
@@ -113,17 +114,18 @@ __global__ void __launch_bounds__(256) simt_mm_kernel(const XT* __restrict__ A, 
 
 // G[H x O] = X^T dY (K = tokens); epilogue scatters lam * g * G into its hash tile:
 // ws[(x*ny + y) * Z1Z2 + pi] (deterministic, reduced by K5) or atomically into dM.
-template <typename XT>
+template <typename XT, int TS>
 __global__ void __launch_bounds__(256) simt_dw_kernel(const XT* __restrict__ X, const XT* __restrict__ dY,
                                                       MapArgs map, int64_t T, int H, int O, float lam,
                                                       float* __restrict__ ws, float* __restrict__ dM) {
+  constexpr int BM = TS, BN = TS, RM = TS / 16;
   __shared__ float Xs[BK][BM + 4];
   __shared__ float Ds[BK][BN + 4];
   const int tid = threadIdx.x;
   const int tr = tid / 16, tc = tid % 16;
   const int h0 = blockIdx.y * BM;
   const int o0 = blockIdx.x * BN;
-  float acc[4][4] = {};
+  float acc[RM][RM] = {};
   for (int64_t t0 = 0; t0 < T; t0 += BK) {
     for (int e = tid; e < BK * BM; e += 256) {
       int kk = e / BM, r = e % BM;
@@ -134,26 +136,26 @@ __global__ void __launch_bounds__(256) simt_dw_kernel(const XT* __restrict__ X, 
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
-      float a[4], b[4];
+      float a[RM], b[RM];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = Xs[kk][tr * 4 + i];
+      for (int i = 0; i < RM; ++i) a[i] = Xs[kk][tr * RM + i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Ds[kk][tc * 4 + j];
+      for (int j = 0; j < RM; ++j) b[j] = Ds[kk][tc * RM + j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < RM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < RM; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
     }
     __syncthreads();
   }
   const int tile_elems = map.z1 * map.z2;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int h = h0 + tr * 4 + i;
+  for (int i = 0; i < RM; ++i) {
+    int h = h0 + tr * RM + i;
     if (h >= H) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int o = o0 + tc * 4 + j;
+    for (int j = 0; j < RM; ++j) {
+      int o = o0 + tc * RM + j;
       if (o >= O) continue;
       int x = h / map.z1, y = o / map.z2;
       int t = x * map.ny + y;
@@ -266,6 +268,41 @@ int grid_1d(int64_t n, int threads) {
   return int(b < 1 ? 1 : b);
 }
 
+// Block tile: 64 x 64 (4 x 4 outputs per thread) unless that leaves most of the 148 SMs idle;
+// small problems (C1: 64 tokens x 256) drop to 32 x 32 or 16 x 16 so more CTAs issue the
+// dependent hashed gathers in parallel (the 64-tile grid there is 4 CTAs).
+int simt_tile(int64_t rows, int64_t cols) {
+  for (int ts : {64, 32}) {
+    int64_t blocks = ((rows + ts - 1) / ts) * ((cols + ts - 1) / ts);
+    if (blocks >= 148) return ts;
+  }
+  return 16;
+}
+
+template <typename XT, typename MT, bool kTransW>
+void simt_fwd_ts(int ts, const XT* X, XT* Y, const MT* Mop, const MapArgs& a, int64_t T, int K, int N, float lam,
+                 const float* bias, cudaStream_t s) {
+  auto grid = [&](int t) { return dim3(unsigned((N + t - 1) / t), unsigned((T + t - 1) / t)); };
+  if (ts == 64)
+    simt_mm_kernel<XT, MT, kTransW, 64><<<grid(64), 256, 0, s>>>(X, Y, Mop, a, T, K, N, lam, bias);
+  else if (ts == 32)
+    simt_mm_kernel<XT, MT, kTransW, 32><<<grid(32), 256, 0, s>>>(X, Y, Mop, a, T, K, N, lam, bias);
+  else
+    simt_mm_kernel<XT, MT, kTransW, 16><<<grid(16), 256, 0, s>>>(X, Y, Mop, a, T, K, N, lam, bias);
+}
+
+template <typename XT>
+void simt_dw_ts(int ts, const XT* X, const XT* dY, const MapArgs& a, int64_t T, int H, int O, float lam, float* ws,
+                float* dM, cudaStream_t s) {
+  auto grid = [&](int t) { return dim3(unsigned((O + t - 1) / t), unsigned((H + t - 1) / t)); };
+  if (ts == 64)
+    simt_dw_kernel<XT, 64><<<grid(64), 256, 0, s>>>(X, dY, a, T, H, O, lam, ws, dM);
+  else if (ts == 32)
+    simt_dw_kernel<XT, 32><<<grid(32), 256, 0, s>>>(X, dY, a, T, H, O, lam, ws, dM);
+  else
+    simt_dw_kernel<XT, 16><<<grid(16), 256, 0, s>>>(X, dY, a, T, H, O, lam, ws, dM);
+}
+
 }  // namespace
 
 cudaError_t launch_simt_fwd(const Ctx* c, const Module& m, const void* X, void* Y, int64_t T, roast_dtype_t dt,
@@ -273,35 +310,34 @@ cudaError_t launch_simt_fwd(const Ctx* c, const Module& m, const void* X, void* 
   if (T == 0) return cudaSuccess;
   const int K = int(transpose_w ? m.O : m.H);
   const int N = int(transpose_w ? m.H : m.O);
-  dim3 grid((N + BN - 1) / BN, unsigned((T + BM - 1) / BM));
+  const int ts = simt_tile(T, N);
   MapArgs a = map_args(c, m);
   if (dt == ROAST_FP32) {
     if (transpose_w)
-      simt_mm_kernel<float, float, true><<<grid, 256, 0, s>>>((const float*)X, (float*)Y, c->M, a, T, K, N, m.lam, bias);
+      simt_fwd_ts<float, float, true>(ts, (const float*)X, (float*)Y, c->M, a, T, K, N, m.lam, bias, s);
     else
-      simt_mm_kernel<float, float, false><<<grid, 256, 0, s>>>((const float*)X, (float*)Y, c->M, a, T, K, N, m.lam, bias);
+      simt_fwd_ts<float, float, false>(ts, (const float*)X, (float*)Y, c->M, a, T, K, N, m.lam, bias, s);
   } else {
     auto* sh = reinterpret_cast<const __nv_bfloat16*>(c->shadow);
     if (transpose_w)
-      simt_mm_kernel<__nv_bfloat16, __nv_bfloat16, true>
-          <<<grid, 256, 0, s>>>((const __nv_bfloat16*)X, (__nv_bfloat16*)Y, sh, a, T, K, N, m.lam, bias);
+      simt_fwd_ts<__nv_bfloat16, __nv_bfloat16, true>(ts, (const __nv_bfloat16*)X, (__nv_bfloat16*)Y, sh, a, T, K, N,
+                                                      m.lam, bias, s);
     else
-      simt_mm_kernel<__nv_bfloat16, __nv_bfloat16, false>
-          <<<grid, 256, 0, s>>>((const __nv_bfloat16*)X, (__nv_bfloat16*)Y, sh, a, T, K, N, m.lam, bias);
+      simt_fwd_ts<__nv_bfloat16, __nv_bfloat16, false>(ts, (const __nv_bfloat16*)X, (__nv_bfloat16*)Y, sh, a, T, K,
+                                                       N, m.lam, bias, s);
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_simt_dw(const Ctx* c, const Module& m, const void* X, const void* dY, int64_t T,
                            roast_dtype_t dt, float* ws, cudaStream_t s) {
-  dim3 grid(unsigned((m.O + BN - 1) / BN), unsigned((m.H + BM - 1) / BM));
+  const int ts = simt_tile(m.H, m.O);
   MapArgs a = map_args(c, m);
   if (dt == ROAST_FP32)
-    simt_dw_kernel<float><<<grid, 256, 0, s>>>((const float*)X, (const float*)dY, a, T, int(m.H), int(m.O), m.lam,
-                                               ws, c->dM);
+    simt_dw_ts<float>(ts, (const float*)X, (const float*)dY, a, T, int(m.H), int(m.O), m.lam, ws, c->dM, s);
   else
-    simt_dw_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)X, (const __nv_bfloat16*)dY, a, T,
-                                                       int(m.H), int(m.O), m.lam, ws, c->dM);
+    simt_dw_ts<__nv_bfloat16>(ts, (const __nv_bfloat16*)X, (const __nv_bfloat16*)dY, a, T, int(m.H), int(m.O),
+                              m.lam, ws, c->dM, s);
   return cudaGetLastError();
 }
 

@@ -182,6 +182,24 @@ def test_ragged_and_empty_tokens_bf16(R, torch, T):
     assert rel_frob(dM, spec.backward_dm(X_np, dY_np)) <= 1e-2
 
 
+@pytest.mark.parametrize("deterministic", [False, True])
+@pytest.mark.parametrize("H,O,T", [(256, 256, 64), (608, 704, 300), (992, 704, 2000), (96, 64, 7)])
+def test_fp32_simt_block_tiles(R, torch, deterministic, H, O, T):
+    """fp32 SIMT path at shapes that select each block tile (64, 32 and 16: kernels_simt.cu
+    simt_tile) in fwd, dX and dW, with ragged block-tile edges; z = 32."""
+    mem = 50_000
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 32, 32, deterministic=deterministic)
+    mid = ctx.linear(H, O)
+    spec = OM.LinearSpec(H, O, 32, 32, mem, HS, mid)
+    X = synth.uniform(synth.SEED_X, (T, H)).astype(np.float32)
+    dY = synth.uniform(synth.SEED_DY, (T, O)).astype(np.float32)
+    Y, dX, dM = run_linear(R, torch, ctx, mid, X, dY, torch.float32)
+    assert rel_frob(Y, spec.forward(X, M_np)) <= 1e-5
+    assert rel_frob(dX, spec.backward_dx(dY, M_np)) <= 1e-5
+    assert rel_frob(dM, spec.backward_dm(X, dY)) <= 1e-5
+
+
 def test_identity_mapping_is_dense_layer(R, torch):
     """North star: |M| >= n, identity mapping -> ROAST-MM == dense X @ reshape(M)."""
     H, O, T = 256, 128, 200
