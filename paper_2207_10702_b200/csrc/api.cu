@@ -2,6 +2,7 @@
 // registration (static tile maps, a0), dispatch to the kernels, sticky errors.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -30,6 +31,9 @@ roast_status_t ensure_ws(Ctx* c, size_t bytes, cudaStream_t s) {
   c->ws_bytes = 0;
   ROAST_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&c->ws), bytes, s));
   c->ws_bytes = bytes;
+  // test hook: fill a new workspace with NaN (0xFFFFFFFF) so any slot a reader consumes
+  // before a kernel wrote it poisons the result (tests/test_gpu_parity.py, poisoned-workspace test)
+  if (getenv("ROAST_POISON_WS")) ROAST_CUDA_CHECK(cudaMemsetAsync(c->ws, 0xFF, bytes, s));
   return ROAST_OK;
 }
 

@@ -365,6 +365,40 @@ def test_embedding_deterministic_parity_and_reproducible(R, torch, dist, align):
     ctx.check()
 
 
+def test_deterministic_workspace_fully_written_before_read(R, torch, monkeypatch):
+    """Deterministic dM reads per-tile (and per-split) partials from a library workspace; with
+    ROAST_POISON_WS every new workspace starts as NaN, so a slot the reducer consumed before a
+    kernel wrote it would poison dM.  Covers the tcgen05 DW (TMA-store partials, split-K),
+    the SIMT DW and the sorted embedding backward; each result still matches the oracle."""
+    monkeypatch.setenv("ROAST_POISON_WS", "1")
+    for dtype, z, (H, O), T, mem in [(torch.bfloat16, 64, (768, 3072), 512, 47192),
+                                     (torch.bfloat16, 64, (3072, 768), 4100, 47192),
+                                     (torch.float32, 32, (256, 256), 64, 8192)]:
+        M_np = store(mem)
+        ctx, _ = make_ctx(R, torch, M_np, z, z, deterministic=True)
+        mid = ctx.linear(H, O)
+        spec = OM.LinearSpec(H, O, z, z, mem, HS, mid)
+        X_np = bf16_input(synth.SEED_X, (T, H))
+        dY_np = bf16_input(synth.SEED_DY, (T, O))
+        ctx.bwd(mid, to_dev(X_np, dtype), to_dev(dY_np, dtype), need_dx=False)
+        dM = ctx.dM.cpu().numpy()
+        assert np.isfinite(dM).all()
+        assert rel_frob(dM, spec.backward_dm(X_np, dY_np)) <= (1e-2 if dtype == torch.bfloat16 else 1e-5)
+        ctx.close()
+    mem, rows, d, Z = 200_000, 10 ** 6, 128, 32
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64, deterministic=True)
+    mid = ctx.embedding(rows, d, Z)
+    idx_np = np.concatenate([synth.zipf_indices(synth.SEED_IDX, 5000, rows), [7, 7, rows - 1]])
+    dout_np = synth.normal(synth.SEED_DY, (len(idx_np), d)).astype(np.float32)
+    ctx.emb_bwd(mid, to_dev(idx_np, torch.int64), to_dev(dout_np, torch.float32))
+    dM = ctx.dM.cpu().numpy()
+    ref = np.zeros(mem)
+    OE.EmbeddingSpec(rows, d, Z, mem, HS, mid).backward(idx_np, dout_np, ref)
+    assert np.isfinite(dM).all() and rel_frob(dM, ref) <= 1e-5
+    ctx.check()
+
+
 @pytest.mark.parametrize("kind,name", [(0, "sgd"), (1, "adagrad"), (2, "adam")])
 @pytest.mark.parametrize("mem", [100_000, 100_003])   # 16-byte vector path / scalar path
 def test_optimizer_step_parity(R, torch, kind, name, mem):
