@@ -330,6 +330,47 @@ roast_status_t roast_optimizer_step(roast_t h, const roast_opt_config_t* cfg, in
 roast_status_t roast_grad_exchange_step(roast_t h, const roast_opt_config_t* cfg, int64_t step,
                                         roast_stream_t stream);
 
+/* ---- one-shot P2P exchange fused with the update ---
+ * The a6 exchange and the a7 update in one pass without NCCL:
+ * every rank maps every other rank's exchange window (CUDA IPC over NVLink / NVSwitch), and
+ * the update kernel reads the W packed gradients of the touched slots straight from the
+ * peers' memory, sums them in rank order 0..W-1 (so all ranks get bit-identical sums and M
+ * stays replicated), and applies the optimizer, the bf16 shadow refresh and the dM zeroing.
+ * Only the touched slots (roast_touched_size) are exchanged and updated, as in
+ * roast_grad_exchange_step with touched_only.  All calls below after every module is
+ * registered; re-registering invalidates the window (ROAST_ERR_STATE until re-opened).
+ *
+ * roast_p2p_window: allocate (once) this handle's window, a device buffer the library owns:
+ *   [0, 256) int32 flags[world] | [256, 512) int32 epoch, uint32 arrival counter |
+ *   [512, ...) two fp32 buffers of
+ *   the touched-slot count (rounded up to 4) each; flags and epoch start at 0.  *window /
+ *   *bytes (either may be NULL) receive its device address and size.
+ * roast_p2p_ipc_handle: the window's cudaIpcMemHandle (64 bytes, host buffer) for the other
+ *   ranks of the node (exchange them out of band, e.g. torch.distributed all_gather).
+ * roast_p2p_open: map every rank's window from handles[world * 64] (rank r's handle at
+ *   r * 64; this rank's own entry is ignored).  1 <= world <= 8, else ROAST_ERR_CONFIG;
+ *   ROAST_ERR_CUDA if a handle cannot be opened.
+ * roast_p2p_attach: the same with device pointers windows[world] already mapped in this
+ *   process (ranks sharing a process; windows[rank] must be this handle's window).
+ * roast_p2p_post (stream-ordered, capturable): pack this rank's dM touched slots into
+ *   buffer (epoch + 1) & 1, then (its last CTA) publish epoch + 1 in every rank's
+ *   flags[rank] (release, system scope) and advance the epoch.  1 launch.
+ * roast_p2p_finish (stream-ordered, capturable): wait until every rank has posted this epoch
+ *   (acquire, system scope), then the fused sum + update (cfg as roast_optimizer_step; dM on
+ *   the touched slots afterwards: zero if zero_grad, else the summed gradient).  1 launch.
+ *   A rank that never posts: after 20 s the kernel sets the sticky error (roast_get_error ->
+ *   ROAST_ERR_STATE) and traps, so the context reports an error instead of hanging.
+ * roast_grad_exchange_p2p: post + finish.  Every rank must call it once per step, in the same
+ *   order as the other ranks; ranks sharing one stream must post all before finishing any. */
+roast_status_t roast_p2p_window(roast_t h, void** window, int64_t* bytes);
+roast_status_t roast_p2p_ipc_handle(roast_t h, uint8_t handle[64]);
+roast_status_t roast_p2p_open(roast_t h, int32_t rank, int32_t world, const uint8_t* handles);
+roast_status_t roast_p2p_attach(roast_t h, int32_t rank, int32_t world, void* const* windows);
+roast_status_t roast_p2p_post(roast_t h, roast_stream_t stream);
+roast_status_t roast_p2p_finish(roast_t h, const roast_opt_config_t* cfg, int64_t step, roast_stream_t stream);
+roast_status_t roast_grad_exchange_p2p(roast_t h, const roast_opt_config_t* cfg, int64_t step,
+                                       roast_stream_t stream);
+
 /* Sticky device-side error (synchronises the handle's bound stream is NOT done:
  * call after a stream synchronize to observe faults of completed work). */
 roast_status_t roast_get_error(roast_t h);

@@ -223,6 +223,7 @@ roast_status_t roast_destroy(roast_t h) {
   cudaFree(c->d_iv);
   cudaFree(c->d_pack);
   comm_destroy(c);
+  p2p_destroy(c);
   delete c;
   return ROAST_OK;
 }
@@ -763,6 +764,7 @@ roast_status_t roast_get_error(roast_t h) {
   int32_t v = 0;
   cudaError_t e = cudaMemcpy(&v, c->d_err, sizeof(v), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "read error flag");
+  if (v & 2) return fail(ROAST_ERR_STATE, "p2p exchange: a peer did not post within 20 s (sticky)");
   if (v) return fail(ROAST_ERR_BOUNDS, "embedding index out of range (sticky)");
   return ROAST_OK;
 }

@@ -21,34 +21,23 @@
 namespace roast {
 namespace {
 
-// largest i with prefix[i] <= p (prefix[0] = 0, strictly increasing)
-__device__ __forceinline__ int find_interval(const int64_t* prefix, int n, int64_t p) {
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(prefix + mid) <= p)
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  return lo;
-}
-
 // dir 0: buf[p] = dM[start_i + p - prefix_i];  dir 1: dM[...] = scale * buf[p]
 template <int V>
 __global__ void pack_kernel(float* __restrict__ dM, float* __restrict__ buf, const int64_t* __restrict__ start,
                             const int64_t* __restrict__ prefix, int n_iv, int64_t total, int dir, float scale) {
   using VT = typename std::conditional<V == 4, float4, float>::type;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x * V;
-  for (int64_t p = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * V; p < total; p += stride) {
-    const int i = find_interval(prefix, n_iv, p);
-    const int64_t src = __ldg(start + i) + (p - __ldg(prefix + i));
+  int64_t b, e;
+  cta_range(total, V, &b, &e);
+  IvWalk w{start, prefix, n_iv};
+  if (b + int64_t(threadIdx.x) * V < e) w.seek(b + int64_t(threadIdx.x) * V);
+  for (int64_t p = b + int64_t(threadIdx.x) * V; p < e; p += int64_t(blockDim.x) * V) {
+    const int64_t src = w.slot(p);
     VT* d = reinterpret_cast<VT*>(dM + src);
-    VT* b = reinterpret_cast<VT*>(buf + p);
+    VT* bp = reinterpret_cast<VT*>(buf + p);
     if (dir == 0) {
-      *b = *d;
+      *bp = *d;
     } else {
-      VT v = *b;
+      VT v = *bp;
       if constexpr (V == 4) {
         v.x *= scale; v.y *= scale; v.z *= scale; v.w *= scale;
       } else {

@@ -416,16 +416,38 @@ struct OptArgs {
   const int64_t* iv_start;
   const int64_t* iv_prefix;
   int n_iv;
+  P2PView p2p;          // world > 0: the gradient of index p is sum_r buf_r[p], read from the peers
 };
 
-__device__ __forceinline__ int64_t opt_slot(const OptArgs& a, int64_t p) {
-  if (a.n_iv == 0) return p;
-  int lo = 0, hi = a.n_iv - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(a.iv_prefix + mid) <= p) lo = mid; else hi = mid - 1;
+// One-shot P2P exchange (p2p.cu): wait until every rank has published this step's packed
+// gradient (flags[r] >= epoch, acquire at system scope), then return the buffer parity.  A
+// rank that never arrives would hang the GPU, so the wait gives up after 20 s: it sets bit 2 of
+// the sticky error word (roast_get_error -> ROAST_ERR_STATE) and traps.
+__device__ int p2p_wait(const P2PView& v) {
+  __shared__ int s_epoch;
+  if (threadIdx.x == 0) {
+    const int e = *reinterpret_cast<const volatile int*>(v.epoch);
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int r = 0; r < v.world; ++r) {
+      int f;
+      for (;;) {
+        asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(f) : "l"(v.flags + r) : "memory");
+        if (f - e >= 0) break;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 20000000000ull) {
+          atomicOr(v.err, 2);
+          __threadfence_system();
+          __trap();
+        }
+        __nanosleep(64);
+      }
+    }
+    s_epoch = e;
   }
-  return __ldg(a.iv_start + lo) + (p - __ldg(a.iv_prefix + lo));
+  __syncthreads();
+  return s_epoch;
 }
 
 // One pass over |M| (or over the touched slots): update M from dM (and the optimizer state),
@@ -434,13 +456,27 @@ __device__ __forceinline__ int64_t opt_slot(const OptArgs& a, int64_t p) {
 // 16-byte aligned), V = 1: scalar.
 template <int KIND, int V>
 __global__ void opt_kernel(OptArgs a) {
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x * V;
-  for (int64_t p = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * V; p < a.n; p += stride) {
-    const int64_t i = opt_slot(a, p);
+  int64_t pbuf = 0;   // P2P: offset of this step's buffer (parity of the epoch)
+  if (a.p2p.world > 0) pbuf = (p2p_wait(a.p2p) & 1) ? a.p2p.stride : 0;
+  int64_t b, e;
+  cta_range(a.n, V, &b, &e);
+  IvWalk walk{a.iv_start, a.iv_prefix, a.n_iv};
+  if (a.n_iv > 0 && b + int64_t(threadIdx.x) * V < e) walk.seek(b + int64_t(threadIdx.x) * V);
+  for (int64_t p = b + int64_t(threadIdx.x) * V; p < e; p += int64_t(blockDim.x) * V) {
+    const int64_t i = a.n_iv == 0 ? p : walk.slot(p);
     float w[V], g[V], x[V], y[V];
     if constexpr (V == 4) {
       const float4 wv = *reinterpret_cast<const float4*>(a.M + i);
-      const float4 gv = *reinterpret_cast<const float4*>(a.gpack ? a.gpack + p : a.dM + i);
+      float4 gv;
+      if (a.p2p.world > 0) {   // fixed rank order: every rank computes the same sum, so M stays replicated
+        gv = __ldcv(reinterpret_cast<const float4*>(a.p2p.buf0[0] + pbuf + p));
+        for (int r = 1; r < a.p2p.world; ++r) {
+          const float4 v = __ldcv(reinterpret_cast<const float4*>(a.p2p.buf0[r] + pbuf + p));
+          gv.x += v.x; gv.y += v.y; gv.z += v.z; gv.w += v.w;
+        }
+      } else {
+        gv = *reinterpret_cast<const float4*>(a.gpack ? a.gpack + p : a.dM + i);
+      }
       w[0] = wv.x; w[1] = wv.y; w[2] = wv.z; w[3] = wv.w;
       g[0] = gv.x; g[1] = gv.y; g[2] = gv.z; g[3] = gv.w;
       if (KIND >= 1) {
@@ -453,7 +489,12 @@ __global__ void opt_kernel(OptArgs a) {
       }
     } else {
       w[0] = a.M[i];
-      g[0] = a.gpack ? a.gpack[p] : a.dM[i];
+      if (a.p2p.world > 0) {
+        g[0] = __ldcv(a.p2p.buf0[0] + pbuf + p);
+        for (int r = 1; r < a.p2p.world; ++r) g[0] += __ldcv(a.p2p.buf0[r] + pbuf + p);
+      } else {
+        g[0] = a.gpack ? a.gpack[p] : a.dM[i];
+      }
       if (KIND >= 1) x[0] = a.s1[i];
       if (KIND == 2) y[0] = a.s2[i];
     }
@@ -471,7 +512,10 @@ __global__ void opt_kernel(OptArgs a) {
       neg.y = pos.y ^ 0x80008000u;
       *reinterpret_cast<uint2*>(a.sh + i) = pos;
       *reinterpret_cast<uint2*>(a.sh + a.neg_base + i) = neg;
-      if (a.zero) *reinterpret_cast<float4*>(a.dM + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (a.zero)
+        *reinterpret_cast<float4*>(a.dM + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+      else if (a.p2p.world > 0)   // keep the documented dM contents: the summed gradient
+        *reinterpret_cast<float4*>(a.dM + i) = make_float4(g[0], g[1], g[2], g[3]);
     } else {
       a.M[i] = w[0];
       if (KIND >= 1) a.s1[i] = x[0];
@@ -479,7 +523,10 @@ __global__ void opt_kernel(OptArgs a) {
       const __nv_bfloat16 b = __float2bfloat16_rn(w[0]);
       a.sh[i] = b;
       a.sh[a.neg_base + i] = __hneg(b);
-      if (a.zero) a.dM[i] = 0.f;
+      if (a.zero)
+        a.dM[i] = 0.f;
+      else if (a.p2p.world > 0)
+        a.dM[i] = g[0];
     }
   }
 }
@@ -498,9 +545,10 @@ void launch_opt_kind(const OptArgs& a, bool vec, cudaStream_t s) {
 }  // namespace
 
 cudaError_t launch_optimizer(Ctx* c, int kind, float lr, float b1, float b2, float eps, float wd, int64_t step,
-                             int zero, bool touched_only, cudaStream_t s, const float* gpack) {
+                             int zero, bool touched_only, cudaStream_t s, const float* gpack, const P2PView* p2p) {
   OptArgs a{};
   a.gpack = gpack;
+  if (p2p) a.p2p = *p2p;
   a.M = c->M;
   a.dM = c->dM;
   a.sh = reinterpret_cast<__nv_bfloat16*>(c->shadow);

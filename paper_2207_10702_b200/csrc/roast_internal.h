@@ -41,6 +41,55 @@ struct Module {
   int32_t dim = 0, chunk = 0, chunks_per_row = 0;
 };
 
+// one-shot P2P exchange: at most one NVSwitch domain (8 GPUs) of ranks
+constexpr int kP2PMaxWorld = 8;
+// window layout (bytes): [0, 256) int32 flags[world] (rank r writes flags[r] = epoch) |
+// [256, 512) int32 epoch of this rank | [512, ...) buffer 0, buffer 1 (p2p_n fp32 each)
+constexpr int64_t kP2PHeader = 512;
+
+struct P2PView {   // what the fused update kernel needs (kernels_simt.cu opt_kernel)
+  int world = 0;
+  const float* buf0[kP2PMaxWorld] = {};   // each rank's buffer 0; buffer 1 = + stride floats
+  int64_t stride = 0;
+  const int* flags = nullptr;             // this rank's flags[world]
+  const int* epoch = nullptr;             // this rank's epoch word
+  int* err = nullptr;                     // sticky device error word (timeout)
+};
+
+#ifdef __CUDACC__
+// Touched-slot traversal (exchange.cu pack, p2p.cu post, kernels_simt.cu opt_kernel): the
+// packed index space [0, n) is cut into one contiguous range per CTA (threads of a CTA still
+// touch consecutive vectors); a thread finds its interval once by binary search and afterwards
+// only steps forward, instead of a dependent binary search per element.
+struct IvWalk {
+  const int64_t* start;    // interval starts in M
+  const int64_t* prefix;   // exclusive prefix of interval lengths (prefix[0] = 0)
+  int n_iv;
+  int i = 0;
+  __device__ void seek(int64_t p) {   // the largest i with prefix[i] <= p
+    int lo = 0, hi = n_iv - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(prefix + mid) <= p) lo = mid; else hi = mid - 1;
+    }
+    i = lo;
+  }
+  __device__ int64_t slot(int64_t p) {   // p must not decrease between calls
+    while (i + 1 < n_iv && __ldg(prefix + i + 1) <= p) ++i;
+    return __ldg(start + i) + (p - __ldg(prefix + i));
+  }
+};
+
+// [*b, *e): this CTA's contiguous share of [0, n), a multiple of blockDim.x * V long
+__device__ inline void cta_range(int64_t n, int V, int64_t* b, int64_t* e) {
+  const int64_t q = int64_t(blockDim.x) * V;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t chunk = (per + q - 1) / q * q;
+  *b = int64_t(blockIdx.x) * chunk;
+  *e = *b + chunk < n ? *b + chunk : n;
+}
+#endif
+
 struct Ctx {
   int64_t mem_size = 0;
   uint64_t seed = 0;
@@ -95,6 +144,13 @@ struct Ctx {
   int32_t n_iv = 0;
   int64_t* d_iv = nullptr;
   float* d_pack = nullptr;
+  // one-shot P2P exchange (p2p.cu): this rank's window (flags | epoch | two packed buffers of
+  // p2p_n fp32) and every rank's window mapped into this process (IPC or attach)
+  char* p2p_win = nullptr;
+  int64_t p2p_bytes = 0, p2p_n = 0;
+  int32_t p2p_rank = 0, p2p_world = 0;
+  char* p2p_peer[kP2PMaxWorld] = {};
+  bool p2p_opened[kP2PMaxWorld] = {};
 };
 
 // error reporting (thread-local detail string)
@@ -107,6 +163,7 @@ roast_status_t cuda_fail(cudaError_t e, const char* what);
   } while (0)
 
 void comm_destroy(Ctx* c);
+void p2p_destroy(Ctx* c);   // p2p.cu: close peer mappings, free the window
 
 // touched-set exchange (exchange.cu): build the interval tables (host, synchronous uploads);
 // pack (dir 0: d_pack <- dM[touched]) or unpack (dir 1: dM[touched] <- scale * d_pack)
@@ -132,7 +189,8 @@ cudaError_t launch_simt_dw(const Ctx* c, const Module& m, const void* X, const v
 cudaError_t launch_det_reduce(Ctx* c, const Module& m, const float* ws, int nsplit, cudaStream_t s);
 cudaError_t launch_sync_shadow(Ctx* c, cudaStream_t s);
 cudaError_t launch_optimizer(Ctx* c, int kind, float lr, float b1, float b2, float eps, float wd, int64_t step,
-                             int zero, bool touched_only, cudaStream_t s, const float* gpack = nullptr);
+                             int zero, bool touched_only, cudaStream_t s, const float* gpack = nullptr,
+                             const P2PView* p2p = nullptr);
 cudaError_t launch_materialize(const Ctx* c, const Module& m, roast_dtype_t dt, void* W, cudaStream_t s);
 cudaError_t launch_embed_fwd(const Ctx* c, const Module& m, const int64_t* idx, int64_t n, float* out,
                              cudaStream_t s);

@@ -30,7 +30,8 @@ EXPORTS = [
     "roast_linear_bwd_dx_chain", "roast_comm_unique_id", "roast_comm_init",
     "roast_grad_allreduce", "roast_set_exchange", "roast_touched_size", "roast_touched_intervals",
     "roast_debug_exchange", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step", "roast_grad_exchange_step",
-    "roast_get_error",
+    "roast_p2p_window", "roast_p2p_ipc_handle", "roast_p2p_open", "roast_p2p_attach", "roast_p2p_post",
+    "roast_p2p_finish", "roast_grad_exchange_p2p", "roast_get_error",
     "roast_status_str", "roast_last_error", "roast_debug_tile_map", "roast_debug_chunk_map",
     "roast_debug_materialize", "roast_debug_hash_host", "roast_launch_count",
 ]
@@ -110,6 +111,13 @@ def _load():
         "roast_sgd_step": (st, [H, ctypes.c_float, S]),
         "roast_optimizer_step": (st, [H, ctypes.POINTER(roast_opt_config_t), I64, S]),
         "roast_grad_exchange_step": (st, [H, ctypes.POINTER(roast_opt_config_t), I64, S]),
+        "roast_p2p_window": (st, [H, ctypes.POINTER(P), ctypes.POINTER(I64)]),
+        "roast_p2p_ipc_handle": (st, [H, ctypes.c_char_p]),
+        "roast_p2p_open": (st, [H, I32, I32, ctypes.c_char_p]),
+        "roast_p2p_attach": (st, [H, I32, I32, ctypes.POINTER(P)]),
+        "roast_p2p_post": (st, [H, S]),
+        "roast_p2p_finish": (st, [H, ctypes.POINTER(roast_opt_config_t), I64, S]),
+        "roast_grad_exchange_p2p": (st, [H, ctypes.POINTER(roast_opt_config_t), I64, S]),
         "roast_get_error": (st, [H]),
         "roast_status_str": (ctypes.c_char_p, [st]),
         "roast_last_error": (ctypes.c_char_p, []),
@@ -361,6 +369,45 @@ def roast_grad_exchange_step(h, kind, lr, step=1, beta1=0.9, beta2=0.999, eps=1e
                              zero_grad=True, stream=0, touched_only=False):
     cfg = roast_opt_config_t(kind, lr, beta1, beta2, eps, weight_decay, int(zero_grad), int(touched_only))
     _check(_lib.roast_grad_exchange_step(h, ctypes.byref(cfg), step, stream), "roast_grad_exchange_step")
+
+
+def roast_p2p_window(h):
+    """(device address, bytes) of this handle's exchange window (allocated on first call)."""
+    ptr, n = ctypes.c_void_p(), ctypes.c_int64()
+    _check(_lib.roast_p2p_window(h, ctypes.byref(ptr), ctypes.byref(n)), "roast_p2p_window")
+    return int(ptr.value or 0), int(n.value)
+
+
+def roast_p2p_ipc_handle(h):
+    buf = ctypes.create_string_buffer(64)
+    _check(_lib.roast_p2p_ipc_handle(h, buf), "roast_p2p_ipc_handle")
+    return buf.raw
+
+
+def roast_p2p_open(h, rank, world, handles: bytes):
+    assert len(handles) == 64 * world
+    _check(_lib.roast_p2p_open(h, rank, world, handles), "roast_p2p_open")
+
+
+def roast_p2p_attach(h, rank, world, windows):
+    arr = (ctypes.c_void_p * world)(*[int(w) for w in windows])
+    _check(_lib.roast_p2p_attach(h, rank, world, arr), "roast_p2p_attach")
+
+
+def roast_p2p_post(h, stream=0):
+    _check(_lib.roast_p2p_post(h, stream), "roast_p2p_post")
+
+
+def roast_p2p_finish(h, kind, lr, step=1, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, zero_grad=True,
+                     stream=0):
+    cfg = roast_opt_config_t(kind, lr, beta1, beta2, eps, weight_decay, int(zero_grad), 1)
+    _check(_lib.roast_p2p_finish(h, ctypes.byref(cfg), step, stream), "roast_p2p_finish")
+
+
+def roast_grad_exchange_p2p(h, kind, lr, step=1, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0,
+                            zero_grad=True, stream=0):
+    cfg = roast_opt_config_t(kind, lr, beta1, beta2, eps, weight_decay, int(zero_grad), 1)
+    _check(_lib.roast_grad_exchange_p2p(h, ctypes.byref(cfg), step, stream), "roast_grad_exchange_p2p")
 
 
 def roast_get_error(h):
@@ -658,6 +705,40 @@ class Roast:
     def exchange_step(self, kind, lr, step=1, stream=None, **kw):
         self.flush_bias_grads(stream)
         roast_grad_exchange_step(self.h, kind, lr, step, stream=self._s(stream), **kw)
+        self._gen += 1
+
+    # ---- one-shot P2P exchange fused with the update (include/roast.h, p2p.cu)
+    def p2p_window(self):
+        return roast_p2p_window(self.h)
+
+    def p2p_init(self, group=None):
+        """Map every rank's exchange window (CUDA IPC; handles exchanged with
+        torch.distributed all_gather_object on `group`).  World 1: this rank alone."""
+        import torch.distributed as dist
+        if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+            w, _ = roast_p2p_window(self.h)
+            roast_p2p_attach(self.h, 0, 1, [w])
+            return
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        mine = roast_p2p_ipc_handle(self.h)
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        roast_p2p_open(self.h, rank, world, b"".join(allh))
+
+    def p2p_attach(self, rank, windows):
+        roast_p2p_attach(self.h, rank, len(windows), windows)
+
+    def p2p_post(self, stream=None):
+        self.flush_bias_grads(stream)
+        roast_p2p_post(self.h, self._s(stream))
+
+    def p2p_finish(self, kind, lr, step=1, stream=None, **kw):
+        roast_p2p_finish(self.h, kind, lr, step, stream=self._s(stream), **kw)
+        self._gen += 1
+
+    def exchange_p2p(self, kind, lr, step=1, stream=None, **kw):
+        self.flush_bias_grads(stream)
+        roast_grad_exchange_p2p(self.h, kind, lr, step, stream=self._s(stream), **kw)
         self._gen += 1
 
     def allreduce(self, stream=None):
