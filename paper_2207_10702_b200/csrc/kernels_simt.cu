@@ -180,47 +180,55 @@ __global__ void det_reduce_kernel(float* __restrict__ dM, const float* __restric
                                   int ntiles, int64_t tile_elems, int nsplit, int64_t mem_size,
                                   const int64_t* __restrict__ iv_start, const int64_t* __restrict__ iv_prefix,
                                   int n_iv, int64_t n_touched) {
-  int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  int64_t s = q * 4;
-  if (n_iv > 0) {
-    if (s >= n_touched) return;
-    int a = 0, b = n_iv - 1;   // interval: the largest i with prefix[i] <= s (runs are multiples of 4)
-    while (a < b) {
-      const int mid = (a + b + 1) >> 1;
-      if (__ldg(iv_prefix + mid) <= s) a = mid; else b = mid - 1;
-    }
-    s = __ldg(iv_start + a) + (s - __ldg(iv_prefix + a));
-  }
-  if (s >= mem_size) return;
-  // lo = first i with sorted_off[i] > s - T ; hi = first i with sorted_off[i] > s
-  int lo = 0, hi = ntiles;
-  {
-    int64_t key = s - tile_elems;
-    int a = 0, b = ntiles;
-    while (a < b) { int mid = (a + b) >> 1; if (sorted_off[mid] > key) b = mid; else a = mid + 1; }
-    lo = a;
-    a = lo; b = ntiles;
-    while (a < b) { int mid = (a + b) >> 1; if (sorted_off[mid] > s) b = mid; else a = mid + 1; }
-    hi = a;
-  }
-  if (lo >= hi) return;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  // each CTA takes a contiguous range of slot groups; a thread's slots increase, so the
+  // touched interval and the covering tile range [lo, hi) are found by binary search once and
+  // then only advanced (the summation order per slot is unchanged)
+  const int64_t n = n_iv > 0 ? n_touched : mem_size;
+  int64_t b, e;
+  cta_range(n, 4, &b, &e);
+  IvWalk walk{iv_start, iv_prefix, n_iv};
+  int lo = -1, hi = 0;
   const int64_t split_stride = int64_t(ntiles) * tile_elems;
-  for (int i = lo; i < hi; ++i) {
-    int64_t base = int64_t(sorted[i]) * tile_elems + (s - sorted_off[i]);
-    for (int sp = 0; sp < nsplit; ++sp) {
-      float4 v = *reinterpret_cast<const float4*>(ws + sp * split_stride + base);
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  for (int64_t p = b + int64_t(threadIdx.x) * 4; p < e; p += int64_t(blockDim.x) * 4) {
+    int64_t s;
+    if (n_iv > 0) {
+      if (lo < 0) walk.seek(p);
+      s = walk.slot(p);
+    } else {
+      s = p;
     }
-  }
-  if (s + 4 <= mem_size) {
-    float4* d = reinterpret_cast<float4*>(dM + s);
-    float4 o = *d;
-    o.x += acc.x; o.y += acc.y; o.z += acc.z; o.w += acc.w;
-    *d = o;
-  } else {   // |M| % 4 != 0: the last group is partial
-    const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
-    for (int k = 0; s + k < mem_size; ++k) dM[s + k] += a4[k];
+    if (s >= mem_size) break;
+    if (lo < 0) {   // lo = first i with sorted_off[i] > s - T ; hi = first i with sorted_off[i] > s
+      const int64_t key = s - tile_elems;
+      int x = 0, y = ntiles;
+      while (x < y) { int mid = (x + y) >> 1; if (sorted_off[mid] > key) y = mid; else x = mid + 1; }
+      lo = x;
+      y = ntiles;
+      while (x < y) { int mid = (x + y) >> 1; if (sorted_off[mid] > s) y = mid; else x = mid + 1; }
+      hi = x;
+    } else {
+      while (lo < ntiles && __ldg(sorted_off + lo) <= s - tile_elems) ++lo;
+      if (hi < lo) hi = lo;
+      while (hi < ntiles && __ldg(sorted_off + hi) <= s) ++hi;
+    }
+    if (lo >= hi) continue;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = lo; i < hi; ++i) {
+      const int64_t base = int64_t(__ldg(sorted + i)) * tile_elems + (s - __ldg(sorted_off + i));
+      for (int sp = 0; sp < nsplit; ++sp) {
+        float4 v = *reinterpret_cast<const float4*>(ws + sp * split_stride + base);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+    }
+    if (s + 4 <= mem_size) {
+      float4* d = reinterpret_cast<float4*>(dM + s);
+      float4 o = *d;
+      o.x += acc.x; o.y += acc.y; o.z += acc.z; o.w += acc.w;
+      *d = o;
+    } else {   // |M| % 4 != 0: the last group is partial
+      const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+      for (int k = 0; s + k < mem_size; ++k) dM[s + k] += a4[k];
+    }
   }
 }
 
@@ -350,7 +358,7 @@ cudaError_t launch_det_reduce(Ctx* c, const Module& m, const float* ws, int nspl
                        c->n_iv > 0;
   int64_t nthreads = ((touched ? c->touched_n : c->mem_size) + 3) / 4;
   int threads = 256;
-  int64_t blocks = (nthreads + threads - 1) / threads;
+  int64_t blocks = std::min<int64_t>((nthreads + threads - 1) / threads, 148 * 32);
   det_reduce_kernel<<<unsigned(blocks), threads, 0, s>>>(c->dM, ws, m.d_sorted, m.d_sorted_off, m.nx * m.ny,
                                                          int64_t(c->tile.z1) * c->tile.z2, nsplit, c->mem_size,
                                                          touched ? c->d_iv : nullptr,
