@@ -246,9 +246,12 @@ roast_status_t roast_embedding_bwd(roast_t h, int32_t id, const int64_t* d_idx, 
  * chunk; a table may repeat) looks up idx[t n + b]; batch rows are table-major, so
  * d_idx is ntables x n int64, d_out / d_dOut are (ntables n) x dim fp32 and row
  * t n + b equals roast_embedding_fwd(ids[t], idx[t n + b]) bit for bit.  Backward
- * adds every table's gradient into dM (same result as ntables single calls,
- * bitwise in deterministic mode).  Errors: CONFIG (null / unaligned pointers, ids
- * of differing dim or chunk), BAD_ID, SHAPE. */
+ * adds every table's gradient into dM (the same sum as ntables single calls, up to
+ * fp32 rounding order).  Deterministic mode sorts the items of up to 32 tables together
+ * (groups of 32 in table order beyond that): bitwise reproducible run to run, but the
+ * per-slot order differs from ntables single calls, so the two agree only to rounding.
+ * Errors: CONFIG (null / unaligned pointers, ids of differing dim or chunk), BAD_ID,
+ * SHAPE. */
 roast_status_t roast_embedding_fwd_multi(roast_t h, const int32_t* ids, int32_t ntables, const int64_t* d_idx,
                                          int64_t n, float* d_out, roast_stream_t stream);
 roast_status_t roast_embedding_bwd_multi(roast_t h, const int32_t* ids, int32_t ntables, const int64_t* d_idx,

@@ -536,7 +536,10 @@ roast_status_t roast_bias_bwd_ld(roast_t h, int32_t bias_id, const void* dY, int
   c->launches += 2;
   if (e == cudaSuccess) {
     if (c->cfg.deterministic) {
-      st = embed_bwd_deterministic(c, *m, c->d_zero_idx, 1, db, s);
+      {
+        const Module* one = m;
+        st = embed_bwd_deterministic(c, &one, 1, c->d_zero_idx, 1, db, s);
+      }
     } else {
       e = launch_embed_bwd(c, *m, c->d_zero_idx, 1, db, s);
       c->launches++;
@@ -636,7 +639,10 @@ roast_status_t roast_embedding_bwd(roast_t h, int32_t id, const int64_t* idx, in
   if (n < 0) return fail(ROAST_ERR_SHAPE, "n < 0");
   if (n > 0 && (!idx || !dOut)) return fail(ROAST_ERR_CONFIG, "null idx / dOut");
   if (reinterpret_cast<uintptr_t>(dOut) & 15) return fail(ROAST_ERR_CONFIG, "dOut must be 16-byte aligned");
-  if (c->cfg.deterministic) return embed_bwd_deterministic(c, *m, idx, n, dOut, reinterpret_cast<cudaStream_t>(stream));
+  if (c->cfg.deterministic) {
+    const Module* one = m;
+    return embed_bwd_deterministic(c, &one, 1, idx, n, dOut, reinterpret_cast<cudaStream_t>(stream));
+  }
   ROAST_CUDA_CHECK(launch_embed_bwd(c, *m, idx, n, dOut, reinterpret_cast<cudaStream_t>(stream)));
   c->launches++;
   return ROAST_OK;
@@ -662,13 +668,8 @@ static roast_status_t embedding_multi(roast_t h, const int32_t* ids, int32_t nt,
   }
   const cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int64_t dim = mods[0]->dim;
-  if (dOut && c->cfg.deterministic) {  // fixed order: table by table, each sorted (K7 det)
-    for (int t = 0; t < nt; ++t) {
-      roast_status_t st = embed_bwd_deterministic(c, *mods[t], idx + t * n, n, dOut + t * n * dim, s);
-      if (st) return st;
-    }
-    return ROAST_OK;
-  }
+  if (dOut && c->cfg.deterministic)  // fixed order: the tables' items sorted together (K7 det)
+    return embed_bwd_deterministic(c, mods.data(), nt, idx, n, dOut, s);
   for (int t0 = 0; t0 < nt; t0 += kEmbMaxTables) {
     const int k = std::min(nt - t0, kEmbMaxTables);
     ROAST_CUDA_CHECK(launch_embed_multi(c, mods.data() + t0, k, idx + t0 * n, n, out ? out + t0 * n * dim : nullptr,

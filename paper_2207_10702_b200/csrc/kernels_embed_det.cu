@@ -24,16 +24,27 @@
 namespace roast {
 namespace {
 
-__global__ void emb_items_kernel(ModuleHash h, const int64_t* __restrict__ idx, int64_t n, int64_t rows, int q,
-                                 int G, uint32_t* __restrict__ keys, int32_t* __restrict__ vals, int32_t* err,
+// up to kDetTables tables of equal dim / chunk in one sorted pass (roast_embedding_bwd_multi):
+// lookup b of the table-major batch belongs to table b / n
+constexpr int kDetTables = 32;
+struct DetTables {
+  ModuleHash h[kDetTables];
+  int64_t rows[kDetTables];
+  float lam[kDetTables];
+  int64_t n;   // lookups per table
+};
+
+__global__ void emb_items_kernel(const __grid_constant__ DetTables T, const int64_t* __restrict__ idx, int64_t nlook, int q, int G,
+                                 uint32_t* __restrict__ keys, int32_t* __restrict__ vals, int32_t* err,
                                  int32_t* __restrict__ nvalid) {
   const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (p == 0) *nvalid = int32_t(n * q * G);   // lowered by emb_heads_kernel if rows were out of range
-  if (p >= n * q) return;
+  if (p == 0) *nvalid = int32_t(nlook * q * G);   // lowered by emb_heads_kernel if rows were out of range
+  if (p >= nlook * q) return;
   const int64_t b = p / q;
   const int j = int(p - b * q);
+  const int t = int(b / T.n);
   const int64_t r = idx[b];
-  if (r < 0 || r >= rows) {
+  if (r < 0 || r >= T.rows[t]) {
     atomicOr(err, 1);
     for (int i = 0; i < G; ++i) {   // sorts last; the reduce skips the sentinel group
       keys[p * G + i] = 0xFFFFFFFFu;
@@ -42,13 +53,18 @@ __global__ void emb_items_kernel(ModuleHash h, const int64_t* __restrict__ idx, 
     return;
   }
   const uint64_t key = uint64_t(r) * uint64_t(q) + uint64_t(j);
-  const uint32_t k0 = uint32_t(h.offset(key) / h.align);
-  const int32_t neg = h.sign(key) < 0 ? int32_t(0x80000000) : 0;
+  const uint32_t k0 = uint32_t(T.h[t].offset(key) / T.h[t].align);
+  const int32_t neg = T.h[t].sign(key) < 0 ? int32_t(0x80000000) : 0;
   for (int i = 0; i < G; ++i) {
     keys[p * G + i] = (k0 + uint32_t(i)) * uint32_t(G) + uint32_t(G - 1 - i);
     vals[p * G + i] = int32_t(p * G + i) | neg;   // item index, sign in the top bit
   }
 }
+
+struct DetLam {   // lambda of each table and lookups per table (pass 1)
+  float lam[kDetTables];
+  int n;
+};
 
 __global__ void emb_heads_kernel(const uint32_t* __restrict__ keys, int64_t nitems, int G, uint8_t* __restrict__ head,
                                  int32_t* __restrict__ nvalid) {
@@ -107,31 +123,43 @@ __global__ void emb_chunkmap_kernel(const uint32_t* __restrict__ keys, const int
   }
 }
 
-// sum of one chunk's terms in item order (8 independent loads in flight)
+// sum of one chunk's terms in item order.  The chunk is warp-uniform; lane k decodes item
+// it0 + k once (index arithmetic, sign, lambda) and the warp broadcasts it with shuffles, so
+// the integer work is per item instead of per item and lane; 8 dOut loads in flight.
 __device__ __forceinline__ float chunk_sum(const ChunkInfo& ci, const int32_t* __restrict__ vals,
                                            const float* __restrict__ dOut, int dim, int chunk, int q, int G, int A,
-                                           float lam, int lane) {
+                                           const DetLam& L, int lane) {
   float acc = 0.f;
   constexpr int U = 8;
-  for (int it0 = ci.begin; it0 < ci.end; it0 += U) {
-    float t[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      t[u] = 0.f;
-      const int it = it0 + u;
-      if (it >= ci.end) continue;
-      const int32_t v = __ldg(vals + it);
-      const int64_t item = int64_t(v & 0x7FFFFFFF);
-      const int64_t p = item / G;
-      const int i = int(item - p * G);
-      const int64_t b = p / q;
-      const int j = int(p - b * q);
-      const int col = j * chunk + i * A + lane;
-      if (lane < A && col < dim)   // padded tail of the last chunk (R16) contributes nothing
-        t[u] = (v < 0 ? -lam : lam) * __ldg(dOut + b * dim + col);
+  for (int it0 = ci.begin; it0 < ci.end; it0 += 32) {
+    int myb = 0, mycb = dim;   // row, first column of the item's A slots (dim = contributes nothing)
+    float mys = 0.f;           // g * lambda
+    if (it0 + lane < ci.end) {
+      const int32_t v = __ldg(vals + it0 + lane);
+      const int item = v & 0x7FFFFFFF;   // < 2^30: 32-bit index arithmetic
+      const int p = item / G;
+      const int i = item - p * G;
+      myb = p / q;
+      mycb = (p - myb * q) * chunk + i * A;
+      const float lam = L.lam[myb / L.n];
+      mys = v < 0 ? -lam : lam;
     }
+    const int cnt = min(32, ci.end - it0);
+    for (int k0 = 0; k0 < cnt; k0 += U) {
+      float t[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) acc += t[u];
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u;   // k < 32 always; items past cnt carry mycb = dim
+        const int b = __shfl_sync(0xffffffffu, myb, k);
+        const int col = __shfl_sync(0xffffffffu, mycb, k) + lane;
+        const float sl = __shfl_sync(0xffffffffu, mys, k);
+        t[u] = 0.f;
+        if (k < cnt && lane < A && col < dim)   // padded tail of the last chunk (R16): nothing
+          t[u] = sl * __ldg(dOut + int64_t(b) * dim + col);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc += t[u];
+    }
   }
   return acc;
 }
@@ -142,7 +170,7 @@ __global__ void emb_chunk_kernel(float* __restrict__ dM, float* __restrict__ par
                                  const int32_t* __restrict__ vals, const ChunkInfo* __restrict__ info,
                                  const int32_t* __restrict__ nseg_p, const int32_t* __restrict__ nch,
                                  const int32_t* __restrict__ choff, const float* __restrict__ dOut, int dim, int chunk,
-                                 int q, int G, int A, float lam, int64_t mem_size) {
+                                 int q, int G, int A, const __grid_constant__ DetLam lam, int64_t mem_size) {
   const int lane = threadIdx.x & 31;
   const int64_t nseg = *nseg_p;
   if (nseg == 0) return;
@@ -192,20 +220,54 @@ __global__ void emb_longseg_kernel(float* __restrict__ dM, const float* __restri
 
 }  // namespace
 
-roast_status_t embed_bwd_deterministic(Ctx* c, const Module& m, const int64_t* idx, int64_t n, const float* dOut,
-                                       cudaStream_t s) {
-  const int64_t np = n * m.chunks_per_row;
+namespace {
+roast_status_t embed_bwd_det_group(Ctx* c, const Module* const* mods, int nt, const int64_t* idx, int64_t n,
+                                   const float* dOut, cudaStream_t s);
+}
+
+roast_status_t embed_bwd_deterministic(Ctx* c, const Module* const* mods, int nt, const int64_t* idx, int64_t n,
+                                       const float* dOut, cudaStream_t s) {
+  // groups of kDetTables tables, one after the other (a fixed order across groups too)
+  for (int t0 = 0; t0 < nt; t0 += kDetTables) {
+    const int k = std::min(nt - t0, kDetTables);
+    if (roast_status_t st = embed_bwd_det_group(c, mods + t0, k, idx + t0 * n, n,
+                                                dOut + t0 * n * int64_t(mods[0]->dim), s))
+      return st;
+  }
+  return ROAST_OK;
+}
+
+namespace {
+roast_status_t embed_bwd_det_group(Ctx* c, const Module* const* mods, int nt, const int64_t* idx, int64_t n,
+                                   const float* dOut, cudaStream_t s) {
+  const Module& m = *mods[0];
+  const int64_t np = int64_t(nt) * n * m.chunks_per_row;
   if (np == 0) return ROAST_OK;
   const int A = int(m.hash.align);
   const int G = m.chunk / A;
   const int64_t ni = np * G;
+  for (int t = 1; t < nt; ++t)
+    if (mods[t]->hash.align != m.hash.align || mods[t]->chunk != m.chunk || mods[t]->dim != m.dim)
+      return fail(ROAST_ERR_CONFIG, "deterministic multi-table backward needs equal dim, chunk and alignment");
   if (ni >= (int64_t(1) << 30) || (c->mem_size / A + G) * G >= (int64_t(1) << 32) - 1 || A > 32)
     return fail(ROAST_ERR_UNSUPPORTED, "deterministic embedding backward: too many items or slot groups");
+  // sort only the key bits in use: keys < (|M| / A + G) * G
+  int end_bit = 1;
+  while (end_bit < 32 && (uint64_t(1) << end_bit) <= uint64_t((c->mem_size / A + G) * G)) ++end_bit;
+  DetTables T{};
+  DetLam L{};
+  for (int t = 0; t < nt; ++t) {
+    T.h[t] = mods[t]->hash;
+    T.rows[t] = mods[t]->rows;
+    T.lam[t] = L.lam[t] = mods[t]->lam;
+  }
+  T.n = n;
+  L.n = int(n);
   const int ni1 = int(ni) + 1;
   size_t t_sort = 0, t_sel = 0, t_scan = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, t_sort, static_cast<const uint32_t*>(nullptr),
                                   static_cast<uint32_t*>(nullptr), static_cast<const int32_t*>(nullptr),
-                                  static_cast<int32_t*>(nullptr), int(ni), 0, 32, s);
+                                  static_cast<int32_t*>(nullptr), int(ni), 0, end_bit, s);
   cub::CountingInputIterator<int32_t> count_it(0);
   cub::DeviceSelect::Flagged(nullptr, t_sel, count_it, static_cast<const uint8_t*>(nullptr),
                              static_cast<int32_t*>(nullptr), static_cast<int32_t*>(nullptr), int(ni), s);
@@ -236,11 +298,11 @@ roast_status_t embed_bwd_deterministic(Ctx* c, const Module& m, const int64_t* i
   int32_t* nseg = scal;
   int32_t* nvalid = scal + 1;
   void* tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(scal + 4) + 255) & ~uintptr_t(255));
-  emb_items_kernel<<<unsigned((np + 255) / 256), 256, 0, s>>>(m.hash, idx, n, m.rows, m.chunks_per_row, G, k_in, v_in,
-                                                              c->d_err, nvalid);
+  emb_items_kernel<<<unsigned((np + 255) / 256), 256, 0, s>>>(T, idx, int64_t(nt) * n, m.chunks_per_row, G, k_in,
+                                                              v_in, c->d_err, nvalid);
   ROAST_CUDA_CHECK(cudaGetLastError());
   size_t t1 = temp;
-  ROAST_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, t1, k_in, k_out, v_in, v_out, int(ni), 0, 32, s));
+  ROAST_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, t1, k_in, k_out, v_in, v_out, int(ni), 0, end_bit, s));
   emb_heads_kernel<<<unsigned((ni + 255) / 256), 256, 0, s>>>(k_out, ni, G, flags, nvalid);
   ROAST_CUDA_CHECK(cudaGetLastError());
   size_t t2 = temp;
@@ -256,12 +318,13 @@ roast_status_t embed_bwd_deterministic(Ctx* c, const Module& m, const int64_t* i
   ROAST_CUDA_CHECK(cudaGetLastError());
   const int grid = 148 * 8;
   emb_chunk_kernel<<<grid, 256, 0, s>>>(c->dM, partial, v_out, info, nseg, nch, choff, dOut, m.dim, m.chunk,
-                                        m.chunks_per_row, G, A, m.lam, c->mem_size);
+                                        m.chunks_per_row, G, A, L, c->mem_size);
   ROAST_CUDA_CHECK(cudaGetLastError());
   emb_longseg_kernel<<<grid, 256, 0, s>>>(c->dM, partial, k_out, heads, nseg, nch, loff, G, A, c->mem_size);
   ROAST_CUDA_CHECK(cudaGetLastError());
   c->launches += 9;
   return ROAST_OK;
 }
+}  // namespace
 
 }  // namespace roast

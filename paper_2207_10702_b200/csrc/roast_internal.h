@@ -206,8 +206,8 @@ cudaError_t launch_chunk_map(const Ctx* c, const Module& m, const int64_t* rows,
 
 // tcgen05 paths (bf16, Z1 = Z2 = 64)
 // deterministic embedding backward: key by offset, stable radix sort, fixed-order per-slot sum
-roast_status_t embed_bwd_deterministic(Ctx* c, const Module& m, const int64_t* idx, int64_t n, const float* dOut,
-                                       cudaStream_t s);
+roast_status_t embed_bwd_deterministic(Ctx* c, const Module* const* mods, int nt, const int64_t* idx, int64_t n,
+                                       const float* dOut, cudaStream_t s);
 roast_status_t sm100_prepare(Ctx* c);  // build shadow tensor map
 roast_status_t sm100_fwd(Ctx* c, const Module& m, const void* X, void* Y, int64_t T, const float* bias,
                          cudaStream_t s);
