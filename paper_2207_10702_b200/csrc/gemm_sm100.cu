@@ -308,6 +308,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // programmatic dependent launch: the next GEMM on this stream may be scheduled as soon as
+  // every CTA of this grid is resident (it lands on SMs as they free up and runs its prologue
+  // under this grid's tail); it waits (griddepcontrol.wait below) before touching global data
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   long long prof_acc[5] = {0, 0, 0, 0, 0};
   long long prof_epi[4] = {0, 0, 0, 0};   // epilogue: TMEM load+wait, staging wait, STS, fence+issue
   const long long t_start = clock64();
@@ -364,6 +368,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // the previous kernel on this stream (launched before us with PDL) has completed and its
+  // writes are visible from here on; everything above touched only smem / TMEM / descriptors
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     // ===================== TMA producer (warp 0, both CTAs) =====================
@@ -826,13 +833,16 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
   cfg.blockDim = dim3(NUM_THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CG;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see griddepcontrol in the kernel
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  static const bool pdl = !(getenv("ROAST_PDL") && atoi(getenv("ROAST_PDL")) == 0);
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   static long long* prof = nullptr;
   Params pp = p, pp1 = p1;
   if (const char* e = getenv("ROAST_EPI")) pp.epi = atoi(e);
