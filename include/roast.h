@@ -22,6 +22,11 @@
  *     was launched.  Device-detected faults (embedding index out of range) are
  *     sticky and reported by roast_get_error() (and by the next call).
  *   - A handle is not thread-safe; use one per thread / rank.
+ *   - The tcgen05 GEMMs use programmatic dependent launch among themselves: each is launched
+ *     with cudaLaunchAttributeProgrammaticStreamSerialization and signals
+ *     griddepcontrol.launch_dependents on entry, so only a following kernel that is itself
+ *     launched with that attribute (and executes griddepcontrol.wait) may start early.
+ *     Ordinary launches after a ROAST call keep full stream order (ROAST_PDL=0 disables it).
  *   - roast_last_error() returns a human-readable detail string for the last
  *     non-OK status returned on the calling thread.
  *
