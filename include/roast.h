@@ -349,8 +349,8 @@ roast_status_t roast_grad_exchange_step(roast_t h, const roast_opt_config_t* cfg
  * registered; re-registering invalidates the window (ROAST_ERR_STATE until re-opened).
  *
  * roast_p2p_window: allocate (once) this handle's window, a device buffer the library owns:
- *   [0, 256) int32 flags[world] | [256, 512) int32 epoch, uint32 arrival counter |
- *   [512, ...) two fp32 buffers of
+ *   [0, 128) int32 flags[world] | [128, 256) int32 flags2[world] (two-shot) |
+ *   [256, 512) int32 epoch, uint32 arrival counter | [512, ...) three fp32 buffers of
  *   the touched-slot count (rounded up to 4) each; flags and epoch start at 0.  *window /
  *   *bytes (either may be NULL) receive its device address and size.
  * roast_p2p_ipc_handle: the window's cudaIpcMemHandle (64 bytes, host buffer) for the other
@@ -378,6 +378,24 @@ roast_status_t roast_p2p_post(roast_t h, roast_stream_t stream);
 roast_status_t roast_p2p_finish(roast_t h, const roast_opt_config_t* cfg, int64_t step, roast_stream_t stream);
 roast_status_t roast_grad_exchange_p2p(roast_t h, const roast_opt_config_t* cfg, int64_t step,
                                        roast_stream_t stream);
+
+/* Two-shot variant (same window, same post): the one-shot finish reads (W - 1) n values
+ * from the peers per rank, which for large touched sets is more NVLink traffic than a ring
+ * (2 (W - 1) / W n).  Here rank r owns the packed-index slice [r per, (r + 1) per),
+ * per = ceil(n / W) rounded up to 4:
+ * roast_p2p_reduce: wait for every post, sum the slice's gradients over the ranks (rank
+ *   order), update M / optimizer state / shadow / dM (zeroed) on the slice, copy the new
+ *   values into this rank's M buffer, then publish flags2 on every rank.  2 launches.
+ * roast_p2p_gather: wait for every rank's flags2, copy the other slices' new values from
+ *   the owners' M buffers into M at the touched slots, refresh the shadow, zero dM.  1 launch.
+ * roast_grad_exchange_p2p2: post + reduce + gather.  Result bit-identical to the one-shot
+ * path for M and the shadow.  The optimizer state of a slice lives on its owner only, so keep
+ * one variant and one world size for a whole run.  zero_grad must be 1 (else
+ * ROAST_ERR_CONFIG).  Ranks sharing one stream: post all, reduce all, then gather all. */
+roast_status_t roast_p2p_reduce(roast_t h, const roast_opt_config_t* cfg, int64_t step, roast_stream_t stream);
+roast_status_t roast_p2p_gather(roast_t h, roast_stream_t stream);
+roast_status_t roast_grad_exchange_p2p2(roast_t h, const roast_opt_config_t* cfg, int64_t step,
+                                        roast_stream_t stream);
 
 /* Sticky device-side error (synchronises the handle's bound stream is NOT done:
  * call after a stream synchronize to observe faults of completed work). */

@@ -466,8 +466,11 @@ template <int KIND, int V>
 __global__ void opt_kernel(OptArgs a) {
   int64_t pbuf = 0;   // P2P: offset of this step's buffer (parity of the epoch)
   if (a.p2p.world > 0) pbuf = (p2p_wait(a.p2p) & 1) ? a.p2p.stride : 0;
+  const int64_t lo = a.p2p.lo, hi = a.p2p.hi < 0 ? a.n : a.p2p.hi;   // two-shot: this rank's slice
   int64_t b, e;
-  cta_range(a.n, V, &b, &e);
+  cta_range(hi - lo, V, &b, &e);
+  b += lo;
+  e += lo;
   IvWalk walk{a.iv_start, a.iv_prefix, a.n_iv};
   if (a.n_iv > 0 && b + int64_t(threadIdx.x) * V < e) walk.seek(b + int64_t(threadIdx.x) * V);
   for (int64_t p = b + int64_t(threadIdx.x) * V; p < e; p += int64_t(blockDim.x) * V) {
@@ -508,6 +511,12 @@ __global__ void opt_kernel(OptArgs a) {
     }
 #pragma unroll
     for (int k = 0; k < V; ++k) w[k] = opt_update<KIND>(w[k], g[k], x[k], y[k], a.lr, a.b1, a.b2, a.eps, a.wd, a.bc1, a.bc2);
+    if (a.p2p.mout) {   // two-shot: publish this slice's new values for the gather phase
+      if constexpr (V == 4)
+        *reinterpret_cast<float4*>(a.p2p.mout + p) = make_float4(w[0], w[1], w[2], w[3]);
+      else
+        a.p2p.mout[p] = w[0];
+    }
     if constexpr (V == 4) {
       *reinterpret_cast<float4*>(a.M + i) = make_float4(w[0], w[1], w[2], w[3]);
       if (KIND >= 1) *reinterpret_cast<float4*>(a.s1 + i) = make_float4(x[0], x[1], x[2], x[3]);
@@ -542,7 +551,8 @@ __global__ void opt_kernel(OptArgs a) {
 template <int KIND>
 void launch_opt_kind(const OptArgs& a, bool vec, cudaStream_t s) {
   const int V = vec ? 4 : 1;
-  int64_t blocks = (a.n / V + 255) / 256;
+  const int64_t len = a.p2p.hi < 0 ? a.n : a.p2p.hi - a.p2p.lo;
+  int64_t blocks = (len / V + 255) / 256;
   blocks = std::min<int64_t>(std::max<int64_t>(blocks, 1), 148 * 16);
   if (vec)
     opt_kernel<KIND, 4><<<unsigned(blocks), 256, 0, s>>>(a);

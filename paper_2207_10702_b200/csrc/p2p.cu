@@ -18,6 +18,7 @@
 // Two buffers make the reuse safe: a rank writes buffer (e & 1) again at epoch e + 2 only after
 // its own finish(e + 1), which waited for every peer's post(e + 1), which each peer issued
 // after its finish(e) had stopped reading that buffer.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -74,6 +75,86 @@ __global__ void p2p_post_kernel(const float* __restrict__ dM, PeerWins peers, in
   }
 }
 
+// two-shot: after this rank's slice of M is updated (and copied to its M buffer), publish the
+// current epoch in every rank's flags2[rank]
+__global__ void p2p_signal2_kernel(PeerWins peers, int world, int rank) {
+  const int e = *reinterpret_cast<const volatile int*>(peers.w[rank] + 256);
+  __threadfence();
+  if (threadIdx.x < world) {
+    int* f = reinterpret_cast<int*>(peers.w[threadIdx.x] + 128) + rank;
+    asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(f), "r"(e) : "memory");
+  }
+}
+
+struct Slices {   // packed-index slice [at[r], at[r + 1]) is updated by rank r
+  int64_t at[kP2PMaxWorld + 1];
+};
+
+// two-shot gather: wait until every rank has published its slice (flags2 >= epoch), then copy
+// the other ranks' new values into M at the touched slots, refresh both shadow halves, zero dM
+template <int V>
+__global__ void p2p_gather_kernel(float* __restrict__ M, float* __restrict__ dM, __nv_bfloat16* __restrict__ sh,
+                                  int64_t neg_base, PeerWins peers, int world, int rank, Slices sl, int64_t stride,
+                                  const int64_t* __restrict__ start, const int64_t* __restrict__ prefix, int n_iv,
+                                  int64_t n, int* err) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    const char* win = peers.w[rank];
+    const int e = *reinterpret_cast<const volatile int*>(win + 256);
+    const int* f2 = reinterpret_cast<const int*>(win + 128);
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int r = 0; r < world; ++r) {
+      int f;
+      for (;;) {
+        asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(f) : "l"(f2 + r) : "memory");
+        if (f - e >= 0) break;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 20000000000ull) {
+          atomicOr(err, 2);
+          __threadfence_system();
+          __trap();
+        }
+        __nanosleep(64);
+      }
+    }
+    s_ok = 1;
+  }
+  __syncthreads();
+  using VT = typename std::conditional<V == 4, float4, float>::type;
+  int64_t b, end;
+  cta_range(n, V, &b, &end);
+  IvWalk w{start, prefix, n_iv};
+  if (b + int64_t(threadIdx.x) * V < end) w.seek(b + int64_t(threadIdx.x) * V);
+  int owner = 0;
+  for (int64_t p = b + int64_t(threadIdx.x) * V; p < end; p += int64_t(blockDim.x) * V) {
+    const int64_t i = w.slot(p);
+    while (owner + 1 < world && sl.at[owner + 1] <= p) ++owner;
+    if (owner == rank) continue;   // updated in place by this rank's reduce phase
+    const float* src = reinterpret_cast<const float*>(peers.w[owner] + kP2PHeader) + 2 * stride + p;
+    const VT v = __ldcv(reinterpret_cast<const VT*>(src));
+    *reinterpret_cast<VT*>(M + i) = v;
+    if constexpr (V == 4) {
+      const __nv_bfloat162 p0 = __floats2bfloat162_rn(v.x, v.y), p1 = __floats2bfloat162_rn(v.z, v.w);
+      uint2 pos, neg;
+      pos.x = *reinterpret_cast<const uint32_t*>(&p0);
+      pos.y = *reinterpret_cast<const uint32_t*>(&p1);
+      neg.x = pos.x ^ 0x80008000u;
+      neg.y = pos.y ^ 0x80008000u;
+      *reinterpret_cast<uint2*>(sh + i) = pos;
+      *reinterpret_cast<uint2*>(sh + neg_base + i) = neg;
+      *reinterpret_cast<float4*>(dM + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      const __nv_bfloat16 bv = __float2bfloat16_rn(v);
+      sh[i] = bv;
+      sh[neg_base + i] = __hneg(bv);
+      dM[i] = 0.f;
+    }
+  }
+  (void)s_ok;
+}
+
 }  // namespace
 }  // namespace roast
 
@@ -115,7 +196,7 @@ roast_status_t roast_p2p_window(roast_t h, void** window, int64_t* bytes) {
   if (!c || !c->dM) return fail(ROAST_ERR_STATE, "not bound");
   if (roast_status_t st = touched_prepare(c, 0)) return st;
   const int64_t n = (c->touched_n + 3) / 4 * 4;   // keep buffer 1 16-byte aligned
-  const int64_t need = kP2PHeader + 2 * n * int64_t(sizeof(float));
+  const int64_t need = kP2PHeader + 3 * n * int64_t(sizeof(float));   // 2 gradient buffers + M buffer
   if (!c->p2p_win || c->p2p_n != c->touched_n) {
     p2p_release(c);
     cudaFree(c->p2p_win);
@@ -230,6 +311,85 @@ roast_status_t roast_grad_exchange_p2p(roast_t h, const roast_opt_config_t* cfg,
   if (roast_status_t st = opt_prepare(c, cfg, step, true, reinterpret_cast<cudaStream_t>(stream))) return st;
   if (roast_status_t st = roast_p2p_post(h, stream)) return st;
   return roast_p2p_finish(h, cfg, step, stream);
+}
+
+// ---- two-shot: reduce-scatter + update of a slice, then gather (traffic 2 (W - 1) / W n per rank)
+namespace {
+Slices p2p_slices(const Ctx* c) {
+  Slices sl{};
+  const int W = c->p2p_world;
+  const int64_t n = c->p2p_n;
+  const int64_t per = ((n + W - 1) / W + 3) / 4 * 4;
+  for (int r = 0; r <= W; ++r) sl.at[r] = std::min<int64_t>(n, int64_t(r) * per);
+  for (int r = W + 1; r <= kP2PMaxWorld; ++r) sl.at[r] = n;
+  return sl;
+}
+}  // namespace
+
+roast_status_t roast_p2p_reduce(roast_t h, const roast_opt_config_t* cfg, int64_t step, roast_stream_t stream) {
+  Ctx* c = pctx(h);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (roast_status_t st = opt_prepare(c, cfg, step, true, s)) return st;
+  if (!p2p_ready(c)) return fail(ROAST_ERR_STATE, "p2p: call roast_p2p_open / roast_p2p_attach after registering every module");
+  if (!cfg->zero_grad) return fail(ROAST_ERR_CONFIG, "two-shot p2p exchange: zero_grad must be 1");
+  const Slices sl = p2p_slices(c);
+  P2PView v;
+  v.world = c->p2p_world;
+  for (int r = 0; r < c->p2p_world; ++r) v.buf0[r] = reinterpret_cast<const float*>(c->p2p_peer[r] + kP2PHeader);
+  v.stride = (c->p2p_n + 3) / 4 * 4;
+  v.flags = reinterpret_cast<const int*>(c->p2p_win);
+  v.epoch = reinterpret_cast<const int*>(c->p2p_win + 256);
+  v.err = c->d_err;
+  v.lo = sl.at[c->p2p_rank];
+  v.hi = sl.at[c->p2p_rank + 1];
+  v.mout = reinterpret_cast<float*>(c->p2p_win + kP2PHeader) + 2 * v.stride;
+  if (c->p2p_n > 0) {   // an empty slice still runs: the kernel waits for every post first
+    ROAST_CUDA_CHECK(launch_optimizer(c, cfg->kind, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay,
+                                      step, 1, true, s, nullptr, &v));
+    c->launches++;
+  }
+  PeerWins pw{};
+  for (int r = 0; r < c->p2p_world; ++r) pw.w[r] = c->p2p_peer[r];
+  p2p_signal2_kernel<<<1, 32, 0, s>>>(pw, c->p2p_world, c->p2p_rank);
+  ROAST_CUDA_CHECK(cudaGetLastError());
+  c->launches++;
+  return ROAST_OK;
+}
+
+roast_status_t roast_p2p_gather(roast_t h, roast_stream_t stream) {
+  Ctx* c = pctx(h);
+  if (!c || !c->dM) return fail(ROAST_ERR_STATE, "not bound");
+  if (!p2p_ready(c)) return fail(ROAST_ERR_STATE, "p2p: call roast_p2p_open / roast_p2p_attach after registering every module");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (c->p2p_n == 0) return ROAST_OK;
+  PeerWins pw{};
+  for (int r = 0; r < c->p2p_world; ++r) pw.w[r] = c->p2p_peer[r];
+  const Slices sl = p2p_slices(c);
+  const int64_t stride = (c->p2p_n + 3) / 4 * 4;
+  const int V = c->touched_vec ? 4 : 1;
+  int64_t blocks = (c->p2p_n / V + 255) / 256;
+  blocks = std::min<int64_t>(std::max<int64_t>(blocks, 1), 148 * 8);
+  auto* sh = reinterpret_cast<__nv_bfloat16*>(c->shadow);
+  if (V == 4)
+    p2p_gather_kernel<4><<<unsigned(blocks), 256, 0, s>>>(c->M, c->dM, sh, c->neg_base, pw, c->p2p_world,
+                                                          c->p2p_rank, sl, stride, c->d_iv, c->d_iv + c->n_iv,
+                                                          c->n_iv, c->p2p_n, c->d_err);
+  else
+    p2p_gather_kernel<1><<<unsigned(blocks), 256, 0, s>>>(c->M, c->dM, sh, c->neg_base, pw, c->p2p_world,
+                                                          c->p2p_rank, sl, stride, c->d_iv, c->d_iv + c->n_iv,
+                                                          c->n_iv, c->p2p_n, c->d_err);
+  ROAST_CUDA_CHECK(cudaGetLastError());
+  c->launches++;
+  return ROAST_OK;
+}
+
+roast_status_t roast_grad_exchange_p2p2(roast_t h, const roast_opt_config_t* cfg, int64_t step,
+                                        roast_stream_t stream) {
+  Ctx* c = pctx(h);
+  if (roast_status_t st = opt_prepare(c, cfg, step, true, reinterpret_cast<cudaStream_t>(stream))) return st;
+  if (roast_status_t st = roast_p2p_post(h, stream)) return st;
+  if (roast_status_t st = roast_p2p_reduce(h, cfg, step, stream)) return st;
+  return roast_p2p_gather(h, stream);
 }
 
 }  // extern "C"

@@ -43,8 +43,10 @@ struct Module {
 
 // one-shot P2P exchange: at most one NVSwitch domain (8 GPUs) of ranks
 constexpr int kP2PMaxWorld = 8;
-// window layout (bytes): [0, 256) int32 flags[world] (rank r writes flags[r] = epoch) |
-// [256, 512) int32 epoch of this rank | [512, ...) buffer 0, buffer 1 (p2p_n fp32 each)
+// window layout (bytes): [0, 128) int32 flags[world] (rank r writes flags[r] = epoch after its
+// post) | [128, 256) int32 flags2[world] (two-shot: rank r's slice of M is updated) |
+// [256] int32 epoch, [260] u32 arrival counter | [512, ...) buffer 0, buffer 1 (packed
+// gradients) and the two-shot M buffer, p2p_n fp32 each (rounded up to 4)
 constexpr int64_t kP2PHeader = 512;
 
 struct P2PView {   // what the fused update kernel needs (kernels_simt.cu opt_kernel)
@@ -54,6 +56,10 @@ struct P2PView {   // what the fused update kernel needs (kernels_simt.cu opt_ke
   const int* flags = nullptr;             // this rank's flags[world]
   const int* epoch = nullptr;             // this rank's epoch word
   int* err = nullptr;                     // sticky device error word (timeout)
+  // two-shot (reduce-scatter phase): only packed indices [lo, hi) are updated, and the new M
+  // values are also written to mout[p] for the other ranks to gather
+  int64_t lo = 0, hi = -1;                // hi < 0: all of [0, n)
+  float* mout = nullptr;
 };
 
 #ifdef __CUDACC__

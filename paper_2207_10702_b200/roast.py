@@ -31,7 +31,8 @@ EXPORTS = [
     "roast_grad_allreduce", "roast_set_exchange", "roast_touched_size", "roast_touched_intervals",
     "roast_debug_exchange", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step", "roast_grad_exchange_step",
     "roast_p2p_window", "roast_p2p_ipc_handle", "roast_p2p_open", "roast_p2p_attach", "roast_p2p_post",
-    "roast_p2p_finish", "roast_grad_exchange_p2p", "roast_get_error",
+    "roast_p2p_finish", "roast_grad_exchange_p2p", "roast_p2p_reduce", "roast_p2p_gather",
+    "roast_grad_exchange_p2p2", "roast_get_error",
     "roast_status_str", "roast_last_error", "roast_debug_tile_map", "roast_debug_chunk_map",
     "roast_debug_materialize", "roast_debug_hash_host", "roast_launch_count",
 ]
@@ -118,6 +119,9 @@ def _load():
         "roast_p2p_post": (st, [H, S]),
         "roast_p2p_finish": (st, [H, ctypes.POINTER(roast_opt_config_t), I64, S]),
         "roast_grad_exchange_p2p": (st, [H, ctypes.POINTER(roast_opt_config_t), I64, S]),
+        "roast_p2p_reduce": (st, [H, ctypes.POINTER(roast_opt_config_t), I64, S]),
+        "roast_p2p_gather": (st, [H, S]),
+        "roast_grad_exchange_p2p2": (st, [H, ctypes.POINTER(roast_opt_config_t), I64, S]),
         "roast_get_error": (st, [H]),
         "roast_status_str": (ctypes.c_char_p, [st]),
         "roast_last_error": (ctypes.c_char_p, []),
@@ -408,6 +412,20 @@ def roast_grad_exchange_p2p(h, kind, lr, step=1, beta1=0.9, beta2=0.999, eps=1e-
                             zero_grad=True, stream=0):
     cfg = roast_opt_config_t(kind, lr, beta1, beta2, eps, weight_decay, int(zero_grad), 1)
     _check(_lib.roast_grad_exchange_p2p(h, ctypes.byref(cfg), step, stream), "roast_grad_exchange_p2p")
+
+
+def roast_p2p_reduce(h, kind, lr, step=1, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, stream=0):
+    cfg = roast_opt_config_t(kind, lr, beta1, beta2, eps, weight_decay, 1, 1)
+    _check(_lib.roast_p2p_reduce(h, ctypes.byref(cfg), step, stream), "roast_p2p_reduce")
+
+
+def roast_p2p_gather(h, stream=0):
+    _check(_lib.roast_p2p_gather(h, stream), "roast_p2p_gather")
+
+
+def roast_grad_exchange_p2p2(h, kind, lr, step=1, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, stream=0):
+    cfg = roast_opt_config_t(kind, lr, beta1, beta2, eps, weight_decay, 1, 1)
+    _check(_lib.roast_grad_exchange_p2p2(h, ctypes.byref(cfg), step, stream), "roast_grad_exchange_p2p2")
 
 
 def roast_get_error(h):
@@ -739,6 +757,18 @@ class Roast:
     def exchange_p2p(self, kind, lr, step=1, stream=None, **kw):
         self.flush_bias_grads(stream)
         roast_grad_exchange_p2p(self.h, kind, lr, step, stream=self._s(stream), **kw)
+        self._gen += 1
+
+    def p2p_reduce(self, kind, lr, step=1, stream=None, **kw):
+        roast_p2p_reduce(self.h, kind, lr, step, stream=self._s(stream), **kw)
+
+    def p2p_gather(self, stream=None):
+        roast_p2p_gather(self.h, self._s(stream))
+        self._gen += 1
+
+    def exchange_p2p2(self, kind, lr, step=1, stream=None, **kw):
+        self.flush_bias_grads(stream)
+        roast_grad_exchange_p2p2(self.h, kind, lr, step, stream=self._s(stream), **kw)
         self._gen += 1
 
     def allreduce(self, stream=None):

@@ -109,6 +109,46 @@ def test_p2p_virtual_ranks(R, torch, W, kind, zero):
     ref.close()
 
 
+@pytest.mark.parametrize("W", [1, 2, 3, 4])
+@pytest.mark.parametrize("kind", [0, 2])
+def test_p2p_two_shot_virtual_ranks(R, torch, W, kind):
+    """Two-shot (reduce-scatter of the packed gradient + update of each rank's slice, then a
+    gather of the slices): every rank's M, shadow and dM equal one handle's update of the
+    summed gradient, bit for bit, over three steps (Adam's state lives on the slice owner)."""
+    M0 = store(MEM)
+    ranks = [_model(R, torch, M0) for _ in range(W)]
+    ids = ranks[0][1]
+    inside = torch.tensor(_touched(ids), device="cuda")
+    wins = [c.p2p_window()[0] for c, _ in ranks]
+    for r, (c, _) in enumerate(ranks):
+        c.p2p_attach(r, wins)
+    ref, _ = _model(R, torch, M0)
+    for t in (1, 2, 3):
+        gs = _grads(torch, inside, W, t)
+        for (c, _), g in zip(ranks, gs):
+            c.dM.copy_(g)
+        for c, _ in ranks:
+            c.p2p_post()
+        for c, _ in ranks:
+            c.p2p_reduce(kind, 1e-2, step=t, weight_decay=0.01)
+        for c, _ in ranks:
+            c.p2p_gather()
+        gsum = gs[0].clone()
+        for g in gs[1:]:
+            gsum += g
+        ref.dM.copy_(gsum)
+        ref.optimizer_step(kind, 1e-2, step=t, weight_decay=0.01, touched_only=True)
+        torch.cuda.synchronize()
+        for c, _ in ranks:
+            assert torch.equal(c.M, ref.M)
+            assert torch.count_nonzero(c.dM).item() == 0
+            for mid in ids[:2]:
+                assert torch.equal(c.materialize(mid, torch.bfloat16), ref.materialize(mid, torch.bfloat16))
+    for c, _ in ranks:
+        c.close()
+    ref.close()
+
+
 def test_p2p_graph_capture_replays_advance_the_epoch(R, torch):
     """post + finish of two ranks captured once and replayed: the epoch and the buffer parity
     live in device memory, so every replay is a new step (same result as eager calls)."""
@@ -168,7 +208,10 @@ _WORKER = textwrap.dedent("""
     ctx.p2p_init()
     for t in (1, 2):
         ctx.dM.copy_(torch.tensor(np.load(out + f"_g{t}_{rank}.npy"), device="cuda"))
-        ctx.exchange_p2p(2, 1e-2, step=t, weight_decay=0.01)
+        if sys.argv[5] == "2":
+            ctx.exchange_p2p2(2, 1e-2, step=t, weight_decay=0.01)
+        else:
+            ctx.exchange_p2p(2, 1e-2, step=t, weight_decay=0.01)
     torch.cuda.synchronize()
     np.save(out + f"_M_{rank}.npy", ctx.M.cpu().numpy())
     ctx.check()
@@ -178,7 +221,8 @@ _WORKER = textwrap.dedent("""
 """)
 
 
-def test_p2p_two_processes_through_cuda_ipc(R, torch, tmp_path):
+@pytest.mark.parametrize("shots", ["1", "2"])
+def test_p2p_two_processes_through_cuda_ipc(R, torch, tmp_path, shots):
     """Two processes on one GPU, windows mapped with cudaIpcOpenMemHandle after a gloo
     all_gather of the handles (what p2p_init does on a node): both end with the single-handle
     update of the summed gradient, bit for bit."""
@@ -195,9 +239,9 @@ def test_p2p_two_processes_through_cuda_ipc(R, torch, tmp_path):
     torch.cuda.synchronize()
     script = tmp_path / "worker.py"
     script.write_text(_WORKER)
-    port = str(29500 + os.getpid() % 1000)
+    port = str(29500 + os.getpid() % 1000 + int(shots))
     env = dict(os.environ, PYTHONPATH=os.getcwd())
-    procs = [subprocess.Popen([sys.executable, str(script), str(r), "2", out, port], cwd=os.getcwd(), env=env)
+    procs = [subprocess.Popen([sys.executable, str(script), str(r), "2", out, port, shots], cwd=os.getcwd(), env=env)
              for r in range(2)]
     codes = [p.wait(timeout=300) for p in procs]
     assert codes == [0, 0]

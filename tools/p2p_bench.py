@@ -1,5 +1,6 @@
 """Exchange + update on one B200: NCCL path (roast_grad_exchange_step: pack, all-reduce, update)
-against the one-shot P2P path (roast_grad_exchange_p2p: pack, signal, sum-of-peers + update).
+against the one-shot P2P path (roast_grad_exchange_p2p: pack + signal, sum-of-peers + update) and
+the two-shot one (roast_grad_exchange_p2p2: pack + signal, slice reduce + update, gather).
 
 On one GPU the NCCL all-reduce is a 1-rank no-op, so this measures what each path costs around
 the communication itself; the P2P path at W virtual ranks (W handles in one process attached by
@@ -96,6 +97,13 @@ def main():
                 state = {0: 0, 1: 1, 2: 2}[kind]
                 # algorithmic bytes of one rank's finish: W packed reads + M, state r/w + shadow write
                 byts = n * (4 * W + 8 + 8 * state + 4)
+                def two_shot():
+                    post()
+                    for c in ranks:
+                        c.p2p_reduce(kind, 1e-4, step=1)
+                    for c in ranks:
+                        c.p2p_gather()
+                res[f"p2p2_W{W}_us_per_rank"] = timed(two_shot) / W
                 res[f"p2p_W{W}_us_per_rank"] = t_both
                 res[f"p2p_W{W}_post_us_per_rank"] = t_post / W
                 res[f"p2p_W{W}_finish_us"] = t_fin
