@@ -465,9 +465,14 @@ def run_gpu(args):
     # region.  As in a training input pipeline, step k + 1's inputs are copied on a second
     # stream into the other of two device buffers while step k computes (double-buffered
     # prefetch), so PCIe and the kernels overlap; each step still waits for its own copy.
-    Xh = X.cpu().pin_memory()
-    dY2h = dY2.cpu().pin_memory()
-    dMh = torch.empty(mem, dtype=torch.float32).pin_memory()
+    # pinned staging buffers from the pinned allocator (torch.empty(pin_memory=True)): on these
+    # boxes `X.cpu().pin_memory()` gave host memory that copies at 13 GB/s instead of 54 GB/s
+    # (tools/e2e_probe.py), which had made e2e swing between 150 and 480 TFLOP/s
+    Xh = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
+    Xh.copy_(X)
+    dY2h = torch.empty(dY2.shape, dtype=dY2.dtype, pin_memory=True)
+    dY2h.copy_(dY2)
+    dMh = torch.empty(mem, dtype=torch.float32, pin_memory=True)
     bufs = [(torch.empty_like(X), torch.empty_like(dY2)) for _ in range(2)]
     copy_s = torch.cuda.Stream(device=dev)
     ready = [torch.cuda.Event() for _ in range(2)]
