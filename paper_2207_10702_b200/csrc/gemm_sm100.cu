@@ -78,6 +78,18 @@ struct Cfg {
 
 enum Mode { FWD = 0, DX = 1, DW = 2 };
 
+// Warp roles.  WM = 2 FWD / DX units fill all 512 TMEM columns, so the accumulator is single-
+// buffered and the next unit's MMAs wait for its drain.  There (RF = true) eight epilogue warps
+// (two per TMEM lane quadrant, one per M sub-tile) copy the accumulator into registers as packed
+// bf16 — 128 x 32-bit per thread — release TMEM, and only then stage and TMA-store the tile while
+// the next unit's MMAs run; setmaxnreg moves registers from the producer / MMA warpgroup to them.
+template <int MODE, int CG, int WM>
+struct Roles {
+  static constexpr bool RF = MODE != DW && WM == 2 && CG == 2;
+  static constexpr int EPI_WARPS = RF ? 8 : 4;
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
+};
+
 #ifdef ROAST_DIAG
 #define DIAG(p) ((p).exp)
 #else
@@ -286,7 +298,7 @@ __device__ __forceinline__ void decode_unit(const Params& p, int u, int& mb, int
 
 // ---------------------------------------------------------------- the kernel
 template <int MODE, int CG, int WM, bool CHAIN = false, int NU = BN>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
     roast_mm_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ WMaps wmaps,
                    const __grid_constant__ Params p0, const __grid_constant__ CUtensorMap mapA1,
@@ -294,6 +306,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                    const __grid_constant__ WMapsHalf hmaps) {
   static_assert(NU == BN || (NU == 192 && MODE != DW && CG == 2 && WM == 2 && !CHAIN), "NU = 192: FWD / DX, 2 x 2");
   using C = Cfg<CG, WM, NU>;
+  constexpr bool RF = Roles<MODE, CG, WM>::RF;
+  constexpr int EPI_WARPS = Roles<MODE, CG, WM>::EPI_WARPS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                        // [STAGES][A_BYTES]
@@ -343,7 +357,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4 * CG);
+      mbar_init(&tempty[a], EPI_WARPS * CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_map(&mapA);
@@ -367,12 +381,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   else
     __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  // TMEM base address: re-read from smem where used, so no register stays live across the
+  // setmaxnreg role branches
+  auto tmem_base_ld = [&]() -> uint32_t { return *reinterpret_cast<volatile uint32_t*>(tmem_slot); };
   // the previous kernel on this stream (launched before us with PDL) has completed and its
   // writes are visible from here on; everything above touched only smem / TMEM / descriptors
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
+  // RF: registers move from warpgroup 0 (producer, MMA, TMEM allocator, idle) to the eight
+  // epilogue warps: 128 x 56 + 256 x 224 = 64512 = 384 x 168.  Each role branch executes its own
+  // setmaxnreg so ptxas allocates every branch under its own budget.
   if (warp == 0) {
+    if constexpr (RF) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     // ===================== TMA producer (warp 0, both CTAs) =====================
     // Per work unit the whole warp stages the unit's packed tile coordinates
     // (k-blocks x 4, FWD/DX) into smem with coalesced loads; lane 0 then walks
@@ -435,7 +455,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 tma_load_2d<CG>(&mapB, b + (j - j0) * 8192, fb, nb * BN + j * 64, kb * BK);
             } else {
               // chain: these 64 columns of A are problem 0's output tile (mb, kb / 4)
-              if (CHAIN && prob == 1 && (kb & 3) == 0) wait_ready(p0.flags + mb * p0.n_tiles + (kb >> 2), 4 * CG);
+              if (CHAIN && prob == 1 && (kb & 3) == 0) wait_ready(p0.flags + mb * p0.n_tiles + (kb >> 2), EPI_WARPS * CG);
               if (!(DIAG(p) & 32)) tma_load_2d<CG>(mA, a, fb, kb * BK, row0);
               const int32_t* cc = sCoord + (kb - kc) * 4;
               if (MODE == FWD && NU == 192 && !(DIAG(p) & 16)) {
@@ -480,6 +500,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
+    if constexpr (RF) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     if (lane == 0 && leader) {
       // ===================== MMA issuer (leader CTA, single thread) =====================
       constexpr uint32_t idesc = make_idesc(MODE == DW ? 1 : 0, MODE == FWD || MODE == DW ? 1 : 0, BM * CG, NU);
@@ -500,7 +521,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&tempty[acc], aph ^ 1);
         if (p.prof) prof_acc[2] += clock64() - tw1;
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+        const uint32_t d_tmem = tmem_base_ld() + uint32_t(acc * BN);
         for (int kb = kb0; kb < kb1; ++kb) {
           long long tw2 = p.prof ? clock64() : 0;
           mbar_wait(&full[s], ph);
@@ -534,7 +555,113 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (acc == 0) aph ^= 1;
       }
     }
-  } else if (warp >= EPI_WARP0) {
+  } else if (RF && warp < EPI_WARP0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");   // warps 2, 3
+  } else if (RF && warp >= EPI_WARP0) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    // ===================== epilogue, register-held (WM = 2 FWD / DX) =====================
+    // Warp (q, jh) owns accumulator rows q*32 + lane of M sub-tile jh: NU fp32 columns.
+    // Phase A: TMEM -> lambda (+ bias) -> packed bf16 in pk[], then release TMEM to the MMA
+    // warp.  Phase B: pk[] -> SW128 staging (4 KB, one per warp) -> TMA store, 64 columns at a
+    // time, overlapping the next unit's MMAs.
+    const int q = warp & 3;
+    const int jh = (warp - EPI_WARP0) >> 2;
+    uint8_t* buf = sStage + (warp - EPI_WARP0) * 4096;
+    const uint32_t tempty_leader0 = map_to_rank(smem_u32(&tempty[0]), 0);
+    uint32_t aph = 0;
+    for (int it = 0;; ++it) {
+      int prob, u;
+      if (!unit_at(it, prob, u)) break;
+      const Params& p = (CHAIN && prob) ? p1 : p0;
+      const CUtensorMap* mO = (CHAIN && prob) ? &mapOut1 : &mapOut;
+      int mb, nb, split;
+      decode_unit(p, u, mb, nb, split);
+      const int nsteps = (DIAG(p) & 1) ? 0 : min(NU, p.N - nb * NU) / 64;
+      long long tw3 = p.prof ? clock64() : 0;
+      mbar_wait(&tfull[0], aph);
+      long long tw4 = p.prof ? clock64() : 0;
+      if (p.prof) prof_acc[3] += tw4 - tw3;
+      tc_fence_after();
+      const uint32_t tbase = tmem_base_ld() + uint32_t(jh * 256) + (uint32_t(q * 32) << 16);
+      uint32_t pk[NU / 2];
+#pragma unroll
+      for (int c = 0; c < NU / 64; ++c) {
+        if (c < nsteps) {
+          uint32_t r[64];
+          if (MODE == FWD && NU == 192) {   // output step c from the permuted accumulator columns
+            const uint32_t lo = c == 0 ? 0u : c == 1 ? 160u : 96u, hi = c == 0 ? 32u : c == 1 ? 64u : 128u;
+            TMEM_LD32(tbase + lo, r);
+            TMEM_LD32(tbase + hi, (r + 32));
+          } else {
+            TMEM_LD32(tbase + uint32_t(c * 64), r);
+            TMEM_LD32(tbase + uint32_t(c * 64 + 32), (r + 32));
+          }
+          tmem_wait_ld();
+          if (MODE == FWD && p.bias) {   // Y = bf16(lambda acc + b)
+            const float4* b4 = reinterpret_cast<const float4*>(p.bias + nb * NU + c * 64);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float4 bv = __ldg(b4 + i);
+              __nv_bfloat162 v0 = __floats2bfloat162_rn(fmaf(p.lam, __uint_as_float(r[4 * i]), bv.x),
+                                                        fmaf(p.lam, __uint_as_float(r[4 * i + 1]), bv.y));
+              __nv_bfloat162 v1 = __floats2bfloat162_rn(fmaf(p.lam, __uint_as_float(r[4 * i + 2]), bv.z),
+                                                        fmaf(p.lam, __uint_as_float(r[4 * i + 3]), bv.w));
+              pk[c * 32 + 2 * i] = *reinterpret_cast<uint32_t*>(&v0);
+              pk[c * 32 + 2 * i + 1] = *reinterpret_cast<uint32_t*>(&v1);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              __nv_bfloat162 v = __floats2bfloat162_rn(p.lam * __uint_as_float(r[2 * i]),
+                                                       p.lam * __uint_as_float(r[2 * i + 1]));
+              pk[c * 32 + i] = *reinterpret_cast<uint32_t*>(&v);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader0);
+      aph ^= 1;
+      if (p.prof) prof_epi[0] += clock64() - tw4;
+      const int row0 = mb * BM * CG * WM + int(rank) * BM * WM + jh * BM + q * 32;
+#pragma unroll
+      for (int c = 0; c < NU / 64; ++c) {
+        if (c < nsteps) {
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            const uint32_t a = smem_u32(buf + lane * 128 + ((cc ^ (lane & 7)) << 4));
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pk[c * 32 + 4 * cc]),
+                         "r"(pk[c * 32 + 4 * cc + 1]), "r"(pk[c * 32 + 4 * cc + 2]), "r"(pk[c * 32 + 4 * cc + 3])
+                         : "memory");
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0 && !(DIAG(p) & 64)) {
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                             reinterpret_cast<uint64_t>(mO)),
+                         "r"(nb * NU + c * 64), "r"(row0), "r"(smem_u32(buf))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+      }
+      if (p.prof) prof_acc[4] += clock64() - tw4;
+      if (CHAIN && prob == 0) {
+        // publish this warp's 32 rows of the problem-0 tile: writes complete, then release
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p0.flags + u) : "memory");
+        }
+        __syncwarp();
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+  } else if (!RF && warp >= EPI_WARP0) {
     // ===================== epilogue: TMEM -> registers -> global =====================
     const int q = warp & 3;          // TMEM lane quadrant this warp may access
     const int row = q * 32 + lane;   // accumulator row owned by this thread
@@ -574,7 +701,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 1
       for (int j = 0; j < WM; ++j) {
         const int row_base = mb * BM * CG * WM + int(rank) * BM * WM + j * BM;
-        const uint32_t tbase = tmem_base + uint32_t(acc * BN + j * 256) + (uint32_t(q * 32) << 16);
+        const uint32_t tbase = tmem_base_ld() + uint32_t(acc * BN + j * 256) + (uint32_t(q * 32) << 16);
         // Each step drains 32 rows x 128 B of output through a 4 KB SW128-swizzled
         // staging buffer (conflict-free st.shared) and one TMA bulk tensor op:
         // FWD/DX store 64 bf16 columns of Y / dX; DW stores (deterministic
@@ -731,8 +858,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
       o[3] = (long long)(g_end - g_start);   // ns
     }
-    if (warp == 1) { o[1] = prof_acc[1]; }
-    if (warp == EPI_WARP0) { o[4] = prof_acc[4]; o[6] = prof_epi[0]; o[7] = prof_epi[1]; o[2] = prof_epi[2]; o[0] = prof_epi[3]; }
+    if (warp == 1) { o[1] = prof_acc[1]; if (RF) o[0] = prof_acc[2]; }   // RF: slot 0 = MMA wait for TMEM
+    if (warp == EPI_WARP0) { o[4] = prof_acc[4]; o[6] = prof_epi[0]; o[7] = prof_epi[1]; o[2] = prof_epi[2]; if (!RF) o[0] = prof_epi[3]; }
   }
   tc_fence_before();
   if (CG == 2)
@@ -742,9 +869,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   if (warp == 2) {
     if (CG == 1)
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_ld()), "r"(TMEM_COLS));
     else
-      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_ld()), "r"(TMEM_COLS));
   }
 }
 
@@ -830,7 +957,7 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
   const int pairs = grid_pairs > 0 ? grid_pairs : std::min(p.units, num_sms() / CG);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(pairs * CG));
-  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.blockDim = dim3(Roles<MODE, CG, WM>::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
@@ -866,6 +993,12 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
       mx = std::max(mx, prof[i * 8 + 5]);
     }
     const int n = pairs * CG, nl = (pairs * CG + CG - 1) / CG;
+    if (Roles<MODE, CG, WM>::RF)   // register-held epilogue: slot 0 = MMA wait for TMEM, 6 = TMEM->RF phase
+      fprintf(stderr, "[roast prof] RF wm %d mode %d nu %d units %d kb %d | total %.0f (max %lld) | mma wait-tmem %.0f "
+              "mma wait-full %.0f | %.0f MHz | epi busy %.0f (tmem->rf %.0f)  (cycles, mean/CTA)\n",
+              WM, MODE, NU, p.units, p.k_blocks, acc[5] / n, mx, acc[0] / nl, acc[1] / nl,
+              acc[5] / (acc[3] > 0 ? acc[3] : 1) * 1e3, acc[4] / n, acc[6] / n);
+    else
     fprintf(stderr, "[roast prof] dw3d %d wm %d mode %d cg %d units %d kb %d | total %.0f (max %lld) | epi-fence %.0f | "
             "mma wait-full %.0f epi-sts %.0f | %.0f MHz | epi busy %.0f (tmem %.0f, stg-wait %.0f)  (cycles, mean/CTA)\n",
             p.dw3d, WM, MODE, CG, p.units, p.k_blocks, acc[5] / n, mx, acc[0] / n, acc[1] / nl, acc[2] / nl, acc[5] / (acc[3] > 0 ? acc[3] : 1) * 1e3,
