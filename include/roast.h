@@ -60,7 +60,8 @@ typedef enum {
   ROAST_ERR_STATE = 6,     /* not bound, unknown module id, comm not initialised, ...          */
   ROAST_ERR_CUDA = 7,      /* a CUDA runtime / driver call failed                              */
   ROAST_ERR_NCCL = 8,      /* an NCCL call failed or libnccl could not be loaded               */
-  ROAST_ERR_UNSUPPORTED = 9 /* valid request with no kernel for it (e.g. bf16 with Z2 != 64)   */
+  ROAST_ERR_UNSUPPORTED = 9 /* valid request with no kernel for it (bf16 off the tcgen05 path  */
+                            /* without roast_config_t.simt_bf16)                               */
 } roast_status_t;
 
 typedef struct roast_ctx* roast_t;
@@ -85,6 +86,9 @@ typedef struct {
   int32_t mapping;       /* roast_mapping_t; IDENTITY = no sharing, lambda 1, g +1 (test mode)        */
   int32_t use_sign;      /* 1 = multiply by g, default 1                                       */
   int32_t deterministic; /* 1 = dM accumulated in a fixed order, bitwise reproducible (default 0)     */
+  int32_t simt_bf16;     /* bf16 linears the tcgen05 path cannot take (tile != 64 x 64, SW128 layout, */
+                         /* A % 8 != 0, tokens >= 2^31): 0 (default) = ROAST_ERR_UNSUPPORTED; 1 = run  */
+                         /* them on the SIMT FFMA kernels (HashedNet 1 x 1 tiles, C1's 32 x 32 tiles) */
 } roast_config_t;
 
 /* Fill *cfg with the defaults listed above. */
@@ -129,6 +133,16 @@ roast_status_t roast_register_linear_seg(roast_t h, int64_t in_features, int64_t
                                          int64_t seg_size, int32_t* id);
 roast_status_t roast_register_embedding_seg(roast_t h, int64_t num_rows, int32_t dim, int32_t chunk,
                                             double fan_in, int64_t seg_base, int64_t seg_size, int32_t* id);
+
+/* LMS partition ("each layer will have independent compressed memory", P:330 f_i =
+ * n_i / n, sum |M_i| = |M|; reading R14/R23): piece i of the n modules, sizes[i] virtual
+ * parameters each, gets |M_i| = floor(sizes[i] |M| / sum sizes) rounded down to a multiple of
+ * `align` (so every base stays A-aligned), the last piece the remainder; bases are contiguous
+ * from 0.  Pure host function (no handle, no GPU).  seg_base / seg_size: caller-owned host
+ * arrays of n entries, written on success.  A tiny module may get size 0 (registering it then
+ * fails with GEOMETRY).  Errors: CONFIG (n < 1, a size < 1, mem_size < 1, align < 1, null). */
+roast_status_t roast_lms_segments(const int64_t* sizes, int32_t n, int64_t mem_size, int32_t align,
+                                  int64_t* seg_base, int64_t* seg_size);
 
 /* Fuse already-registered linears that share in_features into one GEMM along out_features
  * (e.g. BERT's Q, K, V projections of the same input): the group's virtual weight is
@@ -219,6 +233,11 @@ roast_status_t roast_bias_bwd_ld(roast_t h, int32_t bias_id, const void* d_dY, i
  * table) instead of one L backward per bias. */
 roast_status_t roast_colsum(const void* d_dY, int64_t tokens, int32_t n, int64_t ld, roast_dtype_t dt, float* d_db,
                             roast_stream_t stream);
+/* As roast_colsum, but db[j] += sum_t dY[t, j] (accumulate != 0) instead of overwriting: a
+ * bias whose layer runs backward more than once before the scatter (gradient accumulation
+ * over micro-batches, a module applied twice) keeps every contribution. */
+roast_status_t roast_colsum_ex(const void* d_dY, int64_t tokens, int32_t n, int64_t ld, roast_dtype_t dt, float* d_db,
+                               int32_t accumulate, roast_stream_t stream);
 
 /* a2 + a3: dX = lambda * dY W~^T (skipped if d_dX == NULL), and
  * dM[h(x,y) + pi(o1,o2)] += lambda * g(x,y) * (X^T dY)[i, j] for every virtual
@@ -415,6 +434,11 @@ roast_status_t roast_debug_chunk_map(roast_t h, int32_t id, const int64_t* d_row
  * dt = BF16: g * bf16(M) read from the shadow (the tensor-core operand, lambda deferred). */
 roast_status_t roast_debug_materialize(roast_t h, int32_t id, roast_dtype_t dt, void* d_W,
                                        roast_stream_t stream);
+
+/* Test hook: copy the optimizer state of roast_optimizer_step to the host.  which = 0: the
+ * first state array (Adagrad G, Adam m), 1: the second (Adam v); out_host: mem_size fp32.
+ * Synchronous.  Errors: STATE (not bound, or that state was never allocated). */
+roast_status_t roast_debug_opt_state(roast_t h, int32_t which, float* out_host);
 /* Evaluate the library's hash (the same __host__ __device__ code the kernels run,
  * including the reciprocal `mod R`) on the HOST for n keys of module `module`:
  * off_out[i] = A * (poly(key) mod R), R = floor((mem_size - span)/align) + 1, and

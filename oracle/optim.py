@@ -14,6 +14,12 @@ P:749-813); it gives no formulas of its own, so the oracle writes out the standa
 Pinned by tests/test_oracle_optim.py: one SGD step on a quadratic reduces to the
 closed form; Adam's first step moves every coordinate by lr * sign(g) (bias-corrected
 m / sqrt(v) = g / |g|, up to eps); Adagrad's first step likewise by lr * g / (|g| + eps).
+The recurrences with carried state (t >= 2) are pinned by hand-derived exact values for
+the scalar gradient sequence (1, -2, 3) (Adam with b1 = 1/2, b2 = 3/4; Adagrad), the
+Adagrad constant-gradient closed form sum 1/sqrt(s), three SGD steps on a quadratic, and
+torch.optim (a second, independent implementation) over five steps with weight decay.
+Dropping Adam's b1 m / b2 v decay, not carrying Adagrad's G, or a t >= 2 bias-correction
+slip each fails a pin.
 """
 from __future__ import annotations
 

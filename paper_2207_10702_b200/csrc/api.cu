@@ -24,16 +24,12 @@ roast_status_t cuda_fail(cudaError_t e, const char* what) {
   return fail(ROAST_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-roast_status_t ensure_ws(Ctx* c, size_t bytes, cudaStream_t s) {
-  if (c->ws_bytes >= bytes) return ROAST_OK;
-  if (c->ws) ROAST_CUDA_CHECK(cudaFreeAsync(c->ws, s));
-  c->ws = nullptr;
-  c->ws_bytes = 0;
-  ROAST_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&c->ws), bytes, s));
-  c->ws_bytes = bytes;
-  // test hook: fill a new workspace with NaN (0xFFFFFFFF) so any slot a reader consumes
-  // before a kernel wrote it poisons the result (tests/test_gpu_parity.py, poisoned-workspace test)
-  if (getenv("ROAST_POISON_WS")) ROAST_CUDA_CHECK(cudaMemsetAsync(c->ws, 0xFF, bytes, s));
+roast_status_t scratch_alloc(Scratch& w, size_t bytes, cudaStream_t s) {
+  w.s = s;
+  ROAST_CUDA_CHECK(cudaMallocAsync(&w.p, bytes, s));
+  // test hook: fill new scratch with NaN (0xFFFFFFFF) so any slot a reader consumes before a
+  // kernel wrote it poisons the result (tests/test_gpu_parity.py, poisoned-workspace test)
+  if (getenv("ROAST_POISON_WS")) ROAST_CUDA_CHECK(cudaMemsetAsync(w.p, 0xFF, bytes, s));
   return ROAST_OK;
 }
 
@@ -147,6 +143,7 @@ void roast_config_default(roast_config_t* cfg) {
   cfg->mapping = ROAST_MAP_HASH;
   cfg->use_sign = 1;
   cfg->deterministic = 0;
+  cfg->simt_bf16 = 0;
 }
 
 const char* roast_status_str(roast_status_t st) {
@@ -198,6 +195,15 @@ roast_status_t roast_create_ex(roast_t* out, int64_t mem_size, uint64_t seed, ro
     return cuda_fail(e, "cudaMalloc(err flag)");
   }
   cudaMemset(c->d_err, 0, 16);
+  {   // per-call scratch comes from the default pool: keep up to 1 GiB of freed blocks cached
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = uint64_t(1) << 30, cur = 0;
+      if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur) == cudaSuccess && cur < keep)
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   c->d_zero_idx = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(c->d_err) + 8);
   *out = reinterpret_cast<roast_t>(c);
   return ROAST_OK;
@@ -215,11 +221,9 @@ roast_status_t roast_destroy(roast_t h) {
   for (auto& m : c->groups) free_module(m);
   cudaFree(c->shadow);
   cudaFree(c->d_err);
-  cudaFree(c->ws);
   cudaFree(c->opt_s1);
   cudaFree(c->opt_s2);
   for (auto& kv : c->chain_plans) cudaFree(kv.second.first);
-  cudaFree(c->chain_flags);
   cudaFree(c->d_iv);
   cudaFree(c->d_pack);
   comm_destroy(c);
@@ -404,6 +408,16 @@ static bool use_sm100(const Ctx* c, const Module& m) {
          getenv("ROAST_FORCE_SIMT") == nullptr;
 }
 
+// A bf16 call the tcgen05 path did not take runs on the SIMT kernels only if the handle opted in
+// (roast_config_t.simt_bf16, or the ROAST_FORCE_SIMT diagnostic); otherwise it is an error, not
+// a silent second backend.  fp32 calls always use the SIMT kernels (the fp32 path).
+static roast_status_t simt_allowed(const Ctx* c, roast_dtype_t dt) {
+  if (dt != ROAST_BF16 || c->cfg.simt_bf16 || getenv("ROAST_FORCE_SIMT")) return ROAST_OK;
+  return fail(ROAST_ERR_UNSUPPORTED,
+              "bf16 linear off the tcgen05 path (needs 64x64 row-major tiles, A % 8 == 0, tokens < 2^31); "
+              "set roast_config_t.simt_bf16 = 1 to run it on the SIMT kernels");
+}
+
 roast_status_t roast_linear_fwd(roast_t h, int32_t id, const void* X, void* Y, int64_t T, roast_dtype_t dt,
                                 roast_stream_t stream) {
   return roast_linear_fwd_bias(h, id, X, Y, T, dt, nullptr, stream);
@@ -425,6 +439,7 @@ roast_status_t roast_linear_fwd_bias(roast_t h, int32_t id, const void* X, void*
     st = sm100_fwd(c, *m, X, Y, T, bias, s);
     if (st != ROAST_ERR_UNSUPPORTED) return st;
   }
+  if ((st = simt_allowed(c, dt))) return st;
   ROAST_CUDA_CHECK(launch_simt_fwd(c, *m, X, Y, T, dt, false, s, bias));
   c->launches++;
   return ROAST_OK;
@@ -492,6 +507,11 @@ roast_status_t roast_bias_bwd(roast_t h, int32_t bias_id, const void* dY, int64_
 
 roast_status_t roast_colsum(const void* dY, int64_t T, int32_t n, int64_t ld, roast_dtype_t dt, float* db,
                             roast_stream_t stream) {
+  return roast_colsum_ex(dY, T, n, ld, dt, db, 0, stream);
+}
+
+roast_status_t roast_colsum_ex(const void* dY, int64_t T, int32_t n, int64_t ld, roast_dtype_t dt, float* db,
+                               int32_t accumulate, roast_stream_t stream) {
   if (T < 0 || n <= 0) return fail(ROAST_ERR_SHAPE, "tokens < 0 or n <= 0");
   if (dt != ROAST_FP32 && dt != ROAST_BF16) return fail(ROAST_ERR_CONFIG, "bad dtype");
   if (ld < 0) ld = n;
@@ -499,14 +519,14 @@ roast_status_t roast_colsum(const void* dY, int64_t T, int32_t n, int64_t ld, ro
   if (!db || (reinterpret_cast<uintptr_t>(db) & 7)) return fail(ROAST_ERR_CONFIG, "db must be 8-byte aligned");
   const cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (T == 0) {
-    ROAST_CUDA_CHECK(cudaMemsetAsync(db, 0, size_t(n) * sizeof(float), s));
+    if (!accumulate) ROAST_CUDA_CHECK(cudaMemsetAsync(db, 0, size_t(n) * sizeof(float), s));
     return ROAST_OK;
   }
   if (!dY || (reinterpret_cast<uintptr_t>(dY) & 7)) return fail(ROAST_ERR_CONFIG, "dY must be 8-byte aligned");
   const int slabs = colsum_slabs(T, n);
   float* tmp = nullptr;   // stream-ordered scratch for the slab partials (capturable)
   ROAST_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), size_t(slabs) * n * sizeof(float), s));
-  cudaError_t e = launch_colsum(dY, T, n, ld, dt, tmp, db, s);
+  cudaError_t e = launch_colsum(dY, T, n, ld, dt, tmp, db, s, accumulate ? 1 : 0);
   cudaFreeAsync(tmp, s);
   if (e != cudaSuccess) return cuda_fail(e, "column sum");
   return ROAST_OK;
@@ -572,6 +592,7 @@ roast_status_t roast_linear_bwd_dx(roast_t h, int32_t id, const void* dY, void* 
     st = sm100_dx(c, *m, dY, dX, T, s);
     if (st != ROAST_ERR_UNSUPPORTED) return st;
   }
+  if ((st = simt_allowed(c, dt))) return st;
   ROAST_CUDA_CHECK(launch_simt_fwd(c, *m, dY, dX, T, dt, true, s, nullptr));
   c->launches++;
   return ROAST_OK;
@@ -589,12 +610,13 @@ roast_status_t roast_linear_bwd_dm(roast_t h, int32_t id, const void* X, const v
     st = sm100_dw(c, *m, X, dY, T, s);
     if (st != ROAST_ERR_UNSUPPORTED) return st;
   }
+  if ((st = simt_allowed(c, dt))) return st;
   if (c->cfg.deterministic) {
     const size_t bytes = size_t(m->nx) * m->ny * c->tile.z1 * c->tile.z2 * sizeof(float);
-    st = ensure_ws(c, bytes, s);
-    if (st) return st;
-    ROAST_CUDA_CHECK(launch_simt_dw(c, *m, X, dY, T, dt, c->ws, s));
-    ROAST_CUDA_CHECK(launch_det_reduce(c, *m, c->ws, 1, s));
+    Scratch ws;
+    if ((st = scratch_alloc(ws, bytes, s))) return st;
+    ROAST_CUDA_CHECK(launch_simt_dw(c, *m, X, dY, T, dt, ws.as<float>(), s));
+    ROAST_CUDA_CHECK(launch_det_reduce(c, *m, ws.as<float>(), 1, s));
     c->launches += 2;
   } else {
     ROAST_CUDA_CHECK(launch_simt_dw(c, *m, X, dY, T, dt, nullptr, s));
@@ -766,6 +788,9 @@ roast_status_t roast_get_error(roast_t h) {
   cudaError_t e = cudaMemcpy(&v, c->d_err, sizeof(v), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "read error flag");
   if (v & 2) return fail(ROAST_ERR_STATE, "p2p exchange: a peer did not post within 20 s (sticky)");
+  if (v & 4)
+    return fail(ROAST_ERR_STATE, "chained GEMM: a ready-counter wait timed out (grid not co-resident?); "
+                                 "its outputs are invalid (sticky)");
   if (v) return fail(ROAST_ERR_BOUNDS, "embedding index out of range (sticky)");
   return ROAST_OK;
 }
@@ -801,6 +826,38 @@ roast_status_t roast_debug_materialize(roast_t h, int32_t id, roast_dtype_t dt, 
   if (st) return st;
   ROAST_CUDA_CHECK(launch_materialize(c, *m, dt, W, reinterpret_cast<cudaStream_t>(stream)));
   c->launches++;
+  return ROAST_OK;
+}
+
+roast_status_t roast_debug_opt_state(roast_t h, int32_t which, float* out_host) {
+  Ctx* c = ctx(h);
+  if (!c || !c->M) return fail(ROAST_ERR_STATE, "not bound");
+  const float* src = which == 0 ? c->opt_s1 : which == 1 ? c->opt_s2 : nullptr;
+  if (!src) return fail(ROAST_ERR_STATE, "optimizer state not allocated");
+  if (!out_host) return fail(ROAST_ERR_CONFIG, "null output");
+  ROAST_CUDA_CHECK(cudaDeviceSynchronize());
+  ROAST_CUDA_CHECK(cudaMemcpy(out_host, src, size_t(c->mem_size) * sizeof(float), cudaMemcpyDeviceToHost));
+  return ROAST_OK;
+}
+
+roast_status_t roast_lms_segments(const int64_t* sizes, int32_t n, int64_t mem_size, int32_t align,
+                                  int64_t* seg_base, int64_t* seg_size) {
+  if (!sizes || !seg_base || !seg_size || n < 1 || mem_size < 1 || align < 1)
+    return fail(ROAST_ERR_CONFIG, "lms_segments: bad arguments");
+  __int128 total = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    if (sizes[i] < 1) return fail(ROAST_ERR_CONFIG, "lms_segments: module sizes must be >= 1");
+    total += sizes[i];
+  }
+  int64_t base = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    // |M_i| = floor(f_i |M|), f_i = n_i / n, aligned down to A; the last piece takes the rest
+    const int64_t size = i + 1 == n ? mem_size - base
+                                    : int64_t((__int128(sizes[i]) * mem_size) / total) / align * align;
+    seg_base[i] = base;
+    seg_size[i] = size;
+    base += size;
+  }
   return ROAST_OK;
 }
 

@@ -136,6 +136,7 @@ struct Params {
   const int32_t* sched;
   int sched_len;
   int* flags;
+  int* err;             // sticky device error word (chain wait timeout, bit 2)
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -277,13 +278,19 @@ __host__ __device__ constexpr uint32_t make_idesc(int a_mn_major, int b_mn_major
          (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
 }
 
-// spin until *flag >= target (acquire), then order the async proxy (TMA loads) after it
-__device__ __forceinline__ void wait_ready(const int* flag, int target) {
+// spin until *flag >= target (acquire), then order the async proxy (TMA loads) after it.
+// After ~4 s (a grid that is not co-resident, e.g. SMs held by another process) it gives up:
+// sets bit 2 of the sticky error word (roast_get_error -> ROAST_ERR_STATE, outputs invalid) and
+// proceeds, so every CTA still terminates and the context stays usable.
+__device__ __forceinline__ void wait_ready(const int* flag, int target, int* err) {
   int v;
   for (uint32_t spins = 0;; ++spins) {
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
     if (v >= target) break;
-    if (spins > (1u << 26)) __trap();   // ~4 s: a broken schedule fails loudly instead of hanging
+    if (spins > (1u << 26)) {
+      if (err) atomicOr(err, 4);
+      break;
+    }
     __nanosleep(64);
   }
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -455,7 +462,7 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
                 tma_load_2d<CG>(&mapB, b + (j - j0) * 8192, fb, nb * BN + j * 64, kb * BK);
             } else {
               // chain: these 64 columns of A are problem 0's output tile (mb, kb / 4)
-              if (CHAIN && prob == 1 && (kb & 3) == 0) wait_ready(p0.flags + mb * p0.n_tiles + (kb >> 2), EPI_WARPS * CG);
+              if (CHAIN && prob == 1 && (kb & 3) == 0) wait_ready(p0.flags + mb * p0.n_tiles + (kb >> 2), EPI_WARPS * CG, p0.err);
               if (!(DIAG(p) & 32)) tma_load_2d<CG>(mA, a, fb, kb * BK, row0);
               const int32_t* cc = sCoord + (kb - kc) * 4;
               if (MODE == FWD && NU == 192 && !(DIAG(p) & 16)) {
@@ -1295,21 +1302,39 @@ roast_status_t sm100_chain(Ctx* c, const Module& m0, const Module& m1, const voi
       return ROAST_ERR_UNSUPPORTED;   // planning allocates; plan on an eager call first
     ChainPlan plan = plan_chain(m_tiles, nt0, K0 / BK, nt1, K1 / BK, pairs);
     int32_t* d = nullptr;
-    if (plan.makespan < 0.97 * plan.sequential) {
+    // the waits assume every CTA pair of the grid is resident at once: chain only if the
+    // device can hold all `pairs` clusters of this kernel together
+    bool resident = false;
+    {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(unsigned(2 * pairs));
+      q.blockDim = dim3(Roles<FWD, 2, WMC>::THREADS);
+      q.dynamicSmemBytes = Cfg<2, WMC>::SMEM;
+      cudaLaunchAttribute a[1];
+      a[0].id = cudaLaunchAttributeClusterDimension;
+      a[0].val.clusterDim.x = 2;
+      a[0].val.clusterDim.y = 1;
+      a[0].val.clusterDim.z = 1;
+      q.attrs = a;
+      q.numAttrs = 1;
+      auto kfn = dx ? roast_mm_sm100<DX, 2, WMC, true> : roast_mm_sm100<FWD, 2, WMC, true>;
+      int nclusters = 0;
+      if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<2, WMC>::SMEM) == cudaSuccess &&
+          cudaOccupancyMaxActiveClusters(&nclusters, kfn, &q) == cudaSuccess)
+        resident = nclusters >= pairs;
+      cudaGetLastError();
+    }
+    if (resident && plan.makespan < 0.97 * plan.sequential) {
       ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&d), plan.sched.size() * sizeof(int32_t)));
       ROAST_CUDA_CHECK(cudaMemcpy(d, plan.sched.data(), plan.sched.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
     it = c->chain_plans.emplace(key, std::make_pair(d, plan.len)).first;
-    const int64_t need = int64_t(m_tiles) * nt0;
-    if (d && c->chain_flags_n < need) {
-      cudaFree(c->chain_flags);
-      c->chain_flags = nullptr;
-      c->chain_flags_n = 0;
-      ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->chain_flags), need * sizeof(int)));
-      c->chain_flags_n = need;
-    }
   }
   if (!it->second.first) return ROAST_ERR_UNSUPPORTED;
+  // the ready counters of problem 0's tiles: per-call scratch (Scratch), so chained launches on
+  // different streams never share them
+  Scratch fl;
+  if (roast_status_t e = scratch_alloc(fl, size_t(m_tiles) * nt0 * sizeof(int), s)) return e;
   roast_status_t st = sm100_prepare(c);
   if (st) return st;
   auto prob = [&](const Module& m, const void* A, void* out, int N, int K, bool is_dx, const float* bias, Params& p,
@@ -1340,8 +1365,9 @@ roast_status_t sm100_chain(Ctx* c, const Module& m0, const Module& m1, const voi
   p0.chain = 1;
   p0.sched = it->second.first;
   p0.sched_len = it->second.second;
-  p0.flags = c->chain_flags;
-  ROAST_CUDA_CHECK(cudaMemsetAsync(c->chain_flags, 0, size_t(p0.units) * sizeof(int), s));
+  p0.flags = fl.as<int>();
+  p0.err = c->d_err;
+  ROAST_CUDA_CHECK(cudaMemsetAsync(fl.p, 0, size_t(p0.units) * sizeof(int), s));
   const WMaps& w = *reinterpret_cast<const WMaps*>(c->tmap_shadow);
   st = dx ? launch_cg<DX, 2, WMC, true>(a0, a0, o0, w, p0, a1, o1, p1, pairs, s)
           : launch_cg<FWD, 2, WMC, true>(a0, a0, o0, w, p0, a1, o1, p1, pairs, s);
@@ -1413,10 +1439,11 @@ static roast_status_t dw_launch(Ctx* c, const Module& m, const void* X, const vo
   p.units = tiles * splits;
   p.dM = c->dM;
   const bool det = c->cfg.deterministic != 0;
+  Scratch ws;   // deterministic: per-tile partials, freed (stream-ordered) after the reduce
   if (det) {
-    st = ensure_ws(c, size_t(splits) * p.ntiles * 4096 * sizeof(float), s);
+    st = scratch_alloc(ws, size_t(splits) * p.ntiles * 4096 * sizeof(float), s);
     if (st) return st;
-    p.ws = c->ws;
+    p.ws = ws.as<float>();
   }
   // dM viewed as 8 [rows x 64] fp32 tensors, one per 32-byte phase (tile offsets are multiples of A = 8)
   CUtensorMap o;
@@ -1424,7 +1451,7 @@ static roast_status_t dw_launch(Ctx* c, const Module& m, const void* X, const vo
   memset(&o, 0, sizeof(o));
   if (det) {
     const uint64_t rows = uint64_t(splits) * p.ntiles * 64;
-    st = make_map_2d(&o, c->ws, 64, rows, 256, 32, 32, true);
+    st = make_map_2d(&o, p.ws, 64, rows, 256, 32, 32, true);
     if (st) return st;
   } else if (c->tmap_dm_for != c->dM) {   // cached until dM is rebound
     for (int r = 0; r < 8; ++r) {
@@ -1438,7 +1465,7 @@ static roast_status_t dw_launch(Ctx* c, const Module& m, const void* X, const vo
   if (st) return st;
   c->launches++;
   if (det) {
-    cudaError_t e = launch_det_reduce(c, m, c->ws, splits, s);
+    cudaError_t e = launch_det_reduce(c, m, p.ws, splits, s);
     if (e != cudaSuccess) return cuda_fail(e, "det_reduce");
     c->launches++;
   }

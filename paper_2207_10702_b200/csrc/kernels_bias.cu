@@ -69,12 +69,13 @@ __global__ void __launch_bounds__(256) colsum_kernel(const XT* __restrict__ dY, 
   }
 }
 
-__global__ void slab_sum_kernel(const float* __restrict__ partial, int slabs, int n, float* __restrict__ db) {
+__global__ void slab_sum_kernel(const float* __restrict__ partial, int slabs, int n, float* __restrict__ db,
+                                int accumulate) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   float s = 0.f;
   for (int k = 0; k < slabs; ++k) s += partial[int64_t(k) * n + j];
-  db[j] = s;
+  db[j] = accumulate ? db[j] + s : s;
 }
 
 }  // namespace
@@ -87,7 +88,7 @@ int colsum_slabs(int64_t T, int n) {
 }
 
 cudaError_t launch_colsum(const void* dY, int64_t T, int n, int64_t ld, roast_dtype_t dt, float* partial, float* db,
-                          cudaStream_t s) {
+                          cudaStream_t s, int accumulate) {
   const int slabs = colsum_slabs(T, n);
   const int64_t rows = (T + slabs - 1) / slabs;
   dim3 grid(unsigned((n + 63) / 64), unsigned(slabs));
@@ -97,7 +98,7 @@ cudaError_t launch_colsum(const void* dY, int64_t T, int n, int64_t ld, roast_dt
     colsum_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(dY), T, n, ld, rows, partial);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  slab_sum_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(partial, slabs, n, db);
+  slab_sum_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(partial, slabs, n, db, accumulate);
   return cudaGetLastError();
 }
 

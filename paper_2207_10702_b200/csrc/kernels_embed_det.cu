@@ -279,9 +279,10 @@ roast_status_t embed_bwd_det_group(Ctx* c, const Module* const* mods, int nt, co
   //  partial (max_long x A fp32) | flags (u8) | 4 scalars | temp]
   const size_t bytes = size_t(ni) * 16 + size_t(ni1) * 20 + size_t(ni1 + ni / kW + 1) * 16 + 16 +
                        size_t(max_long) * A * 4 + size_t(ni) + 1024 + temp;
-  roast_status_t st = ensure_ws(c, bytes, s);
+  Scratch ws;
+  roast_status_t st = scratch_alloc(ws, bytes, s);
   if (st) return st;
-  uint8_t* base = reinterpret_cast<uint8_t*>(c->ws);
+  uint8_t* base = ws.as<uint8_t>();
   uint32_t* k_in = reinterpret_cast<uint32_t*>(base);
   uint32_t* k_out = k_in + ni;
   int32_t* v_in = reinterpret_cast<int32_t*>(k_out + ni);

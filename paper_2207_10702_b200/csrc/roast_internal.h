@@ -115,9 +115,6 @@ struct Ctx {
   // device error flag (sticky)
   int32_t* d_err = nullptr;
   int64_t* d_zero_idx = nullptr;  // device int64 0 (inside the d_err block): row 0 for biases via L
-  // workspace (deterministic dM / split-K partials), grown on demand
-  float* ws = nullptr;
-  size_t ws_bytes = 0;
   // comm
   void* nccl_comm = nullptr;
   int32_t rank = 0, world = 1;
@@ -139,8 +136,6 @@ struct Ctx {
   // schedules on the device (pointer, per-pair length; null = chaining does not pay) and the
   // ready counters of the first GEMM's output tiles
   std::map<std::array<int64_t, 6>, std::pair<int32_t*, int>> chain_plans;
-  int* chain_flags = nullptr;
-  int64_t chain_flags_n = 0;
   // touched-set dM exchange (exchange.cu): merged intervals of the slots the registered modules
   // can write; d_iv = [starts (n_iv) | exclusive prefix of lengths (n_iv + 1)], d_pack = the
   // packed buffer (touched_n fp32); rebuilt when the module count changes
@@ -178,8 +173,22 @@ roast_status_t touched_prepare(Ctx* c, cudaStream_t s);
 roast_status_t opt_prepare(Ctx* c, const roast_opt_config_t* cfg, int64_t step, bool need_touched, cudaStream_t s);
 cudaError_t launch_pack(Ctx* c, int dir, float scale, cudaStream_t s);
 
-// workspace of at least `bytes`, stream-ordered
-roast_status_t ensure_ws(Ctx* c, size_t bytes, cudaStream_t s);
+// Per-call scratch (deterministic dM partials, the deterministic embedding sort, chain ready
+// counters): allocated with cudaMallocAsync on the call's stream and freed with cudaFreeAsync on
+// the same stream after the kernels that use it are enqueued, so calls on different streams never
+// share scratch and graph capture records alloc / free nodes.  The device's default
+// memory pool keeps freed blocks (release threshold set at roast_create), so steady-state calls
+// do not go back to the driver.
+struct Scratch {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  Scratch() = default;
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  ~Scratch() { if (p) cudaFreeAsync(p, s); }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+roast_status_t scratch_alloc(Scratch& w, size_t bytes, cudaStream_t s);
 
 // ---- kernel launchers (return cudaError_t of the launch) ----------------------
 // SIMT paths (any tile geometry), T = float or bf16 storage selected by dt
@@ -188,7 +197,7 @@ cudaError_t launch_simt_fwd(const Ctx* c, const Module& m, const void* X, void* 
 // bias backward, first half: db[j] = sum_t dY[t, j] in fp32, fixed order (slab partials
 // then an in-order sum over slabs) -> db [n]
 cudaError_t launch_colsum(const void* dY, int64_t T, int n, int64_t ld, roast_dtype_t dt, float* partial, float* db,
-                          cudaStream_t s);
+                          cudaStream_t s, int accumulate = 0);
 int colsum_slabs(int64_t T, int n);
 cudaError_t launch_simt_dw(const Ctx* c, const Module& m, const void* X, const void* dY, int64_t T,
                            roast_dtype_t dt, float* ws, cudaStream_t s);

@@ -26,7 +26,7 @@ EXPORTS = [
     "roast_register_embedding_seg", "roast_linear_fwd", "roast_linear_bwd",
     "roast_linear_bwd_dx", "roast_linear_bwd_dm", "roast_embedding_fwd", "roast_embedding_bwd",
     "roast_embedding_fwd_multi", "roast_embedding_bwd_multi", "roast_set_autotune", "roast_get_tuned", "roast_set_tuned",
-    "roast_linear_fwd_bias", "roast_bias_fwd", "roast_bias_bwd", "roast_bias_bwd_ld", "roast_colsum", "roast_register_linear_concat", "roast_linear_fwd_chain",
+    "roast_linear_fwd_bias", "roast_bias_fwd", "roast_bias_bwd", "roast_bias_bwd_ld", "roast_colsum", "roast_colsum_ex", "roast_register_linear_concat", "roast_linear_fwd_chain",
     "roast_linear_bwd_dx_chain", "roast_comm_unique_id", "roast_comm_init",
     "roast_grad_allreduce", "roast_set_exchange", "roast_touched_size", "roast_touched_intervals",
     "roast_debug_exchange", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step", "roast_grad_exchange_step",
@@ -34,7 +34,8 @@ EXPORTS = [
     "roast_p2p_finish", "roast_grad_exchange_p2p", "roast_p2p_reduce", "roast_p2p_gather",
     "roast_grad_exchange_p2p2", "roast_get_error",
     "roast_status_str", "roast_last_error", "roast_debug_tile_map", "roast_debug_chunk_map",
-    "roast_debug_materialize", "roast_debug_hash_host", "roast_launch_count",
+    "roast_debug_materialize", "roast_debug_hash_host", "roast_launch_count", "roast_lms_segments",
+    "roast_debug_opt_state",
 ]
 
 
@@ -44,7 +45,8 @@ class roast_tile_t(ctypes.Structure):
 
 class roast_config_t(ctypes.Structure):
     _fields_ = [("C", ctypes.c_double), ("align_elems", ctypes.c_int32), ("tile_layout", ctypes.c_int32),
-                ("mapping", ctypes.c_int32), ("use_sign", ctypes.c_int32), ("deterministic", ctypes.c_int32)]
+                ("mapping", ctypes.c_int32), ("use_sign", ctypes.c_int32), ("deterministic", ctypes.c_int32),
+                ("simt_bf16", ctypes.c_int32)]
 
 
 class roast_opt_config_t(ctypes.Structure):
@@ -87,6 +89,7 @@ def _load():
         "roast_bias_bwd": (st, [H, I32, P, I64, ctypes.c_int, S]),
         "roast_bias_bwd_ld": (st, [H, I32, P, I64, I64, ctypes.c_int, S]),
         "roast_colsum": (st, [P, I64, I32, I64, ctypes.c_int, P, S]),
+        "roast_colsum_ex": (st, [P, I64, I32, I64, ctypes.c_int, P, I32, S]),
         "roast_register_linear_concat": (st, [H, P, I32, ctypes.POINTER(I32)]),
         "roast_get_tuned": (st, [H, I32, I32, I64, ctypes.POINTER(I32), ctypes.POINTER(I32)]),
         "roast_set_tuned": (st, [H, I32, I32, I64, I32, I32]),
@@ -130,6 +133,8 @@ def _load():
         "roast_debug_materialize": (st, [H, I32, ctypes.c_int, P, S]),
         "roast_launch_count": (I64, [H]),
         "roast_debug_hash_host": (st, [U64, I32, P, I64, I64, I64, I32, I32, P, P]),
+        "roast_lms_segments": (st, [P, I32, I64, I32, P, P]),
+        "roast_debug_opt_state": (st, [H, I32, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -218,17 +223,17 @@ def roast_set_tuned(h, mid, kernel, tokens, wm, splits):
 
 
 def lms_segments(sizes, mem_size, align=8):
-    """LMS memories: piece i of sizes[i] parameters gets
-    |M_i| = floor(f_i |M|), f_i = n_i / n, aligned down to `align` so every base
-    stays aligned; the remainder goes to the last piece (R23).
-    Returns [(seg_base, seg_size)] for roast_register_*_seg / Roast.linear(segment=)."""
-    n = sum(int(x) for x in sizes)
-    segs, base = [], 0
-    for i, ni in enumerate(sizes):
-        size = mem_size - base if i == len(sizes) - 1 else (int(ni) * mem_size // n) // align * align
-        segs.append((base, size))
-        base += size
-    return segs
+    """LMS memories from the library's roast_lms_segments: piece i of
+    sizes[i] parameters gets |M_i| = floor(f_i |M|), f_i = n_i / n, aligned down to
+    `align`, the remainder to the last piece (R23).  Returns [(seg_base,
+    seg_size)] for roast_register_*_seg / Roast.linear(segment=)."""
+    import numpy as np
+    sz = np.ascontiguousarray([int(x) for x in sizes], dtype=np.int64)
+    base = np.empty(len(sz), dtype=np.int64)
+    size = np.empty(len(sz), dtype=np.int64)
+    _check(_lib.roast_lms_segments(sz.ctypes.data, len(sz), int(mem_size), int(align), base.ctypes.data,
+                                   size.ctypes.data), "roast_lms_segments")
+    return [(int(b), int(s)) for b, s in zip(base, size)]
 
 
 def roast_linear_fwd_bias(h, mid, X_ptr, Y_ptr, tokens, dtype, bias_ptr, stream=0):
@@ -259,6 +264,10 @@ def roast_bias_bwd_ld(h, bias_id, dY_ptr, tokens, ld, dtype, stream=0):
 
 def roast_colsum(dY_ptr, tokens, n, ld, dtype, db_ptr, stream=0):
     _check(_lib.roast_colsum(dY_ptr, tokens, n, ld, dtype, db_ptr, stream), "roast_colsum")
+
+
+def roast_colsum_ex(dY_ptr, tokens, n, ld, dtype, db_ptr, accumulate, stream=0):
+    _check(_lib.roast_colsum_ex(dY_ptr, tokens, n, ld, dtype, db_ptr, int(accumulate), stream), "roast_colsum_ex")
 
 
 def roast_register_linear_concat(h, ids):
@@ -464,7 +473,7 @@ class Roast:
     """One handle + its caller-owned M / dM (torch fp32 CUDA tensors)."""
 
     def __init__(self, M, z1, z2, seed=0x5EED, C=1.0, align=8, tile_layout=ROW_MAJOR, mapping=MAP_HASH,
-                 use_sign=True, deterministic=False, dM=None):
+                 use_sign=True, deterministic=False, dM=None, simt_bf16=False):
         import torch
         assert M.is_cuda and M.dtype == torch.float32 and M.is_contiguous()
         self.torch = torch
@@ -473,6 +482,7 @@ class Roast:
         cfg = roast_config_default()
         cfg.C, cfg.align_elems, cfg.tile_layout = C, align, tile_layout
         cfg.mapping, cfg.use_sign, cfg.deterministic = mapping, int(use_sign), int(deterministic)
+        cfg.simt_bf16 = int(simt_bf16)   # bf16 off the tcgen05 path: error unless opted in
         self.mem_size = M.numel()
         self.z1, self.z2 = z1, z2
         self.h = roast_create(self.mem_size, seed, z1, z2, cfg)
@@ -583,8 +593,10 @@ class Roast:
         ld = dY.stride(0) if dY.shape[0] > 1 else n
         for _, _, grads, _, slot in self._groups():
             if mid in slot:
-                roast_colsum(dY.data_ptr(), dY.shape[0], n, ld, self._dt(dY), grads[slot[mid]].data_ptr(),
-                             self._s(stream))
+                # accumulate: a bias whose layer runs backward twice before the flush (micro-batch
+                # accumulation, a shared module) keeps both contributions; flush / zero_grad clear it
+                roast_colsum_ex(dY.data_ptr(), dY.shape[0], n, ld, self._dt(dY), grads[slot[mid]].data_ptr(), 1,
+                                self._s(stream))
                 self._bias_pending = True
                 return
         raise KeyError(mid)
@@ -593,10 +605,21 @@ class Roast:
         """dM += every collected bias gradient (one multi-table L backward per group)."""
         if not self._bias_pending:
             return
+        s = self._stream_obj(stream)
         for mids, _, grads, idx, _ in self._groups():
             roast_embedding_bwd_multi(self.h, mids, idx.data_ptr(), 1, grads.data_ptr(), self._s(stream))
-            grads.zero_()
+            with self.torch.cuda.stream(s):     # zero after the scatter has read them (same stream)
+                grads.zero_()
         self._bias_pending = False
+
+    def _stream_obj(self, stream):
+        """torch stream object for `stream` (None = the current stream; a raw handle is wrapped)."""
+        torch = self.torch
+        if stream is None:
+            return torch.cuda.current_stream()
+        if isinstance(stream, torch.cuda.Stream):
+            return stream
+        return torch.cuda.ExternalStream(int(stream))
 
     @staticmethod
     def _dt(t):
@@ -705,6 +728,11 @@ class Roast:
 
     def zero_grad(self, stream=None):
         roast_zero_grad(self.h, self._s(stream))
+        if self._bias_pending:            # collected-but-unscattered bias gradients are discarded too
+            with self.torch.cuda.stream(self._stream_obj(stream)):
+                for _, _, grads, _, _ in self._groups():
+                    grads.zero_()
+            self._bias_pending = False
 
     def sync_shadow(self, stream=None):
         roast_sync_shadow(self.h, self._s(stream))
@@ -807,6 +835,13 @@ class Roast:
 
     def check(self):
         _check(roast_get_error(self.h), "roast_get_error")
+
+    def opt_state(self, which):
+        """Host copy (numpy fp32) of optimizer state array `which` (0: Adagrad G / Adam m; 1: Adam v)."""
+        import numpy as np
+        out = np.empty(self.mem_size, dtype=np.float32)
+        _check(_lib.roast_debug_opt_state(self.h, int(which), out.ctypes.data), "roast_debug_opt_state")
+        return out
 
     def launch_count(self):
         return roast_launch_count(self.h)

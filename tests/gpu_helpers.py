@@ -27,3 +27,22 @@ def bf16_input(seed, shape, dist="normal"):
 def store(mem_size, seed=synth.SEED_M):
     """M ~ U(-1, 1) (C = 1, P:325) as fp32."""
     return synth.uniform(seed, (mem_size,)).astype(np.float32)
+
+
+def check_update(M_prev, got, ref_new, tol=1e-5):
+    """The optimizer's UPDATE, not just the new value: M ~ 1 and a step ~ lr, so comparing M
+    alone would check the update only to ~ulp(M) / lr.  Asserts (a) the update dM_got = got -
+    M_prev against the oracle's dM_ref = ref_new - M_prev at relative Frobenius <= tol, and (b)
+    element by element |got - ref_new| <= ulp32(ref_new) / 2 + tol (|dM_ref| + rms(dM_ref) / 10):
+    the update is right to tol, up to the one unavoidable fp32 rounding of the stored M (the
+    rms term covers elements whose step nearly cancels, e.g. Adam's m ~ 0, where the kernel's
+    fp32 state arithmetic has absolute, not relative, error)."""
+    M_prev = np.asarray(M_prev, dtype=np.float64)
+    got = np.asarray(got, dtype=np.float64)
+    ref_new = np.asarray(ref_new, dtype=np.float64)
+    d_got, d_ref = got - M_prev, ref_new - M_prev
+    assert rel_frob(d_got, d_ref) <= tol, rel_frob(d_got, d_ref)
+    half_ulp = 0.5 * np.spacing(np.abs(ref_new).astype(np.float32)).astype(np.float64)
+    rms = float(np.sqrt(np.mean(d_ref * d_ref))) if d_ref.size else 0.0
+    bad = np.abs(got - ref_new) > half_ulp + tol * (np.abs(d_ref) + 0.1 * rms) + 1e-30
+    assert not bad.any(), (int(bad.sum()), np.flatnonzero(bad)[:5])

@@ -108,3 +108,45 @@ def test_c4_full_size(R, torch, dist, align):
     assert abs(lhs - rhs) <= 1e-5 * abs(lhs), (lhs, rhs)
     ctx.check()
     ctx.close()
+
+
+@pytest.mark.parametrize("dist,align,deterministic", [("uniform", 32, False), ("zipf", 32, False),
+                                                      ("zipf", 32, True), ("uniform", 8, True)])
+def test_c4_full_size_backward_element_by_element(R, torch, dist, align, deterministic):
+    """C4's backward at full size, element by element: the launch is the bench's (26 tables x
+    65 536 lookups, all tables in one call), but dOut is non-zero only for two tables, so every
+    slot of dM has an oracle value the oracle can compute (the L rule, over those
+    two tables' 131 072 lookups; duplicates add, R15).  Deterministic mode: bitwise identical
+    over 3 runs as well."""
+    from oracle import embedding as OE
+    tables, rows, dim, Z, batch = 26, 10 ** 7, 128, 32, 65536
+    mem = synth.compressed_size(tables * rows * dim, 1000, align=align)
+    M_np = synth.uniform(synth.SEED_M, (mem,)).astype(np.float32)
+    ctx = R.Roast(to_dev(M_np, torch.float32), 64, 64, seed=HS, align=align, deterministic=deterministic)
+    mids = [ctx.embedding(rows, dim, Z) for _ in range(tables)]
+    gen = synth.uniform_indices if dist == "uniform" else synth.zipf_indices
+    idx_np = np.stack([gen(synth.SEED_IDX + t, batch, rows) for t in range(tables)])
+    live = (3, 17)
+    dout_np = np.zeros((tables, batch, dim), np.float32)
+    for t in live:
+        dout_np[t] = synth.normal(synth.SEED_DY + t, (batch, dim)).astype(np.float32)
+    idx, dout = to_dev(idx_np, torch.int64), to_dev(dout_np.reshape(-1, dim), torch.float32)
+    runs = []
+    for _ in range(3 if deterministic else 1):
+        ctx.zero_grad()
+        ctx.emb_bwd_multi(mids, idx, dout)
+        torch.cuda.synchronize()
+        runs.append(ctx.dM.cpu().numpy())
+    ctx.check()
+    for r in runs[1:]:
+        assert np.array_equal(r, runs[0])
+    ref = np.zeros(mem)
+    for t in live:
+        OE.EmbeddingSpec(rows, dim, Z, mem, HS, mids[t], align=align).backward(idx_np[t], dout_np[t], ref)
+    got = runs[0].astype(np.float64)
+    assert rel_frob(got, ref) <= 1e-5
+    # element by element: fp32 sums of at most a few hundred terms (Zipf-hot rows) of N(0, 1)
+    scale = np.abs(ref).max()
+    assert np.max(np.abs(got - ref)) <= 1e-5 * scale
+    assert np.all(got[ref == 0] == 0)     # slots no live lookup reaches stay exactly zero
+    ctx.close()

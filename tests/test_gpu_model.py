@@ -2,7 +2,8 @@
 linears in one GMS store, trained through torch autograd + the C ABI, against the same
 model in fp32 torch autograd with the recovered weights materialised densely.
 
-The reference dM is the paper's gradient rule applied to the dense model's weight
+The dense reference weights, biases and embedding tables are built by the oracle's own
+materialisation (oracle/), never read back from the library.  The reference dM is the paper's gradient rule applied to the dense model's weight
 gradients: dM[slot] = sum over (i, j) mapped to slot of lambda * g * dL/dW[i, j]
 (R12), scattered by the oracle (oracle/roast_mm.py).  Activations are bf16 on
 the ROAST side (fp32 in the reference), so the tolerance is a composition bound (3e-2),
@@ -43,8 +44,7 @@ def test_encoder_layer_gradients_match_dense_autograd():
 
     # dense fp32 reference with W = lambda * g * bf16(M) (the tensor-core operand, R18)
     lins = [layer.q, layer.k, layer.v, layer.o, layer.ff1, layer.ff2]
-    W = [torch.nn.Parameter(store.materialize(l.mid, torch.bfloat16).float() * store_lam(l, M_np))
-         for l in lins]
+    W = [torch.nn.Parameter(oracle_weight(store, l, M_np)) for l in lins]
     xr = x.float()
 
     def lin(t, i):
@@ -68,9 +68,24 @@ def test_encoder_layer_gradients_match_dense_autograd():
     assert err < 3e-2, err
 
 
-def store_lam(lin, M_np):
-    _, H, O = lin.store.dims[lin.mid]
-    return OM.LinearSpec(H, O, 64, 64, len(M_np), synth.HASH_SEED, lin.mid).lam
+def oracle_weight(store, lin, M_np):
+    """W = lambda * g * bf16(M) (the tensor-core operand, R18) built by the ORACLE's
+    materialisation (oracle/roast_mm.py), fp32 on the GPU."""
+    import torch
+    _, H, O = store.dims[lin.mid]
+    spec = OM.LinearSpec(H, O, 64, 64, len(M_np), synth.HASH_SEED, lin.mid)
+    return torch.tensor(np.float64(spec.lam) * spec.materialize(M_np, "operand"), dtype=torch.float32, device="cuda")
+
+
+def oracle_bias(store, lin, M_np):
+    """A bias via L (R24): row 0 of its own 1 x O embedding, lambda from the linear's fan-in,
+    recovered by the oracle (oracle/embedding.py)."""
+    import torch
+    from oracle import embedding as OE
+    _, H, O = store.dims[lin.mid]
+    v = OE.EmbeddingSpec(1, O, 64, len(M_np), synth.HASH_SEED, lin.bias.mid, fan_in=H).forward(
+        np.zeros(1, np.int64), M_np.astype(np.float64))[0]
+    return torch.tensor(v, dtype=torch.float32, device="cuda")
 
 
 @pytest.mark.parametrize("batch_biases", [False, True])
@@ -104,12 +119,13 @@ def test_roast_bert_embeddings_and_biases_match_dense_autograd(batch_biases):
 
     # dense fp32 reference from the recovered weights
     emb = model.emb
-    tables = [torch.nn.Parameter(store.emb_fwd(m.mid, torch.arange(r, device="cuda")).clone())
-              for m, r in [(emb.word, vocab), (emb.pos, max_pos), (emb.tok_type, 2)]]
+    tables = [torch.nn.Parameter(torch.tensor(
+        OE.EmbeddingSpec(r, d, Z, mem, synth.HASH_SEED, m.mid).forward(np.arange(r), M_np.astype(np.float64)),
+        dtype=torch.float32, device="cuda")) for m, r in [(emb.word, vocab), (emb.pos, max_pos), (emb.tok_type, 2)]]
     layer = model.layers[0]
     lins = [layer.q, layer.k, layer.v, layer.o, layer.ff1, layer.ff2]
-    W = [torch.nn.Parameter(store.materialize(l.mid, torch.bfloat16).float() * store_lam(l, M_np)) for l in lins]
-    bs = [torch.nn.Parameter(l.bias.vector().clone()) for l in lins]
+    W = [torch.nn.Parameter(oracle_weight(store, l, M_np)) for l in lins]
+    bs = [torch.nn.Parameter(oracle_bias(store, l, M_np)) for l in lins]
     pos = torch.arange(S, device="cuda").expand(B, S)
     e = tables[0][ids] + tables[1][pos] + tables[2][types]
     xr = torch.nn.functional.layer_norm(e, (d,))
@@ -139,3 +155,40 @@ def test_roast_bert_embeddings_and_biases_match_dense_autograd(batch_biases):
         assert np.linalg.norm(v) > 1e-3 * np.linalg.norm(dM_ref), k
     err = np.linalg.norm(dM - dM_ref) / np.linalg.norm(dM_ref)
     assert err < 3e-2, err
+
+
+def test_batched_bias_grads_accumulate_over_two_backwards_and_zero_grad_discards():
+    """with batch_biases the bias backward only collects column sums until
+    flush_bias_grads.  Two backwards before the flush (micro-batch accumulation, a layer applied
+    twice) must keep both contributions; zero_grad must discard collected-but-unflushed ones.
+    Reference: the same steps with per-call L backwards (batch_biases = False)."""
+    import torch
+    from paper_2207_10702_b200 import nn as RN, roast as R
+    d, T, mem = 256, 192, 40_000
+    M_np = synth.uniform(synth.SEED_M, (mem,)).astype(np.float32)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    xs = [torch.randn(T, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3)]
+    rs = [torch.randn(T, d, device="cuda", generator=g) for _ in range(3)]
+
+    def run(batched, discard_first):
+        store = R.Roast(torch.tensor(M_np, device="cuda"), 64, 64, seed=synth.HASH_SEED)
+        store.batch_biases = batched
+        lin = RN.RoastLinear(store, d, d, bias=True)
+        store.zero_grad()
+        if discard_first:                       # a step whose gradients are thrown away
+            (lin(xs[2]).float() * rs[2]).sum().backward()
+            store.zero_grad()
+        for x, r in zip(xs[:2], rs[:2]):        # two micro-batches, one flush
+            (lin(x).float() * r).sum().backward()
+        store.flush_bias_grads()
+        torch.cuda.synchronize()
+        out = store.dM.cpu().numpy().astype(np.float64)
+        store.close()
+        return out
+
+    ref = run(False, False)
+    assert np.linalg.norm(ref) > 0
+    for discard in (False, True):
+        got = run(True, discard)
+        assert np.linalg.norm(got - ref) <= 1e-5 * np.linalg.norm(ref), discard

@@ -5,7 +5,7 @@ One GPU stands in for the node: W "ranks" are W handles in one process whose win
 attached to each other by device pointer (the kernels cannot tell a peer's HBM from their own),
 plus a two-process test that maps the windows through CUDA IPC.  Every rank must end with the
 same M, bit for bit, equal to roast_optimizer_step (touched_only) on the fp32 sum of the W
-gradients in rank order, and within 1e-5 of the fp64 oracle update."""
+gradients in rank order, and its update within 1e-5 of the fp64 oracle's (tests.gpu_helpers.check_update)."""
 import os
 import subprocess
 import sys
@@ -18,7 +18,7 @@ import synth
 from oracle import embedding as OE
 from oracle import optim as OO
 from oracle import roast_mm as OM
-from tests.gpu_helpers import store, to_dev
+from tests.gpu_helpers import check_update, rel_frob, store, to_dev
 
 pytestmark = pytest.mark.gpu
 HS = synth.HASH_SEED
@@ -97,12 +97,17 @@ def test_p2p_virtual_ranks(R, torch, W, kind, zero):
             assert torch.equal(c.M, ref.M)
             assert torch.equal(c.dM, ref.dM)
             assert torch.equal(c.materialize(ids[0], torch.bfloat16), ref.materialize(ids[0], torch.bfloat16))
-        # the fp64 oracle on the touched slots (the other slots are dead and stay as they were)
+        # the fp64 oracle on the touched slots (the other slots are dead and stay as they were),
+        # started from the device's M and state; the UPDATE and the new state are compared
         gsum64 = sum(g.double().cpu().numpy() for g in gs)
-        new, st = OO.step(NAMES[kind], ref_M, gsum64, st, lr=1e-2, t=t, wd=0.01)
-        ref_M = np.where(inside_np, new, ref_M)
+        new, st_ref = OO.step(NAMES[kind], ref_M, gsum64, st, lr=1e-2, t=t, wd=0.01)
         got = ranks[0][0].M.cpu().numpy()
-        assert np.max(np.abs(got - ref_M)) <= 1e-5 * max(1.0, np.max(np.abs(ref_M)))
+        check_update(ref_M[inside_np], got[inside_np], new[inside_np])
+        assert np.array_equal(got[~inside_np], M0[~inside_np])
+        keys = {0: [], 1: ["G"], 2: ["m", "v"]}[kind]
+        for i, k in enumerate(keys):
+            assert rel_frob(ranks[0][0].opt_state(i)[inside_np], st_ref[k][inside_np]) <= 1e-6, (k, t)
+        st = {k: ranks[0][0].opt_state(i).astype(np.float64) for i, k in enumerate(keys)}
         ref_M = got.astype(np.float64)
     for c, _ in ranks:
         c.close()

@@ -10,7 +10,7 @@ import pytest
 import synth
 from oracle import embedding as OE
 from oracle import roast_mm as OM
-from tests.gpu_helpers import bf16_input, rel_frob, store, to_dev
+from tests.gpu_helpers import bf16_input, check_update, rel_frob, store, to_dev
 
 pytestmark = pytest.mark.gpu
 
@@ -31,7 +31,12 @@ def R():
 
 
 def make_ctx(R, torch, M_np, z1, z2, **kw):
+    """A handle over M_np.  Geometries the tcgen05 path cannot take (tile != 64 x 64, SW128,
+    A % 8 != 0) opt into the SIMT kernels for bf16 (roast_config_t.simt_bf16) — these tests
+    exercise those kernels on purpose; a 64 x 64 row-major handle never may fall back."""
     M = to_dev(M_np, torch.float32)
+    off_path = (z1, z2) != (64, 64) or kw.get("tile_layout", 0) != 0 or kw.get("align", 8) % 8 != 0
+    kw.setdefault("simt_bf16", off_path)
     return R.Roast(M, z1, z2, seed=HS, **kw), M
 
 
@@ -401,23 +406,29 @@ def test_deterministic_workspace_fully_written_before_read(R, torch, monkeypatch
 @pytest.mark.parametrize("kind,name", [(0, "sgd"), (1, "adagrad"), (2, "adam")])
 @pytest.mark.parametrize("mem", [100_000, 100_003])   # 16-byte vector path / scalar path
 def test_optimizer_step_parity(R, torch, kind, name, mem):
-    """NEXT #1: fused update of M + state + bf16 shadow (+ dM zeroing) vs the oracle formulas."""
+    """NEXT #1: fused update of M + state + bf16 shadow (+ dM zeroing) vs the oracle formulas,
+    three steps (t >= 2 exercises the carried state and the bias corrections).  Each step starts
+    the oracle from the device's M and state, and compares the UPDATE (check_update) and the new
+    state, so an error in the step itself cannot hide under |M| ~ 1 >> lr."""
     from oracle import optim as OO
     M_np = store(mem)
     ctx, M = make_ctx(R, torch, M_np, 64, 64)
     mid = ctx.linear(128, 128)
-    g1 = synth.normal(synth.SEED_DY, (mem,)).astype(np.float32)
-    g2 = synth.normal(synth.SEED_DY + 1, (mem,)).astype(np.float32)
-    ref_M, st = M_np.astype(np.float64), {}
-    for t, g in [(1, g1), (2, g2)]:
+    keys = {"sgd": [], "adagrad": ["G"], "adam": ["m", "v"]}[name]
+    st = {}
+    for t in (1, 2, 3):
+        g = synth.normal(synth.SEED_DY + t, (mem,)).astype(np.float32)
+        M_prev = ctx.M.cpu().numpy().astype(np.float64)
         ctx.dM.copy_(to_dev(g, torch.float32))
         ctx.optimizer_step(kind, 1e-2, step=t, weight_decay=0.01)
         torch.cuda.synchronize()
-        ref_M, st = OO.step(name, ref_M.astype(np.float32).astype(np.float64), g, st, lr=1e-2, t=t, wd=0.01)
-        got = ctx.M.cpu().numpy()
-        assert np.max(np.abs(got - ref_M)) <= 1e-5 * max(1.0, np.max(np.abs(ref_M)))
+        ref_M, st_ref = OO.step(name, M_prev, g, st, lr=1e-2, t=t, wd=0.01)
+        check_update(M_prev, ctx.M.cpu().numpy(), ref_M)
         assert torch.count_nonzero(ctx.dM).item() == 0          # zero_grad fused
-        ref_M = got.astype(np.float64)                           # continue from the device state
+        for i, k in enumerate(keys):                             # optimizer state after the step
+            got_s = ctx.opt_state(i).astype(np.float64)
+            assert rel_frob(got_s, st_ref[k]) <= 1e-6, (k, t)
+        st = {k: ctx.opt_state(i).astype(np.float64) for i, k in enumerate(keys)}   # continue from the device
     # the shadow follows M bit-exactly: operand tile == g * bf16(M)
     spec = OM.LinearSpec(128, 128, 64, 64, mem, HS, mid)
     Wbf = ctx.materialize(mid, torch.bfloat16).float().cpu().numpy()
@@ -776,3 +787,26 @@ def test_tcgen05_shape_fuzz(R, torch):
         assert rel_frob(dM, spec.backward_dm(X_np, dY_np)) <= 1e-2, where
         ctx.check()
         ctx.close()
+
+
+def test_bf16_off_the_tcgen05_path_is_an_error_unless_opted_in(R, torch):
+    """No silent second backend: a bf16 call the tcgen05 kernels cannot
+    take (here 32 x 32 tiles) returns ROAST_ERR_UNSUPPORTED by default, and runs on the SIMT
+    kernels — matching the oracle — only with roast_config_t.simt_bf16 = 1."""
+    mem, H, O, T = 8192, 256, 256, 64
+    M_np = store(mem)
+    X = to_dev(bf16_input(synth.SEED_X, (T, H)), torch.bfloat16)
+    ctx, _ = make_ctx(R, torch, M_np, 32, 32, simt_bf16=False)
+    mid = ctx.linear(H, O)
+    with pytest.raises(R.RoastError) as ei:
+        ctx.fwd(mid, X)
+    assert ei.value.status == R.ERR_UNSUPPORTED
+    with pytest.raises(R.RoastError):
+        ctx.bwd(mid, X, to_dev(bf16_input(synth.SEED_DY, (T, O)), torch.bfloat16))
+    ctx.close()
+    ctx, _ = make_ctx(R, torch, M_np, 32, 32, simt_bf16=True)
+    mid = ctx.linear(H, O)
+    Y = ctx.fwd(mid, X).float().cpu().numpy()
+    spec = OM.LinearSpec(H, O, 32, 32, mem, HS, mid)
+    assert rel_frob(Y, np.float64(spec.lam) * (X.float().cpu().numpy() @ spec.materialize(M_np, "operand"))) <= 1e-2
+    ctx.close()

@@ -54,9 +54,18 @@ def test_rejects_bad_geometry(R):
 
 
 def test_lms_segments_product_matches_oracle():
-    """The binding's LMS partition helper (product) == the oracle's reading R23."""
+    """The library's roast_lms_segments (C ABI, host) == the oracle's reading R23."""
     from oracle import hashing as OH
     from paper_2207_10702_b200 import roast
     for sizes, mem, A in [([768 * 3072, 3072 * 768], 47_192, 8), ([1, 2, 3, 4, 5], 100_000, 32), ([7], 64, 8),
                           ([10 ** 9, 1, 1], 1 << 20, 8)]:
         assert roast.lms_segments(sizes, mem, A) == OH.lms_segments(sizes, mem, A)
+
+
+def test_lms_segments_rejects_bad_arguments(R):
+    with pytest.raises(R.RoastError):
+        R.lms_segments([], 100, 8)
+    with pytest.raises(R.RoastError):
+        R.lms_segments([1, 0], 100, 8)
+    with pytest.raises(R.RoastError):
+        R.lms_segments([1, 2], 100, 0)

@@ -27,6 +27,10 @@ def test_lms_segments_partition(sizes, mem, A):
             assert segs[i + 1][0] == b + s                      # contiguous, disjoint
             assert 0 <= sizes[i] * mem / n - s < A              # floor(f_i m) aligned down (R14/R23)
     assert hashing.lms_segments([1, 1], 16, 8) == [(0, 8), (8, 8)]
+    # worked by hand: f = (3/4, 1/4) of 1000 -> floor(750) aligned down to 8 = 744, rest 256;
+    # f = (1/3, 1/3, 1/3) of 100 (A = 1) -> 33, 33, remainder 34
+    assert hashing.lms_segments([3, 1], 1000, 8) == [(0, 744), (744, 256)]
+    assert hashing.lms_segments([2, 2, 2], 100, 1) == [(0, 33), (33, 33), (66, 34)]
 
 
 def test_lms_linear_is_gms_on_its_submemory():

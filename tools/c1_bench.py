@@ -25,7 +25,8 @@ T, Z, MEM = 64, 32, 8192
 
 def gpu_us(deterministic):
     M_np = synth.uniform(synth.SEED_M, (MEM,)).astype(np.float32)
-    ctx = R.Roast(torch.tensor(M_np, device="cuda"), Z, Z, seed=synth.HASH_SEED, deterministic=deterministic)
+    ctx = R.Roast(torch.tensor(M_np, device="cuda"), Z, Z, seed=synth.HASH_SEED, deterministic=deterministic,
+                  simt_bf16=True)   # C1 (32 x 32 tiles) is the SIMT path by construction
     mid = ctx.linear(H, O)
     X_np = synth.uniform(synth.SEED_X, (T, H)).astype(np.float32)
     dY_np = synth.uniform(synth.SEED_DY, (T, O)).astype(np.float32)

@@ -56,7 +56,7 @@ def main():
         res["dense_fwdbwd_ms"] = timeit(lambda: (X @ W, dY @ W.t(), X.t() @ dY))
         ro.close()
         if D <= args.hashednet_max:
-            hn = R.Roast(M, 1, 1, align=1)
+            hn = R.Roast(M, 1, 1, align=1, simt_bf16=True)
             lh = hn.linear(D, D)
             res["hashednet_fwd_ms"] = timeit(lambda: hn.fwd(lh, X, Y), iters=3)
             res["hashednet_fwdbwd_ms"] = timeit(lambda: (hn.fwd(lh, X, Y), hn.bwd(lh, X, dY, dX)), iters=3)
