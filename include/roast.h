@@ -21,7 +21,13 @@
  *   - Argument / geometry validation is synchronous: on a non-OK return nothing
  *     was launched.  Device-detected faults (embedding index out of range) are
  *     sticky and reported by roast_get_error() (and by the next call).
- *   - A handle is not thread-safe; use one per thread / rank.
+ *   - A handle is not thread-safe; use one per thread / rank.  Calls of one handle may be
+ *     issued to several streams (e.g. dX on one, dM on another): scratch is per call
+ *     (deterministic dM partials and the deterministic embedding sort are allocated with
+ *     cudaMallocAsync / cudaFreeAsync on the call's stream) and a chained launch takes the
+ *     next of 64 ready-counter slots, so concurrent calls never share device scratch.  The
+ *     dM exchange calls (roast_grad_allreduce / _exchange_step / p2p) share the packed
+ *     touched-set buffer and must stay on one stream (they are collectives anyway).
  *   - The tcgen05 GEMMs use programmatic dependent launch among themselves: each is launched
  *     with cudaLaunchAttributeProgrammaticStreamSerialization and signals
  *     griddepcontrol.launch_dependents on entry, so only a following kernel that is itself

@@ -224,6 +224,7 @@ roast_status_t roast_destroy(roast_t h) {
   cudaFree(c->opt_s1);
   cudaFree(c->opt_s2);
   for (auto& kv : c->chain_plans) cudaFree(kv.second.first);
+  cudaFree(c->chain_flags);
   cudaFree(c->d_iv);
   cudaFree(c->d_pack);
   comm_destroy(c);

@@ -1323,6 +1323,9 @@ roast_status_t sm100_chain(Ctx* c, const Module& m0, const Module& m1, const voi
           cudaOccupancyMaxActiveClusters(&nclusters, kfn, &q) == cudaSuccess)
         resident = nclusters >= pairs;
       cudaGetLastError();
+      if (getenv("ROAST_VERBOSE"))
+        fprintf(stderr, "[roast] chain %s: max co-resident clusters %d, grid %d pairs\n", dx ? "dx" : "fwd", nclusters,
+                pairs);
     }
     if (resident && plan.makespan < 0.97 * plan.sequential) {
       ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&d), plan.sched.size() * sizeof(int32_t)));
@@ -1331,10 +1334,21 @@ roast_status_t sm100_chain(Ctx* c, const Module& m0, const Module& m1, const voi
     it = c->chain_plans.emplace(key, std::make_pair(d, plan.len)).first;
   }
   if (!it->second.first) return ROAST_ERR_UNSUPPORTED;
-  // the ready counters of problem 0's tiles: per-call scratch (Scratch), so chained launches on
-  // different streams never share them
-  Scratch fl;
-  if (roast_status_t e = scratch_alloc(fl, size_t(m_tiles) * nt0 * sizeof(int), s)) return e;
+  // the ready counters of problem 0's tiles: the next of kChainSlots slots (chained launches
+  // in flight on different streams never share counters); the slot array grows eagerly only
+  const int64_t need = int64_t(m_tiles) * nt0;
+  if (c->chain_slot_n < need) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+      return ROAST_ERR_UNSUPPORTED;   // first chained call of this size: make it eagerly
+    ROAST_CUDA_CHECK(cudaDeviceSynchronize());   // the old slots may be in use
+    cudaFree(c->chain_flags);
+    c->chain_flags = nullptr;
+    c->chain_slot_n = 0;
+    ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->chain_flags), size_t(kChainSlots) * need * sizeof(int)));
+    c->chain_slot_n = need;
+  }
+  int* flags = c->chain_flags + int64_t(c->chain_next++ % kChainSlots) * c->chain_slot_n;
   roast_status_t st = sm100_prepare(c);
   if (st) return st;
   auto prob = [&](const Module& m, const void* A, void* out, int N, int K, bool is_dx, const float* bias, Params& p,
@@ -1365,9 +1379,9 @@ roast_status_t sm100_chain(Ctx* c, const Module& m0, const Module& m1, const voi
   p0.chain = 1;
   p0.sched = it->second.first;
   p0.sched_len = it->second.second;
-  p0.flags = fl.as<int>();
+  p0.flags = flags;
   p0.err = c->d_err;
-  ROAST_CUDA_CHECK(cudaMemsetAsync(fl.p, 0, size_t(p0.units) * sizeof(int), s));
+  ROAST_CUDA_CHECK(cudaMemsetAsync(flags, 0, size_t(p0.units) * sizeof(int), s));
   const WMaps& w = *reinterpret_cast<const WMaps*>(c->tmap_shadow);
   st = dx ? launch_cg<DX, 2, WMC, true>(a0, a0, o0, w, p0, a1, o1, p1, pairs, s)
           : launch_cg<FWD, 2, WMC, true>(a0, a0, o0, w, p0, a1, o1, p1, pairs, s);

@@ -136,6 +136,12 @@ struct Ctx {
   // schedules on the device (pointer, per-pair length; null = chaining does not pay) and the
   // ready counters of the first GEMM's output tiles
   std::map<std::array<int64_t, 6>, std::pair<int32_t*, int>> chain_plans;
+  // ready counters of chained launches: kChainSlots slots of chain_slot_n ints, handed out round
+  // robin per launch, so chained launches in flight on different streams use different counters
+  // (up to kChainSlots launches in flight per handle); grown only outside graph capture
+  int* chain_flags = nullptr;
+  int64_t chain_slot_n = 0;
+  uint32_t chain_next = 0;
   // touched-set dM exchange (exchange.cu): merged intervals of the slots the registered modules
   // can write; d_iv = [starts (n_iv) | exclusive prefix of lengths (n_iv + 1)], d_pack = the
   // packed buffer (touched_n fp32); rebuilt when the module count changes
@@ -173,8 +179,8 @@ roast_status_t touched_prepare(Ctx* c, cudaStream_t s);
 roast_status_t opt_prepare(Ctx* c, const roast_opt_config_t* cfg, int64_t step, bool need_touched, cudaStream_t s);
 cudaError_t launch_pack(Ctx* c, int dir, float scale, cudaStream_t s);
 
-// Per-call scratch (deterministic dM partials, the deterministic embedding sort, chain ready
-// counters): allocated with cudaMallocAsync on the call's stream and freed with cudaFreeAsync on
+constexpr int kChainSlots = 64;
+// Per-call scratch (deterministic dM partials, the deterministic embedding sort): allocated with cudaMallocAsync on the call's stream and freed with cudaFreeAsync on
 // the same stream after the kernels that use it are enqueued, so calls on different streams never
 // share scratch and graph capture records alloc / free nodes.  The device's default
 // memory pool keeps freed blocks (release threshold set at roast_create), so steady-state calls

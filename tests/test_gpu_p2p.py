@@ -18,7 +18,7 @@ import synth
 from oracle import embedding as OE
 from oracle import optim as OO
 from oracle import roast_mm as OM
-from tests.gpu_helpers import check_update, rel_frob, store, to_dev
+from tests.gpu_helpers import check_update, grad_condition, rel_frob, store, to_dev
 
 pytestmark = pytest.mark.gpu
 HS = synth.HASH_SEED
@@ -102,7 +102,9 @@ def test_p2p_virtual_ranks(R, torch, W, kind, zero):
         gsum64 = sum(g.double().cpu().numpy() for g in gs)
         new, st_ref = OO.step(NAMES[kind], ref_M, gsum64, st, lr=1e-2, t=t, wd=0.01)
         got = ranks[0][0].M.cpu().numpy()
-        check_update(ref_M[inside_np], got[inside_np], new[inside_np])
+        gabs = sum(g.double().abs().cpu().numpy() for g in gs)
+        cond = grad_condition(gsum64[inside_np], ref_M[inside_np], 0.01, dM_abs=gabs[inside_np])
+        check_update(ref_M[inside_np], got[inside_np], new[inside_np], cond=cond)
         assert np.array_equal(got[~inside_np], M0[~inside_np])
         keys = {0: [], 1: ["G"], 2: ["m", "v"]}[kind]
         for i, k in enumerate(keys):
