@@ -22,6 +22,8 @@ from tests.gpu_helpers import check_update, grad_condition, rel_frob, store, to_
 
 pytestmark = pytest.mark.gpu
 HS = synth.HASH_SEED
+# optimizer hyper-parameters exactly as the library receives them (fp32 in roast_opt_config_t)
+HP32 = {k: float(np.float32(v)) for k, v in dict(lr=1e-2, wd=0.01, b1=0.9, b2=0.999, eps=1e-8).items()}
 MEM = 1 << 22
 NAMES = {0: "sgd", 1: "adagrad", 2: "adam"}
 
@@ -100,7 +102,7 @@ def test_p2p_virtual_ranks(R, torch, W, kind, zero):
         # the fp64 oracle on the touched slots (the other slots are dead and stay as they were),
         # started from the device's M and state; the UPDATE and the new state are compared
         gsum64 = sum(g.double().cpu().numpy() for g in gs)
-        new, st_ref = OO.step(NAMES[kind], ref_M, gsum64, st, lr=1e-2, t=t, wd=0.01)
+        new, st_ref = OO.step(NAMES[kind], ref_M, gsum64, st, **HP32, t=t)   # fp32 hyper-parameters, as received
         got = ranks[0][0].M.cpu().numpy()
         gabs = sum(g.double().abs().cpu().numpy() for g in gs)
         cond = grad_condition(gsum64[inside_np], ref_M[inside_np], 0.01, dM_abs=gabs[inside_np])

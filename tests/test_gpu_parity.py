@@ -15,6 +15,8 @@ from tests.gpu_helpers import bf16_input, check_update, grad_condition, rel_frob
 pytestmark = pytest.mark.gpu
 
 HS = synth.HASH_SEED
+# optimizer hyper-parameters exactly as the library receives them (fp32 in roast_opt_config_t)
+HP32 = {k: float(np.float32(v)) for k, v in dict(lr=1e-2, wd=0.01, b1=0.9, b2=0.999, eps=1e-8).items()}
 
 
 @pytest.fixture(scope="module")
@@ -422,7 +424,9 @@ def test_optimizer_step_parity(R, torch, kind, name, mem):
         ctx.dM.copy_(to_dev(g, torch.float32))
         ctx.optimizer_step(kind, 1e-2, step=t, weight_decay=0.01)
         torch.cuda.synchronize()
-        ref_M, st_ref = OO.step(name, M_prev, g, st, lr=1e-2, t=t, wd=0.01)
+        # the hyper-parameters the library receives are fp32 (roast_opt_config_t): the oracle takes
+        # the same values (like R18 for bf16 inputs), e.g. 1 - fp32(0.999) differs from 1e-3 by 1.3e-5
+        ref_M, st_ref = OO.step(name, M_prev, g, st, **HP32, t=t)
         check_update(M_prev, ctx.M.cpu().numpy(), ref_M, cond=grad_condition(g, M_prev, 0.01))
         assert torch.count_nonzero(ctx.dM).item() == 0          # zero_grad fused
         for i, k in enumerate(keys):                             # optimizer state after the step
