@@ -310,13 +310,16 @@ class C2Step:
     tuned and planned eagerly (kernel- and step-level training-optimal tuning)."""
 
     def __init__(self, torch, dev, ratio, deterministic=False, autotune=2, chain=1, streams=2, rank=0, world=1,
-                 tuned_file=None, flush=None):
+                 tuned_file=None, flush=None, bwd="fused"):
         import numpy as np
 
         from paper_2207_10702_b200 import dp
         from paper_2207_10702_b200 import roast as R
         import synth
         self.torch, self.dev, self.chain, self.streams, self.world = torch, dev, chain, streams, world
+        # fused: the whole backward as ONE persistent launch (roast_linear_bwd_chain: dY1, dM of
+        # L2, dX, dM of L1 co-scheduled); deterministic mode has no fused kernel (separate calls)
+        self.bwd = "streams" if deterministic else bwd
         T = self.T = TOKENS
         self.mem = synth.mlp_block(ratio)["mem_size"]
         M = torch.tensor(synth.uniform(synth.SEED_M, (self.mem,)).astype(np.float32), device=dev)
@@ -356,6 +359,8 @@ class C2Step:
             ctx.bwd_dm(l2, Y1, dY2)
             ctx.bwd_dx(l1, dY1, dX)
             ctx.bwd_dm(l1, X, dY1)
+            if self.bwd == "fused":
+                ctx.bwd_chain(l1, l2, X, Y1, dY2, dY1, dX)   # plans the fused backward eagerly
             torch.cuda.synchronize()
         if world > 1:
             # every rank must run the same configuration: the step-level choice below replays steps
@@ -374,7 +379,7 @@ class C2Step:
         # GEMM tuned alone may pick 192-column units, which fill more CTA pairs but leave fewer
         # SMs to the dM GEMM running beside it on the second stream; keep whichever whole step
         # (graph-replayed, L2 flushed) is faster
-        if autotune == 2 and not tuned_file:
+        if autotune == 2 and not tuned_file and self.bwd != "fused":
             for mid in (l1, l2):
                 wm, nu = ctx.tuned(mid, 1, T)
                 if nu == 3:
@@ -407,7 +412,9 @@ class C2Step:
         else:
             ctx.fwd(l1, Xin, Y1)
             ctx.fwd(l2, Y1, Y2)
-        if self.streams == 2 and self.chain == 2:
+        if self.bwd == "fused":
+            ctx.bwd_chain(l1, l2, Xin, Y1, dY2in, dY1, dX)   # a2 + a3 of both layers, one launch
+        elif self.streams == 2 and self.chain == 2:
             side.wait_stream(cur)
             with torch.cuda.stream(side):
                 ctx.bwd_dm(l2, Y1, dY2in)
@@ -503,7 +510,7 @@ def run_gpu(args):
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
     S = C2Step(torch, dev, args.ratio, deterministic=args.deterministic, autotune=args.autotune, chain=args.chain,
-               streams=args.streams, rank=rank, world=world, tuned_file=args.tuned_file, flush=flush)
+               streams=args.streams, rank=rank, world=world, tuned_file=args.tuned_file, flush=flush, bwd=args.bwd)
     ctx, T, mem = S.ctx, S.T, S.mem
     l1, l2, X, dY2, Y1, Y2, dY1, dX = S.l1, S.l2, S.X, S.dY2, S.Y1, S.Y2, S.dY1, S.dX
     step_body = S.step_body
@@ -565,11 +572,14 @@ def run_gpu(args):
         calls = [("fwd_chain", lambda: ctx.fwd_chain(l1, l2, X, Y1, Y2), 2 * gemm_flop)]
     else:
         calls = [("fwd", lambda: ctx.fwd(l1, X, Y1), gemm_flop), ("fwd", lambda: ctx.fwd(l2, Y1, Y2), gemm_flop)]
-    if args.chain == 2:
+    if S.bwd == "fused":
+        calls += [("bwd_fused", lambda: ctx.bwd_chain(l1, l2, X, Y1, dY2, dY1, dX), 4 * gemm_flop)]
+    elif args.chain == 2:
         calls += [("dx_chain", lambda: ctx.bwd_dx_chain(l1, l2, dY2, dY1, dX), 2 * gemm_flop)]
     else:
         calls += [("dx", lambda: ctx.bwd_dx(l2, dY2, dY1), gemm_flop), ("dx", lambda: ctx.bwd_dx(l1, dY1, dX), gemm_flop)]
-    calls += [("dm", lambda: ctx.bwd_dm(l2, Y1, dY2), gemm_flop), ("dm", lambda: ctx.bwd_dm(l1, X, dY1), gemm_flop)]
+    if S.bwd != "fused":
+        calls += [("dm", lambda: ctx.bwd_dm(l2, Y1, dY2), gemm_flop), ("dm", lambda: ctx.bwd_dm(l1, X, dY1), gemm_flop)]
     kinds = list(dict.fromkeys(k for k, _, _ in calls))
     ev = {k: [] for k in kinds}
     kind_flop = {k: f for k, _, f in calls}
@@ -776,6 +786,8 @@ def run_gpu(args):
                     dm_mode="deterministic" if args.deterministic else "atomic",
                     streams=args.streams, cuda_graph=bool(args.graph),
                     chain=["off", "forward pair", "forward + dX pairs"][args.chain],
+                    backward="one fused launch (roast_linear_bwd_chain)" if S.bwd == "fused" else
+                             "separate dX / dM launches on %d stream(s)" % args.streams,
                     autotune=["makespan model", "inference-optimal", "training-optimal"][args.autotune],
                     tuned=S.tuned(), parallelism=f"dp{world}"),
         roofline=dict(bound="tensor", kernel=dom, achieved=achieved, peak=burst, unit="TFLOP/s",
@@ -850,7 +862,7 @@ def c2_extras(torch, dev, args, S, flush, stream, W1, W2):
     for key, ratio, det in (("10x", 10, False), ("1000x", 1000, False), ("100x_deterministic", 100, True)):
         try:
             V = C2Step(torch, dev, ratio, deterministic=det, autotune=args.autotune, chain=args.chain,
-                       streams=args.streams, flush=flush)
+                       streams=args.streams, flush=flush, bwd=args.bwd)
             g = graph_of(torch, V.step_body)
             ms = mean_replay_ms(torch, g, 10, flush, stream)
             variants[key] = dict(value=flops_per_step(T) / (ms * 1e-3) / 1e12, unit=UNIT, ms_per_step=ms,
@@ -1096,6 +1108,8 @@ def main():
     ap.add_argument("--sustained-seconds", type=float, default=2.0,
                     help="also replay the step back to back for this long and report it as `sustained`")
     ap.add_argument("--streams", type=int, default=2, choices=[1, 2])
+    ap.add_argument("--bwd", default="fused", choices=["fused", "streams"],
+                    help="backward: one fused launch (roast_linear_bwd_chain) or separate dX / dM launches")
     ap.add_argument("--ratio", type=float, default=RATIO, help="compression (C2 at 10x / 100x / 1000x)")
     ap.add_argument("--c3-tokens", type=int, default=65536, help="C3 global tokens (512 x 128), split over ranks")
     ap.add_argument("--no-breakdown", action="store_true", help="C3: skip the profiler breakdown step")

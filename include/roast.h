@@ -217,6 +217,22 @@ roast_status_t roast_linear_fwd_chain(roast_t h, int32_t id_a, int32_t id_b, con
 roast_status_t roast_linear_bwd_dx_chain(roast_t h, int32_t id_a, int32_t id_b, const void* d_dY_b, void* d_dY_a,
                                          void* d_dX, int64_t tokens, roast_dtype_t dt, roast_stream_t stream);
 
+/* The whole backward of a chained pair a -> b (the backward of roast_linear_fwd_chain, with
+ * the identity between the layers): given X_a, Y_a (= X_b) and dY_b,
+ *   dY_a = lambda_b dY_b W~_b^T                 (a2 of b; written to d_dY_a, tokens x in_b)
+ *   dM  += scatter_b(lambda_b g Y_a^T dY_b)     (a3 of b)
+ *   dX_a = lambda_a dY_a W~_a^T                 (a2 of a; written to d_dX_a, tokens x in_a)
+ *   dM  += scatter_a(lambda_a g X_a^T dY_a)     (a3 of a)
+ * (P:338-346 with g by the chain rule, R12).  On the tcgen05 path (bf16, 64 x 64 tiles, every
+ * feature dimension a multiple of 256, fast / atomic dM) the four GEMMs run as ONE persistent
+ * launch: their units are list-scheduled over all CTA pairs and the dependent ones (dX_a, the
+ * dM of a) stream behind the published tiles of dY_a; otherwise the four calls run one after
+ * the other.  Requires out_a == in_b; d_dX_a must not be NULL.  The first call of a shape plans
+ * the schedule (synchronous; not under graph capture).  Errors as roast_linear_bwd. */
+roast_status_t roast_linear_bwd_chain(roast_t h, int32_t id_a, int32_t id_b, const void* d_X_a, const void* d_Y_a,
+                                      const void* d_dY_b, void* d_dY_a, void* d_dX_a, int64_t tokens,
+                                      roast_dtype_t dt, roast_stream_t stream);
+
 /* Bias vectors via L ("ROAST uses L to implement ... bias vectors").  A bias of
  * n elements is row 0 of an embedding registered as (num_rows 1, dim n, chunk Z,
  * fan_in = the owning layer's in_features, reading R24).

@@ -489,6 +489,30 @@ roast_status_t roast_linear_bwd_dx_chain(roast_t h, int32_t id_a, int32_t id_b, 
   return roast_linear_bwd_dx(h, id_a, dY_a, dX, T, dt, stream);
 }
 
+roast_status_t roast_linear_bwd_chain(roast_t h, int32_t id_a, int32_t id_b, const void* X_a, const void* Y_a,
+                                      const void* dY_b, void* dY_a, void* dX_a, int64_t T, roast_dtype_t dt,
+                                      roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module *ma, *mb;
+  roast_status_t st = get_module(c, id_a, kLinear, &ma);
+  if (st) return st;
+  if ((st = get_module(c, id_b, kLinear, &mb))) return st;
+  if (ma->O != mb->H) return fail(ROAST_ERR_SHAPE, "chain: out_features of a != in_features of b");
+  if (T < 0) return fail(ROAST_ERR_SHAPE, "tokens < 0");
+  if (T > 0 && (!X_a || !Y_a || !dY_b || !dY_a || !dX_a)) return fail(ROAST_ERR_CONFIG, "null tensor argument");
+  if (dt != ROAST_FP32 && dt != ROAST_BF16) return fail(ROAST_ERR_CONFIG, "bad dtype");
+  if (T == 0) return ROAST_OK;
+  const cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (dt == ROAST_BF16 && use_sm100(c, *ma) && use_sm100(c, *mb)) {
+    st = sm100_bwd_chain(c, *ma, *mb, X_a, Y_a, dY_b, dY_a, dX_a, T, s);
+    if (st != ROAST_ERR_UNSUPPORTED) return st;
+  }
+  if ((st = roast_linear_bwd_dx(h, id_b, dY_b, dY_a, T, dt, stream))) return st;
+  if ((st = roast_linear_bwd_dm(h, id_b, Y_a, dY_b, T, dt, stream))) return st;
+  if ((st = roast_linear_bwd_dx(h, id_a, dY_a, dX_a, T, dt, stream))) return st;
+  return roast_linear_bwd_dm(h, id_a, X_a, dY_a, T, dt, stream);
+}
+
 roast_status_t roast_bias_fwd(roast_t h, int32_t bias_id, float* b, roast_stream_t stream) {
   Ctx* c = ctx(h);
   Module* m;

@@ -882,6 +882,405 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------- fused backward (MIX)
+// The whole backward of a chained layer pair a -> b (Y_a = X_a W_a, Y_b = Y_a W_b) in ONE
+// persistent launch, its four GEMMs co-scheduled on the 74 CTA pairs (Alg. 1):
+//   P0  DX  dY_a = lambda_b dY_b W~_b^T               (WM = 2, register-held epilogue)
+//   P1  DW  dM  += scatter_b(lambda_b g  Y_a^T dY_b)  (WM = 1, split-K, TMA reduce-add)
+//   P2  DX  dX_a = lambda_a dY_a W~_a^T               (A = P0's output: waits on P0's tiles)
+//   P3  DW  dM  += scatter_a(lambda_a g  X_a^T dY_a)  (B = P0's output: waits on P0's tiles)
+// Alone, each GEMM is quantised on its own unit grid (C2: 192 / 72 / 48 / 72 units for 74
+// pairs) and the two-stream overlap of separate launches is left to the hardware.  Here every
+// pair walks a static unit list from a list-scheduling simulation (host, plan_mix): P0's units
+// first on every pair (so no wait can deadlock: all pairs are co-resident, checked at plan
+// time), P1 units as filler, P2 / P3 units as soon as the P0 tiles they read are published.
+// TMEM is split into two 256-column halves with their own full / empty barriers: a DX unit
+// (512 x 256 per pair) takes both, a DW unit (256 x 256) one, alternating, so DW units are
+// double-buffered and DX units drain into registers before their stores.
+struct MixProb {
+  int mode;                 // DX or DW
+  int M, N, K;              // GEMM dims (DX: M = tokens; DW: M = in_features, K = tokens)
+  int m_tiles, n_tiles, k_blocks, kb_per_split, units;
+  const int32_t* coord;     // DX: packed hash-tile TMA coordinates [y][x] (K-major B)
+  int coord_ld;
+  const int64_t* off;       // DW: tile offsets / signs [x][y]
+  const int8_t* sgn;
+  int ny;
+  float lam;
+  int dep;                  // problem whose output tiles this one reads (0) or -1
+  int publish;              // 1: this problem's units publish ready counters (P0)
+};
+struct MixParams {
+  MixProb p[4];
+  int64_t neg_row;          // row (128 B) of the negated shadow copy
+  const int32_t* sched;     // [pairs][sched_len] codes prob << 24 | unit, -1 = end
+  int sched_len;
+  int* flags;               // ready counters of the publishing problem's units
+  int dep_n_tiles;          // n_tiles of the publishing problem (flag index = mb * this + nb)
+  int* err;                 // sticky device error word
+  long long* prof;
+};
+struct MixMaps {
+  CUtensorMap a[4];         // DX: A (tokens x K); DW: X blocks (3-D)
+  CUtensorMap b[4];         // DX: output (tokens x N); DW: dY blocks (3-D)
+  WMaps shadow;             // bf16 shadow, 8 phase views (DX B tiles)
+  WMaps dm;                 // dM, 8 fp32 phase views (DW reduce-add)
+};
+
+constexpr int MIX_THREADS = 384;
+constexpr int MIX_STAGES = 4;
+constexpr int MIX_A = 32768, MIX_B = 16384;          // per-stage A / B slots (DX sizes; DW uses 16 + 16 KB)
+constexpr int MIX_SMEM = MIX_STAGES * (MIX_A + MIX_B) + 8 * 4096 + 1024 + 256 + KB_CHUNK * 4 * 4;
+
+__device__ __forceinline__ void mbar_arrive_cluster_n(uint32_t cluster_addr, uint32_t n) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr), "r"(n)
+               : "memory");
+}
+
+__device__ __forceinline__ void mix_decode(const MixProb& P, int u, int& mb, int& nb, int& split) {
+  split = u / (P.m_tiles * P.n_tiles);
+  const int r = u - split * P.m_tiles * P.n_tiles;
+  mb = r / P.n_tiles;
+  nb = r - mb * P.n_tiles;
+}
+
+__global__ void __launch_bounds__(MIX_THREADS, 1)
+    roast_mix_sm100(const __grid_constant__ MixMaps maps, const __grid_constant__ MixParams mp) {
+  constexpr int CG = 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                                           // [STAGES][32 KB]
+  uint8_t* sB = smem + MIX_STAGES * MIX_A;                      // [STAGES][16 KB]
+  uint8_t* sStage = smem + MIX_STAGES * (MIX_A + MIX_B);        // [8 warps][4 KB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStage + 8 * 4096);
+  uint64_t* empty = full + MIX_STAGES;
+  uint64_t* tfull = empty + MIX_STAGES;                         // per TMEM half
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int32_t* sCoord = reinterpret_cast<int32_t*>(sStage + 8 * 4096 + 256);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x / CG;
+  auto unit_at = [&](int i, int& prob, int& u) -> bool {
+    if (i >= mp.sched_len) return false;
+    const int code = __ldg(mp.sched + pair * mp.sched_len + i);
+    if (code < 0) return false;
+    prob = code >> 24;
+    u = code & 0xFFFFFF;
+    return true;
+  };
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < MIX_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&tfull[h], 1);
+      mbar_init(&tempty[h], 8 * CG);   // DW: 8 warps x 1; DX: the half's 4 warps x 2
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int i = 0; i < 4; ++i) {
+      prefetch_map(&maps.a[i]);
+      prefetch_map(&maps.b[i]);
+    }
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  auto tmem_base_ld = [&]() -> uint32_t { return *reinterpret_cast<volatile uint32_t*>(tmem_slot); };
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp == 0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    // ===================== TMA producer =====================
+    int s = 0;
+    uint32_t ph = 0;
+    for (int it = 0;; ++it) {
+      int prob, u;
+      if (!unit_at(it, prob, u)) break;
+      const MixProb& P = mp.p[prob];
+      const CUtensorMap* mA = &maps.a[prob];
+      int mb, nb, split;
+      mix_decode(P, u, mb, nb, split);
+      const int kb0 = split * P.kb_per_split;
+      const int kb1 = min(kb0 + P.kb_per_split, P.k_blocks);
+      if (P.mode == DX) {
+        const int row0 = mb * 512 + int(rank) * 256;
+        const uint32_t tx = uint32_t(CG * MIX_A + 4 * 8192);
+        for (int kc = kb0; kc < kb1; kc += KB_CHUNK) {
+          const int kc1 = min(kc + KB_CHUNK, kb1);
+          __syncwarp();
+          for (int i = lane; i < (kc1 - kc) * 4; i += 32)
+            sCoord[i] = __ldg(P.coord + int64_t(kc + (i >> 2)) * P.coord_ld + nb * 4 + (i & 3));
+          __syncwarp();
+          if (lane == 0) {
+            for (int kb = kc; kb < kc1; ++kb) {
+              mbar_wait(&empty[s], ph ^ 1);
+              const uint32_t fb = map_to_rank(smem_u32(&full[s]), 0);
+              if (leader) mbar_expect_tx(&full[s], tx);
+              // A = the dependency's output tile (mb, kb / 4) once it is published
+              if (P.dep >= 0 && (kb & 3) == 0) wait_ready(mp.flags + mb * mp.dep_n_tiles + (kb >> 2), 8 * CG, mp.err);
+              tma_load_2d<CG>(mA, sA + s * MIX_A, fb, kb * BK, row0);
+              const int32_t* cc = sCoord + (kb - kc) * 4;
+              for (int j = 0; j < 2; ++j) {   // this CTA's two 64-row K-major B tiles (x = nb*4 + 2 rank + j, y = kb)
+                const int32_t c = cc[int(rank) * 2 + j];
+                const int row = (c >> 4) + ((c & 8) ? int(mp.neg_row) : 0);
+                tma_load_2d<CG>(&maps.shadow.m[c & 7], sB + s * MIX_B + j * 8192, fb, 0, row);
+              }
+              if (++s == MIX_STAGES) {
+                s = 0;
+                ph ^= 1;
+              }
+            }
+          }
+        }
+      } else {   // DW: X^T and dY as 3-D MN-major boxes (2 x 64-wide blocks each per CTA)
+        const int row0 = mb * 256 + int(rank) * 128;
+        const int col0 = nb * 256 + int(rank) * 128;
+        const uint32_t tx = uint32_t(CG * (16384 + 16384));
+        if (lane == 0) {
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(&empty[s], ph ^ 1);
+            const uint32_t fb = map_to_rank(smem_u32(&full[s]), 0);
+            if (leader) mbar_expect_tx(&full[s], tx);
+            // B = the dependency's output rows kb*64.. (its m-block kb / 8), columns of tile nb
+            if (P.dep >= 0 && (kb == kb0 || (kb & 7) == 0))
+              wait_ready(mp.flags + (kb >> 3) * mp.dep_n_tiles + nb, 8 * CG, mp.err);
+            tma_load_3d<CG>(mA, sA + s * MIX_A, fb, 0, kb * BK, row0 >> 6);
+            tma_load_3d<CG>(&maps.b[prob], sB + s * MIX_B, fb, 0, kb * BK, col0 >> 6);
+            if (++s == MIX_STAGES) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    if (lane == 0 && leader) {
+      // ===================== MMA issuer (leader CTA, one thread) =====================
+      constexpr uint32_t idesc_dx = make_idesc(0, 0, 256, 256);
+      constexpr uint32_t idesc_dw = make_idesc(1, 1, 256, 256);
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t use[2] = {0, 0};   // uses of each TMEM half so far (phase of its empty barrier)
+      int dwh = 0;                // TMEM half of the next DW unit (alternates)
+      for (int it = 0;; ++it) {
+        int prob, u;
+        if (!unit_at(it, prob, u)) break;
+        const MixProb& P = mp.p[prob];
+        int mb, nb, split;
+        mix_decode(P, u, mb, nb, split);
+        const int kb0 = split * P.kb_per_split;
+        const int kb1 = min(kb0 + P.kb_per_split, P.k_blocks);
+        const uint32_t tbase = tmem_base_ld();
+        if (P.mode == DX) {
+          mbar_wait(&tempty[0], (use[0] & 1) ^ 1);
+          mbar_wait(&tempty[1], (use[1] & 1) ^ 1);
+          tc_fence_after();
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(sA + s * MIX_A);
+            const uint32_t b0 = smem_u32(sB + s * MIX_B);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t bd = sw128_desc(b0 + k * 32, 16, 1024);   // K-major B
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+                tc_mma<CG>(tbase + uint32_t(j * 256), sw128_desc(a0 + uint32_t(j * BM * 128) + k * 32, 16, 1024), bd,
+                           idesc_dx, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
+            tc_commit<CG>(&empty[s]);
+            if (++s == MIX_STAGES) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+          tc_commit<CG>(&tfull[0]);
+          tc_commit<CG>(&tfull[1]);
+          ++use[0];
+          ++use[1];
+        } else {
+          const int h = dwh;
+          dwh ^= 1;
+          mbar_wait(&tempty[h], (use[h] & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tbase + uint32_t(h * 256);
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(sA + s * MIX_A);
+            const uint32_t b0 = smem_u32(sB + s * MIX_B);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              tc_mma<CG>(d, sw128_desc(a0 + k * 2048, 8192, 1024), sw128_desc(b0 + k * 2048, 8192, 1024), idesc_dw,
+                         (kb > kb0 || k > 0) ? 1u : 0u);
+            tc_commit<CG>(&empty[s]);
+            if (++s == MIX_STAGES) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+          tc_commit<CG>(&tfull[h]);
+          ++use[h];
+        }
+      }
+    }
+  } else if (warp < EPI_WARP0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");   // warps 2, 3
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    // ===================== epilogue (8 warps) =====================
+    const int q = warp & 3;                  // TMEM lane quadrant
+    const int jh = (warp - EPI_WARP0) >> 2;  // DX: M sub-tile (= TMEM half); DW: column half
+    uint8_t* buf = sStage + (warp - EPI_WARP0) * 4096;
+    const uint32_t tempty_leader0 = map_to_rank(smem_u32(&tempty[0]), 0);
+    uint32_t use[2] = {0, 0};
+    int dwh = 0;
+    for (int it = 0;; ++it) {
+      int prob, u;
+      if (!unit_at(it, prob, u)) break;
+      const MixProb& P = mp.p[prob];
+      int mb, nb, split;
+      mix_decode(P, u, mb, nb, split);
+      if (P.mode == DX) {
+        mbar_wait(&tfull[jh], use[jh] & 1);
+        ++use[0];
+        ++use[1];
+        tc_fence_after();
+        const uint32_t tb = tmem_base_ld() + uint32_t(jh * 256) + (uint32_t(q * 32) << 16);
+        const int nsteps = min(256, P.N - nb * 256) / 64;
+        uint32_t pk[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c < nsteps) {
+            uint32_t r[64];
+            TMEM_LD32(tb + uint32_t(c * 64), r);
+            TMEM_LD32(tb + uint32_t(c * 64 + 32), (r + 32));
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              __nv_bfloat162 v = __floats2bfloat162_rn(P.lam * __uint_as_float(r[2 * i]), P.lam * __uint_as_float(r[2 * i + 1]));
+              pk[c * 32 + i] = *reinterpret_cast<uint32_t*>(&v);
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster_n(tempty_leader0 + uint32_t(jh * 8), 2);
+        const int row0 = mb * 512 + int(rank) * 256 + jh * BM + q * 32;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c < nsteps) {
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) {
+              const uint32_t a = smem_u32(buf + lane * 128 + ((cc ^ (lane & 7)) << 4));
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pk[c * 32 + 4 * cc]),
+                           "r"(pk[c * 32 + 4 * cc + 1]), "r"(pk[c * 32 + 4 * cc + 2]), "r"(pk[c * 32 + 4 * cc + 3])
+                           : "memory");
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                               reinterpret_cast<uint64_t>(&maps.b[prob])),
+                           "r"(nb * 256 + c * 64), "r"(row0), "r"(smem_u32(buf))
+                           : "memory");
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+          }
+        }
+        if (P.publish) {   // this warp's 32 rows of the tile are in global memory: release them
+          if (lane == 0) {
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(mp.flags + u) : "memory");
+          }
+          __syncwarp();
+        }
+      } else {
+        // DW: this warp's 32 rows (hash-tile row x) x 128 columns (hash tiles y = 4 nb + 2 jh, +1)
+        const int h = dwh;
+        dwh ^= 1;
+        const int rb = mb * 256 + int(rank) * 128 + q * 32;
+        int64_t t_off = 0;
+        float t_scale = 0.f;
+        {
+          const int y = nb * 4 + (lane & 3);
+          if (lane < 4 && rb < P.M && y * 64 < P.N) {
+            const int t = (rb >> 6) * P.ny + y;
+            t_off = P.off[t];
+            t_scale = P.sgn[t] < 0 ? -P.lam : P.lam;
+          }
+        }
+        mbar_wait(&tfull[h], use[h] & 1);
+        ++use[h];
+        tc_fence_after();
+        const uint32_t tb = tmem_base_ld() + uint32_t(h * 256) + (uint32_t(q * 32) << 16);
+        const int nvalid = min(256, P.N - nb * 256) / 32;
+#pragma unroll 1
+        for (int c = jh * 4; c < jh * 4 + 4; ++c) {
+          const float scale = __shfl_sync(0xffffffffu, t_scale, c >> 1);
+          const int64_t tbo = __shfl_sync(0xffffffffu, t_off, c >> 1);
+          if (c >= nvalid) continue;
+          uint32_t r[32];
+          TMEM_LD32(tb + uint32_t(c * 32), r);
+          tmem_wait_ld();
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            const uint32_t a = smem_u32(buf + lane * 128 + ((cc ^ (lane & 7)) << 4));
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                         "r"(__float_as_uint(scale * __uint_as_float(r[4 * cc]))),
+                         "r"(__float_as_uint(scale * __uint_as_float(r[4 * cc + 1]))),
+                         "r"(__float_as_uint(scale * __uint_as_float(r[4 * cc + 2]))),
+                         "r"(__float_as_uint(scale * __uint_as_float(r[4 * cc + 3])))
+                         : "memory");
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0 && rb < P.M) {   // TMA reduce-add into dM (32 rows x 32 fp32 of one hash tile)
+            const int x0 = (c & 1) * 32;
+            const int y0 = int(tbo >> 6) + (rb & 63);
+            asm volatile(
+                "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                    reinterpret_cast<uint64_t>(&maps.dm.m[(tbo >> 3) & 7])),
+                "r"(x0), "r"(y0), "r"(smem_u32(buf))
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster_n(tempty_leader0 + uint32_t(h * 8), 1);
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_ld()), "r"(TMEM_COLS));
+}
+
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1537,4 +1936,275 @@ roast_status_t sm100_dw(Ctx* c, const Module& m, const void* X, const void* dY, 
   return dw_launch(c, m, X, dY, T, wm, splits, s);
 }
 
+}  // namespace roast
+
+// ---- fused backward of a chained pair (roast_linear_bwd_chain) ------------------------------
+namespace roast {
+namespace {
+struct MixPlan {
+  std::vector<int32_t> sched;   // [pairs][len], -1 padded
+  int len = 0, s1 = 2, s3 = 2;
+  double makespan = 1e30, separate = 0;
+};
+
+// List-scheduling simulation of the four problems on `npairs` CTA pairs, in units of one WM = 2
+// DX k-block (1024 MMA clocks; a DW k-block is half of it).  P0's units go first on every pair
+// (in m- or n-major order); then each pair, when free, takes the next unit of the first class in
+// the priority order whose data is ready (P2: P0 tiles (mb, 0..) published; P3: the P0 tiles of
+// its token range), P1 (no dependency) as filler, else waits for the earliest ready one.
+// Dependent units stream their K loop behind the P0 tiles they read.
+MixPlan plan_mix(int mt0, int nt0, int kb0, int mt1, int nt1, int kbT, int mt2, int nt2, int kb2, int mt3, int nt3,
+                 int npairs) {
+  const double EPI_DX = 3.0, EPI_DW = 1.0, LAT = 1.0;
+  MixPlan best;
+  const int units0 = mt0 * nt0;
+  for (int s : {1, 2, 3, 4}) {
+    const int kps = (kbT + s - 1) / s;
+    const int sp = (kbT + kps - 1) / kps;
+    const int units1 = mt1 * nt1 * sp, units3 = mt3 * nt3 * sp, units2 = mt2 * nt2;
+    for (int order = 0; order < 2; ++order)
+      for (int prio = 0; prio < 3; ++prio) {
+        std::vector<double> free_t(npairs, 0.0), fin0(units0, 0.0);
+        std::vector<std::vector<int32_t>> lists(npairs);
+        auto pick = [&]() { return int(std::min_element(free_t.begin(), free_t.end()) - free_t.begin()); };
+        for (int i = 0; i < units0; ++i) {
+          const int u = order == 0 ? i : (i % mt0) * nt0 + i / mt0;
+          const int q = pick();
+          fin0[u] = free_t[q] + kb0 + EPI_DX;
+          free_t[q] = fin0[u];
+          lists[q].push_back(u);
+        }
+        // dependent units: ready time of their first k-block group, and finish time from a start
+        auto p2_ready = [&](int u) { return fin0[(u / nt2) * nt0] + LAT; };
+        auto p2_finish = [&](int u, double t) {
+          const int mb = u / nt2;
+          for (int g = 0; g < nt0; ++g) t = std::max(t, fin0[mb * nt0 + g] + LAT) + double(kb2) / nt0;
+          return t + EPI_DX;
+        };
+        auto p3_range = [&](int u, int& k0, int& k1, int& nb) {
+          const int split = u / (mt3 * nt3), r = u % (mt3 * nt3);
+          nb = r % nt3;
+          k0 = split * kps;
+          k1 = std::min(k0 + kps, kbT);
+        };
+        auto p3_ready = [&](int u) {
+          int k0, k1, nb;
+          p3_range(u, k0, k1, nb);
+          return fin0[std::min(k0 >> 3, mt0 - 1) * nt0 + nb] + LAT;
+        };
+        auto p3_finish = [&](int u, double t) {
+          int k0, k1, nb;
+          p3_range(u, k0, k1, nb);
+          for (int k = k0; k < k1; k += 8) {
+            const int ke = std::min(k1, (k & ~7) + 8);
+            t = std::max(t, fin0[std::min(k >> 3, mt0 - 1) * nt0 + nb] + LAT) + 0.5 * (ke - k);
+            k = (k & ~7);
+          }
+          return t + EPI_DW;
+        };
+        // P3 units in token order (earliest-ready first), P2 in m order, P1 as given
+        std::vector<int> q1(units1), q2(units2), q3(units3);
+        for (int i = 0; i < units1; ++i) q1[i] = i;
+        for (int i = 0; i < units2; ++i) q2[i] = i;
+        for (int i = 0; i < units3; ++i) q3[i] = i;
+        std::stable_sort(q3.begin(), q3.end(), [&](int a, int b) { return p3_ready(a) < p3_ready(b); });
+        size_t i1 = 0, i2 = 0, i3 = 0;
+        const int classes[3][3] = {{2, 3, 1}, {3, 2, 1}, {2, 1, 3}};
+        while (i1 < q1.size() || i2 < q2.size() || i3 < q3.size()) {
+          const int q = pick();
+          const double now = free_t[q];
+          int cls = -1;
+          for (int c : classes[prio]) {
+            if (c == 1 && i1 < q1.size()) { cls = 1; break; }
+            if (c == 2 && i2 < q2.size() && p2_ready(q2[i2]) <= now + 2.0) { cls = 2; break; }
+            if (c == 3 && i3 < q3.size() && p3_ready(q3[i3]) <= now + 2.0) { cls = 3; break; }
+          }
+          if (cls < 0) {   // nothing ready and no filler left: the earliest-ready dependent unit
+            const double r2 = i2 < q2.size() ? p2_ready(q2[i2]) : 1e30, r3 = i3 < q3.size() ? p3_ready(q3[i3]) : 1e30;
+            cls = r2 <= r3 ? 2 : 3;
+          }
+          if (cls == 1) {
+            free_t[q] = now + 0.5 * kps + EPI_DW;
+            lists[q].push_back((1 << 24) | q1[i1++]);
+          } else if (cls == 2) {
+            free_t[q] = p2_finish(q2[i2], now);
+            lists[q].push_back((2 << 24) | q2[i2++]);
+          } else {
+            free_t[q] = p3_finish(q3[i3], now);
+            lists[q].push_back((3 << 24) | q3[i3++]);
+          }
+        }
+        const double mk = *std::max_element(free_t.begin(), free_t.end());
+        if (mk < best.makespan - 1e-9) {
+          best.makespan = mk;
+          best.s1 = best.s3 = sp;
+          best.len = 0;
+          for (auto& l : lists) best.len = std::max<int>(best.len, int(l.size()));
+          best.sched.assign(size_t(npairs) * best.len, -1);
+          for (int q = 0; q < npairs; ++q)
+            for (size_t i = 0; i < lists[q].size(); ++i) best.sched[size_t(q) * best.len + i] = lists[q][i];
+        }
+      }
+  }
+  return best;
+}
+}  // namespace
+
+roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, const void* X_a, const void* Y_a,
+                               const void* dY_b, void* dY_a, void* dX_a, int64_t T, cudaStream_t s) {
+  using namespace sm100;
+  if (!supported(c, ma) || !supported(c, mbm) || cta_group() != 2 || T <= 0 || T >= (int64_t(1) << 31) ||
+      c->cfg.deterministic || getenv("ROAST_NO_BWD_FUSE"))
+    return ROAST_ERR_UNSUPPORTED;
+  if (ma.H % 256 || ma.O % 256 || mbm.O % 256 || mbm.H != ma.O || !dX_a) return ROAST_ERR_UNSUPPORTED;
+  const int pairs = num_sms() / 2;
+  const int mtT = int((T + 511) / 512), kbT = int((T + BK - 1) / BK);
+  const std::array<int64_t, 6> key{2, ma.H, ma.O, mbm.H, mbm.O, T};
+  auto it = c->chain_plans.find(key);
+  static std::map<std::array<int64_t, 6>, std::pair<int, int>> splits;   // plan key -> (s1, s3)
+  if (it == c->chain_plans.end()) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+      return ROAST_ERR_UNSUPPORTED;   // planning allocates: plan on an eager call first
+    bool resident = false;
+    {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(unsigned(2 * pairs));
+      q.blockDim = dim3(MIX_THREADS);
+      q.dynamicSmemBytes = MIX_SMEM;
+      cudaLaunchAttribute a[1];
+      a[0].id = cudaLaunchAttributeClusterDimension;
+      a[0].val.clusterDim.x = 2;
+      a[0].val.clusterDim.y = 1;
+      a[0].val.clusterDim.z = 1;
+      q.attrs = a;
+      q.numAttrs = 1;
+      int ncl = 0;
+      if (cudaFuncSetAttribute(roast_mix_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, MIX_SMEM) == cudaSuccess &&
+          cudaOccupancyMaxActiveClusters(&ncl, roast_mix_sm100, &q) == cudaSuccess)
+        resident = ncl >= pairs;
+      cudaGetLastError();
+    }
+    MixPlan plan = plan_mix(mtT, int(mbm.H / 256), int(mbm.O / BK), int(mbm.H / 256), int(mbm.O / 256), kbT, mtT,
+                            int(ma.H / 256), int(ma.O / BK), int(ma.H / 256), int(ma.O / 256), pairs);
+    int32_t* d = nullptr;
+    if (resident) {
+      ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&d), plan.sched.size() * sizeof(int32_t)));
+      ROAST_CUDA_CHECK(cudaMemcpy(d, plan.sched.data(), plan.sched.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    if (getenv("ROAST_VERBOSE"))
+      fprintf(stderr, "[roast] bwd chain plan: makespan %.1f (k-block units), split %d, len %d, resident %d\n",
+              plan.makespan, plan.s1, plan.len, int(resident));
+    it = c->chain_plans.emplace(key, std::make_pair(d, plan.len)).first;
+    splits[key] = {plan.s1, plan.s3};
+  }
+  if (!it->second.first) return ROAST_ERR_UNSUPPORTED;
+  roast_status_t st = sm100_prepare(c);
+  if (st) return st;
+  const int s1 = splits[key].first, s3 = splits[key].second;
+  MixMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  MixParams mp;
+  memset(&mp, 0, sizeof(mp));
+  auto dx_prob = [&](MixProb& P, const Module& m, const void* A, void* out, int pi) -> roast_status_t {
+    P.mode = DX;
+    P.M = int(T);
+    P.N = int(m.H);
+    P.K = int(m.O);
+    P.m_tiles = mtT;
+    P.n_tiles = int(m.H / 256);
+    P.k_blocks = int(m.O / BK);
+    P.kb_per_split = P.k_blocks;
+    P.units = P.m_tiles * P.n_tiles;
+    P.coord = m.d_coord_yx;
+    P.coord_ld = m.nx;
+    P.lam = m.lam;
+    P.dep = -1;
+    roast_status_t r = make_map_2d(&maps.a[pi], A, uint64_t(m.O), uint64_t(T), uint64_t(m.O) * 2, BK, 256);
+    if (r) return r;
+    return make_map_2d(&maps.b[pi], out, uint64_t(m.H), uint64_t(T), uint64_t(m.H) * 2, 64, 32);
+  };
+  auto dw_prob = [&](MixProb& P, const Module& m, const void* X, const void* dY, int sp, int pi) -> roast_status_t {
+    P.mode = DW;
+    P.M = int(m.H);
+    P.N = int(m.O);
+    P.K = int(T);
+    P.m_tiles = int(m.H / 256);
+    P.n_tiles = int(m.O / 256);
+    P.k_blocks = kbT;
+    P.kb_per_split = (kbT + sp - 1) / sp;
+    P.units = P.m_tiles * P.n_tiles * ((kbT + P.kb_per_split - 1) / P.kb_per_split);
+    P.off = m.d_off;
+    P.sgn = m.d_sgn;
+    P.ny = m.ny;
+    P.lam = m.lam;
+    P.dep = -1;
+    roast_status_t r = make_map_blocks(&maps.a[pi], X, uint64_t(m.H), uint64_t(T), BK, 2);
+    if (r) return r;
+    return make_map_blocks(&maps.b[pi], dY, uint64_t(m.O), uint64_t(T), BK, 2);
+  };
+  if ((st = dx_prob(mp.p[0], mbm, dY_b, dY_a, 0))) return st;
+  if ((st = dw_prob(mp.p[1], mbm, Y_a, dY_b, s1, 1))) return st;
+  if ((st = dx_prob(mp.p[2], ma, dY_a, dX_a, 2))) return st;
+  if ((st = dw_prob(mp.p[3], ma, X_a, dY_a, s3, 3))) return st;
+  mp.p[0].publish = 1;
+  mp.p[2].dep = 0;
+  mp.p[3].dep = 0;
+  mp.dep_n_tiles = mp.p[0].n_tiles;
+  mp.neg_row = c->neg_base / 64;
+  mp.sched = it->second.first;
+  mp.sched_len = it->second.second;
+  mp.err = c->d_err;
+  maps.shadow = *reinterpret_cast<const WMaps*>(c->tmap_shadow);
+  WMaps& dmaps = *reinterpret_cast<WMaps*>(c->tmap_dm);
+  if (c->tmap_dm_for != c->dM) {   // dM as 8 fp32 phase views (cached until dM is rebound)
+    for (int r = 0; r < 8; ++r) {
+      const int64_t elems = c->mem_size - 8 * r;
+      st = make_map_2d(&dmaps.m[r], c->dM + 8 * r, 64, uint64_t(elems / 64), 256, 32, 32, true);
+      if (st) return st;
+    }
+    c->tmap_dm_for = c->dM;
+  }
+  maps.dm = dmaps;
+  // ready counters of P0's units: the next slot of the chain ring (as sm100_chain)
+  const int64_t need = mp.p[0].units;
+  if (c->chain_slot_n < need) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+      return ROAST_ERR_UNSUPPORTED;
+    ROAST_CUDA_CHECK(cudaDeviceSynchronize());
+    cudaFree(c->chain_flags);
+    c->chain_flags = nullptr;
+    c->chain_slot_n = 0;
+    ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->chain_flags), size_t(kChainSlots) * need * sizeof(int)));
+    c->chain_slot_n = need;
+  }
+  mp.flags = c->chain_flags + int64_t(c->chain_next++ % kChainSlots) * c->chain_slot_n;
+  ROAST_CUDA_CHECK(cudaMemsetAsync(mp.flags, 0, size_t(need) * sizeof(int), s));
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(roast_mix_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, MIX_SMEM);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(mix smem)");
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(pairs * 2));
+  cfg.blockDim = dim3(MIX_THREADS);
+  cfg.dynamicSmemBytes = MIX_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  static const bool pdl = !(getenv("ROAST_PDL") && atoi(getenv("ROAST_PDL")) == 0);
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mix_sm100, maps, mp);
+  if (e != cudaSuccess) return cuda_fail(e, "roast_mix_sm100 launch");
+  c->launches++;
+  return ROAST_OK;
+}
 }  // namespace roast

@@ -239,6 +239,12 @@ roast_status_t sm100_fwd(Ctx* c, const Module& m, const void* X, void* Y, int64_
 roast_status_t sm100_chain(Ctx* c, const Module& m0, const Module& m1, const void* A0, void* out0, void* out1,
                            int64_t T, bool dx, const float* bias0, const float* bias1, cudaStream_t s);
 roast_status_t sm100_dx(Ctx* c, const Module& m, const void* dY, void* dX, int64_t T, cudaStream_t s);
+// the whole backward of a chained pair a -> b (Y_a = X_a W_a, Y_b = Y_a W_b) in one persistent
+// launch: dY_a = dY_b W_b^T, dM += b(Y_a, dY_b), dX_a = dY_a W_a^T, dM += a(X_a, dY_a), the four
+// GEMMs co-scheduled (gemm_sm100.cu roast_mix_sm100).  ROAST_ERR_UNSUPPORTED when the shapes /
+// mode do not allow it (the caller then makes the four launches).
+roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mb, const void* X_a, const void* Y_a,
+                               const void* dY_b, void* dY_a, void* dX_a, int64_t T, cudaStream_t s);
 roast_status_t sm100_dw(Ctx* c, const Module& m, const void* X, const void* dY, int64_t T, cudaStream_t s);
 
 }  // namespace roast

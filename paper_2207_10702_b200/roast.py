@@ -27,7 +27,7 @@ EXPORTS = [
     "roast_linear_bwd_dx", "roast_linear_bwd_dm", "roast_embedding_fwd", "roast_embedding_bwd",
     "roast_embedding_fwd_multi", "roast_embedding_bwd_multi", "roast_set_autotune", "roast_get_tuned", "roast_set_tuned",
     "roast_linear_fwd_bias", "roast_bias_fwd", "roast_bias_bwd", "roast_bias_bwd_ld", "roast_colsum", "roast_colsum_ex", "roast_register_linear_concat", "roast_linear_fwd_chain",
-    "roast_linear_bwd_dx_chain", "roast_comm_unique_id", "roast_comm_init",
+    "roast_linear_bwd_dx_chain", "roast_linear_bwd_chain", "roast_comm_unique_id", "roast_comm_init",
     "roast_grad_allreduce", "roast_set_exchange", "roast_touched_size", "roast_touched_intervals",
     "roast_debug_exchange", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step", "roast_grad_exchange_step",
     "roast_p2p_window", "roast_p2p_ipc_handle", "roast_p2p_open", "roast_p2p_attach", "roast_p2p_post",
@@ -86,6 +86,7 @@ def _load():
         "roast_bias_fwd": (st, [H, I32, P, S]),
         "roast_linear_fwd_chain": (st, [H, I32, I32, P, P, P, I64, ctypes.c_int, P, P, S]),
         "roast_linear_bwd_dx_chain": (st, [H, I32, I32, P, P, P, I64, ctypes.c_int, S]),
+        "roast_linear_bwd_chain": (st, [H, I32, I32, P, P, P, P, P, I64, ctypes.c_int, S]),
         "roast_bias_bwd": (st, [H, I32, P, I64, ctypes.c_int, S]),
         "roast_bias_bwd_ld": (st, [H, I32, P, I64, I64, ctypes.c_int, S]),
         "roast_colsum": (st, [P, I64, I32, I64, ctypes.c_int, P, S]),
@@ -243,6 +244,11 @@ def roast_linear_fwd_bias(h, mid, X_ptr, Y_ptr, tokens, dtype, bias_ptr, stream=
 def roast_linear_fwd_chain(h, id_a, id_b, X_ptr, Ya_ptr, Yb_ptr, tokens, dtype, bias_a=None, bias_b=None, stream=0):
     _check(_lib.roast_linear_fwd_chain(h, id_a, id_b, X_ptr, Ya_ptr, Yb_ptr, tokens, dtype, bias_a, bias_b, stream),
            "roast_linear_fwd_chain")
+
+
+def roast_linear_bwd_chain(h, id_a, id_b, Xa_ptr, Ya_ptr, dYb_ptr, dYa_ptr, dXa_ptr, tokens, dtype, stream=0):
+    _check(_lib.roast_linear_bwd_chain(h, id_a, id_b, Xa_ptr, Ya_ptr, dYb_ptr, dYa_ptr, dXa_ptr, tokens, dtype, stream),
+           "roast_linear_bwd_chain")
 
 
 def roast_linear_bwd_dx_chain(h, id_a, id_b, dYb_ptr, dYa_ptr, dX_ptr, tokens, dtype, stream=0):
@@ -663,6 +669,18 @@ class Roast:
         roast_linear_bwd_dx_chain(self.h, a, b, dYb.data_ptr(), dYa.data_ptr(), dX.data_ptr(), T, self._dt(dYb),
                                   self._s(stream))
         return dYa, dX
+
+    def bwd_chain(self, a, b, Xa, Ya, dYb, dYa=None, dXa=None, stream=None):
+        """The backward of fwd_chain(a, b): dY_a = dY_b W~_b^T, dM += b(Y_a, dY_b), dX_a = dY_a W~_a^T,
+        dM += a(X_a, dY_a) — on the tcgen05 path one persistent launch; returns (dY_a, dX_a)."""
+        _, H, O = self.dims[a]
+        _, H2, O2 = self.dims[b]
+        T = dYb.numel() // O2
+        dYa = self.torch.empty(T, H2, dtype=dYb.dtype, device=dYb.device) if dYa is None else dYa
+        dXa = self.torch.empty(T, H, dtype=dYb.dtype, device=dYb.device) if dXa is None else dXa
+        roast_linear_bwd_chain(self.h, a, b, Xa.data_ptr(), Ya.data_ptr(), dYb.data_ptr(), dYa.data_ptr(),
+                               dXa.data_ptr(), T, self._dt(dYb), self._s(stream))
+        return dYa, dXa
 
     def bias_fwd(self, bias_mid, out=None, stream=None):
         """The bias vector (row 0 of a 1 x n embedding registered for it) recovered with L."""
