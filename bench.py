@@ -379,6 +379,20 @@ class C2Step:
         # GEMM tuned alone may pick 192-column units, which fill more CTA pairs but leave fewer
         # SMs to the dM GEMM running beside it on the second stream; keep whichever whole step
         # (graph-replayed, L2 flushed) is faster
+        # the backward's schedule, training-optimal at the step level: the fused launch unless the
+        # separate dX / dM launches on two streams make the whole step faster (e.g. at 1000x the
+        # tiny dM's reduce-add hot spot favours spreading the dM GEMMs out)
+        if autotune == 2 and not tuned_file and self.bwd == "fused":
+            t_fused = self.step_ms()
+            self.bwd = "streams"
+            t_streams = self.step_ms()
+            keep_fused = t_fused <= t_streams
+            if world > 1:
+                import torch.distributed as dist
+                flag = torch.tensor([int(keep_fused)], dtype=torch.int32, device=dev)
+                dist.broadcast(flag, 0)
+                keep_fused = bool(flag.item())
+            self.bwd = "fused" if keep_fused else "streams"
         if autotune == 2 and not tuned_file and self.bwd != "fused":
             for mid in (l1, l2):
                 wm, nu = ctx.tuned(mid, 1, T)

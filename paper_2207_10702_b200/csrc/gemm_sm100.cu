@@ -1000,6 +1000,9 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
   auto tmem_base_ld = [&]() -> uint32_t { return *reinterpret_cast<volatile uint32_t*>(tmem_slot); };
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
+  const long long t_start = clock64();
+  // ROAST_PROF counters: producer dependency waits; MMA issuer waits for stage data / TMEM (DX, DW)
+  long long pw_dep = 0, mw_full = 0, mw_tmem = 0, mw_full_dw = 0, mw_tmem_dw = 0;
   if (warp == 0) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     // ===================== TMA producer =====================
@@ -1029,7 +1032,11 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
               const uint32_t fb = map_to_rank(smem_u32(&full[s]), 0);
               if (leader) mbar_expect_tx(&full[s], tx);
               // A = the dependency's output tile (mb, kb / 4) once it is published
-              if (P.dep >= 0 && (kb & 3) == 0) wait_ready(mp.flags + mb * mp.dep_n_tiles + (kb >> 2), 8 * CG, mp.err);
+              if (P.dep >= 0 && (kb & 3) == 0) {
+                const long long t0 = mp.prof ? clock64() : 0;
+                wait_ready(mp.flags + mb * mp.dep_n_tiles + (kb >> 2), 8 * CG, mp.err);
+                if (mp.prof) pw_dep += clock64() - t0;
+              }
               tma_load_2d<CG>(mA, sA + s * MIX_A, fb, kb * BK, row0);
               const int32_t* cc = sCoord + (kb - kc) * 4;
               for (int j = 0; j < 2; ++j) {   // this CTA's two 64-row K-major B tiles (x = nb*4 + 2 rank + j, y = kb)
@@ -1054,8 +1061,11 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
             const uint32_t fb = map_to_rank(smem_u32(&full[s]), 0);
             if (leader) mbar_expect_tx(&full[s], tx);
             // B = the dependency's output rows kb*64.. (its m-block kb / 8), columns of tile nb
-            if (P.dep >= 0 && (kb == kb0 || (kb & 7) == 0))
+            if (P.dep >= 0 && (kb == kb0 || (kb & 7) == 0)) {
+              const long long t0 = mp.prof ? clock64() : 0;
               wait_ready(mp.flags + (kb >> 3) * mp.dep_n_tiles + nb, 8 * CG, mp.err);
+              if (mp.prof) pw_dep += clock64() - t0;
+            }
             tma_load_3d<CG>(mA, sA + s * MIX_A, fb, 0, kb * BK, row0 >> 6);
             tma_load_3d<CG>(&maps.b[prob], sB + s * MIX_B, fb, 0, kb * BK, col0 >> 6);
             if (++s == MIX_STAGES) {
@@ -1086,11 +1096,15 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
         const int kb1 = min(kb0 + P.kb_per_split, P.k_blocks);
         const uint32_t tbase = tmem_base_ld();
         if (P.mode == DX) {
+          long long t0 = mp.prof ? clock64() : 0;
           mbar_wait(&tempty[0], (use[0] & 1) ^ 1);
           mbar_wait(&tempty[1], (use[1] & 1) ^ 1);
+          if (mp.prof) mw_tmem += clock64() - t0;
           tc_fence_after();
           for (int kb = kb0; kb < kb1; ++kb) {
+            t0 = mp.prof ? clock64() : 0;
             mbar_wait(&full[s], ph);
+            if (mp.prof) mw_full += clock64() - t0;
             tc_fence_after();
             const uint32_t a0 = smem_u32(sA + s * MIX_A);
             const uint32_t b0 = smem_u32(sB + s * MIX_B);
@@ -1115,11 +1129,15 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
         } else {
           const int h = dwh;
           dwh ^= 1;
+          long long t0 = mp.prof ? clock64() : 0;
           mbar_wait(&tempty[h], (use[h] & 1) ^ 1);
+          if (mp.prof) mw_tmem_dw += clock64() - t0;
           tc_fence_after();
           const uint32_t d = tbase + uint32_t(h * 256);
           for (int kb = kb0; kb < kb1; ++kb) {
+            t0 = mp.prof ? clock64() : 0;
             mbar_wait(&full[s], ph);
+            if (mp.prof) mw_full_dw += clock64() - t0;
             tc_fence_after();
             const uint32_t a0 = smem_u32(sA + s * MIX_A);
             const uint32_t b0 = smem_u32(sB + s * MIX_B);
@@ -1274,6 +1292,11 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
     __syncwarp();
   }
 
+  if (mp.prof && lane == 0) {   // [cta][6]: total, producer dep wait, MMA wait full / TMEM in DX, in DW units
+    long long* o = mp.prof + blockIdx.x * 6;
+    if (warp == 0) { o[0] = clock64() - t_start; o[1] = pw_dep; }
+    if (warp == 1 && leader) { o[2] = mw_full; o[3] = mw_tmem; o[4] = mw_full_dw; o[5] = mw_tmem_dw; }
+  }
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
@@ -2202,8 +2225,26 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
   static const bool pdl = !(getenv("ROAST_PDL") && atoi(getenv("ROAST_PDL")) == 0);
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 2 : 1;
+  static long long* prof = nullptr;
+  if (getenv("ROAST_PROF")) {   // debug: per-role wait counters, printed after a synchronising launch
+    if (!prof) cudaMallocManaged(&prof, sizeof(long long) * 6 * 512);
+    cudaMemset(prof, 0, sizeof(long long) * 6 * 512);
+    mp.prof = prof;
+  }
   cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mix_sm100, maps, mp);
   if (e != cudaSuccess) return cuda_fail(e, "roast_mix_sm100 launch");
+  if (mp.prof) {
+    cudaDeviceSynchronize();
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    long long mx = 0;
+    for (int i = 0; i < 2 * pairs; ++i) {
+      for (int k = 0; k < 6; ++k) acc[k] += double(prof[i * 6 + k]);
+      mx = std::max(mx, prof[i * 6]);
+    }
+    fprintf(stderr, "[roast prof] mix: total %.0f (max %lld) | producer dep-wait %.0f | MMA wait-full DX %.0f DW %.0f | "
+            "wait-tmem DX %.0f DW %.0f (cycles, mean per CTA / per leader)\n", acc[0] / (2 * pairs), mx,
+            acc[1] / (2 * pairs), acc[2] / pairs, acc[4] / pairs, acc[3] / pairs, acc[5] / pairs);
+  }
   c->launches++;
   return ROAST_OK;
 }
