@@ -178,8 +178,12 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 // arrive on a barrier given by its shared::cluster address (own or peer CTA)
+// Arrive on a barrier given by its shared::cluster address (own or peer CTA).  Used to hand TMEM
+// back to the MMA issuer: the data dependency is tcgen05-proxy (ordered by the caller's
+// tcgen05.fence::before_thread_sync), so the default .release.cta semantics suffice; a
+// .release.cluster arrive made the epilogue wait ~1.7k cycles per unit for its store queue.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 template <int CG>
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, void* dst, uint32_t bar_cluster, int c0, int c1) {
@@ -919,6 +923,7 @@ struct MixParams {
   int dep_n_tiles;          // n_tiles of the publishing problem (flag index = mb * this + nb)
   int* err;                 // sticky device error word
   long long* prof;
+  int exp;                  // diagnostics only (ROAST_EXP in a ROAST_DIAG build): bit 0 no conversion math, bit 1 no TMEM loads
 };
 struct MixMaps {
   CUtensorMap a[4];         // DX: A (tokens x K); DW: X blocks (3-D)
@@ -933,7 +938,7 @@ constexpr int MIX_A = 32768, MIX_B = 16384;          // per-stage A / B slots (D
 constexpr int MIX_SMEM = MIX_STAGES * (MIX_A + MIX_B) + 8 * 4096 + 1024 + 256 + KB_CHUNK * 4 * 4;
 
 __device__ __forceinline__ void mbar_arrive_cluster_n(uint32_t cluster_addr, uint32_t n) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr), "r"(n)
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr), "r"(n)
                : "memory");
 }
 
@@ -976,7 +981,7 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < MIX_STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], 2);          // the A and the B producer each arrive (with their tx bytes)
       mbar_init(&empty[s], 1);
     }
     for (int h = 0; h < 2; ++h) {
@@ -1002,47 +1007,56 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
 
   const long long t_start = clock64();
   // ROAST_PROF counters: producer dependency waits; MMA issuer waits for stage data / TMEM (DX, DW)
-  long long pw_dep = 0, mw_full = 0, mw_tmem = 0, mw_full_dw = 0, mw_tmem_dw = 0;
-  if (warp == 0) {
+  long long pw_dep = 0, mw_full = 0, mw_tmem = 0, mw_full_dw = 0, mw_tmem_dw = 0, ep_a = 0, ep_b = 0, ep_n = 0;
+  if (warp == 0 || warp == 3) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
-    // ===================== TMA producer =====================
+    // ===================== TMA producers =====================
+    // warp 0 loads the A operand, warp 3 the B operand of every stage (each arrives on the
+    // stage's full barrier with its own byte count): two issuing threads keep the small-box
+    // TMA stream ahead of the MMAs.  The one whose operand is a dependency's output waits for
+    // the published tiles: A for DX (dY_a), B for DW (dY_a).
+    const bool pa = warp == 0;
     int s = 0;
     uint32_t ph = 0;
     for (int it = 0;; ++it) {
       int prob, u;
       if (!unit_at(it, prob, u)) break;
       const MixProb& P = mp.p[prob];
-      const CUtensorMap* mA = &maps.a[prob];
       int mb, nb, split;
       mix_decode(P, u, mb, nb, split);
       const int kb0 = split * P.kb_per_split;
       const int kb1 = min(kb0 + P.kb_per_split, P.k_blocks);
       if (P.mode == DX) {
         const int row0 = mb * 512 + int(rank) * 256;
-        const uint32_t tx = uint32_t(CG * MIX_A + 4 * 8192);
+        const uint32_t tx = pa ? uint32_t(CG * MIX_A) : uint32_t(4 * 8192);
         for (int kc = kb0; kc < kb1; kc += KB_CHUNK) {
           const int kc1 = min(kc + KB_CHUNK, kb1);
-          __syncwarp();
-          for (int i = lane; i < (kc1 - kc) * 4; i += 32)
-            sCoord[i] = __ldg(P.coord + int64_t(kc + (i >> 2)) * P.coord_ld + nb * 4 + (i & 3));
-          __syncwarp();
+          if (!pa) {
+            __syncwarp();
+            for (int i = lane; i < (kc1 - kc) * 4; i += 32)
+              sCoord[i] = __ldg(P.coord + int64_t(kc + (i >> 2)) * P.coord_ld + nb * 4 + (i & 3));
+            __syncwarp();
+          }
           if (lane == 0) {
             for (int kb = kc; kb < kc1; ++kb) {
               mbar_wait(&empty[s], ph ^ 1);
               const uint32_t fb = map_to_rank(smem_u32(&full[s]), 0);
               if (leader) mbar_expect_tx(&full[s], tx);
-              // A = the dependency's output tile (mb, kb / 4) once it is published
-              if (P.dep >= 0 && (kb & 3) == 0) {
-                const long long t0 = mp.prof ? clock64() : 0;
-                wait_ready(mp.flags + mb * mp.dep_n_tiles + (kb >> 2), 8 * CG, mp.err);
-                if (mp.prof) pw_dep += clock64() - t0;
-              }
-              tma_load_2d<CG>(mA, sA + s * MIX_A, fb, kb * BK, row0);
-              const int32_t* cc = sCoord + (kb - kc) * 4;
-              for (int j = 0; j < 2; ++j) {   // this CTA's two 64-row K-major B tiles (x = nb*4 + 2 rank + j, y = kb)
-                const int32_t c = cc[int(rank) * 2 + j];
-                const int row = (c >> 4) + ((c & 8) ? int(mp.neg_row) : 0);
-                tma_load_2d<CG>(&maps.shadow.m[c & 7], sB + s * MIX_B + j * 8192, fb, 0, row);
+              if (pa) {
+                // A = the dependency's output tile (mb, kb / 4) once it is published
+                if (P.dep >= 0 && (kb & 3) == 0) {
+                  const long long t0 = mp.prof ? clock64() : 0;
+                  wait_ready(mp.flags + mb * mp.dep_n_tiles + (kb >> 2), 8 * CG, mp.err);
+                  if (mp.prof) pw_dep += clock64() - t0;
+                }
+                tma_load_2d<CG>(&maps.a[prob], sA + s * MIX_A, fb, kb * BK, row0);
+              } else {
+                const int32_t* cc = sCoord + (kb - kc) * 4;
+                for (int j = 0; j < 2; ++j) {   // this CTA's two 64-row K-major B tiles (x = nb*4 + 2 rank + j, y = kb)
+                  const int32_t c = cc[int(rank) * 2 + j];
+                  const int row = (c >> 4) + ((c & 8) ? int(mp.neg_row) : 0);
+                  tma_load_2d<CG>(&maps.shadow.m[c & 7], sB + s * MIX_B + j * 8192, fb, 0, row);
+                }
               }
               if (++s == MIX_STAGES) {
                 s = 0;
@@ -1054,20 +1068,23 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
       } else {   // DW: X^T and dY as 3-D MN-major boxes (2 x 64-wide blocks each per CTA)
         const int row0 = mb * 256 + int(rank) * 128;
         const int col0 = nb * 256 + int(rank) * 128;
-        const uint32_t tx = uint32_t(CG * (16384 + 16384));
+        const uint32_t tx = uint32_t(CG * 16384);
         if (lane == 0) {
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&empty[s], ph ^ 1);
             const uint32_t fb = map_to_rank(smem_u32(&full[s]), 0);
             if (leader) mbar_expect_tx(&full[s], tx);
-            // B = the dependency's output rows kb*64.. (its m-block kb / 8), columns of tile nb
-            if (P.dep >= 0 && (kb == kb0 || (kb & 7) == 0)) {
-              const long long t0 = mp.prof ? clock64() : 0;
-              wait_ready(mp.flags + (kb >> 3) * mp.dep_n_tiles + nb, 8 * CG, mp.err);
-              if (mp.prof) pw_dep += clock64() - t0;
+            if (pa) {
+              tma_load_3d<CG>(&maps.a[prob], sA + s * MIX_A, fb, 0, kb * BK, row0 >> 6);
+            } else {
+              // B = the dependency's output rows kb*64.. (its m-block kb / 8), columns of tile nb
+              if (P.dep >= 0 && (kb == kb0 || (kb & 7) == 0)) {
+                const long long t0 = mp.prof ? clock64() : 0;
+                wait_ready(mp.flags + (kb >> 3) * mp.dep_n_tiles + nb, 8 * CG, mp.err);
+                if (mp.prof) pw_dep += clock64() - t0;
+              }
+              tma_load_3d<CG>(&maps.b[prob], sB + s * MIX_B, fb, 0, kb * BK, col0 >> 6);
             }
-            tma_load_3d<CG>(mA, sA + s * MIX_A, fb, 0, kb * BK, row0 >> 6);
-            tma_load_3d<CG>(&maps.b[prob], sB + s * MIX_B, fb, 0, kb * BK, col0 >> 6);
             if (++s == MIX_STAGES) {
               s = 0;
               ph ^= 1;
@@ -1084,7 +1101,7 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
       constexpr uint32_t idesc_dw = make_idesc(1, 1, 256, 256);
       int s = 0;
       uint32_t ph = 0;
-      uint32_t use[2] = {0, 0};   // uses of each TMEM half so far (phase of its empty barrier)
+      uint32_t usep = 0;          // bit h: parity of the number of uses of TMEM half h so far
       int dwh = 0;                // TMEM half of the next DW unit (alternates)
       for (int it = 0;; ++it) {
         int prob, u;
@@ -1097,8 +1114,8 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
         const uint32_t tbase = tmem_base_ld();
         if (P.mode == DX) {
           long long t0 = mp.prof ? clock64() : 0;
-          mbar_wait(&tempty[0], (use[0] & 1) ^ 1);
-          mbar_wait(&tempty[1], (use[1] & 1) ^ 1);
+          mbar_wait(&tempty[0], (usep & 1) ^ 1);
+          mbar_wait(&tempty[1], ((usep >> 1) & 1) ^ 1);
           if (mp.prof) mw_tmem += clock64() - t0;
           tc_fence_after();
           for (int kb = kb0; kb < kb1; ++kb) {
@@ -1124,13 +1141,12 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
           }
           tc_commit<CG>(&tfull[0]);
           tc_commit<CG>(&tfull[1]);
-          ++use[0];
-          ++use[1];
+          usep ^= 3u;
         } else {
           const int h = dwh;
           dwh ^= 1;
           long long t0 = mp.prof ? clock64() : 0;
-          mbar_wait(&tempty[h], (use[h] & 1) ^ 1);
+          mbar_wait(&tempty[h], ((usep >> h) & 1) ^ 1);
           if (mp.prof) mw_tmem_dw += clock64() - t0;
           tc_fence_after();
           const uint32_t d = tbase + uint32_t(h * 256);
@@ -1152,12 +1168,12 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
             }
           }
           tc_commit<CG>(&tfull[h]);
-          ++use[h];
+          usep ^= 1u << h;
         }
       }
     }
   } else if (warp < EPI_WARP0) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");   // warps 2, 3
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");   // warp 2 (TMEM allocator)
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
     // ===================== epilogue (8 warps) =====================
@@ -1165,7 +1181,7 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
     const int jh = (warp - EPI_WARP0) >> 2;  // DX: M sub-tile (= TMEM half); DW: column half
     uint8_t* buf = sStage + (warp - EPI_WARP0) * 4096;
     const uint32_t tempty_leader0 = map_to_rank(smem_u32(&tempty[0]), 0);
-    uint32_t use[2] = {0, 0};
+    uint32_t usep = 0;   // bit h: parity of the uses of TMEM half h so far (as the MMA issuer's)
     int dwh = 0;
     for (int it = 0;; ++it) {
       int prob, u;
@@ -1174,9 +1190,9 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
       int mb, nb, split;
       mix_decode(P, u, mb, nb, split);
       if (P.mode == DX) {
-        mbar_wait(&tfull[jh], use[jh] & 1);
-        ++use[0];
-        ++use[1];
+        mbar_wait(&tfull[jh], (usep >> jh) & 1);
+        const long long ta = mp.prof ? clock64() : 0;
+        usep ^= 3u;
         tc_fence_after();
         const uint32_t tb = tmem_base_ld() + uint32_t(jh * 256) + (uint32_t(q * 32) << 16);
         const int nsteps = min(256, P.N - nb * 256) / 64;
@@ -1185,19 +1201,31 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
         for (int c = 0; c < 4; ++c) {
           if (c < nsteps) {
             uint32_t r[64];
-            TMEM_LD32(tb + uint32_t(c * 64), r);
-            TMEM_LD32(tb + uint32_t(c * 64 + 32), (r + 32));
-            tmem_wait_ld();
+            if (DIAG(mp) & 2) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              __nv_bfloat162 v = __floats2bfloat162_rn(P.lam * __uint_as_float(r[2 * i]), P.lam * __uint_as_float(r[2 * i + 1]));
-              pk[c * 32 + i] = *reinterpret_cast<uint32_t*>(&v);
+              for (int i = 0; i < 64; ++i) r[i] = uint32_t(i * lane);
+            } else {
+              TMEM_LD32(tb + uint32_t(c * 64), r);
+              TMEM_LD32(tb + uint32_t(c * 64 + 32), (r + 32));
+              tmem_wait_ld();
+            }
+            if (DIAG(mp) & 1) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) pk[c * 32 + i] = __byte_perm(r[2 * i], r[2 * i + 1], 0x7632);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                __nv_bfloat162 v = __floats2bfloat162_rn(P.lam * __uint_as_float(r[2 * i]), P.lam * __uint_as_float(r[2 * i + 1]));
+                pk[c * 32 + i] = *reinterpret_cast<uint32_t*>(&v);
+              }
             }
           }
         }
+        const long long tb2 = mp.prof ? clock64() : 0;
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster_n(tempty_leader0 + uint32_t(jh * 8), 2);
+        if (mp.prof) { ep_a += tb2 - ta; ep_b += clock64() - tb2; ++ep_n; }
         const int row0 = mb * 512 + int(rank) * 256 + jh * BM + q * 32;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -1245,8 +1273,8 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
             t_scale = P.sgn[t] < 0 ? -P.lam : P.lam;
           }
         }
-        mbar_wait(&tfull[h], use[h] & 1);
-        ++use[h];
+        mbar_wait(&tfull[h], (usep >> h) & 1);
+        usep ^= 1u << h;
         tc_fence_after();
         const uint32_t tb = tmem_base_ld() + uint32_t(h * 256) + (uint32_t(q * 32) << 16);
         const int nvalid = min(256, P.N - nb * 256) / 32;
@@ -1292,10 +1320,11 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
     __syncwarp();
   }
 
-  if (mp.prof && lane == 0) {   // [cta][6]: total, producer dep wait, MMA wait full / TMEM in DX, in DW units
-    long long* o = mp.prof + blockIdx.x * 6;
-    if (warp == 0) { o[0] = clock64() - t_start; o[1] = pw_dep; }
+  if (mp.prof && lane == 0) {   // [cta][8]: total, producer dep wait, MMA wait full / TMEM in DX, in DW units,
+    long long* o = mp.prof + blockIdx.x * 8;   // DX TMEM->register phase (warp 4), DX units drained (warp 4)
+    if (warp == 0) { o[0] = clock64() - t_start; }
     if (warp == 1 && leader) { o[2] = mw_full; o[3] = mw_tmem; o[4] = mw_full_dw; o[5] = mw_tmem_dw; }
+    if (warp == EPI_WARP0) { o[6] = ep_a; o[7] = ep_n; o[1] = ep_b; }
   }
   tc_fence_before();
   cluster_sync();
@@ -2178,6 +2207,7 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
   mp.sched = it->second.first;
   mp.sched_len = it->second.second;
   mp.err = c->d_err;
+  if (const char* e = getenv("ROAST_EXP")) mp.exp = atoi(e);
   maps.shadow = *reinterpret_cast<const WMaps*>(c->tmap_shadow);
   WMaps& dmaps = *reinterpret_cast<WMaps*>(c->tmap_dm);
   if (c->tmap_dm_for != c->dM) {   // dM as 8 fp32 phase views (cached until dM is rebound)
@@ -2227,23 +2257,24 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
   cfg.numAttrs = pdl ? 2 : 1;
   static long long* prof = nullptr;
   if (getenv("ROAST_PROF")) {   // debug: per-role wait counters, printed after a synchronising launch
-    if (!prof) cudaMallocManaged(&prof, sizeof(long long) * 6 * 512);
-    cudaMemset(prof, 0, sizeof(long long) * 6 * 512);
+    if (!prof) cudaMallocManaged(&prof, sizeof(long long) * 8 * 512);
+    cudaMemset(prof, 0, sizeof(long long) * 8 * 512);
     mp.prof = prof;
   }
   cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mix_sm100, maps, mp);
   if (e != cudaSuccess) return cuda_fail(e, "roast_mix_sm100 launch");
   if (mp.prof) {
     cudaDeviceSynchronize();
-    double acc[6] = {0, 0, 0, 0, 0, 0};
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long mx = 0;
     for (int i = 0; i < 2 * pairs; ++i) {
-      for (int k = 0; k < 6; ++k) acc[k] += double(prof[i * 6 + k]);
-      mx = std::max(mx, prof[i * 6]);
+      for (int k = 0; k < 8; ++k) acc[k] += double(prof[i * 8 + k]);
+      mx = std::max(mx, prof[i * 8]);
     }
-    fprintf(stderr, "[roast prof] mix: total %.0f (max %lld) | producer dep-wait %.0f | MMA wait-full DX %.0f DW %.0f | "
-            "wait-tmem DX %.0f DW %.0f (cycles, mean per CTA / per leader)\n", acc[0] / (2 * pairs), mx,
-            acc[1] / (2 * pairs), acc[2] / pairs, acc[4] / pairs, acc[3] / pairs, acc[5] / pairs);
+    fprintf(stderr, "[roast prof] mix: total %.0f (max %lld) | MMA wait-full DX %.0f DW %.0f | "
+            "wait-tmem DX %.0f DW %.0f | DX tmem->rf per unit %.0f, release %.0f (cycles, mean per CTA / per leader)\n",
+            acc[0] / (2 * pairs), mx, acc[2] / pairs, acc[4] / pairs, acc[3] / pairs,
+            acc[5] / pairs, acc[6] / (acc[7] > 0 ? acc[7] : 1), acc[1] / (acc[7] > 0 ? acc[7] : 1));
   }
   c->launches++;
   return ROAST_OK;
