@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], RF ? 2 : 1);   // RF: the A and the B producer warp each arrive
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -402,8 +402,12 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
   // RF: registers move from warpgroup 0 (producer, MMA, TMEM allocator, idle) to the eight
   // epilogue warps: 128 x 56 + 256 x 224 = 64512 = 384 x 168.  Each role branch executes its own
   // setmaxnreg so ptxas allocates every branch under its own budget.
-  if (warp == 0) {
+  if (warp == 0 || (RF && warp == 3)) {
     if constexpr (RF) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    // RF kernels (WM = 2 FWD / DX) split the producer: warp 0 issues the A box (and waits on the
+    // chain's ready counters), warp 3 stages the tile coordinates and issues the hashed B tiles;
+    // each arrives on the stage's full barrier with its own byte count.  Otherwise warp 0 does both.
+    const bool pa = !RF || warp == 0, pb = !RF || warp == 3;
     // ===================== TMA producer (warp 0, both CTAs) =====================
     // Per work unit the whole warp stages the unit's packed tile coordinates
     // (k-blocks x 4, FWD/DX) into smem with coalesced loads; lane 0 then walks
@@ -431,13 +435,14 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
       // bytes landing on the leader's full barrier per stage (both CTAs)
       // DW: one 3-D box per operand per CTA (2*WM 64-wide h blocks of X, 2 o blocks of dY);
       // out-of-range blocks are zero-filled and still counted
+      const uint32_t tx_a = MODE == DW ? 0u : uint32_t((DIAG(p) & 32) ? 0 : CG * C::A_BYTES);
+      const uint32_t tx_b = MODE == DW ? 0u : uint32_t((DIAG(p) & 16) ? 0 : (MODE == FWD && NU == 192 ? 4 : n_sub) * 64 * 64 * 2);
       const uint32_t tx = MODE == DW ? (p.dw3d ? uint32_t(CG * (C::A_BYTES + C::B_BYTES))
                                                : uint32_t((m_sub_pair + n_sub) * 64 * 64 * 2))
-                                     : uint32_t(((DIAG(p) & 32) ? 0 : CG * C::A_BYTES) +
-                                                ((DIAG(p) & 16) ? 0 : (MODE == FWD && NU == 192 ? 4 : n_sub) * 64 * 64 * 2));
+                                     : (RF ? (pa ? tx_a : tx_b) : tx_a + tx_b);
       for (int kc = kb0; kc < kb1; kc += KB_CHUNK) {
         const int kc1 = min(kc + KB_CHUNK, kb1);
-        if (MODE != DW) {
+        if (MODE != DW && pb) {
           __syncwarp();
           for (int i = lane; i < (kc1 - kc) * 4; i += 32) {
             const int j = i & 3;
@@ -466,10 +471,11 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
                 tma_load_2d<CG>(&mapB, b + (j - j0) * 8192, fb, nb * BN + j * 64, kb * BK);
             } else {
               // chain: these 64 columns of A are problem 0's output tile (mb, kb / 4)
-              if (CHAIN && prob == 1 && (kb & 3) == 0) wait_ready(p0.flags + mb * p0.n_tiles + (kb >> 2), EPI_WARPS * CG, p0.err);
-              if (!(DIAG(p) & 32)) tma_load_2d<CG>(mA, a, fb, kb * BK, row0);
+              if (pa && CHAIN && prob == 1 && (kb & 3) == 0) wait_ready(p0.flags + mb * p0.n_tiles + (kb >> 2), EPI_WARPS * CG, p0.err);
+              if (pa && !(DIAG(p) & 32)) tma_load_2d<CG>(mA, a, fb, kb * BK, row0);
               const int32_t* cc = sCoord + (kb - kc) * 4;
-              if (MODE == FWD && NU == 192 && !(DIAG(p) & 16)) {
+              if (!pb) {
+              } else if (MODE == FWD && NU == 192 && !(DIAG(p) & 16)) {
                 // 96 MN-major B columns per CTA, whole tiles only (a 64-column SW128 atom cannot
                 // be half-filled from its right half): rank 0 = tile 0 | tile 1 loaded from its
                 // column 32 (its right half lands in the atom's left half, zeros after); rank 1 =
@@ -494,7 +500,7 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
                   tma_load_2d<CG>(&wmaps.m[cb & 7], b + 4096, fb, 0, rb);
                 }
               }
-              for (int j = j0; j < j1 && NU == BN && !(DIAG(p) & 16); ++j) {
+              for (int j = j0; j < j1 && pb && NU == BN && !(DIAG(p) & 16); ++j) {
                 // FWD: tile (x = kb, y = nb*4 + j); DX: tile (x = nb*4 + j, y = kb).
                 // Packed: row << 4 | neg << 3 | phase; negative tiles read the negated shadow.
                 const int32_t c = cc[j];
@@ -567,7 +573,7 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
       }
     }
   } else if (RF && warp < EPI_WARP0) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");   // warps 2, 3
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");   // warp 2 (TMEM allocator)
   } else if (RF && warp >= EPI_WARP0) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
     // ===================== epilogue, register-held (WM = 2 FWD / DX) =====================
