@@ -318,8 +318,8 @@ class C2Step:
         import synth
         self.torch, self.dev, self.chain, self.streams, self.world = torch, dev, chain, streams, world
         # fused: the whole backward as ONE persistent launch (roast_linear_bwd_chain: dY1, dM of
-        # L2, dX, dM of L1 co-scheduled); deterministic mode has no fused kernel (separate calls)
-        self.bwd = "streams" if deterministic else bwd
+        # L2, dX, dM of L1 co-scheduled; deterministic mode adds the fixed-order reduces)
+        self.bwd = bwd
         T = self.T = TOKENS
         self.mem = synth.mlp_block(ratio)["mem_size"]
         M = torch.tensor(synth.uniform(synth.SEED_M, (self.mem,)).astype(np.float32), device=dev)

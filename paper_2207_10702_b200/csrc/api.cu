@@ -56,6 +56,7 @@ static void free_module(Module& m) {
   cudaFree(m.d_sgn);
   cudaFree(m.d_sorted);
   cudaFree(m.d_sorted_off);
+  cudaFree(m.d_cover);
   cudaFree(m.d_coord_xy);
   cudaFree(m.d_coord_yx);
 }
@@ -111,6 +112,24 @@ roast_status_t upload_linear_tables(Ctx* c, Module& m) {
   if (e == cudaSuccess) e = cudaMemcpy(m.d_sgn, m.h_sgn.data(), nt * sizeof(int8_t), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(m.d_sorted, order.data(), nt * sizeof(int32_t), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(m.d_sorted_off, soff.data(), nt * sizeof(int64_t), cudaMemcpyHostToDevice);
+  const int64_t span = int64_t(c->tile.z1) * c->tile.z2, ngroups = (c->mem_size + 3) / 4;
+  if (e == cudaSuccess && c->cfg.deterministic && A % 4 == 0 && ngroups * 8 <= (int64_t(64) << 20) &&
+      nt * span >= 16 * c->mem_size) {
+    // covering range of every 4-slot group (two pointers over the offset-sorted tiles): tiles
+    // with off <= s < off + span, i.e. sorted positions [first off > s - span, first off > s)
+    std::vector<int32_t> cov(size_t(ngroups) * 2);
+    int64_t lo = 0, hi = 0;
+    for (int64_t g = 0; g < ngroups; ++g) {
+      const int64_t s = 4 * g;
+      while (lo < nt && soff[lo] <= s - span) ++lo;
+      if (hi < lo) hi = lo;
+      while (hi < nt && soff[hi] <= s) ++hi;
+      cov[2 * g] = int32_t(lo);
+      cov[2 * g + 1] = int32_t(hi);
+    }
+    e = cudaMalloc(reinterpret_cast<void**>(&m.d_cover), cov.size() * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMemcpy(m.d_cover, cov.data(), cov.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  }
   if (e == cudaSuccess && c->mem_size < (int64_t(1) << 33) && A % 8 == 0) {
     std::vector<int32_t> cxy(nt), cyx(nt);
     for (int32_t x = 0; x < m.nx; ++x)

@@ -919,6 +919,8 @@ struct MixProb {
   float lam;
   int dep;                  // problem whose output tiles this one reads (0) or -1
   int publish;              // 1: this problem's units publish ready counters (P0)
+  int ws_slot;              // DW, deterministic: index of its workspace map (maps.ws), else -1
+  int ntiles;               // DW: hash tiles of the module (workspace row = (split * ntiles + t) * 64)
 };
 struct MixParams {
   MixProb p[4];
@@ -936,6 +938,7 @@ struct MixMaps {
   CUtensorMap b[4];         // DX: output (tokens x N); DW: dY blocks (3-D)
   WMaps shadow;             // bf16 shadow, 8 phase views (DX B tiles)
   WMaps dm;                 // dM, 8 fp32 phase views (DW reduce-add)
+  CUtensorMap ws[2];        // deterministic mode: per-tile fp32 workspaces of the two DW problems
 };
 
 constexpr int MIX_THREADS = 384;
@@ -1275,7 +1278,8 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
           const int y = nb * 4 + (lane & 3);
           if (lane < 4 && rb < P.M && y * 64 < P.N) {
             const int t = (rb >> 6) * P.ny + y;
-            t_off = P.off[t];
+            // deterministic: the tile's slot in the workspace (reduced in fixed order afterwards)
+            t_off = P.ws_slot >= 0 ? (int64_t(split) * P.ntiles + t) * 4096 : P.off[t];
             t_scale = P.sgn[t] < 0 ? -P.lam : P.lam;
           }
         }
@@ -1306,14 +1310,20 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if (lane == 0 && rb < P.M) {   // TMA reduce-add into dM (32 rows x 32 fp32 of one hash tile)
+          if (lane == 0 && rb < P.M) {   // 32 rows x 32 fp32 of one hash tile
             const int x0 = (c & 1) * 32;
             const int y0 = int(tbo >> 6) + (rb & 63);
-            asm volatile(
-                "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                    reinterpret_cast<uint64_t>(&maps.dm.m[(tbo >> 3) & 7])),
-                "r"(x0), "r"(y0), "r"(smem_u32(buf))
-                : "memory");
+            if (P.ws_slot >= 0)   // deterministic: plain store into the per-tile workspace
+              asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                               reinterpret_cast<uint64_t>(&maps.ws[P.ws_slot])),
+                           "r"(x0), "r"(y0), "r"(smem_u32(buf))
+                           : "memory");
+            else                  // fast: TMA reduce-add into dM in L2
+              asm volatile(
+                  "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                      reinterpret_cast<uint64_t>(&maps.dm.m[(tbo >> 3) & 7])),
+                  "r"(x0), "r"(y0), "r"(smem_u32(buf))
+                  : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         }
@@ -2112,8 +2122,9 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
                                const void* dY_b, void* dY_a, void* dX_a, int64_t T, cudaStream_t s) {
   using namespace sm100;
   if (!supported(c, ma) || !supported(c, mbm) || cta_group() != 2 || T <= 0 || T >= (int64_t(1) << 31) ||
-      c->cfg.deterministic || getenv("ROAST_NO_BWD_FUSE"))
+      getenv("ROAST_NO_BWD_FUSE"))
     return ROAST_ERR_UNSUPPORTED;
+  const bool det = c->cfg.deterministic != 0;
   if (ma.H % 256 || ma.O % 256 || mbm.O % 256 || mbm.H != ma.O || !dX_a) return ROAST_ERR_UNSUPPORTED;
   const int pairs = num_sms() / 2;
   const int mtT = int((T + 511) / 512), kbT = int((T + BK - 1) / BK);
@@ -2197,6 +2208,8 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
     P.ny = m.ny;
     P.lam = m.lam;
     P.dep = -1;
+    P.ntiles = m.nx * m.ny;
+    P.ws_slot = -1;
     roast_status_t r = make_map_blocks(&maps.a[pi], X, uint64_t(m.H), uint64_t(T), BK, 2);
     if (r) return r;
     return make_map_blocks(&maps.b[pi], dY, uint64_t(m.O), uint64_t(T), BK, 2);
@@ -2208,6 +2221,27 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
   mp.p[0].publish = 1;
   mp.p[2].dep = 0;
   mp.p[3].dep = 0;
+  // deterministic mode (R19): the DW units store their lambda g-scaled tiles into per-tile
+  // workspaces (per call, stream-ordered), reduced per slot in fixed order afterwards
+  Scratch ws;
+  int64_t ws_rows[2] = {0, 0};
+  if (det) {
+    const int dwp[2] = {1, 3};
+    int64_t total = 0;
+    for (int k = 0; k < 2; ++k) {
+      const MixProb& P = mp.p[dwp[k]];
+      ws_rows[k] = int64_t(P.units / (P.m_tiles * P.n_tiles)) * P.ntiles * 64;   // splits x tiles x 64 rows
+      total += ws_rows[k];
+    }
+    if ((st = scratch_alloc(ws, size_t(total) * 64 * sizeof(float), s))) return st;
+    int64_t row = 0;
+    for (int k = 0; k < 2; ++k) {
+      mp.p[dwp[k]].ws_slot = k;
+      st = make_map_2d(&maps.ws[k], ws.as<float>() + row * 64, 64, uint64_t(ws_rows[k]), 256, 32, 32, true);
+      if (st) return st;
+      row += ws_rows[k];
+    }
+  }
   mp.dep_n_tiles = mp.p[0].n_tiles;
   mp.neg_row = c->neg_base / 64;
   mp.sched = it->second.first;
@@ -2269,6 +2303,14 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
   }
   cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mix_sm100, maps, mp);
   if (e != cudaSuccess) return cuda_fail(e, "roast_mix_sm100 launch");
+  if (det) {   // fixed order: module b's slots, then module a's (each: covering tiles, then splits)
+    const int sp_b = mp.p[1].units / (mp.p[1].m_tiles * mp.p[1].n_tiles);
+    const int sp_a = mp.p[3].units / (mp.p[3].m_tiles * mp.p[3].n_tiles);
+    if ((e = launch_det_reduce(c, mbm, ws.as<float>(), sp_b, s)) != cudaSuccess) return cuda_fail(e, "det_reduce");
+    if ((e = launch_det_reduce(c, ma, ws.as<float>() + ws_rows[0] * 64, sp_a, s)) != cudaSuccess)
+      return cuda_fail(e, "det_reduce");
+    c->launches += 2;
+  }
   if (mp.prof) {
     cudaDeviceSynchronize();
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};

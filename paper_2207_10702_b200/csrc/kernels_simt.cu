@@ -240,7 +240,7 @@ __global__ void det_reduce_warp_kernel(float* __restrict__ dM, const float* __re
                                        const int32_t* __restrict__ sorted, const int64_t* __restrict__ sorted_off,
                                        int ntiles, int64_t tile_elems, int nsplit, int64_t mem_size,
                                        const int64_t* __restrict__ iv_start, const int64_t* __restrict__ iv_prefix,
-                                       int n_iv, int64_t n_touched) {
+                                       int n_iv, int64_t n_touched, const int2* __restrict__ cover) {
   const int lane = threadIdx.x & 31;
   const int64_t n = n_iv > 0 ? n_touched : mem_size;
   const int64_t ngroups = (n + 3) / 4;
@@ -254,13 +254,20 @@ __global__ void det_reduce_warp_kernel(float* __restrict__ dM, const float* __re
       s = w.slot(s);
     }
     if (s >= mem_size) continue;
-    int x = 0, y = ntiles;
-    const int64_t key = s - tile_elems;
-    while (x < y) { int mid = (x + y) >> 1; if (__ldg(sorted_off + mid) > key) y = mid; else x = mid + 1; }
-    const int lo = x;
-    y = ntiles;
-    while (x < y) { int mid = (x + y) >> 1; if (__ldg(sorted_off + mid) > s) y = mid; else x = mid + 1; }
-    const int hi = x;
+    int lo, hi;
+    if (cover) {   // static covering range of this 4-slot group (built at registration)
+      const int2 r = __ldg(cover + (s >> 2));
+      lo = r.x;
+      hi = r.y;
+    } else {
+      int x = 0, y = ntiles;
+      const int64_t key = s - tile_elems;
+      while (x < y) { int mid = (x + y) >> 1; if (__ldg(sorted_off + mid) > key) y = mid; else x = mid + 1; }
+      lo = x;
+      y = ntiles;
+      while (x < y) { int mid = (x + y) >> 1; if (__ldg(sorted_off + mid) > s) y = mid; else x = mid + 1; }
+      hi = x;
+    }
     if (lo >= hi) continue;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     const int nterms = (hi - lo) * nsplit;
@@ -427,7 +434,7 @@ cudaError_t launch_det_reduce(Ctx* c, const Module& m, const float* ws, int nspl
     det_reduce_warp_kernel<<<unsigned(blocks), threads, 0, s>>>(
         c->dM, ws, m.d_sorted, m.d_sorted_off, m.nx * m.ny, int64_t(c->tile.z1) * c->tile.z2, nsplit, c->mem_size,
         touched ? c->d_iv : nullptr, touched ? c->d_iv + c->n_iv : nullptr, touched ? c->n_iv : 0,
-        touched ? c->touched_n : 0);
+        touched ? c->touched_n : 0, reinterpret_cast<const int2*>(m.d_cover));
     return cudaGetLastError();
   }
   int64_t blocks = std::min<int64_t>((nthreads + threads - 1) / threads, 148 * 32);

@@ -32,6 +32,10 @@ struct Module {
   // binary-searches the covering range [lo, hi) of every A-aligned slot group.
   int32_t* d_sorted = nullptr;    // [ntiles] tile ids
   int64_t* d_sorted_off = nullptr;// [ntiles]
+  // deterministic mode, heavily shared memories: the covering range [lo, hi) in the sorted
+  // list of every 4-slot group of M (static; built at registration when <= 64 MB), so the
+  // warp-per-group reduce reads it instead of two dependent binary searches per group
+  int32_t* d_cover = nullptr;     // [ceil(|M| / 4)][2]
   // tcgen05 producer: packed TMA coordinates of every tile, (off >> 6) << 4 | neg << 3 | (off >> 3) & 7,
   // in [x][y] order (FWD walks a row) and [y][x] order (DX walks a column).  Empty if off >= 2^33.
   int32_t* d_coord_xy = nullptr;
