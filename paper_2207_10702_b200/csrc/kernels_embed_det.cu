@@ -200,6 +200,86 @@ __global__ void emb_chunk_kernel(float* __restrict__ dM, float* __restrict__ par
   }
 }
 
+// pass 1, sub-warp version (A % 4 == 0, A <= 32): L = A / 4 lanes own one chunk (lane r of the
+// sub-group holds slots 4r .. 4r + 3 of the group as a float4), so a warp works on 32 / L chunks
+// at once (C4 at A = 32: 4, at A = 8: 16) instead of two — the pass is latency-bound (a few
+// items per group, ~4 dependent round trips each), so more chunks in flight is what pays.  Each
+// slot still adds its chunk's terms in item order (the same order as the warp version).
+__global__ void emb_chunk_sub_kernel(float* __restrict__ dM, float* __restrict__ partial,
+                                     const int32_t* __restrict__ vals, const ChunkInfo* __restrict__ info,
+                                     const int32_t* __restrict__ nseg_p, const int32_t* __restrict__ nch,
+                                     const int32_t* __restrict__ choff, const float* __restrict__ dOut, int dim,
+                                     int chunk, int q, int G, int A, const __grid_constant__ DetLam lam,
+                                     int64_t mem_size) {
+  const int L = A >> 2;                       // lanes per chunk
+  const int r = (threadIdx.x & 31) % L;       // this lane's float4 of the group's A slots
+  const int64_t nseg = *nseg_p;
+  if (nseg == 0) return;
+  const int64_t total = int64_t(choff[nseg - 1]) + nch[nseg - 1];
+  const int64_t nsub = (int64_t(gridDim.x) * blockDim.x) / L;
+  for (int64_t c = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / L; c < total; c += nsub) {
+    const ChunkInfo ci = info[c];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int it = ci.begin;
+    constexpr int U = 4;
+    for (; it + U <= ci.end; it += U) {      // U items' loads in flight, summed in item order
+      float4 t[U];
+      float sc[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int32_t v = __ldg(vals + it + u);
+        const int item = v & 0x7FFFFFFF;
+        const int p = item / G;
+        const int i = item - p * G;
+        const int b = p / q;
+        const int col = (p - b * q) * chunk + i * A + 4 * r;
+        const float l = lam.lam[b / lam.n];
+        sc[u] = v < 0 ? -l : l;
+        t[u] = col < dim ? __ldg(reinterpret_cast<const float4*>(dOut + int64_t(b) * dim + col))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);   // padded tail of the last chunk (R16)
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        acc.x += sc[u] * t[u].x;
+        acc.y += sc[u] * t[u].y;
+        acc.z += sc[u] * t[u].z;
+        acc.w += sc[u] * t[u].w;
+      }
+    }
+    for (; it < ci.end; ++it) {
+      const int32_t v = __ldg(vals + it);
+      const int item = v & 0x7FFFFFFF;
+      const int p = item / G;
+      const int i = item - p * G;
+      const int b = p / q;
+      const int col = (p - b * q) * chunk + i * A + 4 * r;
+      const float l = lam.lam[b / lam.n];
+      const float sc = v < 0 ? -l : l;
+      if (col < dim) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(dOut + int64_t(b) * dim + col));
+        acc.x += sc * t.x;
+        acc.y += sc * t.y;
+        acc.z += sc * t.z;
+        acc.w += sc * t.w;
+      }
+    }
+    if (ci.dst < 0) {
+      const int64_t sl = int64_t(ci.group) * A + 4 * r;
+      if (sl + 4 <= mem_size) {
+        float4* d = reinterpret_cast<float4*>(dM + sl);
+        float4 o = *d;
+        o.x += acc.x; o.y += acc.y; o.z += acc.z; o.w += acc.w;
+        *d = o;
+      } else {
+        const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+        for (int k = 0; k < 4 && sl + k < mem_size; ++k) dM[sl + k] += a4[k];
+      }
+    } else {
+      *reinterpret_cast<float4*>(partial + int64_t(ci.dst) * A + 4 * r) = acc;
+    }
+  }
+}
+
 // pass 2: one warp per multi-chunk group: its partials in chunk order, then dM
 __global__ void emb_longseg_kernel(float* __restrict__ dM, const float* __restrict__ partial,
                                    const uint32_t* __restrict__ keys, const int32_t* __restrict__ heads,
@@ -318,8 +398,12 @@ roast_status_t embed_bwd_det_group(Ctx* c, const Module* const* mods, int nt, co
                                                                     info);
   ROAST_CUDA_CHECK(cudaGetLastError());
   const int grid = 148 * 8;
-  emb_chunk_kernel<<<grid, 256, 0, s>>>(c->dM, partial, v_out, info, nseg, nch, choff, dOut, m.dim, m.chunk,
-                                        m.chunks_per_row, G, A, L, c->mem_size);
+  if (A % 4 == 0 && A <= 32 && !getenv("ROAST_EMB_DET_WARP"))
+    emb_chunk_sub_kernel<<<148 * 16, 256, 0, s>>>(c->dM, partial, v_out, info, nseg, nch, choff, dOut, m.dim,
+                                                 m.chunk, m.chunks_per_row, G, A, L, c->mem_size);
+  else
+    emb_chunk_kernel<<<grid, 256, 0, s>>>(c->dM, partial, v_out, info, nseg, nch, choff, dOut, m.dim, m.chunk,
+                                          m.chunks_per_row, G, A, L, c->mem_size);
   ROAST_CUDA_CHECK(cudaGetLastError());
   emb_longseg_kernel<<<grid, 256, 0, s>>>(c->dM, partial, k_out, heads, nseg, nch, loff, G, A, c->mem_size);
   ROAST_CUDA_CHECK(cudaGetLastError());
