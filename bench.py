@@ -880,7 +880,8 @@ def c2_extras(torch, dev, args, S, flush, stream, W1, W2):
             g = graph_of(torch, V.step_body)
             ms = mean_replay_ms(torch, g, 10, flush, stream)
             variants[key] = dict(value=flops_per_step(T) / (ms * 1e-3) / 1e12, unit=UNIT, ms_per_step=ms,
-                                 mem_size=V.mem, dm_mode="deterministic" if det else "atomic", tuned=V.tuned())
+                                 mem_size=V.mem, dm_mode="deterministic" if det else "atomic", bwd=V.bwd,
+                                 tuned=V.tuned())
             V.ctx.close()
             del V, g
         except Exception as e:  # noqa: BLE001

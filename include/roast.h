@@ -438,6 +438,43 @@ roast_status_t roast_p2p_gather(roast_t h, roast_stream_t stream);
 roast_status_t roast_grad_exchange_p2p2(roast_t h, const roast_opt_config_t* cfg, int64_t step,
                                         roast_stream_t stream);
 
+/* NVLS variant (the a6 exchange P:194 fused with the a7
+ * update P:440).  On an NVSwitch system the exchange windows of all ranks can be
+ * bound to one multicast object: the finish / reduce kernels then read the SUM over the ranks
+ * with multimem.ld_reduce (reduced in the switch, one NVLink read per value instead of W - 1),
+ * the two-shot reduce broadcasts its slice's new values with multimem.st (the gather reads only
+ * local memory), and the flags are written to every rank by one multimem.st.  Once bound, the
+ * p2p entry points above run the NVLS kernels unchanged in meaning: roast_grad_exchange_p2p
+ * (one-shot: every rank reduces all n values in the switch and updates all of M; replication
+ * then relies on the switch returning the same fp32 sum to every rank) and
+ * roast_grad_exchange_p2p2 (two-shot: only a slice's owner computes its update and broadcasts
+ * it, so M stays replicated bit for bit by construction).  Set-up, after every module is
+ * registered, all ranks in this order:
+ * roast_nvls_supported: *supported = CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED of `device` (0 when
+ *   the driver lacks the multicast entry points).  Never fails for a valid pointer.
+ * roast_nvls_create (rank 0): cuMulticastCreate for `world` devices (1..8), sized for this
+ *   handle's window (layout as roast_p2p_window); *fd = a POSIX file descriptor of the object,
+ *   owned by the caller (send it to the other ranks, e.g. SCM_RIGHTS; close it afterwards).
+ * roast_nvls_import (ranks != 0): import the object from the descriptor received.
+ * roast_nvls_add_device: add this handle's device.  Every rank must return from it before any
+ *   rank calls roast_nvls_bind.
+ * roast_nvls_bind: allocate this rank's window (cuMemCreate), bind it to the object, map its
+ *   unicast and multicast aliases and zero it; the window then replaces the P2P one (open /
+ *   attach return ROAST_ERR_STATE).  Barrier all ranks before the first exchange.
+ * roast_nvls_bound: *bound = 1 once roast_nvls_bind succeeded.
+ * roast_nvls_reset: release this handle's multicast object / window in any set-up state (a rank
+ *   whose peers failed a step backs out this way); the next P2P call allocates a fresh window.
+ * Errors: ROAST_ERR_UNSUPPORTED without the driver entry points; ROAST_ERR_CUDA with the
+ * CUresult when the driver refuses a step (e.g. no NVSwitch multicast); a failed bind undoes
+ * everything, so the handle stays usable on the P2P and NCCL paths (the binding's fallback). */
+roast_status_t roast_nvls_supported(int32_t device, int32_t* supported);
+roast_status_t roast_nvls_create(roast_t h, int32_t world, int32_t* fd);
+roast_status_t roast_nvls_import(roast_t h, int32_t world, int32_t fd);
+roast_status_t roast_nvls_add_device(roast_t h);
+roast_status_t roast_nvls_bind(roast_t h, int32_t rank);
+roast_status_t roast_nvls_bound(roast_t h, int32_t* bound);
+roast_status_t roast_nvls_reset(roast_t h);
+
 /* Sticky device-side error (synchronises the handle's bound stream is NOT done:
  * call after a stream synchronize to observe faults of completed work). */
 roast_status_t roast_get_error(roast_t h);

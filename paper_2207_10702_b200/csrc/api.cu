@@ -252,6 +252,18 @@ roast_status_t roast_destroy(roast_t h) {
   return ROAST_OK;
 }
 
+// Replicas of the bf16 shadow.  At high compression the whole shadow is a few L2 lines' worth
+// (C2 at 1000x: 19 KB) and every CTA pair's hashed-tile loads land on the same L2 slices; R
+// copies (CTA pair p reads copy p % R) spread them.  Bounded to 1 MB in total; ROAST_SHADOW_REPS
+// overrides (A/B).
+static int shadow_replicas(int64_t elems) {
+  if (const char* e = getenv("ROAST_SHADOW_REPS")) return std::max(1, std::min(74, atoi(e)));
+  const int64_t bytes = elems * int64_t(sizeof(uint16_t));
+  int r = 1;
+  while (r < 16 && bytes * 2 * r <= (int64_t(1) << 20)) r *= 2;
+  return r;
+}
+
 roast_status_t roast_bind(roast_t h, float* d_M, float* d_dM, roast_stream_t stream) {
   Ctx* c = ctx(h);
   if (!c) return fail(ROAST_ERR_STATE, "null handle");
@@ -265,8 +277,10 @@ roast_status_t roast_bind(roast_t h, float* d_M, float* d_dM, roast_stream_t str
     // [+bf16(M) | pad | -bf16(M) | 64-element tail pad]; the negated copy starts 128-B aligned
     c->neg_base = (c->mem_size + 63) / 64 * 64;
     c->shadow_elems = 2 * c->neg_base + 64;
-    ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->shadow), c->shadow_elems * sizeof(uint16_t)));
-    ROAST_CUDA_CHECK(cudaMemsetAsync(c->shadow, 0, c->shadow_elems * sizeof(uint16_t), s));
+    c->shadow_reps = shadow_replicas(c->shadow_elems);
+    const size_t bytes = size_t(c->shadow_reps) * c->shadow_elems * sizeof(uint16_t);
+    ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->shadow), bytes));
+    ROAST_CUDA_CHECK(cudaMemsetAsync(c->shadow, 0, bytes, s));
     c->tmap_shadow_valid = false;
   }
   ROAST_CUDA_CHECK(launch_sync_shadow(c, s));

@@ -113,6 +113,7 @@ struct Params {
   int coord_ld;         // row length of `coord`
   int ny;               // tiles per row of the tile map (out / 64)
   int64_t neg_row;      // row (128 B units) of the negated shadow copy
+  int reps, rep_rows;   // shadow replicas (rep_rows rows apart); CTA pair q reads replica q % reps
   float lam;
   __nv_bfloat16* out;   // FWD: Y [T x N], DX: dX [T x N]
   const float* bias;    // FWD only: fp32 [N] added after lambda (recovered by L), or null
@@ -345,6 +346,7 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
   const bool leader = rank == 0;
   const int pair = blockIdx.x / CG;
+  const int rrow = p0.reps > 1 ? (pair % p0.reps) * p0.rep_rows : 0;   // this pair's shadow replica
   const int npairs = gridDim.x / CG;
   // i-th unit of this pair: round-robin over one problem, or the pair's chain schedule
   auto unit_at = [&](int i, int& prob, int& u) -> bool {
@@ -482,16 +484,16 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
                 // tile 2 | tile 1 (left half used).  Accumulator columns [0,64) [64,96) [96,160)
                 // [160,192) hold output columns 0-63, 96-127, 128-191, 64-95 (epilogue permutes).
                 const int32_t ca = cc[rank ? 2 : 0], cb = cc[1];
-                const int ra = (ca >> 4) + ((ca & 8) ? int(p.neg_row) : 0);
-                const int rb = (cb >> 4) + ((cb & 8) ? int(p.neg_row) : 0);
+                const int ra = (ca >> 4) + ((ca & 8) ? int(p.neg_row) : 0) + rrow;
+                const int rb = (cb >> 4) + ((cb & 8) ? int(p.neg_row) : 0) + rrow;
                 tma_load_2d<CG>(&wmaps.m[ca & 7], b, fb, 0, ra);
                 tma_load_2d<CG>(&wmaps.m[cb & 7], b + 8192, fb, rank ? 0 : 32, rb);
               } else if (NU == 192 && !(DIAG(p) & 16)) {
                 // 96 B rows (N) per CTA: rank 0 = tile 0 + rows 0-31 of tile 1, rank 1 = rows
                 // 32-63 of tile 1 + tile 2; every piece lands at a 1024-B multiple (SW128 phase)
                 const int32_t ca = cc[rank ? 1 : 0], cb = cc[rank ? 2 : 1];
-                const int ra = (ca >> 4) + ((ca & 8) ? int(p.neg_row) : 0);
-                const int rb = (cb >> 4) + ((cb & 8) ? int(p.neg_row) : 0);
+                const int ra = (ca >> 4) + ((ca & 8) ? int(p.neg_row) : 0) + rrow;
+                const int rb = (cb >> 4) + ((cb & 8) ? int(p.neg_row) : 0) + rrow;
                 if (rank == 0) {
                   tma_load_2d<CG>(&wmaps.m[ca & 7], b, fb, 0, ra);
                   tma_load_2d<CG>(&hmaps.m[cb & 7], b + 8192, fb, 0, rb);
@@ -504,7 +506,7 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
                 // FWD: tile (x = kb, y = nb*4 + j); DX: tile (x = nb*4 + j, y = kb).
                 // Packed: row << 4 | neg << 3 | phase; negative tiles read the negated shadow.
                 const int32_t c = cc[j];
-                const int row = (c >> 4) + ((c & 8) ? int(p.neg_row) : 0);
+                const int row = (c >> 4) + ((c & 8) ? int(p.neg_row) : 0) + rrow;
                 tma_load_2d<CG>(&wmaps.m[c & 7], b + (j - j0) * 8192, fb, 0, row);
               }
             }
@@ -925,6 +927,7 @@ struct MixProb {
 struct MixParams {
   MixProb p[4];
   int64_t neg_row;          // row (128 B) of the negated shadow copy
+  int reps, rep_rows;       // shadow replicas (rep_rows rows apart); CTA pair q reads replica q % reps
   const int32_t* sched;     // [pairs][sched_len] codes prob << 24 | unit, -1 = end
   int sched_len;
   int* flags;               // ready counters of the publishing problem's units
@@ -979,6 +982,7 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x / CG;
+  const int rrow = mp.reps > 1 ? (pair % mp.reps) * mp.rep_rows : 0;   // this pair's shadow replica
   auto unit_at = [&](int i, int& prob, int& u) -> bool {
     if (i >= mp.sched_len) return false;
     const int code = __ldg(mp.sched + pair * mp.sched_len + i);
@@ -1063,7 +1067,7 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
                 const int32_t* cc = sCoord + (kb - kc) * 4;
                 for (int j = 0; j < 2; ++j) {   // this CTA's two 64-row K-major B tiles (x = nb*4 + 2 rank + j, y = kb)
                   const int32_t c = cc[int(rank) * 2 + j];
-                  const int row = (c >> 4) + ((c & 8) ? int(mp.neg_row) : 0);
+                  const int row = (c >> 4) + ((c & 8) ? int(mp.neg_row) : 0) + rrow;
                   tma_load_2d<CG>(&maps.shadow.m[c & 7], sB + s * MIX_B + j * 8192, fb, 0, row);
                 }
               }
@@ -1504,7 +1508,7 @@ roast_status_t sm100_prepare(Ctx* c) {
   WMaps* w = reinterpret_cast<WMaps*>(c->tmap_shadow);
   WMapsHalf* hw = reinterpret_cast<WMapsHalf*>(c->tmap_shadow_half);
   for (int r = 0; r < 8; ++r) {
-    const int64_t elems = c->shadow_elems - 8 * r;
+    const int64_t elems = c->shadow_reps * c->shadow_elems - 8 * r;   // every replica
     roast_status_t st = make_map_2d(&w->m[r], c->shadow + 8 * r, 64, uint64_t(elems / 64), 128, 64, 64);
     if (st) return st;
     st = make_map_2d(&hw->m[r], c->shadow + 8 * r, 64, uint64_t(elems / 64), 128, 64, 32);
@@ -1526,6 +1530,8 @@ static Params base_params(const Ctx* c, const Module& m, int64_t T) {
   p.sgn = m.d_sgn;
   p.ny = m.ny;
   p.neg_row = c->neg_base / 64;
+  p.reps = c->shadow_reps;
+  p.rep_rows = int(c->shadow_elems / 64);
   p.lam = m.lam;
   p.ntiles = m.nx * m.ny;
   p.splits = 1;
@@ -2244,6 +2250,8 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
   }
   mp.dep_n_tiles = mp.p[0].n_tiles;
   mp.neg_row = c->neg_base / 64;
+  mp.reps = c->shadow_reps;
+  mp.rep_rows = int(c->shadow_elems / 64);
   mp.sched = it->second.first;
   mp.sched_len = it->second.second;
   mp.err = c->d_err;

@@ -298,13 +298,9 @@ __global__ void det_reduce_warp_kernel(float* __restrict__ dM, const float* __re
   }
 }
 
-__global__ void sync_shadow_kernel(const float* __restrict__ M, __nv_bfloat16* __restrict__ sh, int64_t n,
-                                   int64_t neg_base) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    __nv_bfloat16 b = __float2bfloat16_rn(M[i]);
-    sh[i] = b;
-    sh[neg_base + i] = __hneg(b);
-  }
+__global__ void sync_shadow_kernel(const float* __restrict__ M, ShadowOut so, int64_t n) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    so.store1(i, __bfloat16_as_ushort(__float2bfloat16_rn(M[i])));
 }
 
 __global__ void materialize_kernel(const float* __restrict__ M, const __nv_bfloat16* __restrict__ sh, MapArgs map,
@@ -331,8 +327,8 @@ MapArgs map_args(const Ctx* c, const Module& m) {
   a.z1 = c->tile.z1;
   a.z2 = c->tile.z2;
   a.ny = m.ny;
-  a.layout = c->cfg.tile_layout;
   a.neg_base = c->neg_base;
+  a.layout = c->cfg.tile_layout;
   return a;
 }
 
@@ -447,8 +443,7 @@ cudaError_t launch_det_reduce(Ctx* c, const Module& m, const float* ws, int nspl
 }
 
 cudaError_t launch_sync_shadow(Ctx* c, cudaStream_t s) {
-  sync_shadow_kernel<<<grid_1d(c->mem_size, 256), 256, 0, s>>>(
-      c->M, reinterpret_cast<__nv_bfloat16*>(c->shadow), c->mem_size, c->neg_base);
+  sync_shadow_kernel<<<grid_1d(c->mem_size, 256), 256, 0, s>>>(c->M, shadow_out(c), c->mem_size);
   return cudaGetLastError();
 }
 
@@ -491,10 +486,9 @@ __device__ __forceinline__ float opt_update(float w, float g0, float& a, float& 
 struct OptArgs {
   float* M;
   float* dM;
-  __nv_bfloat16* sh;
+  ShadowOut so;
   float* s1;
   float* s2;
-  int64_t neg_base;
   float lr, b1, b2, eps, wd, bc1, bc2;
   int zero;
   // index space: n elements; slot = p (n_iv == 0) or the p-th touched slot (exchange.cu tables)
@@ -505,6 +499,27 @@ struct OptArgs {
   int n_iv;
   P2PView p2p;          // world > 0: the gradient of index p is sum_r buf_r[p], read from the peers
 };
+
+// NVLS multicast accesses (nvls.cu maps the window's multicast alias): ld_reduce returns the sum
+// of every rank's copy of the address, reduced in the NVSwitch; st writes every rank's copy.
+__device__ __forceinline__ float4 nvls_ld_reduce4(const float* mc) {
+  float4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(mc) : "memory");
+  return v;
+}
+__device__ __forceinline__ float nvls_ld_reduce1(const float* mc) {
+  float v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(v) : "l"(mc) : "memory");
+  return v;
+}
+__device__ __forceinline__ void nvls_st4(float* mc, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};"
+               :: "l"(mc), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ void nvls_st1(float* mc, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" :: "l"(mc), "f"(v) : "memory");
+}
 
 // One-shot P2P exchange (p2p.cu): wait until every rank has published this step's packed
 // gradient (flags[r] >= epoch, acquire at system scope), then return the buffer parity.  A
@@ -545,6 +560,9 @@ template <int KIND, int V>
 __global__ void opt_kernel(OptArgs a) {
   int64_t pbuf = 0;   // P2P: offset of this step's buffer (parity of the epoch)
   if (a.p2p.world > 0) pbuf = (p2p_wait(a.p2p) & 1) ? a.p2p.stride : 0;
+  // NVLS: the peers wrote their buffers through unicast mappings; order the multicast reads after
+  // the flag acquire across the two address aliases
+  if (a.p2p.mc_buf0) asm volatile("fence.proxy.alias;" ::: "memory");
   const int64_t lo = a.p2p.lo, hi = a.p2p.hi < 0 ? a.n : a.p2p.hi;   // two-shot: this rank's slice
   int64_t b, e;
   cta_range(hi - lo, V, &b, &e);
@@ -558,7 +576,9 @@ __global__ void opt_kernel(OptArgs a) {
     if constexpr (V == 4) {
       const float4 wv = *reinterpret_cast<const float4*>(a.M + i);
       float4 gv;
-      if (a.p2p.world > 0) {   // fixed rank order: every rank computes the same sum, so M stays replicated
+      if (a.p2p.mc_buf0) {     // NVLS: the sum over the ranks, reduced in the switch
+        gv = nvls_ld_reduce4(a.p2p.mc_buf0 + pbuf + p);
+      } else if (a.p2p.world > 0) {   // fixed rank order: every rank computes the same sum, so M stays replicated
         gv = __ldcv(reinterpret_cast<const float4*>(a.p2p.buf0[0] + pbuf + p));
         for (int r = 1; r < a.p2p.world; ++r) {
           const float4 v = __ldcv(reinterpret_cast<const float4*>(a.p2p.buf0[r] + pbuf + p));
@@ -579,7 +599,9 @@ __global__ void opt_kernel(OptArgs a) {
       }
     } else {
       w[0] = a.M[i];
-      if (a.p2p.world > 0) {
+      if (a.p2p.mc_buf0) {
+        g[0] = nvls_ld_reduce1(a.p2p.mc_buf0 + pbuf + p);
+      } else if (a.p2p.world > 0) {
         g[0] = __ldcv(a.p2p.buf0[0] + pbuf + p);
         for (int r = 1; r < a.p2p.world; ++r) g[0] += __ldcv(a.p2p.buf0[r] + pbuf + p);
       } else {
@@ -590,7 +612,12 @@ __global__ void opt_kernel(OptArgs a) {
     }
 #pragma unroll
     for (int k = 0; k < V; ++k) w[k] = opt_update<KIND>(w[k], g[k], x[k], y[k], a.lr, a.b1, a.b2, a.eps, a.wd, a.bc1, a.bc2);
-    if (a.p2p.mout) {   // two-shot: publish this slice's new values for the gather phase
+    if (a.p2p.mc_mout) {   // NVLS two-shot: broadcast this slice's new values into every rank's window
+      if constexpr (V == 4)
+        nvls_st4(a.p2p.mc_mout + p, make_float4(w[0], w[1], w[2], w[3]));
+      else
+        nvls_st1(a.p2p.mc_mout + p, w[0]);
+    } else if (a.p2p.mout) {   // two-shot: publish this slice's new values for the gather phase
       if constexpr (V == 4)
         *reinterpret_cast<float4*>(a.p2p.mout + p) = make_float4(w[0], w[1], w[2], w[3]);
       else
@@ -601,13 +628,10 @@ __global__ void opt_kernel(OptArgs a) {
       if (KIND >= 1) *reinterpret_cast<float4*>(a.s1 + i) = make_float4(x[0], x[1], x[2], x[3]);
       if (KIND == 2) *reinterpret_cast<float4*>(a.s2 + i) = make_float4(y[0], y[1], y[2], y[3]);
       const __nv_bfloat162 p0 = __floats2bfloat162_rn(w[0], w[1]), p1 = __floats2bfloat162_rn(w[2], w[3]);
-      uint2 pos, neg;
+      uint2 pos;
       pos.x = *reinterpret_cast<const uint32_t*>(&p0);
       pos.y = *reinterpret_cast<const uint32_t*>(&p1);
-      neg.x = pos.x ^ 0x80008000u;   // bf16 negation = sign flip (exact)
-      neg.y = pos.y ^ 0x80008000u;
-      *reinterpret_cast<uint2*>(a.sh + i) = pos;
-      *reinterpret_cast<uint2*>(a.sh + a.neg_base + i) = neg;
+      a.so.store4(i, pos);   // both halves of every replica
       if (a.zero)
         *reinterpret_cast<float4*>(a.dM + i) = make_float4(0.f, 0.f, 0.f, 0.f);
       else if (a.p2p.world > 0)   // keep the documented dM contents: the summed gradient
@@ -616,9 +640,7 @@ __global__ void opt_kernel(OptArgs a) {
       a.M[i] = w[0];
       if (KIND >= 1) a.s1[i] = x[0];
       if (KIND == 2) a.s2[i] = y[0];
-      const __nv_bfloat16 b = __float2bfloat16_rn(w[0]);
-      a.sh[i] = b;
-      a.sh[a.neg_base + i] = __hneg(b);
+      a.so.store1(i, __bfloat16_as_ushort(__float2bfloat16_rn(w[0])));
       if (a.zero)
         a.dM[i] = 0.f;
       else if (a.p2p.world > 0)
@@ -648,10 +670,9 @@ cudaError_t launch_optimizer(Ctx* c, int kind, float lr, float b1, float b2, flo
   if (p2p) a.p2p = *p2p;
   a.M = c->M;
   a.dM = c->dM;
-  a.sh = reinterpret_cast<__nv_bfloat16*>(c->shadow);
+  a.so = shadow_out(c);
   a.s1 = c->opt_s1;
   a.s2 = c->opt_s2;
-  a.neg_base = c->neg_base;
   a.lr = lr;
   a.b1 = b1;
   a.b2 = b2;

@@ -40,10 +40,18 @@ struct PeerWins {
 // advances the local epoch.  Every CTA read the epoch before it arrived at the counter, so the
 // update cannot change the buffer any CTA chose.  Peers read this window through this GPU's
 // L2, so a GPU-scope fence per CTA orders the packed data before the flag.
+// NVLS (mc_flags = the multicast alias of the flags array): one multimem.st writes flags[rank] on
+// every rank, after fence.proxy.alias orders the unicast packing before the peers' multicast reads.
+__device__ __forceinline__ void nvls_signal(int* mc_flag, int e) {
+  asm volatile("fence.proxy.alias;" ::: "memory");
+  __threadfence_system();
+  asm volatile("multimem.st.release.sys.global.b32 [%0], %1;" ::"l"(mc_flag), "r"(e) : "memory");
+}
+
 template <int V>
 __global__ void p2p_post_kernel(const float* __restrict__ dM, PeerWins peers, int world, int rank, int64_t stride,
                                 const int64_t* __restrict__ start, const int64_t* __restrict__ prefix, int n_iv,
-                                int64_t total) {
+                                int64_t total, int* mc_flags) {
   using VT = typename std::conditional<V == 4, float4, float>::type;
   char* win = peers.w[rank];
   int* epoch = reinterpret_cast<int*>(win + 256);
@@ -65,7 +73,9 @@ __global__ void p2p_post_kernel(const float* __restrict__ dM, PeerWins peers, in
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (threadIdx.x < world) {
+  if (mc_flags) {
+    if (threadIdx.x == 0) nvls_signal(mc_flags + rank, e);
+  } else if (threadIdx.x < world) {
     int* f = reinterpret_cast<int*>(peers.w[threadIdx.x]) + rank;
     asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(f), "r"(e) : "memory");
   }
@@ -77,10 +87,12 @@ __global__ void p2p_post_kernel(const float* __restrict__ dM, PeerWins peers, in
 
 // two-shot: after this rank's slice of M is updated (and copied to its M buffer), publish the
 // current epoch in every rank's flags2[rank]
-__global__ void p2p_signal2_kernel(PeerWins peers, int world, int rank) {
+__global__ void p2p_signal2_kernel(PeerWins peers, int world, int rank, int* mc_flags2) {
   const int e = *reinterpret_cast<const volatile int*>(peers.w[rank] + 256);
   __threadfence();
-  if (threadIdx.x < world) {
+  if (mc_flags2) {
+    if (threadIdx.x == 0) nvls_signal(mc_flags2 + rank, e);
+  } else if (threadIdx.x < world) {
     int* f = reinterpret_cast<int*>(peers.w[threadIdx.x] + 128) + rank;
     asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(f), "r"(e) : "memory");
   }
@@ -93,8 +105,7 @@ struct Slices {   // packed-index slice [at[r], at[r + 1]) is updated by rank r
 // two-shot gather: wait until every rank has published its slice (flags2 >= epoch), then copy
 // the other ranks' new values into M at the touched slots, refresh both shadow halves, zero dM
 template <int V>
-__global__ void p2p_gather_kernel(float* __restrict__ M, float* __restrict__ dM, __nv_bfloat16* __restrict__ sh,
-                                  int64_t neg_base, PeerWins peers, int world, int rank, Slices sl, int64_t stride,
+__global__ void p2p_gather_kernel(float* __restrict__ M, float* __restrict__ dM, ShadowOut so, PeerWins peers, int world, int rank, Slices sl, int64_t stride,
                                   const int64_t* __restrict__ start, const int64_t* __restrict__ prefix, int n_iv,
                                   int64_t n, int* err) {
   __shared__ int s_ok;
@@ -120,6 +131,7 @@ __global__ void p2p_gather_kernel(float* __restrict__ M, float* __restrict__ dM,
       }
     }
     s_ok = 1;
+    asm volatile("fence.proxy.alias;" ::: "memory");   // NVLS: mout arrived through the multicast alias
   }
   __syncthreads();
   using VT = typename std::conditional<V == 4, float4, float>::type;
@@ -137,18 +149,13 @@ __global__ void p2p_gather_kernel(float* __restrict__ M, float* __restrict__ dM,
     *reinterpret_cast<VT*>(M + i) = v;
     if constexpr (V == 4) {
       const __nv_bfloat162 p0 = __floats2bfloat162_rn(v.x, v.y), p1 = __floats2bfloat162_rn(v.z, v.w);
-      uint2 pos, neg;
+      uint2 pos;
       pos.x = *reinterpret_cast<const uint32_t*>(&p0);
       pos.y = *reinterpret_cast<const uint32_t*>(&p1);
-      neg.x = pos.x ^ 0x80008000u;
-      neg.y = pos.y ^ 0x80008000u;
-      *reinterpret_cast<uint2*>(sh + i) = pos;
-      *reinterpret_cast<uint2*>(sh + neg_base + i) = neg;
+      so.store4(i, pos);
       *reinterpret_cast<float4*>(dM + i) = make_float4(0.f, 0.f, 0.f, 0.f);
     } else {
-      const __nv_bfloat16 bv = __float2bfloat16_rn(v);
-      sh[i] = bv;
-      sh[neg_base + i] = __hneg(bv);
+      so.store1(i, __bfloat16_as_ushort(__float2bfloat16_rn(v)));
       dM[i] = 0.f;
     }
   }
@@ -173,6 +180,11 @@ void p2p_release(Ctx* c) {
   c->p2p_world = 0;
 }
 
+// the window's multicast alias at byte offset off (NVLS bound), else null
+int* mc_int(const Ctx* c, int64_t off) {
+  return c->nvls_bound ? reinterpret_cast<int*>(c->nvls_mc_va + off) : nullptr;
+}
+
 bool p2p_ready(const Ctx* c) {
   return c->p2p_world > 0 && c->p2p_win && c->touched_valid && c->touched_for == int64_t(c->modules.size()) &&
          c->touched_n == c->p2p_n;
@@ -183,6 +195,8 @@ bool p2p_ready(const Ctx* c) {
 namespace roast {
 void p2p_destroy(Ctx* c) {
   p2p_release(c);
+  if (c->nvls_bound) c->p2p_win = nullptr;   // the window is the NVLS unicast mapping: nvls_destroy unmaps it
+  nvls_destroy(c);
   cudaFree(c->p2p_win);
   c->p2p_win = nullptr;
   c->p2p_bytes = c->p2p_n = 0;
@@ -195,6 +209,12 @@ roast_status_t roast_p2p_window(roast_t h, void** window, int64_t* bytes) {
   Ctx* c = pctx(h);
   if (!c || !c->dM) return fail(ROAST_ERR_STATE, "not bound");
   if (roast_status_t st = touched_prepare(c, 0)) return st;
+  if (c->nvls_bound) {   // the NVLS window was sized for this touched set at roast_nvls_bind
+    if (c->p2p_n != c->touched_n) return fail(ROAST_ERR_STATE, "NVLS window bound before the last registration");
+    if (window) *window = c->p2p_win;
+    if (bytes) *bytes = c->p2p_bytes;
+    return ROAST_OK;
+  }
   const int64_t n = (c->touched_n + 3) / 4 * 4;   // keep buffer 1 16-byte aligned
   const int64_t need = kP2PHeader + 3 * n * int64_t(sizeof(float));   // 2 gradient buffers + M buffer
   if (!c->p2p_win || c->p2p_n != c->touched_n) {
@@ -225,6 +245,7 @@ roast_status_t roast_p2p_ipc_handle(roast_t h, uint8_t handle[64]) {
 roast_status_t roast_p2p_attach(roast_t h, int32_t rank, int32_t world, void* const* windows) {
   Ctx* c = pctx(h);
   if (!c) return fail(ROAST_ERR_STATE, "null handle");
+  if (c->nvls_bound) return fail(ROAST_ERR_STATE, "p2p: this handle's window is bound to an NVLS multicast object");
   if (world < 1 || world > kP2PMaxWorld || rank < 0 || rank >= world || !windows)
     return fail(ROAST_ERR_CONFIG, "p2p: 1 <= world <= 8, 0 <= rank < world, windows[world]");
   if (roast_status_t st = roast_p2p_window(h, nullptr, nullptr)) return st;
@@ -239,6 +260,7 @@ roast_status_t roast_p2p_attach(roast_t h, int32_t rank, int32_t world, void* co
 roast_status_t roast_p2p_open(roast_t h, int32_t rank, int32_t world, const uint8_t* handles) {
   Ctx* c = pctx(h);
   if (!c) return fail(ROAST_ERR_STATE, "null handle");
+  if (c->nvls_bound) return fail(ROAST_ERR_STATE, "p2p: this handle's window is bound to an NVLS multicast object");
   if (world < 1 || world > kP2PMaxWorld || rank < 0 || rank >= world || !handles)
     return fail(ROAST_ERR_CONFIG, "p2p: 1 <= world <= 8, 0 <= rank < world, handles[world * 64]");
   if (roast_status_t st = roast_p2p_window(h, nullptr, nullptr)) return st;
@@ -277,10 +299,10 @@ roast_status_t roast_p2p_post(roast_t h, roast_stream_t stream) {
   blocks = std::min<int64_t>(std::max<int64_t>(blocks, 1), 148 * 8);
   if (V == 4)
     p2p_post_kernel<4><<<unsigned(blocks), 256, 0, s>>>(c->dM, pw, c->p2p_world, c->p2p_rank, stride, c->d_iv,
-                                                        c->d_iv + c->n_iv, c->n_iv, c->p2p_n);
+                                                        c->d_iv + c->n_iv, c->n_iv, c->p2p_n, mc_int(c, 0));
   else
     p2p_post_kernel<1><<<unsigned(blocks), 256, 0, s>>>(c->dM, pw, c->p2p_world, c->p2p_rank, stride, c->d_iv,
-                                                        c->d_iv + c->n_iv, c->n_iv, c->p2p_n);
+                                                        c->d_iv + c->n_iv, c->n_iv, c->p2p_n, mc_int(c, 0));
   ROAST_CUDA_CHECK(cudaGetLastError());
   c->launches++;
   return ROAST_OK;
@@ -298,6 +320,7 @@ roast_status_t roast_p2p_finish(roast_t h, const roast_opt_config_t* cfg, int64_
   v.flags = reinterpret_cast<const int*>(c->p2p_win);
   v.epoch = reinterpret_cast<const int*>(c->p2p_win + 256);
   v.err = c->d_err;
+  if (c->nvls_bound) v.mc_buf0 = reinterpret_cast<const float*>(c->nvls_mc_va + kP2PHeader);   // NVLS one-shot
   if (c->p2p_n == 0) return ROAST_OK;
   ROAST_CUDA_CHECK(launch_optimizer(c, cfg->kind, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay, step,
                                     cfg->zero_grad, true, s, nullptr, &v));
@@ -343,6 +366,10 @@ roast_status_t roast_p2p_reduce(roast_t h, const roast_opt_config_t* cfg, int64_
   v.lo = sl.at[c->p2p_rank];
   v.hi = sl.at[c->p2p_rank + 1];
   v.mout = reinterpret_cast<float*>(c->p2p_win + kP2PHeader) + 2 * v.stride;
+  if (c->nvls_bound) {   // NVLS: reduce the slice in the switch, broadcast its new values
+    v.mc_buf0 = reinterpret_cast<const float*>(c->nvls_mc_va + kP2PHeader);
+    v.mc_mout = reinterpret_cast<float*>(c->nvls_mc_va + kP2PHeader) + 2 * v.stride;
+  }
   if (c->p2p_n > 0) {   // an empty slice still runs: the kernel waits for every post first
     ROAST_CUDA_CHECK(launch_optimizer(c, cfg->kind, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay,
                                       step, 1, true, s, nullptr, &v));
@@ -350,7 +377,7 @@ roast_status_t roast_p2p_reduce(roast_t h, const roast_opt_config_t* cfg, int64_
   }
   PeerWins pw{};
   for (int r = 0; r < c->p2p_world; ++r) pw.w[r] = c->p2p_peer[r];
-  p2p_signal2_kernel<<<1, 32, 0, s>>>(pw, c->p2p_world, c->p2p_rank);
+  p2p_signal2_kernel<<<1, 32, 0, s>>>(pw, c->p2p_world, c->p2p_rank, mc_int(c, 128));
   ROAST_CUDA_CHECK(cudaGetLastError());
   c->launches++;
   return ROAST_OK;
@@ -369,13 +396,12 @@ roast_status_t roast_p2p_gather(roast_t h, roast_stream_t stream) {
   const int V = c->touched_vec ? 4 : 1;
   int64_t blocks = (c->p2p_n / V + 255) / 256;
   blocks = std::min<int64_t>(std::max<int64_t>(blocks, 1), 148 * 8);
-  auto* sh = reinterpret_cast<__nv_bfloat16*>(c->shadow);
   if (V == 4)
-    p2p_gather_kernel<4><<<unsigned(blocks), 256, 0, s>>>(c->M, c->dM, sh, c->neg_base, pw, c->p2p_world,
+    p2p_gather_kernel<4><<<unsigned(blocks), 256, 0, s>>>(c->M, c->dM, shadow_out(c), pw, c->p2p_world,
                                                           c->p2p_rank, sl, stride, c->d_iv, c->d_iv + c->n_iv,
                                                           c->n_iv, c->p2p_n, c->d_err);
   else
-    p2p_gather_kernel<1><<<unsigned(blocks), 256, 0, s>>>(c->M, c->dM, sh, c->neg_base, pw, c->p2p_world,
+    p2p_gather_kernel<1><<<unsigned(blocks), 256, 0, s>>>(c->M, c->dM, shadow_out(c), pw, c->p2p_world,
                                                           c->p2p_rank, sl, stride, c->d_iv, c->d_iv + c->n_iv,
                                                           c->n_iv, c->p2p_n, c->d_err);
   ROAST_CUDA_CHECK(cudaGetLastError());

@@ -64,9 +64,37 @@ struct P2PView {   // what the fused update kernel needs (kernels_simt.cu opt_ke
   // values are also written to mout[p] for the other ranks to gather
   int64_t lo = 0, hi = -1;                // hi < 0: all of [0, n)
   float* mout = nullptr;
+  // NVLS: the gradient of index p is multimem.ld_reduce(mc_buf0 + parity + p) (the sum over the
+  // ranks, reduced in the switch); two-shot new values go out with multimem.st to mc_mout + p
+  const float* mc_buf0 = nullptr;
+  float* mc_mout = nullptr;
 };
 
 #ifdef __CUDACC__
+// Writers of the bf16 shadow (sync_shadow, the optimizer pass, the P2P gather) refresh every
+// replica: at small |M| the shadow is kept `reps` times (rep_stride elements apart) so the
+// tcgen05 GEMMs' hashed-tile loads spread over reps x more L2 lines (CTA pair p reads replica
+// p % reps); 16-bit halves, V = 4 packed as uint2.
+struct ShadowOut {
+  unsigned short* sh;
+  int64_t neg_base;
+  int64_t rep_stride;
+  int reps;
+  __device__ __forceinline__ void store4(int64_t i, uint2 pos) const {
+    const uint2 neg = make_uint2(pos.x ^ 0x80008000u, pos.y ^ 0x80008000u);   // bf16 negation = sign flip
+    for (int r = 0; r < reps; ++r) {
+      *reinterpret_cast<uint2*>(sh + r * rep_stride + i) = pos;
+      *reinterpret_cast<uint2*>(sh + r * rep_stride + neg_base + i) = neg;
+    }
+  }
+  __device__ __forceinline__ void store1(int64_t i, unsigned short b) const {
+    for (int r = 0; r < reps; ++r) {
+      sh[r * rep_stride + i] = b;
+      sh[r * rep_stride + neg_base + i] = b ^ 0x8000u;
+    }
+  }
+};
+
 // Touched-slot traversal (exchange.cu pack, p2p.cu post, kernels_simt.cu opt_kernel): the
 // packed index space [0, n) is cut into one contiguous range per CTA (threads of a CTA still
 // touch consecutive vectors); a thread finds its interval once by binary search and afterwards
@@ -110,6 +138,7 @@ struct Ctx {
   uint16_t* shadow = nullptr;     // [2 * mem_size + pad] bf16 bits: +bf16(M) then -bf16(M)
   int64_t shadow_elems = 0;
   int64_t neg_base = 0;           // index of the negated copy (128-B aligned)
+  int shadow_reps = 1;            // replicas of the shadow, shadow_elems apart (small |M|: spread L2 lines)
   std::vector<Module> modules;
   // roast_register_linear_concat: linears sharing in_features fused along out_features (their
   // tile maps side by side, one GEMM per call); ids kGroupIdBase + index, outside the module
@@ -162,7 +191,20 @@ struct Ctx {
   int32_t p2p_rank = 0, p2p_world = 0;
   char* p2p_peer[kP2PMaxWorld] = {};
   bool p2p_opened[kP2PMaxWorld] = {};
+  // NVLS (nvls.cu): the window lives in driver-API memory bound to a multicast object; p2p_win
+  // is then its unicast mapping and nvls_mc_va the multicast mapping of the same offsets
+  unsigned long long nvls_mc = 0, nvls_phys = 0;       // CUmemGenericAllocationHandle
+  unsigned long long nvls_uc_va = 0, nvls_mc_va = 0;   // CUdeviceptr
+  size_t nvls_size = 0;
+  int32_t nvls_world = 0, nvls_dev = -1;
+  bool nvls_have_mc = false, nvls_added = false, nvls_memb = false, nvls_bound = false;
 };
+
+#ifdef __CUDACC__
+inline ShadowOut shadow_out(const Ctx* c) {
+  return ShadowOut{c->shadow, c->neg_base, c->shadow_elems, c->shadow_reps};
+}
+#endif
 
 // error reporting (thread-local detail string)
 roast_status_t fail(roast_status_t st, const std::string& msg);
@@ -175,6 +217,7 @@ roast_status_t cuda_fail(cudaError_t e, const char* what);
 
 void comm_destroy(Ctx* c);
 void p2p_destroy(Ctx* c);   // p2p.cu: close peer mappings, free the window
+void nvls_destroy(Ctx* c);  // nvls.cu: unmap and release the multicast object and its memory
 
 // touched-set exchange (exchange.cu): build the interval tables (host, synchronous uploads);
 // pack (dir 0: d_pack <- dM[touched]) or unpack (dir 1: dM[touched] <- scale * d_pack)

@@ -32,7 +32,8 @@ EXPORTS = [
     "roast_debug_exchange", "roast_zero_grad", "roast_sync_shadow", "roast_sgd_step", "roast_optimizer_step", "roast_grad_exchange_step",
     "roast_p2p_window", "roast_p2p_ipc_handle", "roast_p2p_open", "roast_p2p_attach", "roast_p2p_post",
     "roast_p2p_finish", "roast_grad_exchange_p2p", "roast_p2p_reduce", "roast_p2p_gather",
-    "roast_grad_exchange_p2p2", "roast_get_error",
+    "roast_grad_exchange_p2p2", "roast_nvls_supported", "roast_nvls_create", "roast_nvls_import",
+    "roast_nvls_add_device", "roast_nvls_bind", "roast_nvls_bound", "roast_nvls_reset", "roast_get_error",
     "roast_status_str", "roast_last_error", "roast_debug_tile_map", "roast_debug_chunk_map",
     "roast_debug_materialize", "roast_debug_hash_host", "roast_launch_count", "roast_lms_segments",
     "roast_debug_opt_state",
@@ -126,6 +127,13 @@ def _load():
         "roast_p2p_reduce": (st, [H, ctypes.POINTER(roast_opt_config_t), I64, S]),
         "roast_p2p_gather": (st, [H, S]),
         "roast_grad_exchange_p2p2": (st, [H, ctypes.POINTER(roast_opt_config_t), I64, S]),
+        "roast_nvls_supported": (st, [I32, ctypes.POINTER(I32)]),
+        "roast_nvls_create": (st, [H, I32, ctypes.POINTER(I32)]),
+        "roast_nvls_import": (st, [H, I32, I32]),
+        "roast_nvls_add_device": (st, [H]),
+        "roast_nvls_bind": (st, [H, I32]),
+        "roast_nvls_bound": (st, [H, ctypes.POINTER(I32)]),
+        "roast_nvls_reset": (st, [H]),
         "roast_get_error": (st, [H]),
         "roast_status_str": (ctypes.c_char_p, [st]),
         "roast_last_error": (ctypes.c_char_p, []),
@@ -441,6 +449,40 @@ def roast_p2p_gather(h, stream=0):
 def roast_grad_exchange_p2p2(h, kind, lr, step=1, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, stream=0):
     cfg = roast_opt_config_t(kind, lr, beta1, beta2, eps, weight_decay, 1, 1)
     _check(_lib.roast_grad_exchange_p2p2(h, ctypes.byref(cfg), step, stream), "roast_grad_exchange_p2p2")
+
+
+def roast_nvls_supported(device):
+    v = ctypes.c_int32()
+    _check(_lib.roast_nvls_supported(device, ctypes.byref(v)), "roast_nvls_supported")
+    return bool(v.value)
+
+
+def roast_nvls_create(h, world):
+    fd = ctypes.c_int32(-1)
+    _check(_lib.roast_nvls_create(h, world, ctypes.byref(fd)), "roast_nvls_create")
+    return int(fd.value)
+
+
+def roast_nvls_import(h, world, fd):
+    _check(_lib.roast_nvls_import(h, world, fd), "roast_nvls_import")
+
+
+def roast_nvls_add_device(h):
+    _check(_lib.roast_nvls_add_device(h), "roast_nvls_add_device")
+
+
+def roast_nvls_bind(h, rank):
+    _check(_lib.roast_nvls_bind(h, rank), "roast_nvls_bind")
+
+
+def roast_nvls_reset(h):
+    _check(_lib.roast_nvls_reset(h), "roast_nvls_reset")
+
+
+def roast_nvls_bound(h):
+    v = ctypes.c_int32()
+    _check(_lib.roast_nvls_bound(h, ctypes.byref(v)), "roast_nvls_bound")
+    return bool(v.value)
 
 
 def roast_get_error(h):
@@ -788,6 +830,98 @@ class Roast:
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
         roast_p2p_open(self.h, rank, world, b"".join(allh))
+
+    def exchange_init(self, group=None, prefer="auto"):
+        """Set up the fused exchange + update path (include/roast.h: NVLS, p2p).  NVLS when every
+        rank's device reports switch multicast and every driver step succeeds (NVSwitch systems),
+        else the CUDA-IPC P2P window (p2p_init).  prefer: "auto" | "nvls" (raise instead of
+        falling back) | "p2p".  Returns and records (self.exchange_path) "nvls" or "p2p"; the
+        reason for a fallback is kept in self.exchange_fallback."""
+        self.exchange_fallback = None
+        if prefer != "p2p":
+            try:
+                self._nvls_init(group)
+                self.exchange_path = "nvls"
+                return "nvls"
+            except (RoastError, OSError) as e:
+                if prefer == "nvls":
+                    raise
+                self.exchange_fallback = repr(e)
+                roast_nvls_reset(self.h)
+        self.p2p_init(group)
+        self.exchange_path = "p2p"
+        return "p2p"
+
+    def _nvls_init(self, group):
+        """Every rank in the same order: probe, create (rank 0) / import (fd over a unix socket),
+        add device, bind; a failure on any rank makes every rank raise (all_gather of the status
+        after each step), so all fall back together."""
+        import socket
+        import uuid
+        torch = self.torch
+        import torch.distributed as dist
+        multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+        rank = dist.get_rank(group) if multi else 0
+        world = dist.get_world_size(group) if multi else 1
+
+        def agree(ok, what):
+            oks = [None] * world
+            if multi:
+                dist.all_gather_object(oks, ok, group=group)
+            else:
+                oks = [ok]
+            if not all(o is True for o in oks):
+                bad = [f"rank {r}: {o}" for r, o in enumerate(oks) if o is not True]
+                raise RoastError(4, f"nvls {what} ({'; '.join(bad)})")
+
+        def attempt(fn):
+            try:
+                fn()
+                return True
+            except (RoastError, OSError) as e:
+                return repr(e)
+
+        sup = roast_nvls_supported(torch.cuda.current_device())
+        agree(True if sup else "CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED = 0", "probe")
+        fd_box = [-1]
+        agree(attempt(lambda: fd_box.__setitem__(0, roast_nvls_create(self.h, world))) if rank == 0 else True,
+              "create")
+        try:
+            if multi:   # the descriptor travels over an abstract unix socket (SCM_RIGHTS)
+                name = [("\0roast-nvls-" + uuid.uuid4().hex) if rank == 0 else None]
+                dist.broadcast_object_list(name, src=0, group=group)
+                if rank == 0:
+                    srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+                    srv.bind(name[0])
+                    srv.listen(world)
+                    dist.barrier(group=group)
+                    for _ in range(world - 1):
+                        conn, _ = srv.accept()
+                        socket.send_fds(conn, [b"f"], [fd_box[0]])
+                        conn.close()
+                    srv.close()
+                    ok = True
+                else:
+                    dist.barrier(group=group)
+                    cl = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+                    cl.connect(name[0])
+                    _, fds, _, _ = socket.recv_fds(cl, 1, 1)
+                    cl.close()
+                    ok = attempt(lambda: roast_nvls_import(self.h, world, fds[0]))
+                    os.close(fds[0])
+                agree(ok, "import")
+        finally:
+            if fd_box[0] >= 0:
+                os.close(fd_box[0])
+        agree(attempt(lambda: roast_nvls_add_device(self.h)), "add_device")
+        agree(attempt(lambda: roast_nvls_bind(self.h, rank)), "bind")
+        if multi:
+            dist.barrier(group=group)
+
+    def exchange_fused(self, kind, lr, step=1, stream=None, **kw):
+        """The set-up path's two-shot exchange + update (NVLS or P2P; M stays replicated bit for
+        bit on both): dM summed over the ranks, optimizer, shadow refresh, dM zeroed."""
+        self.exchange_p2p2(kind, lr, step, stream=stream, **kw)
 
     def p2p_attach(self, rank, windows):
         roast_p2p_attach(self.h, rank, len(windows), windows)

@@ -41,10 +41,11 @@ def main():
     ap.add_argument("--dims", default="768,3072", help="d_model,d_ff of the two layers (C3 attention: 768,768)")
     ap.add_argument("--wm", default="", help="restrict to these WM values, e.g. 1,2")
     ap.add_argument("--prof", action="store_true", help="also print one ROAST_PROF counter line per config")
+    ap.add_argument("--mem", type=int, default=47192, help="|M| (C2: 471864 / 47192 / 4720 at 10x / 100x / 1000x)")
     args = ap.parse_args()
     T = args.T
     D, F = [int(v) for v in args.dims.split(",")]
-    M = torch.rand(47192, device="cuda") * 2 - 1
+    M = torch.rand(args.mem, device="cuda") * 2 - 1
     ctx = R.Roast(M, 64, 64)
     ctx.set_autotune(0)
     l1 = ctx.linear(D, F)
