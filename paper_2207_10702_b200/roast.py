@@ -872,7 +872,7 @@ class Roast:
                 oks = [ok]
             if not all(o is True for o in oks):
                 bad = [f"rank {r}: {o}" for r, o in enumerate(oks) if o is not True]
-                raise RoastError(4, f"nvls {what} ({'; '.join(bad)})")
+                raise RoastError(9, f"nvls {what} ({'; '.join(bad)})")
 
         def attempt(fn):
             try:
