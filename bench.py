@@ -382,7 +382,7 @@ class C2Step:
         # the backward's schedule, training-optimal at the step level: the fused launch unless the
         # separate dX / dM launches on two streams make the whole step faster (e.g. at 1000x the
         # tiny dM's reduce-add hot spot favours spreading the dM GEMMs out)
-        if autotune == 2 and not tuned_file and self.bwd == "fused":
+        if autotune == 2 and not tuned_file and self.bwd == "fused" and not os.environ.get("ROAST_BENCH_KEEP_BWD"):
             t_fused = self.step_ms()
             self.bwd = "streams"
             t_streams = self.step_ms()

@@ -2314,10 +2314,10 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
   if (det) {   // fixed order: module b's slots, then module a's (each: covering tiles, then splits)
     const int sp_b = mp.p[1].units / (mp.p[1].m_tiles * mp.p[1].n_tiles);
     const int sp_a = mp.p[3].units / (mp.p[3].m_tiles * mp.p[3].n_tiles);
-    if ((e = launch_det_reduce(c, mbm, ws.as<float>(), sp_b, s)) != cudaSuccess) return cuda_fail(e, "det_reduce");
-    if ((e = launch_det_reduce(c, ma, ws.as<float>() + ws_rows[0] * 64, sp_a, s)) != cudaSuccess)
+    if ((e = launch_det_reduce2(c, mbm, ws.as<float>(), sp_b, &ma, ws.as<float>() + ws_rows[0] * 64, sp_a, s)) !=
+        cudaSuccess)
       return cuda_fail(e, "det_reduce");
-    c->launches += 2;
+    c->launches += 1;
   }
   if (mp.prof) {
     cudaDeviceSynchronize();

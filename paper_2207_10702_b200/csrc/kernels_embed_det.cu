@@ -105,7 +105,8 @@ struct ChunkInfo {
 __global__ void emb_chunkmap_kernel(const uint32_t* __restrict__ keys, const int32_t* __restrict__ heads,
                                     const int32_t* __restrict__ nseg_p, const int32_t* __restrict__ nvalid_p,
                                     const int32_t* __restrict__ nch, const int32_t* __restrict__ choff,
-                                    const int32_t* __restrict__ loff, int G, ChunkInfo* __restrict__ info) {
+                                    const int32_t* __restrict__ loff, int G, ChunkInfo* __restrict__ info,
+                                    int32_t* __restrict__ long_n, int32_t* __restrict__ long_list) {
   const int64_t sg = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nseg = *nseg_p;
   if (sg >= nseg) return;
@@ -113,6 +114,7 @@ __global__ void emb_chunkmap_kernel(const uint32_t* __restrict__ keys, const int
   const int32_t e = sg + 1 < nseg ? heads[sg + 1] : *nvalid_p;
   const uint32_t group = keys[h] / uint32_t(G);
   const int c = nch[sg];
+  if (c > 1) long_list[atomicAdd(long_n, 1)] = int32_t(sg);   // pass 2 visits only these (any order)
   for (int k = 0; k < c; ++k) {   // a Zipf-hot group writes its few dozen entries serially
     ChunkInfo ci;
     ci.begin = h + k * kW;
@@ -280,17 +282,20 @@ __global__ void emb_chunk_sub_kernel(float* __restrict__ dM, float* __restrict__
   }
 }
 
-// pass 2: one warp per multi-chunk group: its partials in chunk order, then dM
+// pass 2: one warp per multi-chunk group (the list emb_chunkmap_kernel appended; each group is
+// summed on its own, so the list order does not matter): its partials in chunk order, then dM
 __global__ void emb_longseg_kernel(float* __restrict__ dM, const float* __restrict__ partial,
                                    const uint32_t* __restrict__ keys, const int32_t* __restrict__ heads,
-                                   const int32_t* __restrict__ nseg_p, const int32_t* __restrict__ nch,
-                                   const int32_t* __restrict__ loff, int G, int A, int64_t mem_size) {
+                                   const int32_t* __restrict__ long_n, const int32_t* __restrict__ long_list,
+                                   const int32_t* __restrict__ nch, const int32_t* __restrict__ loff, int G, int A,
+                                   int64_t mem_size) {
   const int lane = threadIdx.x & 31;
-  const int64_t nseg = *nseg_p;
+  const int64_t nlong = *long_n;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t sg = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; sg < nseg; sg += nwarps) {
+  for (int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; j < nlong; j += nwarps) {
+    const int64_t sg = long_list[j];
     const int c = nch[sg];
-    if (c <= 1 || lane >= A) continue;
+    if (lane >= A) continue;
     float acc = 0.f;
     for (int k = 0; k < c; ++k) acc += partial[(int64_t(loff[sg]) + k) * A + lane];
     const int64_t s = int64_t(keys[heads[sg]] / uint32_t(G)) * A + lane;
@@ -358,7 +363,7 @@ roast_status_t embed_bwd_det_group(Ctx* c, const Module* const* mods, int nt, co
   // [keys in | keys out | vals in | vals out | heads | nch | choff | nlong | loff (ni + 1 each) |
   //  partial (max_long x A fp32) | flags (u8) | 4 scalars | temp]
   const size_t bytes = size_t(ni) * 16 + size_t(ni1) * 20 + size_t(ni1 + ni / kW + 1) * 16 + 16 +
-                       size_t(max_long) * A * 4 + size_t(ni) + 1024 + temp;
+                       size_t(max_long) * A * 4 + size_t(ni) + 1024 + size_t(ni / kW + 2) * 4 + 16 + temp;
   Scratch ws;
   roast_status_t st = scratch_alloc(ws, bytes, s);
   if (st) return st;
@@ -378,7 +383,10 @@ roast_status_t embed_bwd_det_group(Ctx* c, const Module* const* mods, int nt, co
   int32_t* scal = reinterpret_cast<int32_t*>((reinterpret_cast<uintptr_t>(flags + ni) + 15) & ~uintptr_t(15));
   int32_t* nseg = scal;
   int32_t* nvalid = scal + 1;
-  void* tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(scal + 4) + 255) & ~uintptr_t(255));
+  int32_t* long_n = scal + 2;
+  int32_t* long_list = scal + 4;   // multi-chunk groups (each has > kW items): <= ni / kW of them
+  void* tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(long_list + ni / kW + 2) + 255) & ~uintptr_t(255));
+  ROAST_CUDA_CHECK(cudaMemsetAsync(long_n, 0, sizeof(int32_t), s));
   emb_items_kernel<<<unsigned((np + 255) / 256), 256, 0, s>>>(T, idx, int64_t(nt) * n, m.chunks_per_row, G, k_in,
                                                               v_in, c->d_err, nvalid);
   ROAST_CUDA_CHECK(cudaGetLastError());
@@ -395,7 +403,7 @@ roast_status_t embed_bwd_det_group(Ctx* c, const Module* const* mods, int nt, co
   t3 = temp;
   ROAST_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp, t3, nlong, loff, ni1, s));
   emb_chunkmap_kernel<<<unsigned((ni1 + 255) / 256), 256, 0, s>>>(k_out, heads, nseg, nvalid, nch, choff, loff, G,
-                                                                    info);
+                                                                    info, long_n, long_list);
   ROAST_CUDA_CHECK(cudaGetLastError());
   const int grid = 148 * 8;
   if (A % 4 == 0 && A <= 32 && !getenv("ROAST_EMB_DET_WARP"))
@@ -405,9 +413,10 @@ roast_status_t embed_bwd_det_group(Ctx* c, const Module* const* mods, int nt, co
     emb_chunk_kernel<<<grid, 256, 0, s>>>(c->dM, partial, v_out, info, nseg, nch, choff, dOut, m.dim, m.chunk,
                                           m.chunks_per_row, G, A, L, c->mem_size);
   ROAST_CUDA_CHECK(cudaGetLastError());
-  emb_longseg_kernel<<<grid, 256, 0, s>>>(c->dM, partial, k_out, heads, nseg, nch, loff, G, A, c->mem_size);
+  emb_longseg_kernel<<<148 * 2, 256, 0, s>>>(c->dM, partial, k_out, heads, long_n, long_list, nch, loff, G, A,
+                                            c->mem_size);
   ROAST_CUDA_CHECK(cudaGetLastError());
-  c->launches += 9;
+  c->launches += 9;   // (+ one memset)
   return ROAST_OK;
 }
 }  // namespace

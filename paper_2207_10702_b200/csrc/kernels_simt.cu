@@ -235,17 +235,69 @@ __global__ void det_reduce_kernel(float* __restrict__ dM, const float* __restric
 // K5 for heavily shared memories (C2 at 100x: ~50 covering tiles x splits per slot): one warp
 // per 4-slot group.  Lane l sums the (tile, split) terms l, l + 32, ... in order, then a fixed
 // xor butterfly combines the lanes: a fixed order (bitwise reproducible), with 32x the
-// parallelism of one thread walking 50+ terms per group.
-__global__ void det_reduce_warp_kernel(float* __restrict__ dM, const float* __restrict__ ws,
-                                       const int32_t* __restrict__ sorted, const int64_t* __restrict__ sorted_off,
-                                       int ntiles, int64_t tile_elems, int nsplit, int64_t mem_size,
-                                       const int64_t* __restrict__ iv_start, const int64_t* __restrict__ iv_prefix,
-                                       int n_iv, int64_t n_touched, const int2* __restrict__ cover) {
+// parallelism of one thread walking 50+ terms per group.  NM = 2 reduces two modules' workspaces
+// in one launch with the result of two NM = 1 launches in module order: dM = (dM + sum_0) + sum_1.
+struct DetMod {
+  const float* ws;
+  const int32_t* sorted;
+  const int64_t* sorted_off;
+  const int2* cover;   // static covering range per 4-slot group (built at registration), or null
+  int ntiles, nsplit;
+};
+
+__device__ __forceinline__ int2 det_cover(const DetMod& m, int64_t s, int64_t tile_elems) {
+  if (m.cover) return __ldg(m.cover + (s >> 2));
+  int x = 0, y = m.ntiles;
+  const int64_t key = s - tile_elems;
+  while (x < y) { int mid = (x + y) >> 1; if (__ldg(m.sorted_off + mid) > key) y = mid; else x = mid + 1; }
+  const int lo = x;
+  y = m.ntiles;
+  while (x < y) { int mid = (x + y) >> 1; if (__ldg(m.sorted_off + mid) > s) y = mid; else x = mid + 1; }
+  return make_int2(lo, x);
+}
+
+// lane l's terms l, l + 32, ..., l + 32 (U - 1) of a module's covering list starting at k0:
+// their workspace offsets (issued together so the loads overlap); -1 past the end
+template <int U>
+__device__ __forceinline__ void det_bases(const DetMod& m, int2 r, int k0, int64_t s, int64_t tile_elems,
+                                          int64_t* base) {
+  const int nterms = (r.y - r.x) * m.nsplit;
+  const int64_t split_stride = int64_t(m.ntiles) * tile_elems;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int k = k0 + 32 * u;
+    base[u] = -1;
+    if (k < nterms) {
+      const int i = r.x + k / m.nsplit, sp = k - (k / m.nsplit) * m.nsplit;
+      base[u] = sp * split_stride + int64_t(__ldg(m.sorted + i)) * tile_elems + (s - __ldg(m.sorted_off + i));
+    }
+  }
+}
+
+__device__ __forceinline__ float4 warp_sum4(float4 a) {   // fixed xor butterfly (same order on every run)
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    a.x += __shfl_xor_sync(0xffffffffu, a.x, off);
+    a.y += __shfl_xor_sync(0xffffffffu, a.y, off);
+    a.z += __shfl_xor_sync(0xffffffffu, a.z, off);
+    a.w += __shfl_xor_sync(0xffffffffu, a.w, off);
+  }
+  return a;
+}
+
+template <int NM>
+struct DetMods {
+  DetMod m[NM];
+};
+
+template <int NM>
+__global__ void det_reduce_warp_kernel(float* __restrict__ dM, const __grid_constant__ DetMods<NM> mods,
+                                       int64_t tile_elems, int64_t mem_size, const int64_t* __restrict__ iv_start,
+                                       const int64_t* __restrict__ iv_prefix, int n_iv, int64_t n_touched) {
   const int lane = threadIdx.x & 31;
   const int64_t n = n_iv > 0 ? n_touched : mem_size;
   const int64_t ngroups = (n + 3) / 4;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  const int64_t split_stride = int64_t(ntiles) * tile_elems;
   for (int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; g < ngroups; g += nwarps) {
     int64_t s = g * 4;
     if (n_iv > 0) {
@@ -254,45 +306,49 @@ __global__ void det_reduce_warp_kernel(float* __restrict__ dM, const float* __re
       s = w.slot(s);
     }
     if (s >= mem_size) continue;
-    int lo, hi;
-    if (cover) {   // static covering range of this 4-slot group (built at registration)
-      const int2 r = __ldg(cover + (s >> 2));
-      lo = r.x;
-      hi = r.y;
-    } else {
-      int x = 0, y = ntiles;
-      const int64_t key = s - tile_elems;
-      while (x < y) { int mid = (x + y) >> 1; if (__ldg(sorted_off + mid) > key) y = mid; else x = mid + 1; }
-      lo = x;
-      y = ntiles;
-      while (x < y) { int mid = (x + y) >> 1; if (__ldg(sorted_off + mid) > s) y = mid; else x = mid + 1; }
-      hi = x;
-    }
-    if (lo >= hi) continue;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int nterms = (hi - lo) * nsplit;
-    for (int k = lane; k < nterms; k += 32) {
-      const int i = lo + k / nsplit, sp = k - (k / nsplit) * nsplit;
-      const int64_t base = int64_t(__ldg(sorted + i)) * tile_elems + (s - __ldg(sorted_off + i));
-      const float4 v = *reinterpret_cast<const float4*>(ws + sp * split_stride + base);
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    // every module's covering range, then, U terms at a time, their offsets, the workspace
+    // loads and the in-order per-lane sums: lane l adds terms l, l + 32, ... of each module
+    // (U = 8 over both modules at once was slower: 35 vs 26 us at C2, 66 registers)
+    constexpr int U = 4;
+    int2 r[NM];
+#pragma unroll
+    for (int j = 0; j < NM; ++j) r[j] = det_cover(mods.m[j], s, tile_elems);
+    float4 acc[NM];
+#pragma unroll
+    for (int j = 0; j < NM; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < NM; ++j) {
+      const int nt = (r[j].y - r[j].x) * mods.m[j].nsplit;
+      for (int k0 = lane; k0 - lane < nt; k0 += 32 * U) {
+        int64_t base[U];
+        det_bases<U>(mods.m[j], r[j], k0, s, tile_elems, base);
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          v[u] = base[u] >= 0 ? *reinterpret_cast<const float4*>(mods.m[j].ws + base[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (base[u] >= 0) {
+            acc[j].x += v[u].x; acc[j].y += v[u].y; acc[j].z += v[u].z; acc[j].w += v[u].w;
+          }
+      }
     }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-      acc.z += __shfl_xor_sync(0xffffffffu, acc.z, off);
-      acc.w += __shfl_xor_sync(0xffffffffu, acc.w, off);
-    }
+    for (int j = 0; j < NM; ++j) acc[j] = warp_sum4(acc[j]);
     if (lane == 0) {
       if (s + 4 <= mem_size) {
         float4* d = reinterpret_cast<float4*>(dM + s);
         float4 o = *d;
-        o.x += acc.x; o.y += acc.y; o.z += acc.z; o.w += acc.w;
+#pragma unroll
+        for (int j = 0; j < NM; ++j) {
+          o.x += acc[j].x; o.y += acc[j].y; o.z += acc[j].z; o.w += acc[j].w;
+        }
         *d = o;
       } else {   // |M| % 4 != 0: the last group is partial
-        const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
-        for (int k = 0; s + k < mem_size; ++k) dM[s + k] += a4[k];
+        for (int j = 0; j < NM; ++j) {
+          const float a4[4] = {acc[j].x, acc[j].y, acc[j].z, acc[j].w};
+          for (int k = 0; s + k < mem_size; ++k) dM[s + k] += a4[k];
+        }
       }
     }
   }
@@ -411,35 +467,65 @@ cudaError_t launch_simt_dw(const Ctx* c, const Module& m, const void* X, const v
   return cudaGetLastError();
 }
 
-cudaError_t launch_det_reduce(Ctx* c, const Module& m, const float* ws, int nsplit, cudaStream_t s) {
+namespace {
+// mean number of covering tiles per visited slot: a warp per slot group when it is high (C2 at
+// 100x: 50; C5: 1-8, where the per-thread incremental walk wins: 0.72 vs 1.23 ms at 8 MB, 0.75
+// vs 4.1 ms at 2 GB)
+bool det_warp_variant(const Ctx* c, const Module& m, bool touched) {
+  const int64_t visited = touched ? c->touched_n : c->mem_size;
+  const double cover = double(int64_t(m.nx) * m.ny) * double(c->tile.z1) * c->tile.z2 / double(std::max<int64_t>(visited, 1));
+  return cover >= 16.0;
+}
+
+bool det_touched(Ctx* c, cudaStream_t s) {
   if (!(c->touched_valid && c->touched_for == int64_t(c->modules.size()))) {   // build once, eagerly
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) touched_prepare(c, s);
   }
-  const bool touched = c->touched_valid && c->touched_for == int64_t(c->modules.size()) && c->touched_vec &&
-                       c->n_iv > 0;
-  int64_t nthreads = ((touched ? c->touched_n : c->mem_size) + 3) / 4;
-  int threads = 256;
-  // mean number of covering tiles per visited slot: a warp per slot group when it is high
-  // (C2 at 100x: 50; C5: 1-8, where the per-thread incremental walk wins: 0.72 vs 1.23 ms at
-  // 8 MB, 0.75 vs 4.1 ms at 2 GB)
-  const int64_t visited = touched ? c->touched_n : c->mem_size;
-  const double cover = double(int64_t(m.nx) * m.ny) * double(c->tile.z1) * c->tile.z2 / double(std::max<int64_t>(visited, 1));
-  if (cover >= 16.0) {
-    const int64_t blocks = std::min<int64_t>((nthreads * 32 + threads - 1) / threads, 148 * 16);
-    det_reduce_warp_kernel<<<unsigned(blocks), threads, 0, s>>>(
-        c->dM, ws, m.d_sorted, m.d_sorted_off, m.nx * m.ny, int64_t(c->tile.z1) * c->tile.z2, nsplit, c->mem_size,
-        touched ? c->d_iv : nullptr, touched ? c->d_iv + c->n_iv : nullptr, touched ? c->n_iv : 0,
-        touched ? c->touched_n : 0, reinterpret_cast<const int2*>(m.d_cover));
+  return c->touched_valid && c->touched_for == int64_t(c->modules.size()) && c->touched_vec && c->n_iv > 0;
+}
+
+DetMod det_mod(const Module& m, const float* ws, int nsplit) {
+  return DetMod{ws, m.d_sorted, m.d_sorted_off, reinterpret_cast<const int2*>(m.d_cover), m.nx * m.ny, nsplit};
+}
+}  // namespace
+
+cudaError_t launch_det_reduce2(Ctx* c, const Module& m0, const float* ws0, int ns0, const Module* m1,
+                               const float* ws1, int ns1, cudaStream_t s) {
+  const bool touched = det_touched(c, s);
+  const int threads = 256;
+  const int64_t ngroups = ((touched ? c->touched_n : c->mem_size) + 3) / 4;
+  const bool warp0 = det_warp_variant(c, m0, touched), warp1 = m1 && det_warp_variant(c, *m1, touched);
+  const int64_t* ivs = touched ? c->d_iv : nullptr;
+  const int64_t* ivp = touched ? c->d_iv + c->n_iv : nullptr;
+  const int niv = touched ? c->n_iv : 0;
+  const int64_t nt = touched ? c->touched_n : 0;
+  const int64_t te = int64_t(c->tile.z1) * c->tile.z2;
+  if (warp0 && (warp1 || !m1)) {
+    const int64_t blocks = std::min<int64_t>((ngroups * 32 + threads - 1) / threads, 148 * 16);
+    if (m1) {
+      const DetMods<2> md{{det_mod(m0, ws0, ns0), det_mod(*m1, ws1, ns1)}};
+      det_reduce_warp_kernel<2><<<unsigned(blocks), threads, 0, s>>>(c->dM, md, te, c->mem_size, ivs, ivp, niv, nt);
+    } else {
+      const DetMods<1> md{{det_mod(m0, ws0, ns0)}};
+      det_reduce_warp_kernel<1><<<unsigned(blocks), threads, 0, s>>>(c->dM, md, te, c->mem_size, ivs, ivp, niv, nt);
+    }
     return cudaGetLastError();
   }
-  int64_t blocks = std::min<int64_t>((nthreads + threads - 1) / threads, 148 * 32);
-  det_reduce_kernel<<<unsigned(blocks), threads, 0, s>>>(c->dM, ws, m.d_sorted, m.d_sorted_off, m.nx * m.ny,
-                                                         int64_t(c->tile.z1) * c->tile.z2, nsplit, c->mem_size,
-                                                         touched ? c->d_iv : nullptr,
-                                                         touched ? c->d_iv + c->n_iv : nullptr,
-                                                         touched ? c->n_iv : 0, touched ? c->touched_n : 0);
-  return cudaGetLastError();
+  // per-thread incremental walk, one module per launch (in module order)
+  for (int j = 0; j < (m1 ? 2 : 1); ++j) {
+    const Module& m = j ? *m1 : m0;
+    const int64_t blocks = std::min<int64_t>((ngroups + threads - 1) / threads, 148 * 32);
+    det_reduce_kernel<<<unsigned(blocks), threads, 0, s>>>(c->dM, j ? ws1 : ws0, m.d_sorted, m.d_sorted_off,
+                                                           m.nx * m.ny, te, j ? ns1 : ns0, c->mem_size, ivs, ivp, niv, nt);
+    if (cudaError_t e = cudaGetLastError()) return e;
+    if (j) c->launches++;   // the caller counts one launch
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_det_reduce(Ctx* c, const Module& m, const float* ws, int nsplit, cudaStream_t s) {
+  return launch_det_reduce2(c, m, ws, nsplit, nullptr, nullptr, 0, s);
 }
 
 cudaError_t launch_sync_shadow(Ctx* c, cudaStream_t s) {

@@ -255,6 +255,9 @@ int colsum_slabs(int64_t T, int n);
 cudaError_t launch_simt_dw(const Ctx* c, const Module& m, const void* X, const void* dY, int64_t T,
                            roast_dtype_t dt, float* ws, cudaStream_t s);
 cudaError_t launch_det_reduce(Ctx* c, const Module& m, const float* ws, int nsplit, cudaStream_t s);
+// two modules' workspaces into dM in one launch: the result of launch_det_reduce(m0) then (m1)
+cudaError_t launch_det_reduce2(Ctx* c, const Module& m0, const float* ws0, int ns0, const Module* m1,
+                               const float* ws1, int ns1, cudaStream_t s);
 cudaError_t launch_sync_shadow(Ctx* c, cudaStream_t s);
 cudaError_t launch_optimizer(Ctx* c, int kind, float lr, float b1, float b2, float eps, float wd, int64_t step,
                              int zero, bool touched_only, cudaStream_t s, const float* gpack = nullptr,
