@@ -374,16 +374,16 @@ def test_embedding_deterministic_parity_and_reproducible(R, torch, dist, align):
 @pytest.mark.parametrize("align", [8, 32])
 def test_embedding_deterministic_hot_rows(R, torch, align):
     """The deterministic backward's per-group ordering at every size class: groups of <= 16 items
-    (sorted by one thread), 17..256 (a warp's bitonic sort), 257..4096 (a CTA's, in shared
-    memory; > 64 items also split into chunks with partials) and > 4096 (the in-place
-    global-memory network): one row looked up 20 000 times, others 3000 / 40 times, among
-    uniform lookups, shuffled.  <= 1e-5 vs the oracle and bitwise identical over 3 runs."""
+    (sorted by one thread), 17..256 (a warp's bitonic sort), 257..8192 (a CTA's block radix
+    sort; > 64 items also split into chunks with partials) and > 8192 (the tiled bitonic
+    network): one row looked up 20 000 times, others 3000 / 40 times, among uniform lookups,
+    shuffled.  <= 1e-5 vs the oracle and bitwise identical over 3 runs."""
     mem, rows, d, Z = 100_000, 1000, 128, 32
     M_np = store(mem)
     ctx, _ = make_ctx(R, torch, M_np, 64, 64, deterministic=True, align=align)
     mid = ctx.embedding(rows, d, Z)
     rng = np.random.default_rng(7)
-    idx_np = np.concatenate([np.full(20_000, 7), np.full(3000, 11), np.full(40, 13),
+    idx_np = np.concatenate([np.full(20_000, 7), np.full(3000, 11), np.full(700, 12), np.full(40, 13),
                              synth.uniform_indices(synth.SEED_IDX, 5000, rows)]).astype(np.int64)
     idx_np = idx_np[rng.permutation(len(idx_np))]
     dout_np = synth.normal(synth.SEED_DY, (len(idx_np), d)).astype(np.float32)
