@@ -2027,8 +2027,16 @@ struct MixPlan {
 // the priority order whose data is ready (P2: P0 tiles (mb, 0..) published; P3: the P0 tiles of
 // its token range), P1 (no dependency) as filler, else waits for the earliest ready one.
 // Dependent units stream their K loop behind the P0 tiles they read.
+// deterministic mode: makespan cost of one more DW split, in DX k-block units (the reduce of the
+// two modules' workspaces reads every split's partial of every covering tile: ~9 us per split at
+// C2, ~0.8 us per k-block).  ROAST_DET_SPLIT_COST overrides (planner experiments).
+double det_split_cost() {
+  const char* e = getenv("ROAST_DET_SPLIT_COST");
+  return e ? atof(e) : 11.0;
+}
+
 MixPlan plan_mix(int mt0, int nt0, int kb0, int mt1, int nt1, int kbT, int mt2, int nt2, int kb2, int mt3, int nt3,
-                 int npairs) {
+                 int npairs, double split_cost) {
   const double EPI_DX = 3.0, EPI_DW = 1.0, LAT = 1.0;
   MixPlan best;
   const int units0 = mt0 * nt0;
@@ -2108,7 +2116,8 @@ MixPlan plan_mix(int mt0, int nt0, int kb0, int mt1, int nt1, int kbT, int mt2, 
             lists[q].push_back((3 << 24) | q3[i3++]);
           }
         }
-        const double mk = *std::max_element(free_t.begin(), free_t.end());
+        // deterministic mode: the fixed-order reduce after the launch reads sp partials per slot
+        const double mk = *std::max_element(free_t.begin(), free_t.end()) + split_cost * sp;
         if (mk < best.makespan - 1e-9) {
           best.makespan = mk;
           best.s1 = best.s3 = sp;
@@ -2134,7 +2143,7 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
   if (ma.H % 256 || ma.O % 256 || mbm.O % 256 || mbm.H != ma.O || !dX_a) return ROAST_ERR_UNSUPPORTED;
   const int pairs = num_sms() / 2;
   const int mtT = int((T + 511) / 512), kbT = int((T + BK - 1) / BK);
-  const std::array<int64_t, 6> key{2, ma.H, ma.O, mbm.H, mbm.O, T};
+  const std::array<int64_t, 6> key{det ? 3 : 2, ma.H, ma.O, mbm.H, mbm.O, T};   // det plans differ (split cost)
   auto it = c->chain_plans.find(key);
   static std::map<std::array<int64_t, 6>, std::pair<int, int>> splits;   // plan key -> (s1, s3)
   if (it == c->chain_plans.end()) {
@@ -2161,7 +2170,8 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
       cudaGetLastError();
     }
     MixPlan plan = plan_mix(mtT, int(mbm.H / 256), int(mbm.O / BK), int(mbm.H / 256), int(mbm.O / 256), kbT, mtT,
-                            int(ma.H / 256), int(ma.O / BK), int(ma.H / 256), int(ma.O / 256), pairs);
+                            int(ma.H / 256), int(ma.O / BK), int(ma.H / 256), int(ma.O / 256), pairs,
+                            det ? det_split_cost() : 0.0);
     int32_t* d = nullptr;
     if (resident) {
       ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&d), plan.sched.size() * sizeof(int32_t)));

@@ -232,11 +232,8 @@ __global__ void det_reduce_kernel(float* __restrict__ dM, const float* __restric
   }
 }
 
-// K5 for heavily shared memories (C2 at 100x: ~50 covering tiles x splits per slot): one warp
-// per 4-slot group.  Lane l sums the (tile, split) terms l, l + 32, ... in order, then a fixed
-// xor butterfly combines the lanes: a fixed order (bitwise reproducible), with 32x the
-// parallelism of one thread walking 50+ terms per group.  NM = 2 reduces two modules' workspaces
-// in one launch with the result of two NM = 1 launches in module order: dM = (dM + sum_0) + sum_1.
+// K5 for heavily shared memories (C2 at 100x: ~50 covering tiles x splits per slot): the slab
+// kernel below.  NM = 2 reduces two modules' workspaces in one launch: dM = (dM + sum_0) + sum_1.
 struct DetMod {
   const float* ws;
   const int32_t* sorted;
@@ -256,101 +253,110 @@ __device__ __forceinline__ int2 det_cover(const DetMod& m, int64_t s, int64_t ti
   return make_int2(lo, x);
 }
 
-// lane l's terms l, l + 32, ..., l + 32 (U - 1) of a module's covering list starting at k0:
-// their workspace offsets (issued together so the loads overlap); -1 past the end
-template <int U>
-__device__ __forceinline__ void det_bases(const DetMod& m, int2 r, int k0, int64_t s, int64_t tile_elems,
-                                          int64_t* base) {
-  const int nterms = (r.y - r.x) * m.nsplit;
-  const int64_t split_stride = int64_t(m.ntiles) * tile_elems;
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int k = k0 + 32 * u;
-    base[u] = -1;
-    if (k < nterms) {
-      const int i = r.x + k / m.nsplit, sp = k - (k / m.nsplit) * m.nsplit;
-      base[u] = sp * split_stride + int64_t(__ldg(m.sorted + i)) * tile_elems + (s - __ldg(m.sorted_off + i));
-    }
-  }
-}
-
-__device__ __forceinline__ float4 warp_sum4(float4 a) {   // fixed xor butterfly (same order on every run)
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    a.x += __shfl_xor_sync(0xffffffffu, a.x, off);
-    a.y += __shfl_xor_sync(0xffffffffu, a.y, off);
-    a.z += __shfl_xor_sync(0xffffffffu, a.z, off);
-    a.w += __shfl_xor_sync(0xffffffffu, a.w, off);
-  }
-  return a;
-}
-
 template <int NM>
 struct DetMods {
   DetMod m[NM];
 };
 
-template <int NM>
-__global__ void det_reduce_warp_kernel(float* __restrict__ dM, const __grid_constant__ DetMods<NM> mods,
-                                       int64_t tile_elems, int64_t mem_size, const int64_t* __restrict__ iv_start,
-                                       const int64_t* __restrict__ iv_prefix, int n_iv, int64_t n_touched) {
-  const int lane = threadIdx.x & 31;
+// K5, slab form (heavily shared memories): a CTA takes 32 consecutive slot groups (128 slots,
+// lane l = group l) and its NW warps split every module's covering-tile range (the union over the
+// 32 groups) into NW contiguous shares.  For each tile of its share a warp reads the partials of
+// all 32 groups at once — consecutive 16-B pieces of the same tile, one coalesced 512-B request —
+// and each lane adds the terms that cover its group (tiles ascending, splits inner).  The NW
+// per-warp sums are combined in warp order through shared memory, then dM += module 0's sum,
+// then module 1's: a fixed order, bitwise reproducible.  (The warp-per-group form issues
+// scattered 16-B reads, each lane a different tile: 24.6 us at C2 for both modules.)
+template <int NM, int NW>
+__global__ void __launch_bounds__(NW * 32) det_reduce_slab_kernel(
+    float* __restrict__ dM, const __grid_constant__ DetMods<NM> mods, int64_t tile_elems, int64_t mem_size,
+    const int64_t* __restrict__ iv_start, const int64_t* __restrict__ iv_prefix, int n_iv, int64_t n_touched) {
+  __shared__ float4 part[NM][NW][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t n = n_iv > 0 ? n_touched : mem_size;
   const int64_t ngroups = (n + 3) / 4;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; g < ngroups; g += nwarps) {
+  for (int64_t gb = int64_t(blockIdx.x) * 32; gb < ngroups; gb += int64_t(gridDim.x) * 32) {
+    const int64_t g = gb + lane;
     int64_t s = g * 4;
-    if (n_iv > 0) {
-      IvWalk w{iv_start, iv_prefix, n_iv};
-      w.seek(s);
-      s = w.slot(s);
+    bool valid = g < ngroups;
+    if (valid && n_iv > 0) {
+      IvWalk iw{iv_start, iv_prefix, n_iv};
+      iw.seek(s);
+      s = iw.slot(s);
     }
-    if (s >= mem_size) continue;
-    // every module's covering range, then, U terms at a time, their offsets, the workspace
-    // loads and the in-order per-lane sums: lane l adds terms l, l + 32, ... of each module
-    // (U = 8 over both modules at once was slower: 35 vs 26 us at C2, 66 registers)
-    constexpr int U = 4;
-    int2 r[NM];
-#pragma unroll
-    for (int j = 0; j < NM; ++j) r[j] = det_cover(mods.m[j], s, tile_elems);
-    float4 acc[NM];
-#pragma unroll
-    for (int j = 0; j < NM; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    valid = valid && s < mem_size;
 #pragma unroll
     for (int j = 0; j < NM; ++j) {
-      const int nt = (r[j].y - r[j].x) * mods.m[j].nsplit;
-      for (int k0 = lane; k0 - lane < nt; k0 += 32 * U) {
-        int64_t base[U];
-        det_bases<U>(mods.m[j], r[j], k0, s, tile_elems, base);
-        float4 v[U];
+      const DetMod& m = mods.m[j];
+      const int2 r = valid ? det_cover(m, s, tile_elems) : make_int2(0x7fffffff, 0);
+      int lo = valid && r.x < r.y ? r.x : 0x7fffffff, hi = valid && r.x < r.y ? r.y : 0;
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          v[u] = base[u] >= 0 ? *reinterpret_cast<const float4*>(mods.m[j].ws + base[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (base[u] >= 0) {
-            acc[j].x += v[u].x; acc[j].y += v[u].y; acc[j].z += v[u].z; acc[j].w += v[u].w;
-          }
+      for (int off = 16; off > 0; off >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, off));
       }
-    }
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (lo < hi) {   // warp-uniform
+        const int per = (hi - lo + NW - 1) / NW;
+        const int a = lo + w * per, b = min(hi, a + per);
+        const int64_t split_stride = int64_t(m.ntiles) * tile_elems;
+        constexpr int U = 4;
+        for (int i0 = a; i0 < b; i0 += U) {
+          int t[U];
+          int64_t o[U];
 #pragma unroll
-    for (int j = 0; j < NM; ++j) acc[j] = warp_sum4(acc[j]);
-    if (lane == 0) {
+          for (int u = 0; u < U; ++u) {
+            const int i = min(i0 + u, b - 1);
+            t[u] = __ldg(m.sorted + i);
+            o[u] = __ldg(m.sorted_off + i);
+          }
+          for (int sp = 0; sp < m.nsplit; ++sp) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int i = i0 + u;
+              const bool cov = i < b && i >= r.x && i < r.y && valid;
+              v[u] = cov ? *reinterpret_cast<const float4*>(m.ws + sp * split_stride + int64_t(t[u]) * tile_elems + (s - o[u]))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            // order: batches of U tiles ascending, then split, then tile -- fixed by the static
+            // covers (the shares and batches do not depend on the data or on timing)
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
+            }
+          }
+        }
+      }
+      part[j][w][lane] = acc;
+    }
+    __syncthreads();
+    if (w == 0 && valid) {
+      float4 tot[NM];
+#pragma unroll
+      for (int j = 0; j < NM; ++j) {
+        tot[j] = part[j][0][lane];
+#pragma unroll
+        for (int k = 1; k < NW; ++k) {
+          const float4 p = part[j][k][lane];
+          tot[j].x += p.x; tot[j].y += p.y; tot[j].z += p.z; tot[j].w += p.w;
+        }
+      }
       if (s + 4 <= mem_size) {
         float4* d = reinterpret_cast<float4*>(dM + s);
         float4 o = *d;
 #pragma unroll
         for (int j = 0; j < NM; ++j) {
-          o.x += acc[j].x; o.y += acc[j].y; o.z += acc[j].z; o.w += acc[j].w;
+          o.x += tot[j].x; o.y += tot[j].y; o.z += tot[j].z; o.w += tot[j].w;
         }
         *d = o;
       } else {   // |M| % 4 != 0: the last group is partial
         for (int j = 0; j < NM; ++j) {
-          const float a4[4] = {acc[j].x, acc[j].y, acc[j].z, acc[j].w};
+          const float a4[4] = {tot[j].x, tot[j].y, tot[j].z, tot[j].w};
           for (int k = 0; s + k < mem_size; ++k) dM[s + k] += a4[k];
         }
       }
     }
+    __syncthreads();
   }
 }
 
@@ -502,13 +508,13 @@ cudaError_t launch_det_reduce2(Ctx* c, const Module& m0, const float* ws0, int n
   const int64_t nt = touched ? c->touched_n : 0;
   const int64_t te = int64_t(c->tile.z1) * c->tile.z2;
   if (warp0 && (warp1 || !m1)) {
-    const int64_t blocks = std::min<int64_t>((ngroups * 32 + threads - 1) / threads, 148 * 16);
+    const int64_t blocks = std::min<int64_t>((ngroups + 31) / 32, 148 * 8);
     if (m1) {
       const DetMods<2> md{{det_mod(m0, ws0, ns0), det_mod(*m1, ws1, ns1)}};
-      det_reduce_warp_kernel<2><<<unsigned(blocks), threads, 0, s>>>(c->dM, md, te, c->mem_size, ivs, ivp, niv, nt);
+      det_reduce_slab_kernel<2, 8><<<unsigned(blocks), 256, 0, s>>>(c->dM, md, te, c->mem_size, ivs, ivp, niv, nt);
     } else {
       const DetMods<1> md{{det_mod(m0, ws0, ns0)}};
-      det_reduce_warp_kernel<1><<<unsigned(blocks), threads, 0, s>>>(c->dM, md, te, c->mem_size, ivs, ivp, niv, nt);
+      det_reduce_slab_kernel<1, 8><<<unsigned(blocks), 256, 0, s>>>(c->dM, md, te, c->mem_size, ivs, ivp, niv, nt);
     }
     return cudaGetLastError();
   }
