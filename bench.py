@@ -998,7 +998,7 @@ def run_gpu_c3(args):
         for ev in prof.key_averages():
             t = getattr(ev, "device_time_total", getattr(ev, "cuda_time_total", 0.0)) / 1e3
             n = ev.key
-            if "roast_mm_sm100" in n:
+            if "roast_mm_sm100" in n or "roast_mix_sm100" in n or "det_reduce" in n:
                 cats["linears"] += t
                 gemm_ms += t
             elif "nccl" in n.lower() or "pack_kernel" in n:
@@ -1007,8 +1007,12 @@ def run_gpu_c3(args):
                 cats["update"] += t
             elif "memset" not in n.lower() and "memcpy" not in n.lower():
                 cats["n_ops"] += t
+        top = sorted(((getattr(ev, "device_time_total", getattr(ev, "cuda_time_total", 0.0)) / 1e3, ev.key)
+                      for ev in prof.key_averages()), reverse=True)[:10]
         breakdown = dict(ms={k: round(v, 4) for k, v in cats.items()},
-                         note="one eager step under torch.profiler: kernel time by category (launch gaps excluded)")
+                         top_kernels_ms=[[round(t, 4), k[:80]] for t, k in top],
+                         note="one eager step under torch.profiler: kernel time by category (launch gaps "
+                              "excluded); linears = the tcgen05 GEMMs incl. the fused backward")
         barrier()
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph):
