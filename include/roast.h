@@ -261,6 +261,24 @@ roast_status_t roast_colsum(const void* d_dY, int64_t tokens, int32_t n, int64_t
 roast_status_t roast_colsum_ex(const void* d_dY, int64_t tokens, int32_t n, int64_t ld, roast_dtype_t dt, float* d_db,
                                int32_t accumulate, roast_stream_t stream);
 
+/* LayerNorm of the ROASTed BERT workload (an N-operation, P:263-265,
+ * not part of the ROAST hashing itself): at C3's 65 536 tokens torch's LayerNorm takes 0.85 ms
+ * per call, more than the layer's ROAST GEMMs.  Rows of n features, n % 8 == 0, n <= 2048
+ * (else ROAST_ERR_SHAPE); 16-byte aligned device arrays; dt = activations, pdt = gamma / beta.
+ * roast_layernorm_fwd: s = x + r (r may be NULL: s = x; with r, s is rounded to dt and written to
+ *   s_out [rows x n], the input the backward needs), y = (s - mean) * rstd * gamma + beta with
+ *   mean / rstd (fp32 [rows], outputs) over the row, rstd = 1 / sqrt(var + eps).
+ * roast_layernorm_bwd: from dy and the LN input s (x, or s_out): ds = d(loss)/ds [rows x n] dt
+ *   (with a residual it is the gradient of x and of r alike), dgamma / dbeta fp32 [n]
+ *   (overwritten) = column sums of dy * xhat / dy in a fixed order (bitwise reproducible).
+ *   Scratch per call (cudaMallocAsync on the stream).  Stream-ordered, capturable. */
+roast_status_t roast_layernorm_fwd(const void* d_x, const void* d_r, const void* d_gamma, const void* d_beta, void* d_y,
+                                   void* d_s_out, float* d_mean, float* d_rstd, int64_t rows, int32_t n, float eps,
+                                   roast_dtype_t dt, roast_dtype_t pdt, roast_stream_t stream);
+roast_status_t roast_layernorm_bwd(const void* d_dy, const void* d_s, const void* d_gamma, const float* d_mean,
+                                   const float* d_rstd, void* d_ds, float* d_dgamma, float* d_dbeta, int64_t rows,
+                                   int32_t n, roast_dtype_t dt, roast_dtype_t pdt, roast_stream_t stream);
+
 /* a2 + a3: dX = lambda * dY W~^T (skipped if d_dX == NULL), and
  * dM[h(x,y) + pi(o1,o2)] += lambda * g(x,y) * (X^T dY)[i, j] for every virtual
  * weight (P:338-346 [§4.3 eq. gradient rule] with g by the chain rule, R12),

@@ -146,6 +146,59 @@ class RoastEmbedding(torch.nn.Module):
         return _EmbeddingFn.apply(idx, _anchor(self.store), self.store, self.mid)
 
 
+def _cdt(t):
+    return R.BF16 if t.dtype == torch.bfloat16 else R.FP32
+
+
+class _LayerNormFn(torch.autograd.Function):
+    """y = LayerNorm(x (+ r)) * weight + bias through roast_layernorm_fwd / _bwd (one pass each
+    way, the residual add fused).  The gradient of x and of r is the same ds."""
+
+    @staticmethod
+    def forward(ctx, x, r, weight, bias, eps):
+        n = x.shape[-1]
+        x = x.contiguous()
+        rows = x.numel() // n
+        y = torch.empty_like(x)
+        s = torch.empty_like(x) if r is not None else x
+        mean = torch.empty(rows, device=x.device, dtype=torch.float32)
+        rstd = torch.empty(rows, device=x.device, dtype=torch.float32)
+        rr = r.contiguous() if r is not None else None
+        strm = torch.cuda.current_stream().cuda_stream
+        R.roast_layernorm_fwd(x.data_ptr(), rr.data_ptr() if rr is not None else None, weight.data_ptr(),
+                              bias.data_ptr(), y.data_ptr(), s.data_ptr() if r is not None else None,
+                              mean.data_ptr(), rstd.data_ptr(), rows, n, float(eps), _cdt(x), _cdt(weight), strm)
+        ctx.save_for_backward(s, weight, mean, rstd)
+        ctx.has_r = r is not None
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        s, weight, mean, rstd = ctx.saved_tensors
+        n = s.shape[-1]
+        rows = s.numel() // n
+        dy = dy.contiguous()
+        ds = torch.empty_like(s)
+        dg = torch.empty(n, device=s.device, dtype=torch.float32)
+        db = torch.empty(n, device=s.device, dtype=torch.float32)
+        R.roast_layernorm_bwd(dy.data_ptr(), s.data_ptr(), weight.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
+                              ds.data_ptr(), dg.data_ptr(), db.data_ptr(), rows, n, _cdt(s), _cdt(weight),
+                              torch.cuda.current_stream().cuda_stream)
+        return ds, (ds if ctx.has_r else None), dg.to(weight.dtype), db.to(weight.dtype), None
+
+
+class LayerNorm(torch.nn.LayerNorm):
+    """torch.nn.LayerNorm (same parameters, same function) computed by libroast's fused kernels;
+    forward(x, residual=None) normalises x + residual in the same pass.  Falls back to torch's
+    kernel off the GPU or without an affine part."""
+
+    def forward(self, x, residual=None):
+        if x.is_cuda and self.elementwise_affine and self.bias is not None and x.shape[-1] % 8 == 0 \
+                and x.shape[-1] <= 2048 and x.dtype in (torch.bfloat16, torch.float32):
+            return _LayerNormFn.apply(x, residual, self.weight, self.bias, self.eps)
+        return super().forward(x if residual is None else x + residual)
+
+
 class EncoderLayer(torch.nn.Module):
     """Post-LN BERT encoder layer whose six linears (and, with bias=True, their biases via L)
     are ROAST modules in one GMS store.  N-operations (attention math, GELU, LayerNorm;
@@ -160,8 +213,8 @@ class EncoderLayer(torch.nn.Module):
         self.o = RoastLinear(store, d_model, d_model, bias)
         self.ff1 = RoastLinear(store, d_model, d_ff, bias)
         self.ff2 = RoastLinear(store, d_ff, d_model, bias)
-        self.ln1 = torch.nn.LayerNorm(d_model)
-        self.ln2 = torch.nn.LayerNorm(d_model)
+        self.ln1 = LayerNorm(d_model)
+        self.ln2 = LayerNorm(d_model)
         # Q, K, V read the same input: one 768 x 2304 GEMM over the three modules' own tiles
         # (registration order and hashes unchanged; the group id lives outside the module ids)
         self.qkv_gid = store.linear_concat([self.q.mid, self.k.mid, self.v.mid]) if fuse_qkv else None
@@ -186,8 +239,8 @@ class EncoderLayer(torch.nn.Module):
         q, k, v = self._qkv(x)
         a = torch.nn.functional.scaled_dot_product_attention(split(q), split(k), split(v))
         a = a.transpose(1, 2).reshape(B, S, d)
-        x = self.ln1(x + self.o(a))
-        return self.ln2(x + self.ff2(torch.nn.functional.gelu(self.ff1(x))))
+        x = self.ln1(self.o(a), x)            # LayerNorm(x + attention), the residual add fused
+        return self.ln2(self.ff2(torch.nn.functional.gelu(self.ff1(x))), x)
 
 
 class BertEmbeddings(torch.nn.Module):
@@ -199,7 +252,7 @@ class BertEmbeddings(torch.nn.Module):
         self.word = RoastEmbedding(store, vocab, d_model, chunk)
         self.pos = RoastEmbedding(store, max_pos, d_model, chunk)
         self.tok_type = RoastEmbedding(store, type_vocab, d_model, chunk)
-        self.ln = torch.nn.LayerNorm(d_model)
+        self.ln = LayerNorm(d_model)
 
     def forward(self, ids, types=None):                 # ids: [B, S] int64
         B, S = ids.shape

@@ -33,7 +33,8 @@ EXPORTS = [
     "roast_p2p_window", "roast_p2p_ipc_handle", "roast_p2p_open", "roast_p2p_attach", "roast_p2p_post",
     "roast_p2p_finish", "roast_grad_exchange_p2p", "roast_p2p_reduce", "roast_p2p_gather",
     "roast_grad_exchange_p2p2", "roast_nvls_supported", "roast_nvls_create", "roast_nvls_import",
-    "roast_nvls_add_device", "roast_nvls_bind", "roast_nvls_bound", "roast_nvls_reset", "roast_get_error",
+    "roast_nvls_add_device", "roast_nvls_bind", "roast_nvls_bound", "roast_nvls_reset", "roast_layernorm_fwd",
+    "roast_layernorm_bwd", "roast_get_error",
     "roast_status_str", "roast_last_error", "roast_debug_tile_map", "roast_debug_chunk_map",
     "roast_debug_materialize", "roast_debug_hash_host", "roast_launch_count", "roast_lms_segments",
     "roast_debug_opt_state",
@@ -134,6 +135,8 @@ def _load():
         "roast_nvls_bind": (st, [H, I32]),
         "roast_nvls_bound": (st, [H, ctypes.POINTER(I32)]),
         "roast_nvls_reset": (st, [H]),
+        "roast_layernorm_fwd": (st, [P, P, P, P, P, P, P, P, I64, I32, ctypes.c_float, ctypes.c_int, ctypes.c_int, S]),
+        "roast_layernorm_bwd": (st, [P, P, P, P, P, P, P, P, I64, I32, ctypes.c_int, ctypes.c_int, S]),
         "roast_get_error": (st, [H]),
         "roast_status_str": (ctypes.c_char_p, [st]),
         "roast_last_error": (ctypes.c_char_p, []),
@@ -473,6 +476,16 @@ def roast_nvls_add_device(h):
 
 def roast_nvls_bind(h, rank):
     _check(_lib.roast_nvls_bind(h, rank), "roast_nvls_bind")
+
+
+def roast_layernorm_fwd(x, r, gamma, beta, y, s_out, mean, rstd, rows, n, eps, dt, pdt, stream=0):
+    _check(_lib.roast_layernorm_fwd(x, r, gamma, beta, y, s_out, mean, rstd, rows, n, eps, dt, pdt, stream),
+           "roast_layernorm_fwd")
+
+
+def roast_layernorm_bwd(dy, s, gamma, mean, rstd, ds, dgamma, dbeta, rows, n, dt, pdt, stream=0):
+    _check(_lib.roast_layernorm_bwd(dy, s, gamma, mean, rstd, ds, dgamma, dbeta, rows, n, dt, pdt, stream),
+           "roast_layernorm_bwd")
 
 
 def roast_nvls_reset(h):

@@ -34,8 +34,8 @@ class DenseLayer(torch.nn.Module):
         super().__init__()
         L = lambda i, o: torch.nn.Linear(i, o, bias=bias, dtype=torch.bfloat16)  # noqa: E731
         self.qkv_dense, self.o, self.ff1, self.ff2 = L(D, 3 * D), L(D, D), L(D, FF), L(FF, D)
-        self.ln1 = torch.nn.LayerNorm(D, dtype=torch.bfloat16)
-        self.ln2 = torch.nn.LayerNorm(D, dtype=torch.bfloat16)
+        self.ln1 = RN.LayerNorm(D, dtype=torch.bfloat16)   # the same LayerNorm kernels as the ROAST layer
+        self.ln2 = RN.LayerNorm(D, dtype=torch.bfloat16)
 
     forward = RN.EncoderLayer.forward
     _qkv = RN.EncoderLayer._qkv
@@ -51,7 +51,7 @@ class DenseBert(torch.nn.Module):
         self.word = torch.nn.Embedding(vocab, D)
         self.pos = torch.nn.Embedding(max_pos, D)
         self.tok_type = torch.nn.Embedding(2, D)
-        self.ln = torch.nn.LayerNorm(D)
+        self.ln = RN.LayerNorm(D)
         self.layers = torch.nn.ModuleList([DenseLayer(bias=True) for _ in range(LAYERS)])
 
     def forward(self, ids, types):
