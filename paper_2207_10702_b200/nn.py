@@ -146,6 +146,12 @@ class RoastEmbedding(torch.nn.Module):
         return _EmbeddingFn.apply(idx, _anchor(self.store), self.store, self.mid)
 
 
+try:   # attention is an N-op of the BERT workload: library kernels, as cuBLAS would be
+    from flash_attn import flash_attn_func as _flash_attn
+except Exception:  # noqa: BLE001
+    _flash_attn = None
+
+
 def _cdt(t):
     return R.BF16 if t.dtype == torch.bfloat16 else R.FP32
 
@@ -234,11 +240,18 @@ class EncoderLayer(torch.nn.Module):
         B, S, d = x.shape
         h = self.heads
 
-        def split(t):
-            return t.reshape(B, S, h, d // h).transpose(1, 2)
         q, k, v = self._qkv(x)
-        a = torch.nn.functional.scaled_dot_product_attention(split(q), split(k), split(v))
-        a = a.transpose(1, 2).reshape(B, S, d)
+        if _flash_attn is not None and x.is_cuda and x.dtype == torch.bfloat16:
+            # flash-attn (library kernel) reads [B, S, heads, d_head] strided views of the QKV
+            # output directly: no transposes either way (0.77 vs 0.88 ms per C3 layer for SDPA)
+            def heads(t):
+                return t.view(B, S, h, d // h) if t.stride(-1) == 1 else t.reshape(B, S, h, d // h)
+            a = _flash_attn(heads(q), heads(k), heads(v)).reshape(B, S, d)
+        else:
+            def split(t):
+                return t.reshape(B, S, h, d // h).transpose(1, 2)
+            a = torch.nn.functional.scaled_dot_product_attention(split(q), split(k), split(v))
+            a = a.transpose(1, 2).reshape(B, S, d)
         x = self.ln1(self.o(a), x)            # LayerNorm(x + attention), the residual add fused
         return self.ln2(self.ff2(torch.nn.functional.gelu(self.ff1(x))), x)
 
