@@ -41,13 +41,16 @@ def build(verbose: bool = False, force: bool = False) -> str:
         glob.glob(os.path.join(ROOT, "include", "*.h"))
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for src in srcs:
-        obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        objs.append(obj)
-        if force or _stale(obj, [src] + hdrs):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
-            r = subprocess.run(cmd, capture_output=True, text=True)
+    objs = [os.path.join(objdir, os.path.basename(src) + ".o") for src in srcs]
+    todo = [(src, obj) for src, obj in zip(srcs, objs) if force or _stale(obj, [src] + hdrs)]
+
+    def compile_one(job):
+        src, obj = job
+        return src, subprocess.run([NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj], capture_output=True, text=True)
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 1))) as ex:
+        for src, r in ex.map(compile_one, todo):   # one nvcc per source file, in parallel
             if r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
                 raise RuntimeError("nvcc failed on " + os.path.basename(src))
