@@ -22,9 +22,11 @@ one training step = forward + backward + (all-reduce + SGD + shadow refresh + dM
 one roast_grad_exchange_step); reports t_step split into linears / N-ops / exchange /
 update and the all-reduce's algbw / busbw.
 
-At N = 1 the default run adds `extra`: C2 at 10x and 1000x, the deterministic C2 step, C4
-embeddings (GB/s, HBM fraction), per-GEMM ROAST / cuBLAS ratios, the oracle at 1 thread
-and all cores with the CPU model, and the paper's own numbers (A100 TF32, context only).
+At N = 1 the default run adds `extra` (about a minute in all): C2 at 10x and 1000x, the
+deterministic C2 step, C4 embeddings (GB/s, HBM fraction), C5's |M| endpoints (8 MB and 2 GB)
+against cuBLAS, C3 at 8192 tokens (encoder and whole BERT, ROAST vs dense), per-GEMM ROAST /
+cuBLAS ratios, the oracle at 1 thread and all cores with the CPU model, and the paper's own
+numbers (A100 TF32, context only).
 
 `--impl reference` times the oracle (oracle/, CPU fp64) as the reference arm.
 """
@@ -891,8 +893,98 @@ def c2_extras(torch, dev, args, S, flush, stream, W1, W2):
         out["c4_embeddings"] = c4_extra(torch, dev, flush, stream)
     except Exception as e:  # noqa: BLE001
         out["c4_embeddings"] = dict(error=repr(e))
+    try:
+        out["c5_sweep_endpoints"] = c5_extra(torch)
+    except Exception as e:  # noqa: BLE001
+        out["c5_sweep_endpoints"] = dict(error=repr(e))
+    out["c3_bert_step"] = c3_extra()
     out["paper_context"] = PAPER_CONTEXT
     out["seconds"] = time.perf_counter() - t0
+    return out
+
+
+def c5_extra(torch, mems=(2 << 20, 512 << 20), T=16384, D=4096):
+    """C5 (BASELINE.json configs[4]) at its two endpoints, |M| = 8 MB (L2-resident) and 2 GB
+    (HBM-resident) fp32: one 4096 x 4096 ROAST linear at batch 16384, fwd + bwd (dX and dM on
+    two streams, as tools/c5_sweep.py), graph-replayed (the 134 MB activations exceed L2: no
+    flush), against dense cuBLAS on the materialised W; plus the touched-only Adam step."""
+    bf = torch.bfloat16
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    X = torch.randn(T, D, device="cuda", generator=gen).to(bf)
+    dY = torch.randn(T, D, device="cuda", generator=gen).to(bf)
+    Y = torch.empty(T, D, device="cuda", dtype=bf)
+    dX = torch.empty(T, D, device="cuda", dtype=bf)
+    flop = 6.0 * T * D * D
+    side = torch.cuda.Stream()
+    stream = torch.cuda.current_stream()
+    res = {}
+    dense_ms = None
+    for mem in mems:
+        M = torch.rand(mem, device="cuda", generator=gen) * 2 - 1
+        ctx = R_mod().Roast(M, 64, 64)
+        ctx.set_autotune(2)
+        lid = ctx.linear(D, D)
+        ctx.fwd(lid, X, Y)
+        ctx.bwd_dx(lid, dY, dX)
+        ctx.bwd_dm(lid, X, dY)
+        torch.cuda.synchronize()
+
+        def step():
+            ctx.fwd(lid, X, Y)
+            side.wait_stream(torch.cuda.current_stream())
+            ctx.bwd_dx(lid, dY, dX)
+            with torch.cuda.stream(side):
+                ctx.bwd_dm(lid, X, dY, stream=side)
+            torch.cuda.current_stream().wait_stream(side)
+        nothing = torch.empty(0, dtype=torch.uint8, device="cuda")
+        ms = mean_replay_ms(torch, graph_of(torch, step), 10, nothing, stream)
+        if dense_ms is None:
+            W = ctx.materialize(lid, bf)
+
+            def dense():
+                torch.matmul(X, W, out=Y)
+                torch.matmul(dY, W.t(), out=dX)
+                torch.matmul(X.t(), dY)
+            dense_ms = mean_replay_ms(torch, graph_of(torch, dense), 10, nothing, stream)
+            del W
+        ctx.optimizer_step(2, 1e-3, step=1, touched_only=True)
+        adam_ms = mean_replay_ms(torch, graph_of(torch, lambda: ctx.optimizer_step(2, 1e-3, step=1, touched_only=True)),
+                                 5, nothing, stream)
+        res["%d_MB" % (mem * 4 >> 20)] = dict(mem_elems=mem, fwd_bwd_ms=ms, tflops=flop / (ms * 1e-3) / 1e12,
+                                            dense_tflops=flop / (dense_ms * 1e-3) / 1e12,
+                                            roast_over_dense=dense_ms / ms, adam_touched_only_ms=adam_ms)
+        ctx.close()
+        del M, ctx
+        torch.cuda.empty_cache()
+    res["config"] = "C5: 4096 x 4096 ROAST-MM, batch 16384, |M| endpoints of the 8 MB - 2 GB sweep (1 GPU)"
+    return res
+
+
+def R_mod():
+    from paper_2207_10702_b200 import roast as R
+    return R
+
+
+def c3_extra(timeout=180):
+    """C3 (BASELINE.json configs[2]) at one GPU, 8192 tokens: the BERT-base encoder step (72
+    ROAST linears in one GMS M) and the whole BERT (embeddings and biases via L), each against the
+    same model with dense bf16 weights (tools/bert_step.py, separate processes, CUDA graphs)."""
+    out = {}
+    for key, extra in (("encoder", []), ("encoder_dense", ["--dense"]), ("full_bert", ["--full"]),
+                       ("full_bert_dense", ["--full", "--dense"])):
+        try:
+            r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "bert_step.py"), "--steps", "10"] + extra,
+                               capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+            line = json.loads(r.stdout.strip().splitlines()[-1])
+            out[key] = dict(ms_per_step=line["ms_per_step"], tokens_per_s=line["tokens_per_s"],
+                            linear_eff_tflops=line["linear_eff_tflops"])
+        except Exception as e:  # noqa: BLE001
+            out[key] = dict(error=repr(e)[:200])
+    try:
+        out["roast_over_dense_encoder"] = out["encoder_dense"]["ms_per_step"] / out["encoder"]["ms_per_step"]
+        out["roast_over_dense_full_bert"] = out["full_bert_dense"]["ms_per_step"] / out["full_bert"]["ms_per_step"]
+    except Exception:  # noqa: BLE001
+        pass
     return out
 
 
