@@ -2037,7 +2037,12 @@ double det_split_cost() {
 
 MixPlan plan_mix(int mt0, int nt0, int kb0, int mt1, int nt1, int kbT, int mt2, int nt2, int kb2, int mt3, int nt3,
                  int npairs, double split_cost) {
-  const double EPI_DX = 3.0, EPI_DW = 1.0, LAT = 1.0;
+  // cost model in DX k-block units: a DW k-block has half the MMA work but needs 64 B/clk of
+  // operands (DX: 47), so it costs DWK = 0.6, not 0.5 (C2 fused backward 120.8 -> 118.8 us; 0.6 -
+  // 0.7 give the same schedule); a unit's drain EPI_*.  ROAST_MIX_{DWK,EPI_DX,EPI_DW} override.
+  auto envd = [](const char* k, double d) { const char* e = getenv(k); return e ? atof(e) : d; };
+  const double EPI_DX = envd("ROAST_MIX_EPI_DX", 3.0), EPI_DW = envd("ROAST_MIX_EPI_DW", 1.0), LAT = 1.0;
+  const double DWK = envd("ROAST_MIX_DWK", 0.6);
   MixPlan best;
   const int units0 = mt0 * nt0;
   for (int s : {1, 2, 3, 4}) {
@@ -2079,7 +2084,7 @@ MixPlan plan_mix(int mt0, int nt0, int kb0, int mt1, int nt1, int kbT, int mt2, 
           p3_range(u, k0, k1, nb);
           for (int k = k0; k < k1; k += 8) {
             const int ke = std::min(k1, (k & ~7) + 8);
-            t = std::max(t, fin0[std::min(k >> 3, mt0 - 1) * nt0 + nb] + LAT) + 0.5 * (ke - k);
+            t = std::max(t, fin0[std::min(k >> 3, mt0 - 1) * nt0 + nb] + LAT) + DWK * (ke - k);
             k = (k & ~7);
           }
           return t + EPI_DW;
@@ -2106,7 +2111,7 @@ MixPlan plan_mix(int mt0, int nt0, int kb0, int mt1, int nt1, int kbT, int mt2, 
             cls = r2 <= r3 ? 2 : 3;
           }
           if (cls == 1) {
-            free_t[q] = now + 0.5 * kps + EPI_DW;
+            free_t[q] = now + DWK * kps + EPI_DW;
             lists[q].push_back((1 << 24) | q1[i1++]);
           } else if (cls == 2) {
             free_t[q] = p2_finish(q2[i2], now);
