@@ -261,6 +261,23 @@ roast_status_t roast_colsum(const void* d_dY, int64_t tokens, int32_t n, int64_t
 roast_status_t roast_colsum_ex(const void* d_dY, int64_t tokens, int32_t n, int64_t ld, roast_dtype_t dt, float* d_db,
                                int32_t accumulate, roast_stream_t stream);
 
+/* Activation fused into the linear's epilogue (the ROASTed BERT MLP, SURVEY.md §8(f) NEXT #3;
+ * the activation itself is an N-operation).  bf16 on the tcgen05 path only (the
+ * WM = 2 register-held epilogue); ROAST_ERR_UNSUPPORTED elsewhere (the caller applies the
+ * activation itself).  act: ROAST_ACT_GELU_TANH, gelu(u) = u/2 (1 + tanh(sqrt(2/pi)(u + 0.044715
+ * u^3))) (torch's gelu(approximate="tanh"), the original BERT's form), tanh evaluated with the
+ * hardware approximation (rel. error ~2^-11, below bf16's 2^-8).
+ * roast_linear_fwd_act: Y = lambda X W~ (+ bias) as roast_linear_fwd_bias, and A = act(Y) from
+ *   the stored (bf16-rounded) Y, both [tokens x out_features] bf16; A 16-byte aligned.
+ * roast_linear_bwd_dx_act: dX = bf16(lambda dY W~^T) * act'(U) elementwise, U [tokens x
+ *   in_features] bf16 the pre-activation whose act(U) was this layer's input (so dX is the
+ *   gradient with respect to U).  No dM: pair it with roast_linear_bwd_dm(X = act(U)). */
+typedef enum { ROAST_ACT_NONE = 0, ROAST_ACT_GELU_TANH = 1 } roast_act_t;
+roast_status_t roast_linear_fwd_act(roast_t h, int32_t id, const void* d_X, void* d_Y, void* d_A, int64_t tokens,
+                                    roast_dtype_t dt, const float* d_bias, int32_t act, roast_stream_t stream);
+roast_status_t roast_linear_bwd_dx_act(roast_t h, int32_t id, const void* d_dY, const void* d_U, void* d_dX,
+                                       int64_t tokens, roast_dtype_t dt, int32_t act, roast_stream_t stream);
+
 /* LayerNorm of the ROASTed BERT workload (an N-operation, P:263-265,
  * not part of the ROAST hashing itself): at C3's 65 536 tokens torch's LayerNorm takes 0.85 ms
  * per call, more than the layer's ROAST GEMMs.  Rows of n features, n % 8 == 0, n <= 2048

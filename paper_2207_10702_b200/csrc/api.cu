@@ -479,6 +479,25 @@ roast_status_t roast_linear_fwd_bias(roast_t h, int32_t id, const void* X, void*
   return ROAST_OK;
 }
 
+roast_status_t roast_linear_fwd_act(roast_t h, int32_t id, const void* X, void* Y, void* A, int64_t T,
+                                    roast_dtype_t dt, const float* bias, int32_t act, roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module* m;
+  roast_status_t st = get_module(c, id, kLinear, &m);
+  if (st) return st;
+  if (T < 0) return fail(ROAST_ERR_SHAPE, "tokens < 0");
+  if (act != ROAST_ACT_GELU_TANH) return fail(ROAST_ERR_CONFIG, "act: ROAST_ACT_GELU_TANH");
+  if (T > 0 && (!X || !Y || !A)) return fail(ROAST_ERR_CONFIG, "null X / Y / A");
+  if ((reinterpret_cast<uintptr_t>(bias) | reinterpret_cast<uintptr_t>(A)) & 15)
+    return fail(ROAST_ERR_CONFIG, "bias and A must be 16-byte aligned");
+  if (T == 0) return ROAST_OK;
+  if (dt != ROAST_BF16 || !use_sm100(c, *m))
+    return fail(ROAST_ERR_UNSUPPORTED, "fused activation: bf16 on the tcgen05 path only");
+  st = sm100_fwd_act(c, *m, X, Y, A, T, bias, act, reinterpret_cast<cudaStream_t>(stream));
+  if (st == ROAST_ERR_UNSUPPORTED) return fail(st, "fused activation: not on this geometry");
+  return st;
+}
+
 roast_status_t roast_linear_fwd_chain(roast_t h, int32_t id_a, int32_t id_b, const void* X, void* Y_a, void* Y_b,
                                       int64_t T, roast_dtype_t dt, const float* bias_a, const float* bias_b,
                                       roast_stream_t stream) {
@@ -654,6 +673,21 @@ roast_status_t roast_linear_bwd_dx(roast_t h, int32_t id, const void* dY, void* 
   ROAST_CUDA_CHECK(launch_simt_fwd(c, *m, dY, dX, T, dt, true, s, nullptr));
   c->launches++;
   return ROAST_OK;
+}
+
+roast_status_t roast_linear_bwd_dx_act(roast_t h, int32_t id, const void* dY, const void* U, void* dX, int64_t T,
+                                       roast_dtype_t dt, int32_t act, roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module* m;
+  roast_status_t st = linear_args(c, id, T, dt, dY, dX, &m);
+  if (st || T == 0) return st;
+  if (act != ROAST_ACT_GELU_TANH) return fail(ROAST_ERR_CONFIG, "act: ROAST_ACT_GELU_TANH");
+  if (!U || (reinterpret_cast<uintptr_t>(U) & 15)) return fail(ROAST_ERR_CONFIG, "U null or not 16-byte aligned");
+  if (dt != ROAST_BF16 || !use_sm100(c, *m))
+    return fail(ROAST_ERR_UNSUPPORTED, "fused activation: bf16 on the tcgen05 path only");
+  st = sm100_dx_act(c, *m, dY, U, dX, T, act, reinterpret_cast<cudaStream_t>(stream));
+  if (st == ROAST_ERR_UNSUPPORTED) return fail(st, "fused activation: not on this geometry");
+  return st;
 }
 
 roast_status_t roast_linear_bwd_dm(roast_t h, int32_t id, const void* X, const void* dY, int64_t T, roast_dtype_t dt,

@@ -117,6 +117,11 @@ struct Params {
   float lam;
   __nv_bfloat16* out;   // FWD: Y [T x N], DX: dX [T x N]
   const float* bias;    // FWD only: fp32 [N] added after lambda (recovered by L), or null
+  // fused activation (RF epilogue only; the BERT MLP's GELU, an N-op): FWD also writes
+  // act_out = act(bf16 Y); DX writes dX = bf16(lambda dY W~^T) * act'(act_in) elementwise
+  int act;
+  const __nv_bfloat16* act_in;
+  __nv_bfloat16* act_out;
   float* dM;            // DW atomic target
   float* ws;            // DW deterministic workspace [splits][ntiles][4096]
   int ntiles;
@@ -308,8 +313,32 @@ __device__ __forceinline__ void decode_unit(const Params& p, int u, int& mb, int
   nb = r - mb * p.n_tiles;
 }
 
+// GELU, tanh form (the original BERT's; torch's gelu(approximate="tanh")), and its derivative
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float t = tanh_approx(0.7978845608f * (x + 0.044715f * x * x * x));
+  return 0.5f * x * (1.f + t);
+}
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+  const float x2 = x * x;
+  const float t = tanh_approx(0.7978845608f * (x + 0.044715f * x2 * x));
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * 0.7978845608f * (1.f + 3.f * 0.044715f * x2);
+}
+// two packed bf16 -> f(a) * g, f(b) * g ... helpers over a packed pair
+__device__ __forceinline__ float2 unpack_bf2(uint32_t v) {
+  return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v));
+}
+__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
 // ---------------------------------------------------------------- the kernel
-template <int MODE, int CG, int WM, bool CHAIN = false, int NU = BN>
+template <int MODE, int CG, int WM, bool CHAIN = false, int NU = BN, bool ACT = false>
 __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
     roast_mm_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ WMaps wmaps,
@@ -644,9 +673,34 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
       aph ^= 1;
       if (p.prof) prof_epi[0] += clock64() - tw4;
       const int row0 = mb * BM * CG * WM + int(rank) * BM * WM + jh * BM + q * 32;
+      // fused activation: this thread's output row (rows past T are neither read nor written)
+      const int64_t arow = int64_t(row0) + lane;
+      const bool arow_ok = arow < p.T;
+      uint4 un[ACT && MODE == DX ? 8 : 1];   // DX: the next chunk's act_in values (prefetched one chunk ahead)
+      if (ACT && MODE == DX && arow_ok && nsteps > 0) {
+        const uint4* src = reinterpret_cast<const uint4*>(p.act_in + arow * p.N + nb * NU);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) un[v] = __ldg(src + v);
+      }
 #pragma unroll
       for (int c = 0; c < NU / 64; ++c) {
         if (c < nsteps) {
+          if (ACT && MODE == DX) {   // dX = bf16(dh) * act'(u), from the rounded dh as an unfused op sees it
+            uint4 uc[8];
+#pragma unroll
+            for (int v = 0; v < 8; ++v) uc[v] = un[v];
+            if (c + 1 < nsteps && arow_ok) {
+              const uint4* src = reinterpret_cast<const uint4*>(p.act_in + arow * p.N + nb * NU + (c + 1) * 64);
+#pragma unroll
+              for (int v = 0; v < 8; ++v) un[v] = __ldg(src + v);
+            }
+            const uint32_t* uw = reinterpret_cast<const uint32_t*>(uc);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float2 d = unpack_bf2(pk[c * 32 + i]), x = unpack_bf2(uw[i]);
+              pk[c * 32 + i] = pack_bf2(d.x * gelu_tanh_grad(x.x), d.y * gelu_tanh_grad(x.y));
+            }
+          }
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           __syncwarp();
 #pragma unroll
@@ -655,6 +709,20 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pk[c * 32 + 4 * cc]),
                          "r"(pk[c * 32 + 4 * cc + 1]), "r"(pk[c * 32 + 4 * cc + 2]), "r"(pk[c * 32 + 4 * cc + 3])
                          : "memory");
+          }
+          if (ACT && MODE == FWD && arow_ok) {   // act_out = act(bf16 Y): each thread its row's 128 B
+            uint4* dst = reinterpret_cast<uint4*>(p.act_out + arow * p.N + nb * NU + c * 64);
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              uint4 o;
+              uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 x = unpack_bf2(pk[c * 32 + 4 * v + e]);
+                ow[e] = pack_bf2(gelu_tanh(x.x), gelu_tanh(x.y));
+              }
+              dst[v] = o;
+            }
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
@@ -1355,6 +1423,15 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
 
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  // a driver-API call: the calling thread needs a current context, which a thread that has made
+  // no runtime call yet lacks (torch's autograd worker running a backward that starts with a
+  // tensor-map build: CUDA_ERROR_INVALID_CONTEXT).  cudaSetDevice makes the primary one current.
+  thread_local bool ctx_ready = false;
+  if (!ctx_ready) {
+    int d = 0;
+    if (cudaGetDevice(&d) == cudaSuccess) cudaSetDevice(d);
+    ctx_ready = true;
+  }
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult q;
@@ -1420,7 +1497,7 @@ int cta_group() {
   return cg;
 }
 
-template <int MODE, int CG, int WM, bool CHAIN = false, int NU = BN>
+template <int MODE, int CG, int WM, bool CHAIN = false, int NU = BN, bool ACT = false>
 roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o, const WMaps& w,
                          const Params& p, const CUtensorMap& a1, const CUtensorMap& o1, const Params& p1,
                          int grid_pairs, cudaStream_t s, const WMapsHalf* hw = nullptr) {
@@ -1428,7 +1505,7 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
-        cudaFuncSetAttribute(roast_mm_sm100<MODE, CG, WM, CHAIN, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(roast_mm_sm100<MODE, CG, WM, CHAIN, NU, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(smem)");
     attr = true;
   }
@@ -1459,7 +1536,7 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
     pp1.prof = prof;
   }
   static const WMapsHalf no_half{};
-  cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mm_sm100<MODE, CG, WM, CHAIN, NU>, a, b, o, w, pp, a1, o1, pp1,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mm_sm100<MODE, CG, WM, CHAIN, NU, ACT>, a, b, o, w, pp, a1, o1, pp1,
                                      hw ? *hw : no_half);
   if (e != cudaSuccess) return cuda_fail(e, "roast_mm_sm100 launch");
   if (pp.prof) {
@@ -1489,6 +1566,10 @@ template <int MODE>
 roast_status_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o, const WMaps& w, Params p,
                       int wm, cudaStream_t s, int nu = BN, const WMapsHalf* hw = nullptr) {
   if constexpr (MODE != DW) {
+    if (p.act) {   // fused activation: the WM = 2 register-held epilogue (checked by the caller)
+      if (nu == 192) return launch_cg<MODE, 2, 2, false, 192, true>(a, b, o, w, p, a, o, p, 0, s, hw);
+      return launch_cg<MODE, 2, 2, false, BN, true>(a, b, o, w, p, a, o, p, 0, s);
+    }
     if (nu == 192) return launch_cg<MODE, 2, 2, false, 192>(a, b, o, w, p, a, o, p, 0, s, hw);
   }
   if (cta_group() == 1) return launch_cg<MODE, 1, 1>(a, b, o, w, p, a, o, p, 0, s);
@@ -1596,7 +1677,9 @@ float time_candidate(F&& f, cudaStream_t s) {
 // nu = output columns per unit (256, or 192 for DX with WM = 2).
 static roast_status_t tok_major_launch(Ctx* c, const Module& m, const void* A, void* out, int64_t T, int N, int K,
                                        const int32_t* coord, int coord_ld, bool dx, int wm, const float* bias,
-                                       cudaStream_t s, int nu = BN) {
+                                       cudaStream_t s, int nu = BN, int act = 0, const void* act_in = nullptr,
+                                       void* act_out = nullptr) {
+  if (act && (wm != 2 || cta_group() != 2)) return ROAST_ERR_UNSUPPORTED;   // the RF epilogue only
   CUtensorMap a;
   roast_status_t st = make_map_2d(&a, A, uint64_t(K), uint64_t(T), uint64_t(K) * 2, BK, BM * wm);
   if (st) return st;
@@ -1613,6 +1696,9 @@ static roast_status_t tok_major_launch(Ctx* c, const Module& m, const void* A, v
   p.bias = dx ? nullptr : bias;
   p.coord = coord;
   p.coord_ld = coord_ld;
+  p.act = act;
+  p.act_in = static_cast<const __nv_bfloat16*>(act_in);
+  p.act_out = static_cast<__nv_bfloat16*>(act_out);
   CUtensorMap o;   // output [T x N] bf16, stored 32 rows x 64 columns per TMA op
   st = make_map_2d(&o, out, uint64_t(N), uint64_t(T), uint64_t(N) * 2, 64, 32);
   if (st) return st;
@@ -1641,8 +1727,28 @@ static void choose_tok_major(int64_t T, int N, bool dx, int& wm, int& nu) {
 }
 
 static roast_status_t run_tok_major(Ctx* c, const Module& m, const void* A, void* out, int64_t T, int N, int K,
-                                    const int32_t* coord, int coord_ld, bool dx, const float* bias, cudaStream_t s) {
+                                    const int32_t* coord, int coord_ld, bool dx, const float* bias, cudaStream_t s,
+                                    int act = 0, const void* act_in = nullptr, void* act_out = nullptr) {
   if (!supported(c, m) || T >= (int64_t(1) << 31)) return ROAST_ERR_UNSUPPORTED;
+  if (act) {   // the fused activation lives in the WM = 2 register-held epilogue: WM = 2, N per unit tuned
+    if (cta_group() != 2) return ROAST_ERR_UNSUPPORTED;
+    roast_status_t st = sm100_prepare(c);
+    if (st) return st;
+    const auto key = tune_key((dx ? kTuneDx : kTuneFwd) + 16, m, T);   // its own cache entry
+    auto it = c->tuned.find(key);
+    int nu = BN;
+    if (it != c->tuned.end()) {
+      nu = it->second.second == 3 ? 192 : BN;
+    } else if (nu192_ok(dx, 2, N) && can_tune(c, s)) {
+      const float t256 = time_candidate([&] {
+        return tok_major_launch(c, m, A, out, T, N, K, coord, coord_ld, dx, 2, bias, s, BN, act, act_in, act_out); }, s);
+      const float t192 = time_candidate([&] {
+        return tok_major_launch(c, m, A, out, T, N, K, coord, coord_ld, dx, 2, bias, s, 192, act, act_in, act_out); }, s);
+      nu = (t192 >= 0.f && t192 < t256) ? 192 : BN;
+      c->tuned[key] = {2, nu / 64};
+    }
+    return tok_major_launch(c, m, A, out, T, N, K, coord, coord_ld, dx, 2, bias, s, nu, act, act_in, act_out);
+  }
   roast_status_t st = sm100_prepare(c);
   if (st) return st;
   const auto key = tune_key(dx ? kTuneDx : kTuneFwd, m, T);
@@ -1681,6 +1787,16 @@ roast_status_t sm100_fwd(Ctx* c, const Module& m, const void* X, void* Y, int64_
 
 roast_status_t sm100_dx(Ctx* c, const Module& m, const void* dY, void* dX, int64_t T, cudaStream_t s) {
   return run_tok_major(c, m, dY, dX, T, int(m.H), int(m.O), m.d_coord_yx, m.nx, true, nullptr, s);
+}
+
+roast_status_t sm100_fwd_act(Ctx* c, const Module& m, const void* X, void* Y, void* A, int64_t T, const float* bias,
+                             int act, cudaStream_t s) {
+  return run_tok_major(c, m, X, Y, T, int(m.O), int(m.H), m.d_coord_xy, m.ny, false, bias, s, act, nullptr, A);
+}
+
+roast_status_t sm100_dx_act(Ctx* c, const Module& m, const void* dY, const void* U, void* dX, int64_t T, int act,
+                            cudaStream_t s) {
+  return run_tok_major(c, m, dY, dX, T, int(m.H), int(m.O), m.d_coord_yx, m.nx, true, nullptr, s, act, U, nullptr);
 }
 
 // ---- chained pair of GEMMs ------------------------------------------------------

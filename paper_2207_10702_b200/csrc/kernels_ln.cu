@@ -190,15 +190,16 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const T* __restrict__ dy, c
 }
 
 // backward, pass 2: dg[c] = sum_w part[w][0][c], db[c] = sum_w part[w][1][c] in a fixed order:
-// thread (ty, tx) of a 32-column block sums warps ty, ty + 8, ... then the 8 partials in ty order
-__global__ void __launch_bounds__(256) ln_param_reduce_kernel(const float* __restrict__ part, int64_t nw, int n,
-                                                             float* __restrict__ dg, float* __restrict__ db) {
-  __shared__ float sh[2][8][33];
+// thread (ty, tx) of a 32-column block (32 x 32 threads) sums warps ty, ty + 32, ... then the 32
+// partials are added in ty order
+__global__ void __launch_bounds__(1024) ln_param_reduce_kernel(const float* __restrict__ part, int64_t nw, int n,
+                                                              float* __restrict__ dg, float* __restrict__ db) {
+  __shared__ float sh[2][32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + tx;
   float a = 0.f, b = 0.f;
   if (c < n)
-    for (int64_t w = ty; w < nw; w += 8) {
+    for (int64_t w = ty; w < nw; w += 32) {
       a += part[(w * 2) * n + c];
       b += part[(w * 2 + 1) * n + c];
     }
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(256) ln_param_reduce_kernel(const float* __res
   __syncthreads();
   if (ty == 0 && c < n) {
     float ta = sh[0][0][tx], tb = sh[1][0][tx];
-    for (int k = 1; k < 8; ++k) {
+    for (int k = 1; k < 32; ++k) {
       ta += sh[0][k][tx];
       tb += sh[1][k][tx];
     }
@@ -314,7 +315,7 @@ roast_status_t roast_layernorm_bwd(const void* dy, const void* s_in, const void*
   else
     e = ln_bwd_launch<float, float>(dy, s_in, gamma, mean, rstd, ds, ws.as<float>(), nw, rows, n, s);
   ROAST_CUDA_CHECK(e);
-  ln_param_reduce_kernel<<<unsigned((n + 31) / 32), 256, 0, s>>>(ws.as<float>(), nw, n, dgamma, dbeta);
+  ln_param_reduce_kernel<<<unsigned((n + 31) / 32), 1024, 0, s>>>(ws.as<float>(), nw, n, dgamma, dbeta);
   ROAST_CUDA_CHECK(cudaGetLastError());
   return ROAST_OK;
 }

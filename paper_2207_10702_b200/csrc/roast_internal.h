@@ -289,6 +289,11 @@ roast_status_t sm100_fwd(Ctx* c, const Module& m, const void* X, void* Y, int64_
 roast_status_t sm100_chain(Ctx* c, const Module& m0, const Module& m1, const void* A0, void* out0, void* out1,
                            int64_t T, bool dx, const float* bias0, const float* bias1, cudaStream_t s);
 roast_status_t sm100_dx(Ctx* c, const Module& m, const void* dY, void* dX, int64_t T, cudaStream_t s);
+// the same with an activation fused into the register-held epilogue (roast_linear_fwd_act / _bwd_dx_act)
+roast_status_t sm100_fwd_act(Ctx* c, const Module& m, const void* X, void* Y, void* A, int64_t T, const float* bias,
+                             int act, cudaStream_t s);
+roast_status_t sm100_dx_act(Ctx* c, const Module& m, const void* dY, const void* U, void* dX, int64_t T, int act,
+                            cudaStream_t s);
 // the whole backward of a chained pair a -> b (Y_a = X_a W_a, Y_b = Y_a W_b) in one persistent
 // launch: dY_a = dY_b W_b^T, dM += b(Y_a, dY_b), dX_a = dY_a W_a^T, dM += a(X_a, dY_a), the four
 // GEMMs co-scheduled (gemm_sm100.cu roast_mix_sm100).  ROAST_ERR_UNSUPPORTED when the shapes /

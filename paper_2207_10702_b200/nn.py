@@ -89,6 +89,77 @@ class _LinearGroupFn(torch.autograd.Function):
         return (dx.reshape(ctx.shape) if dx is not None else None), None, None, None, None
 
 
+def gelu(x):
+    """The BERT MLP's activation: GELU in its tanh form (the original BERT's; torch's
+    gelu(approximate="tanh")), the one roast_linear_fwd_act fuses into the GEMM epilogue."""
+    return torch.nn.functional.gelu(x, approximate="tanh")
+
+
+def _gelu_grad(u):
+    k0, k1 = 0.7978845608028654, 0.044715
+    uf = u.float()
+    t = torch.tanh(k0 * (uf + k1 * uf * uf * uf))
+    return 0.5 * (1 + t) + 0.5 * uf * (1 - t * t) * k0 * (1 + 3 * k1 * uf * uf)
+
+
+class _MLPFn(torch.autograd.Function):
+    """y = ff2(gelu(ff1(x))) with the GELU inside the GEMM epilogues: the forward of ff1 writes
+    u = x W1 (+ b1) and h = gelu(u); the backward's dX GEMM of ff2 writes du = (dy W2^T) * gelu'(u)
+    directly.  Off the fused path (roast_linear_*_act UNSUPPORTED) the same math runs unfused."""
+
+    @staticmethod
+    def forward(ctx, x, anchor, store, m1, b1, m2, b2):
+        H = store.dims[m1][1]
+        x2 = x.reshape(-1, H).contiguous()
+        bv1 = store.bias_vector(b1) if b1 is not None else None
+        bv2 = store.bias_vector(b2) if b2 is not None else None
+        try:
+            u, h = store.fwd_act(m1, x2, bias=bv1)
+            ctx.fused = True
+        except R.RoastError as e:
+            if e.status != R.ERR_UNSUPPORTED:
+                raise
+            u = store.fwd(m1, x2, bias=bv1)
+            h = gelu(u)
+            ctx.fused = False
+        y = store.fwd(m2, h, bias=bv2)
+        ctx.save_for_backward(x2, u, h)
+        ctx.store, ctx.m1, ctx.b1, ctx.m2, ctx.b2, ctx.shape = store, m1, b1, m2, b2, x.shape
+        return y.reshape(*x.shape[:-1], y.shape[-1])
+
+    @staticmethod
+    def backward(ctx, dy):
+        x2, u, h = ctx.saved_tensors
+        store = ctx.store
+        dy2 = dy.reshape(x2.shape[0], -1).contiguous().to(x2.dtype)
+        store.bwd_dm(ctx.m2, h, dy2)
+        if ctx.b2 is not None:
+            store.bias_grad(ctx.b2, dy2)
+        if ctx.fused:
+            du = store.bwd_dx_act(ctx.m2, dy2, u)
+        else:
+            dh = torch.empty_like(h)
+            store.bwd_dx(ctx.m2, dy2, dh)
+            du = (dh.float() * _gelu_grad(u)).to(h.dtype)
+        store.bwd_dm(ctx.m1, x2, du)
+        if ctx.b1 is not None:
+            store.bias_grad(ctx.b1, du)
+        dx = None
+        if ctx.needs_input_grad[0]:
+            dx = torch.empty_like(x2)
+            store.bwd_dx(ctx.m1, du, dx)
+        return (dx.reshape(ctx.shape) if dx is not None else None), None, None, None, None, None, None
+
+
+def mlp(ff1, ff2, x):
+    """ff2(gelu(ff1(x))): one fused autograd op for two ROAST linears, plain modules otherwise."""
+    if isinstance(ff1, RoastLinear) and isinstance(ff2, RoastLinear) and ff1.store is ff2.store and x.is_cuda \
+            and x.dtype == torch.bfloat16:
+        return _MLPFn.apply(x, _anchor(ff1.store), ff1.store, ff1.mid, ff1.bias.mid if ff1.bias is not None else None,
+                            ff2.mid, ff2.bias.mid if ff2.bias is not None else None)
+    return ff2(gelu(ff1(x)))
+
+
 class RoastBias(torch.nn.Module):
     """A bias vector of n elements recovered with L in chunks of `chunk` (reading R24:
     registered as a 1 x n embedding, lambda = fp32(C / sqrt(fan_in)) with fan_in the
@@ -253,7 +324,7 @@ class EncoderLayer(torch.nn.Module):
             a = torch.nn.functional.scaled_dot_product_attention(split(q), split(k), split(v))
             a = a.transpose(1, 2).reshape(B, S, d)
         x = self.ln1(self.o(a), x)            # LayerNorm(x + attention), the residual add fused
-        return self.ln2(self.ff2(torch.nn.functional.gelu(self.ff1(x))), x)
+        return self.ln2(mlp(self.ff1, self.ff2, x), x)
 
 
 class BertEmbeddings(torch.nn.Module):

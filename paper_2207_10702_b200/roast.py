@@ -34,6 +34,7 @@ EXPORTS = [
     "roast_p2p_finish", "roast_grad_exchange_p2p", "roast_p2p_reduce", "roast_p2p_gather",
     "roast_grad_exchange_p2p2", "roast_nvls_supported", "roast_nvls_create", "roast_nvls_import",
     "roast_nvls_add_device", "roast_nvls_bind", "roast_nvls_bound", "roast_nvls_reset", "roast_layernorm_fwd",
+    "roast_linear_fwd_act", "roast_linear_bwd_dx_act",
     "roast_layernorm_bwd", "roast_get_error",
     "roast_status_str", "roast_last_error", "roast_debug_tile_map", "roast_debug_chunk_map",
     "roast_debug_materialize", "roast_debug_hash_host", "roast_launch_count", "roast_lms_segments",
@@ -85,6 +86,8 @@ def _load():
         "roast_register_embedding": (st, [H, I64, I32, I32, ctypes.c_double, ctypes.POINTER(I32)]),
         "roast_set_autotune": (st, [H, ctypes.c_int]),
         "roast_linear_fwd_bias": (st, [H, I32, P, P, I64, ctypes.c_int, P, S]),
+        "roast_linear_fwd_act": (st, [H, I32, P, P, P, I64, ctypes.c_int, P, I32, S]),
+        "roast_linear_bwd_dx_act": (st, [H, I32, P, P, P, I64, ctypes.c_int, I32, S]),
         "roast_bias_fwd": (st, [H, I32, P, S]),
         "roast_linear_fwd_chain": (st, [H, I32, I32, P, P, P, I64, ctypes.c_int, P, P, S]),
         "roast_linear_bwd_dx_chain": (st, [H, I32, I32, P, P, P, I64, ctypes.c_int, S]),
@@ -250,6 +253,20 @@ def lms_segments(sizes, mem_size, align=8):
 
 def roast_linear_fwd_bias(h, mid, X_ptr, Y_ptr, tokens, dtype, bias_ptr, stream=0):
     _check(_lib.roast_linear_fwd_bias(h, mid, X_ptr, Y_ptr, tokens, dtype, bias_ptr, stream), "roast_linear_fwd_bias")
+
+
+ACT_NONE, ACT_GELU_TANH = 0, 1
+ERR_UNSUPPORTED = 9
+
+
+def roast_linear_fwd_act(h, mid, X_ptr, Y_ptr, A_ptr, tokens, dtype, bias_ptr=None, act=ACT_GELU_TANH, stream=0):
+    _check(_lib.roast_linear_fwd_act(h, mid, X_ptr, Y_ptr, A_ptr, tokens, dtype, bias_ptr, act, stream),
+           "roast_linear_fwd_act")
+
+
+def roast_linear_bwd_dx_act(h, mid, dY_ptr, U_ptr, dX_ptr, tokens, dtype, act=ACT_GELU_TANH, stream=0):
+    _check(_lib.roast_linear_bwd_dx_act(h, mid, dY_ptr, U_ptr, dX_ptr, tokens, dtype, act, stream),
+           "roast_linear_bwd_dx_act")
 
 
 def roast_linear_fwd_chain(h, id_a, id_b, X_ptr, Ya_ptr, Yb_ptr, tokens, dtype, bias_a=None, bias_b=None, stream=0):
@@ -763,6 +780,28 @@ class Roast:
             dX = self.torch.empty_like(X)
         roast_linear_bwd(self.h, mid, X.data_ptr(), dY.data_ptr(), dX.data_ptr() if need_dx else None, T,
                          self._dt(X), self._s(stream))
+        return dX
+
+    def fwd_act(self, mid, X, Y=None, A=None, bias=None, act=ACT_GELU_TANH, stream=None):
+        """Y = lambda X W~ (+ bias) and A = act(Y) in the same epilogue (roast_linear_fwd_act)."""
+        _, H, O = self.dims[mid]
+        assert X.is_contiguous() and X.shape[-1] == H
+        T = X.numel() // H
+        Y = self.torch.empty(*X.shape[:-1], O, dtype=X.dtype, device=X.device) if Y is None else Y
+        A = self.torch.empty_like(Y) if A is None else A
+        if bias is not None:
+            assert bias.dtype == self.torch.float32 and bias.numel() == O and bias.is_contiguous()
+        roast_linear_fwd_act(self.h, mid, X.data_ptr(), Y.data_ptr(), A.data_ptr(), T, self._dt(X),
+                             bias.data_ptr() if bias is not None else None, act, self._s(stream))
+        return Y, A
+
+    def bwd_dx_act(self, mid, dY, U, dX=None, act=ACT_GELU_TANH, stream=None):
+        """dX = (lambda dY W~^T) * act'(U) in the dX GEMM's epilogue (roast_linear_bwd_dx_act)."""
+        _, H, O = self.dims[mid]
+        T = dY.numel() // O
+        dX = self.torch.empty(T, H, dtype=dY.dtype, device=dY.device) if dX is None else dX
+        roast_linear_bwd_dx_act(self.h, mid, dY.data_ptr(), U.data_ptr(), dX.data_ptr(), T, self._dt(dY), act,
+                                self._s(stream))
         return dX
 
     def bwd_dx(self, mid, dY, dX, stream=None):

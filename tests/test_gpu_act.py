@@ -1,0 +1,99 @@
+"""GELU fused into the tcgen05 GEMM epilogues (roast_linear_fwd_act / roast_linear_bwd_dx_act,
+include/roast.h): against the fp64 oracle ROAST-MM composed with the tanh-form GELU (the
+activation is an N-op of the BERT workload; the linear is the paper's, P:294-313 / P:338-346)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import roast_mm as OM
+from tests.gpu_helpers import bf16_input, rel_frob, store, to_dev
+
+pytestmark = pytest.mark.gpu
+HS = synth.HASH_SEED
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+@pytest.fixture(scope="module")
+def R():
+    from paper_2207_10702_b200 import roast
+    return roast
+
+
+def gelu(x):
+    return 0.5 * x * (1 + np.tanh(np.sqrt(2 / np.pi) * (x + 0.044715 * x ** 3)))
+
+
+def gelu_grad(x):
+    t = np.tanh(np.sqrt(2 / np.pi) * (x + 0.044715 * x ** 3))
+    return 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * np.sqrt(2 / np.pi) * (1 + 3 * 0.044715 * x * x)
+
+
+@pytest.mark.parametrize("T", [1000, 300, 1, 8192])
+def test_fused_gelu_forward_and_dx(R, torch, T):
+    mem = 47192
+    M_np = store(mem)
+    ctx = R.Roast(to_dev(M_np, torch.float32), 64, 64, seed=HS)
+    a, b = ctx.linear(768, 3072), ctx.linear(3072, 768)
+    sa, sb = OM.LinearSpec(768, 3072, 64, 64, mem, HS, a), OM.LinearSpec(3072, 768, 64, 64, mem, HS, b)
+    X_np = bf16_input(synth.SEED_X, (T, 768))
+    dY_np = bf16_input(synth.SEED_DY, (T, 768))
+    bias_np = synth.normal(synth.SEED_X + 3, (3072,)).astype(np.float32)
+    X, dY = to_dev(X_np, torch.bfloat16), to_dev(dY_np, torch.bfloat16)
+    bias = to_dev(bias_np, torch.float32)
+    for _ in range(2):   # the first call tunes the unit width
+        U, A = ctx.fwd_act(a, X, bias=bias)
+        dU = ctx.bwd_dx_act(b, dY, U)
+    torch.cuda.synchronize()
+    ctx.check()
+    U_np = U.float().cpu().numpy().astype(np.float64)
+    A_np = A.float().cpu().numpy().astype(np.float64)
+    rows = slice(None) if T <= 1000 else np.random.default_rng(1).choice(T, 256, replace=False)
+    u_ref = sa.forward(X_np[rows], M_np, True) + bias_np.astype(np.float64)
+    assert rel_frob(U_np[rows], u_ref) <= 1e-2
+    # the activation is taken of the stored (bf16) U, as an unfused op would see it
+    assert rel_frob(A_np, gelu(U_np)) <= 1e-2
+    assert np.max(np.abs(A_np - gelu(U_np))) <= 2 ** -7 * max(1.0, np.abs(A_np).max())
+    du_ref = sb.backward_dx(dY_np[rows], M_np, True) * gelu_grad(U_np[rows])
+    assert rel_frob(dU.float().cpu().numpy()[rows], du_ref) <= 1e-2
+    ctx.close()
+
+
+def test_fused_gelu_unsupported_geometry_is_an_error(R, torch):
+    """A handle whose tiles the tcgen05 path cannot take (32 x 32) reports UNSUPPORTED; the
+    BERT MLP (nn.mlp) then runs the same math unfused."""
+    ctx = R.Roast(torch.rand(1 << 16, device="cuda"), 32, 32, seed=HS, simt_bf16=True)
+    a = ctx.linear(256, 512)
+    X = torch.randn(64, 256, device="cuda").to(torch.bfloat16)
+    with pytest.raises(R.RoastError) as e:
+        ctx.fwd_act(a, X)
+    assert e.value.status == R.ERR_UNSUPPORTED
+    ctx.close()
+
+
+def test_mlp_fused_equals_unfused_autograd(R, torch):
+    """nn.mlp's fused autograd op against the unfused composition ff2(gelu(ff1(x))) through the
+    same handle: output, input gradient and dM within the bf16 tolerance."""
+    from paper_2207_10702_b200 import nn as RN
+    M = torch.rand(47192, device="cuda") * 2 - 1
+    outs = []
+    for fused in (True, False):
+        ctx = R.Roast(M.clone(), 64, 64, seed=HS)
+        f1, f2 = RN.RoastLinear(ctx, 768, 3072, bias=True), RN.RoastLinear(ctx, 3072, 768, bias=True)
+        g = torch.Generator(device="cuda").manual_seed(3)
+        x = torch.randn(4, 250, 768, device="cuda", generator=g).to(torch.bfloat16).requires_grad_(True)
+        dy = torch.randn(4, 250, 768, device="cuda", generator=g).to(torch.bfloat16)
+        ctx.zero_grad()
+        y = RN.mlp(f1, f2, x) if fused else f2(RN.gelu(f1(x)))
+        y.backward(dy)
+        ctx.flush_bias_grads()
+        torch.cuda.synchronize()
+        outs.append((y.float(), x.grad.float(), ctx.dM.clone()))
+        ctx.close()
+    for a, b in zip(outs[0], outs[1]):
+        assert float((a - b).norm() / b.norm()) <= 1e-2

@@ -55,7 +55,7 @@ def test_encoder_layer_gradients_match_dense_autograd():
     a = torch.nn.functional.scaled_dot_product_attention(split(lin(xr, 0)), split(lin(xr, 1)), split(lin(xr, 2)))
     a = a.transpose(1, 2).reshape(B, S, d)
     h1 = torch.nn.functional.layer_norm(xr + lin(a, 3), (d,))
-    yr = torch.nn.functional.layer_norm(h1 + lin(torch.nn.functional.gelu(lin(h1, 4)), 5), (d,))
+    yr = torch.nn.functional.layer_norm(h1 + lin(torch.nn.functional.gelu(lin(h1, 4), approximate="tanh"), 5), (d,))
     lr = (yr * Rw).sum()
     lr.backward()
     assert abs(float(loss) - float(lr)) <= 2e-2 * float((yr.abs() * Rw.abs()).sum())
@@ -138,7 +138,7 @@ def test_roast_bert_embeddings_and_biases_match_dense_autograd(batch_biases):
     a = torch.nn.functional.scaled_dot_product_attention(split(lin(xr, 0)), split(lin(xr, 1)), split(lin(xr, 2)))
     a = a.transpose(1, 2).reshape(B, S, d)
     h1 = torch.nn.functional.layer_norm(xr + lin(a, 3), (d,))
-    yr = torch.nn.functional.layer_norm(h1 + lin(torch.nn.functional.gelu(lin(h1, 4)), 5), (d,))
+    yr = torch.nn.functional.layer_norm(h1 + lin(torch.nn.functional.gelu(lin(h1, 4), approximate="tanh"), 5), (d,))
     (yr * Rw).sum().backward()
     parts = {k: np.zeros(mem) for k in ("linears", "biases", "embeddings")}
     for l, w, b in zip(lins, W, bs):
