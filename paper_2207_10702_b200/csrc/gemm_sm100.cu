@@ -710,18 +710,12 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
                          "r"(pk[c * 32 + 4 * cc + 1]), "r"(pk[c * 32 + 4 * cc + 2]), "r"(pk[c * 32 + 4 * cc + 3])
                          : "memory");
           }
-          if (ACT && MODE == FWD && arow_ok) {   // act_out = act(bf16 Y): each thread its row's 128 B
-            uint4* dst = reinterpret_cast<uint4*>(p.act_out + arow * p.N + nb * NU + c * 64);
+          uint32_t gk[ACT && MODE == FWD ? 32 : 1];   // FWD: act(bf16 Y) of this chunk, staged after Y
+          if constexpr (ACT && MODE == FWD) {
 #pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              uint4 o;
-              uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 x = unpack_bf2(pk[c * 32 + 4 * v + e]);
-                ow[e] = pack_bf2(gelu_tanh(x.x), gelu_tanh(x.y));
-              }
-              dst[v] = o;
+            for (int i = 0; i < 32; ++i) {
+              const float2 x = unpack_bf2(pk[c * 32 + i]);
+              gk[i] = pack_bf2(gelu_tanh(x.x), gelu_tanh(x.y));
             }
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -732,6 +726,26 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
                          "r"(nb * NU + c * 64), "r"(row0), "r"(smem_u32(buf))
                          : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          if constexpr (ACT && MODE == FWD) {   // the act output through the same staging buffer (map: mapOut1)
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) {
+              const uint32_t a = smem_u32(buf + lane * 128 + ((cc ^ (lane & 7)) << 4));
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(gk[4 * cc]), "r"(gk[4 * cc + 1]),
+                           "r"(gk[4 * cc + 2]), "r"(gk[4 * cc + 3])
+                           : "memory");
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                               reinterpret_cast<uint64_t>(&mapOut1)),
+                           "r"(nb * NU + c * 64), "r"(row0), "r"(smem_u32(buf))
+                           : "memory");
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
           }
         }
       }
@@ -1564,11 +1578,13 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
 
 template <int MODE>
 roast_status_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o, const WMaps& w, Params p,
-                      int wm, cudaStream_t s, int nu = BN, const WMapsHalf* hw = nullptr) {
+                      int wm, cudaStream_t s, int nu = BN, const WMapsHalf* hw = nullptr,
+                      const CUtensorMap* o_act = nullptr) {
   if constexpr (MODE != DW) {
     if (p.act) {   // fused activation: the WM = 2 register-held epilogue (checked by the caller)
-      if (nu == 192) return launch_cg<MODE, 2, 2, false, 192, true>(a, b, o, w, p, a, o, p, 0, s, hw);
-      return launch_cg<MODE, 2, 2, false, BN, true>(a, b, o, w, p, a, o, p, 0, s);
+      const CUtensorMap& o1 = o_act ? *o_act : o;
+      if (nu == 192) return launch_cg<MODE, 2, 2, false, 192, true>(a, b, o, w, p, a, o1, p, 0, s, hw);
+      return launch_cg<MODE, 2, 2, false, BN, true>(a, b, o, w, p, a, o1, p, 0, s);
     }
     if (nu == 192) return launch_cg<MODE, 2, 2, false, 192>(a, b, o, w, p, a, o, p, 0, s, hw);
   }
@@ -1704,7 +1720,9 @@ static roast_status_t tok_major_launch(Ctx* c, const Module& m, const void* A, v
   if (st) return st;
   const WMaps& w = *reinterpret_cast<const WMaps*>(c->tmap_shadow);
   const WMapsHalf* hw = reinterpret_cast<const WMapsHalf*>(c->tmap_shadow_half);
-  st = dx ? launch<DX>(a, a, o, w, p, wm, s, nu, hw) : launch<FWD>(a, a, o, w, p, wm, s, nu, hw);
+  CUtensorMap o2 = o;   // FWD with an activation: its output, stored like Y (the kernel's mapOut1)
+  if (act && !dx && (st = make_map_2d(&o2, act_out, uint64_t(N), uint64_t(T), uint64_t(N) * 2, 64, 32))) return st;
+  st = dx ? launch<DX>(a, a, o, w, p, wm, s, nu, hw) : launch<FWD>(a, a, o, w, p, wm, s, nu, hw, &o2);
   if (!st) c->launches++;
   return st;
 }
