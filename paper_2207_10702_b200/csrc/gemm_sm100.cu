@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ubar = reinterpret_cast<uint64_t*>(sStage + C::STAGING + 128);   // [8] ACT DX: U chunk loaded
   int32_t* sCoord = reinterpret_cast<int32_t*>(sStage + C::STAGING + 256);  // [KB_CHUNK * 4]
 
   const int warp = threadIdx.x >> 5;
@@ -401,6 +402,8 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], EPI_WARPS * CG);
     }
+    if constexpr (ACT && MODE == DX)
+      for (int w = 0; w < 8; ++w) mbar_init(&ubar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_map(&mapA);
     if (CHAIN) prefetch_map(&mapA1);
@@ -617,6 +620,7 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
     uint8_t* buf = sStage + (warp - EPI_WARP0) * 4096;
     const uint32_t tempty_leader0 = map_to_rank(smem_u32(&tempty[0]), 0);
     uint32_t aph = 0;
+    uint32_t uph = 0;   // ACT DX: parity of this warp's U-chunk barrier
     for (int it = 0;; ++it) {
       int prob, u;
       if (!unit_at(it, prob, u)) break;
@@ -625,6 +629,14 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
       int mb, nb, split;
       decode_unit(p, u, mb, nb, split);
       const int nsteps = (DIAG(p) & 1) ? 0 : min(NU, p.N - nb * NU) / 64;
+      if constexpr (ACT && MODE == DX) {   // request U's first chunk now: it lands while the MMAs finish
+        const int r0 = mb * BM * CG * WM + int(rank) * BM * WM + jh * BM + q * 32;
+        if (lane == 0 && nsteps > 0) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          mbar_expect_tx(&ubar[warp - EPI_WARP0], 4096);
+          tma_load_2d<1>(&mapA1, buf, smem_u32(&ubar[warp - EPI_WARP0]), nb * NU, r0);
+        }
+      }
       long long tw3 = p.prof ? clock64() : 0;
       mbar_wait(&tfull[0], aph);
       long long tw4 = p.prof ? clock64() : 0;
@@ -674,32 +686,32 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
       if (p.prof) prof_epi[0] += clock64() - tw4;
       const int row0 = mb * BM * CG * WM + int(rank) * BM * WM + jh * BM + q * 32;
       // fused activation: this thread's output row (rows past T are neither read nor written)
-      const int64_t arow = int64_t(row0) + lane;
-      const bool arow_ok = arow < p.T;
-      uint4 un[ACT && MODE == DX ? 8 : 1];   // DX: the next chunk's act_in values (prefetched one chunk ahead)
-      if (ACT && MODE == DX && arow_ok && nsteps > 0) {
-        const uint4* src = reinterpret_cast<const uint4*>(p.act_in + arow * p.N + nb * NU);
-#pragma unroll
-        for (int v = 0; v < 8; ++v) un[v] = __ldg(src + v);
-      }
 #pragma unroll
       for (int c = 0; c < NU / 64; ++c) {
         if (c < nsteps) {
-          if (ACT && MODE == DX) {   // dX = bf16(dh) * act'(u), from the rounded dh as an unfused op sees it
-            uint4 uc[8];
-#pragma unroll
-            for (int v = 0; v < 8; ++v) uc[v] = un[v];
-            if (c + 1 < nsteps && arow_ok) {
-              const uint4* src = reinterpret_cast<const uint4*>(p.act_in + arow * p.N + nb * NU + (c + 1) * 64);
-#pragma unroll
-              for (int v = 0; v < 8; ++v) un[v] = __ldg(src + v);
+          if constexpr (ACT && MODE == DX) {
+            // dX = bf16(dh) * act'(U): the U chunk (32 rows x 64 columns) arrives by TMA in this warp's
+            // staging buffer (once the previous store has read it); each thread reads its row
+            if (lane == 0 && c > 0) {   // chunk 0 was requested before the accumulator wait
+              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              mbar_expect_tx(&ubar[warp - EPI_WARP0], 4096);
+              tma_load_2d<1>(&mapA1, buf, smem_u32(&ubar[warp - EPI_WARP0]), nb * NU + c * 64, row0);
             }
-            const uint32_t* uw = reinterpret_cast<const uint32_t*>(uc);
+            mbar_wait(&ubar[warp - EPI_WARP0], uph);
+            uph ^= 1;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float2 d = unpack_bf2(pk[c * 32 + i]), x = unpack_bf2(uw[i]);
-              pk[c * 32 + i] = pack_bf2(d.x * gelu_tanh_grad(x.x), d.y * gelu_tanh_grad(x.y));
+            for (int cc = 0; cc < 8; ++cc) {
+              uint32_t w0, w1, w2, w3;
+              const uint32_t a = smem_u32(buf + lane * 128 + ((cc ^ (lane & 7)) << 4));
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(a));
+              const uint32_t uw[4] = {w0, w1, w2, w3};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 d = unpack_bf2(pk[c * 32 + 4 * cc + e]), x = unpack_bf2(uw[e]);
+                pk[c * 32 + 4 * cc + e] = pack_bf2(d.x * gelu_tanh_grad(x.x), d.y * gelu_tanh_grad(x.y));
+              }
             }
+            __syncwarp();   // every row read before the buffer is overwritten with dX
           }
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           __syncwarp();
@@ -1582,9 +1594,11 @@ roast_status_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensor
                       const CUtensorMap* o_act = nullptr) {
   if constexpr (MODE != DW) {
     if (p.act) {   // fused activation: the WM = 2 register-held epilogue (checked by the caller)
-      const CUtensorMap& o1 = o_act ? *o_act : o;
-      if (nu == 192) return launch_cg<MODE, 2, 2, false, 192, true>(a, b, o, w, p, a, o1, p, 0, s, hw);
-      return launch_cg<MODE, 2, 2, false, BN, true>(a, b, o, w, p, a, o1, p, 0, s);
+      // the activation's second tensor: FWD writes it (as mapOut1), DX reads U (as mapA1)
+      const CUtensorMap& o1 = (MODE == FWD && o_act) ? *o_act : o;
+      const CUtensorMap& a1 = (MODE == DX && o_act) ? *o_act : a;
+      if (nu == 192) return launch_cg<MODE, 2, 2, false, 192, true>(a, b, o, w, p, a1, o1, p, 0, s, hw);
+      return launch_cg<MODE, 2, 2, false, BN, true>(a, b, o, w, p, a1, o1, p, 0, s);
     }
     if (nu == 192) return launch_cg<MODE, 2, 2, false, 192>(a, b, o, w, p, a, o, p, 0, s, hw);
   }
@@ -1720,9 +1734,10 @@ static roast_status_t tok_major_launch(Ctx* c, const Module& m, const void* A, v
   if (st) return st;
   const WMaps& w = *reinterpret_cast<const WMaps*>(c->tmap_shadow);
   const WMapsHalf* hw = reinterpret_cast<const WMapsHalf*>(c->tmap_shadow_half);
-  CUtensorMap o2 = o;   // FWD with an activation: its output, stored like Y (the kernel's mapOut1)
-  if (act && !dx && (st = make_map_2d(&o2, act_out, uint64_t(N), uint64_t(T), uint64_t(N) * 2, 64, 32))) return st;
-  st = dx ? launch<DX>(a, a, o, w, p, wm, s, nu, hw) : launch<FWD>(a, a, o, w, p, wm, s, nu, hw, &o2);
+  CUtensorMap o2 = o;   // with an activation: FWD its output (mapOut1), DX the U input (mapA1), 32 x 64 boxes
+  if (act && (st = make_map_2d(&o2, dx ? act_in : act_out, uint64_t(N), uint64_t(T), uint64_t(N) * 2, 64, 32)))
+    return st;
+  st = dx ? launch<DX>(a, a, o, w, p, wm, s, nu, hw, &o2) : launch<FWD>(a, a, o, w, p, wm, s, nu, hw, &o2);
   if (!st) c->launches++;
   return st;
 }
