@@ -933,7 +933,7 @@ class Roast:
             except (RoastError, OSError) as e:
                 return repr(e)
 
-        sup = roast_nvls_supported(torch.cuda.current_device())
+        sup = roast_nvls_supported(self.M.device.index or 0)
         agree(True if sup else "CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED = 0", "probe")
         fd_box = [-1]
         agree(attempt(lambda: fd_box.__setitem__(0, roast_nvls_create(self.h, world))) if rank == 0 else True,
