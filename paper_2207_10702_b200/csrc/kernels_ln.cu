@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ x, co
 
 // backward, pass 1: ds per row, and per-warp partial sums of dy xhat / dy over the warp's rows
 // (rows w, w + nwarps, ... in that order), kept in the warp's slice of shared memory (each lane
-// owns its columns: no atomics) and written to part[warp][2][n] at the end
+// owns its columns: no atomics); at the end the block's 8 warps are combined in warp order and
+// written to part[block][2][n]
 template <class T, class P, int VPL>
 __global__ void __launch_bounds__(256) ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ s,
                                                     const P* __restrict__ g, const float* __restrict__ mean_in,
@@ -182,10 +183,17 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const T* __restrict__ dy, c
       }
     }
   }
-  __syncwarp();
-  for (int c = lane; c < n; c += 32) {   // column c = vector c / 8, element c % 8
-    part[(warp * 2) * n + c] = pg[(c & 7) * nv + (c >> 3)];
-    part[(warp * 2 + 1) * n + c] = pb[(c & 7) * nv + (c >> 3)];
+  // the block's 8 warp partials combined in warp order, one partial row pair per block
+  __syncthreads();
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {   // column c = vector c / 8, element c % 8
+    const int e = (c & 7) * nv + (c >> 3);
+    float a = acc_sm[e], b = acc_sm[n + e];
+    for (int w = 1; w < 8; ++w) {
+      a += acc_sm[w * 2 * n + e];
+      b += acc_sm[w * 2 * n + n + e];
+    }
+    part[(int64_t(blockIdx.x) * 2) * n + c] = a;
+    part[(int64_t(blockIdx.x) * 2 + 1) * n + c] = b;
   }
 }
 
@@ -300,11 +308,13 @@ roast_status_t roast_layernorm_bwd(const void* dy, const void* s_in, const void*
   if (!dy || !s_in || !gamma || !mean || !rstd || !ds || !dgamma || !dbeta)
     return fail(ROAST_ERR_CONFIG, "layernorm: null pointer");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  // warps of pass 1: enough to cover the rows once, at most 148 x 4 blocks; each leaves 2 n
-  // partials (a fixed grid for a given row count: the reduce order is data-independent)
-  const int64_t nw = std::max<int64_t>(8, std::min<int64_t>((rows + 7) / 8 * 8, int64_t(148) * 4 * 8));
+  // warps of pass 1 (a fixed grid for a given row count: the reduce order is data-independent);
+  // each leaves 2 n partials
+  // ~4 rows per warp, at most one resident wave of 148 x 4 blocks; the reduce reads one partial
+  // row pair per block
+  const int64_t nw = std::max<int64_t>(8, std::min<int64_t>((rows / 4 + 7) / 8 * 8, int64_t(148) * 4 * 8));
   Scratch ws;
-  if (roast_status_t st = scratch_alloc(ws, size_t(nw) * 2 * size_t(n) * sizeof(float), s)) return st;
+  if (roast_status_t st = scratch_alloc(ws, size_t(nw / 8) * 2 * size_t(n) * sizeof(float), s)) return st;
   cudaError_t e;
   if (dt == ROAST_BF16 && pdt == ROAST_BF16)
     e = ln_bwd_launch<__nv_bfloat16, __nv_bfloat16>(dy, s_in, gamma, mean, rstd, ds, ws.as<float>(), nw, rows, n, s);
@@ -315,7 +325,7 @@ roast_status_t roast_layernorm_bwd(const void* dy, const void* s_in, const void*
   else
     e = ln_bwd_launch<float, float>(dy, s_in, gamma, mean, rstd, ds, ws.as<float>(), nw, rows, n, s);
   ROAST_CUDA_CHECK(e);
-  ln_param_reduce_kernel<<<unsigned((n + 31) / 32), 1024, 0, s>>>(ws.as<float>(), nw, n, dgamma, dbeta);
+  ln_param_reduce_kernel<<<unsigned((n + 31) / 32), 1024, 0, s>>>(ws.as<float>(), nw / 8, n, dgamma, dbeta);
   ROAST_CUDA_CHECK(cudaGetLastError());
   return ROAST_OK;
 }
