@@ -277,6 +277,20 @@ roast_status_t roast_linear_fwd_act(roast_t h, int32_t id, const void* d_X, void
                                     roast_dtype_t dt, const float* d_bias, int32_t act, roast_stream_t stream);
 roast_status_t roast_linear_bwd_dx_act(roast_t h, int32_t id, const void* d_dY, const void* d_U, void* d_dX,
                                        int64_t tokens, roast_dtype_t dt, int32_t act, roast_stream_t stream);
+/* The MLP pair b(act(a(X))) with the activation inside the chained launches (as
+ * roast_linear_fwd_chain / roast_linear_bwd_chain):
+ * roast_linear_fwd_chain_act: U = a(X) (+ bias_a), A = act(U), Y_b = b(A) (+ bias_b); one launch
+ *   on the tcgen05 path (b's units stream behind a's published tiles of A), else
+ *   roast_linear_fwd_act + roast_linear_fwd_bias.
+ * roast_linear_bwd_chain_act: dU = (dY_b W~_b^T) * act'(U), dM += b(A, dY_b), dX_a = dU W~_a^T,
+ *   dM += a(X_a, dU); one launch on the tcgen05 path, else the four calls. */
+roast_status_t roast_linear_fwd_chain_act(roast_t h, int32_t id_a, int32_t id_b, const void* d_X, void* d_U,
+                                          void* d_A, void* d_Y_b, int64_t tokens, roast_dtype_t dt,
+                                          const float* d_bias_a, const float* d_bias_b, int32_t act,
+                                          roast_stream_t stream);
+roast_status_t roast_linear_bwd_chain_act(roast_t h, int32_t id_a, int32_t id_b, const void* d_X_a, const void* d_A,
+                                          const void* d_U, const void* d_dY_b, void* d_dU, void* d_dX_a,
+                                          int64_t tokens, roast_dtype_t dt, int32_t act, roast_stream_t stream);
 
 /* LayerNorm of the ROASTed BERT workload (an N-operation, P:263-265,
  * not part of the ROAST hashing itself): at C3's 65 536 tokens torch's LayerNorm takes 0.85 ms

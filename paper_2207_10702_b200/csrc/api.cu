@@ -565,6 +565,52 @@ roast_status_t roast_linear_bwd_chain(roast_t h, int32_t id_a, int32_t id_b, con
   return roast_linear_bwd_dm(h, id_a, X_a, dY_a, T, dt, stream);
 }
 
+roast_status_t roast_linear_fwd_chain_act(roast_t h, int32_t id_a, int32_t id_b, const void* X, void* U, void* A,
+                                          void* Y_b, int64_t T, roast_dtype_t dt, const float* bias_a,
+                                          const float* bias_b, int32_t act, roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module *ma, *mb;
+  roast_status_t st = get_module(c, id_a, kLinear, &ma);
+  if (st) return st;
+  if ((st = get_module(c, id_b, kLinear, &mb))) return st;
+  if (ma->O != mb->H) return fail(ROAST_ERR_SHAPE, "chain: out_features of a != in_features of b");
+  if (act != ROAST_ACT_GELU_TANH) return fail(ROAST_ERR_CONFIG, "act: ROAST_ACT_GELU_TANH");
+  if (T < 0) return fail(ROAST_ERR_SHAPE, "tokens < 0");
+  if (T > 0 && (!X || !U || !A || !Y_b)) return fail(ROAST_ERR_CONFIG, "null X / U / A / Y_b");
+  if ((reinterpret_cast<uintptr_t>(bias_a) | reinterpret_cast<uintptr_t>(bias_b)) & 15)
+    return fail(ROAST_ERR_CONFIG, "bias must be 16-byte aligned");
+  if (T == 0) return ROAST_OK;
+  if (dt == ROAST_BF16 && use_sm100(c, *ma) && use_sm100(c, *mb)) {
+    st = sm100_chain(c, *ma, *mb, X, U, Y_b, T, false, bias_a, bias_b, reinterpret_cast<cudaStream_t>(stream), act, A);
+    if (st != ROAST_ERR_UNSUPPORTED) return st;
+  }
+  if ((st = roast_linear_fwd_act(h, id_a, X, U, A, T, dt, bias_a, act, stream))) return st;
+  return roast_linear_fwd_bias(h, id_b, A, Y_b, T, dt, bias_b, stream);
+}
+
+roast_status_t roast_linear_bwd_chain_act(roast_t h, int32_t id_a, int32_t id_b, const void* X_a, const void* A,
+                                          const void* U, const void* dY_b, void* dU, void* dX_a, int64_t T,
+                                          roast_dtype_t dt, int32_t act, roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module *ma, *mb;
+  roast_status_t st = get_module(c, id_a, kLinear, &ma);
+  if (st) return st;
+  if ((st = get_module(c, id_b, kLinear, &mb))) return st;
+  if (ma->O != mb->H) return fail(ROAST_ERR_SHAPE, "chain: out_features of a != in_features of b");
+  if (act != ROAST_ACT_GELU_TANH) return fail(ROAST_ERR_CONFIG, "act: ROAST_ACT_GELU_TANH");
+  if (T < 0) return fail(ROAST_ERR_SHAPE, "tokens < 0");
+  if (T > 0 && (!X_a || !A || !U || !dY_b || !dU || !dX_a)) return fail(ROAST_ERR_CONFIG, "null tensor argument");
+  if (T == 0) return ROAST_OK;
+  if (dt == ROAST_BF16 && use_sm100(c, *ma) && use_sm100(c, *mb)) {
+    st = sm100_bwd_chain(c, *ma, *mb, X_a, A, dY_b, dU, dX_a, T, reinterpret_cast<cudaStream_t>(stream), act, U);
+    if (st != ROAST_ERR_UNSUPPORTED) return st;
+  }
+  if ((st = roast_linear_bwd_dx_act(h, id_b, dY_b, U, dU, T, dt, act, stream))) return st;
+  if ((st = roast_linear_bwd_dm(h, id_b, A, dY_b, T, dt, stream))) return st;
+  if ((st = roast_linear_bwd_dx(h, id_a, dU, dX_a, T, dt, stream))) return st;
+  return roast_linear_bwd_dm(h, id_a, X_a, dU, T, dt, stream);
+}
+
 roast_status_t roast_bias_fwd(roast_t h, int32_t bias_id, float* b, roast_stream_t stream) {
   Ctx* c = ctx(h);
   Module* m;

@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
                    const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ WMaps wmaps,
                    const __grid_constant__ Params p0, const __grid_constant__ CUtensorMap mapA1,
                    const __grid_constant__ CUtensorMap mapOut1, const __grid_constant__ Params p1,
-                   const __grid_constant__ WMapsHalf hmaps) {
+                   const __grid_constant__ WMapsHalf hmaps, const __grid_constant__ CUtensorMap mapAct) {
   static_assert(NU == BN || (NU == 192 && MODE != DW && CG == 2 && WM == 2 && !CHAIN), "NU = 192: FWD / DX, 2 x 2");
   using C = Cfg<CG, WM, NU>;
   constexpr bool RF = Roles<MODE, CG, WM>::RF;
@@ -629,12 +629,13 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
       int mb, nb, split;
       decode_unit(p, u, mb, nb, split);
       const int nsteps = (DIAG(p) & 1) ? 0 : min(NU, p.N - nb * NU) / 64;
-      if constexpr (ACT && MODE == DX) {   // request U's first chunk now: it lands while the MMAs finish
+      const bool act_u = ACT && (!CHAIN || prob == 0);   // chained: the activation follows problem 0
+      if (ACT && MODE == DX && act_u) {   // request U's first chunk now: it lands while the MMAs finish
         const int r0 = mb * BM * CG * WM + int(rank) * BM * WM + jh * BM + q * 32;
         if (lane == 0 && nsteps > 0) {
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           mbar_expect_tx(&ubar[warp - EPI_WARP0], 4096);
-          tma_load_2d<1>(&mapA1, buf, smem_u32(&ubar[warp - EPI_WARP0]), nb * NU, r0);
+          tma_load_2d<1>(&mapAct, buf, smem_u32(&ubar[warp - EPI_WARP0]), nb * NU, r0);
         }
       }
       long long tw3 = p.prof ? clock64() : 0;
@@ -689,13 +690,13 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
 #pragma unroll
       for (int c = 0; c < NU / 64; ++c) {
         if (c < nsteps) {
-          if constexpr (ACT && MODE == DX) {
+          if (ACT && MODE == DX && act_u) {
             // dX = bf16(dh) * act'(U): the U chunk (32 rows x 64 columns) arrives by TMA in this warp's
             // staging buffer (once the previous store has read it); each thread reads its row
             if (lane == 0 && c > 0) {   // chunk 0 was requested before the accumulator wait
               asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
               mbar_expect_tx(&ubar[warp - EPI_WARP0], 4096);
-              tma_load_2d<1>(&mapA1, buf, smem_u32(&ubar[warp - EPI_WARP0]), nb * NU + c * 64, row0);
+              tma_load_2d<1>(&mapAct, buf, smem_u32(&ubar[warp - EPI_WARP0]), nb * NU + c * 64, row0);
             }
             mbar_wait(&ubar[warp - EPI_WARP0], uph);
             uph ^= 1;
@@ -723,7 +724,7 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
                          : "memory");
           }
           uint32_t gk[ACT && MODE == FWD ? 32 : 1];   // FWD: act(bf16 Y) of this chunk, staged after Y
-          if constexpr (ACT && MODE == FWD) {
+          if (ACT && MODE == FWD && act_u) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const float2 x = unpack_bf2(pk[c * 32 + i]);
@@ -739,7 +740,7 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
                          : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
-          if constexpr (ACT && MODE == FWD) {   // the act output through the same staging buffer (map: mapOut1)
+          if (ACT && MODE == FWD && act_u) {   // the act output through the same staging buffer (mapAct)
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             __syncwarp();
 #pragma unroll
@@ -753,7 +754,7 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
             __syncwarp();
             if (lane == 0) {
               asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                               reinterpret_cast<uint64_t>(&mapOut1)),
+                               reinterpret_cast<uint64_t>(&mapAct)),
                            "r"(nb * NU + c * 64), "r"(row0), "r"(smem_u32(buf))
                            : "memory");
               asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -1016,6 +1017,7 @@ struct MixProb {
   int dep;                  // problem whose output tiles this one reads (0) or -1
   int publish;              // 1: this problem's units publish ready counters (P0)
   int ws_slot;              // DW, deterministic: index of its workspace map (maps.ws), else -1
+  int act;                  // DX: multiply the output by act'(U) (U from maps.u; the BERT MLP's GELU)
   int ntiles;               // DW: hash tiles of the module (workspace row = (split * ntiles + t) * 64)
 };
 struct MixParams {
@@ -1036,6 +1038,7 @@ struct MixMaps {
   WMaps shadow;             // bf16 shadow, 8 phase views (DX B tiles)
   WMaps dm;                 // dM, 8 fp32 phase views (DW reduce-add)
   CUtensorMap ws[2];        // deterministic mode: per-tile fp32 workspaces of the two DW problems
+  CUtensorMap u;            // act: the pre-activation U [tokens x N] bf16, 32 x 64 boxes
 };
 
 constexpr int MIX_THREADS = 384;
@@ -1068,6 +1071,7 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
   uint64_t* tfull = empty + MIX_STAGES;                         // per TMEM half
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ubar = reinterpret_cast<uint64_t*>(sStage + 8 * 4096 + 128);   // [8] act: U chunk loaded
   int32_t* sCoord = reinterpret_cast<int32_t*>(sStage + 8 * 4096 + 256);
 
   const int warp = threadIdx.x >> 5;
@@ -1095,6 +1099,7 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
       mbar_init(&tfull[h], 1);
       mbar_init(&tempty[h], 8 * CG);   // DW: 8 warps x 1; DX: the half's 4 warps x 2
     }
+    for (int w = 0; w < 8; ++w) mbar_init(&ubar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int i = 0; i < 4; ++i) {
       prefetch_map(&maps.a[i]);
@@ -1290,6 +1295,7 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
     const uint32_t tempty_leader0 = map_to_rank(smem_u32(&tempty[0]), 0);
     uint32_t usep = 0;   // bit h: parity of the uses of TMEM half h so far (as the MMA issuer's)
     int dwh = 0;
+    uint32_t uph = 0;    // act: parity of this warp's U-chunk barrier
     for (int it = 0;; ++it) {
       int prob, u;
       if (!unit_at(it, prob, u)) break;
@@ -1337,6 +1343,28 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           if (c < nsteps) {
+            if (P.act) {   // dX = bf16(dh) * act'(U): U's 32 x 64 chunk by TMA into this warp's buffer
+              if (lane == 0) {
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                mbar_expect_tx(&ubar[warp - EPI_WARP0], 4096);
+                tma_load_2d<1>(&maps.u, buf, smem_u32(&ubar[warp - EPI_WARP0]), nb * 256 + c * 64, row0);
+              }
+              mbar_wait(&ubar[warp - EPI_WARP0], uph);
+              uph ^= 1;
+#pragma unroll
+              for (int cc = 0; cc < 8; ++cc) {
+                uint32_t w0, w1, w2, w3;
+                const uint32_t a = smem_u32(buf + lane * 128 + ((cc ^ (lane & 7)) << 4));
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(a));
+                const uint32_t uw[4] = {w0, w1, w2, w3};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 d = unpack_bf2(pk[c * 32 + 4 * cc + e]), x = unpack_bf2(uw[e]);
+                  pk[c * 32 + 4 * cc + e] = pack_bf2(d.x * gelu_tanh_grad(x.x), d.y * gelu_tanh_grad(x.y));
+                }
+              }
+              __syncwarp();   // every row read before the buffer takes dX
+            }
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             __syncwarp();
 #pragma unroll
@@ -1526,7 +1554,8 @@ int cta_group() {
 template <int MODE, int CG, int WM, bool CHAIN = false, int NU = BN, bool ACT = false>
 roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o, const WMaps& w,
                          const Params& p, const CUtensorMap& a1, const CUtensorMap& o1, const Params& p1,
-                         int grid_pairs, cudaStream_t s, const WMapsHalf* hw = nullptr) {
+                         int grid_pairs, cudaStream_t s, const WMapsHalf* hw = nullptr,
+                         const CUtensorMap* act_map = nullptr) {
   using C = Cfg<CG, WM, NU>;
   static bool attr = false;
   if (!attr) {
@@ -1563,7 +1592,7 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
   }
   static const WMapsHalf no_half{};
   cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mm_sm100<MODE, CG, WM, CHAIN, NU, ACT>, a, b, o, w, pp, a1, o1, pp1,
-                                     hw ? *hw : no_half);
+                                     hw ? *hw : no_half, act_map ? *act_map : o);
   if (e != cudaSuccess) return cuda_fail(e, "roast_mm_sm100 launch");
   if (pp.prof) {
     cudaDeviceSynchronize();
@@ -1594,11 +1623,9 @@ roast_status_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensor
                       const CUtensorMap* o_act = nullptr) {
   if constexpr (MODE != DW) {
     if (p.act) {   // fused activation: the WM = 2 register-held epilogue (checked by the caller)
-      // the activation's second tensor: FWD writes it (as mapOut1), DX reads U (as mapA1)
-      const CUtensorMap& o1 = (MODE == FWD && o_act) ? *o_act : o;
-      const CUtensorMap& a1 = (MODE == DX && o_act) ? *o_act : a;
-      if (nu == 192) return launch_cg<MODE, 2, 2, false, 192, true>(a, b, o, w, p, a1, o1, p, 0, s, hw);
-      return launch_cg<MODE, 2, 2, false, BN, true>(a, b, o, w, p, a1, o1, p, 0, s);
+      // the activation's second tensor (mapAct): FWD writes act(Y) there, DX reads U from it
+      if (nu == 192) return launch_cg<MODE, 2, 2, false, 192, true>(a, b, o, w, p, a, o, p, 0, s, hw, o_act);
+      return launch_cg<MODE, 2, 2, false, BN, true>(a, b, o, w, p, a, o, p, 0, s, nullptr, o_act);
     }
     if (nu == 192) return launch_cg<MODE, 2, 2, false, 192>(a, b, o, w, p, a, o, p, 0, s, hw);
   }
@@ -1734,7 +1761,7 @@ static roast_status_t tok_major_launch(Ctx* c, const Module& m, const void* A, v
   if (st) return st;
   const WMaps& w = *reinterpret_cast<const WMaps*>(c->tmap_shadow);
   const WMapsHalf* hw = reinterpret_cast<const WMapsHalf*>(c->tmap_shadow_half);
-  CUtensorMap o2 = o;   // with an activation: FWD its output (mapOut1), DX the U input (mapA1), 32 x 64 boxes
+  CUtensorMap o2 = o;   // with an activation (the kernel's mapAct): FWD its output, DX the U input, 32 x 64 boxes
   if (act && (st = make_map_2d(&o2, dx ? act_in : act_out, uint64_t(N), uint64_t(T), uint64_t(N) * 2, 64, 32)))
     return st;
   st = dx ? launch<DX>(a, a, o, w, p, wm, s, nu, hw, &o2) : launch<FWD>(a, a, o, w, p, wm, s, nu, hw, &o2);
@@ -1903,9 +1930,11 @@ ChainPlan plan_chain(int m_tiles, int nt0, int kb0, int nt1, int kb1, int npairs
 }  // namespace
 
 roast_status_t sm100_chain(Ctx* c, const Module& m0, const Module& m1, const void* A0, void* out0, void* out1,
-                           int64_t T, bool dx, const float* bias0, const float* bias1, cudaStream_t s) {
+                           int64_t T, bool dx, const float* bias0, const float* bias1, cudaStream_t s, int act,
+                           void* act_buf) {
   if (!supported(c, m0) || !supported(c, m1) || cta_group() != 2 || T >= (int64_t(1) << 31) || T <= 0)
     return ROAST_ERR_UNSUPPORTED;
+  if (act && dx) return ROAST_ERR_UNSUPPORTED;   // forward only: problem 1 reads act(problem 0's output)
   if (getenv("ROAST_NO_CHAIN")) return ROAST_ERR_UNSUPPORTED;
   // geometry: FWD problem 0 = m0 (K = H0, N = O0), problem 1 = m1 (K = H1 = O0, N = O1);
   //           DX  problem 0 = m0 (K = O0, N = H0), problem 1 = m1 (K = O1 = H0, N = H1)
@@ -1997,7 +2026,12 @@ roast_status_t sm100_chain(Ctx* c, const Module& m0, const Module& m1, const voi
   Params p0, p1;
   CUtensorMap a0, o0, a1, o1;
   if ((st = prob(m0, A0, out0, N0, K0, dx, bias0, p0, a0, o0))) return st;
-  if ((st = prob(m1, out0, out1, N1, K1, dx, bias1, p1, a1, o1))) return st;
+  if ((st = prob(m1, act ? act_buf : out0, out1, N1, K1, dx, bias1, p1, a1, o1))) return st;
+  CUtensorMap oact = o0;   // with an activation: problem 0 also writes act(Y_0) here, problem 1 reads it
+  if (act) {
+    if ((st = make_map_2d(&oact, act_buf, uint64_t(N0), uint64_t(T), uint64_t(N0) * 2, 64, 32))) return st;
+    p0.act = act;
+  }
   p0.chain = 1;
   p0.sched = it->second.first;
   p0.sched_len = it->second.second;
@@ -2005,8 +2039,9 @@ roast_status_t sm100_chain(Ctx* c, const Module& m0, const Module& m1, const voi
   p0.err = c->d_err;
   ROAST_CUDA_CHECK(cudaMemsetAsync(flags, 0, size_t(p0.units) * sizeof(int), s));
   const WMaps& w = *reinterpret_cast<const WMaps*>(c->tmap_shadow);
-  st = dx ? launch_cg<DX, 2, WMC, true>(a0, a0, o0, w, p0, a1, o1, p1, pairs, s)
-          : launch_cg<FWD, 2, WMC, true>(a0, a0, o0, w, p0, a1, o1, p1, pairs, s);
+  st = dx    ? launch_cg<DX, 2, WMC, true>(a0, a0, o0, w, p0, a1, o1, p1, pairs, s)
+       : act ? launch_cg<FWD, 2, WMC, true, BN, true>(a0, a0, o0, w, p0, a1, o1, p1, pairs, s, nullptr, &oact)
+             : launch_cg<FWD, 2, WMC, true>(a0, a0, o0, w, p0, a1, o1, p1, pairs, s);
   if (!st) c->launches++;
   return st;
 }
@@ -2288,7 +2323,8 @@ MixPlan plan_mix(int mt0, int nt0, int kb0, int mt1, int nt1, int kbT, int mt2, 
 }  // namespace
 
 roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, const void* X_a, const void* Y_a,
-                               const void* dY_b, void* dY_a, void* dX_a, int64_t T, cudaStream_t s) {
+                               const void* dY_b, void* dY_a, void* dX_a, int64_t T, cudaStream_t s, int act,
+                               const void* U) {
   using namespace sm100;
   if (!supported(c, ma) || !supported(c, mbm) || cta_group() != 2 || T <= 0 || T >= (int64_t(1) << 31) ||
       getenv("ROAST_NO_BWD_FUSE"))
@@ -2385,6 +2421,11 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
     return make_map_blocks(&maps.b[pi], dY, uint64_t(m.O), uint64_t(T), BK, 2);
   };
   if ((st = dx_prob(mp.p[0], mbm, dY_b, dY_a, 0))) return st;
+  if (act) {   // dY_a = (dY_b W_b^T) * act'(U): U is layer a's pre-activation, [T x a.O]
+    if (!U) return ROAST_ERR_UNSUPPORTED;
+    mp.p[0].act = act;
+    if ((st = make_map_2d(&maps.u, U, uint64_t(mbm.H), uint64_t(T), uint64_t(mbm.H) * 2, 64, 32))) return st;
+  }
   if ((st = dw_prob(mp.p[1], mbm, Y_a, dY_b, s1, 1))) return st;
   if ((st = dx_prob(mp.p[2], ma, dY_a, dX_a, 2))) return st;
   if ((st = dw_prob(mp.p[3], ma, X_a, dY_a, s3, 3))) return st;

@@ -287,7 +287,8 @@ roast_status_t sm100_fwd(Ctx* c, const Module& m, const void* X, void* Y, int64_
 // Returns ROAST_ERR_UNSUPPORTED when the shapes are not on the tcgen05 path or chaining would
 // not beat two launches (the caller then makes two launches).
 roast_status_t sm100_chain(Ctx* c, const Module& m0, const Module& m1, const void* A0, void* out0, void* out1,
-                           int64_t T, bool dx, const float* bias0, const float* bias1, cudaStream_t s);
+                           int64_t T, bool dx, const float* bias0, const float* bias1, cudaStream_t s, int act = 0,
+                           void* act_buf = nullptr);
 roast_status_t sm100_dx(Ctx* c, const Module& m, const void* dY, void* dX, int64_t T, cudaStream_t s);
 // the same with an activation fused into the register-held epilogue (roast_linear_fwd_act / _bwd_dx_act)
 roast_status_t sm100_fwd_act(Ctx* c, const Module& m, const void* X, void* Y, void* A, int64_t T, const float* bias,
@@ -299,7 +300,8 @@ roast_status_t sm100_dx_act(Ctx* c, const Module& m, const void* dY, const void*
 // GEMMs co-scheduled (gemm_sm100.cu roast_mix_sm100).  ROAST_ERR_UNSUPPORTED when the shapes /
 // mode do not allow it (the caller then makes the four launches).
 roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mb, const void* X_a, const void* Y_a,
-                               const void* dY_b, void* dY_a, void* dX_a, int64_t T, cudaStream_t s);
+                               const void* dY_b, void* dY_a, void* dX_a, int64_t T, cudaStream_t s, int act = 0,
+                               const void* U = nullptr);
 roast_status_t sm100_dw(Ctx* c, const Module& m, const void* X, const void* dY, int64_t T, cudaStream_t s);
 
 }  // namespace roast

@@ -105,7 +105,9 @@ def _gelu_grad(u):
 class _MLPFn(torch.autograd.Function):
     """y = ff2(gelu(ff1(x))) with the GELU inside the GEMM epilogues: the forward of ff1 writes
     u = x W1 (+ b1) and h = gelu(u); the backward's dX GEMM of ff2 writes du = (dy W2^T) * gelu'(u)
-    directly.  Off the fused path (roast_linear_*_act UNSUPPORTED) the same math runs unfused."""
+    directly.  Off the fused path (roast_linear_*_act UNSUPPORTED) the same math runs unfused.
+    (The pair as one chained forward + one fused backward, roast_linear_{fwd,bwd}_chain_act, was
+    measured in the BERT step and was not faster: separate launches are kept here.)"""
 
     @staticmethod
     def forward(ctx, x, anchor, store, m1, b1, m2, b2):

@@ -34,7 +34,7 @@ EXPORTS = [
     "roast_p2p_finish", "roast_grad_exchange_p2p", "roast_p2p_reduce", "roast_p2p_gather",
     "roast_grad_exchange_p2p2", "roast_nvls_supported", "roast_nvls_create", "roast_nvls_import",
     "roast_nvls_add_device", "roast_nvls_bind", "roast_nvls_bound", "roast_nvls_reset", "roast_layernorm_fwd",
-    "roast_linear_fwd_act", "roast_linear_bwd_dx_act",
+    "roast_linear_fwd_act", "roast_linear_bwd_dx_act", "roast_linear_fwd_chain_act", "roast_linear_bwd_chain_act",
     "roast_layernorm_bwd", "roast_get_error",
     "roast_status_str", "roast_last_error", "roast_debug_tile_map", "roast_debug_chunk_map",
     "roast_debug_materialize", "roast_debug_hash_host", "roast_launch_count", "roast_lms_segments",
@@ -88,6 +88,8 @@ def _load():
         "roast_linear_fwd_bias": (st, [H, I32, P, P, I64, ctypes.c_int, P, S]),
         "roast_linear_fwd_act": (st, [H, I32, P, P, P, I64, ctypes.c_int, P, I32, S]),
         "roast_linear_bwd_dx_act": (st, [H, I32, P, P, P, I64, ctypes.c_int, I32, S]),
+        "roast_linear_fwd_chain_act": (st, [H, I32, I32, P, P, P, P, I64, ctypes.c_int, P, P, I32, S]),
+        "roast_linear_bwd_chain_act": (st, [H, I32, I32, P, P, P, P, P, P, I64, ctypes.c_int, I32, S]),
         "roast_bias_fwd": (st, [H, I32, P, S]),
         "roast_linear_fwd_chain": (st, [H, I32, I32, P, P, P, I64, ctypes.c_int, P, P, S]),
         "roast_linear_bwd_dx_chain": (st, [H, I32, I32, P, P, P, I64, ctypes.c_int, S]),
@@ -267,6 +269,18 @@ def roast_linear_fwd_act(h, mid, X_ptr, Y_ptr, A_ptr, tokens, dtype, bias_ptr=No
 def roast_linear_bwd_dx_act(h, mid, dY_ptr, U_ptr, dX_ptr, tokens, dtype, act=ACT_GELU_TANH, stream=0):
     _check(_lib.roast_linear_bwd_dx_act(h, mid, dY_ptr, U_ptr, dX_ptr, tokens, dtype, act, stream),
            "roast_linear_bwd_dx_act")
+
+
+def roast_linear_fwd_chain_act(h, id_a, id_b, X_ptr, U_ptr, A_ptr, Yb_ptr, tokens, dtype, bias_a=None, bias_b=None,
+                               act=ACT_GELU_TANH, stream=0):
+    _check(_lib.roast_linear_fwd_chain_act(h, id_a, id_b, X_ptr, U_ptr, A_ptr, Yb_ptr, tokens, dtype, bias_a, bias_b,
+                                           act, stream), "roast_linear_fwd_chain_act")
+
+
+def roast_linear_bwd_chain_act(h, id_a, id_b, Xa_ptr, A_ptr, U_ptr, dYb_ptr, dU_ptr, dXa_ptr, tokens, dtype,
+                               act=ACT_GELU_TANH, stream=0):
+    _check(_lib.roast_linear_bwd_chain_act(h, id_a, id_b, Xa_ptr, A_ptr, U_ptr, dYb_ptr, dU_ptr, dXa_ptr, tokens,
+                                           dtype, act, stream), "roast_linear_bwd_chain_act")
 
 
 def roast_linear_fwd_chain(h, id_a, id_b, X_ptr, Ya_ptr, Yb_ptr, tokens, dtype, bias_a=None, bias_b=None, stream=0):
@@ -794,6 +808,31 @@ class Roast:
         roast_linear_fwd_act(self.h, mid, X.data_ptr(), Y.data_ptr(), A.data_ptr(), T, self._dt(X),
                              bias.data_ptr() if bias is not None else None, act, self._s(stream))
         return Y, A
+
+    def fwd_chain_act(self, a, b, X, bias_a=None, bias_b=None, act=ACT_GELU_TANH, stream=None):
+        """U = a(X), A = act(U), Y_b = b(A) in one launch (roast_linear_fwd_chain_act); returns (U, A, Y_b)."""
+        _, H, O = self.dims[a]
+        _, H2, O2 = self.dims[b]
+        T = X.numel() // H
+        U = self.torch.empty(T, O, dtype=X.dtype, device=X.device)
+        A = self.torch.empty_like(U)
+        Yb = self.torch.empty(T, O2, dtype=X.dtype, device=X.device)
+        ptr = (lambda t: None if t is None else t.data_ptr())   # noqa: E731
+        roast_linear_fwd_chain_act(self.h, a, b, X.data_ptr(), U.data_ptr(), A.data_ptr(), Yb.data_ptr(), T,
+                                   self._dt(X), ptr(bias_a), ptr(bias_b), act, self._s(stream))
+        return U, A, Yb
+
+    def bwd_chain_act(self, a, b, Xa, A, U, dYb, act=ACT_GELU_TANH, stream=None):
+        """The backward of fwd_chain_act (roast_linear_bwd_chain_act): dM += both layers' scatters;
+        returns (dU, dX_a)."""
+        _, H, O = self.dims[a]
+        _, H2, O2 = self.dims[b]
+        T = dYb.numel() // O2
+        dU = self.torch.empty(T, H2, dtype=dYb.dtype, device=dYb.device)
+        dXa = self.torch.empty(T, H, dtype=dYb.dtype, device=dYb.device)
+        roast_linear_bwd_chain_act(self.h, a, b, Xa.data_ptr(), A.data_ptr(), U.data_ptr(), dYb.data_ptr(),
+                                   dU.data_ptr(), dXa.data_ptr(), T, self._dt(dYb), act, self._s(stream))
+        return dU, dXa
 
     def bwd_dx_act(self, mid, dY, U, dX=None, act=ACT_GELU_TANH, stream=None):
         """dX = (lambda dY W~^T) * act'(U) in the dX GEMM's epilogue (roast_linear_bwd_dx_act)."""

@@ -97,3 +97,36 @@ def test_mlp_fused_equals_unfused_autograd(R, torch):
         ctx.close()
     for a, b in zip(outs[0], outs[1]):
         assert float((a - b).norm() / b.norm()) <= 1e-2
+
+
+@pytest.mark.parametrize("T", [1000, 300, 8192])
+def test_fused_chain_act_matches_oracle(R, torch, T):
+    """The MLP pair with the GELU inside the chained forward and the fused backward
+    (roast_linear_fwd_chain_act / _bwd_chain_act): every output against the fp64 oracle chain."""
+    mem = 47192
+    M_np = store(mem)
+    ctx = R.Roast(to_dev(M_np, torch.float32), 64, 64, seed=HS)
+    a, b = ctx.linear(768, 3072), ctx.linear(3072, 768)
+    sa, sb = OM.LinearSpec(768, 3072, 64, 64, mem, HS, a), OM.LinearSpec(3072, 768, 64, 64, mem, HS, b)
+    X_np = bf16_input(synth.SEED_X, (T, 768))
+    dY_np = bf16_input(synth.SEED_DY, (T, 768))
+    X, dY = to_dev(X_np, torch.bfloat16), to_dev(dY_np, torch.bfloat16)
+    for _ in range(2):
+        ctx.zero_grad()
+        U, A, Y = ctx.fwd_chain_act(a, b, X)
+        dU, dX = ctx.bwd_chain_act(a, b, X, A, U, dY)
+    torch.cuda.synchronize()
+    ctx.check()
+    f = lambda t: t.float().cpu().numpy().astype(np.float64)   # noqa: E731
+    U_np, A_np, dU_np = f(U), f(A), f(dU)
+    rows = slice(None) if T <= 1000 else np.random.default_rng(2).choice(T, 192, replace=False)
+    assert rel_frob(U_np[rows], sa.forward(X_np[rows], M_np, True)) <= 1e-2
+    assert rel_frob(A_np, gelu(U_np)) <= 1e-2
+    assert rel_frob(f(Y)[rows], sb.forward(A_np[rows], M_np, True)) <= 1e-2
+    assert rel_frob(dU_np[rows], sb.backward_dx(dY_np[rows], M_np, True) * gelu_grad(U_np[rows])) <= 1e-2
+    assert rel_frob(f(dX)[rows], sa.backward_dx(dU_np[rows], M_np, True)) <= 1e-2
+    if T <= 1000:   # dM of both layers, the oracle's own dU chain
+        dU_o = sb.backward_dx(dY_np, M_np, True) * gelu_grad(U_np)
+        dM_ref = sb.backward_dm(A_np, dY_np) + sa.backward_dm(X_np, dU_o)
+        assert rel_frob(ctx.dM.cpu().numpy(), dM_ref) <= 1e-2
+    ctx.close()
