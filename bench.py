@@ -23,7 +23,7 @@ one roast_grad_exchange_step); reports t_step split into linears / N-ops / excha
 update and the all-reduce's algbw / busbw.
 
 At N = 1 the default run adds `extra` (about a minute in all): C2 at 10x and 1000x, the
-deterministic C2 step, C4 embeddings (GB/s, HBM fraction), C5's |M| endpoints (8 MB and 2 GB)
+deterministic C2 step, C1's fp32 case, C4 embeddings (GB/s, HBM fraction), C5's |M| endpoints (8 MB and 2 GB)
 against cuBLAS, C3 at 8192 tokens (encoder and whole BERT, ROAST vs dense), per-GEMM ROAST /
 cuBLAS ratios, the oracle at 1 thread and all cores with the CPU model, and the paper's own
 numbers (A100 TF32, context only).
@@ -898,6 +898,10 @@ def c2_extras(torch, dev, args, S, flush, stream, W1, W2):
     except Exception as e:  # noqa: BLE001
         out["c5_sweep_endpoints"] = dict(error=repr(e))
     out["c3_bert_step"] = c3_extra()
+    try:
+        out["c1_fp32"] = c1_extra(torch)
+    except Exception as e:  # noqa: BLE001
+        out["c1_fp32"] = dict(error=repr(e))
     out["paper_context"] = PAPER_CONTEXT
     out["seconds"] = time.perf_counter() - t0
     return out
@@ -957,6 +961,42 @@ def c5_extra(torch, mems=(2 << 20, 512 << 20), T=16384, D=4096):
         del M, ctx
         torch.cuda.empty_cache()
     res["config"] = "C5: 4096 x 4096 ROAST-MM, batch 16384, |M| endpoints of the 8 MB - 2 GB sweep (1 GPU)"
+    return res
+
+
+def c1_extra(torch):
+    """C1 (BASELINE.json configs[0]): one ROAST linear 256 x 256, batch 64, tile 32 x 32, |M| =
+    8192 fp32 (8x), fwd + bwd on the fp32 SIMT path (the oracle-comparison case; its parity is
+    tests/test_gpu_parity.py::test_c1_fp32_path).  Latency-bound: no roofline claim."""
+    import numpy as np
+    import synth
+    R = R_mod()
+    res = {}
+    for det in (False, True):
+        M = torch.tensor(synth.uniform(synth.SEED_M, (8192,)).astype(np.float32), device="cuda")
+        ctx = R.Roast(M, 32, 32, seed=synth.HASH_SEED, deterministic=det, simt_bf16=True)
+        mid = ctx.linear(256, 256)
+        X = torch.tensor(synth.uniform(synth.SEED_X, (64, 256)).astype(np.float32), device="cuda")
+        dY = torch.tensor(synth.uniform(synth.SEED_DY, (64, 256)).astype(np.float32), device="cuda")
+        Y, dX = torch.empty(64, 256, device="cuda"), torch.empty(64, 256, device="cuda")
+
+        def step():
+            ctx.zero_grad()
+            ctx.fwd(mid, X, Y)
+            ctx.bwd(mid, X, dY, dX)
+        g = graph_of(torch, step)
+        for _ in range(10):
+            g.replay()
+        a, b = _events(torch, 2)
+        a.record()
+        for _ in range(200):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        us = a.elapsed_time(b) / 200 * 1e3
+        res["deterministic" if det else "atomic"] = dict(us_per_fwd_bwd=us, gflops=6 * 64 * 256 * 256 / us / 1e3)
+        ctx.close()
+    res["config"] = "C1: 256 x 256 linear, batch 64, tile 32 x 32, |M| = 8192 fp32, fp32 SIMT path (graph replays)"
     return res
 
 
