@@ -1020,6 +1020,15 @@ def c3_extra(timeout=180):
                             linear_eff_tflops=line["linear_eff_tflops"])
         except Exception as e:  # noqa: BLE001
             out[key] = dict(error=repr(e)[:200])
+    try:   # the strong-scaling line's 1-GPU point: 65 536 tokens (bench.py --workload c3)
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "c3", "--steps", "5",
+                            "--warmup", "2", "--no-breakdown"], capture_output=True, text=True, timeout=timeout,
+                           cwd=ROOT, env=dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0"))
+        line = json.loads(r.stdout.strip().splitlines()[-1])
+        out["strong_scaling_1gpu_65536_tokens"] = dict(ms_per_step=line["ms_per_step"], value=line["value"],
+                                                       unit=line["unit"], tokens_per_s=line["tokens_per_s"])
+    except Exception as e:  # noqa: BLE001
+        out["strong_scaling_1gpu_65536_tokens"] = dict(error=repr(e)[:200])
     try:
         out["roast_over_dense_encoder"] = out["encoder_dense"]["ms_per_step"] / out["encoder"]["ms_per_step"]
         out["roast_over_dense_full_bert"] = out["full_bert_dense"]["ms_per_step"] / out["full_bert"]["ms_per_step"]
