@@ -1,4 +1,4 @@
-# full GPU suite, smoke, default bench line with extras, C3 65 536-token line
+# GPU validation of a round: full -m gpu suite, smoke(), the default bench line with extras, C3 at 65 536 tokens
 mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; tail -2 gpurun_out/gpu_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
