@@ -130,3 +130,35 @@ def test_fused_chain_act_matches_oracle(R, torch, T):
         dM_ref = sb.backward_dm(A_np, dY_np) + sa.backward_dm(X_np, dU_o)
         assert rel_frob(ctx.dM.cpu().numpy(), dM_ref) <= 1e-2
     ctx.close()
+
+
+def test_fused_gelu_shape_fuzz(R, torch):
+    """Seeded random geometries through the fused-activation epilogues (both unit widths the tuner
+    may pick, ragged tokens, small and odd tile counts, |M| small enough for shadow replicas):
+    act(Y) and (dY W^T) * act'(U) against the oracle."""
+    rng = np.random.default_rng(77)
+    for case in range(8):
+        mem = int(rng.choice([4720, 60_000]))
+        M_np = store(mem)
+        ctx = R.Roast(to_dev(M_np, torch.float32), 64, 64, seed=HS)
+        H = 64 * int(rng.integers(1, 20))
+        O = 192 * int(rng.integers(1, 8)) if rng.random() < 0.5 else 64 * int(rng.integers(1, 25))
+        T = int(rng.integers(1, 3000))
+        mid = ctx.linear(H, O)
+        spec = OM.LinearSpec(H, O, 64, 64, mem, HS, mid)
+        X_np = bf16_input(synth.SEED_X + case, (T, H))
+        dY_np = bf16_input(synth.SEED_DY + case, (T, O))
+        U_in = bf16_input(synth.SEED_X + 100 + case, (T, H))
+        X, dY, Uin = to_dev(X_np, torch.bfloat16), to_dev(dY_np, torch.bfloat16), to_dev(U_in, torch.bfloat16)
+        for _ in range(2):
+            U, A = ctx.fwd_act(mid, X)
+            dX = ctx.bwd_dx_act(mid, dY, Uin)
+        torch.cuda.synchronize()
+        ctx.check()
+        where = (case, mem, H, O, T)
+        U_np = U.float().cpu().numpy().astype(np.float64)
+        assert rel_frob(U_np, spec.forward(X_np, M_np, True)) <= 1e-2, where
+        assert rel_frob(A.float().cpu().numpy(), gelu(U_np)) <= 1e-2, where
+        ref = spec.backward_dx(dY_np, M_np, True) * gelu_grad(U_in.astype(np.float64))
+        assert rel_frob(dX.float().cpu().numpy(), ref) <= 1e-2, where
+        ctx.close()
