@@ -1149,7 +1149,7 @@ def run_gpu_c3(args):
             elif "memset" not in n.lower() and "memcpy" not in n.lower():
                 cats["n_ops"] += t
         top = sorted(((getattr(ev, "device_time_total", getattr(ev, "cuda_time_total", 0.0)) / 1e3, ev.key)
-                      for ev in prof.key_averages()), reverse=True)[:10]
+                      for ev in prof.key_averages()), reverse=True)[:20]
         breakdown = dict(ms={k: round(v, 4) for k, v in cats.items()},
                          top_kernels_ms=[[round(t, 4), k[:80]] for t, k in top],
                          note="one eager step under torch.profiler: kernel time by category (launch gaps "

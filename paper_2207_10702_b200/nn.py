@@ -221,8 +221,9 @@ class RoastEmbedding(torch.nn.Module):
 
 try:   # attention is an N-op of the BERT workload: library kernels, as cuBLAS would be
     from flash_attn import flash_attn_func as _flash_attn
+    from flash_attn import flash_attn_qkvpacked_func as _flash_attn_packed
 except Exception:  # noqa: BLE001
-    _flash_attn = None
+    _flash_attn = _flash_attn_packed = None
 
 
 def _cdt(t):
@@ -298,21 +299,35 @@ class EncoderLayer(torch.nn.Module):
         # (registration order and hashes unchanged; the group id lives outside the module ids)
         self.qkv_gid = store.linear_concat([self.q.mid, self.k.mid, self.v.mid]) if fuse_qkv else None
 
-    def _qkv(self, x):
-        """(q, k, v) projections: fused ROAST group, a fused dense Linear, or three calls."""
-        d = x.shape[-1]
+    def _qkv_packed(self, x):
+        """[q | k | v] as one [.., 3 d] tensor (the fused ROAST group or dense Linear), else None."""
         dense = getattr(self, "qkv_dense", None)
         if dense is not None:
-            return dense(x).split(d, dim=-1)
+            return dense(x)
         if getattr(self, "qkv_gid", None) is not None:
             bias = tuple(lin.bias.mid for lin in (self.q, self.k, self.v)) if self.q.bias is not None else ()
-            return _LinearGroupFn.apply(x, _anchor(self.q.store), self.q.store, self.qkv_gid, bias).split(d, dim=-1)
+            return _LinearGroupFn.apply(x, _anchor(self.q.store), self.q.store, self.qkv_gid, bias)
+        return None
+
+    def _qkv(self, x):
+        """(q, k, v) projections: fused ROAST group, a fused dense Linear, or three calls."""
+        packed = self._qkv_packed(x)
+        if packed is not None:
+            return packed.split(x.shape[-1], dim=-1)
         return self.q(x), self.k(x), self.v(x)
 
     def forward(self, x):                   # x: [B, S, d]
         B, S, d = x.shape
         h = self.heads
 
+        packed = self._qkv_packed(x) if _flash_attn_packed is not None and x.is_cuda and \
+            x.dtype == torch.bfloat16 else None
+        if packed is not None:
+            # the packed QKV GEMM output viewed as [B, S, 3, heads, d_head]: flash-attn's packed form
+            # returns d(qkv) packed too (no concatenation of dq, dk, dv in the backward)
+            a = _flash_attn_packed(packed.view(B, S, 3, h, d // h)).reshape(B, S, d)
+            x = self.ln1(self.o(a), x)
+            return self.ln2(mlp(self.ff1, self.ff2, x), x)
         q, k, v = self._qkv(x)
         if _flash_attn is not None and x.is_cuda and x.dtype == torch.bfloat16:
             # flash-attn (library kernel) reads [B, S, heads, d_head] strided views of the QKV

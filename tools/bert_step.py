@@ -39,6 +39,7 @@ class DenseLayer(torch.nn.Module):
 
     forward = RN.EncoderLayer.forward
     _qkv = RN.EncoderLayer._qkv
+    _qkv_packed = RN.EncoderLayer._qkv_packed
     heads = HEADS
 
 
