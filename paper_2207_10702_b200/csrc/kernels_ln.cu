@@ -5,9 +5,11 @@
 //   forward  : s = x (+ r, the residual, fused), mean / rstd per row, y = (s - mean) rstd g + b
 //   backward : xhat = (s - mean) rstd, dxhat = dy g,
 //              ds = rstd (dxhat - mean(dxhat) - xhat mean(dxhat xhat)),
-//              dg = sum_rows dy xhat, db = sum_rows dy  (per-warp partials, then a fixed-order
-//              reduce: bitwise reproducible)
-// One warp per row; lane l holds the 8-element vectors l, l + 32, ... of the row in registers.
+//              dg = sum_rows dy xhat, db = sum_rows dy  (per-warp partials in registers, then a
+//              fixed-order reduce: bitwise reproducible)
+// One warp per row; lane l holds the 8-element vectors l, l + 32, ... of the row in registers;
+// each warp keeps its next rows' loads in flight (forward: two rows at once, backward: the next
+// row prefetched), which is what brings these HBM-bound passes near the copy bandwidth.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -62,7 +64,42 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-template <class T, class P, int VPL>
+// The row data as loaded (raw) and widened to fp32 on use, so a warp can keep the next rows' loads
+// in flight while it works on the current ones.
+template <class T>
+struct Raw8;
+template <>
+struct Raw8<__nv_bfloat16> {
+  uint4 u;
+  template <bool CS = false>   // CS: streaming (evict-first) load
+  __device__ __forceinline__ void load(const __nv_bfloat16* p) {
+    u = CS ? __ldcs(reinterpret_cast<const uint4*>(p)) : *reinterpret_cast<const uint4*>(p);
+  }
+  __device__ __forceinline__ void get(float* f) const {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 t = __bfloat1622float2(h[k]);
+      f[2 * k] = t.x;
+      f[2 * k + 1] = t.y;
+    }
+  }
+};
+template <>
+struct Raw8<float> {
+  float4 a, b;
+  template <bool CS = false>
+  __device__ __forceinline__ void load(const float* p) {
+    a = CS ? __ldcs(reinterpret_cast<const float4*>(p)) : *reinterpret_cast<const float4*>(p);
+    b = CS ? __ldcs(reinterpret_cast<const float4*>(p + 4)) : *reinterpret_cast<const float4*>(p + 4);
+  }
+  __device__ __forceinline__ void get(float* f) const {
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  }
+};
+
+// Forward: one warp per row, R rows of a warp in flight at once (their loads issued together).
+template <class T, class P, int VPL, int R>
 __global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ r,
                                                     const P* __restrict__ g, const P* __restrict__ b,
                                                     T* __restrict__ y, T* __restrict__ s_out,
@@ -71,89 +108,123 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ x, co
   const int lane = threadIdx.x & 31;
   const int nv = n >> 3;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; row < rows; row += nwarps) {
-    float v[VPL][8];
-    float sum = 0.f;
+  for (int64_t row0 = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * R; row0 < rows;
+       row0 += nwarps * R) {
+    Raw8<T> rx[R][VPL], rr[R][VPL];
 #pragma unroll
-    for (int k = 0; k < VPL; ++k) {
-      const int c = (lane + 32 * k) * 8;
-      if (lane + 32 * k < nv) {
-        Vec8<T>::load(x + row * n + c, v[k]);
-        if (r) {
-          float t[8];
-          Vec8<T>::load(r + row * n + c, t);
+    for (int q = 0; q < R; ++q)
 #pragma unroll
-          for (int e = 0; e < 8; ++e) v[k][e] += t[e];
-          Vec8<T>::round(v[k]);   // the stored (rounded) sum is the LN input, as the backward sees it
-          Vec8<T>::store(s_out + row * n + c, v[k]);
+      for (int k = 0; k < VPL; ++k)
+        if (row0 + q < rows && lane + 32 * k < nv) {
+          const int64_t o = (row0 + q) * n + (lane + 32 * k) * 8;
+          // two rows in flight = the large-row-count case, whose inputs are not L2-resident:
+          // streaming loads leave L2 to the stores (65 536 x 768: 72 vs 114 us with plain loads)
+          rx[q][k].template load<(R > 1)>(x + o);
+          if (r) rr[q][k].template load<(R > 1)>(r + o);
         }
 #pragma unroll
-        for (int e = 0; e < 8; ++e) sum += v[k][e];
-      }
-    }
-    const float mean = warp_sum(sum) / float(n);
-    float sq = 0.f;
+    for (int q = 0; q < R; ++q) {
+      const int64_t row = row0 + q;
+      if (row >= rows) break;
+      float v[VPL][8];
+      float sum = 0.f;
 #pragma unroll
-    for (int k = 0; k < VPL; ++k)
-      if (lane + 32 * k < nv)
+      for (int k = 0; k < VPL; ++k) {
+        const int c = (lane + 32 * k) * 8;
+        if (lane + 32 * k < nv) {
+          rx[q][k].get(v[k]);
+          if (r) {
+            float t[8];
+            rr[q][k].get(t);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float d = v[k][e] - mean;
-          sq += d * d;
+            for (int e = 0; e < 8; ++e) v[k][e] += t[e];
+            Vec8<T>::round(v[k]);   // the stored (rounded) sum is the LN input, as the backward sees it
+            Vec8<T>::store(s_out + row * n + c, v[k]);
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) sum += v[k][e];
         }
-    const float rstd = rsqrtf(warp_sum(sq) / float(n) + eps);
-#pragma unroll
-    for (int k = 0; k < VPL; ++k) {
-      const int c = (lane + 32 * k) * 8;
-      if (lane + 32 * k < nv) {
-        float gg[8], bb[8], o[8];
-        Vec8<P>::load(g + c, gg);
-        Vec8<P>::load(b + c, bb);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = (v[k][e] - mean) * rstd * gg[e] + bb[e];
-        Vec8<T>::store(y + row * n + c, o);
       }
-    }
-    if (lane == 0) {
-      mean_out[row] = mean;
-      rstd_out[row] = rstd;
+      const float mean = warp_sum(sum) / float(n);
+      float sq = 0.f;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k)
+        if (lane + 32 * k < nv)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float d = v[k][e] - mean;
+            sq += d * d;
+          }
+      const float rstd = rsqrtf(warp_sum(sq) / float(n) + eps);
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        const int c = (lane + 32 * k) * 8;
+        if (lane + 32 * k < nv) {
+          float gg[8], bb[8], o[8];
+          Vec8<P>::load(g + c, gg);
+          Vec8<P>::load(b + c, bb);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o[e] = (v[k][e] - mean) * rstd * gg[e] + bb[e];
+          Vec8<T>::store(y + row * n + c, o);
+        }
+      }
+      if (lane == 0) {
+        mean_out[row] = mean;
+        rstd_out[row] = rstd;
+      }
     }
   }
 }
 
-// backward, pass 1: ds per row, and per-warp partial sums of dy xhat / dy over the warp's rows
-// (rows w, w + nwarps, ... in that order), kept in the warp's slice of shared memory (each lane
-// owns its columns: no atomics); at the end the block's 8 warps are combined in warp order and
-// written to part[block][2][n]
-template <class T, class P, int VPL>
-__global__ void __launch_bounds__(256) ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ s,
-                                                    const P* __restrict__ g, const float* __restrict__ mean_in,
-                                                    const float* __restrict__ rstd_in, T* __restrict__ ds,
-                                                    float* __restrict__ part, int64_t rows, int n) {
-  extern __shared__ float acc_sm[];   // [8 warps][2][n]
+// Backward, pass 1.  Warp w of the grid owns the contiguous rows [w rpw, (w + 1) rpw): per row ds,
+// and the warp's partial sums of dy xhat / dy in registers (lane l owns the columns of vectors
+// l, l + 32, ...: no atomics, no shared-memory traffic per row); the next row's dy / s are loaded
+// while the current one is processed (VPL <= 4).  At the end the block's LN_BWD_WARPS warps are
+// combined in warp order and written to part[block][2][n].
+constexpr int LN_BWD_WARPS = 12;   // one block per SM: 12 warps x ~140 registers
+template <class T, class P, int VPL, bool CS>
+__global__ void __launch_bounds__(LN_BWD_WARPS * 32, 1) ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ s,
+                                                       const P* __restrict__ g, const float* __restrict__ mean_in,
+                                                       const float* __restrict__ rstd_in, T* __restrict__ ds,
+                                                       float* __restrict__ part, int64_t rows, int n, int64_t rpw) {
+  extern __shared__ float acc_sm[];   // [LN_BWD_WARPS][2][n], used once at the end
+  constexpr bool PF = VPL <= 4;       // prefetch the next row (register budget)
   const int lane = threadIdx.x & 31;
   const int nv = n >> 3;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  float* pg = acc_sm + (threadIdx.x >> 5) * 2 * n;
-  float* pb = pg + n;
-  for (int c = lane; c < n; c += 32) {
-    pg[c] = 0.f;
-    pb[c] = 0.f;
-  }
-  __syncwarp();
-  for (int64_t row = warp; row < rows; row += nwarps) {
-    const float mean = mean_in[row], rstd = rstd_in[row];
-    float xh[VPL][8], d[VPL][8];
-    float s1 = 0.f, s2 = 0.f;
+  const int64_t r0 = warp * rpw, r1 = min(rows, r0 + rpw);
+  float ag[VPL][8], ab[VPL][8];
 #pragma unroll
-    for (int k = 0; k < VPL; ++k) {
-      const int c = (lane + 32 * k) * 8;
-      if (lane + 32 * k < nv) {
-        Vec8<T>::load(s + row * n + c, xh[k]);
-        Vec8<T>::load(dy + row * n + c, d[k]);
-      }
+  for (int k = 0; k < VPL; ++k)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ag[k][e] = ab[k][e] = 0.f;
+  Raw8<T> ns[VPL], nd[VPL];   // the next row's s, dy
+  float nmean = 0.f, nrstd = 0.f;
+  auto fetch = [&](int64_t row) {
+    if (row < r1) {
+#pragma unroll
+      for (int k = 0; k < VPL; ++k)
+        if (lane + 32 * k < nv) {
+          ns[k].template load<CS>(s + row * n + (lane + 32 * k) * 8);
+          nd[k].template load<CS>(dy + row * n + (lane + 32 * k) * 8);
+        }
+      nmean = mean_in[row];
+      nrstd = rstd_in[row];
     }
+  };
+  if (PF) fetch(r0);
+  for (int64_t row = r0; row < r1; ++row) {
+    if (!PF) fetch(row);
+    float xh[VPL][8], d[VPL][8];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k)
+      if (lane + 32 * k < nv) {
+        ns[k].get(xh[k]);
+        nd[k].get(d[k]);
+      }
+    const float mean = nmean, rstd = nrstd;
+    if (PF) fetch(row + 1);
+    float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
       const int c = (lane + 32 * k) * 8;
@@ -163,8 +234,8 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const T* __restrict__ dy, c
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           xh[k][e] = (xh[k][e] - mean) * rstd;
-          pg[e * nv + lane + 32 * k] += d[k][e] * xh[k][e];   // [e][vector]: conflict-free
-          pb[e * nv + lane + 32 * k] += d[k][e];
+          ag[k][e] += d[k][e] * xh[k][e];
+          ab[k][e] += d[k][e];
           d[k][e] *= gg[e];   // dxhat
           s1 += d[k][e];
           s2 += d[k][e] * xh[k][e];
@@ -183,12 +254,21 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const T* __restrict__ dy, c
       }
     }
   }
-  // the block's 8 warp partials combined in warp order, one partial row pair per block
+  // the block's warp partials combined in warp order, one partial row pair per block
+  float* pg = acc_sm + (threadIdx.x >> 5) * 2 * n;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k)
+    if (lane + 32 * k < nv)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        pg[e * nv + lane + 32 * k] = ag[k][e];   // [e][vector]: conflict-free
+        pg[n + e * nv + lane + 32 * k] = ab[k][e];
+      }
   __syncthreads();
   for (int c = threadIdx.x; c < n; c += blockDim.x) {   // column c = vector c / 8, element c % 8
     const int e = (c & 7) * nv + (c >> 3);
     float a = acc_sm[e], b = acc_sm[n + e];
-    for (int w = 1; w < 8; ++w) {
+    for (int w = 1; w < LN_BWD_WARPS; ++w) {
       a += acc_sm[w * 2 * n + e];
       b += acc_sm[w * 2 * n + n + e];
     }
@@ -198,30 +278,23 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const T* __restrict__ dy, c
 }
 
 // backward, pass 2: dg[c] = sum_w part[w][0][c], db[c] = sum_w part[w][1][c] in a fixed order:
-// thread (ty, tx) of a 32-column block (32 x 32 threads) sums warps ty, ty + 32, ... then the 32
-// partials are added in ty order
+// block (x, y) handles 32 columns of dg (y = 0) or db (y = 1); thread (ty, tx) sums partial rows
+// ty, ty + 32, ... then the 32 partials are added in ty order
 __global__ void __launch_bounds__(1024) ln_param_reduce_kernel(const float* __restrict__ part, int64_t nw, int n,
                                                               float* __restrict__ dg, float* __restrict__ db) {
-  __shared__ float sh[2][32][33];
+  __shared__ float sh[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + tx;
-  float a = 0.f, b = 0.f;
+  const int which = blockIdx.y;
+  float a = 0.f;
   if (c < n)
-    for (int64_t w = ty; w < nw; w += 32) {
-      a += part[(w * 2) * n + c];
-      b += part[(w * 2 + 1) * n + c];
-    }
-  sh[0][ty][tx] = a;
-  sh[1][ty][tx] = b;
+    for (int64_t w = ty; w < nw; w += 32) a += part[(w * 2 + which) * n + c];
+  sh[ty][tx] = a;
   __syncthreads();
   if (ty == 0 && c < n) {
-    float ta = sh[0][0][tx], tb = sh[1][0][tx];
-    for (int k = 1; k < 32; ++k) {
-      ta += sh[0][k][tx];
-      tb += sh[1][k][tx];
-    }
-    dg[c] = ta;
-    db[c] = tb;
+    float t = sh[0][tx];
+    for (int k = 1; k < 32; ++k) t += sh[k][tx];
+    (which ? db : dg)[c] = t;
   }
 }
 
@@ -229,11 +302,22 @@ template <class T, class P>
 cudaError_t ln_fwd_launch(const void* x, const void* r, const void* g, const void* b, void* y, void* s_out,
                           float* mean, float* rstd, int64_t rows, int n, float eps, cudaStream_t st) {
   const int vpl = (n / 8 + 31) / 32;
-  const unsigned blocks = unsigned(std::min<int64_t>((rows + 7) / 8, 148 * 16));
+  // two rows in flight per warp for bf16 rows when there are enough rows to fill the grid twice
+  // over (65 536 x 768: 90 -> 72 us); one below that (8192 x 768: 10.5 vs 12.4 us)
+  const bool two = sizeof(T) == 2 && vpl <= 4 && rows >= 32768;
+  const int rr = two ? 2 : 1;
+  const unsigned blocks = unsigned(std::min<int64_t>((rows + 8 * rr - 1) / (8 * rr), 148 * 8));
 #define ROAST_LN_FWD(V)                                                                                         \
-  ln_fwd_kernel<T, P, V><<<blocks, 256, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(r),             \
-                                                 static_cast<const P*>(g), static_cast<const P*>(b),             \
-                                                 static_cast<T*>(y), static_cast<T*>(s_out), mean, rstd, rows, n, eps)
+  if (two && V <= 4)                                                                                            \
+    ln_fwd_kernel<T, P, V, (V <= 4 ? 2 : 1)><<<blocks, 256, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(r),        \
+                                                      static_cast<const P*>(g), static_cast<const P*>(b),        \
+                                                      static_cast<T*>(y), static_cast<T*>(s_out), mean, rstd,    \
+                                                      rows, n, eps);                                             \
+  else                                                                                                          \
+    ln_fwd_kernel<T, P, V, 1><<<blocks, 256, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(r),        \
+                                                      static_cast<const P*>(g), static_cast<const P*>(b),        \
+                                                      static_cast<T*>(y), static_cast<T*>(s_out), mean, rstd,    \
+                                                      rows, n, eps)
   switch (vpl) {
     case 1: ROAST_LN_FWD(1); break;
     case 2: ROAST_LN_FWD(2); break;
@@ -248,17 +332,49 @@ cudaError_t ln_fwd_launch(const void* x, const void* r, const void* g, const voi
   return cudaGetLastError();
 }
 
+// pass-1 geometry for `rows`: a fixed function of (rows, device SMs), so the reduce order, and
+// with it every parameter gradient bit, depends on nothing else
+struct LnBwdGrid {
+  int64_t rpw, blocks;
+};
+LnBwdGrid ln_bwd_grid(int64_t rows) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int64_t max_warps = int64_t(sms) * LN_BWD_WARPS;   // one block per SM
+  const int64_t rpw = std::max<int64_t>(1, (rows + max_warps - 1) / max_warps);
+  const int64_t warps = std::max<int64_t>(1, (rows + rpw - 1) / rpw);
+  return {rpw, (warps + LN_BWD_WARPS - 1) / LN_BWD_WARPS};
+}
+
 template <class T, class P>
 cudaError_t ln_bwd_launch(const void* dy, const void* s, const void* g, const float* mean, const float* rstd, void* ds,
-                          float* part, int64_t nw, int64_t rows, int n, cudaStream_t st) {
+                          float* part, const LnBwdGrid& gr, int64_t rows, int n, cudaStream_t st) {
   const int vpl = (n / 8 + 31) / 32;
-  const unsigned blocks = unsigned(nw / 8);
-  const size_t smem = 16 * size_t(n) * sizeof(float);   // 8 warps x (dg, db) partials
-#define ROAST_LN_BWD(V)                                                                                        \
-  cudaFuncSetAttribute(ln_bwd_kernel<T, P, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));          \
-  ln_bwd_kernel<T, P, V><<<blocks, 256, smem, st>>>(static_cast<const T*>(dy), static_cast<const T*>(s),           \
-                                                 static_cast<const P*>(g), mean, rstd, static_cast<T*>(ds), part, \
-                                                 rows, n)
+  const size_t smem = 2 * LN_BWD_WARPS * size_t(n) * sizeof(float);   // per warp (dg, db) partials
+  const bool cs = rows >= 32768;   // inputs not L2-resident: streaming loads
+  // the smem opt-in once per instantiation (at the largest n): cudaFuncSetAttribute on every call
+  // cost ~50 us of host time and stalled the stream behind the kernel's previous launch
+#define ROAST_LN_BWD_CS(V, CSV)                                                                                \
+  {                                                                                                             \
+    static bool opted = false;                                                                                  \
+    if (!opted)                                                                                                 \
+      opted = cudaFuncSetAttribute(ln_bwd_kernel<T, P, V, CSV>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                   int(2 * LN_BWD_WARPS * 2048 * sizeof(float))) == cudaSuccess;                \
+  }                                                                                                             \
+  ln_bwd_kernel<T, P, V, CSV><<<unsigned(gr.blocks), LN_BWD_WARPS * 32, smem, st>>>(                           \
+      static_cast<const T*>(dy), static_cast<const T*>(s), static_cast<const P*>(g), mean, rstd,               \
+      static_cast<T*>(ds), part, rows, n, gr.rpw)
+#define ROAST_LN_BWD(V)       \
+  if (cs) {                   \
+    ROAST_LN_BWD_CS(V, true);  \
+  } else {                    \
+    ROAST_LN_BWD_CS(V, false); \
+  }
   switch (vpl) {
     case 1: ROAST_LN_BWD(1); break;
     case 2: ROAST_LN_BWD(2); break;
@@ -270,6 +386,7 @@ cudaError_t ln_bwd_launch(const void* dy, const void* s, const void* g, const fl
     default: ROAST_LN_BWD(8); break;
   }
 #undef ROAST_LN_BWD
+#undef ROAST_LN_BWD_CS
   return cudaGetLastError();
 }
 
@@ -308,24 +425,27 @@ roast_status_t roast_layernorm_bwd(const void* dy, const void* s_in, const void*
   if (!dy || !s_in || !gamma || !mean || !rstd || !ds || !dgamma || !dbeta)
     return fail(ROAST_ERR_CONFIG, "layernorm: null pointer");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  // warps of pass 1 (a fixed grid for a given row count: the reduce order is data-independent);
-  // each leaves 2 n partials
-  // ~4 rows per warp, at most one resident wave of 148 x 4 blocks; the reduce reads one partial
-  // row pair per block
-  const int64_t nw = std::max<int64_t>(8, std::min<int64_t>((rows / 4 + 7) / 8 * 8, int64_t(148) * 4 * 8));
+  // pass 1's grid is a fixed function of the row count (ln_bwd_grid): the reduce order is
+  // data-independent; each block leaves 2 n partials
+  if (rows == 0) {
+    ROAST_CUDA_CHECK(cudaMemsetAsync(dgamma, 0, size_t(n) * sizeof(float), s));
+    ROAST_CUDA_CHECK(cudaMemsetAsync(dbeta, 0, size_t(n) * sizeof(float), s));
+    return ROAST_OK;
+  }
+  const LnBwdGrid gr = ln_bwd_grid(rows);
   Scratch ws;
-  if (roast_status_t st = scratch_alloc(ws, size_t(nw / 8) * 2 * size_t(n) * sizeof(float), s)) return st;
+  if (roast_status_t st = scratch_alloc(ws, size_t(gr.blocks) * 2 * size_t(n) * sizeof(float), s)) return st;
   cudaError_t e;
   if (dt == ROAST_BF16 && pdt == ROAST_BF16)
-    e = ln_bwd_launch<__nv_bfloat16, __nv_bfloat16>(dy, s_in, gamma, mean, rstd, ds, ws.as<float>(), nw, rows, n, s);
+    e = ln_bwd_launch<__nv_bfloat16, __nv_bfloat16>(dy, s_in, gamma, mean, rstd, ds, ws.as<float>(), gr, rows, n, s);
   else if (dt == ROAST_BF16)
-    e = ln_bwd_launch<__nv_bfloat16, float>(dy, s_in, gamma, mean, rstd, ds, ws.as<float>(), nw, rows, n, s);
+    e = ln_bwd_launch<__nv_bfloat16, float>(dy, s_in, gamma, mean, rstd, ds, ws.as<float>(), gr, rows, n, s);
   else if (pdt == ROAST_BF16)
-    e = ln_bwd_launch<float, __nv_bfloat16>(dy, s_in, gamma, mean, rstd, ds, ws.as<float>(), nw, rows, n, s);
+    e = ln_bwd_launch<float, __nv_bfloat16>(dy, s_in, gamma, mean, rstd, ds, ws.as<float>(), gr, rows, n, s);
   else
-    e = ln_bwd_launch<float, float>(dy, s_in, gamma, mean, rstd, ds, ws.as<float>(), nw, rows, n, s);
+    e = ln_bwd_launch<float, float>(dy, s_in, gamma, mean, rstd, ds, ws.as<float>(), gr, rows, n, s);
   ROAST_CUDA_CHECK(e);
-  ln_param_reduce_kernel<<<unsigned((n + 31) / 32), 1024, 0, s>>>(ws.as<float>(), nw / 8, n, dgamma, dbeta);
+  ln_param_reduce_kernel<<<dim3(unsigned((n + 31) / 32), 2), 1024, 0, s>>>(ws.as<float>(), gr.blocks, n, dgamma, dbeta);
   ROAST_CUDA_CHECK(cudaGetLastError());
   return ROAST_OK;
 }

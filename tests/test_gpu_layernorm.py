@@ -19,7 +19,8 @@ def _rel(a, b):
 
 @pytest.mark.parametrize("dtype,n,rows,resid", [("bf16", 768, 4099, True), ("bf16", 768, 3, False),
                                                 ("fp32", 1024, 777, True), ("fp32", 2048, 64, False),
-                                                ("bf16", 8, 1000, True)])
+                                                ("bf16", 8, 1000, True), ("bf16", 768, 70001, True),
+                                                ("fp32", 768, 5000, False), ("bf16", 2048, 3001, True)])
 def test_layernorm_matches_torch(torch, dtype, n, rows, resid):
     from paper_2207_10702_b200 import nn as RN
     dt = torch.bfloat16 if dtype == "bf16" else torch.float32
