@@ -271,8 +271,11 @@ roast_status_t roast_colsum_ex(const void* d_dY, int64_t tokens, int32_t n, int6
  *   the stored (bf16-rounded) Y, both [tokens x out_features] bf16; A 16-byte aligned.
  * roast_linear_bwd_dx_act: dX = bf16(lambda dY W~^T) * act'(U) elementwise, U [tokens x
  *   in_features] bf16 the pre-activation whose act(U) was this layer's input (so dX is the
- *   gradient with respect to U).  No dM: pair it with roast_linear_bwd_dm(X = act(U)). */
-typedef enum { ROAST_ACT_NONE = 0, ROAST_ACT_GELU_TANH = 1 } roast_act_t;
+ *   gradient with respect to U).  No dM: pair it with roast_linear_bwd_dm(X = act(U)).
+ *   act = ROAST_ACT_RESIDUAL (this call only): U is R, the gradient the layer input also
+ *   receives through a residual connection, and dX = bf16(bf16(lambda dY W~^T) + R) — the bits
+ *   of the dX GEMM followed by a separate bf16 add, in one pass (U may alias dX). */
+typedef enum { ROAST_ACT_NONE = 0, ROAST_ACT_GELU_TANH = 1, ROAST_ACT_RESIDUAL = 2 } roast_act_t;
 roast_status_t roast_linear_fwd_act(roast_t h, int32_t id, const void* d_X, void* d_Y, void* d_A, int64_t tokens,
                                     roast_dtype_t dt, const float* d_bias, int32_t act, roast_stream_t stream);
 roast_status_t roast_linear_bwd_dx_act(roast_t h, int32_t id, const void* d_dY, const void* d_U, void* d_dX,

@@ -741,7 +741,8 @@ roast_status_t roast_linear_bwd_dx_act(roast_t h, int32_t id, const void* dY, co
   Module* m;
   roast_status_t st = linear_args(c, id, T, dt, dY, dX, &m);
   if (st || T == 0) return st;
-  if (act != ROAST_ACT_GELU_TANH) return fail(ROAST_ERR_CONFIG, "act: ROAST_ACT_GELU_TANH");
+  if (act != ROAST_ACT_GELU_TANH && act != ROAST_ACT_RESIDUAL)
+    return fail(ROAST_ERR_CONFIG, "act: ROAST_ACT_GELU_TANH or ROAST_ACT_RESIDUAL");
   if (!U || (reinterpret_cast<uintptr_t>(U) & 15)) return fail(ROAST_ERR_CONFIG, "U null or not 16-byte aligned");
   if (dt != ROAST_BF16 || !use_sm100(c, *m))
     return fail(ROAST_ERR_UNSUPPORTED, "fused activation: bf16 on the tcgen05 path only");

@@ -709,7 +709,9 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const float2 d = unpack_bf2(pk[c * 32 + 4 * cc + e]), x = unpack_bf2(uw[e]);
-                pk[c * 32 + 4 * cc + e] = pack_bf2(d.x * gelu_tanh_grad(x.x), d.y * gelu_tanh_grad(x.y));
+                // act 2 (residual): dX = bf16(bf16(dh) + R), the bits of a separate bf16 add
+                pk[c * 32 + 4 * cc + e] = p.act == 2 ? pack_bf2(d.x + x.x, d.y + x.y)
+                                                     : pack_bf2(d.x * gelu_tanh_grad(x.x), d.y * gelu_tanh_grad(x.y));
               }
             }
             __syncwarp();   // every row read before the buffer is overwritten with dX

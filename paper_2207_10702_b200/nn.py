@@ -9,6 +9,8 @@ marshalling only — all compute runs in libroast's kernels.
 """
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import roast as R
@@ -23,6 +25,52 @@ def _anchor(store):
         a = torch.zeros((), device=store.M.device, requires_grad=True)
         store._autograd_anchor = a
     return a
+
+
+class ResidualGrad:
+    """Hand-off of a residual connection's gradient to the GEMM that produces the same input's
+    other gradient.  In y = LayerNorm(f(x) + x) the input x receives ds (through the residual) and
+    f's input gradient; instead of autograd adding the two (a separate bf16 add over the whole
+    activation), the LayerNorm backward leaves ds here and f's first linear writes
+    dX = bf16(dX_gemm) + ds in its dX GEMM's epilogue (roast_linear_bwd_dx_act, ROAST_ACT_RESIDUAL:
+    the same bits).  The LayerNorm backward always runs first: f's backward needs its output."""
+
+    __slots__ = ("ds",)
+
+    def __init__(self):
+        self.ds = None
+
+    def take(self):
+        ds, self.ds = self.ds, None
+        return ds
+
+
+# the fused residual add pays for itself once the dX launch has several units per CTA pair (its
+# epilogue then overlaps the next unit's MMAs): tools/act_probe.py, 768-wide dX GEMMs, vs the plain
+# dX GEMM + a bf16 add: T = 65 536 234 vs 270 us (ff1), 177 vs 215 us (QKV); T = 8192 51 vs 48 us
+RESIDUAL_FUSE_MIN_TOKENS = 32768
+
+
+def _dx_plus_residual(store, mid, dy2, box, like):
+    """dX of module `mid` for dy2, plus the residual gradient left in `box` (fused when possible)."""
+    r = box.take() if box is not None else None
+    if r is not None and like.shape[0] < RESIDUAL_FUSE_MIN_TOKENS:
+        dx = torch.empty_like(like)
+        store.bwd_dx(mid, dy2, dx)
+        return dx.add_(r.reshape(like.shape))
+    if r is not None:
+        r2 = r.reshape(like.shape).contiguous()
+        try:
+            return store.bwd_dx_act(mid, dy2, r2, act=R.ACT_RESIDUAL)
+        except R.RoastError as e:
+            if e.status != R.ERR_UNSUPPORTED:
+                raise
+            dx = torch.empty_like(like)
+            store.bwd_dx(mid, dy2, dx)
+            return dx + r2
+    dx = torch.empty_like(like)
+    store.bwd_dx(mid, dy2, dx)
+    return dx
 
 
 class _LinearFn(torch.autograd.Function):
@@ -61,13 +109,13 @@ class _LinearGroupFn(torch.autograd.Function):
     each member bias's backward reads its column slice of dY in place."""
 
     @staticmethod
-    def forward(ctx, x, anchor, store, gid, bias_mids):
+    def forward(ctx, x, anchor, store, gid, bias_mids, box=None):
         H = store.dims[gid][1]
         x2 = x.reshape(-1, H).contiguous()
         b = torch.cat([store.bias_vector(m) for m in bias_mids]) if bias_mids else None
         y = store.fwd(gid, x2, bias=b)
         ctx.save_for_backward(x2)
-        ctx.store, ctx.gid, ctx.bias_mids, ctx.shape = store, gid, bias_mids, x.shape
+        ctx.store, ctx.gid, ctx.bias_mids, ctx.shape, ctx.box = store, gid, bias_mids, x.shape, box
         return y.reshape(*x.shape[:-1], y.shape[-1])
 
     @staticmethod
@@ -77,8 +125,7 @@ class _LinearGroupFn(torch.autograd.Function):
         dy2 = dy.reshape(x2.shape[0], -1).contiguous().to(x2.dtype)
         dx = None
         if ctx.needs_input_grad[0]:
-            dx = torch.empty_like(x2)
-            store.bwd_dx(gid, dy2, dx)
+            dx = _dx_plus_residual(store, gid, dy2, ctx.box, x2)   # + the residual gradient, if handed off
         store.bwd_dm(gid, x2, dy2)
         if ctx.bias_mids:
             c0 = 0
@@ -86,7 +133,7 @@ class _LinearGroupFn(torch.autograd.Function):
                 n = store.dims[m][2]
                 store.bias_grad(m, dy2[:, c0:c0 + n])
                 c0 += n
-        return (dx.reshape(ctx.shape) if dx is not None else None), None, None, None, None
+        return (dx.reshape(ctx.shape) if dx is not None else None), None, None, None, None, None
 
 
 def gelu(x):
@@ -110,7 +157,7 @@ class _MLPFn(torch.autograd.Function):
     measured in the BERT step and was not faster: separate launches are kept here.)"""
 
     @staticmethod
-    def forward(ctx, x, anchor, store, m1, b1, m2, b2):
+    def forward(ctx, x, anchor, store, m1, b1, m2, b2, box=None):
         H = store.dims[m1][1]
         x2 = x.reshape(-1, H).contiguous()
         bv1 = store.bias_vector(b1) if b1 is not None else None
@@ -127,6 +174,7 @@ class _MLPFn(torch.autograd.Function):
         y = store.fwd(m2, h, bias=bv2)
         ctx.save_for_backward(x2, u, h)
         ctx.store, ctx.m1, ctx.b1, ctx.m2, ctx.b2, ctx.shape = store, m1, b1, m2, b2, x.shape
+        ctx.box = box
         return y.reshape(*x.shape[:-1], y.shape[-1])
 
     @staticmethod
@@ -148,17 +196,22 @@ class _MLPFn(torch.autograd.Function):
             store.bias_grad(ctx.b1, du)
         dx = None
         if ctx.needs_input_grad[0]:
-            dx = torch.empty_like(x2)
-            store.bwd_dx(ctx.m1, du, dx)
-        return (dx.reshape(ctx.shape) if dx is not None else None), None, None, None, None, None, None
+            dx = _dx_plus_residual(store, ctx.m1, du, ctx.box, x2)   # + the residual gradient, if handed off
+        return (dx.reshape(ctx.shape) if dx is not None else None), None, None, None, None, None, None, None
 
 
-def mlp(ff1, ff2, x):
-    """ff2(gelu(ff1(x))): one fused autograd op for two ROAST linears, plain modules otherwise."""
-    if isinstance(ff1, RoastLinear) and isinstance(ff2, RoastLinear) and ff1.store is ff2.store and x.is_cuda \
-            and x.dtype == torch.bfloat16:
+def _mlp_fusable(ff1, ff2, x):
+    return isinstance(ff1, RoastLinear) and isinstance(ff2, RoastLinear) and ff1.store is ff2.store and x.is_cuda \
+        and x.dtype == torch.bfloat16
+
+
+def mlp(ff1, ff2, x, box=None):
+    """ff2(gelu(ff1(x))): one fused autograd op for two ROAST linears, plain modules otherwise.
+    `box` (fused op only): a ResidualGrad whose gradient is added into x's gradient."""
+    if _mlp_fusable(ff1, ff2, x):
         return _MLPFn.apply(x, _anchor(ff1.store), ff1.store, ff1.mid, ff1.bias.mid if ff1.bias is not None else None,
-                            ff2.mid, ff2.bias.mid if ff2.bias is not None else None)
+                            ff2.mid, ff2.bias.mid if ff2.bias is not None else None, box)
+    assert box is None
     return ff2(gelu(ff1(x)))
 
 
@@ -235,7 +288,7 @@ class _LayerNormFn(torch.autograd.Function):
     way, the residual add fused).  The gradient of x and of r is the same ds."""
 
     @staticmethod
-    def forward(ctx, x, r, weight, bias, eps):
+    def forward(ctx, x, r, weight, bias, eps, box=None):
         n = x.shape[-1]
         x = x.contiguous()
         rows = x.numel() // n
@@ -250,6 +303,7 @@ class _LayerNormFn(torch.autograd.Function):
                               mean.data_ptr(), rstd.data_ptr(), rows, n, float(eps), _cdt(x), _cdt(weight), strm)
         ctx.save_for_backward(s, weight, mean, rstd)
         ctx.has_r = r is not None
+        ctx.box = box
         return y
 
     @staticmethod
@@ -264,7 +318,10 @@ class _LayerNormFn(torch.autograd.Function):
         R.roast_layernorm_bwd(dy.data_ptr(), s.data_ptr(), weight.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
                               ds.data_ptr(), dg.data_ptr(), db.data_ptr(), rows, n, _cdt(s), _cdt(weight),
                               torch.cuda.current_stream().cuda_stream)
-        return ds, (ds if ctx.has_r else None), dg.to(weight.dtype), db.to(weight.dtype), None
+        if ctx.box is not None:   # the residual's gradient goes to the GEMM that adds it (ResidualGrad)
+            ctx.box.ds = ds
+            return ds, None, dg.to(weight.dtype), db.to(weight.dtype), None, None
+        return ds, (ds if ctx.has_r else None), dg.to(weight.dtype), db.to(weight.dtype), None, None
 
 
 class LayerNorm(torch.nn.LayerNorm):
@@ -272,11 +329,22 @@ class LayerNorm(torch.nn.LayerNorm):
     forward(x, residual=None) normalises x + residual in the same pass.  Falls back to torch's
     kernel off the GPU or without an affine part."""
 
-    def forward(self, x, residual=None):
-        if x.is_cuda and self.elementwise_affine and self.bias is not None and x.shape[-1] % 8 == 0 \
-                and x.shape[-1] <= 2048 and x.dtype in (torch.bfloat16, torch.float32):
+    def fused(self, x):
+        return x.is_cuda and self.elementwise_affine and self.bias is not None and x.shape[-1] % 8 == 0 \
+            and x.shape[-1] <= 2048 and x.dtype in (torch.bfloat16, torch.float32)
+
+    def forward(self, x, residual=None, residual_grad=None):
+        """residual_grad (fused kernel only): a ResidualGrad that receives the residual's gradient
+        instead of autograd (the residual must then reach the loss through that hand-off)."""
+        if self.fused(x):
+            if residual_grad is not None:
+                return _LayerNormFn.apply(x, residual.detach(), self.weight, self.bias, self.eps, residual_grad)
             return _LayerNormFn.apply(x, residual, self.weight, self.bias, self.eps)
+        assert residual_grad is None
         return super().forward(x if residual is None else x + residual)
+
+
+_RESIDUAL_HANDOFF = os.environ.get("ROAST_RESIDUAL_HANDOFF", "1") != "0"   # A/B switch (ResidualGrad)
 
 
 class EncoderLayer(torch.nn.Module):
@@ -299,14 +367,17 @@ class EncoderLayer(torch.nn.Module):
         # (registration order and hashes unchanged; the group id lives outside the module ids)
         self.qkv_gid = store.linear_concat([self.q.mid, self.k.mid, self.v.mid]) if fuse_qkv else None
 
-    def _qkv_packed(self, x):
-        """[q | k | v] as one [.., 3 d] tensor (the fused ROAST group or dense Linear), else None."""
+    def _qkv_packed(self, x, box=None):
+        """[q | k | v] as one [.., 3 d] tensor (the fused ROAST group or dense Linear), else None.
+        `box` (ROAST group only): a ResidualGrad added into x's gradient by the dX GEMM."""
         dense = getattr(self, "qkv_dense", None)
         if dense is not None:
+            assert box is None
             return dense(x)
         if getattr(self, "qkv_gid", None) is not None:
             bias = tuple(lin.bias.mid for lin in (self.q, self.k, self.v)) if self.q.bias is not None else ()
-            return _LinearGroupFn.apply(x, _anchor(self.q.store), self.q.store, self.qkv_gid, bias)
+            return _LinearGroupFn.apply(x, _anchor(self.q.store), self.q.store, self.qkv_gid, bias, box)
+        assert box is None
         return None
 
     def _qkv(self, x):
@@ -320,14 +391,21 @@ class EncoderLayer(torch.nn.Module):
         B, S, d = x.shape
         h = self.heads
 
-        packed = self._qkv_packed(x) if _flash_attn_packed is not None and x.is_cuda and \
+        # residual gradients handed to the GEMMs that add them (ResidualGrad): the QKV group's and
+        # the MLP's dX epilogues write dX + ds instead of autograd adding the two afterwards
+        hand_off = getattr(self, "fuse_residual_grad", _RESIDUAL_HANDOFF) and self.ln1.fused(x) and \
+            x.dtype == torch.bfloat16
+        box1 = ResidualGrad() if hand_off and getattr(self, "qkv_dense", None) is None and \
+            getattr(self, "qkv_gid", None) is not None else None
+        packed = self._qkv_packed(x, box1) if _flash_attn_packed is not None and x.is_cuda and \
             x.dtype == torch.bfloat16 else None
         if packed is not None:
             # the packed QKV GEMM output viewed as [B, S, 3, heads, d_head]: flash-attn's packed form
             # returns d(qkv) packed too (no concatenation of dq, dk, dv in the backward)
             a = _flash_attn_packed(packed.view(B, S, 3, h, d // h)).reshape(B, S, d)
-            x = self.ln1(self.o(a), x)
-            return self.ln2(mlp(self.ff1, self.ff2, x), x)
+            x = self.ln1(self.o(a), x, residual_grad=box1)
+            box2 = ResidualGrad() if hand_off and _mlp_fusable(self.ff1, self.ff2, x) else None
+            return self.ln2(mlp(self.ff1, self.ff2, x, box2), x, residual_grad=box2)
         q, k, v = self._qkv(x)
         if _flash_attn is not None and x.is_cuda and x.dtype == torch.bfloat16:
             # flash-attn (library kernel) reads [B, S, heads, d_head] strided views of the QKV

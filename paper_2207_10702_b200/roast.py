@@ -257,7 +257,7 @@ def roast_linear_fwd_bias(h, mid, X_ptr, Y_ptr, tokens, dtype, bias_ptr, stream=
     _check(_lib.roast_linear_fwd_bias(h, mid, X_ptr, Y_ptr, tokens, dtype, bias_ptr, stream), "roast_linear_fwd_bias")
 
 
-ACT_NONE, ACT_GELU_TANH = 0, 1
+ACT_NONE, ACT_GELU_TANH, ACT_RESIDUAL = 0, 1, 2
 ERR_UNSUPPORTED = 9
 
 

@@ -162,3 +162,74 @@ def test_fused_gelu_shape_fuzz(R, torch):
         ref = spec.backward_dx(dY_np, M_np, True) * gelu_grad(U_in.astype(np.float64))
         assert rel_frob(dX.float().cpu().numpy(), ref) <= 1e-2, where
         ctx.close()
+
+
+@pytest.mark.parametrize("T", [1, 300, 1000, 8192])
+def test_residual_dx_equals_dx_plus_r(R, torch, T):
+    """ROAST_ACT_RESIDUAL: dX = bf16(bf16(lambda dY W~^T) + R) in the dX epilogue has the bits of
+    the plain dX GEMM followed by a separate bf16 add, for a single module (768-wide dX) and the
+    fused QKV group (K = 2304), both unit widths (the tuner times both on the first call), R
+    aliasing the output too; and it is the oracle's dX + R within the bf16 tolerance."""
+    mem = 47192
+    M_np = store(mem)
+    ctx = R.Roast(to_dev(M_np, torch.float32), 64, 64, seed=HS)
+    f1 = ctx.linear(768, 3072)
+    q, k, v = ctx.linear(768, 768), ctx.linear(768, 768), ctx.linear(768, 768)
+    gid = ctx.linear_concat([q, k, v])
+    for mid, O, spec in ((f1, 3072, OM.LinearSpec(768, 3072, 64, 64, mem, HS, f1)), (gid, 2304, None)):
+        dY_np = bf16_input(synth.SEED_DY + O, (T, O))
+        R_np = bf16_input(synth.SEED_X + O, (T, 768))
+        dY, Rr = to_dev(dY_np, torch.bfloat16), to_dev(R_np, torch.bfloat16)
+        for _ in range(2):   # the first call tunes the unit width (times both)
+            fused = ctx.bwd_dx_act(mid, dY, Rr, act=R.ACT_RESIDUAL)
+        plain = torch.empty(T, 768, device="cuda", dtype=torch.bfloat16)
+        ctx.bwd_dx(mid, dY, plain)
+        inplace = Rr.clone()
+        ctx.bwd_dx_act(mid, dY, inplace, dX=inplace, act=R.ACT_RESIDUAL)
+        torch.cuda.synchronize()
+        ctx.check()
+        assert torch.equal(fused, plain + Rr), (mid, T)
+        assert torch.equal(inplace, fused), (mid, T)
+        if spec is not None:
+            rows = slice(None) if T <= 1000 else np.random.default_rng(3).choice(T, 256, replace=False)
+            ref = spec.backward_dx(dY_np[rows], M_np, True) + R_np[rows].astype(np.float64)
+            assert rel_frob(fused.float().cpu().numpy()[rows], ref) <= 1e-2
+    with pytest.raises(R.RoastError) as e:   # the residual form is a dX-only epilogue
+        ctx.fwd_act(f1, torch.zeros(8, 768, device="cuda", dtype=torch.bfloat16), act=R.ACT_RESIDUAL)
+    assert e.value.status == R.ERR_CONFIG
+    ctx.close()
+
+
+@pytest.mark.parametrize("fuse_min_tokens", [0, None])
+def test_encoder_layer_residual_hand_off_is_bit_identical(R, torch, fuse_min_tokens, monkeypatch):
+    """The BERT layer with the residual gradients handed to the QKV / MLP dX epilogues
+    (nn.ResidualGrad) against the same layer with autograd adding them: output, input gradient,
+    dM (deterministic mode: fast mode's reduce-adds land in any order) and the LayerNorm parameter
+    gradients bit for bit (both add two bf16 tensors once)."""
+    from paper_2207_10702_b200 import nn as RN
+    if fuse_min_tokens is not None:   # 0: the fused epilogue at this size too (else plain dX + add)
+        monkeypatch.setattr(RN, "RESIDUAL_FUSE_MIN_TOKENS", fuse_min_tokens)
+    M = torch.rand(849352, device="cuda") * 2 - 1
+    res = []
+    for hand_off in (True, False):
+        ctx = R.Roast(M.clone(), 64, 64, seed=HS, deterministic=True)
+        layers = torch.nn.ModuleList([RN.EncoderLayer(ctx, 768, 3072, 12) for _ in range(2)]).cuda()
+        for m in layers.modules():
+            if isinstance(m, torch.nn.LayerNorm):
+                m.to(torch.bfloat16)
+        for lay in layers:
+            lay.fuse_residual_grad = hand_off
+        g = torch.Generator(device="cuda").manual_seed(9)
+        x = torch.randn(4, 128, 768, device="cuda", generator=g).to(torch.bfloat16).requires_grad_(True)
+        dy = torch.randn(4, 128, 768, device="cuda", generator=g).to(torch.bfloat16)
+        ctx.zero_grad()
+        y = x
+        for lay in layers:
+            y = lay(y)
+        y.backward(dy)
+        torch.cuda.synchronize()
+        ctx.check()
+        res.append([y, x.grad, ctx.dM.clone()] + [p.grad for lay in layers for p in (lay.ln1.weight, lay.ln2.bias)])
+        ctx.close()
+    for a, b in zip(res[0], res[1]):
+        assert torch.equal(a, b)

@@ -45,4 +45,16 @@ res["dx_act_us"] = t_us(lambda: ctx.bwd_dx_act(b, dY, U, dU))
 res["torch_gelu_fwd_us"] = t_us(lambda: torch.nn.functional.gelu(U, approximate="tanh"))
 Ur = U.clone().requires_grad_(True)
 res["torch_gelu_bwd_us"] = t_us(lambda: torch.ops.aten.gelu_backward(dU, Ur, approximate="tanh"))
+# residual form (ROAST_ACT_RESIDUAL) on the 768-wide dX GEMMs of the layer: ff1 (K = 3072) and the
+# fused QKV group (K = 2304), against the plain dX GEMM + torch's bf16 add
+q, k, v = ctx.linear(768, 768), ctx.linear(768, 768), ctx.linear(768, 768)
+gid = ctx.linear_concat([q, k, v])
+Rr = torch.randn(T, 768, device="cuda").to(bf)
+dX = torch.empty(T, 768, device="cuda", dtype=bf)
+dQ = torch.randn(T, 2304, device="cuda").to(bf)
+res["ff1_dx_plain_us"] = t_us(lambda: ctx.bwd_dx(a, dU, dX))
+res["ff1_dx_residual_us"] = t_us(lambda: ctx.bwd_dx_act(a, dU, Rr, dX, act=R.ACT_RESIDUAL))
+res["qkv_dx_plain_us"] = t_us(lambda: ctx.bwd_dx(gid, dQ, dX))
+res["qkv_dx_residual_us"] = t_us(lambda: ctx.bwd_dx_act(gid, dQ, Rr, dX, act=R.ACT_RESIDUAL))
+res["torch_add_us"] = t_us(lambda: torch.add(dX, Rr))
 print(json.dumps({k: round(v, 1) if isinstance(v, float) else v for k, v in res.items()}))
