@@ -61,7 +61,7 @@ constexpr int KB_CHUNK = 64;  // k-blocks whose tile coordinates are staged in s
 // NU: output columns per unit (MMA N): 256, or 192 (DX, CG = 2, WM = 2 only) for N = 768-wide
 // outputs, whose 48 units of 512 x 256 leave 26 of 74 CTA pairs idle (64 units of 512 x 192
 // fill one round of 74 with 25 % less work per unit).
-template <int CG, int WM, int NU = BN>
+template <int CG, int WM, int NU = BN, bool XBUF = false>
 struct Cfg {
   static constexpr int A_BYTES = BM * WM * BK * 2;       // this CTA's 128*WM rows of A
   // this CTA's NU/CG columns of B, in whole 64-wide tiles (NU = 192: 96 K-major rows for DX,
@@ -69,7 +69,9 @@ struct Cfg {
   static constexpr int B_BYTES = ((NU / CG + 63) / 64) * 64 * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int NBUF = 2;                         // epilogue staging buffers per warp
-  static constexpr int STAGING = 4 * NBUF * 4096;        // 4 warps x NBUF x (32 rows x 128 B)
+  // 4 warps x NBUF x (32 rows x 128 B); XBUF (the GELU dX epilogue, 8 RF warps) gives each warp a
+  // second 4 KB buffer for the activation input, at the cost of a pipeline stage
+  static constexpr int STAGING = (XBUF ? 2 : 1) * 4 * NBUF * 4096;
   static constexpr int FIXED = STAGING + 1024 + 256 + KB_CHUNK * 4 * 4;
   static constexpr int STAGES = (227 * 1024 - FIXED) / STAGE_BYTES > 6 ? 6 : (227 * 1024 - FIXED) / STAGE_BYTES;
   static constexpr int B_SUB = 4 / CG;                   // 64-wide B sub-tiles per CTA
@@ -319,14 +321,23 @@ __device__ __forceinline__ float tanh_approx(float x) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Folded constants (k0 = sqrt(2 / pi), k1 = 0.044715): with u = x^2, t = tanh(x (k0 + k0 k1 u)),
+//   gelu(x)  = h + h t,  h = x / 2
+//   gelu'(x) = (1 + t) / 2 + x (1 - t^2) (k0 / 2 + 3 k0 k1 u / 2)
+// — the same functions in 5 / 8 fp32 operations + one tanh.approx (the epilogue of a fused
+// activation is ALU-bound: 8 warps evaluate it over the whole 256 x 256 tile of each unit).
 __device__ __forceinline__ float gelu_tanh(float x) {
-  const float t = tanh_approx(0.7978845608f * (x + 0.044715f * x * x * x));
-  return 0.5f * x * (1.f + t);
+  const float u = x * x;
+  const float t = tanh_approx(x * fmaf(0.7978845608f * 0.044715f, u, 0.7978845608f));
+  const float h = 0.5f * x;
+  return fmaf(h, t, h);
 }
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
-  const float x2 = x * x;
-  const float t = tanh_approx(0.7978845608f * (x + 0.044715f * x2 * x));
-  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * 0.7978845608f * (1.f + 3.f * 0.044715f * x2);
+  const float u = x * x;
+  const float t = tanh_approx(x * fmaf(0.7978845608f * 0.044715f, u, 0.7978845608f));
+  const float p = fmaf(1.5f * 0.7978845608f * 0.044715f, u, 0.5f * 0.7978845608f);
+  const float r = x * fmaf(-t, t, 1.f);
+  return fmaf(r, p, fmaf(0.5f, t, 0.5f));
 }
 // two packed bf16 -> f(a) * g, f(b) * g ... helpers over a packed pair
 __device__ __forceinline__ float2 unpack_bf2(uint32_t v) {
@@ -338,7 +349,7 @@ __device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int MODE, int CG, int WM, bool CHAIN = false, int NU = BN, bool ACT = false>
+template <int MODE, int CG, int WM, bool CHAIN = false, int NU = BN, bool ACT = false, bool XBUF = false>
 __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
     roast_mm_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ WMaps wmaps,
@@ -346,14 +357,15 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
                    const __grid_constant__ CUtensorMap mapOut1, const __grid_constant__ Params p1,
                    const __grid_constant__ WMapsHalf hmaps, const __grid_constant__ CUtensorMap mapAct) {
   static_assert(NU == BN || (NU == 192 && MODE != DW && CG == 2 && WM == 2 && !CHAIN), "NU = 192: FWD / DX, 2 x 2");
-  using C = Cfg<CG, WM, NU>;
+  static_assert(!XBUF || (ACT && MODE == DX && !CHAIN), "XBUF: the fused-activation dX epilogue");
+  using C = Cfg<CG, WM, NU, XBUF>;
   constexpr bool RF = Roles<MODE, CG, WM>::RF;
   constexpr int EPI_WARPS = Roles<MODE, CG, WM>::EPI_WARPS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                        // [STAGES][A_BYTES]
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;               // [STAGES][B_BYTES]
-  uint8_t* sStage = smem + C::STAGES * C::STAGE_BYTES;      // epilogue staging [4 warps][2][4 KB]
+  uint8_t* sStage = smem + C::STAGES * C::STAGE_BYTES;      // epilogue staging [4 warps][2][4 KB] (x2 with XBUF)
   uint64_t* full = reinterpret_cast<uint64_t*>(sStage + C::STAGING);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
@@ -618,6 +630,9 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
     const int q = warp & 3;
     const int jh = (warp - EPI_WARP0) >> 2;
     uint8_t* buf = sStage + (warp - EPI_WARP0) * 4096;
+    // XBUF: this warp's second buffer, where the U chunks land (chunk c + 1 loads while chunk c is
+    // computed and stored from `buf`); else U chunks and act(Y) share `buf` with the stores
+    uint8_t* buf2 = XBUF ? sStage + 32768 + (warp - EPI_WARP0) * 4096 : buf;
     const uint32_t tempty_leader0 = map_to_rank(smem_u32(&tempty[0]), 0);
     uint32_t aph = 0;
     uint32_t uph = 0;   // ACT DX: parity of this warp's U-chunk barrier
@@ -633,9 +648,15 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
       if (ACT && MODE == DX && act_u) {   // request U's first chunk now: it lands while the MMAs finish
         const int r0 = mb * BM * CG * WM + int(rank) * BM * WM + jh * BM + q * 32;
         if (lane == 0 && nsteps > 0) {
-          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          // chunks 1.. of this warp's rows into L2 now: their loads below then wait on L2, not HBM
+          for (int c = 1; c < nsteps; ++c)
+            asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
+                             reinterpret_cast<uint64_t>(&mapAct)), "r"(nb * NU + c * 64), "r"(r0)
+                         : "memory");
+          // XBUF: buf2 was read out by every lane (syncwarp); else wait for the last store's reads
+          if (!XBUF) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           mbar_expect_tx(&ubar[warp - EPI_WARP0], 4096);
-          tma_load_2d<1>(&mapAct, buf, smem_u32(&ubar[warp - EPI_WARP0]), nb * NU, r0);
+          tma_load_2d<1>(&mapAct, buf2, smem_u32(&ubar[warp - EPI_WARP0]), nb * NU, r0);
         }
       }
       long long tw3 = p.prof ? clock64() : 0;
@@ -691,21 +712,34 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
       for (int c = 0; c < NU / 64; ++c) {
         if (c < nsteps) {
           if (ACT && MODE == DX && act_u) {
-            // dX = bf16(dh) * act'(U): the U chunk (32 rows x 64 columns) arrives by TMA in this warp's
-            // staging buffer (once the previous store has read it); each thread reads its row
-            if (lane == 0 && c > 0) {   // chunk 0 was requested before the accumulator wait
+            // dX = bf16(dh) * act'(U) (or + R): the U chunk (32 rows x 64 columns) arrives by TMA;
+            // each thread reads its row into registers.  XBUF: chunk c + 1 is then requested into the
+            // second buffer (it lands while this chunk is computed and stored); else chunk c is
+            // requested into the staging buffer once the previous store has read it.
+            if (!XBUF && lane == 0 && c > 0) {   // chunk 0 was requested before the accumulator wait
               asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
               mbar_expect_tx(&ubar[warp - EPI_WARP0], 4096);
               tma_load_2d<1>(&mapAct, buf, smem_u32(&ubar[warp - EPI_WARP0]), nb * NU + c * 64, row0);
             }
             mbar_wait(&ubar[warp - EPI_WARP0], uph);
             uph ^= 1;
+            uint32_t uw_all[32];
 #pragma unroll
             for (int cc = 0; cc < 8; ++cc) {
-              uint32_t w0, w1, w2, w3;
-              const uint32_t a = smem_u32(buf + lane * 128 + ((cc ^ (lane & 7)) << 4));
-              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(a));
-              const uint32_t uw[4] = {w0, w1, w2, w3};
+              const uint32_t a = smem_u32(buf2 + lane * 128 + ((cc ^ (lane & 7)) << 4));
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(uw_all[4 * cc]), "=r"(uw_all[4 * cc + 1]), "=r"(uw_all[4 * cc + 2]),
+                             "=r"(uw_all[4 * cc + 3])
+                           : "r"(a));
+            }
+            __syncwarp();   // every row read before the buffer is reused
+            if (XBUF && lane == 0 && c + 1 < nsteps) {
+              mbar_expect_tx(&ubar[warp - EPI_WARP0], 4096);
+              tma_load_2d<1>(&mapAct, buf2, smem_u32(&ubar[warp - EPI_WARP0]), nb * NU + (c + 1) * 64, row0);
+            }
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) {
+              const uint32_t* uw = uw_all + 4 * cc;
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const float2 d = unpack_bf2(pk[c * 32 + 4 * cc + e]), x = unpack_bf2(uw[e]);
@@ -714,7 +748,6 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
                                                      : pack_bf2(d.x * gelu_tanh_grad(x.x), d.y * gelu_tanh_grad(x.y));
               }
             }
-            __syncwarp();   // every row read before the buffer is overwritten with dX
           }
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           __syncwarp();
@@ -747,7 +780,7 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
             __syncwarp();
 #pragma unroll
             for (int cc = 0; cc < 8; ++cc) {
-              const uint32_t a = smem_u32(buf + lane * 128 + ((cc ^ (lane & 7)) << 4));
+              const uint32_t a = smem_u32(buf2 + lane * 128 + ((cc ^ (lane & 7)) << 4));
               asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(gk[4 * cc]), "r"(gk[4 * cc + 1]),
                            "r"(gk[4 * cc + 2]), "r"(gk[4 * cc + 3])
                            : "memory");
@@ -757,7 +790,7 @@ __global__ void __launch_bounds__(Roles<MODE, CG, WM>::THREADS, 1)
             if (lane == 0) {
               asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                                reinterpret_cast<uint64_t>(&mapAct)),
-                           "r"(nb * NU + c * 64), "r"(row0), "r"(smem_u32(buf))
+                           "r"(nb * NU + c * 64), "r"(row0), "r"(smem_u32(buf2))
                            : "memory");
               asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
@@ -1553,16 +1586,16 @@ int cta_group() {
   return cg;
 }
 
-template <int MODE, int CG, int WM, bool CHAIN = false, int NU = BN, bool ACT = false>
+template <int MODE, int CG, int WM, bool CHAIN = false, int NU = BN, bool ACT = false, bool XBUF = false>
 roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o, const WMaps& w,
                          const Params& p, const CUtensorMap& a1, const CUtensorMap& o1, const Params& p1,
                          int grid_pairs, cudaStream_t s, const WMapsHalf* hw = nullptr,
                          const CUtensorMap* act_map = nullptr) {
-  using C = Cfg<CG, WM, NU>;
+  using C = Cfg<CG, WM, NU, XBUF>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
-        cudaFuncSetAttribute(roast_mm_sm100<MODE, CG, WM, CHAIN, NU, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(roast_mm_sm100<MODE, CG, WM, CHAIN, NU, ACT, XBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(smem)");
     attr = true;
   }
@@ -1593,7 +1626,7 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
     pp1.prof = prof;
   }
   static const WMapsHalf no_half{};
-  cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mm_sm100<MODE, CG, WM, CHAIN, NU, ACT>, a, b, o, w, pp, a1, o1, pp1,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mm_sm100<MODE, CG, WM, CHAIN, NU, ACT, XBUF>, a, b, o, w, pp, a1, o1, pp1,
                                      hw ? *hw : no_half, act_map ? *act_map : o);
   if (e != cudaSuccess) return cuda_fail(e, "roast_mm_sm100 launch");
   if (pp.prof) {
@@ -1625,7 +1658,16 @@ roast_status_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensor
                       const CUtensorMap* o_act = nullptr) {
   if constexpr (MODE != DW) {
     if (p.act) {   // fused activation: the WM = 2 register-held epilogue (checked by the caller)
-      // the activation's second tensor (mapAct): FWD writes act(Y) there, DX reads U from it
+      // the activation's second tensor (mapAct): FWD writes act(Y) there, DX reads U from it.
+      // The GELU dX epilogue is ALU-bound: it takes the second staging buffer (XBUF) so U chunk c + 1
+      // loads while chunk c is computed (tools/act_probe.py, T = 65 536: 335 -> 302 us); the others
+      // keep the fourth pipeline stage (residual dX 245 vs 237 us, forward 292 vs 283 us with XBUF)
+      if constexpr (MODE == DX) {
+        if (p.act == 1) {
+          if (nu == 192) return launch_cg<MODE, 2, 2, false, 192, true, true>(a, b, o, w, p, a, o, p, 0, s, hw, o_act);
+          return launch_cg<MODE, 2, 2, false, BN, true, true>(a, b, o, w, p, a, o, p, 0, s, nullptr, o_act);
+        }
+      }
       if (nu == 192) return launch_cg<MODE, 2, 2, false, 192, true>(a, b, o, w, p, a, o, p, 0, s, hw, o_act);
       return launch_cg<MODE, 2, 2, false, BN, true>(a, b, o, w, p, a, o, p, 0, s, nullptr, o_act);
     }
