@@ -253,6 +253,7 @@ roast_status_t roast_destroy(roast_t h) {
   for (auto& m : c->modules) free_module(m);
   for (auto& m : c->groups) free_module(m);
   cudaFree(c->shadow);
+  cudaFree(c->dm_rep);
   cudaFree(c->d_err);
   cudaFree(c->opt_s1);
   cudaFree(c->opt_s2);

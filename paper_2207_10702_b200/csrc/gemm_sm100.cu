@@ -1059,6 +1059,7 @@ struct MixParams {
   MixProb p[4];
   int64_t neg_row;          // row (128 B) of the negated shadow copy
   int reps, rep_rows;       // shadow replicas (rep_rows rows apart); CTA pair q reads replica q % reps
+  int dm_reps, dm_rep_rows; // dM replicas (fast mode, tiny |M|): CTA pair q reduce-adds into replica q % dm_reps
   const int32_t* sched;     // [pairs][sched_len] codes prob << 24 | unit, -1 = end
   int sched_len;
   int* flags;               // ready counters of the publishing problem's units
@@ -1116,6 +1117,7 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
   const bool leader = rank == 0;
   const int pair = blockIdx.x / CG;
   const int rrow = mp.reps > 1 ? (pair % mp.reps) * mp.rep_rows : 0;   // this pair's shadow replica
+  const int drow = mp.dm_reps > 1 ? (pair % mp.dm_reps) * mp.dm_rep_rows : 0;   // ... and dM replica
   auto unit_at = [&](int i, int& prob, int& u) -> bool {
     if (i >= mp.sched_len) return false;
     const int code = __ldg(mp.sched + pair * mp.sched_len + i);
@@ -1473,7 +1475,7 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
           __syncwarp();
           if (lane == 0 && rb < P.M) {   // 32 rows x 32 fp32 of one hash tile
             const int x0 = (c & 1) * 32;
-            const int y0 = int(tbo >> 6) + (rb & 63);
+            const int y0 = int(tbo >> 6) + (rb & 63) + (P.ws_slot >= 0 ? 0 : drow);
             if (P.ws_slot >= 0)   // deterministic: plain store into the per-tile workspace
               asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                                reinterpret_cast<uint64_t>(&maps.ws[P.ws_slot])),
@@ -2366,6 +2368,25 @@ MixPlan plan_mix(int mt0, int nt0, int kb0, int mt1, int nt1, int kbT, int mt2, 
 }
 }  // namespace
 
+// dM += sum of the fused backward's dM replicas, replicas zeroed: atomic exchange / add, so a
+// fold never loses a concurrent launch's reduce-adds (that launch's own fold picks them up)
+__global__ void fold_dm_replicas_kernel(float* __restrict__ dM, float* __restrict__ rep, int64_t n, int reps,
+                                        int64_t stride) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    float acc = 0.f;
+    for (int r = 0; r < reps; ++r) acc += atomicExch(rep + r * stride + i, 0.f);
+    if (acc != 0.f) atomicAdd(dM + i, acc);
+  }
+}
+
+// replicas at tiny |M| only: at C2 1000x (|M| = 4720, 19 KB of dM) every weight-gradient tile of
+// the fused backward reduce-adds into the same few L2 lines (131 vs 123 us at 100x); ROAST_DM_REPS
+// overrides (1 = off)
+static int dm_replicas(const Ctx* c) {
+  if (const char* e = getenv("ROAST_DM_REPS")) return std::max(1, std::min(74, atoi(e)));
+  return c->mem_size * int64_t(sizeof(float)) <= (int64_t(64) << 10) ? 16 : 1;
+}
+
 roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, const void* X_a, const void* Y_a,
                                const void* dY_b, void* dY_a, void* dX_a, int64_t T, cudaStream_t s, int act,
                                const void* U) {
@@ -2516,6 +2537,29 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
     c->tmap_dm_for = c->dM;
   }
   maps.dm = dmaps;
+  mp.dm_reps = 1;
+  mp.dm_rep_rows = 0;
+  if (!det) {
+    if (c->dm_reps == 0) c->dm_reps = dm_replicas(c);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (c->dm_reps > 1 && !c->dm_rep && cudaStreamIsCapturing(s, &cs) == cudaSuccess &&
+        cs == cudaStreamCaptureStatusNone) {   // allocated on an eager call (not under capture)
+      c->dm_rep_elems = (c->mem_size + 63) / 64 * 64;
+      const size_t bytes = size_t(c->dm_reps) * size_t(c->dm_rep_elems) * sizeof(float);
+      ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->dm_rep), bytes));
+      ROAST_CUDA_CHECK(cudaMemsetAsync(c->dm_rep, 0, bytes, s));
+      WMaps& rm = *reinterpret_cast<WMaps*>(c->tmap_dmrep);
+      for (int r = 0; r < 8; ++r) {
+        const int64_t elems = int64_t(c->dm_reps) * c->dm_rep_elems - 8 * r;
+        if ((st = make_map_2d(&rm.m[r], c->dm_rep + 8 * r, 64, uint64_t(elems / 64), 256, 32, 32, true))) return st;
+      }
+    }
+    if (c->dm_reps > 1 && c->dm_rep) {
+      maps.dm = *reinterpret_cast<const WMaps*>(c->tmap_dmrep);
+      mp.dm_reps = c->dm_reps;
+      mp.dm_rep_rows = int(c->dm_rep_elems / 64);
+    }
+  }
   // ready counters of P0's units: the next slot of the chain ring (as sm100_chain)
   const int64_t need = mp.p[0].units;
   if (c->chain_slot_n < need) {
@@ -2560,6 +2604,13 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
   }
   cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mix_sm100, maps, mp);
   if (e != cudaSuccess) return cuda_fail(e, "roast_mix_sm100 launch");
+  if (mp.dm_reps > 1) {
+    const int64_t n = c->mem_size;
+    fold_dm_replicas_kernel<<<unsigned(std::min<int64_t>((n + 255) / 256, 1184)), 256, 0, s>>>(
+        c->dM, c->dm_rep, n, mp.dm_reps, c->dm_rep_elems);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fold dM replicas");
+    c->launches += 1;
+  }
   if (det) {   // fixed order: module b's slots, then module a's (each: covering tiles, then splits)
     const int sp_b = mp.p[1].units / (mp.p[1].m_tiles * mp.p[1].n_tiles);
     const int sp_a = mp.p[3].units / (mp.p[3].m_tiles * mp.p[3].n_tiles);

@@ -159,6 +159,13 @@ struct Ctx {
   // ... and of dM (8 fp32 phase views for the TMA reduce-add epilogue), valid for dM == tmap_dm_for
   alignas(64) unsigned char tmap_dm[1024];
   const float* tmap_dm_for = nullptr;
+  // dM replicas of the fused backward at tiny |M| (fast mode): its weight-gradient tiles reduce-add
+  // into replica (CTA pair % dm_reps) instead of all into the same few L2 lines, and a fold adds
+  // the replicas into dM (and zeroes them) after the launch; [dm_reps][dm_rep_elems] fp32
+  float* dm_rep = nullptr;
+  int dm_reps = 0;                // 0: not decided yet
+  int64_t dm_rep_elems = 0;
+  alignas(64) unsigned char tmap_dmrep[1024];
   // optimizer state, |M| fp32 each (Adagrad: s1 = G; Adam: s1 = m, s2 = v)
   float* opt_s1 = nullptr;
   float* opt_s2 = nullptr;

@@ -712,14 +712,16 @@ def test_chain_fwd_and_dx_match_single_calls(R, torch, T):
 
 
 @pytest.mark.parametrize("T,ratio,det", [(8192, 100, False), (1000, 100, False), (300, 1000, False), (1, 100, False),
-                                         (4096, 10, False), (1000, 100, True), (8192, 1000, True)])
+                                         (4096, 10, False), (1000, 100, True), (8192, 1000, True),
+                                         (8192, 1000, False)])
 def test_bwd_chain_fused_matches_oracle(R, torch, T, ratio, det):
     """roast_linear_bwd_chain: the MLP block's whole backward (dY_a, dM of b, dX_a, dM of a) in ONE
     persistent launch with the four GEMMs co-scheduled.  dY_a and dX_a are bitwise equal to the
     single dX calls at the same kernel configuration (same MMA sequence per output tile; repeated
     to catch a missing wait on the dependency); everything matches the fp64 oracle chain.
     Deterministic mode (dM tiles into a workspace, fixed-order reduce): dM bitwise identical
-    over the repeats."""
+    over the repeats.  At 1000x in fast mode the dM tiles go through the handle's dM replicas and
+    the fold after the launch."""
     cfg = synth.mlp_block(ratio)
     mem = cfg["mem_size"]
     M_np = store(mem)
@@ -766,6 +768,33 @@ def test_bwd_chain_fused_matches_oracle(R, torch, T, ratio, det):
     assert rel_frob(dXa.float().cpu().numpy(), sa.backward_dx(dYa_o, M_np, True)) <= 1e-2
     dM_ref = sb.backward_dm(Ya_np, dY_np) + sa.backward_dm(X_np, dYa_o)
     assert rel_frob(dM, dM_ref) <= 1e-2
+
+
+def test_bwd_chain_dm_replicas_concurrent_streams(R, torch):
+    """The fused backward's dM replicas (1000x, fast mode) under two launches on two streams with
+    no ordering between them: each fold takes the replica values atomically, so dM ends as the
+    sum of both backwards (= twice one backward, within the atomic-order tolerance)."""
+    cfg = synth.mlp_block(1000)
+    M_np = store(cfg["mem_size"])
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64)
+    a, b = [ctx.linear(H, O) for H, O in cfg["layers"]]
+    T = 4096
+    X, Ya, dYb = (to_dev(bf16_input(sd, shp), torch.bfloat16) for sd, shp in
+                  ((synth.SEED_X, (T, 768)), (synth.SEED_X + 7, (T, 3072)), (synth.SEED_DY, (T, 768))))
+    ctx.zero_grad()
+    ctx.bwd_chain(a, b, X, Ya, dYb)
+    torch.cuda.synchronize()
+    one = ctx.dM.clone().double()
+    ctx.zero_grad()
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        for st in (s1, s2):
+            with torch.cuda.stream(st):
+                ctx.bwd_chain(a, b, X, Ya, dYb, stream=st)
+    torch.cuda.synchronize()
+    ctx.check()
+    assert float((ctx.dM.double() - 6 * one).norm() / (6 * one).norm()) <= 1e-5
 
 
 @pytest.mark.parametrize("H,O,T", [(768, 3072, 8192), (768, 3072, 1000), (3072, 768, 129), (768, 192, 513)])

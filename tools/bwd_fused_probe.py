@@ -10,7 +10,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2207_10702_b200 import roast as R  # noqa: E402
 
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
-M = torch.rand(47192, device="cuda") * 2 - 1
+MEM = int(sys.argv[2]) if len(sys.argv) > 2 else 47192   # |M|: 471864 / 47192 / 4720 = 10x / 100x / 1000x
+M = torch.rand(MEM, device="cuda") * 2 - 1
 ctx = R.Roast(M, 64, 64)
 ctx.set_autotune(2)
 a, b = ctx.linear(768, 3072), ctx.linear(3072, 768)
