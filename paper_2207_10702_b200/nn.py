@@ -404,7 +404,7 @@ class EncoderLayer(torch.nn.Module):
             # returns d(qkv) packed too (no concatenation of dq, dk, dv in the backward)
             a = _flash_attn_packed(packed.view(B, S, 3, h, d // h)).reshape(B, S, d)
             x = self.ln1(self.o(a), x, residual_grad=box1)
-            box2 = ResidualGrad() if hand_off and _mlp_fusable(self.ff1, self.ff2, x) else None
+            box2 = ResidualGrad() if hand_off and self.ln2.fused(x) and _mlp_fusable(self.ff1, self.ff2, x) else None
             return self.ln2(mlp(self.ff1, self.ff2, x, box2), x, residual_grad=box2)
         q, k, v = self._qkv(x)
         if _flash_attn is not None and x.is_cuda and x.dtype == torch.bfloat16:
