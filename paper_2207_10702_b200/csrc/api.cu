@@ -29,16 +29,15 @@ roast_status_t scratch_alloc(Scratch& w, size_t bytes, cudaStream_t s) {
   // keep freed scratch in the device's default pool (release threshold: unlimited) instead of
   // returning it to the driver at every synchronisation: re-mapping it on the next call cost up to
   // hundreds of us of host time per call (seen as launch gaps in back-to-back LayerNorm backwards)
-  static bool kept[64] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64 && !kept[dev]) {
+  static std::atomic<unsigned long long> kept{0};
+  if (first_on_device(kept)) {
+    int dev = 0;
     cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t thr = ~uint64_t(0);
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     cudaGetLastError();
-    kept[dev] = true;
   }
   ROAST_CUDA_CHECK(cudaMallocAsync(&w.p, bytes, s));
   // test hook: fill new scratch with NaN (0xFFFFFFFF) so any slot a reader consumes before a

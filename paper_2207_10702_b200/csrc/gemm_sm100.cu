@@ -1594,12 +1594,11 @@ roast_status_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUten
                          int grid_pairs, cudaStream_t s, const WMapsHalf* hw = nullptr,
                          const CUtensorMap* act_map = nullptr) {
   using C = Cfg<CG, WM, NU, XBUF>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};   // smem opt-in, once per device
+  if (first_on_device(attr)) {
     cudaError_t e =
         cudaFuncSetAttribute(roast_mm_sm100<MODE, CG, WM, CHAIN, NU, ACT, XBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(smem)");
-    attr = true;
   }
   const int pairs = grid_pairs > 0 ? grid_pairs : std::min(p.units, num_sms() / CG);
   cudaLaunchConfig_t cfg = {};
@@ -2575,11 +2574,10 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
   }
   mp.flags = c->chain_flags + int64_t(c->chain_next++ % kChainSlots) * c->chain_slot_n;
   ROAST_CUDA_CHECK(cudaMemsetAsync(mp.flags, 0, size_t(need) * sizeof(int), s));
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};   // smem opt-in, once per device
+  if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(roast_mix_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, MIX_SMEM);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(mix smem)");
-    attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(pairs * 2));

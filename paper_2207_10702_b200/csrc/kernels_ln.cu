@@ -357,14 +357,13 @@ cudaError_t ln_bwd_launch(const void* dy, const void* s, const void* g, const fl
   const int vpl = (n / 8 + 31) / 32;
   const size_t smem = 2 * LN_BWD_WARPS * size_t(n) * sizeof(float);   // per warp (dg, db) partials
   const bool cs = rows >= 32768;   // inputs not L2-resident: streaming loads
-  // the smem opt-in once per instantiation (at the largest n): cudaFuncSetAttribute on every call
-  // cost ~50 us of host time and stalled the stream behind the kernel's previous launch
+  // the smem opt-in once per instantiation and device (at the largest n), not on every call
 #define ROAST_LN_BWD_CS(V, CSV)                                                                                \
   {                                                                                                             \
-    static bool opted = false;                                                                                  \
-    if (!opted)                                                                                                 \
-      opted = cudaFuncSetAttribute(ln_bwd_kernel<T, P, V, CSV>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                                   int(2 * LN_BWD_WARPS * 2048 * sizeof(float))) == cudaSuccess;                \
+    static std::atomic<unsigned long long> opted{0};                                                            \
+    if (first_on_device(opted))                                                                                 \
+      cudaFuncSetAttribute(ln_bwd_kernel<T, P, V, CSV>, cudaFuncAttributeMaxDynamicSharedMemorySize,            \
+                           int(2 * LN_BWD_WARPS * 2048 * sizeof(float)));                                       \
   }                                                                                                             \
   ln_bwd_kernel<T, P, V, CSV><<<unsigned(gr.blocks), LN_BWD_WARPS * 32, smem, st>>>(                           \
       static_cast<const T*>(dy), static_cast<const T*>(s), static_cast<const P*>(g), mean, rstd,               \

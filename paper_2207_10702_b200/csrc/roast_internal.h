@@ -1,5 +1,6 @@
 // roast_internal.h — handle state shared by the C-ABI layer and the kernels.
 #pragma once
+#include <atomic>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -239,6 +240,15 @@ constexpr int kChainSlots = 64;
 // share scratch and graph capture records alloc / free nodes.  The device's default
 // memory pool keeps freed blocks (release threshold set at roast_create), so steady-state calls
 // do not go back to the driver.
+// One-time per-device set-up (e.g. a kernel's shared-memory opt-in, which is per device): true
+// the first time it is called for the current device with this mask (one bit per device < 64).
+inline bool first_on_device(std::atomic<unsigned long long>& mask) {
+  int d = 0;
+  cudaGetDevice(&d);
+  const unsigned long long bit = 1ull << (d & 63);
+  return !(mask.fetch_or(bit) & bit);
+}
+
 struct Scratch {
   void* p = nullptr;
   cudaStream_t s = nullptr;
