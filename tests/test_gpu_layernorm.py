@@ -72,3 +72,40 @@ def test_layernorm_errors(torch):
     with pytest.raises(R.RoastError):
         R.roast_layernorm_fwd(buf.data_ptr(), buf.data_ptr(), buf.data_ptr(), buf.data_ptr(), buf.data_ptr(), None,
                               buf.data_ptr(), buf.data_ptr(), 1, 16, 1e-5, R.FP32, R.FP32)   # residual without s_out
+
+
+def test_layernorm_zero_rows(torch):
+    """rows = 0: the forward writes nothing; the backward's parameter gradients are zero (overwritten,
+    as for any row count) and nothing else is touched."""
+    from paper_2207_10702_b200 import roast as R
+    n = 768
+    g = torch.ones(n, device="cuda")
+    b = torch.zeros(n, device="cuda")
+    dg = torch.full((n,), 7.0, device="cuda")
+    db = torch.full((n,), 7.0, device="cuda")
+    buf = torch.empty(16, device="cuda")
+    R.roast_layernorm_fwd(buf.data_ptr(), None, g.data_ptr(), b.data_ptr(), buf.data_ptr(), None,
+                          buf.data_ptr(), buf.data_ptr(), 0, n, 1e-5, R.FP32, R.FP32)
+    R.roast_layernorm_bwd(buf.data_ptr(), buf.data_ptr(), g.data_ptr(), buf.data_ptr(), buf.data_ptr(), buf.data_ptr(),
+                          dg.data_ptr(), db.data_ptr(), 0, n, R.FP32, R.FP32)
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(dg) == 0 and torch.count_nonzero(db) == 0
+
+
+@pytest.mark.parametrize("rows", [1, 7, 2000, 2100])
+def test_layernorm_backward_row_ranges(torch, rows):
+    """The backward's per-warp row ranges (a fixed function of the row count: rows per warp 1 or 2
+    around 148 x 12 warps) against fp64 torch, parameter gradients reproducible."""
+    from paper_2207_10702_b200 import nn as RN
+    n = 256
+    gen = torch.Generator(device="cuda").manual_seed(rows)
+    x = torch.randn(rows, n, device="cuda", generator=gen).to(torch.bfloat16).requires_grad_(True)
+    dy = torch.randn(rows, n, device="cuda", generator=gen).to(torch.bfloat16)
+    ln = RN.LayerNorm(n, device="cuda", dtype=torch.bfloat16)
+    ln(x).backward(dy)
+    ref = torch.nn.LayerNorm(n, device="cuda", dtype=torch.float64)
+    xd = x.detach().double().requires_grad_(True)
+    ref(xd).backward(dy.double())
+    assert _rel(x.grad, xd.grad) <= 1e-2
+    assert _rel(ln.weight.grad, ref.weight.grad) <= 1e-2
+    assert _rel(ln.bias.grad, ref.bias.grad) <= 1e-2
