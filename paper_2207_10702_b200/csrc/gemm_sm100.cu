@@ -1064,6 +1064,7 @@ struct MixParams {
   int sched_len;
   int* flags;               // ready counters of the publishing problem's units
   int dep_n_tiles;          // n_tiles of the publishing problem (flag index = mb * this + nb)
+  int dep_m_tiles;          // ... and its m_tiles
   int* err;                 // sticky device error word
   long long* prof;
   int exp;                  // diagnostics only (ROAST_EXP in a ROAST_DIAG build): bit 0 no conversion math, bit 1 no TMEM loads
@@ -1079,7 +1080,14 @@ struct MixMaps {
 
 constexpr int MIX_THREADS = 384;
 constexpr int MIX_STAGES = 4;
-constexpr int MIX_A = 32768, MIX_B = 16384;          // per-stage A / B slots (DX sizes; DW uses 16 + 16 KB)
+constexpr int MIX_A = 32768, MIX_B = 16384;          // per-stage A / B slots of a DX k-block (32 + 16 KB)
+constexpr int MIX_STAGE = MIX_A + MIX_B;              // one stage: [A | B], 48 KB contiguous
+// A DW k-block spans MIX_DWBK tokens so that it fills a whole 48 KB stage too (X^T and dY boxes of
+// 2 x 64 columns x 96 tokens, 24 KB each): 50 % more weight-gradient operand bytes in flight than
+// 64-token blocks (16 + 16 KB of each 48 KB stage); the fused backward is latency-sensitive
+// (4 -> 3 stages: 120.8 -> 137.2 us)
+constexpr int MIX_DWBK = 96;
+constexpr int MIX_DW_BOX = 2 * MIX_DWBK * 128;        // bytes of one DW operand box (2 blocks of 64 columns)
 constexpr int MIX_SMEM = MIX_STAGES * (MIX_A + MIX_B) + 8 * 4096 + 1024 + 256 + KB_CHUNK * 4 * 4;
 
 __device__ __forceinline__ void mbar_arrive_cluster_n(uint32_t cluster_addr, uint32_t n) {
@@ -1099,8 +1107,9 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
   constexpr int CG = 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;                                           // [STAGES][32 KB]
-  uint8_t* sB = smem + MIX_STAGES * MIX_A;                      // [STAGES][16 KB]
+  // stage s = [A 32 KB | B 16 KB] at smem + s * MIX_STAGE (DW: [X^T 24 KB | dY 24 KB])
+  auto sA = [&](int st) { return smem + st * MIX_STAGE; };
+  auto sB = [&](int st) { return smem + st * MIX_STAGE + MIX_A; };
   uint8_t* sStage = smem + MIX_STAGES * (MIX_A + MIX_B);        // [8 warps][4 KB]
   uint64_t* full = reinterpret_cast<uint64_t*>(sStage + 8 * 4096);
   uint64_t* empty = full + MIX_STAGES;
@@ -1198,13 +1207,13 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
                   wait_ready(mp.flags + mb * mp.dep_n_tiles + (kb >> 2), 8 * CG, mp.err);
                   if (mp.prof) pw_dep += clock64() - t0;
                 }
-                tma_load_2d<CG>(&maps.a[prob], sA + s * MIX_A, fb, kb * BK, row0);
+                tma_load_2d<CG>(&maps.a[prob], sA(s), fb, kb * BK, row0);
               } else {
                 const int32_t* cc = sCoord + (kb - kc) * 4;
                 for (int j = 0; j < 2; ++j) {   // this CTA's two 64-row K-major B tiles (x = nb*4 + 2 rank + j, y = kb)
                   const int32_t c = cc[int(rank) * 2 + j];
                   const int row = (c >> 4) + ((c & 8) ? int(mp.neg_row) : 0) + rrow;
-                  tma_load_2d<CG>(&maps.shadow.m[c & 7], sB + s * MIX_B + j * 8192, fb, 0, row);
+                  tma_load_2d<CG>(&maps.shadow.m[c & 7], sB(s) + j * 8192, fb, 0, row);
                 }
               }
               if (++s == MIX_STAGES) {
@@ -1214,25 +1223,30 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
             }
           }
         }
-      } else {   // DW: X^T and dY as 3-D MN-major boxes (2 x 64-wide blocks each per CTA)
+      } else {   // DW: X^T and dY as 3-D MN-major boxes (2 x 64-wide blocks x MIX_DWBK tokens per CTA)
         const int row0 = mb * 256 + int(rank) * 128;
         const int col0 = nb * 256 + int(rank) * 128;
-        const uint32_t tx = uint32_t(CG * 16384);
+        const uint32_t tx = uint32_t(CG * MIX_DW_BOX);
+        int waited = -1;   // B producer: last m-block of the dependency waited for in this unit
         if (lane == 0) {
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&empty[s], ph ^ 1);
             const uint32_t fb = map_to_rank(smem_u32(&full[s]), 0);
             if (leader) mbar_expect_tx(&full[s], tx);
             if (pa) {
-              tma_load_3d<CG>(&maps.a[prob], sA + s * MIX_A, fb, 0, kb * BK, row0 >> 6);
+              tma_load_3d<CG>(&maps.a[prob], sA(s), fb, 0, kb * MIX_DWBK, row0 >> 6);
             } else {
-              // B = the dependency's output rows kb*64.. (its m-block kb / 8), columns of tile nb
-              if (P.dep >= 0 && (kb == kb0 || (kb & 7) == 0)) {
-                const long long t0 = mp.prof ? clock64() : 0;
-                wait_ready(mp.flags + (kb >> 3) * mp.dep_n_tiles + nb, 8 * CG, mp.err);
-                if (mp.prof) pw_dep += clock64() - t0;
+              // B = the dependency's output rows kb*MIX_DWBK.. (512-row m-blocks), columns of tile nb
+              if (P.dep >= 0) {
+                const int mlast = min((kb * MIX_DWBK + MIX_DWBK - 1) >> 9, mp.dep_m_tiles - 1);
+                for (int mbk = max((kb * MIX_DWBK) >> 9, waited + 1); mbk <= mlast; ++mbk) {
+                  const long long t0 = mp.prof ? clock64() : 0;
+                  wait_ready(mp.flags + mbk * mp.dep_n_tiles + nb, 8 * CG, mp.err);
+                  if (mp.prof) pw_dep += clock64() - t0;
+                  waited = mbk;
+                }
               }
-              tma_load_3d<CG>(&maps.b[prob], sB + s * MIX_B, fb, 0, kb * BK, col0 >> 6);
+              tma_load_3d<CG>(&maps.b[prob], sA(s) + MIX_DW_BOX, fb, 0, kb * MIX_DWBK, col0 >> 6);
             }
             if (++s == MIX_STAGES) {
               s = 0;
@@ -1272,8 +1286,8 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
             mbar_wait(&full[s], ph);
             if (mp.prof) mw_full += clock64() - t0;
             tc_fence_after();
-            const uint32_t a0 = smem_u32(sA + s * MIX_A);
-            const uint32_t b0 = smem_u32(sB + s * MIX_B);
+            const uint32_t a0 = smem_u32(sA(s));
+            const uint32_t b0 = smem_u32(sB(s));
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
               const uint64_t bd = sw128_desc(b0 + k * 32, 16, 1024);   // K-major B
@@ -1304,12 +1318,14 @@ __global__ void __launch_bounds__(MIX_THREADS, 1)
             mbar_wait(&full[s], ph);
             if (mp.prof) mw_full_dw += clock64() - t0;
             tc_fence_after();
-            const uint32_t a0 = smem_u32(sA + s * MIX_A);
-            const uint32_t b0 = smem_u32(sB + s * MIX_B);
+            const uint32_t a0 = smem_u32(sA(s));
+            const uint32_t b0 = a0 + MIX_DW_BOX;
+            // MN-major operands: LBO = the next 64-column block (MIX_DWBK rows of 128 B), SBO = the
+            // next 8 token rows
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              tc_mma<CG>(d, sw128_desc(a0 + k * 2048, 8192, 1024), sw128_desc(b0 + k * 2048, 8192, 1024), idesc_dw,
-                         (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < MIX_DWBK / 16; ++k)
+              tc_mma<CG>(d, sw128_desc(a0 + k * 2048, MIX_DWBK * 128, 1024),
+                         sw128_desc(b0 + k * 2048, MIX_DWBK * 128, 1024), idesc_dw, (kb > kb0 || k > 0) ? 1u : 0u);
             tc_commit<CG>(&empty[s]);
             if (++s == MIX_STAGES) {
               s = 0;
@@ -2271,7 +2287,7 @@ MixPlan plan_mix(int mt0, int nt0, int kb0, int mt1, int nt1, int kbT, int mt2, 
   // 0.7 give the same schedule); a unit's drain EPI_*.  ROAST_MIX_{DWK,EPI_DX,EPI_DW} override.
   auto envd = [](const char* k, double d) { const char* e = getenv(k); return e ? atof(e) : d; };
   const double EPI_DX = envd("ROAST_MIX_EPI_DX", 3.0), EPI_DW = envd("ROAST_MIX_EPI_DW", 1.0), LAT = 1.0;
-  const double DWK = envd("ROAST_MIX_DWK", 0.6);
+  const double DWK = envd("ROAST_MIX_DWK", 0.6) * MIX_DWBK / 64.0;   // per DW k-block of MIX_DWBK tokens
   MixPlan best;
   const int units0 = mt0 * nt0;
   for (int s : {1, 2, 3, 4}) {
@@ -2303,18 +2319,21 @@ MixPlan plan_mix(int mt0, int nt0, int kb0, int mt1, int nt1, int kbT, int mt2, 
           k0 = split * kps;
           k1 = std::min(k0 + kps, kbT);
         };
+        // a DW k-block k of P3 reads dY_a tokens [k MIX_DWBK, (k + 1) MIX_DWBK): P0 m-blocks of 512
+        auto mblk = [&](int64_t tok) { return std::min(int(tok >> 9), mt0 - 1); };
         auto p3_ready = [&](int u) {
           int k0, k1, nb;
           p3_range(u, k0, k1, nb);
-          return fin0[std::min(k0 >> 3, mt0 - 1) * nt0 + nb] + LAT;
+          return fin0[mblk(int64_t(k0) * MIX_DWBK) * nt0 + nb] + LAT;
         };
         auto p3_finish = [&](int u, double t) {
           int k0, k1, nb;
           p3_range(u, k0, k1, nb);
-          for (int k = k0; k < k1; k += 8) {
-            const int ke = std::min(k1, (k & ~7) + 8);
-            t = std::max(t, fin0[std::min(k >> 3, mt0 - 1) * nt0 + nb] + LAT) + DWK * (ke - k);
-            k = (k & ~7);
+          for (int k = k0; k < k1; ++k) {
+            double ready = 0;
+            for (int m = mblk(int64_t(k) * MIX_DWBK); m <= mblk(int64_t(k) * MIX_DWBK + MIX_DWBK - 1); ++m)
+              ready = std::max(ready, fin0[m * nt0 + nb] + LAT);
+            t = std::max(t, ready) + DWK;
           }
           return t + EPI_DW;
         };
@@ -2396,7 +2415,7 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
   const bool det = c->cfg.deterministic != 0;
   if (ma.H % 256 || ma.O % 256 || mbm.O % 256 || mbm.H != ma.O || !dX_a) return ROAST_ERR_UNSUPPORTED;
   const int pairs = num_sms() / 2;
-  const int mtT = int((T + 511) / 512), kbT = int((T + BK - 1) / BK);
+  const int mtT = int((T + 511) / 512), kbT = int((T + MIX_DWBK - 1) / MIX_DWBK);   // DW k-blocks of MIX_DWBK tokens
   const std::array<int64_t, 6> key{det ? 3 : 2, ma.H, ma.O, mbm.H, mbm.O, T};   // det plans differ (split cost)
   auto it = c->chain_plans.find(key);
   static std::map<std::array<int64_t, 6>, std::pair<int, int>> splits;   // plan key -> (s1, s3)
@@ -2480,9 +2499,9 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
     P.dep = -1;
     P.ntiles = m.nx * m.ny;
     P.ws_slot = -1;
-    roast_status_t r = make_map_blocks(&maps.a[pi], X, uint64_t(m.H), uint64_t(T), BK, 2);
+    roast_status_t r = make_map_blocks(&maps.a[pi], X, uint64_t(m.H), uint64_t(T), MIX_DWBK, 2);
     if (r) return r;
-    return make_map_blocks(&maps.b[pi], dY, uint64_t(m.O), uint64_t(T), BK, 2);
+    return make_map_blocks(&maps.b[pi], dY, uint64_t(m.O), uint64_t(T), MIX_DWBK, 2);
   };
   if ((st = dx_prob(mp.p[0], mbm, dY_b, dY_a, 0))) return st;
   if (act) {   // dY_a = (dY_b W_b^T) * act'(U): U is layer a's pre-activation, [T x a.O]
@@ -2518,6 +2537,7 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
     }
   }
   mp.dep_n_tiles = mp.p[0].n_tiles;
+  mp.dep_m_tiles = mp.p[0].m_tiles;
   mp.neg_row = c->neg_base / 64;
   mp.reps = c->shadow_reps;
   mp.rep_rows = int(c->shadow_elems / 64);
