@@ -320,6 +320,14 @@ roast_status_t roast_layernorm_bwd(const void* d_dy, const void* d_s, const void
  * mode sums every slot in a fixed order (bitwise reproducible). */
 roast_status_t roast_linear_bwd(roast_t h, int32_t id, const void* d_X, const void* d_dY, void* d_dX,
                                 int64_t tokens, roast_dtype_t dt, roast_stream_t stream);
+/* roast_linear_bwd_fused: the same result as roast_linear_bwd with dX (dX overwritten, dM +=),
+ * computed on the tcgen05 path by ONE persistent launch that co-schedules the dX GEMM's and the
+ * dM GEMM's units over the CTA pairs when its plan beats the two launches (small token counts:
+ * a 768-wide dX has 48 units of 512 x 256 for 74 pairs), else by the two launches.  dX is
+ * required (ROAST_ERR_CONFIG if NULL).  Fast mode only; in deterministic mode it is exactly
+ * roast_linear_bwd.  Plans are made on an eager call (not under stream capture). */
+roast_status_t roast_linear_bwd_fused(roast_t h, int32_t id, const void* d_X, const void* d_dY, void* d_dX,
+                                      int64_t tokens, roast_dtype_t dt, roast_stream_t stream);
 
 /* The two halves of roast_linear_bwd, for callers that overlap them on two
  * streams (dX is on the critical path of the previous layer, dM is not):

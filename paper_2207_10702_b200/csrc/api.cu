@@ -778,6 +778,20 @@ roast_status_t roast_linear_bwd_dm(roast_t h, int32_t id, const void* X, const v
   return ROAST_OK;
 }
 
+roast_status_t roast_linear_bwd_fused(roast_t h, int32_t id, const void* X, const void* dY, void* dX, int64_t T,
+                                      roast_dtype_t dt, roast_stream_t stream) {
+  Ctx* c = ctx(h);
+  Module* m;
+  roast_status_t st = linear_args(c, id, T, dt, X, dY, &m);
+  if (st || T == 0) return st;
+  if (!dX) return fail(ROAST_ERR_CONFIG, "bwd_fused: dX is required");
+  if (dt == ROAST_BF16 && use_sm100(c, *m)) {
+    st = sm100_bwd_fused1(c, *m, X, dY, dX, T, reinterpret_cast<cudaStream_t>(stream));
+    if (st != ROAST_ERR_UNSUPPORTED) return st;
+  }
+  return roast_linear_bwd(h, id, X, dY, dX, T, dt, stream);   // the two launches
+}
+
 roast_status_t roast_linear_bwd(roast_t h, int32_t id, const void* X, const void* dY, void* dX, int64_t T,
                                 roast_dtype_t dt, roast_stream_t stream) {
   Ctx* c = ctx(h);

@@ -2384,6 +2384,53 @@ MixPlan plan_mix(int mt0, int nt0, int kb0, int mt1, int nt1, int kbT, int mt2, 
   }
   return best;
 }
+
+// One linear's backward, dX and dM, as one launch (roast_linear_bwd_fused): P0 = the dX units
+// (512 x 256, kbx k-blocks), P1 = the dM units (256 x 256 per split, kbT DW k-blocks of MIX_DWBK
+// tokens), no dependency between them.  Longest-first list scheduling over the pairs for each
+// split count 1-8; `separate` = the two launches' own quantised makespans back to back (dX, then dM
+// at its best split), for the caller's fused-or-not decision.  Same cost units as plan_mix.
+MixPlan plan_mix1(int mtx, int ntx, int kbx, int mtw, int ntw, int kbT, int npairs) {
+  auto envd = [](const char* k, double d) { const char* e = getenv(k); return e ? atof(e) : d; };
+  const double EPI_DX = envd("ROAST_MIX_EPI_DX", 3.0), EPI_DW = envd("ROAST_MIX_EPI_DW", 1.0);
+  const double DWK = envd("ROAST_MIX_DWK", 0.6) * MIX_DWBK / 64.0;
+  const int ux = mtx * ntx;
+  const double cx = kbx + EPI_DX;
+  MixPlan best;
+  double dw_alone = 1e30;
+  for (int sp0 = 1; sp0 <= 8; ++sp0) {
+    const int kps = (kbT + sp0 - 1) / sp0;
+    const int sp = (kbT + kps - 1) / kps;
+    const int uw = mtw * ntw * sp;
+    const double cw = DWK * kps + EPI_DW;
+    dw_alone = std::min(dw_alone, double((uw + npairs - 1) / npairs) * cw);
+    std::vector<double> free_t(npairs, 0.0);
+    std::vector<std::vector<int32_t>> lists(npairs);
+    auto pick = [&]() { return int(std::min_element(free_t.begin(), free_t.end()) - free_t.begin()); };
+    for (int u = 0; u < ux; ++u) {   // the longer units first
+      const int q = pick();
+      free_t[q] += cx;
+      lists[q].push_back(u);
+    }
+    for (int u = 0; u < uw; ++u) {
+      const int q = pick();
+      free_t[q] += cw;
+      lists[q].push_back((1 << 24) | u);
+    }
+    const double mk = *std::max_element(free_t.begin(), free_t.end());
+    if (mk < best.makespan - 1e-9) {
+      best.makespan = mk;
+      best.s1 = sp;
+      best.len = 0;
+      for (auto& l : lists) best.len = std::max<int>(best.len, int(l.size()));
+      best.sched.assign(size_t(npairs) * best.len, -1);
+      for (int q = 0; q < npairs; ++q)
+        for (size_t i = 0; i < lists[q].size(); ++i) best.sched[size_t(q) * best.len + i] = lists[q][i];
+    }
+  }
+  best.separate = double((ux + npairs - 1) / npairs) * cx + dw_alone;
+  return best;
+}
 }  // namespace
 
 // dM += sum of the fused backward's dM replicas, replicas zeroed: atomic exchange / add, so a
@@ -2403,6 +2450,107 @@ __global__ void fold_dm_replicas_kernel(float* __restrict__ dM, float* __restric
 static int dm_replicas(const Ctx* c) {
   if (const char* e = getenv("ROAST_DM_REPS")) return std::max(1, std::min(74, atoi(e)));
   return c->mem_size * int64_t(sizeof(float)) <= (int64_t(64) << 10) ? 16 : 1;
+}
+
+// The launch shared by the fused backwards (roast_mix_sm100): shadow / dM views (dM replicas in
+// fast mode at tiny |M|), ready counters, the launch with PDL, and the replica fold after it.
+// `prof` (ROAST_PROF) receives the per-CTA counters.
+static long long* mix_prof = nullptr;
+static roast_status_t mix_launch(Ctx* c, MixMaps& maps, MixParams& mp, const int32_t* sched, int sched_len, bool det,
+                                 int pairs, cudaStream_t s) {
+  roast_status_t st = ROAST_OK;
+  long long*& prof = mix_prof;
+  mp.neg_row = c->neg_base / 64;
+  mp.reps = c->shadow_reps;
+  mp.rep_rows = int(c->shadow_elems / 64);
+  mp.sched = sched;
+  mp.sched_len = sched_len;
+  mp.err = c->d_err;
+  if (const char* e = getenv("ROAST_EXP")) mp.exp = atoi(e);
+  maps.shadow = *reinterpret_cast<const WMaps*>(c->tmap_shadow);
+  WMaps& dmaps = *reinterpret_cast<WMaps*>(c->tmap_dm);
+  if (c->tmap_dm_for != c->dM) {   // dM as 8 fp32 phase views (cached until dM is rebound)
+    for (int r = 0; r < 8; ++r) {
+      const int64_t elems = c->mem_size - 8 * r;
+      st = make_map_2d(&dmaps.m[r], c->dM + 8 * r, 64, uint64_t(elems / 64), 256, 32, 32, true);
+      if (st) return st;
+    }
+    c->tmap_dm_for = c->dM;
+  }
+  maps.dm = dmaps;
+  mp.dm_reps = 1;
+  mp.dm_rep_rows = 0;
+  if (!det) {
+    if (c->dm_reps == 0) c->dm_reps = dm_replicas(c);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (c->dm_reps > 1 && !c->dm_rep && cudaStreamIsCapturing(s, &cs) == cudaSuccess &&
+        cs == cudaStreamCaptureStatusNone) {   // allocated on an eager call (not under capture)
+      c->dm_rep_elems = (c->mem_size + 63) / 64 * 64;
+      const size_t bytes = size_t(c->dm_reps) * size_t(c->dm_rep_elems) * sizeof(float);
+      ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->dm_rep), bytes));
+      ROAST_CUDA_CHECK(cudaMemsetAsync(c->dm_rep, 0, bytes, s));
+      WMaps& rm = *reinterpret_cast<WMaps*>(c->tmap_dmrep);
+      for (int r = 0; r < 8; ++r) {
+        const int64_t elems = int64_t(c->dm_reps) * c->dm_rep_elems - 8 * r;
+        if ((st = make_map_2d(&rm.m[r], c->dm_rep + 8 * r, 64, uint64_t(elems / 64), 256, 32, 32, true))) return st;
+      }
+    }
+    if (c->dm_reps > 1 && c->dm_rep) {
+      maps.dm = *reinterpret_cast<const WMaps*>(c->tmap_dmrep);
+      mp.dm_reps = c->dm_reps;
+      mp.dm_rep_rows = int(c->dm_rep_elems / 64);
+    }
+  }
+  // ready counters of P0's units: the next slot of the chain ring (as sm100_chain)
+  const int64_t need = std::max(1, mp.p[0].units);
+  if (c->chain_slot_n < need) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+      return ROAST_ERR_UNSUPPORTED;
+    ROAST_CUDA_CHECK(cudaDeviceSynchronize());
+    cudaFree(c->chain_flags);
+    c->chain_flags = nullptr;
+    c->chain_slot_n = 0;
+    ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->chain_flags), size_t(kChainSlots) * need * sizeof(int)));
+    c->chain_slot_n = need;
+  }
+  mp.flags = c->chain_flags + int64_t(c->chain_next++ % kChainSlots) * c->chain_slot_n;
+  ROAST_CUDA_CHECK(cudaMemsetAsync(mp.flags, 0, size_t(need) * sizeof(int), s));
+  static std::atomic<unsigned long long> attr{0};   // smem opt-in, once per device
+  if (first_on_device(attr)) {
+    cudaError_t e = cudaFuncSetAttribute(roast_mix_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, MIX_SMEM);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(mix smem)");
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(pairs * 2));
+  cfg.blockDim = dim3(MIX_THREADS);
+  cfg.dynamicSmemBytes = MIX_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  static const bool pdl = !(getenv("ROAST_PDL") && atoi(getenv("ROAST_PDL")) == 0);
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 2 : 1;
+  if (getenv("ROAST_PROF")) {   // debug: per-role wait counters, printed after a synchronising launch
+    if (!prof) cudaMallocManaged(&prof, sizeof(long long) * 8 * 512);
+    cudaMemset(prof, 0, sizeof(long long) * 8 * 512);
+    mp.prof = prof;
+  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mix_sm100, maps, mp);
+  if (e != cudaSuccess) return cuda_fail(e, "roast_mix_sm100 launch");
+  if (mp.dm_reps > 1) {
+    const int64_t n = c->mem_size;
+    fold_dm_replicas_kernel<<<unsigned(std::min<int64_t>((n + 255) / 256, 1184)), 256, 0, s>>>(
+        c->dM, c->dm_rep, n, mp.dm_reps, c->dm_rep_elems);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fold dM replicas");
+    c->launches += 1;
+  }
+  return ROAST_OK;
 }
 
 roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, const void* X_a, const void* Y_a,
@@ -2538,97 +2686,9 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
   }
   mp.dep_n_tiles = mp.p[0].n_tiles;
   mp.dep_m_tiles = mp.p[0].m_tiles;
-  mp.neg_row = c->neg_base / 64;
-  mp.reps = c->shadow_reps;
-  mp.rep_rows = int(c->shadow_elems / 64);
-  mp.sched = it->second.first;
-  mp.sched_len = it->second.second;
-  mp.err = c->d_err;
-  if (const char* e = getenv("ROAST_EXP")) mp.exp = atoi(e);
-  maps.shadow = *reinterpret_cast<const WMaps*>(c->tmap_shadow);
-  WMaps& dmaps = *reinterpret_cast<WMaps*>(c->tmap_dm);
-  if (c->tmap_dm_for != c->dM) {   // dM as 8 fp32 phase views (cached until dM is rebound)
-    for (int r = 0; r < 8; ++r) {
-      const int64_t elems = c->mem_size - 8 * r;
-      st = make_map_2d(&dmaps.m[r], c->dM + 8 * r, 64, uint64_t(elems / 64), 256, 32, 32, true);
-      if (st) return st;
-    }
-    c->tmap_dm_for = c->dM;
-  }
-  maps.dm = dmaps;
-  mp.dm_reps = 1;
-  mp.dm_rep_rows = 0;
-  if (!det) {
-    if (c->dm_reps == 0) c->dm_reps = dm_replicas(c);
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (c->dm_reps > 1 && !c->dm_rep && cudaStreamIsCapturing(s, &cs) == cudaSuccess &&
-        cs == cudaStreamCaptureStatusNone) {   // allocated on an eager call (not under capture)
-      c->dm_rep_elems = (c->mem_size + 63) / 64 * 64;
-      const size_t bytes = size_t(c->dm_reps) * size_t(c->dm_rep_elems) * sizeof(float);
-      ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->dm_rep), bytes));
-      ROAST_CUDA_CHECK(cudaMemsetAsync(c->dm_rep, 0, bytes, s));
-      WMaps& rm = *reinterpret_cast<WMaps*>(c->tmap_dmrep);
-      for (int r = 0; r < 8; ++r) {
-        const int64_t elems = int64_t(c->dm_reps) * c->dm_rep_elems - 8 * r;
-        if ((st = make_map_2d(&rm.m[r], c->dm_rep + 8 * r, 64, uint64_t(elems / 64), 256, 32, 32, true))) return st;
-      }
-    }
-    if (c->dm_reps > 1 && c->dm_rep) {
-      maps.dm = *reinterpret_cast<const WMaps*>(c->tmap_dmrep);
-      mp.dm_reps = c->dm_reps;
-      mp.dm_rep_rows = int(c->dm_rep_elems / 64);
-    }
-  }
-  // ready counters of P0's units: the next slot of the chain ring (as sm100_chain)
-  const int64_t need = mp.p[0].units;
-  if (c->chain_slot_n < need) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
-      return ROAST_ERR_UNSUPPORTED;
-    ROAST_CUDA_CHECK(cudaDeviceSynchronize());
-    cudaFree(c->chain_flags);
-    c->chain_flags = nullptr;
-    c->chain_slot_n = 0;
-    ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&c->chain_flags), size_t(kChainSlots) * need * sizeof(int)));
-    c->chain_slot_n = need;
-  }
-  mp.flags = c->chain_flags + int64_t(c->chain_next++ % kChainSlots) * c->chain_slot_n;
-  ROAST_CUDA_CHECK(cudaMemsetAsync(mp.flags, 0, size_t(need) * sizeof(int), s));
-  static std::atomic<unsigned long long> attr{0};   // smem opt-in, once per device
-  if (first_on_device(attr)) {
-    cudaError_t e = cudaFuncSetAttribute(roast_mix_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, MIX_SMEM);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(mix smem)");
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(pairs * 2));
-  cfg.blockDim = dim3(MIX_THREADS);
-  cfg.dynamicSmemBytes = MIX_SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
-  static const bool pdl = !(getenv("ROAST_PDL") && atoi(getenv("ROAST_PDL")) == 0);
-  cfg.attrs = at;
-  cfg.numAttrs = pdl ? 2 : 1;
-  static long long* prof = nullptr;
-  if (getenv("ROAST_PROF")) {   // debug: per-role wait counters, printed after a synchronising launch
-    if (!prof) cudaMallocManaged(&prof, sizeof(long long) * 8 * 512);
-    cudaMemset(prof, 0, sizeof(long long) * 8 * 512);
-    mp.prof = prof;
-  }
-  cudaError_t e = cudaLaunchKernelEx(&cfg, roast_mix_sm100, maps, mp);
-  if (e != cudaSuccess) return cuda_fail(e, "roast_mix_sm100 launch");
-  if (mp.dm_reps > 1) {
-    const int64_t n = c->mem_size;
-    fold_dm_replicas_kernel<<<unsigned(std::min<int64_t>((n + 255) / 256, 1184)), 256, 0, s>>>(
-        c->dM, c->dm_rep, n, mp.dm_reps, c->dm_rep_elems);
-    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fold dM replicas");
-    c->launches += 1;
-  }
+  if ((st = mix_launch(c, maps, mp, it->second.first, it->second.second, det, pairs, s))) return st;
+  cudaError_t e = cudaSuccess;
+  long long* prof = mix_prof;
   if (det) {   // fixed order: module b's slots, then module a's (each: covering tiles, then splits)
     const int sp_b = mp.p[1].units / (mp.p[1].m_tiles * mp.p[1].n_tiles);
     const int sp_a = mp.p[3].units / (mp.p[3].m_tiles * mp.p[3].n_tiles);
@@ -2650,6 +2710,114 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
             acc[0] / (2 * pairs), mx, acc[2] / pairs, acc[4] / pairs, acc[3] / pairs,
             acc[5] / pairs, acc[6] / (acc[7] > 0 ? acc[7] : 1), acc[1] / (acc[7] > 0 ? acc[7] : 1));
   }
+  c->launches++;
+  return ROAST_OK;
+}
+// roast_linear_bwd_fused: one linear's dX GEMM and dM GEMM co-scheduled in one roast_mix_sm100
+// launch when the plan beats the two launches by >= 5 % (small token counts, where a 768-wide dX
+// has 48 units for 74 CTA pairs), else ROAST_ERR_UNSUPPORTED (the caller runs the two calls).
+// Fast mode only (deterministic mode keeps the fixed-order reduce of the separate dM launch).
+roast_status_t sm100_bwd_fused1(Ctx* c, const Module& m, const void* X, const void* dY, void* dX, int64_t T,
+                                cudaStream_t s) {
+  using namespace sm100;
+  if (!supported(c, m) || cta_group() != 2 || T <= 0 || T >= (int64_t(1) << 31) || c->cfg.deterministic || !dX ||
+      getenv("ROAST_NO_BWD_FUSE"))
+    return ROAST_ERR_UNSUPPORTED;
+  if (m.H % 256 || m.O % 256) return ROAST_ERR_UNSUPPORTED;
+  const int pairs = num_sms() / 2;
+  const int mtT = int((T + 511) / 512), kbT = int((T + MIX_DWBK - 1) / MIX_DWBK);
+  const std::array<int64_t, 6> key{4, m.H, m.O, 0, 0, T};   // the plan depends on the shape only
+  auto it = c->chain_plans.find(key);
+  static std::map<std::array<int64_t, 6>, int> splits;
+  if (it == c->chain_plans.end()) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+      return ROAST_ERR_UNSUPPORTED;   // plan on an eager call first
+    bool resident = false;
+    {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(unsigned(2 * pairs));
+      q.blockDim = dim3(MIX_THREADS);
+      q.dynamicSmemBytes = MIX_SMEM;
+      cudaLaunchAttribute a[1];
+      a[0].id = cudaLaunchAttributeClusterDimension;
+      a[0].val.clusterDim.x = 2;
+      a[0].val.clusterDim.y = 1;
+      a[0].val.clusterDim.z = 1;
+      q.attrs = a;
+      q.numAttrs = 1;
+      int ncl = 0;
+      if (cudaFuncSetAttribute(roast_mix_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, MIX_SMEM) == cudaSuccess &&
+          cudaOccupancyMaxActiveClusters(&ncl, roast_mix_sm100, &q) == cudaSuccess)
+        resident = ncl >= pairs;
+      cudaGetLastError();
+    }
+    MixPlan plan = plan_mix1(mtT, int(m.H / 256), int(m.O / BK), int(m.H / 256), int(m.O / 256), kbT, pairs);
+    int32_t* d = nullptr;
+    const bool pays = getenv("ROAST_FUSE1_ALWAYS") != nullptr || plan.makespan < 0.95 * plan.separate;
+    if (resident && pays) {
+      ROAST_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&d), plan.sched.size() * sizeof(int32_t)));
+      ROAST_CUDA_CHECK(cudaMemcpy(d, plan.sched.data(), plan.sched.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    if (getenv("ROAST_VERBOSE"))
+      fprintf(stderr, "[roast] bwd fused1 %lld x %lld, T %lld: makespan %.1f vs separate %.1f, split %d, used %d\n",
+              (long long)m.H, (long long)m.O, (long long)T, plan.makespan, plan.separate, plan.s1, int(d != nullptr));
+    it = c->chain_plans.emplace(key, std::make_pair(d, plan.len)).first;
+    splits[key] = plan.s1;
+  }
+  if (!it->second.first) return ROAST_ERR_UNSUPPORTED;
+  roast_status_t st = sm100_prepare(c);
+  if (st) return st;
+  const int sp = splits[key];
+  MixMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  MixParams mp;
+  memset(&mp, 0, sizeof(mp));
+  MixProb& P = mp.p[0];   // dX = lambda dY W~^T
+  P.mode = DX;
+  P.M = int(T);
+  P.N = int(m.H);
+  P.K = int(m.O);
+  P.m_tiles = mtT;
+  P.n_tiles = int(m.H / 256);
+  P.k_blocks = int(m.O / BK);
+  P.kb_per_split = P.k_blocks;
+  P.units = P.m_tiles * P.n_tiles;
+  P.coord = m.d_coord_yx;
+  P.coord_ld = m.nx;
+  P.lam = m.lam;
+  P.dep = -1;
+  P.ws_slot = -1;
+  if ((st = make_map_2d(&maps.a[0], dY, uint64_t(m.O), uint64_t(T), uint64_t(m.O) * 2, BK, 256))) return st;
+  if ((st = make_map_2d(&maps.b[0], dX, uint64_t(m.H), uint64_t(T), uint64_t(m.H) * 2, 64, 32))) return st;
+  MixProb& W = mp.p[1];   // dM += scatter(lambda g X^T dY)
+  W.mode = DW;
+  W.M = int(m.H);
+  W.N = int(m.O);
+  W.K = int(T);
+  W.m_tiles = int(m.H / 256);
+  W.n_tiles = int(m.O / 256);
+  W.k_blocks = kbT;
+  W.kb_per_split = (kbT + sp - 1) / sp;
+  W.units = W.m_tiles * W.n_tiles * ((kbT + W.kb_per_split - 1) / W.kb_per_split);
+  W.off = m.d_off;
+  W.sgn = m.d_sgn;
+  W.ny = m.ny;
+  W.lam = m.lam;
+  W.dep = -1;
+  W.ntiles = m.nx * m.ny;
+  W.ws_slot = -1;
+  if ((st = make_map_blocks(&maps.a[1], X, uint64_t(m.H), uint64_t(T), MIX_DWBK, 2))) return st;
+  if ((st = make_map_blocks(&maps.b[1], dY, uint64_t(m.O), uint64_t(T), MIX_DWBK, 2))) return st;
+  for (int k = 2; k < 4; ++k) {   // unused problem slots: valid descriptors (prefetched), no units
+    maps.a[k] = maps.a[0];
+    maps.b[k] = maps.b[0];
+    mp.p[k].ws_slot = -1;
+    mp.p[k].dep = -1;
+  }
+  mp.dep_n_tiles = 1;
+  mp.dep_m_tiles = 1;
+  if ((st = mix_launch(c, maps, mp, it->second.first, it->second.second, false, pairs, s))) return st;
   c->launches++;
   return ROAST_OK;
 }

@@ -316,6 +316,10 @@ roast_status_t sm100_dx_act(Ctx* c, const Module& m, const void* dY, const void*
 // launch: dY_a = dY_b W_b^T, dM += b(Y_a, dY_b), dX_a = dY_a W_a^T, dM += a(X_a, dY_a), the four
 // GEMMs co-scheduled (gemm_sm100.cu roast_mix_sm100).  ROAST_ERR_UNSUPPORTED when the shapes /
 // mode do not allow it (the caller then makes the four launches).
+// one linear's dX and dM GEMMs co-scheduled in one launch (small token counts); UNSUPPORTED when
+// the plan does not beat the two launches, the geometry is not 256-aligned, or in deterministic mode
+roast_status_t sm100_bwd_fused1(Ctx* c, const Module& m, const void* X, const void* dY, void* dX, int64_t T,
+                                cudaStream_t s);
 roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mb, const void* X_a, const void* Y_a,
                                const void* dY_b, void* dY_a, void* dX_a, int64_t T, cudaStream_t s, int act = 0,
                                const void* U = nullptr);

@@ -51,25 +51,31 @@ class ResidualGrad:
 RESIDUAL_FUSE_MIN_TOKENS = 32768
 
 
-def _dx_plus_residual(store, mid, dy2, box, like):
-    """dX of module `mid` for dy2, plus the residual gradient left in `box` (fused when possible)."""
+def _linear_backward(store, mid, x2, dy2, box, need_dx):
+    """dM += module `mid`'s gradient for (x2, dy2) and, if need_dx, its dX plus the residual
+    gradient left in `box`.  Large token counts: the residual added in the dX epilogue, dM
+    separately; otherwise dX and dM from roast_linear_bwd_fused (one co-scheduled launch where
+    that pays: a 768-wide dX alone fills 48 of 74 CTA pairs at 8192 tokens) and the residual
+    added after."""
     r = box.take() if box is not None else None
-    if r is not None and like.shape[0] < RESIDUAL_FUSE_MIN_TOKENS:
-        dx = torch.empty_like(like)
-        store.bwd_dx(mid, dy2, dx)
-        return dx.add_(r.reshape(like.shape))
-    if r is not None:
-        r2 = r.reshape(like.shape).contiguous()
+    if not need_dx:
+        store.bwd_dm(mid, x2, dy2)
+        return None
+    if r is not None and x2.shape[0] >= RESIDUAL_FUSE_MIN_TOKENS:
+        r2 = r.reshape(x2.shape).contiguous()
         try:
-            return store.bwd_dx_act(mid, dy2, r2, act=R.ACT_RESIDUAL)
+            dx = store.bwd_dx_act(mid, dy2, r2, act=R.ACT_RESIDUAL)
         except R.RoastError as e:
             if e.status != R.ERR_UNSUPPORTED:
                 raise
-            dx = torch.empty_like(like)
+            dx = torch.empty_like(x2)
             store.bwd_dx(mid, dy2, dx)
-            return dx + r2
-    dx = torch.empty_like(like)
-    store.bwd_dx(mid, dy2, dx)
+            dx = dx + r2
+        store.bwd_dm(mid, x2, dy2)
+        return dx
+    dx = store.bwd_fused(mid, x2, dy2)
+    if r is not None:
+        dx.add_(r.reshape(x2.shape))
     return dx
 
 
@@ -93,11 +99,8 @@ class _LinearFn(torch.autograd.Function):
         (x2,) = ctx.saved_tensors
         store, mid = ctx.store, ctx.mid
         dy2 = dy.reshape(x2.shape[0], -1).contiguous().to(x2.dtype)
-        dx = None
-        if ctx.needs_input_grad[0]:
-            dx = torch.empty_like(x2)
-            store.bwd_dx(mid, dy2, dx)
-        store.bwd_dm(mid, x2, dy2)          # dM += lambda g X^T dY scattered into M's slots
+        # dM += lambda g X^T dY scattered into M's slots, and dX
+        dx = _linear_backward(store, mid, x2, dy2, None, ctx.needs_input_grad[0])
         if ctx.bias_mid is not None:
             store.bias_grad(ctx.bias_mid, dy2)
         return (dx.reshape(ctx.shape) if dx is not None else None), None, None, None, None
@@ -123,10 +126,8 @@ class _LinearGroupFn(torch.autograd.Function):
         (x2,) = ctx.saved_tensors
         store, gid = ctx.store, ctx.gid
         dy2 = dy.reshape(x2.shape[0], -1).contiguous().to(x2.dtype)
-        dx = None
-        if ctx.needs_input_grad[0]:
-            dx = _dx_plus_residual(store, gid, dy2, ctx.box, x2)   # + the residual gradient, if handed off
-        store.bwd_dm(gid, x2, dy2)
+        # dM, and dX + the residual gradient if handed off
+        dx = _linear_backward(store, gid, x2, dy2, ctx.box, ctx.needs_input_grad[0])
         if ctx.bias_mids:
             c0 = 0
             for m in ctx.bias_mids:
@@ -153,8 +154,9 @@ class _MLPFn(torch.autograd.Function):
     """y = ff2(gelu(ff1(x))) with the GELU inside the GEMM epilogues: the forward of ff1 writes
     u = x W1 (+ b1) and h = gelu(u); the backward's dX GEMM of ff2 writes du = (dy W2^T) * gelu'(u)
     directly.  Off the fused path (roast_linear_*_act UNSUPPORTED) the same math runs unfused.
-    (The pair as one chained forward + one fused backward, roast_linear_{fwd,bwd}_chain_act, was
-    measured in the BERT step and was not faster: separate launches are kept here.)"""
+    The forward keeps separate launches (one chained launch, roast_linear_fwd_chain_act, was not
+    faster in the BERT step); the backward is one fused launch below RESIDUAL_FUSE_MIN_TOKENS
+    (_mlp_fused_bwd), separate launches above."""
 
     @staticmethod
     def forward(ctx, x, anchor, store, m1, b1, m2, b2, box=None):
@@ -182,6 +184,16 @@ class _MLPFn(torch.autograd.Function):
         x2, u, h = ctx.saved_tensors
         store = ctx.store
         dy2 = dy.reshape(x2.shape[0], -1).contiguous().to(x2.dtype)
+        if ctx.fused and _mlp_fused_bwd(x2.shape[0]):   # the four GEMMs in one launch (bwd_chain_act)
+            du, dx = store.bwd_chain_act(ctx.m1, ctx.m2, x2, h, u, dy2)
+            if ctx.b2 is not None:
+                store.bias_grad(ctx.b2, dy2)
+            if ctx.b1 is not None:
+                store.bias_grad(ctx.b1, du)
+            r = ctx.box.take() if ctx.box is not None else None
+            if r is not None:
+                dx.add_(r.reshape(dx.shape))
+            return dx.reshape(ctx.shape), None, None, None, None, None, None, None
         store.bwd_dm(ctx.m2, h, dy2)
         if ctx.b2 is not None:
             store.bias_grad(ctx.b2, dy2)
@@ -191,13 +203,22 @@ class _MLPFn(torch.autograd.Function):
             dh = torch.empty_like(h)
             store.bwd_dx(ctx.m2, dy2, dh)
             du = (dh.float() * _gelu_grad(u)).to(h.dtype)
-        store.bwd_dm(ctx.m1, x2, du)
         if ctx.b1 is not None:
             store.bias_grad(ctx.b1, du)
-        dx = None
-        if ctx.needs_input_grad[0]:
-            dx = _dx_plus_residual(store, ctx.m1, du, ctx.box, x2)   # + the residual gradient, if handed off
+        # dM of ff1, and dX + the residual gradient if handed off
+        dx = _linear_backward(store, ctx.m1, x2, du, ctx.box, ctx.needs_input_grad[0])
         return (dx.reshape(ctx.shape) if dx is not None else None), None, None, None, None, None, None, None
+
+
+def _mlp_fused_bwd(tokens):
+    """The MLP's backward as ONE launch (roast_linear_bwd_chain_act: dY_a with GELU', dM_b, dX_a,
+    dM_a co-scheduled) below RESIDUAL_FUSE_MIN_TOKENS, where its four GEMMs alone quantise badly:
+    C3 at 8192 tokens 6.08 -> 5.93 ms; at 65 536 the separate launches with the residual fused into
+    ff1's dX epilogue are faster (40.1 vs 41.6 ms).  ROAST_MLP_FUSED_BWD=0 / 1 forces it (A/B)."""
+    force = os.environ.get("ROAST_MLP_FUSED_BWD")
+    if force in ("0", "1"):
+        return force == "1"
+    return tokens < RESIDUAL_FUSE_MIN_TOKENS
 
 
 def _mlp_fusable(ff1, ff2, x):

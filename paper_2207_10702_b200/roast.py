@@ -23,7 +23,7 @@ MAP_HASH, MAP_IDENTITY = 0, 1
 EXPORTS = [
     "roast_config_default", "roast_create", "roast_create_ex", "roast_destroy", "roast_bind",
     "roast_register_linear", "roast_register_embedding", "roast_register_linear_seg",
-    "roast_register_embedding_seg", "roast_linear_fwd", "roast_linear_bwd",
+    "roast_register_embedding_seg", "roast_linear_fwd", "roast_linear_bwd", "roast_linear_bwd_fused",
     "roast_linear_bwd_dx", "roast_linear_bwd_dm", "roast_embedding_fwd", "roast_embedding_bwd",
     "roast_embedding_fwd_multi", "roast_embedding_bwd_multi", "roast_set_autotune", "roast_get_tuned", "roast_set_tuned",
     "roast_linear_fwd_bias", "roast_bias_fwd", "roast_bias_bwd", "roast_bias_bwd_ld", "roast_colsum", "roast_colsum_ex", "roast_register_linear_concat", "roast_linear_fwd_chain",
@@ -105,6 +105,7 @@ def _load():
         "roast_register_embedding_seg": (st, [H, I64, I32, I32, ctypes.c_double, I64, I64, ctypes.POINTER(I32)]),
         "roast_linear_fwd": (st, [H, I32, P, P, I64, ctypes.c_int, S]),
         "roast_linear_bwd": (st, [H, I32, P, P, P, I64, ctypes.c_int, S]),
+        "roast_linear_bwd_fused": (st, [H, I32, P, P, P, I64, ctypes.c_int, S]),
         "roast_linear_bwd_dx": (st, [H, I32, P, P, I64, ctypes.c_int, S]),
         "roast_linear_bwd_dm": (st, [H, I32, P, P, I64, ctypes.c_int, S]),
         "roast_embedding_fwd": (st, [H, I32, P, I64, P, S]),
@@ -331,6 +332,10 @@ def roast_linear_fwd(h, mid, X_ptr, Y_ptr, tokens, dtype, stream=0):
 
 def roast_linear_bwd(h, mid, X_ptr, dY_ptr, dX_ptr, tokens, dtype, stream=0):
     _check(_lib.roast_linear_bwd(h, mid, X_ptr, dY_ptr, dX_ptr, tokens, dtype, stream), "roast_linear_bwd")
+
+
+def roast_linear_bwd_fused(h, mid, X_ptr, dY_ptr, dX_ptr, tokens, dtype, stream=0):
+    _check(_lib.roast_linear_bwd_fused(h, mid, X_ptr, dY_ptr, dX_ptr, tokens, dtype, stream), "roast_linear_bwd_fused")
 
 
 def roast_linear_bwd_dx(h, mid, dY_ptr, dX_ptr, tokens, dtype, stream=0):
@@ -794,6 +799,15 @@ class Roast:
             dX = self.torch.empty_like(X)
         roast_linear_bwd(self.h, mid, X.data_ptr(), dY.data_ptr(), dX.data_ptr() if need_dx else None, T,
                          self._dt(X), self._s(stream))
+        return dX
+
+    def bwd_fused(self, mid, X, dY, dX=None, stream=None):
+        """dX and dM += in one co-scheduled launch where that pays (roast_linear_bwd_fused)."""
+        _, H, O = self.dims[mid]
+        T = X.numel() // H
+        assert dY.numel() == T * O and X.dtype == dY.dtype
+        dX = self.torch.empty_like(X) if dX is None else dX
+        roast_linear_bwd_fused(self.h, mid, X.data_ptr(), dY.data_ptr(), dX.data_ptr(), T, self._dt(X), self._s(stream))
         return dX
 
     def fwd_act(self, mid, X, Y=None, A=None, bias=None, act=ACT_GELU_TANH, stream=None):

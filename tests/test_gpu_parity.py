@@ -932,3 +932,53 @@ def test_bf16_off_the_tcgen05_path_is_an_error_unless_opted_in(R, torch):
     spec = OM.LinearSpec(H, O, 32, 32, mem, HS, mid)
     assert rel_frob(Y, np.float64(spec.lam) * (X.float().cpu().numpy() @ spec.materialize(M_np, "operand"))) <= 1e-2
     ctx.close()
+
+
+@pytest.mark.parametrize("H,O,T,always", [(768, 2304, 8192, False), (768, 3072, 8192, False), (768, 768, 300, True),
+                                          (1024, 512, 5000, True), (768, 3072, 65536, False)])
+def test_bwd_fused_single_linear(R, torch, H, O, T, always, monkeypatch):
+    """roast_linear_bwd_fused: one linear's dX and dM units co-scheduled in one launch (when the plan
+    beats the two launches; `always` forces it for the shape through ROAST_FUSE1_ALWAYS) against the
+    oracle — dX on sampled rows at full size, dM per slot; same results as roast_linear_bwd."""
+    if always:
+        monkeypatch.setenv("ROAST_FUSE1_ALWAYS", "1")
+    mem = 849352
+    M_np = store(mem)
+    ctx, _ = make_ctx(R, torch, M_np, 64, 64)
+    mid = ctx.linear(H, O)
+    X_np, dY_np = bf16_input(synth.SEED_X + 5, (T, H)), bf16_input(synth.SEED_DY + 5, (T, O))
+    X, dY = to_dev(X_np, torch.bfloat16), to_dev(dY_np, torch.bfloat16)
+    for _ in range(2):
+        ctx.zero_grad()
+        dX = ctx.bwd_fused(mid, X, dY)
+    torch.cuda.synchronize()
+    ctx.check()
+    spec = OM.LinearSpec(H, O, 64, 64, mem, HS, mid)
+    rows = slice(None) if T <= 8192 else np.random.default_rng(4).choice(T, 128, replace=False)
+    assert rel_frob(dX.float().cpu().numpy()[rows], spec.backward_dx(dY_np[rows], M_np, True)) <= 1e-2
+    dM = ctx.dM.cpu().numpy()
+    if T <= 8192:
+        assert rel_frob(dM, spec.backward_dm(X_np, dY_np)) <= 1e-2
+    else:   # sampled slots
+        slots = sorted({int(o + e) for o in np.random.default_rng(5).choice(spec.off.ravel(), 10, replace=False)
+                        for e in (0, 2047, 4095)})
+        ref = np.array([spec.grad_slot(X_np.astype(np.float64), dY_np.astype(np.float64), sl) for sl in slots])
+        assert rel_frob(dM[slots], ref) <= 1e-2
+    ctx.close()
+
+
+def test_bwd_fused_deterministic_is_bwd(R, torch):
+    """In deterministic mode roast_linear_bwd_fused is roast_linear_bwd: dM bitwise equal."""
+    M_np = store(47192)
+    out = []
+    for fused in (True, False):
+        ctx, _ = make_ctx(R, torch, M_np, 64, 64, deterministic=True)
+        mid = ctx.linear(768, 2304)
+        X = to_dev(bf16_input(synth.SEED_X, (8192, 768)), torch.bfloat16)
+        dY = to_dev(bf16_input(synth.SEED_DY, (8192, 2304)), torch.bfloat16)
+        ctx.zero_grad()
+        dX = ctx.bwd_fused(mid, X, dY) if fused else ctx.bwd(mid, X, dY)
+        torch.cuda.synchronize()
+        out.append((dX.clone(), ctx.dM.clone()))
+        ctx.close()
+    assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
