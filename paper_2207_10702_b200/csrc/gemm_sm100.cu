@@ -2566,7 +2566,7 @@ roast_status_t sm100_bwd_chain(Ctx* c, const Module& ma, const Module& mbm, cons
   const int mtT = int((T + 511) / 512), kbT = int((T + MIX_DWBK - 1) / MIX_DWBK);   // DW k-blocks of MIX_DWBK tokens
   const std::array<int64_t, 6> key{det ? 3 : 2, ma.H, ma.O, mbm.H, mbm.O, T};   // det plans differ (split cost)
   auto it = c->chain_plans.find(key);
-  static std::map<std::array<int64_t, 6>, std::pair<int, int>> splits;   // plan key -> (s1, s3)
+  auto& splits = c->mix_splits;   // plan key -> (s1, s3)
   if (it == c->chain_plans.end()) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
@@ -2728,7 +2728,7 @@ roast_status_t sm100_bwd_fused1(Ctx* c, const Module& m, const void* X, const vo
   const int mtT = int((T + 511) / 512), kbT = int((T + MIX_DWBK - 1) / MIX_DWBK);
   const std::array<int64_t, 6> key{4, m.H, m.O, 0, 0, T};   // the plan depends on the shape only
   auto it = c->chain_plans.find(key);
-  static std::map<std::array<int64_t, 6>, int> splits;
+  auto& splits = c->mix_splits;   // plan key -> (split, unused)
   if (it == c->chain_plans.end()) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
@@ -2763,12 +2763,12 @@ roast_status_t sm100_bwd_fused1(Ctx* c, const Module& m, const void* X, const vo
       fprintf(stderr, "[roast] bwd fused1 %lld x %lld, T %lld: makespan %.1f vs separate %.1f, split %d, used %d\n",
               (long long)m.H, (long long)m.O, (long long)T, plan.makespan, plan.separate, plan.s1, int(d != nullptr));
     it = c->chain_plans.emplace(key, std::make_pair(d, plan.len)).first;
-    splits[key] = plan.s1;
+    splits[key] = {plan.s1, 0};
   }
   if (!it->second.first) return ROAST_ERR_UNSUPPORTED;
   roast_status_t st = sm100_prepare(c);
   if (st) return st;
-  const int sp = splits[key];
+  const int sp = splits[key].first;
   MixMaps maps;
   memset(&maps, 0, sizeof(maps));
   MixParams mp;

@@ -177,6 +177,8 @@ struct Ctx {
   // schedules on the device (pointer, per-pair length; null = chaining does not pay) and the
   // ready counters of the first GEMM's output tiles
   std::map<std::array<int64_t, 6>, std::pair<int32_t*, int>> chain_plans;
+  // ... and the fused backwards' split-K counts of their weight-gradient problems (P1, P3)
+  std::map<std::array<int64_t, 6>, std::pair<int, int>> mix_splits;
   // ready counters of chained launches: kChainSlots slots of chain_slot_n ints, handed out round
   // robin per launch, so chained launches in flight on different streams use different counters
   // (up to kChainSlots launches in flight per handle); grown only outside graph capture
