@@ -399,8 +399,14 @@ __global__ void emb_chunk_sub_kernel(float* __restrict__ dM, float* __restrict__
   if (nseg == 0) return;
   const int64_t total = int64_t(choff[nseg - 1]) + nch[nseg - 1];
   const int64_t nsub = (int64_t(gridDim.x) * blockDim.x) / L;
-  for (int64_t c = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / L; c < total; c += nsub) {
-    const ChunkInfo ci = info[c];
+  // the next chunk's descriptor is loaded an iteration ahead (one dependent round trip fewer per
+  // chunk in this latency-bound pass: C4 0.628 -> 0.597 ms; also pre-loading its first item words
+  // or 8 items per round of loads was slower)
+  int64_t c = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / L;
+  ChunkInfo nxt = c < total ? info[c] : ChunkInfo{0, 0, 0, -2};
+  for (; c < total; c += nsub) {
+    const ChunkInfo ci = nxt;
+    if (c + nsub < total) nxt = info[c + nsub];
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     int it = ci.begin;
     constexpr int U = 4;
