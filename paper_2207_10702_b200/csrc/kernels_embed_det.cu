@@ -388,7 +388,7 @@ __global__ void emb_chunk_kernel(float* __restrict__ dM, float* __restrict__ par
 // at once (C4 at A = 32: 4, at A = 8: 16) instead of two — the pass is latency-bound (a few
 // items per group, ~4 dependent round trips each), so more chunks in flight is what pays.  Each
 // slot still adds its chunk's terms in item order (the same order as the warp version).
-__global__ void emb_chunk_sub_kernel(float* __restrict__ dM, float* __restrict__ partial,
+__global__ void __launch_bounds__(256, 8) emb_chunk_sub_kernel(float* __restrict__ dM, float* __restrict__ partial,
                                      const uint32_t* __restrict__ vals, const ChunkInfo* __restrict__ info,
                                      int64_t nseg, const int32_t* __restrict__ nch,
                                      const int32_t* __restrict__ choff, const float* __restrict__ dOut, int dim,
@@ -401,7 +401,7 @@ __global__ void emb_chunk_sub_kernel(float* __restrict__ dM, float* __restrict__
   const int64_t nsub = (int64_t(gridDim.x) * blockDim.x) / L;
   // the next chunk's descriptor is loaded an iteration ahead (one dependent round trip fewer per
   // chunk in this latency-bound pass: C4 0.628 -> 0.597 ms; also pre-loading its first item words
-  // or 8 items per round of loads was slower)
+  // or 8 items per round of loads was slower); 8 resident blocks per SM (32 registers): 0.563 ms
   int64_t c = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / L;
   ChunkInfo nxt = c < total ? info[c] : ChunkInfo{0, 0, 0, -2};
   for (; c < total; c += nsub) {
