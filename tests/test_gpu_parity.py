@@ -934,15 +934,16 @@ def test_bf16_off_the_tcgen05_path_is_an_error_unless_opted_in(R, torch):
     ctx.close()
 
 
-@pytest.mark.parametrize("H,O,T,always", [(768, 2304, 8192, False), (768, 3072, 8192, False), (768, 768, 300, True),
-                                          (1024, 512, 5000, True), (768, 3072, 65536, False)])
-def test_bwd_fused_single_linear(R, torch, H, O, T, always, monkeypatch):
+@pytest.mark.parametrize("H,O,T,always,mem", [(768, 2304, 8192, False, 849352), (768, 3072, 8192, False, 849352),
+                                              (768, 768, 300, True, 849352), (1024, 512, 5000, True, 849352),
+                                              (768, 3072, 65536, False, 849352), (768, 768, 2000, True, 4720)])
+def test_bwd_fused_single_linear(R, torch, H, O, T, always, mem, monkeypatch):
     """roast_linear_bwd_fused: one linear's dX and dM units co-scheduled in one launch (when the plan
     beats the two launches; `always` forces it for the shape through ROAST_FUSE1_ALWAYS) against the
-    oracle — dX on sampled rows at full size, dM per slot; same results as roast_linear_bwd."""
+    oracle — dX on sampled rows at full size, dM per slot; same results as roast_linear_bwd.  |M| =
+    4720: the dM units reduce-add through the handle's dM replicas and the fold."""
     if always:
         monkeypatch.setenv("ROAST_FUSE1_ALWAYS", "1")
-    mem = 849352
     M_np = store(mem)
     ctx, _ = make_ctx(R, torch, M_np, 64, 64)
     mid = ctx.linear(H, O)
